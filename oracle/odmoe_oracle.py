@@ -1,0 +1,406 @@
+"""Plain, slow, obviously-correct CPU oracle of the OD-MoE decode hot path.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py): never imported by the product.
+
+Every function follows a passage of the paper (P:L = /root/reference/PAPER.md line L)
+or, where the paper is silent, a reading listed in DESIGN.md §4 (Qn = SURVEY.md §8(c)
+reading n). Arithmetic is numpy float64; dot products are numpy matmul (a library
+primitive, allowed as a step). No blocking, fusion or reordering.
+
+Parity pins (tests/test_oracle_pins.py, -m "not gpu"):
+  rms_norm            pinned: closed form on [3,4]; scale invariance; unit RMS.
+  router_logits       pinned: one-hot rows select coordinates; brute force on tiny ints.
+  top_k               pinned: SPEC S:80-81 worked examples; brute force over all C(E,k)
+                      subsets; constructed ties; expert-permutation equivariance.
+  mixture_weights     pinned: k=1 -> 1; k=E -> scipy.special.softmax; sum = 1; hand values.
+  expert_ffn          pinned: zero in -> zero out; selector-matrix closed forms that
+                      distinguish W1 from W3 and W2 from W2^T; silu(1) constant.
+  moe_layer           pinned: identical experts -> y = FFN(u) for any routing; hand example.
+  decode_token        pinned: determinism; override neutrality; constructed
+                      LM-head argmax ties.
+  quantize_int8_rows  pinned: SPEC S:70 example ([1,-0.5] -> codes [127,-64]); half-step
+                      bound; zero fixed point.
+  shadow_predict      pinned: same-precision shadow => recall exactly 1.0.
+  plan_* / misprediction_reloads / max_load_budget
+                      pinned: SPEC examples S:271-273.
+  recall_eq2/eq3      pinned: SPEC S:201-202 examples; brute-force triple loop.
+  random predictor    pinned: closed form E[recall] = k/E ("recall in Case 5 is only ~25%").
+  recall VALUE on random weights: parity unpinned (paper's 99.94/97.34/95.67% are Mixtral +
+                      LongWriter values); only the accounting is pinned.
+"""
+from __future__ import annotations
+
+import math
+from fractions import Fraction
+from itertools import combinations
+
+import numpy as np
+
+__all__ = [
+    "rms_norm", "router_logits", "top_k", "top_k_bruteforce", "mixture_weights", "silu",
+    "expert_ffn", "moe_layer", "final_logits", "greedy_argmax", "decode_token", "decode_sequence",
+    "quantize_int8_rows", "dequantize_int8_rows", "quantize_model_int8", "shadow_predict",
+    "near_tie", "plan_group_size", "plan_groups", "assign_layer", "assign_experts",
+    "misprediction_reloads", "max_load_budget", "residency_bound", "recall_eq2", "recall_eq3",
+    "recall_bruteforce", "prefill_permutation", "prefill_reference", "expert_counts",
+]
+
+
+# ---------------------------------------------------------------- O1 RMSNorm (Q7)
+def rms_norm(h, gamma=None, eps: float = 1e-5):
+    """u = h * gamma / sqrt(mean(h^2) + eps).
+
+    The paper places "normalization networks" on the main node and in M_l
+    but does not print the formula; Mixtral's RMSNorm with eps=1e-5 and gamma=1 is the
+    reading Q7. Works on [d] or [m, d].
+    """
+    h = np.asarray(h, dtype=np.float64)
+    ms = np.mean(h * h, axis=-1, keepdims=True)
+    u = h / np.sqrt(ms + eps)
+    if gamma is not None:
+        u = u * np.asarray(gamma, dtype=np.float64)
+    return u
+
+
+# ---------------------------------------------------------------- O2 router logits
+def router_logits(w_gate, u):
+    """r_e = sum_j W_g[e, j] * u_j  ("the gating network is activated as in a standard MoE
+    system to determine expert routing"). w_gate [E, d], u [d] or [m, d]."""
+    W = np.asarray(w_gate, dtype=np.float64)
+    return np.asarray(u, dtype=np.float64) @ W.T
+
+
+# ---------------------------------------------------------------- O3 top-k (Q3)
+def top_k(r, k: int):
+    """Indices of the k largest logits, ordered by (logit descending, index ascending).
+
+    Top-k activation (k=2 for Mixtral); ties go to the lower expert index
+    (reading Q3). r is a 1-D array of E logits.
+    """
+    r = [float(x) for x in np.asarray(r, dtype=np.float64).ravel()]
+    order = sorted(range(len(r)), key=lambda e: (-r[e], e))
+    return order[:k]
+
+
+def top_k_bruteforce(r, k: int):
+    """Brute force: among all C(E, k) subsets, the one whose sorted logit vector is
+    lexicographically largest, ties resolved toward lower indices."""
+    r = [float(x) for x in np.asarray(r, dtype=np.float64).ravel()]
+    best = None
+    for sub in combinations(range(len(r)), k):
+        key = sorted(((-r[e], e) for e in sub))
+        if best is None or key < best[0]:
+            best = (key, sub)
+    return [e for _, e in best[0]]
+
+
+# ---------------------------------------------------------------- O4 mixture weights (Q2)
+def mixture_weights(r, S):
+    """w_i = exp(r_i - m) / sum_{j in S} exp(r_j - m), m = max_{j in S} r_j.
+
+    The paper does not restate Mixtral's mixture rule; softmax over the k selected logits
+    (reading Q2) equals Mixtral's softmax-then-renormalise. Returned in the
+    order of S."""
+    r = np.asarray(r, dtype=np.float64).ravel()
+    sel = np.array([r[i] for i in S], dtype=np.float64)
+    m = sel.max()
+    e = np.exp(sel - m)
+    return e / e.sum()
+
+
+# ---------------------------------------------------------------- O5 expert FFN (Q1)
+def silu(x):
+    x = np.asarray(x, dtype=np.float64)
+    return x / (1.0 + np.exp(-x))
+
+
+def expert_ffn(W1, W3, W2, u):
+    """Expert computation EC_l: the Mixtral SwiGLU expert (reading Q1):
+    g = W1 u, v = W3 u, a = silu(g) * v, y = W2 a.
+    W1, W3 [F, d]; W2 [d, F]; u [d]."""
+    u = np.asarray(u, dtype=np.float64)
+    g = np.asarray(W1, dtype=np.float64) @ u
+    v = np.asarray(W3, dtype=np.float64) @ u
+    a = silu(g) * v
+    return np.asarray(W2, dtype=np.float64) @ a
+
+
+# ---------------------------------------------------------------- O6 one MoE layer
+def moe_layer(h, w_gate, experts, k: int, eps: float = 1e-5, u=None, S=None):
+    """One decode layer of the MoE block: norm -> gate -> top-k -> weighted expert sum ->
+    residual (combine rule S:125; residual in fp32/fp64, reading Q6).
+
+    `experts` maps expert id -> (W1, W3, W2). `u` (teacher forcing of the normalised input)
+    and `S` (routing override) are optional. Returns a dict of every intermediate.
+    """
+    h = np.asarray(h, dtype=np.float64)
+    if u is None:
+        u = rms_norm(h, eps=eps)
+    u = np.asarray(u, dtype=np.float64)
+    r = router_logits(w_gate, u)
+    sel = top_k(r, k)
+    if S is None:
+        S = sel
+    w = mixture_weights(r, S)
+    wmap = {int(e): float(wi) for e, wi in zip(S, w)}
+    ys = {}
+    y = np.zeros_like(h)
+    for e in sorted(int(x) for x in S):  # O6: ascending expert order
+        W1, W3, W2 = experts[e]
+        ys[e] = wmap[e] * expert_ffn(W1, W3, W2, u)
+        y = y + ys[e]
+    return dict(u=u, logits=r, S=list(S), topk=sel, w=wmap, y_parts=ys, y=y, h_next=h + y)
+
+
+# ---------------------------------------------------------------- O7 LM head + greedy
+def final_logits(lm_head, h, eps: float = 1e-5):
+    """z = W_o RMSNorm(h_L)."""
+    return np.asarray(lm_head, dtype=np.float64) @ rms_norm(h, eps=eps)
+
+
+def greedy_argmax(z):
+    """Greedy decoding selects the maximum-likelihood token; ties to the lowest id
+    (S:95). np.argmax returns the first maximal index."""
+    return int(np.argmax(np.asarray(z, dtype=np.float64)))
+
+
+def decode_token(weights, token: int, k: int, eps: float = 1e-5, override=None, layers=None):
+    """One decode iteration on the hot path (reading Q22: no attention):
+    h0 = Emb[t]; for l: h = moe_layer(h); t' = argmax(W_o RMSNorm(h_L)).
+    `weights` as produced by inputs.gen_model_weights (stored values). Returns
+    (next_token, [per-layer dict])."""
+    L = sorted(weights["router"].keys()) if layers is None else layers
+    h = np.asarray(weights["emb"][token], dtype=np.float64)
+    recs = []
+    for li, l in enumerate(L):
+        S = None if override is None else override[li]
+        out = moe_layer(h, weights["router"][l], weights["experts"][l], k, eps, S=S)
+        out["h_in"] = h
+        recs.append(out)
+        h = out["h_next"]
+    z = final_logits(weights["lm_head"], h, eps)
+    return greedy_argmax(z), recs, z
+
+
+def decode_sequence(weights, first_token: int, n_tokens: int, k: int, eps: float = 1e-5):
+    """Greedy decode n_tokens starting from first_token; returns (tokens, routing[n][l])."""
+    toks, routes, t = [], [], int(first_token)
+    for _ in range(n_tokens):
+        t_next, recs, _ = decode_token(weights, t, k, eps)
+        routes.append([sorted(r["S"]) for r in recs])
+        toks.append(t_next)
+        t = t_next
+    return toks, routes
+
+
+# ---------------------------------------------------------------- O8 shadow / SEP
+def quantize_int8_rows(W):
+    """INT8 shadow quantiser (P:86, P:164 name INT8 without a format; reading Q9):
+    per output row r, m_r = max_j |W_rj|; q_rj = clamp(RNE((W_rj * 127) / m_r), -127, 127)
+    with the product and quotient in fp64; s_r = fl32(m_r / 127) (fp64 quotient rounded to
+    fp32). A row with m_r = 0 gives q = 0, s = 1. Generalises SPEC's per-matrix grid
+    (S:65): for one row they coincide.
+    Returns (q int8 [R, C], s float32 [R])."""
+    W = np.asarray(W, dtype=np.float64)
+    if W.ndim == 1:
+        W = W[None, :]
+    m = np.max(np.abs(W), axis=1)
+    q = np.zeros(W.shape, dtype=np.int8)
+    s = np.ones(W.shape[0], dtype=np.float32)
+    nz = m > 0
+    quot = (W[nz] * 127.0) / m[nz][:, None]
+    q[nz] = np.clip(np.rint(quot), -127, 127).astype(np.int8)  # np.rint = round half to even
+    s[nz] = (m[nz] / 127.0).astype(np.float32)
+    return q, s
+
+
+def dequantize_int8_rows(q, s):
+    """Q(W)_rj = s_r * q_rj (exact in fp64)."""
+    return np.asarray(s, dtype=np.float64)[:, None] * np.asarray(q, dtype=np.float64)
+
+
+def quantize_model_int8(weights):
+    """Q(W) for every matrix of the model: embedding, routers, experts. Returns a
+    weights dict of the same structure holding the dequantised fp64 values."""
+    dq = lambda W: dequantize_int8_rows(*quantize_int8_rows(W))  # noqa: E731
+    out = {"emb": dq(weights["emb"]), "router": {}, "experts": {}}
+    for l, Wg in weights["router"].items():
+        out["router"][l] = dq(Wg)
+        out["experts"][l] = {e: tuple(dq(M) for M in mats) for e, mats in weights["experts"][l].items()}
+    return out
+
+
+def shadow_predict(shadow_weights, main_token: int, k: int, eps: float = 1e-5):
+    """SEP, Mode A (reading Q10): token alignment every iteration -- the
+    shadow starts from ITS OWN embedding row of the MAIN model's token and runs all L layers
+    with its own (quantised) weights and its own routing; P[l] = its top-k at layer l
+    ("uses the future expert activations that are already unfolded by the scaled-down
+    shadow model"). No attention => no KV state, i.e. the paper's T1_KV1 regime.
+    Returns (P [L][k] in rank order, per-layer dicts)."""
+    L = sorted(shadow_weights["router"].keys())
+    h = np.asarray(shadow_weights["emb"][main_token], dtype=np.float64)
+    P, recs = [], []
+    for l in L:
+        out = moe_layer(h, shadow_weights["router"][l], shadow_weights["experts"][l], k, eps)
+        out["h_in"] = h
+        P.append(out["S"])
+        recs.append(out)
+        h = out["h_next"]
+    return P, recs
+
+
+def near_tie(r, k: int, rel: float = 1e-3) -> bool:
+    """North-star excuse window (reading Q4): the oracle's k-th and (k+1)-th largest logits
+    differ by less than rel * max(|r_(k)|, |r_(k+1)|); both zero counts as a tie."""
+    srt = sorted((float(x) for x in np.asarray(r).ravel()), reverse=True)
+    if k >= len(srt):
+        return False
+    a, b = srt[k - 1], srt[k]
+    if a == 0.0 and b == 0.0:
+        return True
+    return abs(a - b) < rel * max(abs(a), abs(b))
+
+
+# ---------------------------------------------------------------- O9 placement
+def plan_group_size(k: int, n_gpus: int) -> int:
+    """G = k in the paper ("G=2 since a top-2 activation policy"); with fewer GPUs
+    than k one GPU takes several experts: G = min(k, N) (reading Q14)."""
+    return min(k, n_gpus)
+
+
+def plan_groups(n_workers: int, G: int):
+    """N_W/G groups of G contiguous workers. N_W must be divisible by G."""
+    if G <= 0 or n_workers % G != 0:
+        raise ValueError("n_workers must be divisible by the group size")
+    return [list(range(g * G, (g + 1) * G)) for g in range(n_workers // G)]
+
+
+def assign_layer(layer: int, n_groups: int) -> int:
+    """Round-robin layer -> group (Fig. 2): l mod N_G."""
+    return layer % n_groups
+
+
+def assign_experts(experts, workers):
+    """One-to-one expert -> worker: sorted experts paired with sorted workers.
+    With fewer workers than experts (G < k), sorted expert i goes to sorted worker
+    i * G // k (each worker takes k/G consecutive experts; reading Q14)."""
+    ex = sorted(int(e) for e in experts)
+    wk = sorted(int(w) for w in workers)
+    k, G = len(ex), len(wk)
+    if G == 0 or k % G != 0:
+        raise ValueError("cardinality mismatch in placement")
+    return {e: wk[i * G // k] for i, e in enumerate(ex)}
+
+
+def misprediction_reloads(true_S, resident):
+    """Misprediction fallback ("the expert computation task waits for the completion
+    of expert reloading"). `resident` maps expert -> worker for the layer's loaded
+    (predicted) experts. Reload set = true \\ resident, placed on the workers holding the
+    wrong experts, sorted-paired (reading Q15). Returns sorted [(expert, worker)]."""
+    true_S = sorted(int(e) for e in true_S)
+    missing = [e for e in true_S if e not in resident]
+    stale_workers = sorted(w for e, w in resident.items() if e not in true_S)
+    if len(stale_workers) < len(missing):
+        raise ValueError("not enough stale workers for the reload set")
+    return list(zip(missing, stale_workers[: len(missing)]))
+
+
+def max_load_budget(t_M: float, t_W: float, n_groups: int) -> float:
+    """Eq. 1 with the worked example's reading (4t^M+3t^W at four groups;
+    reading Q12): t_maxload = N_G * t_M + (N_G - 1) * t_W."""
+    if t_M < 0 or t_W < 0:
+        raise ValueError("negative time")
+    return n_groups * t_M + (n_groups - 1) * t_W
+
+
+def residency_bound(lookahead: int, n_groups: int) -> int:
+    """Per-worker residency bound ceil(D / N_G) + 1 experts."""
+    return -(-lookahead // n_groups) + 1
+
+
+# ---------------------------------------------------------------- O10 recall (Eqs. 2-3)
+def _c_count(true_S, pred_S, avail=True):
+    """c(q,n,l) = |true ∩ predicted| in [0, k]; 0 if the prediction was unavailable."""
+    if not avail or pred_S is None:
+        return 0
+    return len(set(int(x) for x in true_S) & set(int(x) for x in pred_S))
+
+
+def recall_eq2(c, A, k: int):
+    """Eq. 2: recall(n) = sum_q sum_l c(q,n,l) A(q,n) / (k L sum_q A(q,n)).
+    c: int array [Q, N, L]; A: {0,1} array [Q, N]. Returns list of Fraction (None where
+    the denominator is 0)."""
+    c = np.asarray(c, dtype=np.int64)
+    A = np.asarray(A, dtype=np.int64)
+    Q, N, L = c.shape
+    out = []
+    for n in range(N):
+        num = int(sum(int(c[q, n, l]) * int(A[q, n]) for q in range(Q) for l in range(L)))
+        den = k * L * int(sum(int(A[q, n]) for q in range(Q)))
+        out.append(Fraction(num, den) if den else None)
+    return out
+
+
+def recall_eq3(c, A, k: int):
+    """Eq. 3: sum_n sum_q sum_l c A / (k L sum_n sum_q A), one exact division."""
+    c = np.asarray(c, dtype=np.int64)
+    A = np.asarray(A, dtype=np.int64)
+    Q, N, L = c.shape
+    num = 0
+    den = 0
+    for n in range(N):
+        for q in range(Q):
+            den += int(A[q, n])
+            for l in range(L):
+                num += int(c[q, n, l]) * int(A[q, n])
+    return Fraction(num, k * L * den) if den else None
+
+
+def recall_bruteforce(records, k: int, L: int):
+    """Triple loop straight from the definition "the number of correctly predicted experts
+    out of all activated experts" over explicit records
+    {(q, n): [(true_S, pred_S, avail) per layer]}."""
+    correct = 0
+    activated = 0
+    for (_q, _n), layers in records.items():
+        for (true_S, pred_S, avail) in layers:
+            activated += len(true_S)
+            correct += _c_count(true_S, pred_S, avail)
+    return Fraction(correct, activated) if activated else None
+
+
+# ---------------------------------------------------------------- prefill
+def prefill_permutation(ids):
+    """Group (token, expert) pairs by expert, stable by token ("embeddings are grouped
+    by their desired experts"). ids int [T, k]. Returns (perm_token [T*k], perm_slot [T*k],
+    offsets [E+1]) for E = max id + 1 ... computed by a plain stable sort."""
+    ids = np.asarray(ids)
+    T, k = ids.shape
+    pairs = [(int(ids[t, j]), t, j) for t in range(T) for j in range(k)]
+    pairs.sort(key=lambda p: (p[0], p[1], p[2]))
+    return pairs
+
+
+def expert_counts(ids, E: int):
+    """Tokens routed to each expert (P:214 footnote counts activated experts)."""
+    ids = np.asarray(ids)
+    return np.array([int(np.sum(ids == e)) for e in range(E)], dtype=np.int64)
+
+
+def prefill_reference(h, w_gate, experts, k: int, eps: float = 1e-5, u=None):
+    """Prefill MoE layer over T tokens: without attention tokens are independent, so
+    each row is the decode layer's computation; grouping only changes the order of work.
+    Returns per-token dicts from moe_layer."""
+    h = np.asarray(h, dtype=np.float64)
+    return [moe_layer(h[t], w_gate, experts, k, eps, u=None if u is None else u[t]) for t in range(h.shape[0])]
+
+
+def softmax_all(r):
+    """Plain softmax over all logits (used only to pin mixture_weights at k=E)."""
+    r = np.asarray(r, dtype=np.float64)
+    e = np.exp(r - r.max())
+    return e / e.sum()
+
+
+def _isclose(a, b, tol=1e-12):
+    return math.isclose(a, b, rel_tol=tol, abs_tol=tol)
