@@ -1,0 +1,384 @@
+"""OD-MoE decode benchmark (BASELINE.json metric: decode tokens/s vs fully-resident, and
+expert-prediction accuracy).
+
+One step = one batch-1 decode iteration of the whole hot path:
+embed -> 32 x [router/top-k -> prediction check -> just-in-time H2D expert loads -> SwiGLU
+expert GEMVs -> combine] -> LM head -> argmax, with the INT8 shadow predictor running ahead.
+Workload at N=1: BASELINE.json configs[1] (Mixtral-8x7B shape, bf16, 1 GPU, on-demand, 2 slots
+= 705 MB of experts per GPU). At N>1 (torchrun): configs[3]/[2] layout, experts spread
+round-robin over groups of 2 GPUs, lookahead D = N/2.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "decode tokens/s vs fully-resident (1/2/4/8 B200); expert-prediction accuracy"
+UNIT = "tok/s"
+SHAPE = dict(L=32, E=8, k=2, d=4096, F=14336, V=32000)
+EXPERT_BYTES = 3 * SHAPE["d"] * SHAPE["F"] * 2          # 352,321,536 (bf16)
+W13_BYTES = 2 * SHAPE["d"] * SHAPE["F"] * 2
+W2_BYTES = SHAPE["d"] * SHAPE["F"] * 2
+SEED = 2512
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=16)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--predictor", default="shadow_int8")
+    ap.add_argument("--slots", type=int, default=2)
+    ap.add_argument("--lookahead", type=int, default=0, help="0 => max(1, N/2)")
+    ap.add_argument("--no-resident", action="store_true", help="skip the fully-resident baseline")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--first-token", type=int, default=-1)
+    ap.add_argument("--out", default="")
+    return ap.parse_args()
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                smax = float(p[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def h2d_peak_gbs(torch, dev):
+    """Pinned host->device copy of one expert blob (352 MB), best of 3: the host-link roofline
+    measured in the same run (concurrently on every rank at N > 1)."""
+    src = torch.empty(EXPERT_BYTES, dtype=torch.uint8).pin_memory()
+    dst = torch.empty(EXPERT_BYTES, dtype=torch.uint8, device=dev)
+    best = 0.0
+    for _ in range(3):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        dst.copy_(src, non_blocking=True)
+        b.record()
+        torch.cuda.synchronize()
+        best = max(best, EXPERT_BYTES / (a.elapsed_time(b) * 1e-3) / 1e9)
+    del src, dst
+    return best
+
+
+# ---------------------------------------------------------------------------- CPU oracle leg
+def oracle_sample(n_layers=1, seed=SEED, first_token=1):
+    """Time the CPU oracle (as it stands) on a bounded sample of the decode step: `n_layers`
+    Mixtral-shape MoE layers (router + top-k + 2 SwiGLU experts from the bf16 stored weights, in
+    fp64) plus the LM head + argmax; scaled to one 32-layer token. Weight generation is not timed
+    (in the real system the weights sit in DRAM)."""
+    import numpy as np
+    import oracle as O
+    from inputs import MIXTRAL, gen_model_weights
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    W = gen_model_weights(MIXTRAL, seed, dtype="bf16", layers=list(range(n_layers)))
+    h = np.asarray(W["emb"][first_token], dtype=np.float64)
+    t0 = time.perf_counter()
+    for l in range(n_layers):
+        out = O.moe_layer(h, W["router"][l], W["experts"][l], MIXTRAL.k)
+        h = out["h_next"]
+    t_layers = time.perf_counter() - t0
+    t1 = time.perf_counter()
+    O.greedy_argmax(O.final_logits(W["lm_head"], h))
+    t_lm = time.perf_counter() - t1
+    s_per_token = t_layers / n_layers * MIXTRAL.L + t_lm
+    return {"value": 1.0 / s_per_token, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{n_layers} of 32 Mixtral-shape MoE layers (router+top-k+2 SwiGLU experts, "
+                      f"fp64 numpy from bf16 weights) + LM head/argmax of one decode token, scaled "
+                      f"to 32 layers; {t_layers + t_lm:.1f} s of CPU work"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle as the reference arm, on our arm's metric/config."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import numpy as np
+    import oracle as O
+    from inputs import MIXTRAL, gen_model_weights
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    W = gen_model_weights(MIXTRAL, SEED, dtype="bf16", layers=[0])
+    h0 = np.asarray(W["emb"][1], dtype=np.float64)
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        out = O.moe_layer(h0, W["router"][0], W["experts"][0], MIXTRAL.k)
+        z = O.final_logits(W["lm_head"], out["h_next"]) if i == 0 else None  # noqa: F841
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+    # one step = one layer of a token (bounded sample), scaled to a 32-layer token
+    s_tok = statistics.mean(times) * MIXTRAL.L
+    v = 1.0 / s_tok
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": s_tok * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": workload_config(args, 1),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": "each step = 1 of 32 Mixtral-shape MoE layers of a decode token "
+                                       "(router+top-k+2 SwiGLU experts, fp64), scaled x32"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(args, n):
+    ng = max(1, n // 2)
+    return {"workload": ("configs[1]: Mixtral-8x7B shape (L=32, E=8, top-2, d=4096, F=14336, V=32000), "
+                         "bf16, batch-1 decode, on-demand expert loading" if n == 1 else
+                         f"configs[2]/[3]: Mixtral-8x7B shape, bf16, batch-1 decode, experts round-robin "
+                         f"over {ng} groups of 2 GPUs, lookahead {args.lookahead or ng}"),
+            "predictor": args.predictor, "slots_per_gpu": args.slots,
+            "expert_bytes_per_gpu": args.slots * EXPERT_BYTES,
+            "lookahead": args.lookahead or max(1, n // 2), "weight_seed": SEED,
+            "attention": "none on the hot path (reading Q22)",
+            "l2": "inputs larger than L2: every step streams 64 distinct 352 MB experts"}
+
+
+# ---------------------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    n = world
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2512_03927_b200 import odmoe
+    peaks, peak_src = measured_peaks()
+
+    uid = None
+    if world > 1:
+        obj = [odmoe.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    D = args.lookahead or max(1, n // 2)
+    pred = odmoe.PREDICTORS[args.predictor]
+    t_create = time.time()
+    eng = odmoe.Engine(device=local, rank=rank, world_size=world, nccl_id=uid, predictor=pred,
+                       slots_per_gpu=args.slots, lookahead=D, time_kernels=1, weight_seed=SEED,
+                       **SHAPE)
+    t_create = time.time() - t_create
+    link = h2d_peak_gbs(torch, torch.device("cuda", local))
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    tok = args.first_token if args.first_token >= 0 else 1
+    for _ in range(args.warmup):
+        tok, _ = eng.decode_step(tok, records=False)
+    eng.reset_stats()
+    recs_all = []
+    clocks = ClockSampler(local)
+    barrier()
+    clocks.start()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    ev0.record()
+    for _ in range(args.steps):
+        tok, recs = eng.decode_step(tok, records=(rank == 0))
+        if rank == 0:
+            recs_all.append([(tuple(r.true_ids[:2]), tuple(r.pred_ids[:2]), r.correct) for r in recs])
+    ev1.record()
+    barrier()
+    wall = time.perf_counter() - t0
+    clk = clocks.stop()
+    dev_s = ev0.elapsed_time(ev1) * 1e-3
+    st = eng.stats()
+    if dist is not None:
+        tt = torch.tensor([dev_s, wall], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dev_s, wall = float(tt[0]), float(tt[1])
+        agg = torch.tensor([st["bytes_h2d"], link], dtype=torch.float64, device="cuda")
+        dist.all_reduce(agg, op=dist.ReduceOp.SUM)
+        bytes_all, link_all = float(agg[0]), float(agg[1])
+    else:
+        bytes_all, link_all = float(st["bytes_h2d"]), link
+    eng.close()
+    del eng
+
+    value = args.steps / dev_s
+    e2e = args.steps / wall
+    res = None
+    if not args.no_resident and world == 1 and rank == 0:
+        res = resident_baseline(odmoe, torch, args, local)
+
+    if rank == 0:
+        n_exp = max(1, st["n_w13"])
+        gemv_ms = (st["ms_w13"] + st["ms_w2"]) / n_exp
+        achieved = EXPERT_BYTES / (gemv_ms * 1e-3) / 1e9
+        traffic = None
+        prof = os.path.join(ROOT, "profiles", "ncu_expert_gemv_r01.json")
+        if os.path.exists(prof):
+            try:
+                traffic = json.load(open(prof)).get("dram_bytes_per_expert")
+            except Exception:
+                traffic = None
+        recall = st["correct"] / st["predicted_total"] if st["predicted_total"] else None
+        roof_tok = link_all * 1e9 / (64 * EXPERT_BYTES)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dev_s / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (counter-based splitmix64 weights, U(+-1/sqrt(fan_in)), seed 2512; "
+                    "greedy token feedback)",
+            "config": workload_config(args, n),
+            "recall_eq3": recall,
+            "roofline": {"bound": "hbm", "kernel": "expert SwiGLU GEMV (W13+SwiGLU, W2+gate)",
+                         "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                         "peak_source": peak_src, "bytes_per_launch_pair": EXPERT_BYTES,
+                         "avg_us_per_expert": gemv_ms * 1e3, "w13_us": st["ms_w13"] / n_exp * 1e3,
+                         "w2_us": st["ms_w2"] / n_exp * 1e3},
+            "host_link": {"bound": "pcie_h2d", "achieved": bytes_all / dev_s / 1e9,
+                          "peak": link_all, "unit": "GB/s", "frac": bytes_all / dev_s / 1e9 / link_all,
+                          "roofline_tok_s": roof_tok, "frac_tok_s": value / roof_tok,
+                          "bytes_h2d_per_step": bytes_all / args.steps,
+                          "algorithmic_bytes_per_step": 64 * EXPERT_BYTES},
+            "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(bytes_all / args.steps) + 4,
+                    "d2h_bytes_per_step": 4 + (32 * 2 * 4 if True else 0),
+                    "note": "odmoe_decode_step with a host token in/out; the H2D bytes are the "
+                            "step's expert loads from the pinned host pool"},
+            "gpu_launches": st["kernel_launches"],
+            "clocks": clk,
+            "engine": {"create_s": t_create, "pool_build_s": st["pool_build_s"],
+                       "pool_bytes": st["pool_bytes"], "resident_expert_bytes": st["resident_bytes"],
+                       "shadow_bytes": st["shadow_bytes"], "reloads": st["reloads"],
+                       "loads_cancelled": st["loads_cancelled"], "max_resident": st["max_resident"],
+                       "ms_router": st["ms_router"] / max(1, st["n_router"]) * 1e3,
+                       "us_shadow_per_step": st["ms_shadow"] / args.steps * 1e3,
+                       "us_lm_head": st["ms_lm_head"] / max(1, st["n_lm_head"]) * 1e3},
+        }
+        if res is not None:
+            line["resident"] = res
+            line["ratio_vs_resident"] = value / res["value"]
+        if not args.no_cpu_baseline and n == 1:
+            try:
+                line["cpu_baseline"] = oracle_sample(1)
+            except Exception as e:  # report, never hide
+                line["cpu_baseline"] = {"value": None, "error": repr(e)}
+        out = json.dumps(line)
+        print(out, flush=True)
+        if args.out:
+            with open(args.out, "w") as f:
+                f.write(out + "\n")
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def resident_baseline(odmoe, torch, args, dev):
+    """Fully-resident baseline (same kernels and placement; all 256 experts in HBM; routing
+    consumed on the device, no per-layer host sync)."""
+    eng = odmoe.Engine(device=dev, predictor=odmoe.PRED_NONE, slots_per_gpu=-1, time_kernels=1,
+                       weight_seed=SEED, **SHAPE)
+    tok = 1
+    for _ in range(args.warmup):
+        tok, _ = eng.decode_step(tok, records=False)
+    eng.reset_stats()
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(args.steps):
+        tok, _ = eng.decode_step(tok, records=False)
+    b.record()
+    torch.cuda.synchronize()
+    s = a.elapsed_time(b) * 1e-3
+    st = eng.stats()
+    eng.close()
+    n_exp = max(1, st["n_w13"])
+    gemv_ms = (st["ms_w13"] + st["ms_w2"]) / n_exp
+    return {"value": args.steps / s, "unit": UNIT, "ms_per_step": s / args.steps * 1e3,
+            "expert_gemv_us": gemv_ms * 1e3, "expert_gemv_GBps": EXPERT_BYTES / (gemv_ms * 1e-3) / 1e9,
+            "resident_expert_bytes": st["resident_bytes"],
+            "hbm_roofline_tok_s": 6541.5e9 / (64 * EXPERT_BYTES + SHAPE["V"] * SHAPE["d"] * 2)}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,241 @@
+/*
+ * odmoe.h — C ABI of the B200-native OD-MoE decode hot path (arXiv 2512.03927).
+ *
+ * "P:L" cites /root/reference/PAPER.md line L; "S:L" cites SPEC.md line L; "Qn" is a
+ * reading of the paper listed in DESIGN.md §4.
+ *
+ * The library (paper_2512_03927_b200/libodmoe.so) is CUDA sm_100a code plus a C++
+ * runtime. Every entry point returns an odmoe_status; nothing aborts and no C++
+ * exception crosses this boundary. Two families of calls:
+ *
+ *  1. Stateless kernels (odmoe_route_topk, odmoe_expert_ffn, odmoe_shadow_expert_ffn,
+ *     odmoe_lm_head_argmax, odmoe_quantize_int8_rows, odmoe_gen_weights):
+ *     every pointer is CALLER-OWNED DEVICE memory on the current CUDA device, row-major,
+ *     16-byte aligned; `stream` is a cudaStream_t (NULL = legacy default stream).
+ *     They only enqueue work and return; results are valid when the stream reaches them.
+ *     Shape errors return ODMOE_E_CONFIG before anything is enqueued; a launch error
+ *     returns ODMOE_E_CUDA.
+ *
+ *  2. The stateful decode engine (odmoe_create ... odmoe_destroy): one odmoe_ctx per
+ *     process, bound to one GPU (one process per GPU; ranks talk over NCCL). The ctx
+ *     owns the pinned host expert pool, the device expert slots, the resident
+ *     non-expert weights, the INT8 shadow model (rank 0), the copy-stream loader thread,
+ *     the NCCL communicators, streams and events. Host output buffers of these calls are
+ *     caller-owned and valid when the call returns. A ctx is used by one host thread.
+ *
+ * Data layout of one expert blob (host pool and device slot, dtype T = bf16 | fp32):
+ *   W13 [F][2][d]  row 2f = W1 row f ("gate"), row 2f+1 = W3 row f ("up")   (interleaved)
+ *   W2  [d][F]                                                               (row-major)
+ *   blob = W13 followed immediately by W2; 3*d*F*sizeof(T) bytes.
+ */
+#ifndef ODMOE_H_
+#define ODMOE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ODMOE_ABI_VERSION 1
+
+typedef enum {
+  ODMOE_OK = 0,
+  ODMOE_E_CONFIG = 1,    /* bad shape/config: k>E, zero dims, d%8, world % G, ... */
+  ODMOE_E_RANGE = 2,     /* layer / expert / token out of range                      */
+  ODMOE_E_NONFINITE = 3, /* NaN/Inf in a hidden state or logits                             */
+  ODMOE_E_BUDGET = 4,    /* a load would exceed the per-GPU slot budget                    */
+  ODMOE_E_STATE = 5,     /* evict of a non-resident expert, call on a destroyed/poisoned ctx, ...  */
+  ODMOE_E_PLAN = 6,      /* cardinality mismatch in placement                              */
+  ODMOE_E_NOMEM = 7,     /* host pin or device allocation failed                                   */
+  ODMOE_E_CUDA = 8,      /* CUDA error; the ctx is poisoned (every later call returns E_STATE)     */
+  ODMOE_E_NCCL = 9       /* NCCL error; the ctx is poisoned                                         */
+} odmoe_status;
+
+typedef enum { ODMOE_BF16 = 0, ODMOE_FP32 = 1 } odmoe_dtype;
+
+/* Where the loader's expert IDs come from (P:250-258 ablation cases in B200 form). */
+typedef enum {
+  ODMOE_PRED_SHADOW_INT8 = 0, /* SEP with an INT8-row quantised shadow (Q9, Q10)    */
+  ODMOE_PRED_NONE = 1,        /* load only after the main router (P:257 case 6)                         */
+  ODMOE_PRED_RANDOM = 2,      /* uniformly random k experts per layer (P:256 case 5; E[recall] = k/E)    */
+  ODMOE_PRED_PERFECT = 3,     /* replay of the true routing recorded by an earlier run of the same ctx   */
+  ODMOE_PRED_SHADOW_SAME = 4  /* shadow with the main model's own weights (recall must be exactly 1.0)   */
+} odmoe_predictor;
+
+typedef struct {
+  int32_t L, E, k, d, F, V;  /* Mixtral 32,8,2,4096,14336,32000; tiny 4,8,2,256,512,1024           */
+  int32_t dtype;             /* odmoe_dtype of the main model's weights and of the normalised input u */
+  int32_t predictor;         /* odmoe_predictor                                                       */
+  int32_t lookahead;         /* D >= 1: loads may be issued for layers <= current + D (Q11)           */
+  int32_t slots_per_gpu;     /* device expert slots per GPU (>= k/G); -1 = fully resident baseline     */
+  float rms_eps;             /* RMSNorm epsilon (1e-5, Q7)                                             */
+  uint64_t weight_seed;      /* synthetic weights: counter-based generator               */
+  uint64_t aux_seed;         /* RANDOM predictor stream                                                */
+  int32_t rank, world_size;  /* this process's rank; number of GPUs (1, 2, 4, 8)                       */
+  int32_t group_size;        /* G; 0 => min(k, world_size) (Q14)                                */
+  int32_t device;            /* CUDA device ordinal of this rank                                       */
+  int64_t chunk_bytes;       /* H2D copy chunk (0 => 32 MiB)                                            */
+  int32_t debug_capture;     /* 1 => keep every per-layer intermediate on the host (parity tests)      */
+  int32_t time_kernels;      /* 1 => CUDA events around every kernel (bench roofline)                  */
+  int32_t pool_threads;      /* host threads used to build the pool (0 => all)                         */
+  int32_t reserved[7];
+  const void* nccl_id;       /* 128-byte ncclUniqueId from rank 0 (NULL when world_size == 1)          */
+} odmoe_config;
+
+/* One per layer per decode step (S:154-157 RoutingRecord). k <= 8. */
+typedef struct {
+  int32_t true_ids[8];       /* main-router top-k, rank order                                          */
+  int32_t pred_ids[8];       /* predictor's ids for this layer (-1 = none)                             */
+  float weights[8];          /* mixture weights, aligned with true_ids                                 */
+  int32_t pred_available;    /* 0 => no prediction existed when the router ran (c = 0)          */
+  int32_t correct;           /* c(n, l) = |true ∩ pred| (Eq. 2 numerator term)                   */
+  int32_t n_reloads;         /* experts loaded after the router because the prediction missed  */
+  float load_wait_us;        /* host-observed wait for this layer's experts                            */
+} odmoe_layer_record;
+
+typedef struct {
+  int64_t tokens;            /* decode steps since reset                                              */
+  int64_t loads_issued;      /* expert loads started (incl. reloads and wasted loads)                 */
+  int64_t loads_completed;
+  int64_t loads_cancelled;   /* mispredicted loads stopped before their last chunk                    */
+  int64_t reloads;           /* loads issued after the router (misprediction fallback)         */
+  int64_t bytes_h2d;         /* bytes copied host->device by the loader                              */
+  int64_t kernel_launches;   /* kernels this library launched                                        */
+  int64_t max_resident;      /* peak number of occupied expert slots on this GPU (S:326 audit)       */
+  int64_t resident_bytes;    /* device bytes of expert slots (slots_per_gpu * blob)                   */
+  int64_t shadow_bytes;      /* device bytes of the shadow model on this GPU                          */
+  int64_t pool_bytes;        /* pinned host pool bytes on this rank                                   */
+  double pool_build_s;       /* seconds spent pinning + generating the pool                           */
+  /* time_kernels: summed device time (ms) and launch count per kernel family */
+  double ms_router, ms_w13, ms_w2, ms_shadow, ms_lm_head, ms_embed;
+  int64_t n_router, n_w13, n_w2, n_shadow, n_lm_head, n_embed;
+  double wait_us;            /* host time blocked on loads                                            */
+  int64_t correct, predicted_total; /* Σc and Σ k over layers with a prediction (rank 0)              */
+} odmoe_stats;
+
+/* ------------------------------------------------------------------ lifecycle */
+int32_t odmoe_abi_version(void);
+odmoe_status odmoe_create(const odmoe_config* cfg, void** ctx_out);
+/* Generates the synthetic model from cfg->weight_seed, pins + fills this rank's host pool,
+ * quantises the shadow (rank 0), allocates slots, joins the NCCL communicator.
+ * Errors: E_CONFIG (validation), E_NOMEM, E_CUDA, E_NCCL. *ctx_out is NULL on error. */
+void odmoe_destroy(void* ctx);
+const char* odmoe_last_error(const void* ctx); /* ctx==NULL => last create error of this thread */
+odmoe_status odmoe_get_stats(const void* ctx, odmoe_stats* out);
+odmoe_status odmoe_reset_stats(void* ctx);
+int odmoe_nccl_unique_id(void* out128); /* fills a 128-byte ncclUniqueId; returns 0 on success */
+
+/* ------------------------------------------------------------------ stateless kernels */
+
+/* Fused residual-combine + RMSNorm + router GEMV + softmax/top-k + renormalise
+ * (a2+a3 of SURVEY §8(a); Q2, Q3, Q7).
+ *   h      [m,d] fp32 residual stream (in/out): h += y_add[0] + ... + y_add[n_add-1]
+ *          (added in the order given), written back to h.
+ *   y_add  device array of n_add device pointers to fp32 [m,d] partial outputs (may be NULL)
+ *   gamma  [d] of dtype dt, or NULL (=1)
+ *   w_gate [E,d] of dtype dt
+ *   u_out  [m,d] dtype dt: RMSNorm(h) rounded to dt (RNE)
+ *   ids    [m,k] int32, rank order (logit desc, lower index on ties)
+ *   w      [m,k] fp32 softmax over the selected logits
+ *   logits [m,E] fp32 or NULL
+ *   flag   int32 device scalar or NULL: set to 1 if any logit is non-finite
+ * Limits: 1 <= k <= E <= 64, k <= 8, d % 8 == 0. */
+odmoe_status odmoe_route_topk(float* h, const float* const* y_add, int n_add, const void* gamma,
+                              const void* w_gate, int m, int E, int d, int k, int dt, float eps,
+                              void* u_out, int32_t* ids, float* w, float* logits, int32_t* flag,
+                              void* stream);
+
+/* Expert SwiGLU FFN at batch 1 (a8; Q1, Q8):
+ *   a = silu(W1 u) * (W3 u)  (fp32, scratch [F]),  y = gate_w[gate_idx] * (W2 a)  (fp32 [d]).
+ *   w13 [F][2][d] dt, w2 [d][F] dt, u [d] dt, gate_w device fp32 array (NULL => 1.0),
+ *   a_scratch fp32 [F] device, y fp32 [d] (overwritten).
+ * Limits: d % 8 == 0, F % 8 == 0. */
+odmoe_status odmoe_expert_ffn(const void* w13, const void* w2, const void* u, const float* gate_w,
+                              int gate_idx, int d, int F, int dt, float* a_scratch, float* y,
+                              void* stream);
+
+/* Shadow expert FFN with INT8-row weights (a4; Q9):
+ *   q13 [F][2][d] int8 with s13 [2F] fp32 row scales; q2 [d][F] int8 with s2 [d] fp32;
+ *   u [d] bf16. Same math as odmoe_expert_ffn with W = s_r * q_r. */
+odmoe_status odmoe_shadow_expert_ffn(const int8_t* q13, const float* s13, const int8_t* q2,
+                                     const float* s2, const void* u, const float* gate_w,
+                                     int gate_idx, int d, int F, float* a_scratch, float* y,
+                                     void* stream);
+
+/* Router over INT8-row weights (shadow gating): like odmoe_route_topk with w_gate = s_e*q_e,
+ * gamma = 1, u_out bf16. */
+odmoe_status odmoe_shadow_route_topk(float* h, const float* const* y_add, int n_add,
+                                     const int8_t* q_gate, const float* s_gate, int m, int E, int d,
+                                     int k, float eps, void* u_out, int32_t* ids, float* w,
+                                     float* logits, int32_t* flag, void* stream);
+
+/* Final RMSNorm + LM head GEMV + greedy argmax (a10; S:95 lowest id on ties).
+ *   h [d] fp32 (h_L), lm_head [V,d] dt; token_out int32 device scalar;
+ *   logits [V] fp32 or NULL; scratch: device buffer of >= 16*4096 bytes. */
+odmoe_status odmoe_lm_head_argmax(const float* h, const void* lm_head, int V, int d, int dt,
+                                  float eps, int32_t* token_out, float* logits, void* scratch,
+                                  void* stream);
+
+/* INT8 per-row quantiser (Q9): q = clamp(RNE((W*127)/m_r), -127, 127) in fp64,
+ * s = fl32(m_r/127); zero rows -> q = 0, s = 1.  w [R,C] dt -> q [R,C] int8, s [R] fp32. */
+odmoe_status odmoe_quantize_int8_rows(const void* w, int64_t R, int64_t C, int dt, int8_t* q,
+                                      float* s, void* stream);
+
+/* Synthetic weight generator: out[i] = dt(fl32(v_i * fl32(1/sqrt(fan_in)))),
+ * v_i from splitmix64(seed, tensor_id, i). kind: 1 emb, 2 router, 3 W1, 4 W3, 5 W2, 6 LM head;
+ * kind 0 = the interleaved expert blob of (layer, expert) (W13 then W2; rows/cols ignored). */
+odmoe_status odmoe_gen_weights(void* out, int kind, int layer, int expert, int64_t rows,
+                               int64_t cols, int64_t fan_in, int d, int F, uint64_t seed, int dt,
+                               void* stream);
+
+/* ------------------------------------------------------------------ stateful engine */
+
+/* Async H2D load of expert (layer, expert) into a free slot of this rank's GPU.
+ * OK no-op if already resident or loading; E_BUDGET if every slot is occupied;
+ * E_RANGE if this rank's pool does not hold that expert. */
+odmoe_status odmoe_load(void* ctx, int layer, int expert);
+/* Block until (layer, expert) is resident; *w13 / *w2 receive its device pointers. */
+odmoe_status odmoe_load_wait(void* ctx, int layer, int expert, void** w13, void** w2);
+/* Free the slot once work already enqueued on the compute stream is done ("promptly evicts
+ * it afterward"; Q16). E_STATE if the expert is not resident/loading. */
+odmoe_status odmoe_evict(void* ctx, int layer, int expert);
+
+/* SEP Mode A (Q10): run the shadow from the main model's token `token`
+ * through all L layers (token alignment, T1), cache the predictions for that token and
+ * copy P[from_layer .. from_layer+depth) x k (rank order) into pred_ids (host, int32).
+ * Rank 0 only (E_STATE elsewhere). */
+odmoe_status odmoe_predict_ahead(void* ctx, int32_t token, int from_layer, int depth,
+                                 int32_t* pred_ids);
+
+/* One decode iteration: embed token_in, L x [router -> (prediction check,
+ * reload) -> expert FFNs on their GPUs -> combine], LM head, argmax. Collective: every rank
+ * calls it with the same token_in. token_out (host) is valid on every rank. rec [L] host or
+ * NULL (filled on rank 0). Synchronous. */
+odmoe_status odmoe_decode_step(void* ctx, int32_t token_in, int32_t* token_out,
+                               odmoe_layer_record* rec);
+
+/* Batched prefill of T tokens: no prediction; tokens grouped per expert; grouped
+ * expert GEMM; token_out = argmax after the last prompt token; expert_counts [L,E] host or
+ * NULL. Collective, synchronous. */
+odmoe_status odmoe_prefill(void* ctx, const int32_t* tokens, int T, int32_t* token_out,
+                           int32_t* expert_counts);
+
+/* Parity capture (cfg.debug_capture == 1), rank 0, last decode step. Copies `bytes` bytes of
+ * field `what` for `layer` into host `dst`. Fields and sizes:
+ *   0 H_IN fp32[d]  1 U dt[d]  2 LOGITS fp32[E]  3 IDS int32[k]  4 W fp32[k]
+ *   5 Y fp32[d] (combined)  6 Y_PART fp32[k][d] (N=1: per selected expert, rank order)
+ *   7 SH_H_IN fp32[d]  8 SH_U bf16[d]  9 SH_LOGITS fp32[E]  10 SH_IDS int32[k]
+ *   11 H_FINAL fp32[d] (layer ignored)  12 LM_LOGITS fp32[V] (layer ignored) */
+odmoe_status odmoe_debug_read(const void* ctx, int what, int layer, void* dst, int64_t bytes);
+
+/* Device pointers of ctx-owned tensors (tests): 0 emb, 1 lm_head, 2 router[layer],
+ * 3 shadow q_gate[layer], 4 shadow s_gate[layer], 5 shadow q13[layer*E+e] (layer, expert via
+ * `index` = layer*E+expert), 6 s13, 7 q2, 8 s2, 9 shadow q_emb, 10 shadow s_emb. */
+odmoe_status odmoe_tensor_ptr(const void* ctx, int what, int index, void** ptr);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ODMOE_H_ */

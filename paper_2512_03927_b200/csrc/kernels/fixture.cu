@@ -1,0 +1,132 @@
+// Synthetic-weight generator and the INT8-row shadow quantiser (product side).
+//
+// The generator is the counter-based recipe of DESIGN.md §3, implemented here independently of
+// inputs/fixture.py (tests check both give identical bytes). It is setup, not the hot path: the
+// engine uses it to fill the pinned host expert pool and the resident non-expert weights.
+//
+// The quantiser is the shadow's INT8 format (P:86, P:164 name INT8 without a format; reading Q9):
+// per output row, m = max|w|, q = clamp(RNE((w*127)/m), -127, 127) with the product and quotient
+// in fp64 (so exact half-ties are resolved by RNE), s = fl32(m/127); zero rows -> q=0, s=1.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace odmoe {
+
+constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;
+
+__host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
+  z += kGolden;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+static uint64_t stream_base(uint64_t seed, uint64_t tid) { return splitmix64(splitmix64(seed) ^ tid); }
+static uint64_t tensor_id(int kind, int layer, int expert) {
+  return ((uint64_t)kind << 40) | ((uint64_t)layer << 20) | (uint64_t)expert;
+}
+static float fan_in_scale(int64_t fan_in) { return (float)(1.0 / sqrt((double)fan_in)); }
+
+__device__ __forceinline__ float gen_value(uint64_t base, uint64_t i, float scale) {
+  const uint64_t x = splitmix64(base + i);
+  const int32_t u24 = (int32_t)(x >> 40);
+  const float v = (float)(2 * u24 - 16777215) * 5.9604644775390625e-08f;  // exact: odd / 2^24
+  return __fmul_rn(v, scale);
+}
+
+template <typename T> __device__ __forceinline__ T to_t(float v);
+template <> __device__ __forceinline__ __nv_bfloat16 to_t<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+template <> __device__ __forceinline__ float to_t<float>(float v) { return v; }
+
+template <typename T>
+__global__ void gen_plain_kernel(T* __restrict__ out, uint64_t base, long long n, float scale) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = to_t<T>(gen_value(base, (uint64_t)i, scale));
+}
+
+// Expert blob: W13 [F][2][d] interleaved (row 2f = W1 row f, 2f+1 = W3 row f), then W2 [d][F].
+template <typename T>
+__global__ void gen_blob_kernel(T* __restrict__ out, uint64_t b1, uint64_t b3, uint64_t b2, int d,
+                                int F, float s_d, float s_f) {
+  const long long n13 = 2LL * F * d, n = 3LL * F * d;
+  for (long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x; o < n; o += (long long)gridDim.x * blockDim.x) {
+    float v;
+    if (o < n13) {
+      const long long row = o / d, j = o - row * d;
+      const long long f = row >> 1;
+      v = gen_value((row & 1) ? b3 : b1, (uint64_t)(f * d + j), s_d);
+    } else {
+      v = gen_value(b2, (uint64_t)(o - n13), s_f);
+    }
+    out[o] = to_t<T>(v);
+  }
+}
+
+cudaError_t launch_gen(void* out, int kind, int layer, int expert, int64_t rows, int64_t cols,
+                       int64_t fan_in, int d, int F, uint64_t seed, WType wt, cudaStream_t s) {
+  const int grid = num_sms() * 8, block = 256;
+  if (kind == 0) {
+    const uint64_t b1 = stream_base(seed, tensor_id(3, layer, expert));
+    const uint64_t b3 = stream_base(seed, tensor_id(4, layer, expert));
+    const uint64_t b2 = stream_base(seed, tensor_id(5, layer, expert));
+    const float sd = fan_in_scale(d), sf = fan_in_scale(F);
+    if (wt == W_BF16) gen_blob_kernel<__nv_bfloat16><<<grid, block, 0, s>>>((__nv_bfloat16*)out, b1, b3, b2, d, F, sd, sf);
+    else if (wt == W_F32) gen_blob_kernel<float><<<grid, block, 0, s>>>((float*)out, b1, b3, b2, d, F, sd, sf);
+    else return cudaErrorInvalidValue;
+  } else {
+    const uint64_t b = stream_base(seed, tensor_id(kind, layer, expert));
+    const float sc = fan_in_scale(fan_in);
+    if (wt == W_BF16) gen_plain_kernel<__nv_bfloat16><<<grid, block, 0, s>>>((__nv_bfloat16*)out, b, rows * cols, sc);
+    else if (wt == W_F32) gen_plain_kernel<float><<<grid, block, 0, s>>>((float*)out, b, rows * cols, sc);
+    else return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- INT8-row quantiser
+template <typename T> __device__ __forceinline__ float ld_f(const T* p, long long i);
+template <> __device__ __forceinline__ float ld_f<__nv_bfloat16>(const __nv_bfloat16* p, long long i) { return __bfloat162float(p[i]); }
+template <> __device__ __forceinline__ float ld_f<float>(const float* p, long long i) { return p[i]; }
+
+template <typename T>
+__global__ void __launch_bounds__(256) quantize_rows_kernel(const T* __restrict__ w, long long C,
+                                                            int8_t* __restrict__ q, float* __restrict__ sc) {
+  __shared__ float red[8];
+  const long long r = blockIdx.x;
+  const T* wr = w + r * C;
+  float m = 0.f;
+  for (long long j = threadIdx.x; j < C; j += blockDim.x) m = fmaxf(m, fabsf(ld_f<T>(wr, j)));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t = fmaxf(t, red[i]);
+    red[0] = t;
+  }
+  __syncthreads();
+  m = red[0];
+  if (threadIdx.x == 0) sc[r] = m > 0.f ? __double2float_rn((double)m / 127.0) : 1.0f;
+  const double md = (double)m;
+  for (long long j = threadIdx.x; j < C; j += blockDim.x) {
+    int8_t code = 0;
+    if (m > 0.f) {
+      int qi = __double2int_rn(((double)ld_f<T>(wr, j) * 127.0) / md);
+      qi = qi > 127 ? 127 : (qi < -127 ? -127 : qi);
+      code = (int8_t)qi;
+    }
+    q[r * C + j] = code;
+  }
+}
+
+cudaError_t launch_quantize(const void* w, int64_t R, int64_t C, WType wt, int8_t* q, float* sc,
+                            cudaStream_t s) {
+  if (R <= 0) return cudaSuccess;
+  if (wt == W_BF16) quantize_rows_kernel<__nv_bfloat16><<<(unsigned)R, 256, 0, s>>>((const __nv_bfloat16*)w, C, q, sc);
+  else if (wt == W_F32) quantize_rows_kernel<float><<<(unsigned)R, 256, 0, s>>>((const float*)w, C, q, sc);
+  else return cudaErrorInvalidValue;
+  return cudaGetLastError();
+}
+
+}  // namespace odmoe

@@ -1,0 +1,62 @@
+// Host-side launchers of the OD-MoE sm_100a kernels (internal to libodmoe.so).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace odmoe {
+
+enum WType { W_BF16 = 0, W_F32 = 1, W_I8 = 2 };
+
+int num_sms();  // cached SM count of the current device
+
+// a2+a3: h += sum(y_add); u = RMSNorm(h) (rounded to u's dtype); logits = W_g u; top-k; softmax.
+// wt: weight type of w_gate (W_I8 uses wg_scale[E]); u dtype = fp32 iff wt == W_F32, else bf16.
+cudaError_t launch_router(float* h, const float* const* y_add, int n_add, const void* gamma,
+                          const void* w_gate, const float* wg_scale, WType wt, int m, int E, int d,
+                          int k, float eps, void* u_out, int32_t* ids, float* w, float* logits,
+                          int32_t* flag, cudaStream_t s);
+
+// h += (y_0 + ... + y_{n-1}) (final residual combine before the LM head).
+cudaError_t launch_combine(float* h, const float* const* y_add, int n_add, int d, cudaStream_t s);
+
+// Which expert a GEMV reads. Direct: blob/scales given. Indirect (tbl != NULL): the expert id is
+// read on the device, so routing never round-trips through the host:
+//   pick = sorted ? (index of the `sel`-th smallest id among ids[0..k)) : sel
+//   blob = tbl[base + ids[pick]], scales = stbl ? stbl[base + ids[pick]] : NULL, gate = gate_w[pick]
+// Blob layout: W13 [F][2][d] then W2 [d][F]; int8 scales: s13 [2F] then s2 [d].
+struct ExpertRef {
+  const void* blob;
+  const float* scales;
+  const void* const* tbl;
+  const float* const* stbl;
+  const int32_t* ids;
+  int sel, base, k, sorted;
+};
+inline ExpertRef direct_ref(const void* blob, const float* scales, int gate_idx) {
+  return ExpertRef{blob, scales, nullptr, nullptr, nullptr, gate_idx, 0, 0, 0};
+}
+
+// a8 phase 1: a[f] = silu(g_f) * v_f with [g_f; v_f] = W13[2f:2f+2] u (int8: row scales).
+cudaError_t launch_w13(ExpertRef ex, WType wt, const void* u, int u_f32, float* a, int d, int F,
+                       cudaStream_t s);
+// a8 phase 2: y = gate_w[pick] * (W2 a) (int8: row scales); gate_w may be NULL (=1).
+cudaError_t launch_w2(ExpertRef ex, WType wt, const float* a, const float* gate_w, float* y, int d,
+                      int F, cudaStream_t s);
+
+// a10: token = argmax_v (W_o RMSNorm(h))_v, lowest id on ties. scratch >= 8*(grid+2) bytes.
+cudaError_t launch_lm_head(const float* h, const void* W, WType wt, int V, int d, float eps,
+                           int32_t* token_out, float* logits, void* scratch, cudaStream_t s);
+
+// a1: h = Emb[token] (fp32); int8 rows use emb_scale.
+cudaError_t launch_embed(const void* emb, const float* emb_scale, WType wt, const int32_t* token,
+                         int d, float* h, cudaStream_t s);
+
+// Synthetic weights. kind 1..6 plain tensor rows x cols; kind 0 = expert blob.
+cudaError_t launch_gen(void* out, int kind, int layer, int expert, int64_t rows, int64_t cols,
+                       int64_t fan_in, int d, int F, uint64_t seed, WType wt, cudaStream_t s);
+
+// Q9 int8-row quantiser of a [R, C] matrix of type wt (bf16 / fp32).
+cudaError_t launch_quantize(const void* w, int64_t R, int64_t C, WType wt, int8_t* q, float* sc,
+                            cudaStream_t s);
+
+}  // namespace odmoe

@@ -1,0 +1,142 @@
+// Decode engine state (internal to libodmoe.so). See odmoe.h for the contract and DESIGN.md §5
+// for the HBM layout.
+#pragma once
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../../include/odmoe.h"
+#include "../kernels/kernels.h"
+#include "loader.h"
+
+namespace odmoe {
+
+enum Family { K_ROUTER = 0, K_W13, K_W2, K_SHADOW, K_LM, K_EMBED, K_NFAM };
+
+struct Slot {
+  char* dev = nullptr;
+  int layer = -1, expert = -1;
+  bool occupied = false;
+  int64_t token = -1;              // decode step the occupant belongs to
+  cudaEvent_t ev_w13 = nullptr, ev_done = nullptr, ev_free = nullptr;
+  bool free_recorded = false;
+  std::shared_ptr<LoadReq> req;
+};
+
+struct Ctx {
+  odmoe_config cfg{};
+  std::string err;
+  bool poisoned = false;
+  int L = 0, E = 0, k = 0, d = 0, F = 0, V = 0;
+  WType wt = W_BF16;
+  size_t esz = 2;
+  int64_t blob_elems = 0, blob_bytes = 0, w13_bytes = 0;
+  int world = 1, rank = 0, G = 1, NG = 1, my_group = 0, my_pos = 0;
+  bool resident = false;
+  int dev = 0;
+  cudaStream_t s_main = nullptr, s_shadow = nullptr, s_copy = nullptr;
+
+  // non-expert weights (rank 0): embedding [V,d], LM head [V,d], routers [L][E][d]
+  void* d_emb = nullptr;
+  void* d_lm = nullptr;
+  void* d_router = nullptr;
+
+  // shadow model (rank 0)
+  bool has_shadow = false;
+  WType sh_wt = W_I8;
+  void* sh_emb = nullptr;      // int8 [V,d] (or main dtype for SHADOW_SAME)
+  float* sh_semb = nullptr;    // [V]
+  void* sh_router = nullptr;   // [L][E][d]
+  float* sh_srouter = nullptr; // [L][E]
+  std::vector<void*> sh_blob;  // [L*E] int8 blobs (q13 then q2)
+  std::vector<float*> sh_sc;   // [L*E] scales (s13 [2F] then s2 [d])
+  void** d_sh_tbl = nullptr;
+  float** d_sh_stbl = nullptr;
+
+  // host pool (pinned): blob of (l, e) at pool + pool_off[l*E+e] (-1 if not on this rank)
+  char* pool = nullptr;
+  int64_t pool_bytes = 0;
+  std::vector<int64_t> pool_off;
+
+  // resident experts (slots_per_gpu == -1, or SHADOW_SAME)
+  std::vector<char*> res_blob;
+  void** d_res_tbl = nullptr;
+
+  std::vector<Slot> slots;
+  Loader loader;
+
+  // device work buffers
+  float* d_h = nullptr;          // residual [d]
+  char* d_pkt = nullptr;         // [L] packets: u [d] dt | ids [k] int32 | w [k] fp32
+  int64_t pkt_bytes = 0, pkt_ids_off = 0, pkt_w_off = 0;
+  float* d_logits = nullptr;     // [L][E]
+  float* d_a = nullptr;          // [k][F]
+  float* d_y = nullptr;          // [k][d] per-expert outputs (this GPU)
+  float* d_yred = nullptr;       // [d] reduced output (rank 0, N > 1)
+  float* d_zero = nullptr;       // [d] zeros (idle ranks' reduce contribution)
+  const float** d_yptr = nullptr;    // [k] -> d_y parts (N = 1)
+  const float** d_yredptr = nullptr; // [1] -> d_yred
+  int32_t* d_tok_in = nullptr;
+  int32_t* d_tok_out = nullptr;
+  int32_t* d_flag = nullptr;
+  void* d_lmscratch = nullptr;
+  float* d_lmlogits = nullptr;   // [V] (debug)
+
+  // shadow work buffers (rank 0)
+  float* sh_h = nullptr;
+  void* sh_u = nullptr;
+  int32_t* sh_ids = nullptr;     // [L][k]
+  float* sh_w = nullptr;         // [L][k]
+  float* sh_logits = nullptr;    // [L][E]
+  float* sh_a = nullptr;         // [k][F]
+  float* sh_y = nullptr;         // [k][d]
+  const float** sh_yptr = nullptr;
+
+  // pinned host mirrors
+  int32_t* h_ids = nullptr;      // [L][k]
+  float* h_w = nullptr;          // [L][k]
+  int32_t* h_pred = nullptr;     // [L][k]
+  int32_t* h_tok = nullptr;      // [2]: in, out
+  int32_t* h_flag = nullptr;
+  cudaEvent_t ev_ids = nullptr, ev_tok = nullptr, ev_shadow_done = nullptr, ev_step = nullptr;
+  std::vector<cudaEvent_t> ev_pred;  // [L] (per layer at N = 1; per chunk at N > 1)
+  int pred_chunk = 4;
+
+  ncclComm_t comm = nullptr, comm_pred = nullptr;
+
+  // per-step scheduler state
+  int64_t step = 0;
+  std::vector<char> pred_ready;  // [L]
+  bool pred_valid = false;       // a prediction source exists this step
+  int next_plan = 0;             // next layer whose predicted loads are not yet planned
+  int l_cur = 0;
+  std::vector<int32_t> pred_tbl; // [L][k] predictions this step (host)
+
+  // PERFECT predictor: routing recorded per input token (Mode A: routing is a function of the
+  // token only, there is no KV state on the hot path)
+  std::map<int32_t, std::vector<int32_t>> route_cache;
+  int32_t predict_cache_token = -1;
+
+  // kernel timing (time_kernels)
+  struct Timed { int fam; cudaEvent_t a, b; };
+  std::vector<Timed> timed;
+  std::vector<cudaEvent_t> tev_pool;
+
+  odmoe_stats stats{};
+
+  // debug capture (rank 0)
+  float* dbg_h = nullptr;        // device [L][d]
+  float* dbg_ypart = nullptr;    // device [L][k][d]
+  float* dbg_yred = nullptr;     // device [L][d]
+  float* dbg_sh_h = nullptr;     // device [L][d]
+  void* dbg_sh_u = nullptr;      // device [L][d] bf16/dt
+  float* dbg_hfinal = nullptr;   // device [d]
+  std::vector<char> hdbg;        // host copy of everything after the step
+  std::map<int, std::pair<int64_t, int64_t>> hdbg_index;  // what -> (offset, per-layer bytes)
+};
+
+}  // namespace odmoe

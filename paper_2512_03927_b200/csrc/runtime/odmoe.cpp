@@ -1,0 +1,1182 @@
+// C ABI of libodmoe.so: stateless kernel entry points and the stateful OD-MoE decode engine.
+// Contract: include/odmoe.h. Design: DESIGN.md §5-§7.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "engine.h"
+
+using namespace odmoe;
+
+namespace {
+
+thread_local std::string t_create_err;
+
+struct Fail {
+  odmoe_status st;
+};
+
+// Every internal error path throws Fail (caught at the ABI boundary).
+[[noreturn]] void fail(Ctx* c, odmoe_status st, const std::string& msg) {
+  if (c) {
+    c->err = msg;
+    if (st == ODMOE_E_CUDA || st == ODMOE_E_NCCL) c->poisoned = true;
+  } else {
+    t_create_err = msg;
+  }
+  throw Fail{st};
+}
+
+#define CUDA_OK(c, x)                                                                          \
+  do {                                                                                         \
+    cudaError_t _e = (x);                                                                      \
+    if (_e != cudaSuccess)                                                                     \
+      fail((c), ODMOE_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(_e) + " @" +         \
+                                  std::to_string(__LINE__));                                   \
+  } while (0)
+
+#define NCCL_OK(c, x)                                                                          \
+  do {                                                                                         \
+    ncclResult_t _r = (x);                                                                     \
+    if (_r != ncclSuccess)                                                                     \
+      fail((c), ODMOE_E_NCCL, std::string(#x) + ": " + ncclGetErrorString(_r));                \
+  } while (0)
+
+template <typename F>
+odmoe_status guard(Ctx* c, F&& f) {
+  try {
+    f();
+    return ODMOE_OK;
+  } catch (const Fail& e) {
+    return e.st;
+  } catch (const std::bad_alloc&) {
+    if (c) c->err = "host allocation failed";
+    return ODMOE_E_NOMEM;
+  } catch (...) {
+    if (c) c->err = "unexpected exception";
+    return ODMOE_E_STATE;
+  }
+}
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+inline WType wtype(int dt) { return dt == ODMOE_FP32 ? W_F32 : W_BF16; }
+inline size_t dsize(int dt) { return dt == ODMOE_FP32 ? 4 : 2; }
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+template <typename T>
+T* dmalloc(Ctx* c, size_t n, const char* what) {
+  void* p = nullptr;
+  if (n == 0) n = 1;
+  cudaError_t e = cudaMalloc(&p, n * sizeof(T));
+  if (e != cudaSuccess) fail(c, ODMOE_E_NOMEM, std::string("cudaMalloc ") + what + " (" + std::to_string(n * sizeof(T)) + " B): " + cudaGetErrorString(e));
+  return reinterpret_cast<T*>(p);
+}
+
+template <typename T>
+T* hmalloc(Ctx* c, size_t n, const char* what) {
+  void* p = nullptr;
+  if (n == 0) n = 1;
+  cudaError_t e = cudaHostAlloc(&p, n * sizeof(T), cudaHostAllocPortable);
+  if (e != cudaSuccess) fail(c, ODMOE_E_NOMEM, std::string("cudaHostAlloc ") + what + " (" + std::to_string(n * sizeof(T)) + " B): " + cudaGetErrorString(e));
+  return reinterpret_cast<T*>(p);
+}
+
+// ------------------------------------------------------------------ kernel timing + counting
+struct KTimer {
+  Ctx* c;
+  int fam;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr, b = nullptr;
+  KTimer(Ctx* c_, int fam_, cudaStream_t s_) : c(c_), fam(fam_), s(s_) {
+    c->stats.kernel_launches++;
+    if (!c->cfg.time_kernels) return;
+    a = get();
+    b = get();
+    cudaEventRecord(a, s);
+  }
+  ~KTimer() {
+    if (!a) return;
+    cudaEventRecord(b, s);
+    c->timed.push_back(Ctx::Timed{fam, a, b});
+  }
+  cudaEvent_t get() {
+    if (!c->tev_pool.empty()) {
+      cudaEvent_t e = c->tev_pool.back();
+      c->tev_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+
+void harvest_timers(Ctx* c) {
+  for (auto& t : c->timed) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, t.a, t.b) == cudaSuccess) {
+      switch (t.fam) {
+        case K_ROUTER: c->stats.ms_router += ms; c->stats.n_router++; break;
+        case K_W13: c->stats.ms_w13 += ms; c->stats.n_w13++; break;
+        case K_W2: c->stats.ms_w2 += ms; c->stats.n_w2++; break;
+        case K_SHADOW: c->stats.ms_shadow += ms; c->stats.n_shadow++; break;
+        case K_LM: c->stats.ms_lm_head += ms; c->stats.n_lm_head++; break;
+        case K_EMBED: c->stats.ms_embed += ms; c->stats.n_embed++; break;
+      }
+    }
+    c->tev_pool.push_back(t.a);
+    c->tev_pool.push_back(t.b);
+  }
+  c->timed.clear();
+}
+
+// ------------------------------------------------------------------ placement
+// Experts of layer l handled by this rank given routing S (k ids): empty unless this rank is in
+// group l mod N_G; sorted experts paired with sorted group GPUs; with G < k a GPU takes
+// k/G consecutive sorted experts (reading Q14).
+std::vector<int> my_experts(const Ctx* c, int l, const int32_t* S) {
+  std::vector<int> out;
+  if ((l % c->NG) != c->my_group) return out;
+  std::vector<int> s(S, S + c->k);
+  std::sort(s.begin(), s.end());
+  for (int i = 0; i < c->k; ++i)
+    if (i * c->G / c->k == c->my_pos) out.push_back(s[i]);
+  return out;
+}
+
+bool holds_expert(const Ctx* c, int l, int e) { return c->pool_off[(size_t)l * c->E + e] >= 0; }
+
+// ------------------------------------------------------------------ validation
+void validate(const odmoe_config* g) {
+  auto bad = [](const std::string& m) { fail(nullptr, ODMOE_E_CONFIG, m); };
+  if (!g) bad("null config");
+  if (g->L < 1 || g->E < 1 || g->k < 1 || g->d < 8 || g->F < 8 || g->V < 2) bad("non-positive dimension");
+  if (g->k > g->E || g->k > 8 || g->E > 64) bad("need 1 <= k <= E <= 64 and k <= 8");
+  if (g->d % 8 || g->F % 8) bad("d and F must be multiples of 8");
+  if (g->dtype != ODMOE_BF16 && g->dtype != ODMOE_FP32) bad("dtype");
+  if (g->predictor < 0 || g->predictor > 4) bad("predictor");
+  if (g->lookahead < 1) bad("lookahead must be >= 1");
+  if (g->world_size < 1 || g->rank < 0 || g->rank >= g->world_size) bad("rank/world_size");
+  const int G = g->group_size > 0 ? g->group_size : std::min(g->k, g->world_size);
+  if (g->world_size % G) bad("world_size must be divisible by the group size (S:251, S:269)");
+  if (g->k % G) bad("k must be divisible by the group size");
+  if (g->world_size > 1 && G != g->k) bad("multi-GPU needs group_size == k (one expert per GPU per layer)");
+  if (g->slots_per_gpu != -1 && g->slots_per_gpu < g->k / G) bad("slots_per_gpu must be >= k/G or -1");
+  if (g->world_size > 1 && g->nccl_id == nullptr) bad("nccl_id required when world_size > 1");
+}
+
+// ------------------------------------------------------------------ setup
+void build_nonexpert(Ctx* c) {
+  const int L = c->L, E = c->E, d = c->d, V = c->V;
+  const uint64_t seed = c->cfg.weight_seed;
+  c->d_emb = dmalloc<char>(c, (size_t)V * d * c->esz, "emb");
+  c->d_lm = dmalloc<char>(c, (size_t)V * d * c->esz, "lm_head");
+  c->d_router = dmalloc<char>(c, (size_t)L * E * d * c->esz, "router");
+  CUDA_OK(c, launch_gen(c->d_emb, 1, 0, 0, V, d, d, d, c->F, seed, c->wt, c->s_main));
+  CUDA_OK(c, launch_gen(c->d_lm, 6, 0, 0, V, d, d, d, c->F, seed, c->wt, c->s_main));
+  for (int l = 0; l < L; ++l)
+    CUDA_OK(c, launch_gen((char*)c->d_router + (size_t)l * E * d * c->esz, 2, l, 0, E, d, d, d, c->F, seed, c->wt, c->s_main));
+}
+
+void build_shadow(Ctx* c, char* staging) {
+  const int L = c->L, E = c->E, d = c->d, V = c->V, F = c->F;
+  if (c->cfg.predictor == ODMOE_PRED_SHADOW_SAME) {
+    // The shadow runs the main model's own weights (recall must be exactly 1.0).
+    c->sh_wt = c->wt;
+    c->sh_emb = c->d_emb;
+    c->sh_router = c->d_router;
+    c->d_sh_tbl = c->d_res_tbl;
+    c->d_sh_stbl = nullptr;
+    return;
+  }
+  c->sh_wt = W_I8;
+  c->sh_emb = dmalloc<int8_t>(c, (size_t)V * d, "shadow emb");
+  c->sh_semb = dmalloc<float>(c, V, "shadow emb scales");
+  c->sh_router = dmalloc<int8_t>(c, (size_t)L * E * d, "shadow router");
+  c->sh_srouter = dmalloc<float>(c, (size_t)L * E, "shadow router scales");
+  CUDA_OK(c, launch_quantize(c->d_emb, V, d, c->wt, (int8_t*)c->sh_emb, c->sh_semb, c->s_main));
+  CUDA_OK(c, launch_quantize(c->d_router, (int64_t)L * E, d, c->wt, (int8_t*)c->sh_router, c->sh_srouter, c->s_main));
+  c->sh_blob.assign((size_t)L * E, nullptr);
+  c->sh_sc.assign((size_t)L * E, nullptr);
+  for (int l = 0; l < L; ++l)
+    for (int e = 0; e < E; ++e) {
+      const size_t i = (size_t)l * E + e;
+      int8_t* q = dmalloc<int8_t>(c, (size_t)3 * F * d, "shadow expert");
+      float* s = dmalloc<float>(c, (size_t)2 * F + d, "shadow scales");
+      const char* src = staging;
+      if (!c->res_blob.empty() && c->res_blob[i]) {
+        src = c->res_blob[i];
+      } else {
+        CUDA_OK(c, launch_gen(staging, 0, l, e, 0, 0, 0, d, F, c->cfg.weight_seed, c->wt, c->s_main));
+      }
+      CUDA_OK(c, launch_quantize(src, 2LL * F, d, c->wt, q, s, c->s_main));
+      CUDA_OK(c, launch_quantize(src + (size_t)2 * F * d * c->esz, d, F, c->wt, q + (size_t)2 * F * d, s + 2 * F, c->s_main));
+      c->sh_blob[i] = q;
+      c->sh_sc[i] = s;
+      c->stats.shadow_bytes += (int64_t)3 * F * d + (int64_t)(2 * F + d) * 4;
+    }
+  c->stats.shadow_bytes += (int64_t)V * d + V * 4 + (int64_t)L * E * d + L * E * 4;
+  c->d_sh_tbl = dmalloc<void*>(c, (size_t)L * E, "shadow tbl");
+  c->d_sh_stbl = dmalloc<float*>(c, (size_t)L * E, "shadow stbl");
+  CUDA_OK(c, cudaMemcpyAsync(c->d_sh_tbl, c->sh_blob.data(), sizeof(void*) * L * E, cudaMemcpyHostToDevice, c->s_main));
+  CUDA_OK(c, cudaMemcpyAsync(c->d_sh_stbl, c->sh_sc.data(), sizeof(float*) * L * E, cudaMemcpyHostToDevice, c->s_main));
+  CUDA_OK(c, cudaStreamSynchronize(c->s_main));
+}
+
+// Which (layer, expert) blobs this rank may ever need: all experts of the layers of its group
+// that the sorted pairing can assign to its position.
+bool rank_may_need(const Ctx* c, int l, int e) {
+  if ((l % c->NG) != c->my_group) return false;
+  // with sorted pairing position p receives only experts with >= p*k/G smaller and
+  // >= (G-1-p)*k/G larger ids among the k selected
+  const int lo = c->my_pos * (c->k / c->G);
+  const int hi = (c->G - 1 - c->my_pos) * (c->k / c->G);
+  return e >= lo && e <= c->E - 1 - hi;
+}
+
+void build_pool(Ctx* c, char* staging) {
+  const int L = c->L, E = c->E, d = c->d, F = c->F;
+  const double t0 = now_s();
+  c->pool_off.assign((size_t)L * E, -1);
+  int64_t n = 0;
+  for (int l = 0; l < L; ++l)
+    for (int e = 0; e < E; ++e)
+      if (rank_may_need(c, l, e)) c->pool_off[(size_t)l * E + e] = (n++) * c->blob_bytes;
+  c->pool_bytes = n * c->blob_bytes;
+  if (c->resident) {
+    // fully-resident baseline: every blob this rank may need lives in HBM (same placement)
+    c->res_blob.assign((size_t)L * E, nullptr);
+    for (int l = 0; l < L; ++l)
+      for (int e = 0; e < E; ++e)
+        if (c->pool_off[(size_t)l * E + e] >= 0 || (c->rank == 0 && c->cfg.predictor == ODMOE_PRED_SHADOW_SAME)) {
+          char* p = dmalloc<char>(c, c->blob_bytes, "resident expert");
+          CUDA_OK(c, launch_gen(p, 0, l, e, 0, 0, 0, d, F, c->cfg.weight_seed, c->wt, c->s_main));
+          c->res_blob[(size_t)l * E + e] = p;
+          c->stats.resident_bytes += c->blob_bytes;
+        }
+    c->pool_bytes = 0;
+  } else {
+    if (c->rank == 0 && c->cfg.predictor == ODMOE_PRED_SHADOW_SAME) {
+      // SHADOW_SAME keeps a device copy of every expert for the shadow (tiny configs)
+      c->res_blob.assign((size_t)L * E, nullptr);
+      for (int l = 0; l < L; ++l)
+        for (int e = 0; e < E; ++e) {
+          char* p = dmalloc<char>(c, c->blob_bytes, "shadow-same expert");
+          CUDA_OK(c, launch_gen(p, 0, l, e, 0, 0, 0, d, F, c->cfg.weight_seed, c->wt, c->s_main));
+          c->res_blob[(size_t)l * E + e] = p;
+        }
+    }
+    c->pool = hmalloc<char>(c, (size_t)c->pool_bytes, "expert pool");
+    // Fill the pool: generate each blob on the GPU, copy D2H into its pinned slot.
+    char* stg[2] = {staging, staging + c->blob_bytes};
+    cudaEvent_t done[2];
+    CUDA_OK(c, cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming));
+    CUDA_OK(c, cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming));
+    bool used[2] = {false, false};
+    int i = 0;
+    for (int l = 0; l < L; ++l)
+      for (int e = 0; e < E; ++e) {
+        const int64_t off = c->pool_off[(size_t)l * E + e];
+        if (off < 0) continue;
+        const int b = i++ & 1;
+        if (used[b]) CUDA_OK(c, cudaEventSynchronize(done[b]));
+        CUDA_OK(c, launch_gen(stg[b], 0, l, e, 0, 0, 0, d, F, c->cfg.weight_seed, c->wt, c->s_main));
+        CUDA_OK(c, cudaMemcpyAsync(c->pool + off, stg[b], c->blob_bytes, cudaMemcpyDeviceToHost, c->s_main));
+        CUDA_OK(c, cudaEventRecord(done[b], c->s_main));
+        used[b] = true;
+      }
+    CUDA_OK(c, cudaStreamSynchronize(c->s_main));
+    cudaEventDestroy(done[0]);
+    cudaEventDestroy(done[1]);
+  }
+  if (!c->res_blob.empty()) {
+    c->d_res_tbl = dmalloc<void*>(c, (size_t)L * E, "resident tbl");
+    CUDA_OK(c, cudaMemcpy(c->d_res_tbl, c->res_blob.data(), sizeof(void*) * L * E, cudaMemcpyHostToDevice));
+  }
+  c->stats.pool_bytes = c->pool_bytes;
+  c->stats.pool_build_s = now_s() - t0;
+}
+
+void build_slots(Ctx* c) {
+  if (c->resident) return;
+  const int n = c->cfg.slots_per_gpu;
+  c->slots.resize(n);
+  for (auto& s : c->slots) {
+    s.dev = dmalloc<char>(c, c->blob_bytes, "expert slot");
+    CUDA_OK(c, cudaEventCreateWithFlags(&s.ev_w13, cudaEventDisableTiming));
+    CUDA_OK(c, cudaEventCreateWithFlags(&s.ev_done, cudaEventDisableTiming));
+    CUDA_OK(c, cudaEventCreateWithFlags(&s.ev_free, cudaEventDisableTiming));
+    s.req = std::make_shared<LoadReq>();
+  }
+  c->stats.resident_bytes = (int64_t)n * c->blob_bytes;
+}
+
+void build_buffers(Ctx* c) {
+  const int L = c->L, E = c->E, k = c->k, d = c->d, F = c->F, V = c->V;
+  c->pkt_ids_off = (int64_t)d * c->esz;
+  c->pkt_w_off = c->pkt_ids_off + 4 * k;
+  c->pkt_bytes = (c->pkt_w_off + 4 * k + 15) / 16 * 16;
+  c->d_h = dmalloc<float>(c, d, "h");
+  c->d_pkt = dmalloc<char>(c, (size_t)L * c->pkt_bytes, "packets");
+  c->d_logits = dmalloc<float>(c, (size_t)L * E, "logits");
+  c->d_a = dmalloc<float>(c, (size_t)k * F, "a");
+  c->d_y = dmalloc<float>(c, (size_t)k * d, "y");
+  c->d_yred = dmalloc<float>(c, d, "yred");
+  c->d_zero = dmalloc<float>(c, d, "zero");
+  CUDA_OK(c, cudaMemset(c->d_zero, 0, sizeof(float) * d));
+  CUDA_OK(c, cudaMemset(c->d_y, 0, sizeof(float) * k * d));
+  c->d_yptr = dmalloc<const float*>(c, k, "yptr");
+  c->d_yredptr = dmalloc<const float*>(c, 1, "yredptr");
+  std::vector<const float*> yp(k);
+  for (int j = 0; j < k; ++j) yp[j] = c->d_y + (size_t)j * d;
+  CUDA_OK(c, cudaMemcpy(c->d_yptr, yp.data(), sizeof(float*) * k, cudaMemcpyHostToDevice));
+  const float* yr = c->d_yred;
+  CUDA_OK(c, cudaMemcpy(c->d_yredptr, &yr, sizeof(float*), cudaMemcpyHostToDevice));
+  c->d_tok_in = dmalloc<int32_t>(c, 1, "tok_in");
+  c->d_tok_out = dmalloc<int32_t>(c, 1, "tok_out");
+  c->d_flag = dmalloc<int32_t>(c, 1, "flag");
+  CUDA_OK(c, cudaMemset(c->d_flag, 0, 4));
+  c->d_lmscratch = dmalloc<char>(c, 16 * 4096, "lm scratch");
+  CUDA_OK(c, cudaMemset(c->d_lmscratch, 0, 16 * 4096));
+  c->d_lmlogits = dmalloc<float>(c, V, "lm logits");
+  c->h_ids = hmalloc<int32_t>(c, (size_t)L * k, "h_ids");
+  c->h_w = hmalloc<float>(c, (size_t)L * k, "h_w");
+  c->h_pred = hmalloc<int32_t>(c, (size_t)L * k, "h_pred");
+  c->h_tok = hmalloc<int32_t>(c, 2, "h_tok");
+  c->h_flag = hmalloc<int32_t>(c, 1, "h_flag");
+  CUDA_OK(c, cudaEventCreateWithFlags(&c->ev_ids, cudaEventDisableTiming));
+  CUDA_OK(c, cudaEventCreateWithFlags(&c->ev_tok, cudaEventDisableTiming));
+  CUDA_OK(c, cudaEventCreateWithFlags(&c->ev_shadow_done, cudaEventDisableTiming));
+  CUDA_OK(c, cudaEventCreateWithFlags(&c->ev_step, cudaEventDisableTiming));
+  c->ev_pred.resize(L);
+  for (auto& e : c->ev_pred) CUDA_OK(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  c->pred_ready.assign(L, 0);
+  c->pred_tbl.assign((size_t)L * k, -1);
+  if (c->has_shadow) {
+    c->sh_h = dmalloc<float>(c, d, "sh_h");
+    c->sh_u = dmalloc<char>(c, (size_t)d * 4, "sh_u");
+    c->sh_ids = dmalloc<int32_t>(c, (size_t)L * k, "sh_ids");
+    c->sh_w = dmalloc<float>(c, (size_t)L * k, "sh_w");
+    c->sh_logits = dmalloc<float>(c, (size_t)L * E, "sh_logits");
+    c->sh_a = dmalloc<float>(c, (size_t)k * F, "sh_a");
+    c->sh_y = dmalloc<float>(c, (size_t)k * d, "sh_y");
+    c->sh_yptr = dmalloc<const float*>(c, k, "sh_yptr");
+    for (int j = 0; j < k; ++j) yp[j] = c->sh_y + (size_t)j * d;
+    CUDA_OK(c, cudaMemcpy(c->sh_yptr, yp.data(), sizeof(float*) * k, cudaMemcpyHostToDevice));
+  } else if (c->world > 1) {
+    c->sh_ids = dmalloc<int32_t>(c, (size_t)L * k, "sh_ids");  // receive buffer for P
+  }
+  if (c->cfg.debug_capture && c->rank == 0) {
+    c->dbg_h = dmalloc<float>(c, (size_t)L * d, "dbg_h");
+    c->dbg_ypart = dmalloc<float>(c, (size_t)L * k * d, "dbg_ypart");
+    c->dbg_yred = dmalloc<float>(c, (size_t)L * d, "dbg_yred");
+    c->dbg_sh_h = dmalloc<float>(c, (size_t)L * d, "dbg_sh_h");
+    c->dbg_sh_u = dmalloc<char>(c, (size_t)L * d * 4, "dbg_sh_u");
+    c->dbg_hfinal = dmalloc<float>(c, d, "dbg_hfinal");
+    CUDA_OK(c, cudaMemset(c->dbg_ypart, 0, sizeof(float) * L * k * d));
+    CUDA_OK(c, cudaMemset(c->dbg_yred, 0, sizeof(float) * L * d));
+  }
+}
+
+// ------------------------------------------------------------------ shadow forward (SEP, Mode A)
+// Enqueue the shadow pass for `token_dev` on s_shadow: embed, then L x [router, k expert FFNs]
+// with the shadow's own routing chosen on the device (Q10). Predictions land
+// in sh_ids [L][k]; at N = 1 each layer's ids are copied to h_pred with event ev_pred[l].
+void enqueue_shadow(Ctx* c, const int32_t* token_dev) {
+  const int L = c->L, E = c->E, k = c->k, d = c->d, F = c->F;
+  cudaStream_t s = c->s_shadow;
+  const bool same = c->cfg.predictor == ODMOE_PRED_SHADOW_SAME;
+  const WType swt = c->sh_wt;
+  const size_t sesz = swt == W_I8 ? 1 : c->esz;
+  {
+    KTimer t(c, K_SHADOW, s);
+    CUDA_OK(c, launch_embed(c->sh_emb, c->sh_semb, swt, token_dev, d, c->sh_h, s));
+  }
+  for (int l = 0; l < L; ++l) {
+    {
+      KTimer t(c, K_SHADOW, s);
+      CUDA_OK(c, launch_router(c->sh_h, c->sh_yptr, l > 0 ? k : 0, nullptr,
+                               (const char*)c->sh_router + (size_t)l * E * d * sesz,
+                               same ? nullptr : c->sh_srouter + (size_t)l * E, swt, 1, E, d, k,
+                               c->cfg.rms_eps, c->sh_u, c->sh_ids + (size_t)l * k,
+                               c->sh_w + (size_t)l * k, c->sh_logits + (size_t)l * E, nullptr, s));
+    }
+    if (c->dbg_sh_h) {
+      CUDA_OK(c, cudaMemcpyAsync(c->dbg_sh_h + (size_t)l * d, c->sh_h, sizeof(float) * d, cudaMemcpyDeviceToDevice, s));
+      CUDA_OK(c, cudaMemcpyAsync((char*)c->dbg_sh_u + (size_t)l * d * 4, c->sh_u, (size_t)d * (swt == W_F32 ? 4 : 2), cudaMemcpyDeviceToDevice, s));
+    }
+    if (c->world == 1) {
+      CUDA_OK(c, cudaMemcpyAsync(c->h_pred + (size_t)l * k, c->sh_ids + (size_t)l * k, 4 * k, cudaMemcpyDeviceToHost, s));
+      CUDA_OK(c, cudaEventRecord(c->ev_pred[l], s));
+    }
+    const int u_f32 = swt == W_F32;
+    for (int j = 0; j < k; ++j) {
+      ExpertRef ex{nullptr, nullptr, (const void* const*)c->d_sh_tbl, (const float* const*)c->d_sh_stbl,
+                   c->sh_ids + (size_t)l * k, j, l * E, k, 0};
+      {
+        KTimer t(c, K_SHADOW, s);
+        CUDA_OK(c, launch_w13(ex, swt, c->sh_u, u_f32, c->sh_a + (size_t)j * F, d, F, s));
+      }
+      {
+        KTimer t(c, K_SHADOW, s);
+        CUDA_OK(c, launch_w2(ex, swt, c->sh_a + (size_t)j * F, c->sh_w + (size_t)l * k, c->sh_y + (size_t)j * d, d, F, s));
+      }
+    }
+  }
+  CUDA_OK(c, cudaEventRecord(c->ev_shadow_done, s));
+}
+
+// At N > 1 rank 0 broadcasts the prediction table in chunks of pred_chunk layers over comm_pred
+// on s_shadow; every rank copies each chunk to h_pred and records ev_pred[first layer of chunk].
+void enqueue_pred_broadcast(Ctx* c) {
+  const int L = c->L, k = c->k;
+  cudaStream_t s = c->s_shadow;
+  for (int l0 = 0; l0 < L; l0 += c->pred_chunk) {
+    const int n = std::min(c->pred_chunk, L - l0);
+    NCCL_OK(c, ncclBroadcast(c->sh_ids + (size_t)l0 * k, c->sh_ids + (size_t)l0 * k, (size_t)n * k, ncclInt32, 0, c->comm_pred, s));
+    CUDA_OK(c, cudaMemcpyAsync(c->h_pred + (size_t)l0 * k, c->sh_ids + (size_t)l0 * k, 4 * n * k, cudaMemcpyDeviceToHost, s));
+    CUDA_OK(c, cudaEventRecord(c->ev_pred[l0], s));
+  }
+}
+
+// Prediction for layer m available on the host? (non-blocking)
+bool pred_available(Ctx* c, int m) {
+  if (!c->pred_valid) return false;
+  if (c->pred_ready[m]) return true;
+  const int p = c->cfg.predictor;
+  if (p == ODMOE_PRED_SHADOW_INT8 || p == ODMOE_PRED_SHADOW_SAME) {
+    const int evl = c->world == 1 ? m : (m / c->pred_chunk) * c->pred_chunk;
+    const cudaError_t q = cudaEventQuery(c->ev_pred[evl]);
+    if (q == cudaErrorNotReady) return false;
+    CUDA_OK(c, q);
+    const int hi = c->world == 1 ? m + 1 : std::min(c->L, evl + c->pred_chunk);
+    for (int l = evl; l < hi; ++l) {
+      c->pred_ready[l] = 1;
+      std::copy(c->h_pred + (size_t)l * c->k, c->h_pred + (size_t)(l + 1) * c->k, c->pred_tbl.begin() + (size_t)l * c->k);
+    }
+    return true;
+  }
+  return false;
+}
+
+// RANDOM predictor (P:256 case 5): k distinct uniform experts from splitmix64(aux_seed, step, l).
+uint64_t sm64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+void random_prediction(Ctx* c, int64_t step, int l, int32_t* out) {
+  uint64_t x = sm64(sm64(c->cfg.aux_seed) ^ ((uint64_t)step << 20) ^ (uint64_t)l);
+  int n = 0;
+  while (n < c->k) {
+    x = sm64(x);
+    const int e = (int)(x % (uint64_t)c->E);
+    bool dup = false;
+    for (int i = 0; i < n; ++i) dup |= out[i] == e;
+    if (!dup) out[n++] = e;
+  }
+}
+
+// ------------------------------------------------------------------ slots + loads
+int find_slot(Ctx* c, int64_t tok, int l, int e) {
+  for (int i = 0; i < (int)c->slots.size(); ++i) {
+    const Slot& s = c->slots[i];
+    if (s.occupied && s.token == tok && s.layer == l && s.expert == e) return i;
+  }
+  return -1;
+}
+int free_slot(Ctx* c) {
+  for (int i = 0; i < (int)c->slots.size(); ++i)
+    if (!c->slots[i].occupied) return i;
+  return -1;
+}
+int occupied_count(const Ctx* c) {
+  int n = 0;
+  for (auto& s : c->slots) n += s.occupied;
+  return n;
+}
+
+void submit_load(Ctx* c, int slot, int64_t tok, int l, int e, int64_t key) {
+  if (!holds_expert(c, l, e)) fail(c, ODMOE_E_RANGE, "expert not in this rank's pool");
+  Slot& s = c->slots[slot];
+  s.occupied = true;
+  s.token = tok;
+  s.layer = l;
+  s.expert = e;
+  auto r = std::make_shared<LoadReq>();
+  r->layer = l;
+  r->expert = e;
+  r->slot = slot;
+  r->key = key;
+  r->src = c->pool + c->pool_off[(size_t)l * c->E + e];
+  r->dst = s.dev;
+  r->bytes = c->blob_bytes;
+  r->w13_bytes = c->w13_bytes;
+  r->ev_w13 = s.ev_w13;
+  r->ev_done = s.ev_done;
+  r->wait_ev = s.free_recorded ? s.ev_free : nullptr;
+  s.req = r;
+  c->loader.submit(r);
+  c->stats.max_resident = std::max<int64_t>(c->stats.max_resident, occupied_count(c));
+}
+
+void release_slot(Ctx* c, int slot) {
+  Slot& s = c->slots[slot];
+  if (s.req) c->loader.cancel(s.req);
+  s.occupied = false;
+  s.layer = s.expert = -1;
+  s.token = -1;
+}
+
+int64_t load_key(const Ctx* c, int64_t tok, int l, int j) { return (tok * c->L + l) * 16 + j; }
+
+// Issue predicted loads for layers next_plan .. l_cur + D while slots are free (Q11).
+void pump(Ctx* c) {
+  if (c->resident) return;
+  while (c->next_plan < c->L) {
+    const int m = c->next_plan;
+    if (m > c->l_cur + c->cfg.lookahead) break;
+    if (!pred_available(c, m)) break;
+    std::vector<int> mine = my_experts(c, m, c->pred_tbl.data() + (size_t)m * c->k);
+    std::vector<int> todo;
+    for (int e : mine)
+      if (find_slot(c, c->step, m, e) < 0) todo.push_back(e);
+    int nfree = 0;
+    for (auto& s : c->slots) nfree += !s.occupied;
+    if (nfree < (int)todo.size()) break;
+    for (size_t j = 0; j < todo.size(); ++j)
+      submit_load(c, free_slot(c), c->step, m, todo[j], load_key(c, c->step, m, 1 + (int)j));
+    c->next_plan++;
+  }
+}
+
+// ------------------------------------------------------------------ one decode step
+void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_record* rec) {
+  const int L = c->L, E = c->E, k = c->k, d = c->d, F = c->F;
+  if (token_in < 0 || token_in >= c->V) fail(c, ODMOE_E_RANGE, "token out of range");
+  cudaStream_t s = c->s_main;
+  const int p = c->cfg.predictor;
+  const bool r0 = c->rank == 0;
+  const int u_f32 = c->wt == W_F32;
+
+  // token in (pinned -> device); the previous step's shadow must be done with d_tok_in
+  c->h_tok[0] = token_in;
+  CUDA_OK(c, cudaStreamWaitEvent(s, c->ev_shadow_done, 0));
+  CUDA_OK(c, cudaMemcpyAsync(c->d_tok_in, c->h_tok, 4, cudaMemcpyHostToDevice, s));
+  CUDA_OK(c, cudaEventRecord(c->ev_tok, s));
+
+  // predictions for this step
+  std::fill(c->pred_ready.begin(), c->pred_ready.end(), 0);
+  std::fill(c->pred_tbl.begin(), c->pred_tbl.end(), -1);
+  c->pred_valid = false;
+  if (!c->resident) {
+    if (p == ODMOE_PRED_SHADOW_INT8 || p == ODMOE_PRED_SHADOW_SAME) {
+      if (r0) {
+        CUDA_OK(c, cudaStreamWaitEvent(c->s_shadow, c->ev_tok, 0));
+        enqueue_shadow(c, c->d_tok_in);
+      }
+      if (c->world > 1) enqueue_pred_broadcast(c);
+      c->pred_valid = true;
+    } else if (p == ODMOE_PRED_RANDOM) {
+      for (int l = 0; l < L; ++l) random_prediction(c, c->step, l, c->pred_tbl.data() + (size_t)l * k);
+      std::fill(c->pred_ready.begin(), c->pred_ready.end(), 1);
+      c->pred_valid = true;
+    } else if (p == ODMOE_PRED_PERFECT) {
+      auto it = c->route_cache.find(token_in);
+      if (it != c->route_cache.end()) {
+        std::copy(it->second.begin(), it->second.end(), c->pred_tbl.begin());
+        std::fill(c->pred_ready.begin(), c->pred_ready.end(), 1);
+        c->pred_valid = true;
+      }
+    }
+  }
+  c->next_plan = 0;
+  c->l_cur = 0;
+  pump(c);
+
+  // embedding (rank 0)
+  if (r0) {
+    KTimer t(c, K_EMBED, s);
+    CUDA_OK(c, launch_embed(c->d_emb, nullptr, c->wt, c->d_tok_in, d, c->d_h, s));
+  }
+
+  std::vector<int32_t> true_ids((size_t)L * k);
+  const float* const* yadd = c->world == 1 ? c->d_yptr : c->d_yredptr;
+  int n_add = 0;
+  for (int l = 0; l < L; ++l) {
+    c->l_cur = l;
+    char* pkt = c->d_pkt + (size_t)l * c->pkt_bytes;
+    int32_t* ids_dev = (int32_t*)(pkt + c->pkt_ids_off);
+    float* w_dev = (float*)(pkt + c->pkt_w_off);
+    if (r0) {
+      KTimer t(c, K_ROUTER, s);
+      CUDA_OK(c, launch_router(c->d_h, yadd, n_add, nullptr, (const char*)c->d_router + (size_t)l * E * d * c->esz,
+                               nullptr, c->wt, 1, E, d, k, c->cfg.rms_eps, pkt, ids_dev, w_dev,
+                               c->d_logits + (size_t)l * E, c->d_flag, s));
+      if (c->dbg_h) CUDA_OK(c, cudaMemcpyAsync(c->dbg_h + (size_t)l * d, c->d_h, sizeof(float) * d, cudaMemcpyDeviceToDevice, s));
+    }
+    if (c->world > 1) NCCL_OK(c, ncclBroadcast(pkt, pkt, c->pkt_bytes, ncclChar, 0, c->comm, s));
+    n_add = c->world == 1 ? k : 1;
+
+    const bool in_group = (l % c->NG) == c->my_group;
+    if (c->resident) {
+      // routing consumed on the device: no host round trip per layer
+      if (in_group) {
+        const int mine = k / c->G;
+        for (int j = 0; j < mine; ++j) {
+          ExpertRef ex{nullptr, nullptr, (const void* const*)c->d_res_tbl, nullptr, ids_dev,
+                       c->world == 1 ? j : c->my_pos, l * E, k, c->world == 1 ? 0 : 1};
+          float* y = c->d_y + (size_t)j * d;
+          { KTimer t(c, K_W13, s); CUDA_OK(c, launch_w13(ex, c->wt, pkt, u_f32, c->d_a + (size_t)j * F, d, F, s)); }
+          { KTimer t(c, K_W2, s); CUDA_OK(c, launch_w2(ex, c->wt, c->d_a + (size_t)j * F, w_dev, y, d, F, s)); }
+          if (c->dbg_ypart) CUDA_OK(c, cudaMemcpyAsync(c->dbg_ypart + ((size_t)l * k + j) * d, y, sizeof(float) * d, cudaMemcpyDeviceToDevice, s));
+        }
+      }
+    } else {
+      // the host learns the router's ids (every rank: they arrive with the broadcast packet)
+      CUDA_OK(c, cudaMemcpyAsync(c->h_ids + (size_t)l * k, ids_dev, 4 * k, cudaMemcpyDeviceToHost, s));
+      CUDA_OK(c, cudaEventRecord(c->ev_ids, s));
+      const double tw = now_s();
+      for (;;) {
+        const cudaError_t q = cudaEventQuery(c->ev_ids);
+        if (q == cudaSuccess) break;
+        if (q != cudaErrorNotReady) CUDA_OK(c, q);
+        pump(c);
+        if (c->loader.error() != cudaSuccess) CUDA_OK(c, c->loader.error());
+        std::this_thread::sleep_for(std::chrono::microseconds(5));
+      }
+      const double wait_us = (now_s() - tw) * 1e6;
+      const int32_t* S = c->h_ids + (size_t)l * k;
+      std::copy(S, S + k, true_ids.begin() + (size_t)l * k);
+      pred_available(c, l);  // refresh (shadow may have finished meanwhile)
+      int reloads = 0;
+      if (in_group) {
+        std::vector<int> mine = my_experts(c, l, S);
+        // Misprediction fallback: experts of this layer loaded for a wrong prediction
+        // are stopped and their slots reused for the true experts (Q15).
+        for (int i = 0; i < (int)c->slots.size(); ++i) {
+          Slot& sl = c->slots[i];
+          if (sl.occupied && sl.token == c->step && sl.layer == l &&
+              std::find(mine.begin(), mine.end(), sl.expert) == mine.end())
+            release_slot(c, i);
+        }
+        for (int e : mine) {
+          if (find_slot(c, c->step, l, e) >= 0) continue;
+          int fs = free_slot(c);
+          if (fs < 0) {
+            // every slot holds a future prefetch: drop the furthest one and re-plan it later
+            int far = -1;
+            for (int i = 0; i < (int)c->slots.size(); ++i)
+              if (c->slots[i].occupied && (far < 0 || c->slots[i].layer > c->slots[far].layer)) far = i;
+            if (far < 0 || c->slots[far].layer <= l) fail(c, ODMOE_E_BUDGET, "no slot for a reload");
+            c->next_plan = std::min(c->next_plan, c->slots[far].layer);
+            release_slot(c, far);
+            fs = far;
+          }
+          submit_load(c, fs, c->step, l, e, load_key(c, c->step, l, 0));
+          reloads++;
+          c->stats.reloads++;
+        }
+        // compute, in rank order of the router's output
+        int jj = 0;
+        for (int j = 0; j < k; ++j) {
+          if (std::find(mine.begin(), mine.end(), S[j]) == mine.end()) continue;
+          const int si = find_slot(c, c->step, l, S[j]);
+          Slot& sl = c->slots[si];
+          if (!c->loader.wait_issued(sl.req)) {
+            if (c->loader.error() != cudaSuccess) CUDA_OK(c, c->loader.error());
+            fail(c, ODMOE_E_STATE, "load was cancelled before compute");
+          }
+          const int ypos = c->world == 1 ? j : jj;
+          float* y = c->d_y + (size_t)ypos * d;
+          ExpertRef e13 = direct_ref(sl.dev, nullptr, j);
+          ExpertRef e2 = direct_ref(sl.dev + c->w13_bytes, nullptr, j);
+          CUDA_OK(c, cudaStreamWaitEvent(s, sl.ev_w13, 0));
+          { KTimer t(c, K_W13, s); CUDA_OK(c, launch_w13(e13, c->wt, pkt, u_f32, c->d_a + (size_t)ypos * F, d, F, s)); }
+          CUDA_OK(c, cudaStreamWaitEvent(s, sl.ev_done, 0));
+          { KTimer t(c, K_W2, s); CUDA_OK(c, launch_w2(e2, c->wt, c->d_a + (size_t)ypos * F, w_dev, y, d, F, s)); }
+          // evict right after use: the slot is reusable once this event fires (Q16)
+          CUDA_OK(c, cudaEventRecord(sl.ev_free, s));
+          sl.free_recorded = true;
+          sl.req.reset();
+          sl.occupied = false;
+          sl.layer = sl.expert = -1;
+          sl.token = -1;
+          if (c->dbg_ypart) CUDA_OK(c, cudaMemcpyAsync(c->dbg_ypart + ((size_t)l * k + j) * d, y, sizeof(float) * d, cudaMemcpyDeviceToDevice, s));
+          jj++;
+        }
+      }
+      if (c->next_plan <= l) c->next_plan = l + 1;
+      pump(c);
+      if (rec && r0) {
+        odmoe_layer_record& R = rec[l];
+        std::memset(&R, 0, sizeof(R));
+        for (int j = 0; j < 8; ++j) { R.true_ids[j] = -1; R.pred_ids[j] = -1; }
+        for (int j = 0; j < k; ++j) R.true_ids[j] = S[j];
+        R.n_reloads = reloads;
+        R.load_wait_us = (float)wait_us;
+        c->stats.wait_us += wait_us;
+      }
+    }
+    if (c->world > 1) {
+      const float* send = (in_group ? c->d_y : c->d_zero);
+      NCCL_OK(c, ncclReduce(send, c->d_yred, d, ncclFloat32, ncclSum, 0, c->comm, s));
+      if (c->dbg_yred && r0) CUDA_OK(c, cudaMemcpyAsync(c->dbg_yred + (size_t)l * d, c->d_yred, sizeof(float) * d, cudaMemcpyDeviceToDevice, s));
+    }
+  }
+
+  // final combine + LM head + argmax (rank 0)
+  if (r0) {
+    CUDA_OK(c, launch_combine(c->d_h, yadd, n_add, d, s));
+    c->stats.kernel_launches++;
+    if (c->dbg_hfinal) CUDA_OK(c, cudaMemcpyAsync(c->dbg_hfinal, c->d_h, sizeof(float) * d, cudaMemcpyDeviceToDevice, s));
+    KTimer t(c, K_LM, s);
+    CUDA_OK(c, launch_lm_head(c->d_h, c->d_lm, c->wt, c->V, d, c->cfg.rms_eps, c->d_tok_out,
+                              c->cfg.debug_capture ? c->d_lmlogits : nullptr, c->d_lmscratch, s));
+  }
+  if (c->world > 1) NCCL_OK(c, ncclBroadcast(c->d_tok_out, c->d_tok_out, 1, ncclInt32, 0, c->comm, s));
+  CUDA_OK(c, cudaMemcpyAsync(c->h_tok + 1, c->d_tok_out, 4, cudaMemcpyDeviceToHost, s));
+  CUDA_OK(c, cudaMemcpyAsync(c->h_flag, c->d_flag, 4, cudaMemcpyDeviceToHost, s));
+  if (c->resident) CUDA_OK(c, cudaMemcpyAsync(c->h_ids, c->d_pkt + c->pkt_ids_off, 4 * k, cudaMemcpyDeviceToHost, s));
+  if (c->resident && r0) {
+    for (int l = 0; l < L; ++l)
+      CUDA_OK(c, cudaMemcpyAsync(c->h_ids + (size_t)l * k, c->d_pkt + (size_t)l * c->pkt_bytes + c->pkt_ids_off, 4 * k, cudaMemcpyDeviceToHost, s));
+  }
+  CUDA_OK(c, cudaStreamSynchronize(s));
+  if (c->has_shadow && r0 && !c->resident) CUDA_OK(c, cudaEventSynchronize(c->ev_shadow_done));
+  if (!c->resident && c->world > 1 && c->pred_valid &&
+      (p == ODMOE_PRED_SHADOW_INT8 || p == ODMOE_PRED_SHADOW_SAME))
+    CUDA_OK(c, cudaStreamSynchronize(c->s_shadow));
+  if (c->h_flag[0]) fail(c, ODMOE_E_NONFINITE, "non-finite router logits");
+  if (c->resident) std::copy(c->h_ids, c->h_ids + (size_t)L * k, true_ids.begin());
+
+  // predictions as they stood (recall accounting, Eqs. 2-3); Mode A computes all of them
+  for (int l = 0; l < L; ++l) pred_available(c, l);
+  if (r0) {
+    for (int l = 0; l < L; ++l) {
+      const int32_t* S = true_ids.data() + (size_t)l * k;
+      const int32_t* P = c->pred_tbl.data() + (size_t)l * k;
+      const bool have = c->pred_valid && P[0] >= 0;
+      int corr = 0;
+      if (have)
+        for (int a = 0; a < k; ++a)
+          for (int b = 0; b < k; ++b) corr += S[a] == P[b];
+      if (have) { c->stats.correct += corr; c->stats.predicted_total += k; }
+      if (rec) {
+        odmoe_layer_record& R = rec[l];
+        if (c->resident) {
+          std::memset(&R, 0, sizeof(R));
+          for (int j = 0; j < 8; ++j) { R.true_ids[j] = -1; R.pred_ids[j] = -1; }
+          for (int j = 0; j < k; ++j) R.true_ids[j] = S[j];
+        }
+        for (int j = 0; j < k; ++j) R.pred_ids[j] = have ? P[j] : -1;
+        R.pred_available = have;
+        R.correct = corr;
+      }
+    }
+    if (rec) {
+      std::vector<float> wv((size_t)L * k);
+      for (int l = 0; l < L; ++l)
+        CUDA_OK(c, cudaMemcpy(wv.data() + (size_t)l * k, c->d_pkt + (size_t)l * c->pkt_bytes + c->pkt_w_off, 4 * k, cudaMemcpyDeviceToHost));
+      for (int l = 0; l < L; ++l)
+        for (int j = 0; j < k; ++j) rec[l].weights[j] = wv[(size_t)l * k + j];
+    }
+  }
+  c->route_cache[token_in] = true_ids;
+  *token_out = c->h_tok[1];
+  c->stats.tokens++;
+  c->step++;
+  if (c->cfg.time_kernels) harvest_timers(c);
+  // loader statistics
+  c->stats.loads_issued = c->loader.loads_issued.load();
+  c->stats.loads_completed = c->loader.loads_completed.load();
+  c->stats.loads_cancelled = c->loader.loads_cancelled.load();
+  c->stats.bytes_h2d = c->loader.bytes_h2d.load();
+
+  if (c->cfg.debug_capture && r0) {
+    // host copy of the capture
+    auto& H = c->hdbg;
+    auto& I = c->hdbg_index;
+    H.clear();
+    I.clear();
+    auto add = [&](int what, const void* dev, int64_t per_layer, int layers) {
+      const int64_t off = (int64_t)H.size();
+      H.resize(H.size() + (size_t)per_layer * layers);
+      if (dev) CUDA_OK(c, cudaMemcpy(H.data() + off, dev, (size_t)per_layer * layers, cudaMemcpyDeviceToHost));
+      I[what] = {off, per_layer};
+    };
+    std::vector<char> ubuf((size_t)L * d * c->esz), idb((size_t)L * k * 4), wb((size_t)L * k * 4);
+    for (int l = 0; l < L; ++l) {
+      const char* pk = c->d_pkt + (size_t)l * c->pkt_bytes;
+      CUDA_OK(c, cudaMemcpy(ubuf.data() + (size_t)l * d * c->esz, pk, (size_t)d * c->esz, cudaMemcpyDeviceToHost));
+      CUDA_OK(c, cudaMemcpy(idb.data() + (size_t)l * k * 4, pk + c->pkt_ids_off, 4 * k, cudaMemcpyDeviceToHost));
+      CUDA_OK(c, cudaMemcpy(wb.data() + (size_t)l * k * 4, pk + c->pkt_w_off, 4 * k, cudaMemcpyDeviceToHost));
+    }
+    add(0, c->dbg_h, (int64_t)d * 4, L);
+    {
+      const int64_t off = (int64_t)H.size();
+      H.insert(H.end(), ubuf.begin(), ubuf.end());
+      I[1] = {off, (int64_t)d * (int64_t)c->esz};
+    }
+    add(2, c->d_logits, (int64_t)E * 4, L);
+    {
+      int64_t off = (int64_t)H.size();
+      H.insert(H.end(), idb.begin(), idb.end());
+      I[3] = {off, (int64_t)k * 4};
+      off = (int64_t)H.size();
+      H.insert(H.end(), wb.begin(), wb.end());
+      I[4] = {off, (int64_t)k * 4};
+    }
+    add(5, c->dbg_yred, (int64_t)d * 4, L);
+    add(6, c->dbg_ypart, (int64_t)k * d * 4, L);
+    if (c->has_shadow && c->dbg_sh_h) {
+      add(7, c->dbg_sh_h, (int64_t)d * 4, L);
+      add(8, c->dbg_sh_u, (int64_t)d * 4, L);
+      add(9, c->sh_logits, (int64_t)E * 4, L);
+      add(10, c->sh_ids, (int64_t)k * 4, L);
+    }
+    add(11, c->dbg_hfinal, (int64_t)d * 4, 1);
+    add(12, c->d_lmlogits, (int64_t)c->V * 4, 1);
+  }
+}
+
+void destroy_ctx(Ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->dev);
+  c->loader.stop();
+  if (c->s_main) cudaStreamSynchronize(c->s_main);
+  if (c->s_shadow) cudaStreamSynchronize(c->s_shadow);
+  if (c->s_copy) cudaStreamSynchronize(c->s_copy);
+  auto F = [](void* p) { if (p) cudaFree(p); };
+  F(c->d_emb); F(c->d_lm); F(c->d_router);
+  if (c->cfg.predictor != ODMOE_PRED_SHADOW_SAME) {
+    F(c->sh_emb); F(c->sh_semb); F(c->sh_router); F(c->sh_srouter);
+    for (auto p : c->sh_blob) F(p);
+    for (auto p : c->sh_sc) F(p);
+    F(c->d_sh_tbl); F(c->d_sh_stbl);
+  }
+  for (auto p : c->res_blob) F(p);
+  F(c->d_res_tbl);
+  for (auto& s : c->slots) {
+    F(s.dev);
+    if (s.ev_w13) cudaEventDestroy(s.ev_w13);
+    if (s.ev_done) cudaEventDestroy(s.ev_done);
+    if (s.ev_free) cudaEventDestroy(s.ev_free);
+  }
+  F(c->d_h); F(c->d_pkt); F(c->d_logits); F(c->d_a); F(c->d_y); F(c->d_yred); F(c->d_zero);
+  F((void*)c->d_yptr); F((void*)c->d_yredptr); F(c->d_tok_in); F(c->d_tok_out); F(c->d_flag);
+  F(c->d_lmscratch); F(c->d_lmlogits);
+  F(c->sh_h); F(c->sh_u); F(c->sh_ids); F(c->sh_w); F(c->sh_logits); F(c->sh_a); F(c->sh_y); F((void*)c->sh_yptr);
+  F(c->dbg_h); F(c->dbg_ypart); F(c->dbg_yred); F(c->dbg_sh_h); F(c->dbg_sh_u); F(c->dbg_hfinal);
+  auto FH = [](void* p) { if (p) cudaFreeHost(p); };
+  FH(c->pool); FH(c->h_ids); FH(c->h_w); FH(c->h_pred); FH(c->h_tok); FH(c->h_flag);
+  for (auto e : c->ev_pred) cudaEventDestroy(e);
+  for (auto e : {c->ev_ids, c->ev_tok, c->ev_shadow_done, c->ev_step}) if (e) cudaEventDestroy(e);
+  for (auto& t : c->timed) { c->tev_pool.push_back(t.a); c->tev_pool.push_back(t.b); }
+  for (auto e : c->tev_pool) cudaEventDestroy(e);
+  if (c->comm_pred) ncclCommDestroy(c->comm_pred);
+  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->s_main) cudaStreamDestroy(c->s_main);
+  if (c->s_shadow) cudaStreamDestroy(c->s_shadow);
+  if (c->s_copy) cudaStreamDestroy(c->s_copy);
+  delete c;
+}
+
+}  // namespace
+
+// ==================================================================== C ABI
+extern "C" {
+
+int32_t odmoe_abi_version(void) { return ODMOE_ABI_VERSION; }
+
+int odmoe_nccl_unique_id(void* out128) {
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return 1;
+  std::memcpy(out128, &id, sizeof(id));
+  return 0;
+}
+
+odmoe_status odmoe_create(const odmoe_config* cfg, void** ctx_out) {
+  if (ctx_out) *ctx_out = nullptr;
+  Ctx* c = nullptr;
+  t_create_err.clear();
+  odmoe_status st = guard(nullptr, [&] {
+    validate(cfg);
+    if (!ctx_out) fail(nullptr, ODMOE_E_CONFIG, "null ctx_out");
+    c = new Ctx();
+    c->cfg = *cfg;
+    if (c->cfg.rms_eps <= 0.f) c->cfg.rms_eps = 1e-5f;
+    c->L = cfg->L; c->E = cfg->E; c->k = cfg->k; c->d = cfg->d; c->F = cfg->F; c->V = cfg->V;
+    c->wt = wtype(cfg->dtype);
+    c->esz = dsize(cfg->dtype);
+    c->blob_elems = 3LL * c->F * c->d;
+    c->blob_bytes = c->blob_elems * (int64_t)c->esz;
+    c->w13_bytes = 2LL * c->F * c->d * (int64_t)c->esz;
+    c->world = cfg->world_size;
+    c->rank = cfg->rank;
+    c->G = cfg->group_size > 0 ? cfg->group_size : std::min(c->k, c->world);
+    c->NG = c->world / c->G;
+    c->my_group = c->rank / c->G;
+    c->my_pos = c->rank % c->G;
+    c->resident = cfg->slots_per_gpu == -1;
+    c->dev = cfg->device;
+    c->has_shadow = c->rank == 0 && !c->resident &&
+                    (cfg->predictor == ODMOE_PRED_SHADOW_INT8 || cfg->predictor == ODMOE_PRED_SHADOW_SAME);
+    try {
+      CUDA_OK(c, cudaSetDevice(c->dev));
+      CUDA_OK(c, cudaStreamCreateWithFlags(&c->s_main, cudaStreamNonBlocking));
+      CUDA_OK(c, cudaStreamCreateWithFlags(&c->s_shadow, cudaStreamNonBlocking));
+      CUDA_OK(c, cudaStreamCreateWithFlags(&c->s_copy, cudaStreamNonBlocking));
+      if (c->world > 1) {
+        ncclUniqueId id;
+        std::memcpy(&id, cfg->nccl_id, sizeof(id));
+        NCCL_OK(c, ncclCommInitRank(&c->comm, c->world, id, c->rank));
+        NCCL_OK(c, ncclCommSplit(c->comm, 0, c->rank, &c->comm_pred, nullptr));
+      }
+      char* staging = dmalloc<char>(c, (size_t)c->blob_bytes * 2, "staging");
+      if (c->rank == 0) build_nonexpert(c);
+      build_pool(c, staging);
+      if (c->has_shadow) build_shadow(c, staging);
+      CUDA_OK(c, cudaStreamSynchronize(c->s_main));
+      cudaFree(staging);
+      build_slots(c);
+      build_buffers(c);
+      if (!c->resident) c->loader.start(c->dev, c->s_copy, cfg->chunk_bytes > 0 ? cfg->chunk_bytes : (32LL << 20), 2);
+      CUDA_OK(c, cudaDeviceSynchronize());
+    } catch (const Fail& f) {
+      t_create_err = c->err;
+      destroy_ctx(c);
+      c = nullptr;
+      throw;
+    }
+  });
+  if (st == ODMOE_OK) *ctx_out = c;
+  return st;
+}
+
+void odmoe_destroy(void* ctx) { destroy_ctx(reinterpret_cast<Ctx*>(ctx)); }
+
+const char* odmoe_last_error(const void* ctx) {
+  if (!ctx) return t_create_err.c_str();
+  return reinterpret_cast<const Ctx*>(ctx)->err.c_str();
+}
+
+odmoe_status odmoe_get_stats(const void* ctx, odmoe_stats* out) {
+  if (!ctx || !out) return ODMOE_E_STATE;
+  *out = reinterpret_cast<const Ctx*>(ctx)->stats;
+  return ODMOE_OK;
+}
+
+odmoe_status odmoe_reset_stats(void* ctx) {
+  if (!ctx) return ODMOE_E_STATE;
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  odmoe_stats keep = c->stats;
+  c->stats = odmoe_stats{};
+  c->stats.resident_bytes = keep.resident_bytes;
+  c->stats.shadow_bytes = keep.shadow_bytes;
+  c->stats.pool_bytes = keep.pool_bytes;
+  c->stats.pool_build_s = keep.pool_build_s;
+  c->loader.bytes_h2d = 0;
+  c->loader.loads_issued = 0;
+  c->loader.loads_completed = 0;
+  c->loader.loads_cancelled = 0;
+  return ODMOE_OK;
+}
+
+#define CTX_GUARD(ctxp)                                                   \
+  Ctx* c = reinterpret_cast<Ctx*>(ctxp);                                  \
+  if (!c || c->poisoned) return ODMOE_E_STATE;                            \
+  cudaSetDevice(c->dev);
+
+odmoe_status odmoe_decode_step(void* ctx, int32_t token_in, int32_t* token_out, odmoe_layer_record* rec) {
+  CTX_GUARD(ctx);
+  if (!token_out) return ODMOE_E_CONFIG;
+  return guard(c, [&] { decode_step_impl(c, token_in, token_out, rec); });
+}
+
+odmoe_status odmoe_predict_ahead(void* ctx, int32_t token, int from_layer, int depth, int32_t* pred_ids) {
+  CTX_GUARD(ctx);
+  return guard(c, [&] {
+    if (!c->has_shadow) fail(c, ODMOE_E_STATE, "no shadow on this rank");
+    if (token < 0 || token >= c->V || from_layer < 0 || depth < 0 || from_layer + depth > c->L)
+      fail(c, ODMOE_E_RANGE, "range");
+    if (c->predict_cache_token != token) {
+      c->h_tok[0] = token;
+      CUDA_OK(c, cudaMemcpyAsync(c->d_tok_in, c->h_tok, 4, cudaMemcpyHostToDevice, c->s_shadow));
+      enqueue_shadow(c, c->d_tok_in);
+      CUDA_OK(c, cudaStreamSynchronize(c->s_shadow));
+      if (c->cfg.time_kernels) harvest_timers(c);
+      c->predict_cache_token = token;
+    }
+    std::vector<int32_t> P((size_t)c->L * c->k);
+    CUDA_OK(c, cudaMemcpy(P.data(), c->sh_ids, 4 * P.size(), cudaMemcpyDeviceToHost));
+    std::copy(P.begin() + (size_t)from_layer * c->k, P.begin() + (size_t)(from_layer + depth) * c->k, pred_ids);
+  });
+}
+
+odmoe_status odmoe_load(void* ctx, int layer, int expert) {
+  CTX_GUARD(ctx);
+  return guard(c, [&] {
+    if (c->resident) fail(c, ODMOE_E_STATE, "fully-resident ctx has no loader");
+    if (layer < 0 || layer >= c->L || expert < 0 || expert >= c->E) fail(c, ODMOE_E_RANGE, "range");
+    if (!holds_expert(c, layer, expert)) fail(c, ODMOE_E_RANGE, "expert not in this rank's pool");
+    if (find_slot(c, -2, layer, expert) >= 0) return;
+    const int fs = free_slot(c);
+    if (fs < 0) fail(c, ODMOE_E_BUDGET, "all slots occupied");
+    submit_load(c, fs, -2, layer, expert, -1);
+  });
+}
+
+odmoe_status odmoe_load_wait(void* ctx, int layer, int expert, void** w13, void** w2) {
+  CTX_GUARD(ctx);
+  return guard(c, [&] {
+    const int si = find_slot(c, -2, layer, expert);
+    if (si < 0) fail(c, ODMOE_E_STATE, "not loading");
+    Slot& s = c->slots[si];
+    if (!c->loader.wait_issued(s.req)) fail(c, ODMOE_E_STATE, "load cancelled");
+    CUDA_OK(c, cudaEventSynchronize(s.ev_done));
+    if (w13) *w13 = s.dev;
+    if (w2) *w2 = s.dev + c->w13_bytes;
+  });
+}
+
+odmoe_status odmoe_evict(void* ctx, int layer, int expert) {
+  CTX_GUARD(ctx);
+  return guard(c, [&] {
+    const int si = find_slot(c, -2, layer, expert);
+    if (si < 0) fail(c, ODMOE_E_STATE, "expert not resident");
+    Slot& s = c->slots[si];
+    CUDA_OK(c, cudaEventRecord(s.ev_free, c->s_main));  // after work already on the compute stream
+    s.free_recorded = true;
+    release_slot(c, si);
+  });
+}
+
+odmoe_status odmoe_prefill(void* ctx, const int32_t* tokens, int T, int32_t* token_out, int32_t* expert_counts) {
+  CTX_GUARD(ctx);
+  (void)tokens; (void)T; (void)token_out; (void)expert_counts;
+  c->err = "odmoe_prefill: grouped-GEMM prefill not built in this revision";
+  return ODMOE_E_STATE;
+}
+
+odmoe_status odmoe_debug_read(const void* ctx, int what, int layer, void* dst, int64_t bytes) {
+  const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
+  if (!c || !dst) return ODMOE_E_STATE;
+  auto it = c->hdbg_index.find(what);
+  if (it == c->hdbg_index.end()) return ODMOE_E_STATE;
+  const int64_t off = it->second.first + (int64_t)(what >= 11 ? 0 : layer) * it->second.second;
+  if (layer < 0 || layer >= c->L || bytes > it->second.second || off + bytes > (int64_t)c->hdbg.size()) return ODMOE_E_RANGE;
+  std::memcpy(dst, c->hdbg.data() + off, (size_t)bytes);
+  return ODMOE_OK;
+}
+
+odmoe_status odmoe_tensor_ptr(const void* ctx, int what, int index, void** ptr) {
+  const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
+  if (!c || !ptr) return ODMOE_E_STATE;
+  const int LE = c->L * c->E;
+  switch (what) {
+    case 0: *ptr = c->d_emb; break;
+    case 1: *ptr = c->d_lm; break;
+    case 2: if (index < 0 || index >= c->L) return ODMOE_E_RANGE; *ptr = (char*)c->d_router + (size_t)index * c->E * c->d * c->esz; break;
+    case 3: if (!c->sh_srouter || index < 0 || index >= c->L) return ODMOE_E_RANGE; *ptr = (char*)c->sh_router + (size_t)index * c->E * c->d; break;
+    case 4: if (!c->sh_srouter || index < 0 || index >= c->L) return ODMOE_E_RANGE; *ptr = c->sh_srouter + (size_t)index * c->E; break;
+    case 5: if (c->sh_blob.empty() || index < 0 || index >= LE) return ODMOE_E_RANGE; *ptr = c->sh_blob[index]; break;
+    case 6: if (c->sh_sc.empty() || index < 0 || index >= LE) return ODMOE_E_RANGE; *ptr = c->sh_sc[index]; break;
+    case 7: if (c->sh_blob.empty() || index < 0 || index >= LE) return ODMOE_E_RANGE; *ptr = (int8_t*)c->sh_blob[index] + 2LL * c->F * c->d; break;
+    case 8: if (c->sh_sc.empty() || index < 0 || index >= LE) return ODMOE_E_RANGE; *ptr = c->sh_sc[index] + 2 * c->F; break;
+    case 9: if (!c->sh_semb) return ODMOE_E_RANGE; *ptr = c->sh_emb; break;
+    case 10: if (!c->sh_semb) return ODMOE_E_RANGE; *ptr = c->sh_semb; break;
+    default: return ODMOE_E_RANGE;
+  }
+  return ODMOE_OK;
+}
+
+// ------------------------------------------------------------------ stateless kernels
+static bool router_shape_ok(int m, int E, int d, int k) {
+  return m >= 1 && E >= 1 && E <= 64 && k >= 1 && k <= 8 && k <= E && d >= 8 && d % 8 == 0;
+}
+
+odmoe_status odmoe_route_topk(float* h, const float* const* y_add, int n_add, const void* gamma,
+                              const void* w_gate, int m, int E, int d, int k, int dt, float eps,
+                              void* u_out, int32_t* ids, float* w, float* logits, int32_t* flag,
+                              void* stream) {
+  if (!router_shape_ok(m, E, d, k) || (dt != ODMOE_BF16 && dt != ODMOE_FP32) || n_add < 0 ||
+      (n_add > 0 && !y_add) || !h || !w_gate || !u_out || !ids || !w)
+    return ODMOE_E_CONFIG;
+  return launch_router(h, y_add, n_add, gamma, w_gate, nullptr, wtype(dt), m, E, d, k, eps, u_out,
+                       ids, w, logits, flag, S(stream)) == cudaSuccess ? ODMOE_OK : ODMOE_E_CUDA;
+}
+
+odmoe_status odmoe_shadow_route_topk(float* h, const float* const* y_add, int n_add,
+                                     const int8_t* q_gate, const float* s_gate, int m, int E, int d,
+                                     int k, float eps, void* u_out, int32_t* ids, float* w,
+                                     float* logits, int32_t* flag, void* stream) {
+  if (!router_shape_ok(m, E, d, k) || d % 16 || n_add < 0 || (n_add > 0 && !y_add) || !h || !q_gate ||
+      !s_gate || !u_out || !ids || !w)
+    return ODMOE_E_CONFIG;
+  return launch_router(h, y_add, n_add, nullptr, q_gate, s_gate, W_I8, m, E, d, k, eps, u_out, ids, w,
+                       logits, flag, S(stream)) == cudaSuccess ? ODMOE_OK : ODMOE_E_CUDA;
+}
+
+odmoe_status odmoe_expert_ffn(const void* w13, const void* w2, const void* u, const float* gate_w,
+                              int gate_idx, int d, int F, int dt, float* a_scratch, float* y,
+                              void* stream) {
+  if (!w13 || !w2 || !u || !a_scratch || !y || d < 8 || F < 8 || d % 8 || F % 8 || gate_idx < 0 ||
+      (dt != ODMOE_BF16 && dt != ODMOE_FP32))
+    return ODMOE_E_CONFIG;
+  const WType wt = wtype(dt);
+  if (launch_w13(direct_ref(w13, nullptr, gate_idx), wt, u, dt == ODMOE_FP32, a_scratch, d, F, S(stream)) != cudaSuccess)
+    return ODMOE_E_CUDA;
+  if (launch_w2(direct_ref(w2, nullptr, gate_idx), wt, a_scratch, gate_w, y, d, F, S(stream)) != cudaSuccess)
+    return ODMOE_E_CUDA;
+  return ODMOE_OK;
+}
+
+odmoe_status odmoe_shadow_expert_ffn(const int8_t* q13, const float* s13, const int8_t* q2,
+                                     const float* s2, const void* u, const float* gate_w,
+                                     int gate_idx, int d, int F, float* a_scratch, float* y,
+                                     void* stream) {
+  if (!q13 || !s13 || !q2 || !s2 || !u || !a_scratch || !y || d < 16 || F < 16 || d % 16 || F % 16 || gate_idx < 0)
+    return ODMOE_E_CONFIG;
+  if (launch_w13(direct_ref(q13, s13, gate_idx), W_I8, u, 0, a_scratch, d, F, S(stream)) != cudaSuccess)
+    return ODMOE_E_CUDA;
+  if (launch_w2(direct_ref(q2, s2, gate_idx), W_I8, a_scratch, gate_w, y, d, F, S(stream)) != cudaSuccess)
+    return ODMOE_E_CUDA;
+  return ODMOE_OK;
+}
+
+odmoe_status odmoe_lm_head_argmax(const float* h, const void* lm_head, int V, int d, int dt, float eps,
+                                  int32_t* token_out, float* logits, void* scratch, void* stream) {
+  if (!h || !lm_head || !token_out || !scratch || V < 1 || d < 8 || d % 8 || (dt != ODMOE_BF16 && dt != ODMOE_FP32))
+    return ODMOE_E_CONFIG;
+  // zero the ticket word (the kernel re-zeroes it after use)
+  if (cudaMemsetAsync((char*)scratch + 1024 * 8, 0, 8, S(stream)) != cudaSuccess) return ODMOE_E_CUDA;
+  return launch_lm_head(h, lm_head, wtype(dt), V, d, eps, token_out, logits, scratch, S(stream)) == cudaSuccess
+             ? ODMOE_OK : ODMOE_E_CUDA;
+}
+
+odmoe_status odmoe_quantize_int8_rows(const void* w, int64_t R, int64_t C, int dt, int8_t* q, float* s,
+                                      void* stream) {
+  if (!w || !q || !s || R < 0 || C < 1 || (dt != ODMOE_BF16 && dt != ODMOE_FP32)) return ODMOE_E_CONFIG;
+  return launch_quantize(w, R, C, wtype(dt), q, s, S(stream)) == cudaSuccess ? ODMOE_OK : ODMOE_E_CUDA;
+}
+
+odmoe_status odmoe_gen_weights(void* out, int kind, int layer, int expert, int64_t rows, int64_t cols,
+                               int64_t fan_in, int d, int F, uint64_t seed, int dt, void* stream) {
+  if (!out || kind < 0 || kind > 6 || (dt != ODMOE_BF16 && dt != ODMOE_FP32)) return ODMOE_E_CONFIG;
+  if (kind == 0 && (d < 1 || F < 1)) return ODMOE_E_CONFIG;
+  if (kind != 0 && (rows < 0 || cols < 0 || fan_in < 1)) return ODMOE_E_CONFIG;
+  return launch_gen(out, kind, layer, expert, rows, cols, fan_in, d, F, seed, wtype(dt), S(stream)) == cudaSuccess
+             ? ODMOE_OK : ODMOE_E_CUDA;
+}
+
+}  // extern "C"

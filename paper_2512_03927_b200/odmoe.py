@@ -1,0 +1,289 @@
+"""Thin ctypes binding of libodmoe.so (include/odmoe.h). Argument marshalling only: every step
+of the hot path runs in the library's CUDA kernels / C++ runtime. PyTorch tensors are used
+only as device-memory holders (``data_ptr()``) and for the current CUDA stream.
+
+There is no fallback: if the library is missing the import raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libodmoe.so")
+
+BF16, FP32 = 0, 1
+PRED_SHADOW_INT8, PRED_NONE, PRED_RANDOM, PRED_PERFECT, PRED_SHADOW_SAME = 0, 1, 2, 3, 4
+PREDICTORS = {"shadow_int8": 0, "none": 1, "random": 2, "perfect": 3, "shadow_same": 4}
+
+STATUS = {0: "OK", 1: "E_CONFIG", 2: "E_RANGE", 3: "E_NONFINITE", 4: "E_BUDGET", 5: "E_STATE",
+          6: "E_PLAN", 7: "E_NOMEM", 8: "E_CUDA", 9: "E_NCCL"}
+
+# debug_read fields
+DBG = dict(H_IN=0, U=1, LOGITS=2, IDS=3, W=4, Y=5, Y_PART=6, SH_H_IN=7, SH_U=8, SH_LOGITS=9,
+           SH_IDS=10, H_FINAL=11, LM_LOGITS=12)
+
+
+class OdmoeError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built: run `make -C paper_2512_03927_b200` "
+                          "(or __graft_entry__.build()); there is no CPU fallback")
+    return ctypes.CDLL(LIB_PATH)
+
+
+_lib = _load()
+
+
+class Config(ctypes.Structure):
+    _fields_ = [("L", ctypes.c_int32), ("E", ctypes.c_int32), ("k", ctypes.c_int32), ("d", ctypes.c_int32),
+                ("F", ctypes.c_int32), ("V", ctypes.c_int32), ("dtype", ctypes.c_int32),
+                ("predictor", ctypes.c_int32), ("lookahead", ctypes.c_int32),
+                ("slots_per_gpu", ctypes.c_int32), ("rms_eps", ctypes.c_float),
+                ("weight_seed", ctypes.c_uint64), ("aux_seed", ctypes.c_uint64),
+                ("rank", ctypes.c_int32), ("world_size", ctypes.c_int32), ("group_size", ctypes.c_int32),
+                ("device", ctypes.c_int32), ("chunk_bytes", ctypes.c_int64),
+                ("debug_capture", ctypes.c_int32), ("time_kernels", ctypes.c_int32),
+                ("pool_threads", ctypes.c_int32), ("reserved", ctypes.c_int32 * 7),
+                ("nccl_id", ctypes.c_void_p)]
+
+
+class LayerRecord(ctypes.Structure):
+    _fields_ = [("true_ids", ctypes.c_int32 * 8), ("pred_ids", ctypes.c_int32 * 8),
+                ("weights", ctypes.c_float * 8), ("pred_available", ctypes.c_int32),
+                ("correct", ctypes.c_int32), ("n_reloads", ctypes.c_int32),
+                ("load_wait_us", ctypes.c_float)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in (
+        "tokens", "loads_issued", "loads_completed", "loads_cancelled", "reloads", "bytes_h2d",
+        "kernel_launches", "max_resident", "resident_bytes", "shadow_bytes", "pool_bytes")] + [
+        ("pool_build_s", ctypes.c_double)] + [
+        (n, ctypes.c_double) for n in ("ms_router", "ms_w13", "ms_w2", "ms_shadow", "ms_lm_head", "ms_embed")] + [
+        (n, ctypes.c_int64) for n in ("n_router", "n_w13", "n_w2", "n_shadow", "n_lm_head", "n_embed")] + [
+        ("wait_us", ctypes.c_double), ("correct", ctypes.c_int64), ("predicted_total", ctypes.c_int64)]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_F = ctypes.c_float
+_I64 = ctypes.c_int64
+
+
+def _sig(name, args, res=ctypes.c_int):
+    f = getattr(_lib, name)
+    f.argtypes = args
+    f.restype = res
+    return f
+
+
+_abi_version = _sig("odmoe_abi_version", [], ctypes.c_int32)
+_create = _sig("odmoe_create", [ctypes.POINTER(Config), ctypes.POINTER(ctypes.c_void_p)])
+_destroy = _sig("odmoe_destroy", [_P], None)
+_last_error = _sig("odmoe_last_error", [_P], ctypes.c_char_p)
+_get_stats = _sig("odmoe_get_stats", [_P, ctypes.POINTER(Stats)])
+_reset_stats = _sig("odmoe_reset_stats", [_P])
+_nccl_uid = _sig("odmoe_nccl_unique_id", [_P])
+_route = _sig("odmoe_route_topk", [_P, _P, _I, _P, _P, _I, _I, _I, _I, _I, _F, _P, _P, _P, _P, _P, _P])
+_sh_route = _sig("odmoe_shadow_route_topk", [_P, _P, _I, _P, _P, _I, _I, _I, _I, _F, _P, _P, _P, _P, _P, _P])
+_ffn = _sig("odmoe_expert_ffn", [_P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P])
+_sh_ffn = _sig("odmoe_shadow_expert_ffn", [_P, _P, _P, _P, _P, _P, _I, _I, _I, _P, _P, _P])
+_lm = _sig("odmoe_lm_head_argmax", [_P, _P, _I, _I, _I, _F, _P, _P, _P, _P])
+_quant = _sig("odmoe_quantize_int8_rows", [_P, _I64, _I64, _I, _P, _P, _P])
+_gen = _sig("odmoe_gen_weights", [_P, _I, _I, _I, _I64, _I64, _I64, _I, _I, ctypes.c_uint64, _I, _P])
+_load_ = _sig("odmoe_load", [_P, _I, _I])
+_load_wait = _sig("odmoe_load_wait", [_P, _I, _I, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p)])
+_evict = _sig("odmoe_evict", [_P, _I, _I])
+_predict = _sig("odmoe_predict_ahead", [_P, ctypes.c_int32, _I, _I, _P])
+_decode = _sig("odmoe_decode_step", [_P, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32), _P])
+_prefill = _sig("odmoe_prefill", [_P, _P, _I, ctypes.POINTER(ctypes.c_int32), _P])
+_dbg = _sig("odmoe_debug_read", [_P, _I, _I, _P, _I64])
+_tensor_ptr = _sig("odmoe_tensor_ptr", [_P, _I, _I, ctypes.POINTER(ctypes.c_void_p)])
+
+EXPORTED = ["odmoe_abi_version", "odmoe_create", "odmoe_destroy", "odmoe_last_error", "odmoe_get_stats",
+            "odmoe_reset_stats", "odmoe_nccl_unique_id", "odmoe_route_topk", "odmoe_expert_ffn",
+            "odmoe_shadow_expert_ffn", "odmoe_shadow_route_topk", "odmoe_lm_head_argmax",
+            "odmoe_quantize_int8_rows", "odmoe_gen_weights", "odmoe_load", "odmoe_load_wait",
+            "odmoe_evict", "odmoe_predict_ahead", "odmoe_decode_step", "odmoe_prefill",
+            "odmoe_debug_read", "odmoe_tensor_ptr"]
+
+
+def abi_version() -> int:
+    return int(_abi_version())
+
+
+def _check(st: int, ctx=None):
+    if st != 0:
+        msg = _last_error(ctx).decode(errors="replace") if ctx is not None or st else ""
+        raise OdmoeError(st, msg)
+
+
+def _ptr(t) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _ptr_array(tensors: Sequence, device):
+    import torch
+    return torch.tensor([t.data_ptr() for t in tensors], dtype=torch.int64, device=device)
+
+
+# ------------------------------------------------------------------ stateless kernels
+def route_topk(h, w_gate, k: int, u_out, ids, w, logits=None, y_add=(), gamma=None, eps=1e-5,
+               dtype=BF16, flag=None, stream=None):
+    """h [m,d] fp32 (updated in place by the residual add), w_gate [E,d] (bf16 or fp32)."""
+    m, d = h.shape
+    E = w_gate.shape[0]
+    yp = _ptr_array(y_add, h.device) if len(y_add) else None
+    _check(_route(_ptr(h), _ptr(yp), len(y_add), _ptr(gamma), _ptr(w_gate), m, E, d, k, dtype, eps,
+                  _ptr(u_out), _ptr(ids), _ptr(w), _ptr(logits), _ptr(flag), _stream(stream)))
+    return yp  # keep the pointer array alive until the stream passes
+
+
+def shadow_route_topk(h, q_gate, s_gate, k: int, u_out, ids, w, logits=None, y_add=(), eps=1e-5,
+                      flag=None, stream=None):
+    m, d = h.shape
+    E = q_gate.shape[0]
+    yp = _ptr_array(y_add, h.device) if len(y_add) else None
+    _check(_sh_route(_ptr(h), _ptr(yp), len(y_add), _ptr(q_gate), _ptr(s_gate), m, E, d, k, eps,
+                     _ptr(u_out), _ptr(ids), _ptr(w), _ptr(logits), _ptr(flag), _stream(stream)))
+    return yp
+
+
+def expert_ffn(w13, w2, u, a_scratch, y, gate_w=None, gate_idx=0, dtype=BF16, stream=None):
+    """w13 [F,2,d] (or [2F,d]), w2 [d,F], u [d]; y [d] fp32 = gate_w[gate_idx] * FFN(u)."""
+    d = w2.shape[0]
+    F = w2.shape[1]
+    _check(_ffn(_ptr(w13), _ptr(w2), _ptr(u), _ptr(gate_w), gate_idx, d, F, dtype, _ptr(a_scratch),
+                _ptr(y), _stream(stream)))
+
+
+def shadow_expert_ffn(q13, s13, q2, s2, u, a_scratch, y, gate_w=None, gate_idx=0, stream=None):
+    d, F = q2.shape
+    _check(_sh_ffn(_ptr(q13), _ptr(s13), _ptr(q2), _ptr(s2), _ptr(u), _ptr(gate_w), gate_idx, d, F,
+                   _ptr(a_scratch), _ptr(y), _stream(stream)))
+
+
+def lm_head_argmax(h, lm_head, token_out, scratch, logits=None, eps=1e-5, dtype=BF16, stream=None):
+    V, d = lm_head.shape
+    _check(_lm(_ptr(h), _ptr(lm_head), V, d, dtype, eps, _ptr(token_out), _ptr(logits), _ptr(scratch),
+               _stream(stream)))
+
+
+def quantize_int8_rows(w, q, s, dtype=BF16, stream=None):
+    R, C = w.shape
+    _check(_quant(_ptr(w), R, C, dtype, _ptr(q), _ptr(s), _stream(stream)))
+
+
+def gen_weights(out, kind, layer=0, expert=0, rows=0, cols=0, fan_in=1, d=0, F=0, seed=2512, dtype=BF16,
+                stream=None):
+    _check(_gen(_ptr(out), kind, layer, expert, rows, cols, fan_in, d, F, seed, dtype, _stream(stream)))
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    if _nccl_uid(buf) != 0:
+        raise OdmoeError(9, "ncclGetUniqueId failed")
+    return buf.raw
+
+
+# ------------------------------------------------------------------ stateful engine
+class Engine:
+    """One decode engine per process/GPU (odmoe_create ... odmoe_destroy)."""
+
+    def __init__(self, L, E, k, d, F, V, dtype=BF16, predictor=PRED_SHADOW_INT8, lookahead=1,
+                 slots_per_gpu=2, rms_eps=1e-5, weight_seed=2512, aux_seed=1, rank=0, world_size=1,
+                 group_size=0, device=0, chunk_bytes=0, debug_capture=0, time_kernels=0,
+                 nccl_id: Optional[bytes] = None):
+        self.cfg = Config(L=L, E=E, k=k, d=d, F=F, V=V, dtype=dtype, predictor=predictor,
+                          lookahead=lookahead, slots_per_gpu=slots_per_gpu, rms_eps=rms_eps,
+                          weight_seed=weight_seed, aux_seed=aux_seed, rank=rank, world_size=world_size,
+                          group_size=group_size, device=device, chunk_bytes=chunk_bytes,
+                          debug_capture=debug_capture, time_kernels=time_kernels, pool_threads=0)
+        self._uid = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        self.cfg.nccl_id = ctypes.cast(self._uid, ctypes.c_void_p) if self._uid is not None else None
+        self.L, self.E, self.k, self.d, self.F, self.V = L, E, k, d, F, V
+        self.rank = rank
+        h = ctypes.c_void_p()
+        st = _create(ctypes.byref(self.cfg), ctypes.byref(h))
+        if st != 0:
+            raise OdmoeError(st, _last_error(None).decode(errors="replace"))
+        self.ctx = h
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            _destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _ck(self, st):
+        if st != 0:
+            raise OdmoeError(st, _last_error(self.ctx).decode(errors="replace"))
+
+    def decode_step(self, token: int, records: bool = True):
+        out = ctypes.c_int32(-1)
+        recs = (LayerRecord * self.L)() if records else None
+        self._ck(_decode(self.ctx, int(token), ctypes.byref(out), recs))
+        return out.value, recs
+
+    def predict_ahead(self, token: int, from_layer: int = 0, depth: Optional[int] = None):
+        depth = self.L - from_layer if depth is None else depth
+        buf = (ctypes.c_int32 * (depth * self.k))()
+        self._ck(_predict(self.ctx, int(token), from_layer, depth, buf))
+        return [list(buf[i * self.k:(i + 1) * self.k]) for i in range(depth)]
+
+    def load(self, layer, expert):
+        self._ck(_load_(self.ctx, layer, expert))
+
+    def load_wait(self, layer, expert):
+        a, b = ctypes.c_void_p(), ctypes.c_void_p()
+        self._ck(_load_wait(self.ctx, layer, expert, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
+    def evict(self, layer, expert):
+        self._ck(_evict(self.ctx, layer, expert))
+
+    def prefill(self, tokens):
+        arr = (ctypes.c_int32 * len(tokens))(*tokens)
+        out = ctypes.c_int32(-1)
+        counts = (ctypes.c_int32 * (self.L * self.E))()
+        self._ck(_prefill(self.ctx, arr, len(tokens), ctypes.byref(out), counts))
+        return out.value, list(counts)
+
+    def debug_read(self, what: str, layer: int, nbytes: int) -> bytes:
+        buf = ctypes.create_string_buffer(nbytes)
+        self._ck(_dbg(self.ctx, DBG[what], layer, buf, nbytes))
+        return buf.raw
+
+    def tensor_ptr(self, what: int, index: int = 0) -> int:
+        p = ctypes.c_void_p()
+        self._ck(_tensor_ptr(self.ctx, what, index, ctypes.byref(p)))
+        return p.value
+
+    def stats(self) -> dict:
+        s = Stats()
+        self._ck(_get_stats(self.ctx, ctypes.byref(s)))
+        return s.as_dict()
+
+    def reset_stats(self):
+        self._ck(_reset_stats(self.ctx))

@@ -1,0 +1,299 @@
+"""The stateful decode engine through the C ABI vs the CPU oracle (-m gpu).
+
+Parity is teacher-forced per layer (SURVEY §8(c) protocol): the engine's debug capture exports
+h_l, u_l, logits, ids, w and the per-expert outputs of every layer; the oracle recomputes each
+layer from the GPU's own inputs. Because the hot path has no attention/KV state, a decode step
+is a pure function of its input token, so feeding the GPU's previous token to the oracle is the
+token-level teacher forcing."""
+import numpy as np
+import pytest
+
+import oracle as O
+from inputs import MIXTRAL, TINY, gen_expert, gen_model_weights, gen_prompt
+from tests.gpu_util import TOL_BF16, TOL_FP32, ids_match, l2rel, torch
+
+pytestmark = pytest.mark.gpu
+SEED = 2512
+
+
+@pytest.fixture(scope="module")
+def od():
+    t = torch()
+    assert t.cuda.is_available(), "gpu tests need a B200"
+    from paper_2512_03927_b200 import odmoe
+    return odmoe
+
+
+def engine(od, shape, dtype="bf16", **kw):
+    args = dict(dtype=od.BF16 if dtype == "bf16" else od.FP32, weight_seed=SEED)
+    args.update(kw)
+    return od.Engine(shape.L, shape.E, shape.k, shape.d, shape.F, shape.V, **args)
+
+
+def read_f32(eng, what, layer, n):
+    return np.frombuffer(eng.debug_read(what, layer, 4 * n), dtype=np.float32).astype(np.float64)
+
+
+def read_u(eng, what, layer, d, dtype):
+    if dtype == "bf16":
+        b = np.frombuffer(eng.debug_read(what, layer, 2 * d), dtype=np.uint16)
+        return (b.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    return read_f32(eng, what, layer, d)
+
+
+def read_i32(eng, what, layer, n):
+    return np.frombuffer(eng.debug_read(what, layer, 4 * n), dtype=np.int32)
+
+
+def check_step_teacher_forced(eng, W, shape, dtype, token_in, token_out, shadow_W=None):
+    """Per-layer teacher-forced comparison of one captured decode step. Returns #excused."""
+    L, E, k, d = shape.L, shape.E, shape.k, shape.d
+    tol = TOL_BF16 if dtype == "bf16" else TOL_FP32
+    excused = 0
+    h0 = read_f32(eng, "H_IN", 0, d)
+    assert np.array_equal(h0.astype(np.float32), np.asarray(W["emb"][token_in], dtype=np.float32))
+    for l in range(L):
+        h = read_f32(eng, "H_IN", l, d)
+        u = read_u(eng, "U", l, d, dtype)
+        u_ref = O.rms_norm(h)
+        utol = 2.0 ** -8 if dtype == "bf16" else 1e-6
+        assert np.all(np.abs(u - u_ref) <= utol * np.abs(u_ref) + 1e-6), l
+        lg = read_f32(eng, "LOGITS", l, E)
+        r_ref = O.router_logits(W["router"][l], u)
+        assert np.allclose(lg, r_ref, rtol=0, atol=1e-5 * np.abs(r_ref).max() + 1e-7), l
+        ids = read_i32(eng, "IDS", l, k)
+        ok, diff = ids_match(ids, r_ref, k)
+        assert ok, (l, ids, r_ref)
+        excused += diff
+        w = read_f32(eng, "W", l, k)
+        assert np.allclose(w, O.mixture_weights(r_ref, list(ids)), atol=2e-6)
+        yp = read_f32(eng, "Y_PART", l, k * d).reshape(k, d)
+        y_ref_total = np.zeros(d)
+        for j in range(k):
+            W1, W3, W2 = W["experts"][l][int(ids[j])]
+            yr = w[j] * O.expert_ffn(W1, W3, W2, u)
+            assert l2rel(yp[j], yr) <= tol, (l, j, l2rel(yp[j], yr))
+            y_ref_total += yr
+        h_next = read_f32(eng, "H_IN", l + 1, d) if l + 1 < L else read_f32(eng, "H_FINAL", 0, d)
+        assert l2rel(h_next, h + y_ref_total) <= tol, l
+    # LM head + argmax from the captured final hidden state
+    hf = read_f32(eng, "H_FINAL", 0, d)
+    z = read_f32(eng, "LM_LOGITS", 0, shape.V)
+    z_ref = O.final_logits(W["lm_head"], hf)
+    assert np.allclose(z, z_ref, rtol=0, atol=2e-2 * np.abs(z_ref).max())
+    if token_out != O.greedy_argmax(z_ref):
+        zs = np.sort(z_ref)[::-1]
+        assert abs(zs[0] - zs[1]) < 1e-3 * abs(zs[0]) or abs(z_ref[token_out] - zs[0]) < 1e-3 * abs(zs[0])
+        excused += 1
+    if shadow_W is not None:
+        for l in range(L):
+            sh = read_f32(eng, "SH_H_IN", l, d)
+            su = read_u(eng, "SH_U", l, d, "bf16")
+            assert np.all(np.abs(su - O.rms_norm(sh)) <= 2.0 ** -8 * np.abs(O.rms_norm(sh)) + 1e-6)
+            sr_ref = O.router_logits(shadow_W["router"][l], su)
+            sids = read_i32(eng, "SH_IDS", l, k)
+            ok, diff = ids_match(sids, sr_ref, k)
+            assert ok, ("shadow", l, sids, sr_ref)
+            excused += diff
+        # the shadow starts from ITS embedding row of the main token (token alignment)
+        assert np.allclose(read_f32(eng, "SH_H_IN", 0, d), shadow_W["emb"][token_in], rtol=1e-6, atol=1e-9)
+    return excused
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_tiny_decode_teacher_forced(od, dtype):
+    W = gen_model_weights(TINY, SEED, dtype=dtype)
+    SW = O.quantize_model_int8(W)
+    eng = engine(od, TINY, dtype, predictor=od.PRED_SHADOW_INT8, slots_per_gpu=2, debug_capture=1)
+    tok = int(gen_prompt(TINY, 1, 1)[0])
+    excused = 0
+    for n in range(16):
+        nxt, recs = eng.decode_step(tok)
+        excused += check_step_teacher_forced(eng, W, TINY, dtype, tok, nxt, SW)
+        # recall accounting recomputed from the records (Eq. 3, exact)
+        for l in range(TINY.L):
+            S = set(recs[l].true_ids[: TINY.k])
+            P = set(recs[l].pred_ids[: TINY.k])
+            assert recs[l].correct == len(S & P)
+        tok = nxt
+    assert excused <= 3
+    st = eng.stats()
+    assert st["tokens"] == 16
+    assert st["max_resident"] <= 2   # S:326 residency audit at 2 slots
+    eng.close()
+
+
+def test_tiny_fp32_free_run_tokens(od):
+    """fp32 path, 16 tokens x 4 prompts: every token equals the oracle's greedy token for the
+    same input token (no KV state => per-token teacher forcing), barring near-ties."""
+    W = gen_model_weights(TINY, SEED, dtype="fp32")
+    eng = engine(od, TINY, "fp32", predictor=od.PRED_NONE, slots_per_gpu=2)
+    bad = 0
+    for q in range(4):
+        tok = int(gen_prompt(TINY, q + 1, 1)[0])
+        for _ in range(16):
+            nxt, _ = eng.decode_step(tok)
+            ref, _, z = O.decode_token(W, tok, TINY.k)
+            if nxt != ref:
+                zs = np.sort(z)[::-1]
+                assert abs(zs[0] - zs[1]) < 1e-3 * abs(zs[0])
+                bad += 1
+            tok = nxt
+    assert bad <= 1
+    eng.close()
+
+
+def _run(od, shape, n, first, dtype="bf16", **kw):
+    eng = engine(od, shape, dtype, **kw)
+    toks, routes, t = [], [], first
+    for _ in range(n):
+        t, recs = eng.decode_step(t)
+        toks.append(t)
+        routes.append([tuple(r.true_ids[: shape.k]) for r in recs])
+    st = eng.stats()
+    return eng, toks, routes, st
+
+
+def test_output_invariance_across_predictors_slots_and_modes(od):
+    """Placement, prediction and loading change time, never values: bitwise
+    identical tokens and routing for every predictor, slot budget, lookahead and the
+    fully-resident baseline."""
+    first = int(gen_prompt(TINY, 3, 1)[0])
+    base_eng, base, base_r, _ = _run(od, TINY, 12, first, predictor=od.PRED_NONE, slots_per_gpu=2)
+    base_eng.close()
+    for kw in (dict(predictor=od.PRED_SHADOW_INT8, slots_per_gpu=2),
+               dict(predictor=od.PRED_SHADOW_INT8, slots_per_gpu=5, lookahead=3),
+               dict(predictor=od.PRED_RANDOM, slots_per_gpu=3, lookahead=2),
+               dict(predictor=od.PRED_SHADOW_SAME, slots_per_gpu=4, lookahead=2),
+               dict(predictor=od.PRED_NONE, slots_per_gpu=-1),
+               dict(predictor=od.PRED_SHADOW_INT8, slots_per_gpu=2, chunk_bytes=65536)):
+        eng, toks, routes, _ = _run(od, TINY, 12, first, **kw)
+        assert toks == base, kw
+        assert routes == base_r, kw
+        eng.close()
+
+
+def test_same_precision_shadow_recall_exactly_one(od):
+    eng, toks, _, st = _run(od, TINY, 10, 5, predictor=od.PRED_SHADOW_SAME, slots_per_gpu=4, lookahead=2)
+    assert st["predicted_total"] == 10 * TINY.L * TINY.k
+    assert st["correct"] == st["predicted_total"]
+    # with every prediction right, loads = L*k per token (no reloads)
+    assert st["reloads"] <= TINY.L * TINY.k  # layer-0 loads may start after the router (late departure)
+    eng.close()
+
+
+def test_random_predictor_recall_closed_form(od):
+    """random prefetch recall ~ k/E = 0.25 (closed form for uniform k-subsets)."""
+    n = 64
+    eng, _, _, st = _run(od, TINY, n, 7, predictor=od.PRED_RANDOM, slots_per_gpu=2, aux_seed=11)
+    r = st["correct"] / st["predicted_total"]
+    p = TINY.k / TINY.E
+    sigma = (p * (1 - p) / (TINY.k * TINY.L * n)) ** 0.5
+    assert abs(r - p) < 4 * sigma * 1.5, r
+    eng.close()
+
+
+def test_perfect_predictor_replays_routing(od):
+    eng = engine(od, TINY, predictor=od.PRED_PERFECT, slots_per_gpu=4, lookahead=2)
+    t = 9
+    seq = []
+    for _ in range(6):
+        t, _ = eng.decode_step(t)
+        seq.append(t)
+    eng.reset_stats()
+    t = 9
+    for _ in range(6):
+        t, recs = eng.decode_step(t)
+    st = eng.stats()
+    assert st["correct"] == st["predicted_total"] == 6 * TINY.L * TINY.k
+    eng.close()
+
+
+def test_loader_roundtrip_bytes(od):
+    """odmoe_load / load_wait / evict: the slot holds exactly the generator's bytes (H2D path)."""
+    from tests.gpu_util import d2h, w13_interleaved
+    eng = engine(od, TINY, predictor=od.PRED_NONE, slots_per_gpu=2)
+    F, d = TINY.F, TINY.d
+    n = 3 * F * d
+    for (l, e) in [(0, 0), (3, 7), (2, 5)]:
+        eng.load(l, e)
+        p13, p2 = eng.load_wait(l, e)
+        assert p2 - p13 == 2 * 2 * F * d
+        raw = np.frombuffer(d2h(p13, 2 * n), dtype=np.uint16)
+        got = (raw.astype(np.uint32) << 16).view(np.float32)
+        W1, W3, W2 = gen_expert(TINY, SEED, l, e, "bf16")
+        assert np.array_equal(got[: 2 * F * d].reshape(F, 2, d), w13_interleaved(W1, W3))
+        assert np.array_equal(got[2 * F * d:].reshape(d, F), W2)
+        eng.evict(l, e)
+    with pytest.raises(od.OdmoeError):
+        eng.evict(0, 0)
+    eng.load(1, 1)
+    eng.load(1, 2)
+    with pytest.raises(od.OdmoeError):
+        eng.load(1, 3)  # E_BUDGET: both slots occupied
+    eng.close()
+
+
+def test_predict_ahead_matches_decode_records(od):
+    eng = engine(od, TINY, predictor=od.PRED_SHADOW_INT8, slots_per_gpu=2)
+    P = eng.predict_ahead(33)
+    nxt, recs = eng.decode_step(33)
+    for l in range(TINY.L):
+        assert sorted(P[l]) == sorted(recs[l].pred_ids[: TINY.k])
+    assert eng.predict_ahead(33, 1, 2) == P[1:3]
+    eng.close()
+
+
+def test_config_errors(od):
+    with pytest.raises(od.OdmoeError) as ei:
+        od.Engine(4, 8, 9, 256, 512, 1024)
+    assert ei.value.status == 1
+    with pytest.raises(od.OdmoeError):
+        od.Engine(4, 8, 2, 250, 512, 1024)
+    with pytest.raises(od.OdmoeError):
+        od.Engine(4, 8, 2, 256, 512, 1024, world_size=3, rank=0)
+    eng = engine(od, TINY, predictor=od.PRED_NONE)
+    with pytest.raises(od.OdmoeError) as ei:
+        eng.decode_step(TINY.V)
+    assert ei.value.status == 2
+    eng.close()
+
+
+# ------------------------------------------------------------------ Mixtral shape (full size)
+@pytest.mark.slow
+def test_mixtral_decode_sampled_layers(od):
+    """BASELINE.json configs[1] shape in the bench's launch configuration (1 GPU, 2 slots,
+    INT8 shadow): two decode steps; teacher-forced oracle checks on sampled layers (the oracle
+    regenerates those experts itself from the seed)."""
+    shape = MIXTRAL
+    eng = engine(od, shape, "bf16", predictor=od.PRED_SHADOW_INT8, slots_per_gpu=2, debug_capture=1)
+    tok = int(gen_prompt(shape, 1, 1)[0])
+    W = gen_model_weights(shape, SEED, dtype="bf16", layers=[])  # emb + LM head (+ no layers)
+    from inputs import KIND_ROUTER, tensor_id, weight_fp32, bf16_bits_to_f32, f32_to_bf16_bits
+    for step in range(2):
+        nxt, recs = eng.decode_step(tok)
+        d, k, E = shape.d, shape.k, shape.E
+        h0 = read_f32(eng, "H_IN", 0, d)
+        assert np.array_equal(h0.astype(np.float32), W["emb"][tok])
+        for l in ([0, 31] if step == 0 else [17]):
+            Wg = bf16_bits_to_f32(f32_to_bf16_bits(weight_fp32(SEED, tensor_id(KIND_ROUTER, l), E, d, d))).reshape(E, d)
+            h = read_f32(eng, "H_IN", l, d)
+            u = read_u(eng, "U", l, d, "bf16")
+            assert np.all(np.abs(u - O.rms_norm(h)) <= 2.0 ** -8 * np.abs(O.rms_norm(h)) + 1e-6)
+            r_ref = O.router_logits(Wg, u)
+            ids = read_i32(eng, "IDS", l, k)
+            assert ids_match(ids, r_ref, k)[0]
+            w = read_f32(eng, "W", l, k)
+            yp = read_f32(eng, "Y_PART", l, k * d).reshape(k, d)
+            for j in range(k):
+                W1, W3, W2 = gen_expert(shape, SEED, l, int(ids[j]), "bf16")
+                assert l2rel(yp[j], w[j] * O.expert_ffn(W1, W3, W2, u)) <= 1e-5
+        z = read_f32(eng, "LM_LOGITS", 0, shape.V)
+        z_ref = O.final_logits(W["lm_head"], read_f32(eng, "H_FINAL", 0, d))
+        assert np.allclose(z, z_ref, rtol=0, atol=2e-2 * np.abs(z_ref).max())
+        zs = np.sort(z_ref)[::-1]
+        assert nxt == O.greedy_argmax(z_ref) or abs(zs[0] - zs[1]) < 1e-3 * abs(zs[0])
+        tok = nxt
+    st = eng.stats()
+    assert st["max_resident"] <= 2 and st["resident_bytes"] < 1e9  # < 1 GB of experts per GPU
+    eng.close()
