@@ -127,6 +127,20 @@ odmoe_status odmoe_get_stats(const void* ctx, odmoe_stats* out);
 odmoe_status odmoe_reset_stats(void* ctx);
 int odmoe_nccl_unique_id(void* out128); /* fills a 128-byte ncclUniqueId; returns 0 on success */
 
+/* ------------------------------------------------------------------ placement plan (host only) */
+
+/* Experts of `layer` that `rank` computes for router output ids[k] (P:104 groups of G workers,
+ * one-to-one assignment; P:113-120 layer -> group l mod N_G round robin
+ * sorted pairing; Q14 G = min(k, N) when group_size == 0, a GPU takes k/G experts when G < k).
+ * Writes *n_out (0..k) ascending expert ids to out[k] (host). Pure function; no GPU needed.
+ * E_CONFIG on invalid sizes (world % G, k % G, rank range). */
+odmoe_status odmoe_plan_layer(int k, int world_size, int group_size, int layer, const int32_t* ids,
+                              int rank, int32_t* out, int32_t* n_out);
+/* 1 if `rank`'s host pool must hold expert (layer, expert) (some routing can send it there under
+ * the sorted pairing), 0 if not, -1 on invalid sizes. Pure function. */
+int32_t odmoe_plan_pool_holds(int E, int k, int world_size, int group_size, int layer, int expert,
+                              int rank);
+
 /* ------------------------------------------------------------------ stateless kernels */
 
 /* Fused residual-combine + RMSNorm + router GEMV + softmax/top-k + renormalise
@@ -170,6 +184,29 @@ odmoe_status odmoe_shadow_route_topk(float* h, const float* const* y_add, int n_
                                      const int8_t* q_gate, const float* s_gate, int m, int E, int d,
                                      int k, float eps, void* u_out, int32_t* ids, float* w,
                                      float* logits, int32_t* flag, void* stream);
+
+/* Prefill grouping ("embeddings are grouped by their desired experts"): stable
+ * counting sort of the T*k (token, slot) pairs of ids [T,k] by expert. Outputs (device):
+ * offsets [E+1] (rows of expert e are [offsets[e], offsets[e+1])), src_pair [T*k] (pair index
+ * t*k+j of each grouped row), inv [T*k] (grouped row of each pair), gate_perm [T*k] (w of that
+ * pair). Stable: within an expert, pairs keep ascending (t, j) order. */
+odmoe_status odmoe_prefill_group(const int32_t* ids, const float* w, int T, int k, int E,
+                                 int32_t* offsets, int32_t* src_pair, int32_t* inv,
+                                 float* gate_perm, void* stream);
+
+/* Grouped expert SwiGLU FFN for prefill on the tcgen05 tensor cores (a11; Q8):
+ * for every expert e and grouped row r in [offsets[e], offsets[e+1]):
+ *   a2[r] = bf16(silu(W1_e x[r]) * (W3_e x[r]))   and   y[r] = gate_perm[r] * (W2_e a2[r]).
+ * w13[e], w2[e]: HOST arrays of DEVICE pointers (bf16 [F][2][d] and [d][F]); x_perm [M,d] bf16,
+ * gate_perm [M] fp32, a2_scratch [M,F] bf16, y_perm [M,d] fp32 (device); offsets [n_experts+1]
+ * HOST int32, M = offsets[n_experts]; tiles_scratch device >= 16*(M/128 + n_experts)*(2F/256 +
+ * d/128) bytes. Limits: n_experts <= 8, d % 256 == 0, F % 128 == 0, bf16 only. Synchronous on
+ * `stream` (returns after the GEMMs complete). */
+odmoe_status odmoe_expert_ffn_grouped(const void* const* w13, const void* const* w2, int n_experts,
+                                      const void* x_perm, const int32_t* offsets,
+                                      const float* gate_perm, int d, int F, void* a2_scratch,
+                                      float* y_perm, void* tiles_scratch,
+                                      int64_t tiles_scratch_bytes, void* stream);
 
 /* Final RMSNorm + LM head GEMV + greedy argmax (a10; S:95 lowest id on ties).
  *   h [d] fp32 (h_L), lm_head [V,d] dt; token_out int32 device scalar;
@@ -216,11 +253,19 @@ odmoe_status odmoe_predict_ahead(void* ctx, int32_t token, int from_layer, int d
 odmoe_status odmoe_decode_step(void* ctx, int32_t token_in, int32_t* token_out,
                                odmoe_layer_record* rec);
 
-/* Batched prefill of T tokens: no prediction; tokens grouped per expert; grouped
- * expert GEMM; token_out = argmax after the last prompt token; expert_counts [L,E] host or
- * NULL. Collective, synchronous. */
+/* Batched prefill of T tokens: no prediction; layer by layer: batched router (T rows),
+ * grouping by expert, tcgen05 grouped expert GEMMs, deterministic scatter-combine. Layer l's E
+ * experts are loaded onto the G GPUs of group l mod N_G (expert e -> position e*G/E), so loads
+ * round-robin over the groups. token_out = greedy token after the last prompt token;
+ * expert_counts [L,E] host or NULL (tokens routed per expert, P:214 footnote). Needs the bf16
+ * model and 2*E/G extra device expert slots. Collective, synchronous. */
 odmoe_status odmoe_prefill(void* ctx, const int32_t* tokens, int T, int32_t* token_out,
                            int32_t* expert_counts);
+
+/* Prefill capture (cfg.debug_capture == 1), rank 0, last prefill: what 0 = residual h entering
+ * layer `layer` ([T][d] fp32; layer == L gives the final h), what 1 = router ids of `layer`
+ * ([T][k] int32). */
+odmoe_status odmoe_prefill_debug_read(const void* ctx, int what, int layer, void* dst, int64_t bytes);
 
 /* Parity capture (cfg.debug_capture == 1), rank 0, last decode step. Copies `bytes` bytes of
  * field `what` for `layer` into host `dst`. Fields and sizes:

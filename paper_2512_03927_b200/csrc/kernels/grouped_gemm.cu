@@ -1,0 +1,260 @@
+// Prefill grouped expert GEMM on the 5th-generation tensor cores (P:214
+// "token embeddings routed to the same expert can be grouped and computed via a larger matrix
+// multiplication"). This is the one place on the path where the work is a real dense contraction
+// (m_e ~ T*k/E = 128 rows per expert at T = 512), so it runs on tcgen05:
+//
+//   C_e[m_e x N] = A[rows of expert e] (K-major bf16) . B_e[N x K]^T (K-major bf16), fp32 in TMEM
+//
+// GEMM1: A = X_perm [M, d], B_e = W13_e [2F, d] (gate/up interleaved) -> SwiGLU epilogue ->
+//        A2 [M, F] bf16 (reading Q8: the prefill intermediate is bf16, the tensor-core input type).
+// GEMM2: A = A2 [M, F], B_e = W2_e [d, F] -> gate-scale epilogue -> Y_perm [M, d] fp32.
+//
+// Kernel anatomy (one 128 x BN output tile per CTA, 6 warps):
+//   warp 0   : TMA producer, 4-stage ring of {A 128x64, B BNx64} bf16 tiles (128B swizzle)
+//   warp 1   : TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN, K=16 per MMA),
+//              tcgen05.commit -> stage "empty" mbarriers and the accumulator-ready mbarrier
+//   warps 2-5: epilogue, tcgen05.ld 32x32b (each warp owns its 32-lane TMEM quadrant)
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace odmoe {
+
+constexpr int kGG_BM = 128;
+constexpr int kGG_BK = 64;  // 64 bf16 = 128 bytes = one swizzle row
+constexpr int kGG_STAGES = 4;
+constexpr int kGG_THREADS = 192;
+
+struct GGMaps {
+  CUtensorMap b[kMaxGGExperts];
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+// K-major operand, 128-byte swizzle: rows of 128 B, 8-row atoms 1024 B apart (SBO), LBO unused (1),
+// descriptor version 1 (sm100), layout type 2 (SWIZZLE_128B).
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+// kind::f16 instruction descriptor: D fp32, A/B bf16, both K-major, M = 128, N = BN.
+__host__ __device__ constexpr uint32_t umma_idesc_bf16(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+template <int BN, int MODE>  // MODE 0: SwiGLU -> bf16 [M, N/2]; MODE 1: gate-scale -> fp32 [M, N]
+__global__ void __launch_bounds__(kGG_THREADS, 1)
+grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ GGMaps maps_b,
+                    const int4* __restrict__ tiles, int K, int N, void* __restrict__ out,
+                    const float* __restrict__ gate) {
+  constexpr int A_BYTES = kGG_BM * kGG_BK * 2;
+  constexpr int B_BYTES = BN * kGG_BK * 2;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kGG_STAGES * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + kGG_STAGES * B_BYTES);
+  uint64_t* empty = full + kGG_STAGES;
+  uint64_t* acc_ready = empty + kGG_STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_ready + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int4 tile = tiles[blockIdx.x];  // {expert, row0, rows, n0}
+  const int expert = tile.x, row0 = tile.y, rows = tile.z, n0 = tile.w;
+  const int KB = K / kGG_BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kGG_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    mbar_init(acc_ready, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps_b.b[expert])) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kb = 0; kb < KB; ++kb) {
+        const int s = kb % kGG_STAGES;
+        const uint32_t ph = (uint32_t)(kb / kGG_STAGES) & 1u;
+        mbar_wait(&empty[s], ph ^ 1u);
+        mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
+        tma_load_2d(sA + s * A_BYTES, &map_a, &full[s], kb * kGG_BK, row0);
+        tma_load_2d(sB + s * B_BYTES, &maps_b.b[expert], &full[s], kb * kGG_BK, n0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(kGG_BM, BN);
+      for (int kb = 0; kb < KB; ++kb) {
+        const int s = kb % kGG_STAGES;
+        const uint32_t ph = (uint32_t)(kb / kGG_STAGES) & 1u;
+        mbar_wait(&full[s], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t a0 = smem_u32(sA + s * A_BYTES), b0 = smem_u32(sB + s * B_BYTES);
+#pragma unroll
+        for (int k = 0; k < kGG_BK / 16; ++k)
+          umma_bf16(tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc, (kb | k) != 0);
+        umma_commit(&empty[s]);  // smem slot free once these MMAs have read it
+      }
+      umma_commit(acc_ready);
+    }
+  } else {
+    // epilogue: warp w owns TMEM lanes [32*(w%4), +32) = tile rows
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    mbar_wait(acc_ready, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const bool valid = r < rows;
+    const long long grow = (long long)row0 + r;
+    const float g = (MODE == 1 && valid) ? gate[grow] : 0.f;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 16) {
+      uint32_t v[16];
+      tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, v);
+      if (!valid) continue;
+      if constexpr (MODE == 0) {
+        uint32_t packed[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float a0 = silu_mul(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]));
+          const float a1 = silu_mul(__uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+          const __nv_bfloat162 b = __floats2bfloat162_rn(a0, a1);
+          packed[i] = *reinterpret_cast<const uint32_t*>(&b);
+        }
+        __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(out) + grow * (N / 2) + (n0 + c0) / 2;
+        *reinterpret_cast<uint4*>(o) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+      } else {
+        float* o = reinterpret_cast<float*>(out) + grow * N + n0 + c0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          reinterpret_cast<float4*>(o)[i] =
+              make_float4(g * __uint_as_float(v[4 * i]), g * __uint_as_float(v[4 * i + 1]),
+                          g * __uint_as_float(v[4 * i + 2]), g * __uint_as_float(v[4 * i + 3]));
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+  }
+}
+
+// ---------------------------------------------------------------- host side
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 2-D bf16 row-major [rows, cols] tensor, box = {64 cols, box_rows rows}, 128B swizzle.
+static bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {(cuuint32_t)kGG_BK, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int BN, int MODE>
+static cudaError_t gg_launch(const GroupedGemmArgs& g, cudaStream_t s) {
+  CUtensorMap ma;
+  GGMaps mb;
+  if (!make_map(&ma, g.a, (uint64_t)g.M, (uint64_t)g.K, kGG_BM)) return cudaErrorInvalidValue;
+  for (int e = 0; e < g.n_experts; ++e)
+    if (g.b[e] && !make_map(&mb.b[e], g.b[e], (uint64_t)g.N, (uint64_t)g.K, BN)) return cudaErrorInvalidValue;
+  const size_t smem = 1024 + (size_t)kGG_STAGES * (kGG_BM + BN) * kGG_BK * 2 + 256;
+  auto kern = grouped_gemm_kernel<BN, MODE>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<g.n_tiles, kGG_THREADS, smem, s>>>(ma, mb, g.tiles, g.K, g.N, g.out, g.gate);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_grouped_gemm(const GroupedGemmArgs& g, cudaStream_t s) {
+  if (g.n_experts > kMaxGGExperts || g.K % kGG_BK) return cudaErrorInvalidValue;
+  if (g.n_tiles == 0) return cudaSuccess;
+  if (g.mode == 0) {
+    if (g.N % 256) return cudaErrorInvalidValue;
+    return gg_launch<256, 0>(g, s);
+  }
+  if (g.N % 128) return cudaErrorInvalidValue;
+  return gg_launch<128, 1>(g, s);
+}
+
+int grouped_gemm_bn(int mode) { return mode == 0 ? 256 : 128; }
+
+}  // namespace odmoe

@@ -51,6 +51,37 @@ cudaError_t launch_lm_head(const float* h, const void* W, WType wt, int V, int d
 cudaError_t launch_embed(const void* emb, const float* emb_scale, WType wt, const int32_t* token,
                          int d, float* h, cudaStream_t s);
 
+// Prefill grouped expert GEMM on tcgen05. Tiles are {expert, row0, rows, n0} (device
+// int4 array): rows [row0, row0+rows) of A belong to `expert`; A is [M, K] bf16 (rows of all
+// experts, grouped), b[e] is expert e's [N, K] bf16 matrix (K-major), out is
+// mode 0: SwiGLU of interleaved column pairs -> bf16 [M, N/2]; mode 1: gate[row] * C -> fp32 [M, N].
+constexpr int kMaxGGExperts = 8;
+struct GroupedGemmArgs {
+  const void* a;
+  const void* b[kMaxGGExperts];
+  int n_experts;
+  const int4* tiles;
+  int n_tiles;
+  int M, N, K;
+  int mode;
+  void* out;
+  const float* gate;
+};
+cudaError_t launch_grouped_gemm(const GroupedGemmArgs& g, cudaStream_t s);
+int grouped_gemm_bn(int mode);  // output-tile width for the mode (tile n0 step)
+
+// Prefill permutation: stable counting sort of the T*k pairs by expert.
+cudaError_t launch_route_group(const int32_t* ids, const float* w, int n_pairs, int E, int32_t* offsets,
+                               int32_t* src_pair, int32_t* inv, float* gate_perm, cudaStream_t s);
+cudaError_t launch_gather_rows(const void* u, const int32_t* src_pair, int k, int M, int d, void* out,
+                               cudaStream_t s);
+// h[t] += sum_j y[inv[t*k+j]] (partial == 0), or h[t] = that sum (partial == 1, N > 1 share).
+cudaError_t launch_scatter_combine(float* h, const float* y, const int32_t* inv, int T, int k, int d,
+                                   int partial, cudaStream_t s);
+cudaError_t launch_add_rows(float* h, const float* y, long long n, cudaStream_t s);
+cudaError_t launch_embed_rows(const void* emb, WType wt, const int32_t* tokens, int T, int d, float* h,
+                              cudaStream_t s);
+
 // Synthetic weights. kind 1..6 plain tensor rows x cols; kind 0 = expert blob.
 cudaError_t launch_gen(void* out, int kind, int layer, int expert, int64_t rows, int64_t cols,
                        int64_t fan_in, int d, int F, uint64_t seed, WType wt, cudaStream_t s);

@@ -142,6 +142,28 @@ __global__ void embed_kernel(const WT* __restrict__ emb, const float* __restrict
   }
 }
 
+// Batched embedding gather for prefill: h[t] = Emb[tokens[t]].
+template <typename WT>
+__global__ void embed_rows_kernel(const WT* __restrict__ emb, const int32_t* __restrict__ tokens, int d,
+                                  float* __restrict__ h) {
+  const long long t = tokens[blockIdx.x];
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    float v;
+    if constexpr (std::is_same<WT, __nv_bfloat16>::value) v = __bfloat162float(emb[t * d + j]);
+    else v = emb[t * d + j];
+    h[(size_t)blockIdx.x * d + j] = v;
+  }
+}
+
+cudaError_t launch_embed_rows(const void* emb, WType wt, const int32_t* tokens, int T, int d, float* h,
+                              cudaStream_t s) {
+  if (T == 0) return cudaSuccess;
+  if (wt == W_BF16) embed_rows_kernel<__nv_bfloat16><<<T, 256, 0, s>>>((const __nv_bfloat16*)emb, tokens, d, h);
+  else if (wt == W_F32) embed_rows_kernel<float><<<T, 256, 0, s>>>((const float*)emb, tokens, d, h);
+  else return cudaErrorInvalidValue;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_embed(const void* emb, const float* emb_scale, WType wt, const int32_t* token,
                          int d, float* h, cudaStream_t s) {
   const int grid = (d + 255) / 256 < 16 ? (d + 255) / 256 : 16;

@@ -128,6 +128,27 @@ struct Ctx {
 
   odmoe_stats stats{};
 
+  // prefill: batch buffers sized for T_cap tokens, E/G expert slots x 2 (double buffer)
+  int T_cap = 0;
+  float* p_h = nullptr;          // [T, d] residual
+  char* p_pkt = nullptr;         // [T] u (bf16 [T,d]) | ids [T,k] | w [T,k]  (broadcast at N > 1)
+  int64_t p_pkt_bytes = 0, p_ids_off = 0, p_w_off = 0;
+  int32_t* p_tok = nullptr;      // [T]
+  int32_t* p_off = nullptr;      // [E+1]
+  int32_t* p_src = nullptr;      // [T*k]
+  int32_t* p_inv = nullptr;      // [T*k]
+  float* p_gate = nullptr;       // [T*k]
+  void* p_x = nullptr;           // [T*k, d] bf16 grouped rows
+  void* p_a2 = nullptr;          // [T*k, F] bf16
+  float* p_y = nullptr;          // [T*k, d] fp32
+  float* p_part = nullptr;       // [T, d] fp32 (N > 1 partial combine)
+  int4* p_tiles = nullptr;       // [tiles_cap]
+  int tiles_cap = 0;
+  int32_t* h_off = nullptr;      // pinned [E+1]
+  std::vector<Slot> pslots;
+  std::vector<float> p_dbg;      // debug: [L+1][T][d] h per layer (rank 0)
+  std::vector<int32_t> p_dbg_ids;  // [L][T][k]
+
   // debug capture (rank 0)
   float* dbg_h = nullptr;        // device [L][d]
   float* dbg_ypart = nullptr;    // device [L][k][d]

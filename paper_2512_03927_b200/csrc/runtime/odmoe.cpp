@@ -139,17 +139,42 @@ void harvest_timers(Ctx* c) {
 }
 
 // ------------------------------------------------------------------ placement
-// Experts of layer l handled by this rank given routing S (k ids): empty unless this rank is in
-// group l mod N_G; sorted experts paired with sorted group GPUs; with G < k a GPU takes
-// k/G consecutive sorted experts (reading Q14).
+// Pure placement functions (also exported as odmoe_plan_* for host-side tests).
+// Experts of layer l that `rank` computes for routing S (k ids): none unless the rank is in group
+// l mod N_G; sorted experts paired with sorted group GPUs; with G < k a GPU takes k/G
+// consecutive sorted experts (reading Q14).
+int plan_layer(int k, int world, int G, int l, const int32_t* S, int rank, int32_t* out) {
+  const int NG = world / G;
+  if ((l % NG) != rank / G) return 0;
+  const int pos = rank % G;
+  int32_t s[8];
+  if (k < 1 || k > 8) return 0;
+  for (int i = 0; i < k; ++i) s[i] = S[i];
+  // insertion sort (k <= 8)
+  for (int i = 1; i < k; ++i)
+    for (int j = i; j > 0 && s[j - 1] > s[j]; --j) std::swap(s[j - 1], s[j]);
+  int n = 0;
+  for (int i = 0; i < k; ++i)
+    if (i * G / k == pos) out[n++] = s[i];
+  return n;
+}
+
+// Can the sorted pairing ever send (l, e) to `rank`? Position p receives the i-th smallest of k
+// distinct ids for i in [p*k/G, (p+1)*k/G), so it needs >= p*k/G smaller and >= (G-1-p)*k/G larger
+// ids among E experts.
+bool plan_pool_holds(int E, int k, int world, int G, int l, int e, int rank) {
+  const int NG = world / G;
+  if ((l % NG) != rank / G) return false;
+  const int pos = rank % G;
+  const int lo = pos * (k / G);
+  const int hi = (G - 1 - pos) * (k / G);
+  return e >= lo && e <= E - 1 - hi;
+}
+
 std::vector<int> my_experts(const Ctx* c, int l, const int32_t* S) {
-  std::vector<int> out;
-  if ((l % c->NG) != c->my_group) return out;
-  std::vector<int> s(S, S + c->k);
-  std::sort(s.begin(), s.end());
-  for (int i = 0; i < c->k; ++i)
-    if (i * c->G / c->k == c->my_pos) out.push_back(s[i]);
-  return out;
+  int32_t buf[8];
+  const int n = plan_layer(c->k, c->world, c->G, l, S, c->rank, buf);
+  return std::vector<int>(buf, buf + n);
 }
 
 bool holds_expert(const Ctx* c, int l, int e) { return c->pool_off[(size_t)l * c->E + e] >= 0; }
@@ -231,15 +256,9 @@ void build_shadow(Ctx* c, char* staging) {
   CUDA_OK(c, cudaStreamSynchronize(c->s_main));
 }
 
-// Which (layer, expert) blobs this rank may ever need: all experts of the layers of its group
-// that the sorted pairing can assign to its position.
+// Which (layer, expert) blobs this rank may ever need.
 bool rank_may_need(const Ctx* c, int l, int e) {
-  if ((l % c->NG) != c->my_group) return false;
-  // with sorted pairing position p receives only experts with >= p*k/G smaller and
-  // >= (G-1-p)*k/G larger ids among the k selected
-  const int lo = c->my_pos * (c->k / c->G);
-  const int hi = (c->G - 1 - c->my_pos) * (c->k / c->G);
-  return e >= lo && e <= c->E - 1 - hi;
+  return plan_pool_holds(c->E, c->k, c->world, c->G, l, e, c->rank);
 }
 
 void build_pool(Ctx* c, char* staging) {
@@ -505,9 +524,8 @@ int occupied_count(const Ctx* c) {
   return n;
 }
 
-void submit_load(Ctx* c, int slot, int64_t tok, int l, int e, int64_t key) {
+void submit_into(Ctx* c, Slot& s, int slot, int64_t tok, int l, int e, int64_t key) {
   if (!holds_expert(c, l, e)) fail(c, ODMOE_E_RANGE, "expert not in this rank's pool");
-  Slot& s = c->slots[slot];
   s.occupied = true;
   s.token = tok;
   s.layer = l;
@@ -526,6 +544,10 @@ void submit_load(Ctx* c, int slot, int64_t tok, int l, int e, int64_t key) {
   r->wait_ev = s.free_recorded ? s.ev_free : nullptr;
   s.req = r;
   c->loader.submit(r);
+}
+
+void submit_load(Ctx* c, int slot, int64_t tok, int l, int e, int64_t key) {
+  submit_into(c, c->slots[slot], slot, tok, l, e, key);
   c->stats.max_resident = std::max<int64_t>(c->stats.max_resident, occupied_count(c));
 }
 
@@ -849,6 +871,225 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
   }
 }
 
+// ------------------------------------------------------------------ prefill
+// Layer l's E experts are split over the G GPUs of group l mod N_G in sorted order (expert e ->
+// position e*G/E): with N = E = G this is the paper's "each worker handles one expert of every
+// layer"; with fewer GPUs it keeps the decode pool placement and round-robins the loads over the
+// groups, so group g loads layer l + 1 while another group computes layer l.
+bool prefill_mine(const Ctx* c, int l, int e) {
+  return (l % c->NG) == c->my_group && e * c->G / c->E == c->my_pos;
+}
+
+void ensure_prefill(Ctx* c, int T) {
+  const int E = c->E, k = c->k, d = c->d, F = c->F;
+  if (c->pslots.empty() && !c->resident) {
+    c->pslots.resize((size_t)2 * std::max(1, E / c->G));
+    for (auto& s : c->pslots) {
+      s.dev = dmalloc<char>(c, c->blob_bytes, "prefill slot");
+      CUDA_OK(c, cudaEventCreateWithFlags(&s.ev_w13, cudaEventDisableTiming));
+      CUDA_OK(c, cudaEventCreateWithFlags(&s.ev_done, cudaEventDisableTiming));
+      CUDA_OK(c, cudaEventCreateWithFlags(&s.ev_free, cudaEventDisableTiming));
+    }
+  }
+  if (!c->h_off) c->h_off = hmalloc<int32_t>(c, (size_t)E + 1, "h_off");
+  if (T <= c->T_cap) return;
+  auto F_ = [](void* p) { if (p) cudaFree(p); };
+  F_(c->p_h); F_(c->p_pkt); F_(c->p_tok); F_(c->p_off); F_(c->p_src); F_(c->p_inv); F_(c->p_gate);
+  F_(c->p_x); F_(c->p_a2); F_(c->p_y); F_(c->p_part); F_(c->p_tiles);
+  const int64_t M = (int64_t)T * k;
+  c->p_ids_off = (int64_t)T * d * 2;
+  c->p_w_off = c->p_ids_off + 4 * M;
+  c->p_pkt_bytes = c->p_w_off + 4 * M;
+  c->p_h = dmalloc<float>(c, (size_t)T * d, "p_h");
+  c->p_pkt = dmalloc<char>(c, (size_t)c->p_pkt_bytes, "p_pkt");
+  c->p_tok = dmalloc<int32_t>(c, T, "p_tok");
+  c->p_off = dmalloc<int32_t>(c, (size_t)E + 1, "p_off");
+  c->p_src = dmalloc<int32_t>(c, M, "p_src");
+  c->p_inv = dmalloc<int32_t>(c, M, "p_inv");
+  c->p_gate = dmalloc<float>(c, M, "p_gate");
+  c->p_x = dmalloc<char>(c, (size_t)M * d * 2, "p_x");
+  c->p_a2 = dmalloc<char>(c, (size_t)M * F * 2, "p_a2");
+  c->p_y = dmalloc<float>(c, (size_t)M * d, "p_y");
+  c->p_part = dmalloc<float>(c, (size_t)T * d, "p_part");
+  c->tiles_cap = (int)(((M + 127) / 128 + E) * (2 * F / grouped_gemm_bn(0) + d / grouped_gemm_bn(1)));
+  c->p_tiles = dmalloc<int4>(c, (size_t)c->tiles_cap, "p_tiles");
+  c->T_cap = T;
+}
+
+// Tile list {expert, row0, rows, n0} for the experts in `mine` (host offsets).
+void build_tiles(const std::vector<int32_t>& off, const std::vector<int>& mine, int N, int BN,
+                 std::vector<int4>& out) {
+  for (int e : mine) {
+    const int m = off[e + 1] - off[e];
+    for (int m0 = 0; m0 < m; m0 += 128)
+      for (int n0 = 0; n0 < N; n0 += BN) out.push_back(make_int4(e, off[e] + m0, std::min(128, m - m0), n0));
+  }
+}
+
+void prefill_impl(Ctx* c, const int32_t* tokens, int T, int32_t* token_out, int32_t* counts_out) {
+  const int L = c->L, E = c->E, k = c->k, d = c->d, F = c->F;
+  if (c->wt != W_BF16) fail(c, ODMOE_E_CONFIG, "prefill runs the bf16 tensor-core GEMM: needs dtype BF16");
+  if (E > kMaxGGExperts) fail(c, ODMOE_E_CONFIG, "prefill supports E <= 8");
+  if (d % 256 || F % 128) fail(c, ODMOE_E_CONFIG, "prefill needs d % 256 == 0 and F % 128 == 0");
+  if (T < 1 || !tokens) fail(c, ODMOE_E_CONFIG, "empty prompt (S:108)");
+  for (int t = 0; t < T; ++t)
+    if (tokens[t] < 0 || tokens[t] >= c->V) fail(c, ODMOE_E_RANGE, "token out of range");
+  ensure_prefill(c, T);
+  cudaStream_t s = c->s_main;
+  const bool r0 = c->rank == 0;
+  const int64_t M = (int64_t)T * k;
+  if (r0) {
+    CUDA_OK(c, cudaMemcpy(c->p_tok, tokens, 4 * (size_t)T, cudaMemcpyHostToDevice));
+    CUDA_OK(c, launch_embed_rows(c->d_emb, c->wt, c->p_tok, T, d, c->p_h, s));
+    c->stats.kernel_launches++;
+  }
+  // this rank's expert loads, in layer order (no prediction in prefill)
+  std::vector<std::pair<int, int>> need;
+  for (int l = 0; l < L; ++l)
+    for (int e = 0; e < E; ++e)
+      if (prefill_mine(c, l, e)) need.push_back({l, e});
+  size_t next = 0;
+  auto find_p = [&](int l, int e) {
+    for (int i = 0; i < (int)c->pslots.size(); ++i)
+      if (c->pslots[i].occupied && c->pslots[i].layer == l && c->pslots[i].expert == e) return i;
+    return -1;
+  };
+  auto ppump = [&]() {
+    if (c->resident) return;
+    while (next < need.size()) {
+      int fs = -1;
+      for (int i = 0; i < (int)c->pslots.size(); ++i)
+        if (!c->pslots[i].occupied) { fs = i; break; }
+      if (fs < 0) break;
+      submit_into(c, c->pslots[fs], fs, -3, need[next].first, need[next].second, (int64_t)need[next].first * 16);
+      next++;
+    }
+  };
+  ppump();
+  if (c->cfg.debug_capture && r0) {
+    c->p_dbg.assign((size_t)(L + 1) * T * d, 0.f);
+    c->p_dbg_ids.assign((size_t)L * T * k, -1);
+    CUDA_OK(c, cudaMemcpyAsync(c->p_dbg.data(), c->p_h, sizeof(float) * T * d, cudaMemcpyDeviceToHost, s));
+  }
+  std::vector<int32_t> counts((size_t)L * E, 0), off(E + 1);
+  std::vector<int4> tiles;
+  char* u = c->p_pkt;
+  int32_t* ids = (int32_t*)(c->p_pkt + c->p_ids_off);
+  float* w = (float*)(c->p_pkt + c->p_w_off);
+  for (int l = 0; l < L; ++l) {
+    if (r0) {
+      KTimer t(c, K_ROUTER, s);
+      CUDA_OK(c, launch_router(c->p_h, nullptr, 0, nullptr, (const char*)c->d_router + (size_t)l * E * d * c->esz,
+                               nullptr, c->wt, T, E, d, k, c->cfg.rms_eps, u, ids, w, nullptr, c->d_flag, s));
+    }
+    if (c->world > 1) NCCL_OK(c, ncclBroadcast(c->p_pkt, c->p_pkt, (size_t)c->p_pkt_bytes, ncclChar, 0, c->comm, s));
+    CUDA_OK(c, launch_route_group(ids, w, (int)M, E, c->p_off, c->p_src, c->p_inv, c->p_gate, s));
+    CUDA_OK(c, cudaMemcpyAsync(c->h_off, c->p_off, 4 * (size_t)(E + 1), cudaMemcpyDeviceToHost, s));
+    CUDA_OK(c, cudaEventRecord(c->ev_ids, s));
+    for (;;) {
+      const cudaError_t q = cudaEventQuery(c->ev_ids);
+      if (q == cudaSuccess) break;
+      if (q != cudaErrorNotReady) CUDA_OK(c, q);
+      ppump();
+      if (c->loader.error() != cudaSuccess) CUDA_OK(c, c->loader.error());
+      std::this_thread::sleep_for(std::chrono::microseconds(5));
+    }
+    std::copy(c->h_off, c->h_off + E + 1, off.begin());
+    for (int e = 0; e < E; ++e) counts[(size_t)l * E + e] = off[e + 1] - off[e];
+    if (c->cfg.debug_capture && r0)
+      CUDA_OK(c, cudaMemcpy(c->p_dbg_ids.data() + (size_t)l * T * k, ids, 4 * (size_t)M, cudaMemcpyDeviceToHost));
+    const bool in_group = (l % c->NG) == c->my_group;
+    if (in_group) {
+      std::vector<int> mine;
+      for (int e = 0; e < E; ++e)
+        if (prefill_mine(c, l, e)) mine.push_back(e);
+      CUDA_OK(c, launch_gather_rows(u, c->p_src, k, (int)M, d, c->p_x, s));
+      tiles.clear();
+      build_tiles(off, mine, 2 * F, grouped_gemm_bn(0), tiles);
+      const int n1 = (int)tiles.size();
+      build_tiles(off, mine, d, grouped_gemm_bn(1), tiles);
+      const int n2 = (int)tiles.size() - n1;
+      if ((int)tiles.size() > c->tiles_cap) fail(c, ODMOE_E_STATE, "tile list overflow");
+      if (!tiles.empty())
+        CUDA_OK(c, cudaMemcpyAsync(c->p_tiles, tiles.data(), sizeof(int4) * tiles.size(), cudaMemcpyHostToDevice, s));
+      GroupedGemmArgs g1{}, g2{};
+      g1.n_experts = g2.n_experts = E;
+      std::vector<int> used;
+      for (int e : mine) {
+        const char* blob = nullptr;
+        if (c->resident) {
+          blob = c->res_blob[(size_t)l * E + e];
+        } else {
+          const int si = find_p(l, e);
+          if (si < 0) fail(c, ODMOE_E_STATE, "prefill expert not loading");
+          Slot& sl = c->pslots[si];
+          if (!c->loader.wait_issued(sl.req)) {
+            if (c->loader.error() != cudaSuccess) CUDA_OK(c, c->loader.error());
+            fail(c, ODMOE_E_STATE, "prefill load cancelled");
+          }
+          CUDA_OK(c, cudaStreamWaitEvent(s, sl.ev_done, 0));
+          blob = sl.dev;
+          used.push_back(si);
+        }
+        g1.b[e] = blob;
+        g2.b[e] = blob + c->w13_bytes;
+      }
+      g1.a = c->p_x; g1.tiles = c->p_tiles; g1.n_tiles = n1; g1.M = (int)M; g1.N = 2 * F; g1.K = d;
+      g1.mode = 0; g1.out = c->p_a2; g1.gate = nullptr;
+      g2.a = c->p_a2; g2.tiles = c->p_tiles + n1; g2.n_tiles = n2; g2.M = (int)M; g2.N = d; g2.K = F;
+      g2.mode = 1; g2.out = c->p_y; g2.gate = c->p_gate;
+      if (c->world > 1) CUDA_OK(c, cudaMemsetAsync(c->p_y, 0, sizeof(float) * M * d, s));
+      { KTimer t(c, K_W13, s); CUDA_OK(c, launch_grouped_gemm(g1, s)); }
+      { KTimer t(c, K_W2, s); CUDA_OK(c, launch_grouped_gemm(g2, s)); }
+      for (int si : used) {
+        Slot& sl = c->pslots[si];
+        CUDA_OK(c, cudaEventRecord(sl.ev_free, s));
+        sl.free_recorded = true;
+        sl.req.reset();
+        sl.occupied = false;
+        sl.layer = sl.expert = -1;
+      }
+    }
+    if (c->world == 1) {
+      CUDA_OK(c, launch_scatter_combine(c->p_h, c->p_y, c->p_inv, T, k, d, 0, s));
+    } else {
+      if (in_group) CUDA_OK(c, launch_scatter_combine(c->p_part, c->p_y, c->p_inv, T, k, d, 1, s));
+      else CUDA_OK(c, cudaMemsetAsync(c->p_part, 0, sizeof(float) * T * d, s));
+      NCCL_OK(c, ncclReduce(c->p_part, c->p_y, (size_t)T * d, ncclFloat32, ncclSum, 0, c->comm, s));
+      if (r0) CUDA_OK(c, launch_add_rows(c->p_h, c->p_y, (long long)T * d, s));
+    }
+    c->stats.kernel_launches += 4;
+    ppump();
+    if (c->cfg.debug_capture && r0)
+      CUDA_OK(c, cudaMemcpyAsync(c->p_dbg.data() + (size_t)(l + 1) * T * d, c->p_h, sizeof(float) * T * d,
+                                 cudaMemcpyDeviceToHost, s));
+  }
+  if (r0) {
+    KTimer t(c, K_LM, s);
+    CUDA_OK(c, launch_lm_head(c->p_h + (size_t)(T - 1) * d, c->d_lm, c->wt, c->V, d, c->cfg.rms_eps,
+                              c->d_tok_out, c->cfg.debug_capture ? c->d_lmlogits : nullptr, c->d_lmscratch, s));
+  }
+  if (c->world > 1) NCCL_OK(c, ncclBroadcast(c->d_tok_out, c->d_tok_out, 1, ncclInt32, 0, c->comm, s));
+  CUDA_OK(c, cudaMemcpyAsync(c->h_tok + 1, c->d_tok_out, 4, cudaMemcpyDeviceToHost, s));
+  CUDA_OK(c, cudaMemcpyAsync(c->h_flag, c->d_flag, 4, cudaMemcpyDeviceToHost, s));
+  CUDA_OK(c, cudaStreamSynchronize(s));
+  if (c->h_flag[0]) fail(c, ODMOE_E_NONFINITE, "non-finite router logits");
+  if (c->cfg.time_kernels) harvest_timers(c);
+  c->stats.bytes_h2d = c->loader.bytes_h2d.load();
+  c->stats.loads_issued = c->loader.loads_issued.load();
+  c->stats.loads_completed = c->loader.loads_completed.load();
+  *token_out = c->h_tok[1];
+  if (counts_out) std::copy(counts.begin(), counts.end(), counts_out);
+  if (c->cfg.debug_capture && r0) {
+    // last-token LM logits for the argmax check
+    c->hdbg_index.erase(12);
+    const int64_t off12 = (int64_t)c->hdbg.size();
+    c->hdbg.resize(c->hdbg.size() + (size_t)c->V * 4);
+    CUDA_OK(c, cudaMemcpy(c->hdbg.data() + off12, c->d_lmlogits, (size_t)c->V * 4, cudaMemcpyDeviceToHost));
+    c->hdbg_index[12] = {off12, (int64_t)c->V * 4};
+  }
+}
+
 void destroy_ctx(Ctx* c) {
   if (!c) return;
   cudaSetDevice(c->dev);
@@ -877,6 +1118,15 @@ void destroy_ctx(Ctx* c) {
   F(c->d_lmscratch); F(c->d_lmlogits);
   F(c->sh_h); F(c->sh_u); F(c->sh_ids); F(c->sh_w); F(c->sh_logits); F(c->sh_a); F(c->sh_y); F((void*)c->sh_yptr);
   F(c->dbg_h); F(c->dbg_ypart); F(c->dbg_yred); F(c->dbg_sh_h); F(c->dbg_sh_u); F(c->dbg_hfinal);
+  F(c->p_h); F(c->p_pkt); F(c->p_tok); F(c->p_off); F(c->p_src); F(c->p_inv); F(c->p_gate);
+  F(c->p_x); F(c->p_a2); F(c->p_y); F(c->p_part); F(c->p_tiles);
+  for (auto& s : c->pslots) {
+    F(s.dev);
+    if (s.ev_w13) cudaEventDestroy(s.ev_w13);
+    if (s.ev_done) cudaEventDestroy(s.ev_done);
+    if (s.ev_free) cudaEventDestroy(s.ev_free);
+  }
+  if (c->h_off) cudaFreeHost(c->h_off);
   auto FH = [](void* p) { if (p) cudaFreeHost(p); };
   FH(c->pool); FH(c->h_ids); FH(c->h_w); FH(c->h_pred); FH(c->h_tok); FH(c->h_flag);
   for (auto e : c->ev_pred) cudaEventDestroy(e);
@@ -897,6 +1147,23 @@ void destroy_ctx(Ctx* c) {
 extern "C" {
 
 int32_t odmoe_abi_version(void) { return ODMOE_ABI_VERSION; }
+
+odmoe_status odmoe_plan_layer(int k, int world_size, int group_size, int layer, const int32_t* ids,
+                              int rank, int32_t* out, int32_t* n_out) {
+  const int G = group_size > 0 ? group_size : std::min(k, world_size);
+  if (k < 1 || k > 8 || world_size < 1 || G < 1 || world_size % G || k % G || rank < 0 ||
+      rank >= world_size || layer < 0 || !ids || !out || !n_out)
+    return ODMOE_E_CONFIG;
+  *n_out = plan_layer(k, world_size, G, layer, ids, rank, out);
+  return ODMOE_OK;
+}
+
+int32_t odmoe_plan_pool_holds(int E, int k, int world_size, int group_size, int layer, int expert, int rank) {
+  const int G = group_size > 0 ? group_size : std::min(k, world_size);
+  if (k < 1 || E < k || world_size < 1 || G < 1 || world_size % G || k % G || rank < 0 || rank >= world_size)
+    return -1;
+  return plan_pool_holds(E, k, world_size, G, layer, expert, rank) ? 1 : 0;
+}
 
 int odmoe_nccl_unique_id(void* out128) {
   ncclUniqueId id;
@@ -1063,9 +1330,31 @@ odmoe_status odmoe_evict(void* ctx, int layer, int expert) {
 
 odmoe_status odmoe_prefill(void* ctx, const int32_t* tokens, int T, int32_t* token_out, int32_t* expert_counts) {
   CTX_GUARD(ctx);
-  (void)tokens; (void)T; (void)token_out; (void)expert_counts;
-  c->err = "odmoe_prefill: grouped-GEMM prefill not built in this revision";
-  return ODMOE_E_STATE;
+  if (!token_out) return ODMOE_E_CONFIG;
+  return guard(c, [&] { prefill_impl(c, tokens, T, token_out, expert_counts); });
+}
+
+odmoe_status odmoe_prefill_debug_read(const void* ctx, int what, int layer, void* dst, int64_t bytes) {
+  const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
+  if (!c || !dst) return ODMOE_E_STATE;
+  if (what == 0) {  // h entering layer `layer` (layer == L: final), [T][d] fp32
+    const int64_t per = (int64_t)c->T_cap * c->d * 4;
+    if (c->p_dbg.empty() || layer < 0 || layer > c->L) return ODMOE_E_RANGE;
+    const int64_t T = (int64_t)c->p_dbg.size() / ((int64_t)(c->L + 1) * c->d);
+    const int64_t per_l = T * c->d * 4;
+    (void)per;
+    if (bytes > per_l) return ODMOE_E_RANGE;
+    std::memcpy(dst, reinterpret_cast<const char*>(c->p_dbg.data()) + layer * per_l, (size_t)bytes);
+    return ODMOE_OK;
+  }
+  if (what == 1) {  // router ids of layer `layer`, [T][k] int32
+    if (c->p_dbg_ids.empty() || layer < 0 || layer >= c->L) return ODMOE_E_RANGE;
+    const int64_t per_l = (int64_t)c->p_dbg_ids.size() / c->L * 4;
+    if (bytes > per_l) return ODMOE_E_RANGE;
+    std::memcpy(dst, reinterpret_cast<const char*>(c->p_dbg_ids.data()) + layer * per_l, (size_t)bytes);
+    return ODMOE_OK;
+  }
+  return ODMOE_E_RANGE;
 }
 
 odmoe_status odmoe_debug_read(const void* ctx, int what, int layer, void* dst, int64_t bytes) {
@@ -1139,6 +1428,49 @@ odmoe_status odmoe_expert_ffn(const void* w13, const void* w2, const void* u, co
   if (launch_w2(direct_ref(w2, nullptr, gate_idx), wt, a_scratch, gate_w, y, d, F, S(stream)) != cudaSuccess)
     return ODMOE_E_CUDA;
   return ODMOE_OK;
+}
+
+odmoe_status odmoe_expert_ffn_grouped(const void* const* w13, const void* const* w2, int n_experts,
+                                      const void* x_perm, const int32_t* offsets, const float* gate_perm,
+                                      int d, int F, void* a2_scratch, float* y_perm, void* tiles_scratch,
+                                      int64_t tiles_scratch_bytes, void* stream) {
+  if (!w13 || !w2 || !x_perm || !offsets || !gate_perm || !a2_scratch || !y_perm || !tiles_scratch ||
+      n_experts < 1 || n_experts > kMaxGGExperts || d % 256 || F % 128 || d < 256 || F < 128)
+    return ODMOE_E_CONFIG;
+  std::vector<int32_t> off(offsets, offsets + n_experts + 1);
+  for (int e = 0; e < n_experts; ++e)
+    if (off[e + 1] < off[e]) return ODMOE_E_CONFIG;
+  std::vector<int> all(n_experts);
+  for (int e = 0; e < n_experts; ++e) all[e] = e;
+  std::vector<int4> tiles;
+  build_tiles(off, all, 2 * F, grouped_gemm_bn(0), tiles);
+  const int n1 = (int)tiles.size();
+  build_tiles(off, all, d, grouped_gemm_bn(1), tiles);
+  if ((int64_t)(tiles.size() * sizeof(int4)) > tiles_scratch_bytes) return ODMOE_E_CONFIG;
+  const int M = off[n_experts];
+  if (M == 0) return ODMOE_OK;
+  if (cudaMemcpyAsync(tiles_scratch, tiles.data(), sizeof(int4) * tiles.size(), cudaMemcpyHostToDevice, S(stream)) != cudaSuccess)
+    return ODMOE_E_CUDA;
+  GroupedGemmArgs g1{}, g2{};
+  g1.n_experts = g2.n_experts = n_experts;
+  for (int e = 0; e < n_experts; ++e) { g1.b[e] = w13[e]; g2.b[e] = w2[e]; }
+  g1.a = x_perm; g1.tiles = (const int4*)tiles_scratch; g1.n_tiles = n1; g1.M = M; g1.N = 2 * F; g1.K = d;
+  g1.mode = 0; g1.out = a2_scratch;
+  g2.a = a2_scratch; g2.tiles = (const int4*)tiles_scratch + n1; g2.n_tiles = (int)tiles.size() - n1;
+  g2.M = M; g2.N = d; g2.K = F; g2.mode = 1; g2.out = y_perm; g2.gate = gate_perm;
+  if (launch_grouped_gemm(g1, S(stream)) != cudaSuccess) return ODMOE_E_CUDA;
+  if (launch_grouped_gemm(g2, S(stream)) != cudaSuccess) return ODMOE_E_CUDA;
+  // the host tile list must outlive the async copy from pageable memory
+  if (cudaStreamSynchronize(S(stream)) != cudaSuccess) return ODMOE_E_CUDA;
+  return ODMOE_OK;
+}
+
+odmoe_status odmoe_prefill_group(const int32_t* ids, const float* w, int T, int k, int E, int32_t* offsets,
+                                 int32_t* src_pair, int32_t* inv, float* gate_perm, void* stream) {
+  if (!ids || !w || !offsets || !src_pair || !inv || !gate_perm || T < 0 || k < 1 || E < 1 || E > 64)
+    return ODMOE_E_CONFIG;
+  return launch_route_group(ids, w, T * k, E, offsets, src_pair, inv, gate_perm, S(stream)) == cudaSuccess
+             ? ODMOE_OK : ODMOE_E_CUDA;
 }
 
 odmoe_status odmoe_shadow_expert_ffn(const int8_t* q13, const float* s13, const int8_t* q2,

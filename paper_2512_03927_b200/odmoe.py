@@ -110,7 +110,14 @@ _prefill = _sig("odmoe_prefill", [_P, _P, _I, ctypes.POINTER(ctypes.c_int32), _P
 _dbg = _sig("odmoe_debug_read", [_P, _I, _I, _P, _I64])
 _tensor_ptr = _sig("odmoe_tensor_ptr", [_P, _I, _I, ctypes.POINTER(ctypes.c_void_p)])
 
-EXPORTED = ["odmoe_abi_version", "odmoe_create", "odmoe_destroy", "odmoe_last_error", "odmoe_get_stats",
+_ffn_grouped = _sig("odmoe_expert_ffn_grouped", [_P, _P, _I, _P, _P, _P, _I, _I, _P, _P, _P, _I64, _P])
+_prefill_group = _sig("odmoe_prefill_group", [_P, _P, _I, _I, _I, _P, _P, _P, _P, _P])
+_prefill_dbg = _sig("odmoe_prefill_debug_read", [_P, _I, _I, _P, _I64])
+_plan_layer = _sig("odmoe_plan_layer", [_I, _I, _I, _I, _P, _I, _P, ctypes.POINTER(ctypes.c_int32)])
+_plan_pool = _sig("odmoe_plan_pool_holds", [_I, _I, _I, _I, _I, _I, _I], ctypes.c_int32)
+
+EXPORTED = ["odmoe_expert_ffn_grouped", "odmoe_prefill_group", "odmoe_prefill_debug_read",
+            "odmoe_plan_layer", "odmoe_plan_pool_holds", "odmoe_abi_version", "odmoe_create", "odmoe_destroy", "odmoe_last_error", "odmoe_get_stats",
             "odmoe_reset_stats", "odmoe_nccl_unique_id", "odmoe_route_topk", "odmoe_expert_ffn",
             "odmoe_shadow_expert_ffn", "odmoe_shadow_route_topk", "odmoe_lm_head_argmax",
             "odmoe_quantize_int8_rows", "odmoe_gen_weights", "odmoe_load", "odmoe_load_wait",
@@ -179,6 +186,27 @@ def shadow_expert_ffn(q13, s13, q2, s2, u, a_scratch, y, gate_w=None, gate_idx=0
                    _ptr(a_scratch), _ptr(y), _stream(stream)))
 
 
+def prefill_group(ids, w, E: int, offsets, src_pair, inv, gate_perm, stream=None):
+    """ids [T,k] int32, w [T,k] fp32 -> offsets [E+1], src_pair/inv [T*k] int32, gate_perm [T*k]."""
+    T, k = ids.shape
+    _check(_prefill_group(_ptr(ids), _ptr(w), T, k, E, _ptr(offsets), _ptr(src_pair), _ptr(inv),
+                          _ptr(gate_perm), _stream(stream)))
+
+
+def expert_ffn_grouped(w13s, w2s, x_perm, offsets: Sequence[int], gate_perm, a2_scratch, y_perm, tiles_scratch,
+                       stream=None):
+    """Grouped SwiGLU FFN on tcgen05: w13s/w2s lists of bf16 device tensors (one per expert),
+    offsets host list [E+1]. Synchronous on the stream."""
+    n = len(w13s)
+    d = w2s[0].shape[0]
+    F = w2s[0].shape[1]
+    a13 = (ctypes.c_void_p * n)(*[t.data_ptr() for t in w13s])
+    a2 = (ctypes.c_void_p * n)(*[t.data_ptr() for t in w2s])
+    off = (ctypes.c_int32 * (n + 1))(*offsets)
+    _check(_ffn_grouped(a13, a2, n, _ptr(x_perm), off, _ptr(gate_perm), d, F, _ptr(a2_scratch), _ptr(y_perm),
+                        _ptr(tiles_scratch), tiles_scratch.numel() * tiles_scratch.element_size(), _stream(stream)))
+
+
 def lm_head_argmax(h, lm_head, token_out, scratch, logits=None, eps=1e-5, dtype=BF16, stream=None):
     V, d = lm_head.shape
     _check(_lm(_ptr(h), _ptr(lm_head), V, d, dtype, eps, _ptr(token_out), _ptr(logits), _ptr(scratch),
@@ -193,6 +221,22 @@ def quantize_int8_rows(w, q, s, dtype=BF16, stream=None):
 def gen_weights(out, kind, layer=0, expert=0, rows=0, cols=0, fan_in=1, d=0, F=0, seed=2512, dtype=BF16,
                 stream=None):
     _check(_gen(_ptr(out), kind, layer, expert, rows, cols, fan_in, d, F, seed, dtype, _stream(stream)))
+
+
+def plan_layer(k: int, world_size: int, layer: int, ids: Sequence[int], rank: int, group_size: int = 0):
+    """Experts of `layer` computed by `rank` (host-only placement plan)."""
+    arr = (ctypes.c_int32 * k)(*ids)
+    out = (ctypes.c_int32 * k)()
+    n = ctypes.c_int32(0)
+    _check(_plan_layer(k, world_size, group_size, layer, arr, rank, out, ctypes.byref(n)))
+    return list(out[: n.value])
+
+
+def plan_pool_holds(E: int, k: int, world_size: int, layer: int, expert: int, rank: int, group_size: int = 0) -> bool:
+    r = _plan_pool(E, k, world_size, group_size, layer, expert, rank)
+    if r < 0:
+        raise OdmoeError(1, "invalid plan sizes")
+    return bool(r)
 
 
 def nccl_unique_id() -> bytes:
@@ -269,6 +313,11 @@ class Engine:
         counts = (ctypes.c_int32 * (self.L * self.E))()
         self._ck(_prefill(self.ctx, arr, len(tokens), ctypes.byref(out), counts))
         return out.value, list(counts)
+
+    def prefill_debug_read(self, what: int, layer: int, nbytes: int) -> bytes:
+        buf = ctypes.create_string_buffer(nbytes)
+        self._ck(_prefill_dbg(self.ctx, what, layer, buf, nbytes))
+        return buf.raw
 
     def debug_read(self, what: str, layer: int, nbytes: int) -> bytes:
         buf = ctypes.create_string_buffer(nbytes)

@@ -1,0 +1,148 @@
+"""Prefill (a11): grouping kernel, tcgen05 grouped expert GEMM and the engine's prefill,
+through the C ABI, vs the CPU oracle (-m gpu)."""
+import numpy as np
+import pytest
+
+import oracle as O
+from inputs import MIXTRAL, TINY, gen_expert, gen_model_weights, gen_prompt
+from tests.gpu_util import TOL_BF16, host, ids_match, l2rel, to_dev, torch, w13_interleaved
+
+pytestmark = pytest.mark.gpu
+SEED = 2512
+
+
+@pytest.fixture(scope="module")
+def od():
+    t = torch()
+    assert t.cuda.is_available(), "gpu tests need a B200"
+    from paper_2512_03927_b200 import odmoe
+    return odmoe
+
+
+@pytest.mark.parametrize("T,E,k", [(37, 8, 2), (512, 8, 2), (1, 8, 2), (300, 64, 4)])
+def test_prefill_group_matches_oracle_permutation(od, T, E, k):
+    t = torch()
+    rng = np.random.default_rng(T + E)
+    ids = np.stack([rng.choice(E, size=k, replace=False) for _ in range(T)]).astype(np.int32)
+    w = rng.random((T, k)).astype(np.float32)
+    offs = t.empty(E + 1, dtype=t.int32, device="cuda")
+    src = t.empty(T * k, dtype=t.int32, device="cuda")
+    inv = t.empty(T * k, dtype=t.int32, device="cuda")
+    gate = t.empty(T * k, dtype=t.float32, device="cuda")
+    od.prefill_group(t.from_numpy(ids).cuda(), t.from_numpy(w).cuda(), E, offs, src, inv, gate)
+    t.cuda.synchronize()
+    pairs = O.prefill_permutation(ids)  # stable (expert, token, slot) order
+    want_src = [tt * k + j for _, tt, j in pairs]
+    assert src.cpu().tolist() == want_src
+    cnt = O.expert_counts(ids, E)
+    assert offs.cpu().tolist() == [0] + list(np.cumsum(cnt))
+    invh = inv.cpu().numpy()
+    assert np.array_equal(np.asarray(want_src)[invh], np.arange(T * k))
+    assert np.array_equal(gate.cpu().numpy(), w.reshape(-1)[want_src])
+
+
+def _grouped_case(od, shape, counts, check_rows):
+    t = torch()
+    d, F = shape.d, shape.F
+    E = len(counts)
+    off = [0] + list(np.cumsum(counts))
+    M = off[-1]
+    rng = np.random.default_rng(M)
+    x = np.stack([O.rms_norm(rng.uniform(-1, 1, d)) for _ in range(M)]).astype(np.float32)
+    xb = to_dev(x, "bf16")
+    x_st = host(xb)  # the bf16 values the GPU sees
+    gate = rng.random(M).astype(np.float32)
+    mats = [gen_expert(shape, SEED, 1, e, "bf16") for e in range(E)]
+    w13s = [to_dev(w13_interleaved(W1, W3), "bf16") for (W1, W3, _) in mats]
+    w2s = [to_dev(W2, "bf16") for (_, _, W2) in mats]
+    a2 = t.empty((max(M, 1), F), dtype=t.bfloat16, device="cuda")
+    y = t.full((max(M, 1), d), float("nan"), dtype=t.float32, device="cuda")
+    tiles = t.empty(16 * ((M // 128 + E + 1) * (2 * F // 256 + d // 128)), dtype=t.uint8, device="cuda")
+    od.expert_ffn_grouped(w13s, w2s, xb, off, t.from_numpy(gate).cuda(), a2, y, tiles)
+    yh = host(y)
+    errs = []
+    for e in range(E):
+        rows = list(range(off[e], off[e + 1]))
+        if check_rows is not None and len(rows) > check_rows:
+            rows = rows[:2] + rows[len(rows) // 2: len(rows) // 2 + 1] + rows[-1:]
+        for r in rows:
+            W1, W3, W2 = mats[e]
+            ref = gate[r] * O.expert_ffn(W1, W3, W2, x_st[r])
+            err = l2rel(yh[r], ref)
+            errs.append(err)
+            assert err <= TOL_BF16, (e, r, err)
+    return max(errs) if errs else 0.0
+
+
+def test_grouped_ffn_tiny_ragged(od):
+    """Ragged per-expert row counts spanning 0, 1, a full 128-row tile, tile+1 and several tiles."""
+    shape = type(TINY)(L=1, E=8, k=2, d=256, F=512, V=16)
+    err = _grouped_case(od, shape, [0, 1, 127, 128, 129, 300, 5, 33], None)
+    print("grouped tiny max l2rel", err)
+
+
+@pytest.mark.slow
+def test_grouped_ffn_mixtral_shape(od):
+    """Mixtral shape, T=512 prompt tokens x top-2 = 1024 grouped rows over 8 experts."""
+    rng = np.random.default_rng(3)
+    ids = np.stack([rng.choice(8, size=2, replace=False) for _ in range(512)])
+    counts = list(O.expert_counts(ids, 8))
+    err = _grouped_case(od, MIXTRAL, counts, 4)
+    print("grouped mixtral max l2rel", err)
+
+
+def _prefill_engine(od, **kw):
+    return od.Engine(TINY.L, TINY.E, TINY.k, TINY.d, TINY.F, TINY.V, dtype=od.BF16, weight_seed=SEED, **kw)
+
+
+def test_prefill_engine_tiny_teacher_forced(od):
+    W = gen_model_weights(TINY, SEED, dtype="bf16")
+    prompt = [int(x) for x in gen_prompt(TINY, 5, 37)]
+    T, d, k = len(prompt), TINY.d, TINY.k
+    eng = _prefill_engine(od, predictor=od.PRED_NONE, slots_per_gpu=2, debug_capture=1)
+    tok, counts = eng.prefill(prompt)
+    counts = np.array(counts).reshape(TINY.L, TINY.E)
+    assert np.all(counts.sum(axis=1) == T * k)
+    h = np.frombuffer(eng.prefill_debug_read(0, 0, T * d * 4), dtype=np.float32).reshape(T, d)
+    assert np.array_equal(h, np.stack([W["emb"][p] for p in prompt]))
+    excused = 0
+    for l in range(TINY.L):
+        h = np.frombuffer(eng.prefill_debug_read(0, l, T * d * 4), dtype=np.float32).reshape(T, d).astype(np.float64)
+        h2 = np.frombuffer(eng.prefill_debug_read(0, l + 1, T * d * 4), dtype=np.float32).reshape(T, d)
+        ids = np.frombuffer(eng.prefill_debug_read(1, l, T * k * 4), dtype=np.int32).reshape(T, k)
+        assert np.array_equal(np.bincount(ids.reshape(-1), minlength=TINY.E), counts[l])
+        for t_ in range(T):
+            u = O.rms_norm(h[t_])
+            r = O.router_logits(W["router"][l], u)
+            ok, diff = ids_match(ids[t_], r, k)
+            assert ok, (l, t_, ids[t_], r)
+            excused += diff
+            out = O.moe_layer(h[t_], W["router"][l], W["experts"][l], k, S=list(ids[t_]))
+            assert l2rel(h2[t_], out["h_next"]) <= TOL_BF16, (l, t_, l2rel(h2[t_], out["h_next"]))
+    hf = np.frombuffer(eng.prefill_debug_read(0, TINY.L, T * d * 4), dtype=np.float32).reshape(T, d)
+    z = O.final_logits(W["lm_head"], hf[-1])
+    zs = np.sort(z)[::-1]
+    assert tok == O.greedy_argmax(z) or abs(zs[0] - zs[1]) < 1e-3 * abs(zs[0])
+    assert excused <= 3
+    # the last prompt token's prefill output agrees with a decode step of that token (no KV state)
+    nxt, _ = eng.decode_step(prompt[-1])
+    assert nxt == tok
+    eng.close()
+
+
+def test_prefill_resident_equals_on_demand(od):
+    prompt = [int(x) for x in gen_prompt(TINY, 6, 64)]
+    a = _prefill_engine(od, predictor=od.PRED_NONE, slots_per_gpu=2)
+    ta, ca = a.prefill(prompt)
+    a.close()
+    b = _prefill_engine(od, predictor=od.PRED_NONE, slots_per_gpu=-1)
+    tb, cb = b.prefill(prompt)
+    b.close()
+    assert ta == tb and ca == cb
+    # prefill of a single token
+    c = _prefill_engine(od, predictor=od.PRED_NONE, slots_per_gpu=2)
+    t1, c1 = c.prefill(prompt[:1])
+    assert sum(c1) == TINY.L * TINY.k
+    with pytest.raises(od.OdmoeError):
+        c.prefill([])
+    c.close()

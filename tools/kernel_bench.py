@@ -1,0 +1,131 @@
+"""Microbenchmark of the hot kernels through the C ABI (stateless calls, small memory footprint,
+suitable for ncu): expert SwiGLU GEMV pair (bf16 / int8 shadow), router, LM head, grouped GEMM.
+Times with CUDA events on the launching stream, L2 flushed (256 MB write) before every launch.
+
+    python tools/kernel_bench.py [--iters 20] [--only gemv]
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_2512_03927_b200 import odmoe  # noqa: E402
+
+d, F, E, V = 4096, 14336, 8, 32000
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
+
+
+def timeit(fn, iters, flush):
+    ts = []
+    s = torch.cuda.current_stream()
+    for i in range(iters + 3):
+        flush.add_(1)  # evict the weights from L2 (256 MB > 126 MB L2)
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        fn()
+        b.record(s)
+        torch.cuda.synchronize()
+        if i >= 3:
+            ts.append(a.elapsed_time(b) * 1e-3)
+    ts.sort()
+    return ts[len(ts) // 2], ts[0]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--only", default="")
+    args = ap.parse_args()
+    dev = torch.device("cuda", 0)
+    flush = torch.zeros(64 << 20, dtype=torch.float32, device=dev)
+    pk = peaks()
+    out = {}
+    bf = torch.bfloat16
+    if args.only in ("", "gemv"):
+        blob = torch.empty(3 * F * d, dtype=bf, device=dev)
+        odmoe.gen_weights(blob, 0, layer=0, expert=0, d=d, F=F, seed=2512)
+        w13, w2 = blob[: 2 * F * d], blob[2 * F * d:].view(d, F)
+        u = (torch.rand(d, device=dev) - 0.5).to(bf)
+        a = torch.empty(F, device=dev)
+        y = torch.empty(d, device=dev)
+        gw = torch.ones(2, device=dev)
+        med, best = timeit(lambda: odmoe.expert_ffn(w13, w2, u, a, y, gate_w=gw), args.iters, flush)
+        nbytes = 3 * F * d * 2
+        out["expert_ffn_bf16"] = dict(us_median=med * 1e6, us_best=best * 1e6, GBps=nbytes / med / 1e9,
+                                      frac_hbm=nbytes / med / 1e9 / pk["hbm_gbs"], bytes=nbytes)
+        # int8 shadow expert
+        q = torch.empty((3 * F * d,), dtype=torch.int8, device=dev)
+        sc = torch.empty(2 * F + d, device=dev)
+        odmoe.quantize_int8_rows(w13.view(2 * F, d), q[: 2 * F * d].view(2 * F, d), sc[: 2 * F])
+        odmoe.quantize_int8_rows(w2, q[2 * F * d:].view(d, F), sc[2 * F:])
+        med, best = timeit(lambda: odmoe.shadow_expert_ffn(q[: 2 * F * d], sc[: 2 * F], q[2 * F * d:].view(d, F),
+                                                           sc[2 * F:], u, a, y, gate_w=gw), args.iters, flush)
+        nb = 3 * F * d + (2 * F + d) * 4
+        out["expert_ffn_int8"] = dict(us_median=med * 1e6, us_best=best * 1e6, GBps=nb / med / 1e9,
+                                      frac_hbm=nb / med / 1e9 / pk["hbm_gbs"], bytes=nb)
+        del blob, q
+    if args.only in ("", "lm"):
+        W = torch.empty((V, d), dtype=bf, device=dev)
+        odmoe.gen_weights(W, 6, rows=V, cols=d, fan_in=d, seed=2512)
+        h = torch.randn(d, device=dev)
+        tok = torch.empty(1, dtype=torch.int32, device=dev)
+        scratch = torch.zeros(16 * 4096, dtype=torch.uint8, device=dev)
+        med, best = timeit(lambda: odmoe.lm_head_argmax(h, W, tok, scratch), args.iters, flush)
+        nb = V * d * 2
+        out["lm_head_argmax"] = dict(us_median=med * 1e6, us_best=best * 1e6, GBps=nb / med / 1e9,
+                                     frac_hbm=nb / med / 1e9 / pk["hbm_gbs"], bytes=nb)
+        del W
+    if args.only in ("", "router"):
+        Wg = torch.empty((E, d), dtype=bf, device=dev)
+        odmoe.gen_weights(Wg, 2, rows=E, cols=d, fan_in=d, seed=2512)
+        h = torch.randn(1, d, device=dev)
+        y0 = torch.randn(1, d, device=dev) * 0.1
+        y1 = torch.randn(1, d, device=dev) * 0.1
+        uo = torch.empty(1, d, dtype=bf, device=dev)
+        ids = torch.empty(1, 2, dtype=torch.int32, device=dev)
+        w = torch.empty(1, 2, device=dev)
+        med, best = timeit(lambda: odmoe.route_topk(h, Wg, 2, uo, ids, w, y_add=[y0, y1]), args.iters, flush)
+        out["router_topk"] = dict(us_median=med * 1e6, us_best=best * 1e6)
+    if args.only in ("", "grouped"):
+        import numpy as np
+        rng = np.random.default_rng(3)
+        ids = np.stack([rng.choice(E, size=2, replace=False) for _ in range(512)])
+        counts = np.bincount(ids.reshape(-1), minlength=E)
+        off = [0] + list(np.cumsum(counts))
+        M = off[-1]
+        blobs = []
+        for e in range(E):
+            b = torch.empty(3 * F * d, dtype=bf, device=dev)
+            odmoe.gen_weights(b, 0, layer=0, expert=e, d=d, F=F, seed=2512)
+            blobs.append(b)
+        w13s = [b[: 2 * F * d] for b in blobs]
+        w2s = [b[2 * F * d:].view(d, F) for b in blobs]
+        x = (torch.rand(M, d, device=dev) - 0.5).to(bf)
+        gate = torch.rand(M, device=dev)
+        a2 = torch.empty(M, F, dtype=bf, device=dev)
+        y = torch.empty(M, d, device=dev)
+        tiles = torch.empty(16 * ((M // 128 + E + 1) * (2 * F // 256 + d // 128)), dtype=torch.uint8, device=dev)
+        med, best = timeit(lambda: odmoe.expert_ffn_grouped(w13s, w2s, x, off, gate, a2, y, tiles), max(5, args.iters // 4), flush)
+        flops = 2.0 * M * 3 * d * F
+        nb = E * 3 * F * d * 2
+        out["grouped_ffn_T512"] = dict(ms_median=med * 1e3, TFLOPs=flops / med / 1e12, GBps=nb / med / 1e9,
+                                       frac_tensor=flops / med / 1e12 / pk["bf16_tflops"],
+                                       frac_hbm=nb / med / 1e9 / pk["hbm_gbs"], rows=M,
+                                       note="includes the host tile-list build + a stream sync")
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()
