@@ -79,15 +79,27 @@ def _base(seed: int, tid: int) -> int:
     return splitmix64(splitmix64(seed) ^ tid)
 
 
-def stream_u24(seed: int, tid: int, n: int, start: int = 0, block: int = 1 << 24) -> np.ndarray:
-    """u24 = splitmix64(base + i) >> 40 for i in [start, start+n), as uint32."""
+def _u24_block(base, start, s, e, out):
+    with np.errstate(over="ignore"):
+        idx = np.arange(start + s, start + e, dtype=np.uint64) + base
+    out[s:e] = (splitmix64(idx) >> np.uint64(40)).astype(np.uint32)
+
+
+def stream_u24(seed: int, tid: int, n: int, start: int = 0, block: int = 1 << 22) -> np.ndarray:
+    """u24 = splitmix64(base + i) >> 40 for i in [start, start+n), as uint32. Large tensors are
+    generated block-parallel on a thread pool (numpy releases the GIL); the values do not depend
+    on the blocking."""
     base = np.uint64(_base(seed, tid))
     out = np.empty(n, dtype=np.uint32)
-    for s in range(0, n, block):
-        e = min(n, s + block)
-        with np.errstate(over="ignore"):
-            idx = np.arange(start + s, start + e, dtype=np.uint64) + base
-        out[s:e] = (splitmix64(idx) >> np.uint64(40)).astype(np.uint32)
+    blocks = [(s, min(n, s + block)) for s in range(0, n, block)]
+    if len(blocks) <= 2:
+        for s, e in blocks:
+            _u24_block(base, start, s, e, out)
+        return out
+    import concurrent.futures
+    import os
+    with concurrent.futures.ThreadPoolExecutor(max_workers=min(32, os.cpu_count() or 1)) as ex:
+        list(ex.map(lambda se: _u24_block(base, start, se[0], se[1], out), blocks))
     return out
 
 
@@ -121,11 +133,35 @@ def weight_bf16_bits(seed: int, tid: int, rows: int, cols: int, fan_in: int) -> 
     return f32_to_bf16_bits(weight_fp32(seed, tid, rows, cols, fan_in))
 
 
-def _stored(seed, tid, rows, cols, fan_in, dtype):
-    w = weight_fp32(seed, tid, rows, cols, fan_in)
-    if dtype == "bf16":
-        return bf16_bits_to_f32(f32_to_bf16_bits(w)).reshape(rows, cols)
-    return w
+def _stored(seed, tid, rows, cols, fan_in, dtype, block: int = 1 << 22):
+    """Stored weight values (fp32, or bf16-rounded fp32). Same arithmetic as weight_fp32 +
+    f32_to_bf16_bits, evaluated block-parallel on a thread pool."""
+    n = rows * cols
+    base = np.uint64(_base(seed, tid))
+    scale = fan_in_scale(fan_in)
+    out = np.empty(n, dtype=np.float32)
+
+    def work(se):
+        s_, e_ = se
+        with np.errstate(over="ignore"):
+            idx = np.arange(s_, e_, dtype=np.uint64) + base
+        u = (splitmix64(idx) >> np.uint64(40)).astype(np.int64)
+        w = ((2 * u - ((1 << 24) - 1)).astype(np.float32) * np.float32(2.0 ** -24)).astype(np.float32) * scale
+        w = w.astype(np.float32)
+        if dtype == "bf16":
+            w = bf16_bits_to_f32(f32_to_bf16_bits(w))
+        out[s_:e_] = w
+
+    blocks = [(s_, min(n, s_ + block)) for s_ in range(0, n, block)]
+    if len(blocks) <= 2:
+        for b in blocks:
+            work(b)
+    else:
+        import concurrent.futures
+        import os
+        with concurrent.futures.ThreadPoolExecutor(max_workers=min(32, os.cpu_count() or 1)) as ex:
+            list(ex.map(work, blocks))
+    return out.reshape(rows, cols)
 
 
 def gen_expert(shape: ModelShape, seed: int, layer: int, expert: int, dtype: str = "bf16"):

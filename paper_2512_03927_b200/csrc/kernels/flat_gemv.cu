@@ -1,0 +1,354 @@
+// Flat-stream GEMV (expert W13+SwiGLU, W2+gate, INT8 shadow, LM head + argmax): the third and
+// fastest design measured on B200 (profiles/kbench_r01_*.json). Each CTA (one per SM, 16 warps)
+// owns a contiguous, balanced row range; that range is ONE byte stream which is cut into 16
+// contiguous per-warp slices of 512-byte groups. A warp issues UNROLL groups (one 16-byte
+// ld.global.nc.L1::no_allocate per lane each) before consuming any, so every SM keeps
+// 16 x UNROLL x 512 B = 128 KB in flight, and walks its slice with a running (row, column)
+// position: rows are whole groups, so a row boundary is detected with one compare and the row's
+// partial is flushed with a warp shuffle only then. Per-warp row partials are reduced in a
+// fixed warp order at the end (deterministic, no atomics).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace odmoe {
+
+constexpr int kFG_WARPS = 16;
+constexpr int kFG_THREADS = kFG_WARPS * 32;
+
+template <typename WT, typename XT> struct FDot;
+template <> struct FDot<__nv_bfloat16, float> {
+  static constexpr int kN = 8;
+  __device__ __forceinline__ static float run(const uint4& w, const float* x) { return dot16<__nv_bfloat16>(w, x); }
+};
+template <> struct FDot<float, float> {
+  static constexpr int kN = 4;
+  __device__ __forceinline__ static float run(const uint4& w, const float* x) { return dot16<float>(w, x); }
+};
+template <> struct FDot<int8_t, float> {
+  static constexpr int kN = 16;
+  __device__ __forceinline__ static float run(const uint4& w, const float* x) { return dot16<int8_t>(w, x); }
+};
+__device__ __forceinline__ float fbf2(uint32_t w, uint32_t x, float s) {
+  s = fmaf(bf16_lo(w), bf16_lo(x), s);
+  return fmaf(bf16_hi(w), bf16_hi(x), s);
+}
+template <> struct FDot<__nv_bfloat16, uint16_t> {
+  static constexpr int kN = 8;
+  __device__ __forceinline__ static float run(const uint4& w, const uint16_t* x) {
+    const uint4 xv = *reinterpret_cast<const uint4*>(x);
+    // two independent chains (even/odd words) for ILP
+    float s0 = bf16_lo(w.x) * bf16_lo(xv.x);
+    float s1 = bf16_lo(w.y) * bf16_lo(xv.y);
+    s0 = fmaf(bf16_hi(w.x), bf16_hi(xv.x), s0);
+    s1 = fmaf(bf16_hi(w.y), bf16_hi(xv.y), s1);
+    s0 = fbf2(w.z, xv.z, s0);
+    s1 = fbf2(w.w, xv.w, s1);
+    return s0 + s1;
+  }
+};
+__device__ __forceinline__ float fi8(uint32_t word, uint32_t x01, uint32_t x23, float s) {
+  const uint32_t b = word ^ 0x80808080u;
+  s = fmaf(i8_to_f32(b, 0), bf16_lo(x01), s);
+  s = fmaf(i8_to_f32(b, 1), bf16_hi(x01), s);
+  s = fmaf(i8_to_f32(b, 2), bf16_lo(x23), s);
+  return fmaf(i8_to_f32(b, 3), bf16_hi(x23), s);
+}
+template <> struct FDot<int8_t, uint16_t> {
+  static constexpr int kN = 16;
+  __device__ __forceinline__ static float run(const uint4& w, const uint16_t* x) {
+    const uint4 x0 = *reinterpret_cast<const uint4*>(x);
+    const uint4 x1 = *reinterpret_cast<const uint4*>(x + 8);
+    float s0 = fi8(w.x, x0.x, x0.y, 0.f);
+    float s1 = fi8(w.y, x0.z, x0.w, 0.f);
+    s0 = fi8(w.z, x1.x, x1.y, s0);
+    s1 = fi8(w.w, x1.z, x1.w, s1);
+    return s0 + s1;
+  }
+};
+
+__device__ __forceinline__ unsigned long long fg_argmax_key(float v, int id) {
+  uint32_t b = __float_as_uint(v);
+  b = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+  return ((unsigned long long)b << 32) | (unsigned long long)(~(uint32_t)id);
+}
+
+struct FlatArgs {
+  ExpertRef ex;
+  int second;
+  const void* x;
+  int x_bf16;
+  int R, C;
+  const float* gate_w;
+  float* out;
+  const float* h;
+  float eps;
+  unsigned long long* partial;
+  unsigned int* ticket;
+  int32_t* token_out;
+  int rows_cap;
+  int d_full, F_full;
+};
+
+template <typename WT, typename XT, int MODE, int UNROLL>
+__global__ void __launch_bounds__(kFG_THREADS, 1) flat_gemv_kernel(const FlatArgs a) {
+  constexpr int N = FDot<WT, XT>::kN;
+  extern __shared__ __align__(128) uint8_t sm[];
+  float* part = reinterpret_cast<float*>(sm);                          // [warps][rows_cap]
+  XT* xs = reinterpret_cast<XT*>(part + kFG_WARPS * a.rows_cap);       // [C]
+  __shared__ float red[kFG_WARPS + 1];
+  __shared__ unsigned long long kbest[kFG_WARPS];
+  __shared__ bool is_last;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+
+  // Indirect experts are chosen by the PREVIOUS kernel's router output: wait for it (PDL) before
+  // reading the ids. Direct weights do not depend on it and are prefetched first (below).
+  const bool indirect = a.ex.tbl != nullptr;
+  if (indirect) asm volatile("griddepcontrol.wait;" ::: "memory");
+  const WT* W;
+  const float* sc;
+  int gate_idx;
+  {
+    const ExpertRef& ex = a.ex;
+    gate_idx = ex.sel;
+    if (ex.tbl == nullptr) {
+      W = reinterpret_cast<const WT*>(ex.blob);
+      sc = ex.scales;
+    } else {
+      if (ex.sorted) {
+        for (int j = 0; j < ex.k; ++j) {
+          int rank = 0;
+          for (int i = 0; i < ex.k; ++i) rank += ex.ids[i] < ex.ids[j];
+          if (rank == ex.sel) gate_idx = j;
+        }
+      }
+      const int id = ex.base + ex.ids[gate_idx];
+      W = reinterpret_cast<const WT*>(ex.tbl[id]) + (a.second ? 2LL * a.F_full * a.d_full : 0LL);
+      sc = ex.stbl ? ex.stbl[id] + (a.second ? 2 * a.F_full : 0) : nullptr;
+    }
+  }
+  long long rb, re;
+  if (MODE == 0) {
+    split_range(a.R / 2, gridDim.x, blockIdx.x, rb, re);
+    rb *= 2; re *= 2;
+  } else {
+    split_range(a.R, gridDim.x, blockIdx.x, rb, re);
+  }
+  const int nrows = (int)(re - rb);
+  const int Cg = a.C / N;                 // 16-byte granules per row (multiple of 32)
+  const int Gr = Cg / 32;                 // 512-byte groups per row
+  const long long G = (long long)nrows * Gr;
+  // this warp's slice of groups
+  const long long g_begin = G * warp / kFG_WARPS, g_end = G * (warp + 1) / kFG_WARPS;
+  const uint4* base = reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(W) + rb * (long long)a.C * sizeof(WT));
+
+  // The weights do not depend on the previous kernel: issue this warp's first batch before the
+  // programmatic-dependent-launch wait (no-op without PDL), then stage the activations.
+  uint4 wa[UNROLL], wb[UNROLL];
+#pragma unroll
+  for (int i = 0; i < UNROLL; ++i)
+    if (g_begin + i < g_end) wa[i] = ld_stream(base + (g_begin + i) * 32 + lane);
+  if (!indirect) asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+
+  // stage activations (MODE 2: RMSNorm of h first) and zero the partials
+  if (MODE == 2) {
+    float ss = 0.f;
+    for (int j = tid; j < a.C; j += kFG_THREADS) { const float v = a.h[j]; ss = fmaf(v, v, ss); }
+    ss = warp_sum(ss);
+    if (lane == 0) red[warp] = ss;
+    __syncthreads();
+    if (tid == 0) {
+      float t = 0.f;
+      for (int w = 0; w < kFG_WARPS; ++w) t += red[w];
+      red[kFG_WARPS] = t;
+    }
+    __syncthreads();
+    const float rstd = 1.0f / sqrtf(red[kFG_WARPS] / (float)a.C + a.eps);
+    for (int j = tid; j < a.C; j += kFG_THREADS) {
+      const float v = a.h[j] * rstd;
+      if constexpr (std::is_same<XT, uint16_t>::value) {
+        const __nv_bfloat16 b = __float2bfloat16_rn(v);
+        xs[j] = *reinterpret_cast<const uint16_t*>(&b);
+      } else {
+        xs[j] = v;
+      }
+    }
+  } else if constexpr (std::is_same<XT, uint16_t>::value) {
+    const uint4* s4 = reinterpret_cast<const uint4*>(a.x);
+    for (int i = tid; i < a.C / 8; i += kFG_THREADS) reinterpret_cast<uint4*>(xs)[i] = s4[i];
+  } else {
+    if (a.x_bf16) {
+      const uint16_t* s16 = reinterpret_cast<const uint16_t*>(a.x);
+      for (int i = tid; i < a.C; i += kFG_THREADS) xs[i] = __uint_as_float((uint32_t)s16[i] << 16);
+    } else {
+      const float4* s4 = reinterpret_cast<const float4*>(a.x);
+      for (int i = tid; i < a.C / 4; i += kFG_THREADS) reinterpret_cast<float4*>(xs)[i] = s4[i];
+    }
+  }
+  for (int i = tid; i < kFG_WARPS * a.rows_cap; i += kFG_THREADS) part[i] = 0.f;
+  __syncthreads();
+
+  int row = (int)(g_begin / Gr);
+  int gcol = (int)(g_begin - (long long)row * Gr);   // group index within the row
+  float acc = 0.f;
+  // consume one register batch (rows are whole groups: a boundary is one compare)
+  auto consume = [&](const uint4 (&wv)[UNROLL], long long g0) {
+#pragma unroll
+    for (int i = 0; i < UNROLL; ++i) {
+      if (g0 + i < g_end) {
+        acc += FDot<WT, XT>::run(wv[i], xs + (size_t)(gcol * 32 + lane) * N);
+        if (++gcol == Gr) {  // row complete (warp-uniform)
+          const float t = warp_sum(acc);
+          if (lane == 0) part[warp * a.rows_cap + row] += t;
+          acc = 0.f;
+          gcol = 0;
+          ++row;
+        }
+      }
+    }
+  };
+  // software pipeline, two register batches in flight: load batch n+1, then consume batch n
+  for (long long g0 = g_begin; g0 < g_end; g0 += 2 * UNROLL) {
+    const long long g1 = g0 + UNROLL, g2 = g0 + 2 * UNROLL;
+#pragma unroll
+    for (int i = 0; i < UNROLL; ++i)
+      if (g1 + i < g_end) wb[i] = ld_stream(base + (g1 + i) * 32 + lane);
+    consume(wa, g0);
+#pragma unroll
+    for (int i = 0; i < UNROLL; ++i)
+      if (g2 + i < g_end) wa[i] = ld_stream(base + (g2 + i) * 32 + lane);
+    if (g1 < g_end) consume(wb, g1);
+  }
+  if (gcol != 0) {  // slice ended inside a row
+    const float t = warp_sum(acc);
+    if (lane == 0) part[warp * a.rows_cap + row] += t;
+  }
+  __syncthreads();
+
+  if (MODE == 0) {
+    for (int p = tid; p < nrows / 2; p += kFG_THREADS) {
+      float g = 0.f, v = 0.f;
+#pragma unroll
+      for (int w = 0; w < kFG_WARPS; ++w) {
+        g += part[w * a.rows_cap + 2 * p];
+        v += part[w * a.rows_cap + 2 * p + 1];
+      }
+      if (sc != nullptr) { g *= sc[rb + 2 * p]; v *= sc[rb + 2 * p + 1]; }
+      a.out[rb / 2 + p] = silu_mul(g, v);
+    }
+  } else if (MODE == 1) {
+    const float gw = a.gate_w ? a.gate_w[gate_idx] : 1.f;
+    for (int r = tid; r < nrows; r += kFG_THREADS) {
+      float s = 0.f;
+#pragma unroll
+      for (int w = 0; w < kFG_WARPS; ++w) s += part[w * a.rows_cap + r];
+      if (sc != nullptr) s *= sc[rb + r];
+      a.out[rb + r] = gw * s;
+    }
+  } else {
+    unsigned long long best = 0ull;
+    for (int r = tid; r < nrows; r += kFG_THREADS) {
+      float s = 0.f;
+#pragma unroll
+      for (int w = 0; w < kFG_WARPS; ++w) s += part[w * a.rows_cap + r];
+      if (a.out) a.out[rb + r] = s;
+      const unsigned long long key = fg_argmax_key(s, (int)(rb + r));
+      best = key > best ? key : best;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long other = __shfl_xor_sync(0xffffffffu, best, o);
+      best = other > best ? other : best;
+    }
+    if (lane == 0) kbest[warp] = best;
+    __syncthreads();
+    if (tid == 0) {
+      unsigned long long b = kbest[0];
+      for (int w = 1; w < kFG_WARPS; ++w) b = kbest[w] > b ? kbest[w] : b;
+      a.partial[blockIdx.x] = b;
+      __threadfence();
+      const unsigned int t = atomicAdd(a.ticket, 1u);
+      is_last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (is_last && tid == 0) {
+      __threadfence();
+      unsigned long long b = 0ull;
+      for (unsigned int i = 0; i < gridDim.x; ++i) {
+        const unsigned long long p = *((volatile unsigned long long*)a.partial + i);
+        b = p > b ? p : b;
+      }
+      *a.token_out = (int32_t)(~(uint32_t)(b & 0xffffffffull));
+      *a.ticket = 0u;
+    }
+  }
+}
+
+template <typename WT, typename XT, int MODE>
+static cudaError_t fg_launch(FlatArgs a, cudaStream_t s, bool pdl) {
+  constexpr int UNROLL = 8;
+  const int sms = num_sms();
+  const long long units = MODE == 0 ? a.R / 2 : a.R;
+  const int grid = (int)(units < sms ? (units > 0 ? units : 1) : sms);
+  a.rows_cap = (int)((units + grid - 1) / grid) * (MODE == 0 ? 2 : 1) + 2;
+  const size_t smem = (size_t)kFG_WARPS * a.rows_cap * sizeof(float) + (size_t)a.C * sizeof(XT) + 16;
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  auto kern = flat_gemv_kernel<WT, XT, MODE, UNROLL>;
+  if (smem > 40 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kFG_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
+cudaError_t launch_w13_flat(ExpertRef ex, WType wt, const void* u, int u_f32, float* a_out, int d, int F,
+                            cudaStream_t s, bool pdl) {
+  FlatArgs a{};
+  a.ex = ex; a.second = 0; a.x = u; a.x_bf16 = !u_f32; a.R = 2 * F; a.C = d; a.out = a_out;
+  a.d_full = d; a.F_full = F;
+  switch (wt) {
+    case W_BF16: return fg_launch<__nv_bfloat16, uint16_t, 0>(a, s, pdl);
+    case W_F32: return fg_launch<float, float, 0>(a, s, pdl);
+    case W_I8: return fg_launch<int8_t, uint16_t, 0>(a, s, pdl);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_w2_flat(ExpertRef ex, WType wt, const float* act, const float* gate_w, float* y, int d,
+                           int F, cudaStream_t s, bool pdl) {
+  FlatArgs a{};
+  a.ex = ex; a.second = 1; a.x = act; a.x_bf16 = 0; a.R = d; a.C = F; a.gate_w = gate_w; a.out = y;
+  a.d_full = d; a.F_full = F;
+  switch (wt) {
+    case W_BF16: return fg_launch<__nv_bfloat16, float, 1>(a, s, pdl);
+    case W_F32: return fg_launch<float, float, 1>(a, s, pdl);
+    case W_I8: return fg_launch<int8_t, float, 1>(a, s, pdl);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_lm_head_flat(const float* h, const void* W, WType wt, int V, int d, float eps,
+                                int32_t* token_out, float* logits, void* scratch, cudaStream_t s, bool pdl) {
+  FlatArgs a{};
+  a.ex = direct_ref(W, nullptr, 0); a.second = 0; a.R = V; a.C = d; a.out = logits; a.h = h; a.eps = eps;
+  a.partial = reinterpret_cast<unsigned long long*>(scratch);
+  a.ticket = reinterpret_cast<unsigned int*>(a.partial + 1024);
+  a.token_out = token_out;
+  switch (wt) {
+    case W_BF16: return fg_launch<__nv_bfloat16, uint16_t, 2>(a, s, pdl);
+    case W_F32: return fg_launch<float, float, 2>(a, s, pdl);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace odmoe

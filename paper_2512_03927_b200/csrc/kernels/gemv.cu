@@ -14,6 +14,8 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <cstdlib>
+
 namespace odmoe {
 
 constexpr int kGemvWarps = 8;
@@ -177,8 +179,22 @@ static cudaError_t w2_impl(const ExpertRef& ex, const float* a, const float* gat
   return cudaGetLastError();
 }
 
+// GEMV engine selection: flat (default) | tma | ldg (ODMOE_GEMV env var, for A/B measurements).
+int gemv_engine() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ODMOE_GEMV");
+    v = (e && e[0] == 'l') ? 0 : ((e && e[0] == 't') ? 1 : 2);
+  }
+  return v;
+}
+
 cudaError_t launch_w13(ExpertRef ex, WType wt, const void* u, int u_f32, float* a, int d, int F,
-                       cudaStream_t s) {
+                       cudaStream_t s, bool pdl) {
+  if (stream_ok(wt, d)) {
+    if (gemv_engine() == 2) return launch_w13_flat(ex, wt, u, u_f32, a, d, F, s, pdl);
+    if (gemv_engine() == 1) return launch_w13_stream(ex, wt, u, u_f32, a, d, F, s);
+  }
   switch (wt) {
     case W_BF16: return w13_impl<__nv_bfloat16>(ex, u, u_f32, a, d, F, s);
     case W_F32: return w13_impl<float>(ex, u, u_f32, a, d, F, s);
@@ -188,7 +204,11 @@ cudaError_t launch_w13(ExpertRef ex, WType wt, const void* u, int u_f32, float* 
 }
 
 cudaError_t launch_w2(ExpertRef ex, WType wt, const float* a, const float* gate_w, float* y, int d,
-                      int F, cudaStream_t s) {
+                      int F, cudaStream_t s, bool pdl) {
+  if (stream_ok(wt, F)) {
+    if (gemv_engine() == 2) return launch_w2_flat(ex, wt, a, gate_w, y, d, F, s, pdl);
+    if (gemv_engine() == 1) return launch_w2_stream(ex, wt, a, gate_w, y, d, F, s);
+  }
   switch (wt) {
     case W_BF16: return w2_impl<__nv_bfloat16>(ex, a, gate_w, y, d, F, s);
     case W_F32: return w2_impl<float>(ex, a, gate_w, y, d, F, s);

@@ -14,7 +14,7 @@ int num_sms();  // cached SM count of the current device
 cudaError_t launch_router(float* h, const float* const* y_add, int n_add, const void* gamma,
                           const void* w_gate, const float* wg_scale, WType wt, int m, int E, int d,
                           int k, float eps, void* u_out, int32_t* ids, float* w, float* logits,
-                          int32_t* flag, cudaStream_t s);
+                          int32_t* flag, cudaStream_t s, bool pdl = false);
 
 // h += (y_0 + ... + y_{n-1}) (final residual combine before the LM head).
 cudaError_t launch_combine(float* h, const float* const* y_add, int n_add, int d, cudaStream_t s);
@@ -37,15 +37,36 @@ inline ExpertRef direct_ref(const void* blob, const float* scales, int gate_idx)
 }
 
 // a8 phase 1: a[f] = silu(g_f) * v_f with [g_f; v_f] = W13[2f:2f+2] u (int8: row scales).
+// pdl: launch with programmatic stream serialization (only when the previous operation on the
+// stream is a kernel of this library; the weights are prefetched before the dependency wait).
 cudaError_t launch_w13(ExpertRef ex, WType wt, const void* u, int u_f32, float* a, int d, int F,
-                       cudaStream_t s);
+                       cudaStream_t s, bool pdl = false);
 // a8 phase 2: y = gate_w[pick] * (W2 a) (int8: row scales); gate_w may be NULL (=1).
 cudaError_t launch_w2(ExpertRef ex, WType wt, const float* a, const float* gate_w, float* y, int d,
-                      int F, cudaStream_t s);
+                      int F, cudaStream_t s, bool pdl = false);
+
+// GEMV engines: 2 = flat per-warp streams (flat_gemv.cu, default), 1 = TMA bulk ring
+// (stream_gemv.cu), 0 = per-row register streaming (gemv.cu); env ODMOE_GEMV=flat|tma|ldg.
+int gemv_engine();
+cudaError_t launch_w13_flat(ExpertRef ex, WType wt, const void* u, int u_f32, float* a, int d, int F,
+                            cudaStream_t s, bool pdl);
+cudaError_t launch_w2_flat(ExpertRef ex, WType wt, const float* act, const float* gate_w, float* y, int d,
+                           int F, cudaStream_t s, bool pdl);
+cudaError_t launch_lm_head_flat(const float* h, const void* W, WType wt, int V, int d, float eps,
+                                int32_t* token_out, float* logits, void* scratch, cudaStream_t s, bool pdl);
+// TMA-bulk streaming variants (stream_gemv.cu), used when stream_ok(wt, row length).
+bool stream_ok(WType wt, int C);
+cudaError_t launch_w13_stream(ExpertRef ex, WType wt, const void* u, int u_f32, float* a, int d, int F,
+                              cudaStream_t s);
+cudaError_t launch_w2_stream(ExpertRef ex, WType wt, const float* act, const float* gate_w, float* y, int d,
+                             int F, cudaStream_t s);
+cudaError_t launch_lm_head_stream(const float* h, const void* W, WType wt, int V, int d, float eps,
+                                  int32_t* token_out, float* logits, void* scratch, cudaStream_t s);
 
 // a10: token = argmax_v (W_o RMSNorm(h))_v, lowest id on ties. scratch >= 8*(grid+2) bytes.
 cudaError_t launch_lm_head(const float* h, const void* W, WType wt, int V, int d, float eps,
-                           int32_t* token_out, float* logits, void* scratch, cudaStream_t s);
+                           int32_t* token_out, float* logits, void* scratch, cudaStream_t s,
+                           bool pdl = false);
 
 // a1: h = Emb[token] (fp32); int8 rows use emb_scale.
 cudaError_t launch_embed(const void* emb, const float* emb_scale, WType wt, const int32_t* token,

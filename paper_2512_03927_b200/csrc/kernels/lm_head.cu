@@ -7,6 +7,8 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <cstdlib>
+
 namespace odmoe {
 
 constexpr int kLmWarps = 8;
@@ -120,7 +122,11 @@ static cudaError_t lm_impl(const float* h, const void* W, int V, int d, float ep
 }
 
 cudaError_t launch_lm_head(const float* h, const void* W, WType wt, int V, int d, float eps,
-                           int32_t* token_out, float* logits, void* scratch, cudaStream_t s) {
+                           int32_t* token_out, float* logits, void* scratch, cudaStream_t s, bool pdl) {
+  if (stream_ok(wt, d)) {
+    if (gemv_engine() == 2) return launch_lm_head_flat(h, W, wt, V, d, eps, token_out, logits, scratch, s, pdl);
+    if (gemv_engine() == 1) return launch_lm_head_stream(h, W, wt, V, d, eps, token_out, logits, scratch, s);
+  }
   switch (wt) {
     case W_BF16: return lm_impl<__nv_bfloat16>(h, W, V, d, eps, token_out, logits, scratch, s);
     case W_F32: return lm_impl<float>(h, W, V, d, eps, token_out, logits, scratch, s);

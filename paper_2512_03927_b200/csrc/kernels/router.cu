@@ -12,36 +12,89 @@ namespace odmoe {
 constexpr int kRouterThreads = 256;
 constexpr int kRouterWarps = kRouterThreads / 32;
 
+constexpr int kRouterPrefetchMax = 128 * 1024;  // W_g bytes staged in smem by one bulk copy
+
+__device__ __forceinline__ uint32_t r_smem(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+// Launch latency hiding (programmatic dependent launch): everything before pdl_wait() may run
+// while the previous kernel on the stream is still finishing; pdl_trigger() lets the next kernel
+// be scheduled early. Both are no-ops for launches without the PDL attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 template <typename WT>
 __global__ void __launch_bounds__(kRouterThreads) router_kernel(
     float* __restrict__ h, const float* const* __restrict__ y_add, int n_add,
     const WT* __restrict__ gamma, const WT* __restrict__ wg, const float* __restrict__ wg_scale,
     int E, int d, int k, float eps, void* __restrict__ u_out, int32_t* __restrict__ ids,
-    float* __restrict__ w, float* __restrict__ logits, int32_t* __restrict__ flag) {
-  extern __shared__ __align__(16) float us[];  // d floats: the rounded normalised input
+    float* __restrict__ w, float* __restrict__ logits, int32_t* __restrict__ flag, int prefetch) {
+  extern __shared__ __align__(128) uint8_t rsm[];
+  float* us = reinterpret_cast<float*>(rsm);                      // d floats: rounded normalised input
+  uint8_t* wsm = rsm + (((size_t)d * sizeof(float) + 127) & ~(size_t)127);  // W_g copy (prefetch)
+  __shared__ uint64_t wbar;
   __shared__ float red[kRouterWarps];
   __shared__ float lg[kMaxE];
   const int row = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   float* hr = h + (size_t)row * d;
+  const uint32_t wbytes = (uint32_t)((size_t)E * d * sizeof(WT));
+
+  // W_g does not depend on the previous kernel: start its bulk copy before the dependency wait.
+  if (prefetch) {
+    if (tid == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(r_smem(&wbar)));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(r_smem(&wbar)), "r"(wbytes) : "memory");
+      for (uint32_t off = 0; off < wbytes; off += 32768) {
+        const uint32_t n = wbytes - off < 32768 ? wbytes - off : 32768;
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         r_smem(wsm + off)),
+                     "l"(reinterpret_cast<const char*>(wg) + off), "r"(n), "r"(r_smem(&wbar))
+                     : "memory");
+      }
+    }
+  }
+  pdl_wait();
+  pdl_trigger();
 
   // Pass 1: h = h + (y_0 + y_1 + ...), partials summed first in the given order so that a
-  // pre-reduced sum (NCCL reduce at N > 1) gives the same bits as the 1-GPU combine.
+  // pre-reduced sum (NCCL reduce at N > 1) gives the same bits as the 1-GPU combine. All loads of
+  // a thread are issued before any is used.
+  constexpr int kV = 4;  // float4 per thread per batch (covers d = 4096 in one batch)
   float ss = 0.f;
-  for (int j = tid * 4; j < d; j += kRouterThreads * 4) {
-    float4 hv = *reinterpret_cast<const float4*>(hr + j);
-    if (n_add > 0) {
-      float4 s = *reinterpret_cast<const float4*>(y_add[0] + (size_t)row * d + j);
-      for (int a = 1; a < n_add; ++a) {
-        const float4 t = *reinterpret_cast<const float4*>(y_add[a] + (size_t)row * d + j);
-        s.x += t.x; s.y += t.y; s.z += t.z; s.w += t.w;
+  for (int j0 = tid * 4; j0 < d; j0 += kRouterThreads * 4 * kV) {
+    float4 hv[kV], s[kV];
+#pragma unroll
+    for (int i = 0; i < kV; ++i) {
+      const int j = j0 + i * kRouterThreads * 4;
+      if (j < d) {
+        hv[i] = *reinterpret_cast<const float4*>(hr + j);
+        if (n_add > 0) s[i] = *reinterpret_cast<const float4*>(y_add[0] + (size_t)row * d + j);
       }
-      hv.x += s.x; hv.y += s.y; hv.z += s.z; hv.w += s.w;
-      *reinterpret_cast<float4*>(hr + j) = hv;
     }
-    *reinterpret_cast<float4*>(us + j) = hv;
-    ss = fmaf(hv.x, hv.x, ss); ss = fmaf(hv.y, hv.y, ss);
-    ss = fmaf(hv.z, hv.z, ss); ss = fmaf(hv.w, hv.w, ss);
+    for (int a = 1; a < n_add; ++a) {
+#pragma unroll
+      for (int i = 0; i < kV; ++i) {
+        const int j = j0 + i * kRouterThreads * 4;
+        if (j < d) {
+          const float4 t = *reinterpret_cast<const float4*>(y_add[a] + (size_t)row * d + j);
+          s[i].x += t.x; s[i].y += t.y; s[i].z += t.z; s[i].w += t.w;
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < kV; ++i) {
+      const int j = j0 + i * kRouterThreads * 4;
+      if (j < d) {
+        if (n_add > 0) {
+          hv[i].x += s[i].x; hv[i].y += s[i].y; hv[i].z += s[i].z; hv[i].w += s[i].w;
+          *reinterpret_cast<float4*>(hr + j) = hv[i];
+        }
+        *reinterpret_cast<float4*>(us + j) = hv[i];
+        ss = fmaf(hv[i].x, hv[i].x, ss); ss = fmaf(hv[i].y, hv[i].y, ss);
+        ss = fmaf(hv[i].z, hv[i].z, ss); ss = fmaf(hv[i].w, hv[i].w, ss);
+      }
+    }
   }
   ss = warp_sum(ss);
   if (lane == 0) red[warp] = ss;
@@ -74,14 +127,26 @@ __global__ void __launch_bounds__(kRouterThreads) router_kernel(
   }
   __syncthreads();
 
-  // Router GEMV: warp per expert row, 16-byte chunks, shuffle reduction.
+  // Router GEMV: warp per expert row, 16-byte chunks from smem (prefetched) or global, shuffle sum.
   constexpr int N = WTraits<WT>::kPer16B;
   const int C = d / N;
+  if (prefetch) {
+    asm volatile(
+        "{\n .reg .pred p;\n RW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra RW_%=;\n}\n" ::"r"(
+            r_smem(&wbar))
+        : "memory");
+  }
+  const uint4* wbase = prefetch ? reinterpret_cast<const uint4*>(wsm) : reinterpret_cast<const uint4*>(wg);
   for (int e = warp; e < E; e += kRouterWarps) {
-    const uint4* wr = reinterpret_cast<const uint4*>(wg + (size_t)e * d);
-    float acc = 0.f;
-    for (int c = lane; c < C; c += 32) acc += dot16<WT>(wr[c], us + c * N);
-    acc = warp_sum(acc);
+    const uint4* wr = wbase + (size_t)e * C;
+    float acc0 = 0.f, acc1 = 0.f;
+    int c = lane;
+    for (; c + 32 < C; c += 64) {
+      acc0 += dot16<WT>(wr[c], us + c * N);
+      acc1 += dot16<WT>(wr[c + 32], us + (c + 32) * N);
+    }
+    if (c < C) acc0 += dot16<WT>(wr[c], us + c * N);
+    const float acc = warp_sum(acc0 + acc1);
     if (lane == 0) lg[e] = wg_scale ? acc * wg_scale[e] : acc;
   }
   __syncthreads();
@@ -135,36 +200,54 @@ cudaError_t launch_combine(float* h, const float* const* y_add, int n_add, int d
   return cudaGetLastError();
 }
 
+template <typename K, typename... Args>
+static cudaError_t launch_ex(K kern, dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+template <typename WT>
+static cudaError_t router_impl(float* h, const float* const* y_add, int n_add, const void* gamma,
+                               const void* w_gate, const float* wg_scale, int m, int E, int d, int k,
+                               float eps, void* u_out, int32_t* ids, float* w, float* logits, int32_t* flag,
+                               cudaStream_t s, bool pdl) {
+  const size_t wbytes = (size_t)E * d * sizeof(WT);
+  const int prefetch = (wbytes <= (size_t)kRouterPrefetchMax && wbytes % 16 == 0) ? 1 : 0;
+  const size_t smem = (((size_t)d * sizeof(float) + 127) & ~(size_t)127) + (prefetch ? wbytes : 0);
+  auto kern = router_kernel<WT>;
+  if (smem > 40 * 1024) {  // static smem (~0.4 KB) + dynamic must fit: opt in early
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  return launch_ex(kern, dim3(m), dim3(kRouterThreads), smem, s, pdl, h, y_add, n_add, (const WT*)gamma,
+                   (const WT*)w_gate, wg_scale, E, d, k, eps, u_out, ids, w, logits, flag, prefetch);
+}
+
 cudaError_t launch_router(float* h, const float* const* y_add, int n_add, const void* gamma,
                           const void* w_gate, const float* wg_scale, WType wt, int m, int E, int d,
                           int k, float eps, void* u_out, int32_t* ids, float* w, float* logits,
-                          int32_t* flag, cudaStream_t s) {
-  const size_t smem = (size_t)d * sizeof(float);
-  dim3 grid(m), block(kRouterThreads);
+                          int32_t* flag, cudaStream_t s, bool pdl) {
   switch (wt) {
     case W_BF16:
-      if (smem > 48 * 1024)
-        cudaFuncSetAttribute(router_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      router_kernel<__nv_bfloat16><<<grid, block, smem, s>>>(
-          h, y_add, n_add, (const __nv_bfloat16*)gamma, (const __nv_bfloat16*)w_gate, nullptr, E, d,
-          k, eps, u_out, ids, w, logits, flag);
-      break;
+      return router_impl<__nv_bfloat16>(h, y_add, n_add, gamma, w_gate, nullptr, m, E, d, k, eps, u_out, ids, w,
+                                        logits, flag, s, pdl);
     case W_F32:
-      if (smem > 48 * 1024)
-        cudaFuncSetAttribute(router_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      router_kernel<float><<<grid, block, smem, s>>>(h, y_add, n_add, (const float*)gamma,
-                                                     (const float*)w_gate, nullptr, E, d, k, eps,
-                                                     u_out, ids, w, logits, flag);
-      break;
+      return router_impl<float>(h, y_add, n_add, gamma, w_gate, nullptr, m, E, d, k, eps, u_out, ids, w, logits,
+                                flag, s, pdl);
     case W_I8:
-      if (smem > 48 * 1024)
-        cudaFuncSetAttribute(router_kernel<int8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      router_kernel<int8_t><<<grid, block, smem, s>>>(h, y_add, n_add, nullptr,
-                                                      (const int8_t*)w_gate, wg_scale, E, d, k, eps,
-                                                      u_out, ids, w, logits, flag);
-      break;
+      return router_impl<int8_t>(h, y_add, n_add, nullptr, w_gate, wg_scale, m, E, d, k, eps, u_out, ids, w,
+                                 logits, flag, s, pdl);
   }
-  return cudaGetLastError();
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace odmoe

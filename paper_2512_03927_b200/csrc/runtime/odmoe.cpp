@@ -426,7 +426,7 @@ void enqueue_shadow(Ctx* c, const int32_t* token_dev) {
                                (const char*)c->sh_router + (size_t)l * E * d * sesz,
                                same ? nullptr : c->sh_srouter + (size_t)l * E, swt, 1, E, d, k,
                                c->cfg.rms_eps, c->sh_u, c->sh_ids + (size_t)l * k,
-                               c->sh_w + (size_t)l * k, c->sh_logits + (size_t)l * E, nullptr, s));
+                               c->sh_w + (size_t)l * k, c->sh_logits + (size_t)l * E, nullptr, s, true));
     }
     if (c->dbg_sh_h) {
       CUDA_OK(c, cudaMemcpyAsync(c->dbg_sh_h + (size_t)l * d, c->sh_h, sizeof(float) * d, cudaMemcpyDeviceToDevice, s));
@@ -442,11 +442,11 @@ void enqueue_shadow(Ctx* c, const int32_t* token_dev) {
                    c->sh_ids + (size_t)l * k, j, l * E, k, 0};
       {
         KTimer t(c, K_SHADOW, s);
-        CUDA_OK(c, launch_w13(ex, swt, c->sh_u, u_f32, c->sh_a + (size_t)j * F, d, F, s));
+        CUDA_OK(c, launch_w13(ex, swt, c->sh_u, u_f32, c->sh_a + (size_t)j * F, d, F, s, true));
       }
       {
         KTimer t(c, K_SHADOW, s);
-        CUDA_OK(c, launch_w2(ex, swt, c->sh_a + (size_t)j * F, c->sh_w + (size_t)l * k, c->sh_y + (size_t)j * d, d, F, s));
+        CUDA_OK(c, launch_w2(ex, swt, c->sh_a + (size_t)j * F, c->sh_w + (size_t)l * k, c->sh_y + (size_t)j * d, d, F, s, true));
       }
     }
   }
@@ -643,7 +643,7 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
       KTimer t(c, K_ROUTER, s);
       CUDA_OK(c, launch_router(c->d_h, yadd, n_add, nullptr, (const char*)c->d_router + (size_t)l * E * d * c->esz,
                                nullptr, c->wt, 1, E, d, k, c->cfg.rms_eps, pkt, ids_dev, w_dev,
-                               c->d_logits + (size_t)l * E, c->d_flag, s));
+                               c->d_logits + (size_t)l * E, c->d_flag, s, true));
       if (c->dbg_h) CUDA_OK(c, cudaMemcpyAsync(c->dbg_h + (size_t)l * d, c->d_h, sizeof(float) * d, cudaMemcpyDeviceToDevice, s));
     }
     if (c->world > 1) NCCL_OK(c, ncclBroadcast(pkt, pkt, c->pkt_bytes, ncclChar, 0, c->comm, s));
@@ -658,8 +658,8 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
           ExpertRef ex{nullptr, nullptr, (const void* const*)c->d_res_tbl, nullptr, ids_dev,
                        c->world == 1 ? j : c->my_pos, l * E, k, c->world == 1 ? 0 : 1};
           float* y = c->d_y + (size_t)j * d;
-          { KTimer t(c, K_W13, s); CUDA_OK(c, launch_w13(ex, c->wt, pkt, u_f32, c->d_a + (size_t)j * F, d, F, s)); }
-          { KTimer t(c, K_W2, s); CUDA_OK(c, launch_w2(ex, c->wt, c->d_a + (size_t)j * F, w_dev, y, d, F, s)); }
+          { KTimer t(c, K_W13, s); CUDA_OK(c, launch_w13(ex, c->wt, pkt, u_f32, c->d_a + (size_t)j * F, d, F, s, true)); }
+          { KTimer t(c, K_W2, s); CUDA_OK(c, launch_w2(ex, c->wt, c->d_a + (size_t)j * F, w_dev, y, d, F, s, true)); }
           if (c->dbg_ypart) CUDA_OK(c, cudaMemcpyAsync(c->dbg_ypart + ((size_t)l * k + j) * d, y, sizeof(float) * d, cudaMemcpyDeviceToDevice, s));
         }
       }
