@@ -324,8 +324,8 @@ def main():
     value = args.steps / dev_s
     e2e = args.steps / wall
     res = None
-    if not args.no_resident and world == 1 and rank == 0:
-        res = resident_baseline(odmoe, torch, args, local)
+    if not args.no_resident:
+        res = resident_baseline(odmoe, torch, args, local, rank, world, dist)
 
     if rank == 0:
         n_exp = max(1, st["n_w13"])
@@ -392,15 +392,23 @@ def main():
     return 0
 
 
-def resident_baseline(odmoe, torch, args, dev):
-    """Fully-resident baseline (same kernels and placement; all 256 experts in HBM; routing
-    consumed on the device, no per-layer host sync)."""
-    eng = odmoe.Engine(device=dev, predictor=odmoe.PRED_NONE, slots_per_gpu=-1, time_kernels=1,
-                       weight_seed=SEED, **SHAPE)
+def resident_baseline(odmoe, torch, args, dev, rank, world, dist):
+    """Fully-resident baseline (same kernels and placement; every expert a GPU can be assigned is
+    preloaded in its HBM; routing consumed on the device, no per-layer host sync). Collective at
+    N > 1 (its own NCCL communicator); timed like our arm (events, max over ranks)."""
+    uid = None
+    if world > 1:
+        obj = [odmoe.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    eng = odmoe.Engine(device=dev, rank=rank, world_size=world, nccl_id=uid, predictor=odmoe.PRED_NONE,
+                       slots_per_gpu=-1, time_kernels=1, weight_seed=SEED, **SHAPE)
     tok = 1
     for _ in range(args.warmup):
         tok, _ = eng.decode_step(tok, records=False)
     eng.reset_stats()
+    if dist is not None:
+        dist.barrier()
     torch.cuda.synchronize()
     a = torch.cuda.Event(enable_timing=True)
     b = torch.cuda.Event(enable_timing=True)
@@ -412,12 +420,16 @@ def resident_baseline(odmoe, torch, args, dev):
     s = a.elapsed_time(b) * 1e-3
     st = eng.stats()
     eng.close()
+    if dist is not None:
+        t = torch.tensor([s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        s = float(t[0])
     n_exp = max(1, st["n_w13"])
     gemv_ms = (st["ms_w13"] + st["ms_w2"]) / n_exp
     return {"value": args.steps / s, "unit": UNIT, "ms_per_step": s / args.steps * 1e3,
             "expert_gemv_us": gemv_ms * 1e3, "expert_gemv_GBps": EXPERT_BYTES / (gemv_ms * 1e-3) / 1e9,
-            "resident_expert_bytes": st["resident_bytes"],
-            "hbm_roofline_tok_s": 6541.5e9 / (64 * EXPERT_BYTES + SHAPE["V"] * SHAPE["d"] * 2)}
+            "resident_expert_bytes_per_gpu": st["resident_bytes"],
+            "hbm_roofline_tok_s_1gpu": 6541.5e9 / (64 * EXPERT_BYTES + SHAPE["V"] * SHAPE["d"] * 2)}
 
 
 if __name__ == "__main__":
