@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--no-resident", action="store_true", help="skip the fully-resident baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--first-token", type=int, default=-1)
+    ap.add_argument("--prefill", type=int, default=512,
+                    help="prompt tokens prefilled (configs[4]: TTFT + grouped GEMM) before the decode warm-up; 0 = skip")
     ap.add_argument("--out", default="")
     return ap.parse_args()
 
@@ -288,6 +290,23 @@ def main():
     link = h2d_peak_gbs(torch, torch.device("cuda", local), barrier if dist is not None else None)
 
     tok = args.first_token if args.first_token >= 0 else 1
+    prefill = None
+    if args.prefill > 0:
+        from inputs import MIXTRAL, gen_prompt
+        prompt = [int(x) for x in gen_prompt(MIXTRAL, 1, args.prefill)]
+        eng.prefill(prompt[:8])  # allocate the prefill buffers / slots outside the timed call
+        eng.reset_stats()
+        barrier()
+        t0 = time.perf_counter()
+        tok, counts = eng.prefill(prompt)
+        ttft = time.perf_counter() - t0
+        pst = eng.stats()
+        gg_ms = (pst["ms_w13"] + pst["ms_w2"])
+        flops = 2.0 * args.prefill * SHAPE["k"] * 3 * SHAPE["d"] * SHAPE["F"] * SHAPE["L"]
+        prefill = {"tokens": args.prefill, "ttft_ms_rank": ttft * 1e3, "h2d_bytes": pst["bytes_h2d"],
+                   "grouped_gemm_ms_total": gg_ms, "grouped_gemm_TFLOPs": flops / max(gg_ms, 1e-9) / 1e9 / n,
+                   "experts_activated_per_layer": sum(1 for c in counts if c > 0) / SHAPE["L"],
+                   "note": "host wall clock of odmoe_prefill (synchronous); GEMM time from CUDA events"}
     for _ in range(args.warmup):
         tok, _ = eng.decode_step(tok, records=False)
     eng.reset_stats()
@@ -373,6 +392,8 @@ def main():
                        "us_shadow_per_step": st["ms_shadow"] / args.steps * 1e3,
                        "us_lm_head": st["ms_lm_head"] / max(1, st["n_lm_head"]) * 1e3},
         }
+        if prefill is not None:
+            line["prefill"] = prefill
         if res is not None:
             line["resident"] = res
             line["ratio_vs_resident"] = value / res["value"]

@@ -30,6 +30,22 @@ __device__ __forceinline__ uint4 ld_stream(const void* p) {
   return r;
 }
 
+// Same, with an explicit L2 cache policy (createpolicy): evict_first keeps streamed weights from
+// displacing other L2 lines (e.g. dirty lines just written by the H2D copy engine).
+__device__ __forceinline__ uint4 ld_stream_pol(const void* p, uint64_t pol) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ uint64_t l2_policy(bool evict_first) {
+  uint64_t pol;
+  if (evict_first) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  else asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
 // int8 -> fp32 without I2F: place (q ^ 0x80) in the low mantissa byte of 2^23 and subtract
 // 2^23 + 128. Exact for every int8 value.
 __device__ __forceinline__ float i8_to_f32(uint32_t biased_word, int byte_sel) {

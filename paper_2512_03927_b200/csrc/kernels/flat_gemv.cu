@@ -10,6 +10,8 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <cstdlib>
+
 namespace odmoe {
 
 constexpr int kFG_WARPS = 16;
@@ -87,6 +89,7 @@ struct FlatArgs {
   int32_t* token_out;
   int rows_cap;
   int d_full, F_full;
+  int evict_first;       // L2 policy of the weight stream
 };
 
 template <typename WT, typename XT, int MODE, int UNROLL>
@@ -143,10 +146,11 @@ __global__ void __launch_bounds__(kFG_THREADS, 1) flat_gemv_kernel(const FlatArg
 
   // The weights do not depend on the previous kernel: issue this warp's first batch before the
   // programmatic-dependent-launch wait (no-op without PDL), then stage the activations.
+  const uint64_t pol = l2_policy(a.evict_first != 0);
   uint4 wa[UNROLL], wb[UNROLL];
 #pragma unroll
   for (int i = 0; i < UNROLL; ++i)
-    if (g_begin + i < g_end) wa[i] = ld_stream(base + (g_begin + i) * 32 + lane);
+    if (g_begin + i < g_end) wa[i] = ld_stream_pol(base + (g_begin + i) * 32 + lane, pol);
   if (!indirect) asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
@@ -212,11 +216,11 @@ __global__ void __launch_bounds__(kFG_THREADS, 1) flat_gemv_kernel(const FlatArg
     const long long g1 = g0 + UNROLL, g2 = g0 + 2 * UNROLL;
 #pragma unroll
     for (int i = 0; i < UNROLL; ++i)
-      if (g1 + i < g_end) wb[i] = ld_stream(base + (g1 + i) * 32 + lane);
+      if (g1 + i < g_end) wb[i] = ld_stream_pol(base + (g1 + i) * 32 + lane, pol);
     consume(wa, g0);
 #pragma unroll
     for (int i = 0; i < UNROLL; ++i)
-      if (g2 + i < g_end) wa[i] = ld_stream(base + (g2 + i) * 32 + lane);
+      if (g2 + i < g_end) wa[i] = ld_stream_pol(base + (g2 + i) * 32 + lane, pol);
     if (g1 < g_end) consume(wb, g1);
   }
   if (gcol != 0) {  // slice ended inside a row
@@ -287,6 +291,12 @@ __global__ void __launch_bounds__(kFG_THREADS, 1) flat_gemv_kernel(const FlatArg
 template <typename WT, typename XT, int MODE>
 static cudaError_t fg_launch(FlatArgs a, cudaStream_t s, bool pdl) {
   constexpr int UNROLL = 8;
+  static int ef = -1;
+  if (ef < 0) {
+    const char* e = getenv("ODMOE_L2_EVICT_FIRST");
+    ef = (e && e[0] == '0') ? 0 : 1;
+  }
+  a.evict_first = ef;
   const int sms = num_sms();
   const long long units = MODE == 0 ? a.R / 2 : a.R;
   const int grid = (int)(units < sms ? (units > 0 ? units : 1) : sms);
