@@ -239,6 +239,11 @@ odmoe_status odmoe_load_wait(void* ctx, int layer, int expert, void** w13, void*
  * it afterward"; Q16). E_STATE if the expert is not resident/loading. */
 odmoe_status odmoe_evict(void* ctx, int layer, int expert);
 
+/* Runtime options (take effect at the next decode step; every rank must set the same value):
+ *   key 1 = lookahead D (>= 1, Q11); key 2 = predictor (odmoe_predictor; the shadow predictors
+ *   need a ctx created with a shadow predictor: E_STATE otherwise). E_CONFIG on a bad key/value. */
+odmoe_status odmoe_set_option(void* ctx, int key, int64_t value);
+
 /* SEP Mode A (Q10): run the shadow from the main model's token `token`
  * through all L layers (token alignment, T1), cache the predictions for that token and
  * copy P[from_layer .. from_layer+depth) x k (rank order) into pred_ids (host, int32).

@@ -37,6 +37,7 @@ struct Ctx {
   int64_t blob_elems = 0, blob_bytes = 0, w13_bytes = 0;
   int world = 1, rank = 0, G = 1, NG = 1, my_group = 0, my_pos = 0;
   bool resident = false;
+  int built_pred = -1;           // predictor the ctx was created with (decides whether a shadow exists)
   int dev = 0;
   cudaStream_t s_main = nullptr, s_shadow = nullptr, s_copy = nullptr;
 

@@ -1195,6 +1195,7 @@ odmoe_status odmoe_create(const odmoe_config* cfg, void** ctx_out) {
     c->my_group = c->rank / c->G;
     c->my_pos = c->rank % c->G;
     c->resident = cfg->slots_per_gpu == -1;
+    c->built_pred = cfg->predictor;
     c->dev = cfg->device;
     c->has_shadow = c->rank == 0 && !c->resident &&
                     (cfg->predictor == ODMOE_PRED_SHADOW_INT8 || cfg->predictor == ODMOE_PRED_SHADOW_SAME);
@@ -1287,6 +1288,25 @@ odmoe_status odmoe_predict_ahead(void* ctx, int32_t token, int from_layer, int d
     std::vector<int32_t> P((size_t)c->L * c->k);
     CUDA_OK(c, cudaMemcpy(P.data(), c->sh_ids, 4 * P.size(), cudaMemcpyDeviceToHost));
     std::copy(P.begin() + (size_t)from_layer * c->k, P.begin() + (size_t)(from_layer + depth) * c->k, pred_ids);
+  });
+}
+
+odmoe_status odmoe_set_option(void* ctx, int key, int64_t value) {
+  CTX_GUARD(ctx);
+  return guard(c, [&] {
+    if (key == 1) {
+      if (value < 1) fail(c, ODMOE_E_CONFIG, "lookahead must be >= 1");
+      c->cfg.lookahead = (int32_t)value;
+    } else if (key == 2) {
+      if (value < 0 || value > 4) fail(c, ODMOE_E_CONFIG, "predictor");
+      const bool wants_shadow = value == ODMOE_PRED_SHADOW_INT8 || value == ODMOE_PRED_SHADOW_SAME;
+      if (wants_shadow && value != c->built_pred)
+        fail(c, ODMOE_E_STATE, "this ctx was not created with that shadow predictor");
+      if (c->resident && value != ODMOE_PRED_NONE) fail(c, ODMOE_E_STATE, "fully-resident ctx loads nothing");
+      c->cfg.predictor = (int32_t)value;
+    } else {
+      fail(c, ODMOE_E_CONFIG, "unknown option key");
+    }
   });
 }
 

@@ -113,10 +113,11 @@ _tensor_ptr = _sig("odmoe_tensor_ptr", [_P, _I, _I, ctypes.POINTER(ctypes.c_void
 _ffn_grouped = _sig("odmoe_expert_ffn_grouped", [_P, _P, _I, _P, _P, _P, _I, _I, _P, _P, _P, _I64, _P])
 _prefill_group = _sig("odmoe_prefill_group", [_P, _P, _I, _I, _I, _P, _P, _P, _P, _P])
 _prefill_dbg = _sig("odmoe_prefill_debug_read", [_P, _I, _I, _P, _I64])
+_set_option = _sig("odmoe_set_option", [_P, _I, _I64])
 _plan_layer = _sig("odmoe_plan_layer", [_I, _I, _I, _I, _P, _I, _P, ctypes.POINTER(ctypes.c_int32)])
 _plan_pool = _sig("odmoe_plan_pool_holds", [_I, _I, _I, _I, _I, _I, _I], ctypes.c_int32)
 
-EXPORTED = ["odmoe_expert_ffn_grouped", "odmoe_prefill_group", "odmoe_prefill_debug_read",
+EXPORTED = ["odmoe_set_option", "odmoe_expert_ffn_grouped", "odmoe_prefill_group", "odmoe_prefill_debug_read",
             "odmoe_plan_layer", "odmoe_plan_pool_holds", "odmoe_abi_version", "odmoe_create", "odmoe_destroy", "odmoe_last_error", "odmoe_get_stats",
             "odmoe_reset_stats", "odmoe_nccl_unique_id", "odmoe_route_topk", "odmoe_expert_ffn",
             "odmoe_shadow_expert_ffn", "odmoe_shadow_route_topk", "odmoe_lm_head_argmax",
@@ -295,6 +296,12 @@ class Engine:
         buf = (ctypes.c_int32 * (depth * self.k))()
         self._ck(_predict(self.ctx, int(token), from_layer, depth, buf))
         return [list(buf[i * self.k:(i + 1) * self.k]) for i in range(depth)]
+
+    def set_lookahead(self, D: int):
+        self._ck(_set_option(self.ctx, 1, int(D)))
+
+    def set_predictor(self, p: int):
+        self._ck(_set_option(self.ctx, 2, int(p)))
 
     def load(self, layer, expert):
         self._ck(_load_(self.ctx, layer, expert))
