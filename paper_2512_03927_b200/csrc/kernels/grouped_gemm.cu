@@ -9,11 +9,15 @@
 //        A2 [M, F] bf16 (reading Q8: the prefill intermediate is bf16, the tensor-core input type).
 // GEMM2: A = A2 [M, F], B_e = W2_e [d, F] -> gate-scale epilogue -> Y_perm [M, d] fp32.
 //
-// Kernel anatomy (one 128 x BN output tile per CTA, 6 warps):
-//   warp 0   : TMA producer, 4-stage ring of {A 128x64, B BNx64} bf16 tiles (128B swizzle)
-//   warp 1   : TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN, K=16 per MMA),
-//              tcgen05.commit -> stage "empty" mbarriers and the accumulator-ready mbarrier
-//   warps 2-5: epilogue, tcgen05.ld 32x32b (each warp owns its 32-lane TMEM quadrant)
+// Kernel anatomy (one (up to) 256 x BN output tile per CTA, 6 warps). An expert's rows (m_e ~ 128
+// at T = 512, often a little more) are covered by ONE CTA column with two M=128 accumulators in
+// TMEM, so every weight (B) stage fetched by TMA feeds both halves and the expert's weights stream
+// from HBM exactly once (a 128-row tiling would re-read them for every expert with m_e > 128):
+//   warp 0   : TMA producer, ring of {A 2x128x64, B BNx64} bf16 tiles (128B swizzle); the second
+//              A half is skipped when the tile has <= 128 rows
+//   warp 1   : TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN, K=16 per MMA, one
+//              or two accumulators), tcgen05.commit -> stage "empty" barriers / accumulator ready
+//   warps 2-5: epilogue, tcgen05.ld 32x32b (each warp owns its 32-lane TMEM quadrant), both halves
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -22,10 +26,11 @@
 
 namespace odmoe {
 
-constexpr int kGG_BM = 128;
-constexpr int kGG_BK = 64;  // 64 bf16 = 128 bytes = one swizzle row
-constexpr int kGG_STAGES = 4;
+constexpr int kGG_BM = 128;   // rows per accumulator (UMMA M)
+constexpr int kGG_MT = 2;     // accumulators per CTA -> up to 256 rows per tile
+constexpr int kGG_BK = 64;    // 64 bf16 = 128 bytes = one swizzle row
 constexpr int kGG_THREADS = 192;
+template <int BN> __host__ __device__ constexpr int gg_stages() { return BN == 256 ? 3 : 4; }
 
 struct GGMaps {
   CUtensorMap b[kMaxGGExperts];
@@ -100,24 +105,26 @@ __global__ void __launch_bounds__(kGG_THREADS, 1)
 grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ GGMaps maps_b,
                     const int4* __restrict__ tiles, int K, int N, void* __restrict__ out,
                     const float* __restrict__ gate) {
-  constexpr int A_BYTES = kGG_BM * kGG_BK * 2;
+  constexpr int STAGES = gg_stages<BN>();
+  constexpr int A_BYTES = kGG_BM * kGG_BK * 2;          // one 128-row half
   constexpr int B_BYTES = BN * kGG_BK * 2;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + kGG_STAGES * A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + kGG_STAGES * B_BYTES);
-  uint64_t* empty = full + kGG_STAGES;
-  uint64_t* acc_ready = empty + kGG_STAGES;
+  uint8_t* sA = smem;                                   // [STAGES][2 halves]
+  uint8_t* sB = smem + STAGES * kGG_MT * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* acc_ready = empty + STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_ready + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int4 tile = tiles[blockIdx.x];  // {expert, row0, rows, n0}
+  const int4 tile = tiles[blockIdx.x];  // {expert, row0, rows (<= 256), n0}
   const int expert = tile.x, row0 = tile.y, rows = tile.z, n0 = tile.w;
+  const int halves = rows > kGG_BM ? 2 : 1;
   const int KB = K / kGG_BK;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kGG_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     mbar_init(acc_ready, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
@@ -125,7 +132,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_cons
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(BN));
+                 "r"(kGG_MT * BN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -135,12 +142,14 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_cons
 
   if (warp == 0) {
     if (lane == 0) {
+      const uint32_t tx = (uint32_t)(halves * A_BYTES + B_BYTES);
       for (int kb = 0; kb < KB; ++kb) {
-        const int s = kb % kGG_STAGES;
-        const uint32_t ph = (uint32_t)(kb / kGG_STAGES) & 1u;
+        const int s = kb % STAGES;
+        const uint32_t ph = (uint32_t)(kb / STAGES) & 1u;
         mbar_wait(&empty[s], ph ^ 1u);
-        mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
-        tma_load_2d(sA + s * A_BYTES, &map_a, &full[s], kb * kGG_BK, row0);
+        mbar_expect_tx(&full[s], tx);
+        for (int hh = 0; hh < halves; ++hh)
+          tma_load_2d(sA + (s * kGG_MT + hh) * A_BYTES, &map_a, &full[s], kb * kGG_BK, row0 + hh * kGG_BM);
         tma_load_2d(sB + s * B_BYTES, &maps_b.b[expert], &full[s], kb * kGG_BK, n0);
       }
     }
@@ -148,50 +157,56 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_cons
     if (lane == 0) {
       constexpr uint32_t idesc = umma_idesc_bf16(kGG_BM, BN);
       for (int kb = 0; kb < KB; ++kb) {
-        const int s = kb % kGG_STAGES;
-        const uint32_t ph = (uint32_t)(kb / kGG_STAGES) & 1u;
+        const int s = kb % STAGES;
+        const uint32_t ph = (uint32_t)(kb / STAGES) & 1u;
         mbar_wait(&full[s], ph);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t a0 = smem_u32(sA + s * A_BYTES), b0 = smem_u32(sB + s * B_BYTES);
+        const uint32_t b0 = smem_u32(sB + s * B_BYTES);
+        for (int hh = 0; hh < halves; ++hh) {
+          const uint32_t a0 = smem_u32(sA + (s * kGG_MT + hh) * A_BYTES);
 #pragma unroll
-        for (int k = 0; k < kGG_BK / 16; ++k)
-          umma_bf16(tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc, (kb | k) != 0);
+          for (int k = 0; k < kGG_BK / 16; ++k)
+            umma_bf16(tmem + (uint32_t)(hh * BN), umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32),
+                      idesc, (kb | k) != 0);
+        }
         umma_commit(&empty[s]);  // smem slot free once these MMAs have read it
       }
       umma_commit(acc_ready);
     }
   } else {
-    // epilogue: warp w owns TMEM lanes [32*(w%4), +32) = tile rows
+    // epilogue: warp w owns TMEM lanes [32*(w%4), +32) of each accumulator half
     const int q = warp & 3;
-    const int r = q * 32 + lane;
     mbar_wait(acc_ready, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const bool valid = r < rows;
-    const long long grow = (long long)row0 + r;
-    const float g = (MODE == 1 && valid) ? gate[grow] : 0.f;
+    for (int hh = 0; hh < halves; ++hh) {
+      const int r = hh * kGG_BM + q * 32 + lane;
+      const bool valid = r < rows;
+      const long long grow = (long long)row0 + r;
+      const float g = (MODE == 1 && valid) ? gate[grow] : 0.f;
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-      uint32_t v[16];
-      tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, v);
-      if (!valid) continue;
-      if constexpr (MODE == 0) {
-        uint32_t packed[4];
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        uint32_t v[16];
+        tmem_ld16(tmem + (uint32_t)(hh * BN) + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, v);
+        if (!valid) continue;
+        if constexpr (MODE == 0) {
+          uint32_t packed[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float a0 = silu_mul(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]));
-          const float a1 = silu_mul(__uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
-          const __nv_bfloat162 b = __floats2bfloat162_rn(a0, a1);
-          packed[i] = *reinterpret_cast<const uint32_t*>(&b);
+          for (int i = 0; i < 4; ++i) {
+            const float a0 = silu_mul(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]));
+            const float a1 = silu_mul(__uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+            const __nv_bfloat162 b = __floats2bfloat162_rn(a0, a1);
+            packed[i] = *reinterpret_cast<const uint32_t*>(&b);
+          }
+          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(out) + grow * (N / 2) + (n0 + c0) / 2;
+          *reinterpret_cast<uint4*>(o) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+        } else {
+          float* o = reinterpret_cast<float*>(out) + grow * N + n0 + c0;
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            reinterpret_cast<float4*>(o)[i] =
+                make_float4(g * __uint_as_float(v[4 * i]), g * __uint_as_float(v[4 * i + 1]),
+                            g * __uint_as_float(v[4 * i + 2]), g * __uint_as_float(v[4 * i + 3]));
         }
-        __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(out) + grow * (N / 2) + (n0 + c0) / 2;
-        *reinterpret_cast<uint4*>(o) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-      } else {
-        float* o = reinterpret_cast<float*>(out) + grow * N + n0 + c0;
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          reinterpret_cast<float4*>(o)[i] =
-              make_float4(g * __uint_as_float(v[4 * i]), g * __uint_as_float(v[4 * i + 1]),
-                          g * __uint_as_float(v[4 * i + 2]), g * __uint_as_float(v[4 * i + 3]));
       }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -199,7 +214,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_cons
   __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kGG_MT * BN));
   }
 }
 
@@ -236,7 +251,7 @@ static cudaError_t gg_launch(const GroupedGemmArgs& g, cudaStream_t s) {
   if (!make_map(&ma, g.a, (uint64_t)g.M, (uint64_t)g.K, kGG_BM)) return cudaErrorInvalidValue;
   for (int e = 0; e < g.n_experts; ++e)
     if (g.b[e] && !make_map(&mb.b[e], g.b[e], (uint64_t)g.N, (uint64_t)g.K, BN)) return cudaErrorInvalidValue;
-  const size_t smem = 1024 + (size_t)kGG_STAGES * (kGG_BM + BN) * kGG_BK * 2 + 256;
+  const size_t smem = 1024 + (size_t)gg_stages<BN>() * (kGG_MT * kGG_BM + BN) * kGG_BK * 2 + 256;
   auto kern = grouped_gemm_kernel<BN, MODE>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -256,5 +271,6 @@ cudaError_t launch_grouped_gemm(const GroupedGemmArgs& g, cudaStream_t s) {
 }
 
 int grouped_gemm_bn(int mode) { return mode == 0 ? 256 : 128; }
+int grouped_gemm_bm() { return kGG_MT * kGG_BM; }
 
 }  // namespace odmoe

@@ -921,8 +921,9 @@ void build_tiles(const std::vector<int32_t>& off, const std::vector<int>& mine, 
                  std::vector<int4>& out) {
   for (int e : mine) {
     const int m = off[e + 1] - off[e];
-    for (int m0 = 0; m0 < m; m0 += 128)
-      for (int n0 = 0; n0 < N; n0 += BN) out.push_back(make_int4(e, off[e] + m0, std::min(128, m - m0), n0));
+    const int BM = grouped_gemm_bm();
+    for (int m0 = 0; m0 < m; m0 += BM)
+      for (int n0 = 0; n0 < N; n0 += BN) out.push_back(make_int4(e, off[e] + m0, std::min(BM, m - m0), n0));
   }
 }
 

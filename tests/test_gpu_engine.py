@@ -297,3 +297,32 @@ def test_mixtral_decode_sampled_layers(od):
     st = eng.stats()
     assert st["max_resident"] <= 2 and st["resident_bytes"] < 1e9  # < 1 GB of experts per GPU
     eng.close()
+
+
+def test_runtime_options_switch_predictor_and_lookahead(od):
+    """odmoe_set_option: switching predictor / lookahead between steps changes time and recall
+    accounting only; tokens stay identical."""
+    first = 21
+    eng = engine(od, TINY, predictor=od.PRED_SHADOW_INT8, slots_per_gpu=4, lookahead=1)
+    seqs = []
+    for pred, D in ((od.PRED_SHADOW_INT8, 1), (od.PRED_NONE, 2), (od.PRED_PERFECT, 3), (od.PRED_RANDOM, 1),
+                    (od.PRED_SHADOW_INT8, 3)):
+        eng.set_predictor(pred)
+        eng.set_lookahead(D)
+        eng.reset_stats()
+        t, toks = first, []
+        for _ in range(6):
+            t, _ = eng.decode_step(t)
+            toks.append(t)
+        seqs.append(toks)
+        st = eng.stats()
+        if pred == od.PRED_PERFECT:
+            assert st["correct"] == st["predicted_total"] > 0
+        if pred == od.PRED_NONE:
+            assert st["predicted_total"] == 0
+    assert all(s == seqs[0] for s in seqs)
+    with pytest.raises(od.OdmoeError):
+        eng.set_predictor(od.PRED_SHADOW_SAME)  # no such shadow in this ctx
+    with pytest.raises(od.OdmoeError):
+        eng.set_lookahead(0)
+    eng.close()

@@ -26,11 +26,22 @@ def peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
 
 
+GAP_S = 0.0
+DIRTY = False
+
+
 def timeit(fn, iters, flush):
     ts = []
     s = torch.cuda.current_stream()
     for i in range(iters + 3):
-        flush.sum()  # read 256 MB (> 126 MB L2): evicts the weights with CLEAN lines
+        if DIRTY:
+            flush.add_(1)  # write 256 MB: L2 full of DIRTY lines (like just after an H2D load)
+        else:
+            flush.sum()  # read 256 MB (> 126 MB L2): evicts the weights with CLEAN lines
+        if GAP_S > 0:
+            torch.cuda.synchronize()
+            import time as _t
+            _t.sleep(GAP_S)  # idle GPU before the launch (like the on-demand path waiting on PCIe)
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(s)
@@ -47,7 +58,12 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--only", default="")
+    ap.add_argument("--gap-ms", type=float, default=0.0)
+    ap.add_argument("--dirty", action="store_true")
     args = ap.parse_args()
+    global GAP_S, DIRTY
+    GAP_S = args.gap_ms * 1e-3
+    DIRTY = args.dirty
     dev = torch.device("cuda", 0)
     flush = torch.zeros(64 << 20, dtype=torch.float32, device=dev)
     pk = peaks()
