@@ -80,7 +80,10 @@ typedef struct {
   int32_t debug_capture;     /* 1 => keep every per-layer intermediate on the host (parity tests)      */
   int32_t time_kernels;      /* 1 => CUDA events around every kernel (bench roofline)                  */
   int32_t pool_threads;      /* host threads used to build the pool (0 => all)                         */
-  int32_t reserved[7];
+  int32_t refine_depth;      /* R >= 0: SEP refinement ("Mode B"): after the main router of
+                                layer l the shadow re-runs layers l..l+R-1 from the main model's exact
+                                state and corrects the loads of layers l+1..l+R; 0 = off (paper's Mode A) */
+  int32_t reserved[6];
   const void* nccl_id;       /* 128-byte ncclUniqueId from rank 0 (NULL when world_size == 1)          */
 } odmoe_config;
 
@@ -113,6 +116,8 @@ typedef struct {
   int64_t n_router, n_w13, n_w2, n_shadow, n_lm_head, n_embed;
   double wait_us;            /* host time blocked on loads                                            */
   int64_t correct, predicted_total; /* Σc and Σ k over layers with a prediction (rank 0)              */
+  int64_t refine_corrections;        /* layer predictions changed by the SEP refinement                */
+  int64_t refine_correct, refine_total; /* Σc, Σk of the refined predictions (rank 0)                  */
 } odmoe_stats;
 
 /* ------------------------------------------------------------------ lifecycle */
@@ -241,7 +246,8 @@ odmoe_status odmoe_evict(void* ctx, int layer, int expert);
 
 /* Runtime options (take effect at the next decode step; every rank must set the same value):
  *   key 1 = lookahead D (>= 1, Q11); key 2 = predictor (odmoe_predictor; the shadow predictors
- *   need a ctx created with a shadow predictor: E_STATE otherwise). E_CONFIG on a bad key/value. */
+ *   need a ctx created with a shadow predictor: E_STATE otherwise); key 3 = refine_depth R (0..4;
+ *   only with a shadow predictor). E_CONFIG on a bad key/value. */
 odmoe_status odmoe_set_option(void* ctx, int key, int64_t value);
 
 /* SEP Mode A (Q10): run the shadow from the main model's token `token`

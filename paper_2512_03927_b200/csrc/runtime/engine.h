@@ -117,6 +117,25 @@ struct Ctx {
   int l_cur = 0;
   std::vector<int32_t> pred_tbl; // [L][k] predictions this step (host)
 
+  // SEP refinement ("Mode B"; refine_depth R > 0): after the main router of layer l the shadow
+  // re-runs from the main's exact state (h_l, u_l, true ids of layer l) and predicts l+1..l+R.
+  int R = 0;
+  std::vector<cudaEvent_t> ev_router;   // [L] main router of layer l done (h_hist[l], pkt[l] valid)
+  std::vector<cudaEvent_t> ev_ref;      // [L] refined predictions of refinement l on the host
+  std::vector<char> ref_enq;            // [L] refinement l enqueued this step (its event is current)
+  float* h_hist = nullptr;              // device [L][d] residual entering layer l (rank 0)
+  float* rf_h = nullptr;
+  void* rf_u = nullptr;
+  int32_t* rf_ids = nullptr;            // device [L][4][k] refined ids (received at N > 1)
+  float* rf_w = nullptr;                // device [4][k]
+  float* rf_y = nullptr;                // device [k][d]
+  float* rf_a = nullptr;                // device [k][F]
+  const float** rf_yptr = nullptr;
+  int32_t* h_ref = nullptr;             // pinned [L][4][k]
+  int ref_next = 0;                     // next refinement to apply (host, this step)
+  std::vector<int32_t> predA_tbl;       // [L][k] Mode A predictions (the paper's SEP: recall Eq. 3)
+  std::vector<int32_t> predB_tbl;       // [L][k] refined predictions (-1 = none)
+
   // PERFECT predictor: routing recorded per input token (Mode A: routing is a function of the
   // token only, there is no KV state on the hot path)
   std::map<int32_t, std::vector<int32_t>> route_cache;

@@ -196,6 +196,10 @@ void validate(const odmoe_config* g) {
   if (g->world_size > 1 && G != g->k) bad("multi-GPU needs group_size == k (one expert per GPU per layer)");
   if (g->slots_per_gpu != -1 && g->slots_per_gpu < g->k / G) bad("slots_per_gpu must be >= k/G or -1");
   if (g->world_size > 1 && g->nccl_id == nullptr) bad("nccl_id required when world_size > 1");
+  if (g->refine_depth < 0 || g->refine_depth > 4) bad("refine_depth must be in 0..4");
+  if (g->refine_depth > 0 && g->predictor != ODMOE_PRED_SHADOW_INT8 && g->predictor != ODMOE_PRED_SHADOW_SAME)
+    bad("refine_depth needs a shadow predictor");
+  if (g->refine_depth > 0 && g->dtype != ODMOE_BF16) bad("refine_depth needs the bf16 model");
 }
 
 // ------------------------------------------------------------------ setup
@@ -393,6 +397,29 @@ void build_buffers(Ctx* c) {
   } else if (c->world > 1) {
     c->sh_ids = dmalloc<int32_t>(c, (size_t)L * k, "sh_ids");  // receive buffer for P
   }
+  // SEP refinement buffers (allocated for any shadow ctx so the depth can be switched at run time)
+  if (c->built_pred == ODMOE_PRED_SHADOW_INT8 || c->built_pred == ODMOE_PRED_SHADOW_SAME) {
+    c->ev_router.resize(L);
+    c->ev_ref.resize(L);
+    for (auto& e : c->ev_router) CUDA_OK(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : c->ev_ref) CUDA_OK(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->ref_enq.assign(L, 0);
+    c->rf_ids = dmalloc<int32_t>(c, (size_t)L * 4 * k, "rf_ids");
+    c->h_ref = hmalloc<int32_t>(c, (size_t)L * 4 * k, "h_ref");
+    if (c->rank == 0) {
+      c->h_hist = dmalloc<float>(c, (size_t)L * d, "h_hist");
+      c->rf_h = dmalloc<float>(c, d, "rf_h");
+      c->rf_u = dmalloc<char>(c, (size_t)d * 4, "rf_u");
+      c->rf_w = dmalloc<float>(c, (size_t)4 * k, "rf_w");
+      c->rf_y = dmalloc<float>(c, (size_t)k * d, "rf_y");
+      c->rf_a = dmalloc<float>(c, (size_t)k * F, "rf_a");
+      c->rf_yptr = dmalloc<const float*>(c, k, "rf_yptr");
+      for (int j = 0; j < k; ++j) yp[j] = c->rf_y + (size_t)j * d;
+      CUDA_OK(c, cudaMemcpy(c->rf_yptr, yp.data(), sizeof(float*) * k, cudaMemcpyHostToDevice));
+    }
+  }
+  c->predA_tbl.assign((size_t)L * k, -1);
+  c->predB_tbl.assign((size_t)L * k, -1);
   if (c->cfg.debug_capture && c->rank == 0) {
     c->dbg_h = dmalloc<float>(c, (size_t)L * d, "dbg_h");
     c->dbg_ypart = dmalloc<float>(c, (size_t)L * k * d, "dbg_ypart");
@@ -479,7 +506,9 @@ bool pred_available(Ctx* c, int m) {
     const int hi = c->world == 1 ? m + 1 : std::min(c->L, evl + c->pred_chunk);
     for (int l = evl; l < hi; ++l) {
       c->pred_ready[l] = 1;
-      std::copy(c->h_pred + (size_t)l * c->k, c->h_pred + (size_t)(l + 1) * c->k, c->pred_tbl.begin() + (size_t)l * c->k);
+      std::copy(c->h_pred + (size_t)l * c->k, c->h_pred + (size_t)(l + 1) * c->k, c->predA_tbl.begin() + (size_t)l * c->k);
+      if (c->predB_tbl[(size_t)l * c->k] < 0)  // a refined prediction, if any, supersedes Mode A
+        std::copy(c->h_pred + (size_t)l * c->k, c->h_pred + (size_t)(l + 1) * c->k, c->pred_tbl.begin() + (size_t)l * c->k);
     }
     return true;
   }
@@ -503,6 +532,60 @@ void random_prediction(Ctx* c, int64_t step, int l, int32_t* out) {
     for (int i = 0; i < n; ++i) dup |= out[i] == e;
     if (!dup) out[n++] = e;
   }
+}
+
+// ------------------------------------------------------------------ SEP refinement ("Mode B")
+// Rank 0, shadow stream, after the main router of layer j: re-anchor the INT8 shadow at the main
+// model's exact state -- h_j, u_j and the TRUE experts of layer j -- and run it R layers ahead:
+// y'_j = sum_i w_i Q-FFN_i(u_j); h' = h_j + y'_j; router_{j+1}(h') -> P_B[j+1]; (experts, router)...
+// Its error covers at most R quantised layers instead of the whole token (Mode A), so it corrects
+// most mispredictions one or two layers before the main router would discover them.
+void enqueue_refine(Ctx* c, int j) {
+  const int L = c->L, E = c->E, k = c->k, d = c->d, F = c->F, R = c->R;
+  cudaStream_t s = c->s_shadow;
+  const WType swt = c->sh_wt;
+  const size_t sesz = swt == W_I8 ? 1 : c->esz;
+  const bool same = swt != W_I8;
+  char* pkt = c->d_pkt + (size_t)j * c->pkt_bytes;
+  int32_t* out = c->rf_ids + (size_t)j * 4 * k;
+  CUDA_OK(c, cudaStreamWaitEvent(s, c->ev_router[j], 0));
+  CUDA_OK(c, cudaMemcpyAsync(c->rf_h, c->h_hist + (size_t)j * d, sizeof(float) * d, cudaMemcpyDeviceToDevice, s));
+  CUDA_OK(c, cudaMemsetAsync(out, 0xff, sizeof(int32_t) * 4 * k, s));
+  // layer j with the main's u_j and true ids
+  for (int i = 0; i < k; ++i) {
+    ExpertRef ex{nullptr, nullptr, (const void* const*)c->d_sh_tbl, (const float* const*)c->d_sh_stbl,
+                 (const int32_t*)(pkt + c->pkt_ids_off), i, j * E, k, 0};
+    { KTimer t(c, K_SHADOW, s); CUDA_OK(c, launch_w13(ex, swt, pkt, 0, c->rf_a + (size_t)i * F, d, F, s)); }
+    { KTimer t(c, K_SHADOW, s); CUDA_OK(c, launch_w2(ex, swt, c->rf_a + (size_t)i * F, (const float*)(pkt + c->pkt_w_off), c->rf_y + (size_t)i * d, d, F, s, true)); }
+  }
+  for (int r = 1; r <= R && j + r < L; ++r) {
+    const int m = j + r;
+    {
+      KTimer t(c, K_SHADOW, s);
+      CUDA_OK(c, launch_router(c->rf_h, c->rf_yptr, k, nullptr, (const char*)c->sh_router + (size_t)m * E * d * sesz,
+                               same ? nullptr : c->sh_srouter + (size_t)m * E, swt, 1, E, d, k, c->cfg.rms_eps,
+                               c->rf_u, out + (size_t)(r - 1) * k, c->rf_w + (size_t)(r - 1) * k, nullptr, nullptr, s, true));
+    }
+    if (r < R && m + 1 < L) {
+      for (int i = 0; i < k; ++i) {
+        ExpertRef ex{nullptr, nullptr, (const void* const*)c->d_sh_tbl, (const float* const*)c->d_sh_stbl,
+                     out + (size_t)(r - 1) * k, i, m * E, k, 0};
+        { KTimer t(c, K_SHADOW, s); CUDA_OK(c, launch_w13(ex, swt, c->rf_u, 0, c->rf_a + (size_t)i * F, d, F, s, true)); }
+        { KTimer t(c, K_SHADOW, s); CUDA_OK(c, launch_w2(ex, swt, c->rf_a + (size_t)i * F, c->rf_w + (size_t)(r - 1) * k, c->rf_y + (size_t)i * d, d, F, s, true)); }
+      }
+    }
+  }
+}
+
+// Broadcast (N > 1) and copy to the host the refined ids of refinement j; record ev_ref[j].
+void enqueue_refine_delivery(Ctx* c, int j) {
+  const int k = c->k;
+  cudaStream_t s = c->s_shadow;
+  int32_t* buf = c->rf_ids + (size_t)j * 4 * k;
+  if (c->world > 1) NCCL_OK(c, ncclBroadcast(buf, buf, (size_t)4 * k, ncclInt32, 0, c->comm_pred, s));
+  CUDA_OK(c, cudaMemcpyAsync(c->h_ref + (size_t)j * 4 * k, buf, sizeof(int32_t) * 4 * k, cudaMemcpyDeviceToHost, s));
+  CUDA_OK(c, cudaEventRecord(c->ev_ref[j], s));
+  c->ref_enq[j] = 1;
 }
 
 // ------------------------------------------------------------------ slots + loads
@@ -561,9 +644,60 @@ void release_slot(Ctx* c, int slot) {
 
 int64_t load_key(const Ctx* c, int64_t tok, int l, int j) { return (tok * c->L + l) * 16 + j; }
 
+// Consume finished refinements in order; for every layer whose refined prediction differs from the
+// plan: take it as the plan and, if that layer's loads were already issued, stop the wrong ones and
+// load the right experts now (before the main router of that layer runs).
+void apply_refinements(Ctx* c) {
+  const int k = c->k;
+  while (c->ref_next < c->L - 1 && c->ref_enq[c->ref_next]) {
+    const int j = c->ref_next;
+    const cudaError_t q = cudaEventQuery(c->ev_ref[j]);
+    if (q == cudaErrorNotReady) return;
+    CUDA_OK(c, q);
+    c->ref_next++;
+    for (int r = 1; r <= c->R && j + r < c->L; ++r) {
+      const int m = j + r;
+      const int32_t* P = c->h_ref + ((size_t)j * 4 + (r - 1)) * k;
+      if (P[0] < 0) continue;
+      int32_t* B = c->predB_tbl.data() + (size_t)m * k;
+      std::copy(P, P + k, B);
+      if (m <= c->l_cur) continue;  // that layer's router already decided
+      int32_t* plan = c->pred_tbl.data() + (size_t)m * k;
+      bool same = c->pred_ready[m] != 0;
+      for (int a = 0; a < k && same; ++a) {
+        bool found = false;
+        for (int b = 0; b < k; ++b) found |= P[a] == plan[b];
+        same &= found;
+      }
+      if (same) continue;
+      c->stats.refine_corrections++;
+      std::copy(P, P + k, plan);
+      c->pred_ready[m] = 1;
+      if (m >= c->next_plan) continue;  // not planned yet: pump() will use the refined plan
+      const std::vector<int> mine = my_experts(c, m, P);
+      for (int i = 0; i < (int)c->slots.size(); ++i) {
+        Slot& sl = c->slots[i];
+        if (sl.occupied && sl.token == c->step && sl.layer == m &&
+            std::find(mine.begin(), mine.end(), sl.expert) == mine.end())
+          release_slot(c, i);
+      }
+      for (size_t jj = 0; jj < mine.size(); ++jj) {
+        if (find_slot(c, c->step, m, mine[jj]) >= 0) continue;
+        const int fs = free_slot(c);
+        if (fs < 0) {  // no room now: re-plan this layer when a slot frees
+          c->next_plan = std::min(c->next_plan, m);
+          break;
+        }
+        submit_load(c, fs, c->step, m, mine[jj], load_key(c, c->step, m, 1 + (int)jj));
+      }
+    }
+  }
+}
+
 // Issue predicted loads for layers next_plan .. l_cur + D while slots are free (Q11).
 void pump(Ctx* c) {
   if (c->resident) return;
+  if (c->R > 0) apply_refinements(c);
   while (c->next_plan < c->L) {
     const int m = c->next_plan;
     if (m > c->l_cur + c->cfg.lookahead) break;
@@ -599,23 +733,34 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
   // predictions for this step
   std::fill(c->pred_ready.begin(), c->pred_ready.end(), 0);
   std::fill(c->pred_tbl.begin(), c->pred_tbl.end(), -1);
+  std::fill(c->predA_tbl.begin(), c->predA_tbl.end(), -1);
+  std::fill(c->predB_tbl.begin(), c->predB_tbl.end(), -1);
+  const bool shadow_pred = p == ODMOE_PRED_SHADOW_INT8 || p == ODMOE_PRED_SHADOW_SAME;
+  c->R = (!c->resident && shadow_pred) ? c->cfg.refine_depth : 0;
+  c->ref_next = 0;
+  std::fill(c->ref_enq.begin(), c->ref_enq.end(), 0);
   c->pred_valid = false;
   if (!c->resident) {
-    if (p == ODMOE_PRED_SHADOW_INT8 || p == ODMOE_PRED_SHADOW_SAME) {
+    if (shadow_pred) {
       if (r0) {
         CUDA_OK(c, cudaStreamWaitEvent(c->s_shadow, c->ev_tok, 0));
         enqueue_shadow(c, c->d_tok_in);
       }
       if (c->world > 1) enqueue_pred_broadcast(c);
+      // receivers enqueue every refinement delivery now (same collective order as rank 0)
+      if (c->world > 1 && !r0 && c->R > 0)
+        for (int j = 0; j < L - 1; ++j) enqueue_refine_delivery(c, j);
       c->pred_valid = true;
     } else if (p == ODMOE_PRED_RANDOM) {
       for (int l = 0; l < L; ++l) random_prediction(c, c->step, l, c->pred_tbl.data() + (size_t)l * k);
+      c->predA_tbl = c->pred_tbl;
       std::fill(c->pred_ready.begin(), c->pred_ready.end(), 1);
       c->pred_valid = true;
     } else if (p == ODMOE_PRED_PERFECT) {
       auto it = c->route_cache.find(token_in);
       if (it != c->route_cache.end()) {
         std::copy(it->second.begin(), it->second.end(), c->pred_tbl.begin());
+        c->predA_tbl = c->pred_tbl;
         std::fill(c->pred_ready.begin(), c->pred_ready.end(), 1);
         c->pred_valid = true;
       }
@@ -645,6 +790,12 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
                                nullptr, c->wt, 1, E, d, k, c->cfg.rms_eps, pkt, ids_dev, w_dev,
                                c->d_logits + (size_t)l * E, c->d_flag, s, true));
       if (c->dbg_h) CUDA_OK(c, cudaMemcpyAsync(c->dbg_h + (size_t)l * d, c->d_h, sizeof(float) * d, cudaMemcpyDeviceToDevice, s));
+      if (c->R > 0 && l < L - 1) {
+        CUDA_OK(c, cudaMemcpyAsync(c->h_hist + (size_t)l * d, c->d_h, sizeof(float) * d, cudaMemcpyDeviceToDevice, s));
+        CUDA_OK(c, cudaEventRecord(c->ev_router[l], s));
+        enqueue_refine(c, l);
+        enqueue_refine_delivery(c, l);
+      }
     }
     if (c->world > 1) NCCL_OK(c, ncclBroadcast(pkt, pkt, c->pkt_bytes, ncclChar, 0, c->comm, s));
     n_add = c->world == 1 ? k : 1;
@@ -774,25 +925,32 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
       CUDA_OK(c, cudaMemcpyAsync(c->h_ids + (size_t)l * k, c->d_pkt + (size_t)l * c->pkt_bytes + c->pkt_ids_off, 4 * k, cudaMemcpyDeviceToHost, s));
   }
   CUDA_OK(c, cudaStreamSynchronize(s));
-  if (c->has_shadow && r0 && !c->resident) CUDA_OK(c, cudaEventSynchronize(c->ev_shadow_done));
-  if (!c->resident && c->world > 1 && c->pred_valid &&
-      (p == ODMOE_PRED_SHADOW_INT8 || p == ODMOE_PRED_SHADOW_SAME))
-    CUDA_OK(c, cudaStreamSynchronize(c->s_shadow));
+  if (!c->resident && shadow_pred && (r0 || c->world > 1)) CUDA_OK(c, cudaStreamSynchronize(c->s_shadow));
   if (c->h_flag[0]) fail(c, ODMOE_E_NONFINITE, "non-finite router logits");
   if (c->resident) std::copy(c->h_ids, c->h_ids + (size_t)L * k, true_ids.begin());
 
-  // predictions as they stood (recall accounting, Eqs. 2-3); Mode A computes all of them
+  // predictions as they stood (recall accounting, Eqs. 2-3): the paper's SEP (Mode A) predictions
+  // drive recall_eq3; the refined ones are counted separately
   for (int l = 0; l < L; ++l) pred_available(c, l);
+  if (c->R > 0) apply_refinements(c);
   if (r0) {
     for (int l = 0; l < L; ++l) {
       const int32_t* S = true_ids.data() + (size_t)l * k;
-      const int32_t* P = c->pred_tbl.data() + (size_t)l * k;
+      const int32_t* P = c->predA_tbl.data() + (size_t)l * k;
       const bool have = c->pred_valid && P[0] >= 0;
       int corr = 0;
       if (have)
         for (int a = 0; a < k; ++a)
           for (int b = 0; b < k; ++b) corr += S[a] == P[b];
       if (have) { c->stats.correct += corr; c->stats.predicted_total += k; }
+      const int32_t* PB = c->predB_tbl.data() + (size_t)l * k;
+      if (PB[0] >= 0) {
+        int cb = 0;
+        for (int a = 0; a < k; ++a)
+          for (int b = 0; b < k; ++b) cb += S[a] == PB[b];
+        c->stats.refine_correct += cb;
+        c->stats.refine_total += k;
+      }
       if (rec) {
         odmoe_layer_record& R = rec[l];
         if (c->resident) {
@@ -1128,6 +1286,10 @@ void destroy_ctx(Ctx* c) {
     if (s.ev_free) cudaEventDestroy(s.ev_free);
   }
   if (c->h_off) cudaFreeHost(c->h_off);
+  F(c->h_hist); F(c->rf_h); F(c->rf_u); F(c->rf_ids); F(c->rf_w); F(c->rf_y); F(c->rf_a); F((void*)c->rf_yptr);
+  if (c->h_ref) cudaFreeHost(c->h_ref);
+  for (auto e : c->ev_router) cudaEventDestroy(e);
+  for (auto e : c->ev_ref) cudaEventDestroy(e);
   auto FH = [](void* p) { if (p) cudaFreeHost(p); };
   FH(c->pool); FH(c->h_ids); FH(c->h_w); FH(c->h_pred); FH(c->h_tok); FH(c->h_flag);
   for (auto e : c->ev_pred) cudaEventDestroy(e);
@@ -1305,6 +1467,11 @@ odmoe_status odmoe_set_option(void* ctx, int key, int64_t value) {
         fail(c, ODMOE_E_STATE, "this ctx was not created with that shadow predictor");
       if (c->resident && value != ODMOE_PRED_NONE) fail(c, ODMOE_E_STATE, "fully-resident ctx loads nothing");
       c->cfg.predictor = (int32_t)value;
+    } else if (key == 3) {
+      if (value < 0 || value > 4) fail(c, ODMOE_E_CONFIG, "refine_depth must be in 0..4");
+      if (value > 0 && (c->ev_ref.empty() || c->wt != W_BF16))
+        fail(c, ODMOE_E_STATE, "refinement needs a bf16 ctx created with a shadow predictor");
+      c->cfg.refine_depth = (int32_t)value;
     } else {
       fail(c, ODMOE_E_CONFIG, "unknown option key");
     }

@@ -50,7 +50,8 @@ class Config(ctypes.Structure):
                 ("rank", ctypes.c_int32), ("world_size", ctypes.c_int32), ("group_size", ctypes.c_int32),
                 ("device", ctypes.c_int32), ("chunk_bytes", ctypes.c_int64),
                 ("debug_capture", ctypes.c_int32), ("time_kernels", ctypes.c_int32),
-                ("pool_threads", ctypes.c_int32), ("reserved", ctypes.c_int32 * 7),
+                ("pool_threads", ctypes.c_int32), ("refine_depth", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 6),
                 ("nccl_id", ctypes.c_void_p)]
 
 
@@ -68,7 +69,8 @@ class Stats(ctypes.Structure):
         ("pool_build_s", ctypes.c_double)] + [
         (n, ctypes.c_double) for n in ("ms_router", "ms_w13", "ms_w2", "ms_shadow", "ms_lm_head", "ms_embed")] + [
         (n, ctypes.c_int64) for n in ("n_router", "n_w13", "n_w2", "n_shadow", "n_lm_head", "n_embed")] + [
-        ("wait_us", ctypes.c_double), ("correct", ctypes.c_int64), ("predicted_total", ctypes.c_int64)]
+        ("wait_us", ctypes.c_double), ("correct", ctypes.c_int64), ("predicted_total", ctypes.c_int64),
+        ("refine_corrections", ctypes.c_int64), ("refine_correct", ctypes.c_int64), ("refine_total", ctypes.c_int64)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
@@ -254,12 +256,13 @@ class Engine:
     def __init__(self, L, E, k, d, F, V, dtype=BF16, predictor=PRED_SHADOW_INT8, lookahead=1,
                  slots_per_gpu=2, rms_eps=1e-5, weight_seed=2512, aux_seed=1, rank=0, world_size=1,
                  group_size=0, device=0, chunk_bytes=0, debug_capture=0, time_kernels=0,
-                 nccl_id: Optional[bytes] = None):
+                 nccl_id: Optional[bytes] = None, refine_depth=0):
         self.cfg = Config(L=L, E=E, k=k, d=d, F=F, V=V, dtype=dtype, predictor=predictor,
                           lookahead=lookahead, slots_per_gpu=slots_per_gpu, rms_eps=rms_eps,
                           weight_seed=weight_seed, aux_seed=aux_seed, rank=rank, world_size=world_size,
                           group_size=group_size, device=device, chunk_bytes=chunk_bytes,
-                          debug_capture=debug_capture, time_kernels=time_kernels, pool_threads=0)
+                          debug_capture=debug_capture, time_kernels=time_kernels, pool_threads=0,
+                          refine_depth=refine_depth)
         self._uid = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
         self.cfg.nccl_id = ctypes.cast(self._uid, ctypes.c_void_p) if self._uid is not None else None
         self.L, self.E, self.k, self.d, self.F, self.V = L, E, k, d, F, V
@@ -302,6 +305,9 @@ class Engine:
 
     def set_predictor(self, p: int):
         self._ck(_set_option(self.ctx, 2, int(p)))
+
+    def set_refine_depth(self, R: int):
+        self._ck(_set_option(self.ctx, 3, int(R)))
 
     def load(self, layer, expert):
         self._ck(_load_(self.ctx, layer, expert))

@@ -166,7 +166,9 @@ def test_output_invariance_across_predictors_slots_and_modes(od):
                dict(predictor=od.PRED_RANDOM, slots_per_gpu=3, lookahead=2),
                dict(predictor=od.PRED_SHADOW_SAME, slots_per_gpu=4, lookahead=2),
                dict(predictor=od.PRED_NONE, slots_per_gpu=-1),
-               dict(predictor=od.PRED_SHADOW_INT8, slots_per_gpu=2, chunk_bytes=65536)):
+               dict(predictor=od.PRED_SHADOW_INT8, slots_per_gpu=2, chunk_bytes=65536),
+               dict(predictor=od.PRED_SHADOW_INT8, slots_per_gpu=4, lookahead=2, refine_depth=2),
+               dict(predictor=od.PRED_SHADOW_INT8, slots_per_gpu=2, refine_depth=1)):
         eng, toks, routes, _ = _run(od, TINY, 12, first, **kw)
         assert toks == base, kw
         assert routes == base_r, kw
@@ -325,4 +327,25 @@ def test_runtime_options_switch_predictor_and_lookahead(od):
         eng.set_predictor(od.PRED_SHADOW_SAME)  # no such shadow in this ctx
     with pytest.raises(od.OdmoeError):
         eng.set_lookahead(0)
+    eng.close()
+
+
+def test_sep_refinement_improves_prediction_accuracy(od):
+    """Refinement ("Mode B"): predictions re-anchored at the main model's exact
+    state are at least as accurate as the token-start shadow (Mode A) and never change outputs."""
+    eng = engine(od, TINY, predictor=od.PRED_SHADOW_INT8, slots_per_gpu=4, lookahead=2, refine_depth=2)
+    t = 5
+    for _ in range(24):
+        t, recs = eng.decode_step(t)
+    st = eng.stats()
+    assert st["refine_total"] > 0
+    ra = st["correct"] / st["predicted_total"]
+    rb = st["refine_correct"] / st["refine_total"]
+    assert rb >= ra - 0.02, (ra, rb)
+    eng.set_refine_depth(0)
+    eng.reset_stats()
+    t = 5
+    for _ in range(4):
+        t, _ = eng.decode_step(t)
+    assert eng.stats()["refine_total"] == 0
     eng.close()

@@ -14,7 +14,7 @@ SEED = 2512
 N_TOK = 10
 
 
-def _run_rank(rank, world, port, q, predictor, slots, lookahead, prompt):
+def _run_rank(rank, world, port, q, predictor, slots, lookahead, prompt, refine=0):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     import torch as t
@@ -27,7 +27,7 @@ def _run_rank(rank, world, port, q, predictor, slots, lookahead, prompt):
     try:
         eng = odmoe.Engine(TINY.L, TINY.E, TINY.k, TINY.d, TINY.F, TINY.V, dtype=odmoe.BF16, predictor=predictor,
                            slots_per_gpu=slots, lookahead=lookahead, weight_seed=SEED, rank=rank, world_size=world,
-                           device=rank, nccl_id=obj[0])
+                           device=rank, nccl_id=obj[0], refine_depth=refine)
         toks, routes = [], []
         pf = None
         if prompt:
@@ -47,12 +47,12 @@ def _run_rank(rank, world, port, q, predictor, slots, lookahead, prompt):
     dist.destroy_process_group()
 
 
-def _multi(world, predictor, slots=2, lookahead=1, prompt=None):
+def _multi(world, predictor, slots=2, lookahead=1, prompt=None, refine=0):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29600 + world * 11 + predictor * 3 + os.getpid() % 50
-    ps = [ctx.Process(target=_run_rank, args=(r, world, port, q, predictor, slots, lookahead, prompt))
+    port = 29600 + world * 11 + predictor * 3 + refine * 2 + (5 if slots == -1 else 0) + os.getpid() % 50
+    ps = [ctx.Process(target=_run_rank, args=(r, world, port, q, predictor, slots, lookahead, prompt, refine))
           for r in range(world)]
     for p in ps:
         p.start()
@@ -93,6 +93,10 @@ def test_multi_gpu_bitwise_invariance(world):
             assert r[4] == base_pf, (world, pred, r[0])          # prefill: token + expert counts
             assert r[5] <= 2                                     # residency bound at 2 slots
         assert res[0][3] == base_routes
+    # SEP refinement at N GPUs (refined ids broadcast over the prediction communicator)
+    res = _multi(world, odmoe.PRED_SHADOW_INT8, lookahead=max(1, world // 2), refine=2)
+    for r in res:
+        assert r[2] == base_toks
     # fully resident at N GPUs (device-side routing, no host sync per layer)
     res = _multi(world, odmoe.PRED_NONE, slots=-1)
     for r in res:

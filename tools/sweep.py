@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--lookaheads", default="1,2,3,4")
     ap.add_argument("--predictors", default="shadow_int8,perfect,none,random")
     ap.add_argument("--slots", type=int, default=2)
+    ap.add_argument("--refine", default="0", help="comma list of SEP refinement depths (shadow predictor only)")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
@@ -47,10 +48,16 @@ def main():
     eng = odmoe.Engine(device=local, rank=rank, world_size=world, nccl_id=uid, predictor=odmoe.PRED_SHADOW_INT8,
                        slots_per_gpu=args.slots, lookahead=1, weight_seed=2512, **SHAPE)
     lines = []
+    combos = []
     for pname in args.predictors.split(","):
         for D in [int(x) for x in args.lookaheads.split(",")]:
+            for R in ([int(x) for x in args.refine.split(",")] if pname.startswith("shadow") else [0]):
+                combos.append((pname, D, R))
+    for pname, D, R in combos:
+        if True:
             eng.set_predictor(odmoe.PREDICTORS[pname])
             eng.set_lookahead(D)
+            eng.set_refine_depth(R)
             tok = 1
             for _ in range(args.warmup):
                 tok, _ = eng.decode_step(tok, records=False)
@@ -78,7 +85,10 @@ def main():
                 bytes_all = float(t[1])
             if rank == 0:
                 rec = st["correct"] / st["predicted_total"] if st["predicted_total"] else None
-                line = {"n_gpus": world, "predictor": pname, "lookahead": D, "tok_s": args.steps / s,
+                recb = st["refine_correct"] / st["refine_total"] if st["refine_total"] else None
+                line = {"n_gpus": world, "predictor": pname, "lookahead": D, "refine_depth": R,
+                        "recall_refined": recb, "refine_corrections_per_token": st["refine_corrections"] / args.steps,
+                        "tok_s": args.steps / s,
                         "ms_per_token": s / args.steps * 1e3, "recall_eq3": rec,
                         "h2d_GBps_aggregate": bytes_all / s / 1e9,
                         "h2d_bytes_per_token": bytes_all / args.steps,
