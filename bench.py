@@ -392,6 +392,17 @@ def main():
                        "us_shadow_per_step": st["ms_shadow"] / args.steps * 1e3,
                        "us_lm_head": st["ms_lm_head"] / max(1, st["n_lm_head"]) * 1e3},
         }
+        # Eq. 1 (reading Q12): t_maxload = N_G t^M + (N_G - 1) t^W; the method is I/O-bound
+        # when one expert's load takes longer ("compare it with t^maxload")
+        ng = max(1, n // 2)
+        t_M = st["ms_router"] / max(1, st["n_router"]) * 1e3
+        t_W = gemv_ms * 1e3 * (2 if n == 1 else 1)
+        t_load = EXPERT_BYTES / (link_all / n * 1e9) * 1e6 * (2 if n == 1 else 1)
+        t_max = ng * t_M + (ng - 1) * t_W
+        line["eq1"] = {"N_G": ng, "t_M_us": t_M, "t_W_us": t_W, "t_load_us": t_load, "t_maxload_us": t_max,
+                       "io_bottlenecked": t_load > t_max,
+                       "note": "t^M = router kernel, t^W = expert GEMVs of one GPU for one layer (CUDA events); "
+                               "t_load = that GPU's expert bytes per layer / measured H2D GB/s"}
         if prefill is not None:
             line["prefill"] = prefill
         if res is not None:

@@ -134,6 +134,7 @@ struct Ctx {
   int32_t* h_ref = nullptr;             // pinned [L][4][k]
   int ref_next = 0;                     // next refinement to apply (host, this step)
   std::vector<int32_t> predA_tbl;       // [L][k] Mode A predictions (the paper's SEP: recall Eq. 3)
+  std::vector<char> predA_ready;        // [L] Mode A prediction of layer l copied to predA_tbl
   std::vector<int32_t> predB_tbl;       // [L][k] refined predictions (-1 = none)
 
   // PERFECT predictor: routing recorded per input token (Mode A: routing is a function of the

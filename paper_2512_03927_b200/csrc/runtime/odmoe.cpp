@@ -419,6 +419,7 @@ void build_buffers(Ctx* c) {
     }
   }
   c->predA_tbl.assign((size_t)L * k, -1);
+  c->predA_ready.assign(L, 0);
   c->predB_tbl.assign((size_t)L * k, -1);
   if (c->cfg.debug_capture && c->rank == 0) {
     c->dbg_h = dmalloc<float>(c, (size_t)L * d, "dbg_h");
@@ -493,26 +494,28 @@ void enqueue_pred_broadcast(Ctx* c) {
   }
 }
 
-// Prediction for layer m available on the host? (non-blocking)
+// Prediction for layer m available on the host? (non-blocking). Mode A (token-start shadow)
+// results are copied to predA_tbl as their events complete; the plan (pred_tbl) takes Mode A
+// unless a refined prediction for that layer already arrived.
 bool pred_available(Ctx* c, int m) {
   if (!c->pred_valid) return false;
-  if (c->pred_ready[m]) return true;
   const int p = c->cfg.predictor;
-  if (p == ODMOE_PRED_SHADOW_INT8 || p == ODMOE_PRED_SHADOW_SAME) {
+  if ((p == ODMOE_PRED_SHADOW_INT8 || p == ODMOE_PRED_SHADOW_SAME) && !c->predA_ready[m]) {
     const int evl = c->world == 1 ? m : (m / c->pred_chunk) * c->pred_chunk;
     const cudaError_t q = cudaEventQuery(c->ev_pred[evl]);
-    if (q == cudaErrorNotReady) return false;
+    if (q == cudaErrorNotReady) return c->pred_ready[m] != 0;
     CUDA_OK(c, q);
     const int hi = c->world == 1 ? m + 1 : std::min(c->L, evl + c->pred_chunk);
     for (int l = evl; l < hi; ++l) {
-      c->pred_ready[l] = 1;
+      c->predA_ready[l] = 1;
       std::copy(c->h_pred + (size_t)l * c->k, c->h_pred + (size_t)(l + 1) * c->k, c->predA_tbl.begin() + (size_t)l * c->k);
-      if (c->predB_tbl[(size_t)l * c->k] < 0)  // a refined prediction, if any, supersedes Mode A
+      if (c->predB_tbl[(size_t)l * c->k] < 0) {  // a refined prediction, if any, supersedes Mode A
         std::copy(c->h_pred + (size_t)l * c->k, c->h_pred + (size_t)(l + 1) * c->k, c->pred_tbl.begin() + (size_t)l * c->k);
+        c->pred_ready[l] = 1;
+      }
     }
-    return true;
   }
-  return false;
+  return c->pred_ready[m] != 0;
 }
 
 // RANDOM predictor (P:256 case 5): k distinct uniform experts from splitmix64(aux_seed, step, l).
@@ -662,6 +665,7 @@ void apply_refinements(Ctx* c) {
       int32_t* B = c->predB_tbl.data() + (size_t)m * k;
       std::copy(P, P + k, B);
       if (m <= c->l_cur) continue;  // that layer's router already decided
+      pred_available(c, m);          // compare against Mode A's prediction if it has arrived
       int32_t* plan = c->pred_tbl.data() + (size_t)m * k;
       bool same = c->pred_ready[m] != 0;
       for (int a = 0; a < k && same; ++a) {
@@ -734,6 +738,7 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
   std::fill(c->pred_ready.begin(), c->pred_ready.end(), 0);
   std::fill(c->pred_tbl.begin(), c->pred_tbl.end(), -1);
   std::fill(c->predA_tbl.begin(), c->predA_tbl.end(), -1);
+  std::fill(c->predA_ready.begin(), c->predA_ready.end(), 0);
   std::fill(c->predB_tbl.begin(), c->predB_tbl.end(), -1);
   const bool shadow_pred = p == ODMOE_PRED_SHADOW_INT8 || p == ODMOE_PRED_SHADOW_SAME;
   c->R = (!c->resident && shadow_pred) ? c->cfg.refine_depth : 0;
