@@ -92,10 +92,17 @@ struct FlatArgs {
   int evict_first;       // L2 policy of the weight stream
 };
 
-template <typename WT, typename XT, int MODE, int UNROLL>
-__global__ void __launch_bounds__(kFG_THREADS, 1) flat_gemv_kernel(const FlatArgs a) {
+struct PdlWait {
+  __device__ __forceinline__ void operator()() const { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+};
+
+// One streaming pass (see the file comment). `wait_dep` is called once the data this pass consumes
+// from earlier work may be read: griddepcontrol.wait (PDL) for a stand-alone launch, a grid-wide
+// barrier for the W2 phase of the fused expert kernel. Weights are prefetched before it.
+template <typename WT, typename XT, int MODE, int UNROLL, typename WaitFn>
+__device__ __forceinline__ void flat_phase(const FlatArgs& a, uint8_t* sm, const WaitFn& wait_dep,
+                                           bool ids_ready = false) {
   constexpr int N = FDot<WT, XT>::kN;
-  extern __shared__ __align__(128) uint8_t sm[];
   float* part = reinterpret_cast<float*>(sm);                          // [warps][rows_cap]
   XT* xs = reinterpret_cast<XT*>(part + kFG_WARPS * a.rows_cap);       // [C]
   __shared__ float red[kFG_WARPS + 1];
@@ -106,7 +113,8 @@ __global__ void __launch_bounds__(kFG_THREADS, 1) flat_gemv_kernel(const FlatArg
   // Indirect experts are chosen by the PREVIOUS kernel's router output: wait for it (PDL) before
   // reading the ids. Direct weights do not depend on it and are prefetched first (below).
   const bool indirect = a.ex.tbl != nullptr;
-  if (indirect) asm volatile("griddepcontrol.wait;" ::: "memory");
+  const bool early = indirect && !ids_ready;  // the expert ids come from the previous kernel
+  if (early) wait_dep();
   const WT* W;
   const float* sc;
   int gate_idx;
@@ -151,7 +159,7 @@ __global__ void __launch_bounds__(kFG_THREADS, 1) flat_gemv_kernel(const FlatArg
 #pragma unroll
   for (int i = 0; i < UNROLL; ++i)
     if (g_begin + i < g_end) wa[i] = ld_stream_pol(base + (g_begin + i) * 32 + lane, pol);
-  if (!indirect) asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (!early) wait_dep();
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   // stage activations (MODE 2: RMSNorm of h first) and zero the partials
@@ -288,6 +296,42 @@ __global__ void __launch_bounds__(kFG_THREADS, 1) flat_gemv_kernel(const FlatArg
   }
 }
 
+template <typename WT, typename XT, int MODE, int UNROLL>
+__global__ void __launch_bounds__(kFG_THREADS, 1) flat_gemv_kernel(const FlatArgs a) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  flat_phase<WT, XT, MODE, UNROLL>(a, sm, PdlWait{});
+}
+
+// Grid-wide barrier for a cooperative launch (all CTAs co-resident): one arrival counter per
+// launch slot; `target` grows by gridDim.x every launch so the counter never needs resetting.
+struct GridBarrier {
+  unsigned int* counter;
+  unsigned int target;
+  __device__ __forceinline__ void operator()() const {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(counter, 1u);
+      unsigned int v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
+      } while ((int)(v - target) < 0);
+    }
+    __syncthreads();
+  }
+};
+
+// Fused expert FFN: phase 1 = W13 + SwiGLU -> a (global), grid barrier, phase 2 = W2 + gate -> y.
+// One launch per expert; phase 2's first weight batches are in flight before the barrier.
+template <typename WT, typename XT, int UNROLL>
+__global__ void __launch_bounds__(kFG_THREADS, 1)
+flat_expert_kernel(const FlatArgs a13, const FlatArgs a2, unsigned int* counter, unsigned int target) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  flat_phase<WT, XT, 0, UNROLL>(a13, sm, PdlWait{});
+  __syncthreads();
+  flat_phase<WT, float, 1, UNROLL>(a2, sm, GridBarrier{counter, target}, /*ids_ready=*/true);
+}
+
 template <typename WT, typename XT, int MODE>
 static cudaError_t fg_launch(FlatArgs a, cudaStream_t s, bool pdl) {
   constexpr int UNROLL = 8;
@@ -359,6 +403,81 @@ cudaError_t launch_lm_head_flat(const float* h, const void* W, WType wt, int V, 
     case W_F32: return fg_launch<float, float, 2>(a, s, pdl);
     default: return cudaErrorInvalidValue;
   }
+}
+
+// ---------------------------------------------------------------- fused expert FFN launcher
+template <typename WT, typename XT>
+static cudaError_t fused_launch(FlatArgs a13, FlatArgs a2, cudaStream_t s, bool pdl) {
+  constexpr int UNROLL = 8;
+  static unsigned int* counters = nullptr;  // one per device
+  static unsigned int epochs[64] = {0};
+  static unsigned int* dev_counters[64] = {nullptr};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!dev_counters[dev]) {
+    cudaError_t e = cudaMalloc(&dev_counters[dev], sizeof(unsigned int));
+    if (e != cudaSuccess) return e;
+    e = cudaMemset(dev_counters[dev], 0, sizeof(unsigned int));
+    if (e != cudaSuccess) return e;
+  }
+  (void)counters;
+  static int ef = -1;
+  if (ef < 0) {
+    const char* e = getenv("ODMOE_L2_EVICT_FIRST");
+    ef = (e && e[0] == '0') ? 0 : 1;
+  }
+  a13.evict_first = a2.evict_first = ef;
+  const int sms = num_sms();
+  long long units = a13.R / 2 < a2.R ? a13.R / 2 : a2.R;
+  const int grid = (int)(units < sms ? (units > 0 ? units : 1) : sms);
+  a13.rows_cap = (int)((a13.R / 2 + grid - 1) / grid) * 2 + 2;
+  a2.rows_cap = (int)((a2.R + grid - 1) / grid) + 2;
+  const size_t s1 = (size_t)kFG_WARPS * a13.rows_cap * sizeof(float) + (size_t)a13.C * sizeof(XT) + 16;
+  const size_t s2 = (size_t)kFG_WARPS * a2.rows_cap * sizeof(float) + (size_t)a2.C * sizeof(float) + 16;
+  const size_t smem = s1 > s2 ? s1 : s2;
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  auto kern = flat_expert_kernel<WT, XT, UNROLL>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  // Stream-ordered launches on this device use increasing barrier targets. Only ONE stream may
+  // run these kernels (the engine's compute stream): two cooperative kernels spinning on barriers
+  // on different streams could hold each other's SMs.
+  const unsigned int target = epochs[dev] + (unsigned int)grid;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kFG_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 2 : 1;
+  e = cudaLaunchKernelEx(&cfg, kern, a13, a2, dev_counters[dev], target);
+  if (e == cudaSuccess) epochs[dev] = target;
+  return e;
+}
+
+cudaError_t launch_expert_fused(ExpertRef ex, const void* w2_direct, const float* s2_direct, WType wt,
+                                const void* u, int u_f32, float* a_buf, const float* gate_w, float* y, int d,
+                                int F, cudaStream_t s, bool pdl) {
+  FlatArgs a13{}, a2{};
+  a13.ex = ex; a13.second = 0; a13.x = u; a13.x_bf16 = !u_f32; a13.R = 2 * F; a13.C = d; a13.out = a_buf;
+  a13.d_full = d; a13.F_full = F;
+  a2.ex = ex; a2.second = 1; a2.x = a_buf; a2.x_bf16 = 0; a2.R = d; a2.C = F; a2.gate_w = gate_w; a2.out = y;
+  a2.d_full = d; a2.F_full = F;
+  if (ex.tbl == nullptr) {  // direct: W2 has its own pointer
+    a2.ex.blob = w2_direct;
+    a2.ex.scales = s2_direct;
+  }
+  switch (wt) {
+    case W_BF16: return fused_launch<__nv_bfloat16, uint16_t>(a13, a2, s, pdl);
+    case W_F32: return fused_launch<float, float>(a13, a2, s, pdl);
+    case W_I8: return fused_launch<int8_t, uint16_t>(a13, a2, s, pdl);
+  }
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace odmoe

@@ -217,6 +217,15 @@ cudaError_t launch_w2(ExpertRef ex, WType wt, const float* a, const float* gate_
   return cudaErrorInvalidValue;
 }
 
+bool use_fused_expert() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ODMOE_FUSED");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1 && gemv_engine() == 2;
+}
+
 int num_sms() {
   static int cached[64] = {0};
   int dev = 0;

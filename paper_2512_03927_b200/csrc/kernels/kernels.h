@@ -54,6 +54,13 @@ cudaError_t launch_w2_flat(ExpertRef ex, WType wt, const float* act, const float
                            int F, cudaStream_t s, bool pdl);
 cudaError_t launch_lm_head_flat(const float* h, const void* W, WType wt, int V, int d, float eps,
                                 int32_t* token_out, float* logits, void* scratch, cudaStream_t s, bool pdl);
+bool use_fused_expert();  // env ODMOE_FUSED=0 disables (A/B)
+// Fused expert FFN (flat engine): W13+SwiGLU -> grid barrier -> W2+gate in ONE cooperative
+// launch. Direct mode: ex.blob/ex.scales = W13 (+ scales), w2_direct/s2_direct = W2 (+ scales);
+// indirect mode: the expert table entries (whole blobs). a_buf: fp32 [F] scratch.
+cudaError_t launch_expert_fused(ExpertRef ex, const void* w2_direct, const float* s2_direct, WType wt,
+                                const void* u, int u_f32, float* a_buf, const float* gate_w, float* y, int d,
+                                int F, cudaStream_t s, bool pdl);
 // TMA-bulk streaming variants (stream_gemv.cu), used when stream_ok(wt, row length).
 bool stream_ok(WType wt, int C);
 cudaError_t launch_w13_stream(ExpertRef ex, WType wt, const void* u, int u_f32, float* a, int d, int F,

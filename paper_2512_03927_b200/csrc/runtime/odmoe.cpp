@@ -727,6 +727,8 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
   const int p = c->cfg.predictor;
   const bool r0 = c->rank == 0;
   const int u_f32 = c->wt == W_F32;
+  // fused W13->W2 cooperative kernel on the compute stream only (never on the shadow stream)
+  const bool fused = use_fused_expert() && stream_ok(c->wt, d) && stream_ok(c->wt, F);
 
   // token in (pinned -> device); the previous step's shadow must be done with d_tok_in
   c->h_tok[0] = token_in;
@@ -752,9 +754,6 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
         enqueue_shadow(c, c->d_tok_in);
       }
       if (c->world > 1) enqueue_pred_broadcast(c);
-      // receivers enqueue every refinement delivery now (same collective order as rank 0)
-      if (c->world > 1 && !r0 && c->R > 0)
-        for (int j = 0; j < L - 1; ++j) enqueue_refine_delivery(c, j);
       c->pred_valid = true;
     } else if (p == ODMOE_PRED_RANDOM) {
       for (int l = 0; l < L; ++l) random_prediction(c, c->step, l, c->pred_tbl.data() + (size_t)l * k);
@@ -786,6 +785,10 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
   int n_add = 0;
   for (int l = 0; l < L; ++l) {
     c->l_cur = l;
+    // Receivers enqueue refinement l's broadcast only now, after their layer l-1 reduce: a receive
+    // that spins on the shadow stream must never sit (in a shared hardware queue) in front of the
+    // layer traffic rank 0 needs before it can send it. Same comm_pred order as rank 0.
+    if (c->world > 1 && !r0 && c->R > 0 && l < L - 1) enqueue_refine_delivery(c, l);
     char* pkt = c->d_pkt + (size_t)l * c->pkt_bytes;
     int32_t* ids_dev = (int32_t*)(pkt + c->pkt_ids_off);
     float* w_dev = (float*)(pkt + c->pkt_w_off);
@@ -814,8 +817,13 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
           ExpertRef ex{nullptr, nullptr, (const void* const*)c->d_res_tbl, nullptr, ids_dev,
                        c->world == 1 ? j : c->my_pos, l * E, k, c->world == 1 ? 0 : 1};
           float* y = c->d_y + (size_t)j * d;
-          { KTimer t(c, K_W13, s); CUDA_OK(c, launch_w13(ex, c->wt, pkt, u_f32, c->d_a + (size_t)j * F, d, F, s, true)); }
-          { KTimer t(c, K_W2, s); CUDA_OK(c, launch_w2(ex, c->wt, c->d_a + (size_t)j * F, w_dev, y, d, F, s, true)); }
+          if (fused) {
+            KTimer t(c, K_W13, s);
+            CUDA_OK(c, launch_expert_fused(ex, nullptr, nullptr, c->wt, pkt, u_f32, c->d_a + (size_t)j * F, w_dev, y, d, F, s, true));
+          } else {
+            { KTimer t(c, K_W13, s); CUDA_OK(c, launch_w13(ex, c->wt, pkt, u_f32, c->d_a + (size_t)j * F, d, F, s, true)); }
+            { KTimer t(c, K_W2, s); CUDA_OK(c, launch_w2(ex, c->wt, c->d_a + (size_t)j * F, w_dev, y, d, F, s, true)); }
+          }
           if (c->dbg_ypart) CUDA_OK(c, cudaMemcpyAsync(c->dbg_ypart + ((size_t)l * k + j) * d, y, sizeof(float) * d, cudaMemcpyDeviceToDevice, s));
         }
       }
@@ -878,10 +886,17 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
           float* y = c->d_y + (size_t)ypos * d;
           ExpertRef e13 = direct_ref(sl.dev, nullptr, j);
           ExpertRef e2 = direct_ref(sl.dev + c->w13_bytes, nullptr, j);
-          CUDA_OK(c, cudaStreamWaitEvent(s, sl.ev_w13, 0));
-          { KTimer t(c, K_W13, s); CUDA_OK(c, launch_w13(e13, c->wt, pkt, u_f32, c->d_a + (size_t)ypos * F, d, F, s)); }
-          CUDA_OK(c, cudaStreamWaitEvent(s, sl.ev_done, 0));
-          { KTimer t(c, K_W2, s); CUDA_OK(c, launch_w2(e2, c->wt, c->d_a + (size_t)ypos * F, w_dev, y, d, F, s)); }
+          if (fused) {  // one launch once the whole blob has landed
+            CUDA_OK(c, cudaStreamWaitEvent(s, sl.ev_done, 0));
+            KTimer t(c, K_W13, s);
+            CUDA_OK(c, launch_expert_fused(e13, sl.dev + c->w13_bytes, nullptr, c->wt, pkt, u_f32, c->d_a + (size_t)ypos * F,
+                                           w_dev, y, d, F, s, false));
+          } else {  // W13 starts as soon as its part has landed, W2 after the rest
+            CUDA_OK(c, cudaStreamWaitEvent(s, sl.ev_w13, 0));
+            { KTimer t(c, K_W13, s); CUDA_OK(c, launch_w13(e13, c->wt, pkt, u_f32, c->d_a + (size_t)ypos * F, d, F, s)); }
+            CUDA_OK(c, cudaStreamWaitEvent(s, sl.ev_done, 0));
+            { KTimer t(c, K_W2, s); CUDA_OK(c, launch_w2(e2, c->wt, c->d_a + (size_t)ypos * F, w_dev, y, d, F, s)); }
+          }
           // evict right after use: the slot is reusable once this event fires (Q16)
           CUDA_OK(c, cudaEventRecord(sl.ev_free, s));
           sl.free_recorded = true;
@@ -1616,6 +1631,9 @@ odmoe_status odmoe_expert_ffn(const void* w13, const void* w2, const void* u, co
       (dt != ODMOE_BF16 && dt != ODMOE_FP32))
     return ODMOE_E_CONFIG;
   const WType wt = wtype(dt);
+  if (use_fused_expert() && stream_ok(wt, d) && stream_ok(wt, F))
+    return launch_expert_fused(direct_ref(w13, nullptr, gate_idx), w2, nullptr, wt, u, dt == ODMOE_FP32, a_scratch,
+                               gate_w, y, d, F, S(stream), false) == cudaSuccess ? ODMOE_OK : ODMOE_E_CUDA;
   if (launch_w13(direct_ref(w13, nullptr, gate_idx), wt, u, dt == ODMOE_FP32, a_scratch, d, F, S(stream)) != cudaSuccess)
     return ODMOE_E_CUDA;
   if (launch_w2(direct_ref(w2, nullptr, gate_idx), wt, a_scratch, gate_w, y, d, F, S(stream)) != cudaSuccess)
@@ -1672,6 +1690,9 @@ odmoe_status odmoe_shadow_expert_ffn(const int8_t* q13, const float* s13, const 
                                      void* stream) {
   if (!q13 || !s13 || !q2 || !s2 || !u || !a_scratch || !y || d < 16 || F < 16 || d % 16 || F % 16 || gate_idx < 0)
     return ODMOE_E_CONFIG;
+  if (use_fused_expert() && stream_ok(W_I8, d) && stream_ok(W_I8, F))
+    return launch_expert_fused(direct_ref(q13, s13, gate_idx), q2, s2, W_I8, u, 0, a_scratch, gate_w, y, d, F,
+                               S(stream), false) == cudaSuccess ? ODMOE_OK : ODMOE_E_CUDA;
   if (launch_w13(direct_ref(q13, s13, gate_idx), W_I8, u, 0, a_scratch, d, F, S(stream)) != cudaSuccess)
     return ODMOE_E_CUDA;
   if (launch_w2(direct_ref(q2, s2, gate_idx), W_I8, a_scratch, gate_w, y, d, F, S(stream)) != cudaSuccess)
