@@ -34,9 +34,15 @@ __device__ __forceinline__ uint4 ld_stream(const void* p) {
 // displacing other L2 lines (e.g. dirty lines just written by the H2D copy engine).
 __device__ __forceinline__ uint4 ld_stream_pol(const void* p, uint64_t pol) {
   uint4 r;
+#ifdef FG_NOPF
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p), "l"(pol));
+#else
   asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                : "l"(p), "l"(pol));
+#endif
   return r;
 }
 __device__ __forceinline__ uint64_t l2_policy(bool evict_first) {

@@ -15,6 +15,15 @@
 namespace odmoe {
 
 constexpr int kFG_WARPS = 16;
+#ifndef FG_PIPE
+#define FG_PIPE 0  // register pipeline variant (0: 2 batches, load-then-consume; 1: 2 batches
+                   // prefetched before the wait; 2: 3 batches of UNROLL 6), see profiles/kbench_r01_*
+#endif
+#if FG_PIPE == 2
+constexpr int kFG_UNROLL = 6;
+#else
+constexpr int kFG_UNROLL = 8;
+#endif
 constexpr int kFG_THREADS = kFG_WARPS * 32;
 
 template <typename WT, typename XT> struct FDot;
@@ -149,16 +158,34 @@ __device__ __forceinline__ void flat_phase(const FlatArgs& a, uint8_t* sm, const
   const int Gr = Cg / 32;                 // 512-byte groups per row
   const long long G = (long long)nrows * Gr;
   // this warp's slice of groups
+#if FG_PIPE == 3
+  // interleaved: warp w takes batches w, w + 16, ... of UNROLL groups -> one sequential stream per SM
+  const long long g_begin = (long long)warp * UNROLL, g_end = G;
+#else
   const long long g_begin = G * warp / kFG_WARPS, g_end = G * (warp + 1) / kFG_WARPS;
+#endif
   const uint4* base = reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(W) + rb * (long long)a.C * sizeof(WT));
 
   // The weights do not depend on the previous kernel: issue this warp's first batch before the
   // programmatic-dependent-launch wait (no-op without PDL), then stage the activations.
   const uint64_t pol = l2_policy(a.evict_first != 0);
   uint4 wa[UNROLL], wb[UNROLL];
+#if FG_PIPE == 2
+  uint4 wc[UNROLL];
+#endif
 #pragma unroll
   for (int i = 0; i < UNROLL; ++i)
     if (g_begin + i < g_end) wa[i] = ld_stream_pol(base + (g_begin + i) * 32 + lane, pol);
+#if FG_PIPE >= 1
+#pragma unroll
+  for (int i = 0; i < UNROLL; ++i)
+    if (g_begin + UNROLL + i < g_end) wb[i] = ld_stream_pol(base + (g_begin + UNROLL + i) * 32 + lane, pol);
+#endif
+#if FG_PIPE == 2
+#pragma unroll
+  for (int i = 0; i < UNROLL; ++i)
+    if (g_begin + 2 * UNROLL + i < g_end) wc[i] = ld_stream_pol(base + (g_begin + 2 * UNROLL + i) * 32 + lane, pol);
+#endif
   if (!early) wait_dep();
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
@@ -193,8 +220,18 @@ __device__ __forceinline__ void flat_phase(const FlatArgs& a, uint8_t* sm, const
       const uint16_t* s16 = reinterpret_cast<const uint16_t*>(a.x);
       for (int i = tid; i < a.C; i += kFG_THREADS) xs[i] = __uint_as_float((uint32_t)s16[i] << 16);
     } else {
+      // all loads of a thread first (latency-bound otherwise: 57 KB per CTA for W2)
       const float4* s4 = reinterpret_cast<const float4*>(a.x);
-      for (int i = tid; i < a.C / 4; i += kFG_THREADS) reinterpret_cast<float4*>(xs)[i] = s4[i];
+      const int n4 = a.C / 4;
+      for (int i0 = tid; i0 < n4; i0 += 8 * kFG_THREADS) {
+        float4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (i0 + u * kFG_THREADS < n4) v[u] = s4[i0 + u * kFG_THREADS];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (i0 + u * kFG_THREADS < n4) reinterpret_cast<float4*>(xs)[i0 + u * kFG_THREADS] = v[u];
+      }
     }
   }
   for (int i = tid; i < kFG_WARPS * a.rows_cap; i += kFG_THREADS) part[i] = 0.f;
@@ -219,6 +256,34 @@ __device__ __forceinline__ void flat_phase(const FlatArgs& a, uint8_t* sm, const
       }
     }
   };
+#if FG_PIPE == 3
+  {
+    // two batches in flight; batch b covers groups [b0, b0 + UNROLL) with b0 = (w + 16 i) * UNROLL
+    constexpr long long STEP = (long long)kFG_WARPS * UNROLL;
+    auto consume_at = [&](const uint4 (&wv)[UNROLL], long long g0) {
+      row = (int)(g0 / Gr);
+      gcol = (int)(g0 - (long long)row * Gr);
+      consume(wv, g0);
+      if (gcol != 0) {  // batch ended inside a row: flush the partial now (rows are shared by warps)
+        const float t = warp_sum(acc);
+        if (lane == 0) part[warp * a.rows_cap + row] += t;
+        acc = 0.f;
+      }
+    };
+    for (long long g0 = g_begin; g0 < g_end; g0 += 2 * STEP) {
+      const long long g1 = g0 + STEP, g2 = g0 + 2 * STEP;
+#pragma unroll
+      for (int i = 0; i < UNROLL; ++i)
+        if (g1 + i < g_end) wb[i] = ld_stream_pol(base + (g1 + i) * 32 + lane, pol);
+      consume_at(wa, g0);
+#pragma unroll
+      for (int i = 0; i < UNROLL; ++i)
+        if (g2 + i < g_end) wa[i] = ld_stream_pol(base + (g2 + i) * 32 + lane, pol);
+      if (g1 < g_end) consume_at(wb, g1);
+    }
+    gcol = 0;  // everything flushed
+  }
+#elif FG_PIPE == 0
   // software pipeline, two register batches in flight: load batch n+1, then consume batch n
   for (long long g0 = g_begin; g0 < g_end; g0 += 2 * UNROLL) {
     const long long g1 = g0 + UNROLL, g2 = g0 + 2 * UNROLL;
@@ -231,6 +296,37 @@ __device__ __forceinline__ void flat_phase(const FlatArgs& a, uint8_t* sm, const
       if (g2 + i < g_end) wa[i] = ld_stream_pol(base + (g2 + i) * 32 + lane, pol);
     if (g1 < g_end) consume(wb, g1);
   }
+#elif FG_PIPE == 1
+  // both batches issued before the dependency wait; consume one, re-issue it two batches ahead
+  for (long long g0 = g_begin; g0 < g_end; g0 += 2 * UNROLL) {
+    const long long g1 = g0 + UNROLL, g2 = g0 + 2 * UNROLL, g3 = g0 + 3 * UNROLL;
+    consume(wa, g0);
+#pragma unroll
+    for (int i = 0; i < UNROLL; ++i)
+      if (g2 + i < g_end) wa[i] = ld_stream_pol(base + (g2 + i) * 32 + lane, pol);
+    if (g1 < g_end) consume(wb, g1);
+#pragma unroll
+    for (int i = 0; i < UNROLL; ++i)
+      if (g3 + i < g_end) wb[i] = ld_stream_pol(base + (g3 + i) * 32 + lane, pol);
+  }
+#else
+  // three register batches: two stay in flight while one is consumed
+  for (long long g0 = g_begin; g0 < g_end; g0 += 3 * UNROLL) {
+    const long long g1 = g0 + UNROLL, g2 = g0 + 2 * UNROLL;
+    consume(wa, g0);
+#pragma unroll
+    for (int i = 0; i < UNROLL; ++i)
+      if (g0 + 3 * UNROLL + i < g_end) wa[i] = ld_stream_pol(base + (g0 + 3 * UNROLL + i) * 32 + lane, pol);
+    if (g1 < g_end) consume(wb, g1);
+#pragma unroll
+    for (int i = 0; i < UNROLL; ++i)
+      if (g0 + 4 * UNROLL + i < g_end) wb[i] = ld_stream_pol(base + (g0 + 4 * UNROLL + i) * 32 + lane, pol);
+    if (g2 < g_end) consume(wc, g2);
+#pragma unroll
+    for (int i = 0; i < UNROLL; ++i)
+      if (g0 + 5 * UNROLL + i < g_end) wc[i] = ld_stream_pol(base + (g0 + 5 * UNROLL + i) * 32 + lane, pol);
+  }
+#endif
   if (gcol != 0) {  // slice ended inside a row
     const float t = warp_sum(acc);
     if (lane == 0) part[warp * a.rows_cap + row] += t;
@@ -334,7 +430,7 @@ flat_expert_kernel(const FlatArgs a13, const FlatArgs a2, unsigned int* counter,
 
 template <typename WT, typename XT, int MODE>
 static cudaError_t fg_launch(FlatArgs a, cudaStream_t s, bool pdl) {
-  constexpr int UNROLL = 8;
+  constexpr int UNROLL = kFG_UNROLL;
   static int ef = -1;
   if (ef < 0) {
     const char* e = getenv("ODMOE_L2_EVICT_FIRST");
@@ -408,7 +504,7 @@ cudaError_t launch_lm_head_flat(const float* h, const void* W, WType wt, int V, 
 // ---------------------------------------------------------------- fused expert FFN launcher
 template <typename WT, typename XT>
 static cudaError_t fused_launch(FlatArgs a13, FlatArgs a2, cudaStream_t s, bool pdl) {
-  constexpr int UNROLL = 8;
+  constexpr int UNROLL = kFG_UNROLL;
   static unsigned int* counters = nullptr;  // one per device
   static unsigned int epochs[64] = {0};
   static unsigned int* dev_counters[64] = {nullptr};

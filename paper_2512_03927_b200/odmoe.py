@@ -11,7 +11,7 @@ import os
 from typing import Optional, Sequence
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libodmoe.so")
+LIB_PATH = os.environ.get("ODMOE_LIB") or os.path.join(_HERE, "libodmoe.so")
 
 BF16, FP32 = 0, 1
 PRED_SHADOW_INT8, PRED_NONE, PRED_RANDOM, PRED_PERFECT, PRED_SHADOW_SAME = 0, 1, 2, 3, 4
