@@ -15,6 +15,9 @@
 namespace odmoe {
 
 constexpr int kFG_WARPS = 16;
+#ifndef FG_NO_F32X2
+#define FG_F32X2 1  // packed fp32x2 FMA/ADD (sm_100 FFMA2/FADD2) in the bf16-x and INT8 dot products
+#endif
 #ifndef FG_PIPE
 #define FG_PIPE 0  // register pipeline variant (0: 2 batches, load-then-consume; 1: 2 batches
                    // prefetched before the wait; 2: 3 batches of UNROLL 6), see profiles/kbench_r01_*
@@ -39,6 +42,32 @@ template <> struct FDot<int8_t, float> {
   static constexpr int kN = 16;
   __device__ __forceinline__ static float run(const uint4& w, const float* x) { return dot16<int8_t>(w, x); }
 };
+#ifdef FG_F32X2
+// Packed fp32x2 arithmetic (sm_100 FFMA2 / FADD2): one instruction per element PAIR.
+typedef unsigned long long f2_t;
+__device__ __forceinline__ f2_t f2_pack(float lo, float hi) {
+  f2_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ f2_t f2_fma(f2_t a, f2_t b, f2_t c) {
+  f2_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ f2_t f2_add(f2_t a, f2_t b) {
+  f2_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ float f2_sum(f2_t a) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a));
+  return lo + hi;
+}
+__device__ __forceinline__ f2_t bf2_unpack(uint32_t v) { return f2_pack(bf16_lo(v), bf16_hi(v)); }
+#endif
+
 __device__ __forceinline__ float fbf2(uint32_t w, uint32_t x, float s) {
   s = fmaf(bf16_lo(w), bf16_lo(x), s);
   return fmaf(bf16_hi(w), bf16_hi(x), s);
@@ -47,6 +76,13 @@ template <> struct FDot<__nv_bfloat16, uint16_t> {
   static constexpr int kN = 8;
   __device__ __forceinline__ static float run(const uint4& w, const uint16_t* x) {
     const uint4 xv = *reinterpret_cast<const uint4*>(x);
+#ifdef FG_F32X2
+    f2_t s = f2_fma(bf2_unpack(w.x), bf2_unpack(xv.x), 0ull);
+    s = f2_fma(bf2_unpack(w.y), bf2_unpack(xv.y), s);
+    s = f2_fma(bf2_unpack(w.z), bf2_unpack(xv.z), s);
+    s = f2_fma(bf2_unpack(w.w), bf2_unpack(xv.w), s);
+    return f2_sum(s);
+#endif
     // two independent chains (even/odd words) for ILP
     float s0 = bf16_lo(w.x) * bf16_lo(xv.x);
     float s1 = bf16_lo(w.y) * bf16_lo(xv.y);
@@ -64,11 +100,31 @@ __device__ __forceinline__ float fi8(uint32_t word, uint32_t x01, uint32_t x23, 
   s = fmaf(i8_to_f32(b, 2), bf16_lo(x23), s);
   return fmaf(i8_to_f32(b, 3), bf16_hi(x23), s);
 }
+#ifdef FG_F32X2
+// 4 int8 of one word -> two fp32 pairs (exact: byte into the mantissa of 2^23, one FADD2 per pair)
+__device__ __forceinline__ f2_t i8x4_dot2(uint32_t word, uint32_t x01, uint32_t x23, f2_t s) {
+  const uint32_t b = word ^ 0x80808080u;
+  const f2_t m = f2_pack(-8388736.0f, -8388736.0f);
+  const f2_t q01 = f2_add(f2_pack(__uint_as_float(__byte_perm(b, 0x4B000000u, 0x7540)),
+                                  __uint_as_float(__byte_perm(b, 0x4B000000u, 0x7541))), m);
+  const f2_t q23 = f2_add(f2_pack(__uint_as_float(__byte_perm(b, 0x4B000000u, 0x7542)),
+                                  __uint_as_float(__byte_perm(b, 0x4B000000u, 0x7543))), m);
+  s = f2_fma(q01, bf2_unpack(x01), s);
+  return f2_fma(q23, bf2_unpack(x23), s);
+}
+#endif
 template <> struct FDot<int8_t, uint16_t> {
   static constexpr int kN = 16;
   __device__ __forceinline__ static float run(const uint4& w, const uint16_t* x) {
     const uint4 x0 = *reinterpret_cast<const uint4*>(x);
     const uint4 x1 = *reinterpret_cast<const uint4*>(x + 8);
+#ifdef FG_F32X2
+    f2_t s = i8x4_dot2(w.x, x0.x, x0.y, 0ull);
+    s = i8x4_dot2(w.y, x0.z, x0.w, s);
+    s = i8x4_dot2(w.z, x1.x, x1.y, s);
+    s = i8x4_dot2(w.w, x1.z, x1.w, s);
+    return f2_sum(s);
+#endif
     float s0 = fi8(w.x, x0.x, x0.y, 0.f);
     float s1 = fi8(w.y, x0.z, x0.w, 0.f);
     s0 = fi8(w.z, x1.x, x1.y, s0);
