@@ -61,7 +61,9 @@ typedef enum {
   ODMOE_PRED_NONE = 1,        /* load only after the main router (P:257 case 6)                         */
   ODMOE_PRED_RANDOM = 2,      /* uniformly random k experts per layer (P:256 case 5; E[recall] = k/E)    */
   ODMOE_PRED_PERFECT = 3,     /* replay of the true routing recorded by an earlier run of the same ctx   */
-  ODMOE_PRED_SHADOW_SAME = 4  /* shadow with the main model's own weights (recall must be exactly 1.0)   */
+  ODMOE_PRED_SHADOW_SAME = 4, /* shadow with the main model's own weights (recall must be exactly 1.0)   */
+  ODMOE_PRED_GATE_REUSE = 5   /* prior work: after the main router of layer l,
+                                 apply the gates of layers l+1..l+D to layer l's normalised input   */
 } odmoe_predictor;
 
 typedef struct {

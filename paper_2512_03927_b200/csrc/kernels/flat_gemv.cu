@@ -14,7 +14,10 @@
 
 namespace odmoe {
 
-constexpr int kFG_WARPS = 16;
+#ifndef FG_WARPS
+#define FG_WARPS 16
+#endif
+constexpr int kFG_WARPS = FG_WARPS;
 #ifndef FG_NO_F32X2
 #define FG_F32X2 1  // packed fp32x2 FMA/ADD (sm_100 FFMA2/FADD2) in the bf16-x and INT8 dot products
 #endif
@@ -22,7 +25,9 @@ constexpr int kFG_WARPS = 16;
 #define FG_PIPE 0  // register pipeline variant (0: 2 batches, load-then-consume; 1: 2 batches
                    // prefetched before the wait; 2: 3 batches of UNROLL 6), see profiles/kbench_r01_*
 #endif
-#if FG_PIPE == 2
+#if defined(FG_UNROLL)
+constexpr int kFG_UNROLL = FG_UNROLL;
+#elif FG_PIPE == 2
 constexpr int kFG_UNROLL = 6;
 #else
 constexpr int kFG_UNROLL = 8;

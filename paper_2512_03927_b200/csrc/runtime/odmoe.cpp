@@ -187,7 +187,7 @@ void validate(const odmoe_config* g) {
   if (g->k > g->E || g->k > 8 || g->E > 64) bad("need 1 <= k <= E <= 64 and k <= 8");
   if (g->d % 8 || g->F % 8) bad("d and F must be multiples of 8");
   if (g->dtype != ODMOE_BF16 && g->dtype != ODMOE_FP32) bad("dtype");
-  if (g->predictor < 0 || g->predictor > 4) bad("predictor");
+  if (g->predictor < 0 || g->predictor > 5) bad("predictor");
   if (g->lookahead < 1) bad("lookahead must be >= 1");
   if (g->world_size < 1 || g->rank < 0 || g->rank >= g->world_size) bad("rank/world_size");
   const int G = g->group_size > 0 ? g->group_size : std::min(g->k, g->world_size);
@@ -398,7 +398,8 @@ void build_buffers(Ctx* c) {
     c->sh_ids = dmalloc<int32_t>(c, (size_t)L * k, "sh_ids");  // receive buffer for P
   }
   // SEP refinement buffers (allocated for any shadow ctx so the depth can be switched at run time)
-  if (c->built_pred == ODMOE_PRED_SHADOW_INT8 || c->built_pred == ODMOE_PRED_SHADOW_SAME) {
+  if (c->built_pred == ODMOE_PRED_SHADOW_INT8 || c->built_pred == ODMOE_PRED_SHADOW_SAME ||
+      c->built_pred == ODMOE_PRED_GATE_REUSE) {
     c->ev_router.resize(L);
     c->ev_ref.resize(L);
     for (auto& e : c->ev_router) CUDA_OK(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -543,7 +544,26 @@ void random_prediction(Ctx* c, int64_t step, int l, int32_t* out) {
 // y'_j = sum_i w_i Q-FFN_i(u_j); h' = h_j + y'_j; router_{j+1}(h') -> P_B[j+1]; (experts, router)...
 // Its error covers at most R quantised layers instead of the whole token (Mode A), so it corrects
 // most mispredictions one or two layers before the main router would discover them.
+// Gate reuse (prior work): the MAIN model's gates of layers j+1..j+R applied to layer j's
+// state h_j (no expert outputs, no shadow): HOBBIT-style multi-layer look-ahead.
+void enqueue_gate_reuse(Ctx* c, int j) {
+  const int L = c->L, E = c->E, k = c->k, d = c->d, R = c->R;
+  cudaStream_t s = c->s_shadow;
+  int32_t* out = c->rf_ids + (size_t)j * 4 * k;
+  CUDA_OK(c, cudaStreamWaitEvent(s, c->ev_router[j], 0));
+  CUDA_OK(c, cudaMemsetAsync(out, 0xff, sizeof(int32_t) * 4 * k, s));
+  for (int r = 1; r <= R && j + r < L; ++r) {
+    const int m = j + r;
+    CUDA_OK(c, cudaMemcpyAsync(c->rf_h, c->h_hist + (size_t)j * d, sizeof(float) * d, cudaMemcpyDeviceToDevice, s));
+    KTimer t(c, K_SHADOW, s);
+    CUDA_OK(c, launch_router(c->rf_h, nullptr, 0, nullptr, (const char*)c->d_router + (size_t)m * E * d * c->esz,
+                             nullptr, c->wt, 1, E, d, k, c->cfg.rms_eps, c->rf_u, out + (size_t)(r - 1) * k,
+                             c->rf_w + (size_t)(r - 1) * k, nullptr, nullptr, s, false));
+  }
+}
+
 void enqueue_refine(Ctx* c, int j) {
+  if (c->cfg.predictor == ODMOE_PRED_GATE_REUSE) return enqueue_gate_reuse(c, j);
   const int L = c->L, E = c->E, k = c->k, d = c->d, F = c->F, R = c->R;
   cudaStream_t s = c->s_shadow;
   const WType swt = c->sh_wt;
@@ -727,8 +747,13 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
   const int p = c->cfg.predictor;
   const bool r0 = c->rank == 0;
   const int u_f32 = c->wt == W_F32;
-  // fused W13->W2 cooperative kernel on the compute stream only (never on the shadow stream)
-  const bool fused = use_fused_expert() && stream_ok(c->wt, d) && stream_ok(c->wt, F);
+  // Fused W13->W2 cooperative kernel: only on the compute stream and only where no kernel that
+  // spins on ANOTHER GPU can occupy SMs concurrently (N = 1, or fully resident where the
+  // prediction communicator is idle). At N > 1 the prediction broadcasts spin on the shadow
+  // stream; a cooperative grid that cannot become fully resident would wait at its barrier for
+  // SMs held by a kernel that waits for a peer that waits for us.
+  const bool fused = use_fused_expert() && stream_ok(c->wt, d) && stream_ok(c->wt, F) &&
+                     (c->world == 1 || c->resident);
 
   // token in (pinned -> device); the previous step's shadow must be done with d_tok_in
   c->h_tok[0] = token_in;
@@ -743,7 +768,8 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
   std::fill(c->predA_ready.begin(), c->predA_ready.end(), 0);
   std::fill(c->predB_tbl.begin(), c->predB_tbl.end(), -1);
   const bool shadow_pred = p == ODMOE_PRED_SHADOW_INT8 || p == ODMOE_PRED_SHADOW_SAME;
-  c->R = (!c->resident && shadow_pred) ? c->cfg.refine_depth : 0;
+  const bool gate_reuse = p == ODMOE_PRED_GATE_REUSE;
+  c->R = c->resident ? 0 : (shadow_pred ? c->cfg.refine_depth : (gate_reuse ? std::min(4, c->cfg.lookahead) : 0));
   c->ref_next = 0;
   std::fill(c->ref_enq.begin(), c->ref_enq.end(), 0);
   c->pred_valid = false;
@@ -755,6 +781,8 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
       }
       if (c->world > 1) enqueue_pred_broadcast(c);
       c->pred_valid = true;
+    } else if (gate_reuse) {
+      c->pred_valid = true;  // predictions arrive per layer through the refinement path
     } else if (p == ODMOE_PRED_RANDOM) {
       for (int l = 0; l < L; ++l) random_prediction(c, c->step, l, c->pred_tbl.data() + (size_t)l * k);
       c->predA_tbl = c->pred_tbl;
@@ -945,7 +973,7 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
       CUDA_OK(c, cudaMemcpyAsync(c->h_ids + (size_t)l * k, c->d_pkt + (size_t)l * c->pkt_bytes + c->pkt_ids_off, 4 * k, cudaMemcpyDeviceToHost, s));
   }
   CUDA_OK(c, cudaStreamSynchronize(s));
-  if (!c->resident && shadow_pred && (r0 || c->world > 1)) CUDA_OK(c, cudaStreamSynchronize(c->s_shadow));
+  if (!c->resident && (shadow_pred || gate_reuse) && (r0 || c->world > 1)) CUDA_OK(c, cudaStreamSynchronize(c->s_shadow));
   if (c->h_flag[0]) fail(c, ODMOE_E_NONFINITE, "non-finite router logits");
   if (c->resident) std::copy(c->h_ids, c->h_ids + (size_t)L * k, true_ids.begin());
 
@@ -953,6 +981,7 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
   // drive recall_eq3; the refined ones are counted separately
   for (int l = 0; l < L; ++l) pred_available(c, l);
   if (c->R > 0) apply_refinements(c);
+  if (gate_reuse) c->predA_tbl = c->predB_tbl;  // the gate-reuse predictions are this predictor's output
   if (r0) {
     for (int l = 0; l < L; ++l) {
       const int32_t* S = true_ids.data() + (size_t)l * k;
@@ -1481,11 +1510,13 @@ odmoe_status odmoe_set_option(void* ctx, int key, int64_t value) {
       if (value < 1) fail(c, ODMOE_E_CONFIG, "lookahead must be >= 1");
       c->cfg.lookahead = (int32_t)value;
     } else if (key == 2) {
-      if (value < 0 || value > 4) fail(c, ODMOE_E_CONFIG, "predictor");
+      if (value < 0 || value > 5) fail(c, ODMOE_E_CONFIG, "predictor");
       const bool wants_shadow = value == ODMOE_PRED_SHADOW_INT8 || value == ODMOE_PRED_SHADOW_SAME;
       if (wants_shadow && value != c->built_pred)
         fail(c, ODMOE_E_STATE, "this ctx was not created with that shadow predictor");
       if (c->resident && value != ODMOE_PRED_NONE) fail(c, ODMOE_E_STATE, "fully-resident ctx loads nothing");
+      if (value == ODMOE_PRED_GATE_REUSE && (c->ev_ref.empty() || c->wt != W_BF16))
+        fail(c, ODMOE_E_STATE, "gate reuse needs a bf16 ctx created with a shadow or gate-reuse predictor");
       c->cfg.predictor = (int32_t)value;
     } else if (key == 3) {
       if (value < 0 || value > 4) fail(c, ODMOE_E_CONFIG, "refine_depth must be in 0..4");

@@ -168,7 +168,8 @@ def test_output_invariance_across_predictors_slots_and_modes(od):
                dict(predictor=od.PRED_NONE, slots_per_gpu=-1),
                dict(predictor=od.PRED_SHADOW_INT8, slots_per_gpu=2, chunk_bytes=65536),
                dict(predictor=od.PRED_SHADOW_INT8, slots_per_gpu=4, lookahead=2, refine_depth=2),
-               dict(predictor=od.PRED_SHADOW_INT8, slots_per_gpu=2, refine_depth=1)):
+               dict(predictor=od.PRED_SHADOW_INT8, slots_per_gpu=2, refine_depth=1),
+               dict(predictor=od.PRED_GATE_REUSE, slots_per_gpu=4, lookahead=2)):
         eng, toks, routes, _ = _run(od, TINY, 12, first, **kw)
         assert toks == base, kw
         assert routes == base_r, kw
@@ -348,4 +349,23 @@ def test_sep_refinement_improves_prediction_accuracy(od):
     for _ in range(4):
         t, _ = eng.decode_step(t)
     assert eng.stats()["refine_total"] == 0
+    eng.close()
+
+
+def test_gate_reuse_predictor(od):
+    """Prior-work next-layer gate reuse as an ablation predictor: predictions
+    exist for layers >= 1, recall is recomputed exactly from the records, outputs unchanged."""
+    eng = engine(od, TINY, predictor=od.PRED_GATE_REUSE, slots_per_gpu=4, lookahead=2)
+    t, hits, tot = 13, 0, 0
+    for _ in range(12):
+        t, recs = eng.decode_step(t)
+        for l in range(TINY.L):
+            if recs[l].pred_available:
+                S, P = set(recs[l].true_ids[:2]), set(recs[l].pred_ids[:2])
+                assert recs[l].correct == len(S & P)
+                hits += recs[l].correct
+                tot += 2
+        assert not recs[0].pred_available  # nothing precedes layer 0
+    st = eng.stats()
+    assert st["predicted_total"] == tot > 0 and st["correct"] == hits
     eng.close()

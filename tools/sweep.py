@@ -26,7 +26,7 @@ def main():
     ap.add_argument("--steps", type=int, default=8)
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--lookaheads", default="1,2,3,4")
-    ap.add_argument("--predictors", default="shadow_int8,perfect,none,random")
+    ap.add_argument("--predictors", default="shadow_int8,perfect,gate_reuse,none,random")
     ap.add_argument("--slots", type=int, default=2)
     ap.add_argument("--refine", default="0", help="comma list of SEP refinement depths (shadow predictor only)")
     ap.add_argument("--out", default="")
