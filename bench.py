@@ -416,6 +416,12 @@ def main():
         if res is not None:
             line["resident"] = res
             line["ratio_vs_resident"] = value / res["value"]
+            # the same kernel measured live inside the fully-resident decode step of this run
+            # (back-to-back launches with PDL; no idle-to-busy ramp per expert)
+            line["roofline_resident"] = {"bound": "hbm", "kernel": line["roofline"]["kernel"],
+                                         "achieved": res["expert_gemv_GBps"], "peak": peaks["hbm_gbs"],
+                                         "unit": "GB/s", "frac": res["expert_gemv_GBps"] / peaks["hbm_gbs"],
+                                         "traffic": traffic, "avg_us_per_expert": res["expert_gemv_us"]}
         if not args.no_cpu_baseline and n == 1:
             try:
                 line["cpu_baseline"] = oracle_sample(8)
