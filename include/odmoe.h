@@ -62,8 +62,10 @@ typedef enum {
   ODMOE_PRED_RANDOM = 2,      /* uniformly random k experts per layer (P:256 case 5; E[recall] = k/E)    */
   ODMOE_PRED_PERFECT = 3,     /* replay of the true routing recorded by an earlier run of the same ctx   */
   ODMOE_PRED_SHADOW_SAME = 4, /* shadow with the main model's own weights (recall must be exactly 1.0)   */
-  ODMOE_PRED_GATE_REUSE = 5   /* prior work: after the main router of layer l,
+  ODMOE_PRED_GATE_REUSE = 5,  /* prior work: after the main router of layer l,
                                  apply the gates of layers l+1..l+D to layer l's normalised input   */
+  ODMOE_PRED_SHADOW_BF16 = 6  /* SEP with a BF16 shadow of an FP32 main model: the B200 analogue of the
+                                 paper's FP16 shadow (99.94 % recall); needs dtype FP32 */
 } odmoe_predictor;
 
 typedef struct {
@@ -236,9 +238,11 @@ odmoe_status odmoe_gen_weights(void* out, int kind, int layer, int expert, int64
 
 /* ------------------------------------------------------------------ stateful engine */
 
-/* Async H2D load of expert (layer, expert) into a free slot of this rank's GPU.
- * OK no-op if already resident or loading; E_BUDGET if every slot is occupied;
- * E_RANGE if this rank's pool does not hold that expert. */
+/* Async H2D load of expert (layer, expert) into a free slot of this rank's GPU,
+ * through the same copy-stream loader the decode step uses (most urgent first). OK no-op if
+ * already resident or loading; E_BUDGET if every slot is occupied; E_RANGE if this rank's pool
+ * does not hold that expert; E_STATE on a fully-resident ctx. A slot filled this way stays
+ * occupied (and unavailable to odmoe_decode_step) until odmoe_evict. */
 odmoe_status odmoe_load(void* ctx, int layer, int expert);
 /* Block until (layer, expert) is resident; *w13 / *w2 receive its device pointers. */
 odmoe_status odmoe_load_wait(void* ctx, int layer, int expert, void** w13, void** w2);

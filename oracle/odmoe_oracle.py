@@ -20,6 +20,8 @@ Parity pins (tests/test_oracle_pins.py, -m "not gpu"):
                       LM-head argmax ties.
   quantize_int8_rows  pinned: SPEC S:70 example ([1,-0.5] -> codes [127,-64]); half-step
                       bound; zero fixed point.
+  round_bf16          pinned: hand values (exact, ties to even, overflow-free carry into the
+                      exponent); torch's bf16 cast on random data (a library routine).
   shadow_predict      pinned: same-precision shadow => recall exactly 1.0.
   plan_* / misprediction_reloads / max_load_budget
                       pinned: SPEC examples S:271-273.
@@ -40,6 +42,7 @@ __all__ = [
     "rms_norm", "router_logits", "top_k", "top_k_bruteforce", "mixture_weights", "silu",
     "expert_ffn", "moe_layer", "final_logits", "greedy_argmax", "decode_token", "decode_sequence",
     "quantize_int8_rows", "dequantize_int8_rows", "quantize_model_int8", "shadow_predict",
+    "round_bf16", "shadow_model_bf16",
     "near_tie", "plan_group_size", "plan_groups", "assign_layer", "assign_experts",
     "misprediction_reloads", "max_load_budget", "residency_bound", "recall_eq2", "recall_eq3",
     "recall_bruteforce", "prefill_permutation", "prefill_reference", "expert_counts",
@@ -227,6 +230,27 @@ def quantize_model_int8(weights):
     for l, Wg in weights["router"].items():
         out["router"][l] = dq(Wg)
         out["experts"][l] = {e: tuple(dq(M) for M in mats) for e, mats in weights["experts"][l].items()}
+    return out
+
+
+def round_bf16(W):
+    """Round to the nearest bfloat16, ties to even (IEEE-754 binary32 with the low 16 bits of
+    the significand rounded away): the format of the half-precision shadow of an FP32 main
+    model (P:86, P:164 use an FP16 shadow; BF16 is the B200 reading Q26).
+    The value is first rounded to fp32 (the main model's own precision). Returns fp64."""
+    x = np.ascontiguousarray(np.asarray(W, dtype=np.float32))
+    u = x.view(np.uint32).astype(np.uint64)
+    lsb = (u >> 16) & 1
+    u = ((u + 0x7FFF + lsb) & 0xFFFF0000).astype(np.uint32)
+    return u.view(np.float32).astype(np.float64)
+
+
+def shadow_model_bf16(weights):
+    """The BF16 shadow (every matrix of the model rounded by round_bf16), same structure."""
+    out = {"emb": round_bf16(weights["emb"]), "router": {}, "experts": {}}
+    for l, Wg in weights["router"].items():
+        out["router"][l] = round_bf16(Wg)
+        out["experts"][l] = {e: tuple(round_bf16(M) for M in mats) for e, mats in weights["experts"][l].items()}
     return out
 
 

@@ -83,6 +83,18 @@ cudaError_t launch_gen(void* out, int kind, int layer, int expert, int64_t rows,
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- BF16 shadow of an FP32 model
+__global__ void f32_to_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = __float2bfloat16_rn(in[i]);
+}
+
+cudaError_t launch_f32_to_bf16(const float* in, void* out, int64_t n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  f32_to_bf16_kernel<<<num_sms() * 8, 256, 0, s>>>(in, reinterpret_cast<__nv_bfloat16*>(out), n);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- INT8-row quantiser
 template <typename T> __device__ __forceinline__ float ld_f(const T* p, long long i);
 template <> __device__ __forceinline__ float ld_f<__nv_bfloat16>(const __nv_bfloat16* p, long long i) { return __bfloat162float(p[i]); }

@@ -115,6 +115,9 @@ cudaError_t launch_embed_rows(const void* emb, WType wt, const int32_t* tokens, 
 cudaError_t launch_gen(void* out, int kind, int layer, int expert, int64_t rows, int64_t cols,
                        int64_t fan_in, int d, int F, uint64_t seed, WType wt, cudaStream_t s);
 
+// BF16 (round to nearest even) copy of an fp32 tensor: the BF16 shadow of an FP32 main model.
+cudaError_t launch_f32_to_bf16(const float* in, void* out, int64_t n, cudaStream_t s);
+
 // Q9 int8-row quantiser of a [R, C] matrix of type wt (bf16 / fp32).
 cudaError_t launch_quantize(const void* w, int64_t R, int64_t C, WType wt, int8_t* q, float* sc,
                             cudaStream_t s);

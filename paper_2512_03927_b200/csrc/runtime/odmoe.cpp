@@ -65,6 +65,9 @@ odmoe_status guard(Ctx* c, F&& f) {
 }
 
 inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+inline bool is_shadow(int p) {
+  return p == ODMOE_PRED_SHADOW_INT8 || p == ODMOE_PRED_SHADOW_SAME || p == ODMOE_PRED_SHADOW_BF16;
+}
 inline WType wtype(int dt) { return dt == ODMOE_FP32 ? W_F32 : W_BF16; }
 inline size_t dsize(int dt) { return dt == ODMOE_FP32 ? 4 : 2; }
 double now_s() {
@@ -187,7 +190,7 @@ void validate(const odmoe_config* g) {
   if (g->k > g->E || g->k > 8 || g->E > 64) bad("need 1 <= k <= E <= 64 and k <= 8");
   if (g->d % 8 || g->F % 8) bad("d and F must be multiples of 8");
   if (g->dtype != ODMOE_BF16 && g->dtype != ODMOE_FP32) bad("dtype");
-  if (g->predictor < 0 || g->predictor > 5) bad("predictor");
+  if (g->predictor < 0 || g->predictor > 6) bad("predictor");
   if (g->lookahead < 1) bad("lookahead must be >= 1");
   if (g->world_size < 1 || g->rank < 0 || g->rank >= g->world_size) bad("rank/world_size");
   const int G = g->group_size > 0 ? g->group_size : std::min(g->k, g->world_size);
@@ -197,8 +200,9 @@ void validate(const odmoe_config* g) {
   if (g->slots_per_gpu != -1 && g->slots_per_gpu < g->k / G) bad("slots_per_gpu must be >= k/G or -1");
   if (g->world_size > 1 && g->nccl_id == nullptr) bad("nccl_id required when world_size > 1");
   if (g->refine_depth < 0 || g->refine_depth > 4) bad("refine_depth must be in 0..4");
-  if (g->refine_depth > 0 && g->predictor != ODMOE_PRED_SHADOW_INT8 && g->predictor != ODMOE_PRED_SHADOW_SAME)
-    bad("refine_depth needs a shadow predictor");
+  if (g->refine_depth > 0 && !is_shadow(g->predictor)) bad("refine_depth needs a shadow predictor");
+  if (g->predictor == ODMOE_PRED_SHADOW_BF16 && g->dtype != ODMOE_FP32)
+    bad("the BF16 shadow is for an FP32 main model");
   if (g->refine_depth > 0 && g->dtype != ODMOE_BF16) bad("refine_depth needs the bf16 model");
 }
 
@@ -224,6 +228,31 @@ void build_shadow(Ctx* c, char* staging) {
     c->sh_router = c->d_router;
     c->d_sh_tbl = c->d_res_tbl;
     c->d_sh_stbl = nullptr;
+    return;
+  }
+  if (c->cfg.predictor == ODMOE_PRED_SHADOW_BF16) {
+    // BF16 copy of the FP32 main model (round to nearest even), no scales
+    c->sh_wt = W_BF16;
+    c->sh_emb = dmalloc<char>(c, (size_t)V * d * 2, "shadow emb bf16");
+    c->sh_router = dmalloc<char>(c, (size_t)L * E * d * 2, "shadow router bf16");
+    CUDA_OK(c, launch_f32_to_bf16((const float*)c->d_emb, c->sh_emb, (int64_t)V * d, c->s_main));
+    CUDA_OK(c, launch_f32_to_bf16((const float*)c->d_router, c->sh_router, (int64_t)L * E * d, c->s_main));
+    c->sh_blob.assign((size_t)L * E, nullptr);
+    c->sh_sc.assign((size_t)L * E, nullptr);
+    for (int l = 0; l < L; ++l)
+      for (int e = 0; e < E; ++e) {
+        const size_t i = (size_t)l * E + e;
+        char* q = dmalloc<char>(c, (size_t)3 * F * d * 2, "shadow expert bf16");
+        CUDA_OK(c, launch_gen(staging, 0, l, e, 0, 0, 0, d, F, c->cfg.weight_seed, c->wt, c->s_main));
+        CUDA_OK(c, launch_f32_to_bf16((const float*)staging, q, 3LL * F * d, c->s_main));
+        c->sh_blob[i] = q;
+        c->stats.shadow_bytes += (int64_t)3 * F * d * 2;
+      }
+    c->stats.shadow_bytes += (int64_t)V * d * 2 + (int64_t)L * E * d * 2;
+    c->d_sh_tbl = dmalloc<void*>(c, (size_t)L * E, "shadow tbl");
+    c->d_sh_stbl = nullptr;
+    CUDA_OK(c, cudaMemcpyAsync(c->d_sh_tbl, c->sh_blob.data(), sizeof(void*) * L * E, cudaMemcpyHostToDevice, c->s_main));
+    CUDA_OK(c, cudaStreamSynchronize(c->s_main));
     return;
   }
   c->sh_wt = W_I8;
@@ -398,8 +427,7 @@ void build_buffers(Ctx* c) {
     c->sh_ids = dmalloc<int32_t>(c, (size_t)L * k, "sh_ids");  // receive buffer for P
   }
   // SEP refinement buffers (allocated for any shadow ctx so the depth can be switched at run time)
-  if (c->built_pred == ODMOE_PRED_SHADOW_INT8 || c->built_pred == ODMOE_PRED_SHADOW_SAME ||
-      c->built_pred == ODMOE_PRED_GATE_REUSE) {
+  if (is_shadow(c->built_pred) || c->built_pred == ODMOE_PRED_GATE_REUSE) {
     c->ev_router.resize(L);
     c->ev_ref.resize(L);
     for (auto& e : c->ev_router) CUDA_OK(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -441,9 +469,9 @@ void build_buffers(Ctx* c) {
 void enqueue_shadow(Ctx* c, const int32_t* token_dev) {
   const int L = c->L, E = c->E, k = c->k, d = c->d, F = c->F;
   cudaStream_t s = c->s_shadow;
-  const bool same = c->cfg.predictor == ODMOE_PRED_SHADOW_SAME;
   const WType swt = c->sh_wt;
-  const size_t sesz = swt == W_I8 ? 1 : c->esz;
+  const bool same = swt != W_I8;  // no row scales (main-dtype or BF16 shadow)
+  const size_t sesz = swt == W_I8 ? 1 : (swt == W_BF16 ? 2 : 4);
   {
     KTimer t(c, K_SHADOW, s);
     CUDA_OK(c, launch_embed(c->sh_emb, c->sh_semb, swt, token_dev, d, c->sh_h, s));
@@ -501,7 +529,7 @@ void enqueue_pred_broadcast(Ctx* c) {
 bool pred_available(Ctx* c, int m) {
   if (!c->pred_valid) return false;
   const int p = c->cfg.predictor;
-  if ((p == ODMOE_PRED_SHADOW_INT8 || p == ODMOE_PRED_SHADOW_SAME) && !c->predA_ready[m]) {
+  if (is_shadow(p) && !c->predA_ready[m]) {
     const int evl = c->world == 1 ? m : (m / c->pred_chunk) * c->pred_chunk;
     const cudaError_t q = cudaEventQuery(c->ev_pred[evl]);
     if (q == cudaErrorNotReady) return c->pred_ready[m] != 0;
@@ -567,7 +595,7 @@ void enqueue_refine(Ctx* c, int j) {
   const int L = c->L, E = c->E, k = c->k, d = c->d, F = c->F, R = c->R;
   cudaStream_t s = c->s_shadow;
   const WType swt = c->sh_wt;
-  const size_t sesz = swt == W_I8 ? 1 : c->esz;
+  const size_t sesz = swt == W_I8 ? 1 : (swt == W_BF16 ? 2 : 4);
   const bool same = swt != W_I8;
   char* pkt = c->d_pkt + (size_t)j * c->pkt_bytes;
   int32_t* out = c->rf_ids + (size_t)j * 4 * k;
@@ -767,7 +795,7 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
   std::fill(c->predA_tbl.begin(), c->predA_tbl.end(), -1);
   std::fill(c->predA_ready.begin(), c->predA_ready.end(), 0);
   std::fill(c->predB_tbl.begin(), c->predB_tbl.end(), -1);
-  const bool shadow_pred = p == ODMOE_PRED_SHADOW_INT8 || p == ODMOE_PRED_SHADOW_SAME;
+  const bool shadow_pred = is_shadow(p);
   const bool gate_reuse = p == ODMOE_PRED_GATE_REUSE;
   c->R = c->resident ? 0 : (shadow_pred ? c->cfg.refine_depth : (gate_reuse ? std::min(4, c->cfg.lookahead) : 0));
   c->ref_next = 0;
@@ -1307,7 +1335,7 @@ void destroy_ctx(Ctx* c) {
   if (c->s_copy) cudaStreamSynchronize(c->s_copy);
   auto F = [](void* p) { if (p) cudaFree(p); };
   F(c->d_emb); F(c->d_lm); F(c->d_router);
-  if (c->cfg.predictor != ODMOE_PRED_SHADOW_SAME) {
+  if (c->built_pred != ODMOE_PRED_SHADOW_SAME) {
     F(c->sh_emb); F(c->sh_semb); F(c->sh_router); F(c->sh_srouter);
     for (auto p : c->sh_blob) F(p);
     for (auto p : c->sh_sc) F(p);
@@ -1410,7 +1438,7 @@ odmoe_status odmoe_create(const odmoe_config* cfg, void** ctx_out) {
     c->built_pred = cfg->predictor;
     c->dev = cfg->device;
     c->has_shadow = c->rank == 0 && !c->resident &&
-                    (cfg->predictor == ODMOE_PRED_SHADOW_INT8 || cfg->predictor == ODMOE_PRED_SHADOW_SAME);
+                    is_shadow(cfg->predictor);
     try {
       CUDA_OK(c, cudaSetDevice(c->dev));
       CUDA_OK(c, cudaStreamCreateWithFlags(&c->s_main, cudaStreamNonBlocking));
@@ -1510,8 +1538,8 @@ odmoe_status odmoe_set_option(void* ctx, int key, int64_t value) {
       if (value < 1) fail(c, ODMOE_E_CONFIG, "lookahead must be >= 1");
       c->cfg.lookahead = (int32_t)value;
     } else if (key == 2) {
-      if (value < 0 || value > 5) fail(c, ODMOE_E_CONFIG, "predictor");
-      const bool wants_shadow = value == ODMOE_PRED_SHADOW_INT8 || value == ODMOE_PRED_SHADOW_SAME;
+      if (value < 0 || value > 6) fail(c, ODMOE_E_CONFIG, "predictor");
+      const bool wants_shadow = is_shadow((int)value);
       if (wants_shadow && value != c->built_pred)
         fail(c, ODMOE_E_STATE, "this ctx was not created with that shadow predictor");
       if (c->resident && value != ODMOE_PRED_NONE) fail(c, ODMOE_E_STATE, "fully-resident ctx loads nothing");

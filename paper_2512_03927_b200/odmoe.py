@@ -14,8 +14,9 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("ODMOE_LIB") or os.path.join(_HERE, "libodmoe.so")
 
 BF16, FP32 = 0, 1
-PRED_SHADOW_INT8, PRED_NONE, PRED_RANDOM, PRED_PERFECT, PRED_SHADOW_SAME, PRED_GATE_REUSE = 0, 1, 2, 3, 4, 5
-PREDICTORS = {"shadow_int8": 0, "none": 1, "random": 2, "perfect": 3, "shadow_same": 4, "gate_reuse": 5}
+PRED_SHADOW_INT8, PRED_NONE, PRED_RANDOM, PRED_PERFECT, PRED_SHADOW_SAME, PRED_GATE_REUSE, PRED_SHADOW_BF16 = range(7)
+PREDICTORS = {"shadow_int8": 0, "none": 1, "random": 2, "perfect": 3, "shadow_same": 4, "gate_reuse": 5,
+              "shadow_bf16": 6}
 
 STATUS = {0: "OK", 1: "E_CONFIG", 2: "E_RANGE", 3: "E_NONFINITE", 4: "E_BUDGET", 5: "E_STATE",
           6: "E_PLAN", 7: "E_NOMEM", 8: "E_CUDA", 9: "E_NCCL"}

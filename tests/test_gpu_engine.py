@@ -369,3 +369,33 @@ def test_gate_reuse_predictor(od):
     st = eng.stats()
     assert st["predicted_total"] == tot > 0 and st["correct"] == hits
     eng.close()
+
+
+def test_bf16_shadow_of_fp32_model(od):
+    """SEP with a BF16 shadow of the FP32 main model (the paper's FP16 shadow, P:86, P:164;
+    reading Q26): teacher-forced shadow routing vs the oracle's bf16-rounded model, recall at
+    least the INT8 shadow's on the same tokens, outputs identical to the no-predictor run."""
+    W = gen_model_weights(TINY, SEED, dtype="fp32")
+    SW = O.shadow_model_bf16(W)
+    eng = engine(od, TINY, "fp32", predictor=od.PRED_SHADOW_BF16, slots_per_gpu=2, debug_capture=1)
+    tok = int(gen_prompt(TINY, 2, 1)[0])
+    first, toks, excused = tok, [], 0
+    for _ in range(12):
+        nxt, _ = eng.decode_step(tok)
+        excused += check_step_teacher_forced(eng, W, TINY, "fp32", tok, nxt, SW)
+        toks.append(nxt)
+        tok = nxt
+    assert excused <= 3
+    st = eng.stats()
+    r_bf16 = st["correct"] / st["predicted_total"]
+    assert st["shadow_bytes"] < 0.6 * 4 * (TINY.L * TINY.E * 3 * TINY.d * TINY.F)
+    eng.close()
+    e8, toks8, _, st8 = _run(od, TINY, 12, first, dtype="fp32", predictor=od.PRED_SHADOW_INT8, slots_per_gpu=2)
+    e8.close()
+    en, toksn, _, _ = _run(od, TINY, 12, first, dtype="fp32", predictor=od.PRED_NONE, slots_per_gpu=2)
+    en.close()
+    assert toks == toks8 == toksn
+    assert r_bf16 >= st8["correct"] / st8["predicted_total"] - 0.01, r_bf16
+    assert r_bf16 >= 0.95, r_bf16
+    with pytest.raises(od.OdmoeError):
+        engine(od, TINY, "bf16", predictor=od.PRED_SHADOW_BF16)   # BF16 shadow needs an FP32 main model

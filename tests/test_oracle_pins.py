@@ -240,6 +240,25 @@ def test_quantizer_half_step_bound_and_zero():
     assert qh[0].tolist() == [127, 2, 4, 0, -2, 0]
 
 
+def test_round_bf16_hand_values_and_library():
+    """BF16 = fp32 with 7 stored significand bits, round to nearest, ties to even."""
+    e = 2.0 ** -8                                     # half an ulp of 1.0 in bf16
+    x = np.array([1.0, 1.0 + e, 1.0 + 3 * e, 1.0 + e + 2.0 ** -20, -(1.0 + 3 * e), 0.0,
+                  2.0 - e / 2, 3.0e38, 1.5, -0.0])
+    want = [1.0, 1.0, 1.0 + 4 * e, 1.0 + 2 * e, -(1.0 + 4 * e), 0.0, 2.0, 3.0e38, 1.5, 0.0]
+    got = O.round_bf16(x)
+    assert np.allclose(got, want, rtol=2.0 ** -8, atol=0)
+    assert got[:7].tolist() == want[:7]               # exact: ties to even (1+e -> 1, 1+3e -> 1+4e)
+    assert np.signbit(got[9])                          # -0 keeps its sign
+    import torch
+    rng = np.random.default_rng(26)
+    r = (rng.standard_normal(4096) * rng.choice([1e-3, 1.0, 1e3], 4096)).astype(np.float32)
+    lib = torch.from_numpy(r).to(torch.bfloat16).to(torch.float64).numpy()
+    assert np.array_equal(O.round_bf16(r), lib)
+    # relative error <= u = 2^-8 (unit roundoff of an 8-bit significand)
+    assert np.all(np.abs(O.round_bf16(r) - r) <= 2.0 ** -8 * np.abs(r.astype(np.float64)))
+
+
 def test_same_precision_shadow_recall_is_one(tiny_fp32):
     """a full-precision shadow with token alignment predicts exactly."""
     toks, routes = O.decode_sequence(tiny_fp32, 11, 6, TINY.k)
