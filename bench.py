@@ -255,10 +255,20 @@ def workload_config(args, n):
 
 
 # ---------------------------------------------------------------------------- our arm
+_T0 = time.time()
+
+
+def log(rank, msg):
+    """Phase log on stderr (locates a stall in a multi-rank run; never on stdout)."""
+    print(f"[bench r{rank} +{time.time() - _T0:7.1f}s] {msg}", file=sys.stderr, flush=True)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    import faulthandler
+    faulthandler.dump_traceback_later(480, repeat=True, file=sys.stderr)  # stack dump if a phase stalls
     import torch
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
@@ -279,6 +289,7 @@ def main():
         uid = obj[0]
     D = args.lookahead or max(1, n // 2)
     pred = odmoe.PREDICTORS[args.predictor]
+    log(rank, "create engine")
     t_create = time.time()
     refine = args.refine if args.predictor.startswith("shadow") else 0
     eng = odmoe.Engine(device=local, rank=rank, world_size=world, nccl_id=uid, predictor=pred,
@@ -295,6 +306,7 @@ def main():
     tok = args.first_token if args.first_token >= 0 else 1
     prefill = None
     if args.prefill > 0:
+        log(rank, f"prefill {args.prefill}")
         from inputs import MIXTRAL, gen_prompt
         prompt = [int(x) for x in gen_prompt(MIXTRAL, 1, args.prefill)]
         eng.prefill(prompt[:8])  # allocate the prefill buffers / slots outside the timed call
@@ -310,9 +322,11 @@ def main():
                    "grouped_gemm_ms_total": gg_ms, "grouped_gemm_TFLOPs": flops / max(gg_ms, 1e-9) / 1e9 / n,
                    "experts_activated_per_layer": sum(1 for c in counts if c > 0) / SHAPE["L"],
                    "note": "host wall clock of odmoe_prefill (synchronous); GEMM time from CUDA events"}
+    log(rank, "warmup")
     for _ in range(args.warmup):
         tok, _ = eng.decode_step(tok, records=False)
     eng.reset_stats()
+    log(rank, "timed decode")
     recs_all = []
     clocks = ClockSampler(local)
     barrier()
@@ -347,6 +361,7 @@ def main():
     e2e = args.steps / wall
     res = None
     if not args.no_resident:
+        log(rank, "resident baseline")
         res = resident_baseline(odmoe, torch, args, local, rank, world, dist)
 
     if rank == 0:
@@ -423,6 +438,7 @@ def main():
                                          "unit": "GB/s", "frac": res["expert_gemv_GBps"] / peaks["hbm_gbs"],
                                          "traffic": traffic, "avg_us_per_expert": res["expert_gemv_us"]}
         if not args.no_cpu_baseline and n == 1:
+            log(rank, "cpu baseline (oracle sample)")
             try:
                 line["cpu_baseline"] = oracle_sample(8)
             except Exception as e:  # report, never hide
@@ -435,6 +451,8 @@ def main():
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
+    faulthandler.cancel_dump_traceback_later()
+    log(rank, "done")
     return 0
 
 

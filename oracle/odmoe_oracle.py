@@ -22,6 +22,11 @@ Parity pins (tests/test_oracle_pins.py, -m "not gpu"):
                       bound; zero fixed point.
   round_bf16          pinned: hand values (exact, ties to even, overflow-free carry into the
                       exponent); torch's bf16 cast on random data (a library routine).
+  NF4_CODEBOOK        pinned: QLoRA's construction from normal quantiles (nf4_codebook_from_
+                      quantiles, scipy.stats.norm) within 2 fp32 ulp; symmetry ends, exact 0.
+  quantize_nf4_blocks pinned: brute-force nearest-code search with Python floats; codes of the
+                      codebook values themselves map to themselves; midpoint ties; zero blocks;
+                      dequantised error <= half the local codebook gap x absmax.
   shadow_predict      pinned: same-precision shadow => recall exactly 1.0.
   plan_* / misprediction_reloads / max_load_budget
                       pinned: SPEC examples S:271-273.
@@ -42,7 +47,8 @@ __all__ = [
     "rms_norm", "router_logits", "top_k", "top_k_bruteforce", "mixture_weights", "silu",
     "expert_ffn", "moe_layer", "final_logits", "greedy_argmax", "decode_token", "decode_sequence",
     "quantize_int8_rows", "dequantize_int8_rows", "quantize_model_int8", "shadow_predict",
-    "round_bf16", "shadow_model_bf16",
+    "round_bf16", "shadow_model_bf16", "NF4_CODEBOOK", "NF4_BLOCK", "nf4_codebook_from_quantiles",
+    "quantize_nf4_blocks", "dequantize_nf4_blocks", "quantize_model_nf4",
     "near_tie", "plan_group_size", "plan_groups", "assign_layer", "assign_experts",
     "misprediction_reloads", "max_load_budget", "residency_bound", "recall_eq2", "recall_eq3",
     "recall_bruteforce", "prefill_permutation", "prefill_reference", "expert_counts",
@@ -251,6 +257,71 @@ def shadow_model_bf16(weights):
     for l, Wg in weights["router"].items():
         out["router"][l] = round_bf16(Wg)
         out["experts"][l] = {e: tuple(round_bf16(M) for M in mats) for e, mats in weights["experts"][l].items()}
+    return out
+
+
+# NF4 codebook, as published with QLoRA (Dettmers et al. 2023, "NormalFloat4"; the table of its
+# reference implementation). The paper's third shadow precision (95.67 % recall)
+# names NF4 without further detail: reading Q27 takes QLoRA's NF4 with blocks of 64 weights
+# along a row and one fp32 absmax per block (no double quantisation).
+NF4_CODEBOOK = (
+    -1.0, -0.6961928009986877, -0.5250730514526367, -0.39491748809814453,
+    -0.28444138169288635, -0.18477343022823334, -0.09105003625154495, 0.0,
+    0.07958029955625534, 0.16093020141124725, 0.24611230194568634, 0.33791524171829224,
+    0.44070982933044434, 0.5626170039176941, 0.7229568362236023, 1.0,
+)
+NF4_BLOCK = 64
+
+
+def nf4_codebook_from_quantiles(offset: float = 0.9677083):
+    """NF4's construction (QLoRA §3): 8 positive and 7 negative quantiles of N(0, 1) at evenly
+    spaced probabilities from `offset` to 1/2, plus an exact zero, normalised to [-1, 1]."""
+    from scipy.stats import norm
+    pos = norm.ppf(np.linspace(offset, 0.5, 9)[:-1])
+    neg = -norm.ppf(np.linspace(offset, 0.5, 8)[:-1])
+    v = np.sort(np.concatenate([pos, [0.0], neg]))
+    return v / np.max(np.abs(v))
+
+
+def quantize_nf4_blocks(W, block: int = NF4_BLOCK):
+    """NF4 blockwise quantiser (reading Q27): per block of `block` consecutive weights of a row,
+    a = max |w| (exact, stored fp32); x = w / a in fp64; code = index of the codebook entry
+    nearest to x (|x - c_i| in fp64, the lower index on an exact tie). a = 0 -> all codes 7
+    (the codebook's 0.0). Returns (codes uint8 [R, C] in 0..15, absmax float32 [R, C/block])."""
+    W = np.asarray(W, dtype=np.float64)
+    if W.ndim == 1:
+        W = W[None, :]
+    R, C = W.shape
+    assert C % block == 0
+    cb = np.asarray(NF4_CODEBOOK, dtype=np.float32).astype(np.float64)
+    Wb = W.reshape(R, C // block, block)
+    a = np.max(np.abs(Wb), axis=2)
+    x = np.zeros_like(Wb)
+    nz = a > 0
+    x[nz] = Wb[nz] / a[nz][:, None]
+    dist = np.abs(x[..., None] - cb)                        # [R, nb, block, 16]
+    codes = np.argmin(dist, axis=-1).astype(np.uint8)      # argmin returns the first minimum
+    codes[~nz] = 7
+    return codes.reshape(R, C), a.astype(np.float32)
+
+
+def dequantize_nf4_blocks(codes, absmax, block: int = NF4_BLOCK):
+    """Q(W)_rj = c[code_rj] * a_r,j/block (fp64)."""
+    cb = np.asarray(NF4_CODEBOOK, dtype=np.float32).astype(np.float64)
+    codes = np.asarray(codes)
+    a = np.repeat(np.asarray(absmax, dtype=np.float64), block, axis=1)
+    return cb[codes] * a
+
+
+def quantize_model_nf4(weights):
+    """The NF4 shadow (reading Q27): every expert matrix NF4-blockwise; the embedding and the
+    routers int8-row as in the INT8 shadow (0.3 % of the bytes). Dequantised fp64, same structure."""
+    dq8 = lambda W: dequantize_int8_rows(*quantize_int8_rows(W))  # noqa: E731
+    dq4 = lambda W: dequantize_nf4_blocks(*quantize_nf4_blocks(W))  # noqa: E731
+    out = {"emb": dq8(weights["emb"]), "router": {}, "experts": {}}
+    for l, Wg in weights["router"].items():
+        out["router"][l] = dq8(Wg)
+        out["experts"][l] = {e: tuple(dq4(M) for M in mats) for e, mats in weights["experts"][l].items()}
     return out
 
 

@@ -259,6 +259,45 @@ def test_round_bf16_hand_values_and_library():
     assert np.all(np.abs(O.round_bf16(r) - r) <= 2.0 ** -8 * np.abs(r.astype(np.float64)))
 
 
+def test_nf4_codebook_matches_quantile_construction():
+    pub = np.asarray(O.NF4_CODEBOOK, dtype=np.float32)
+    der = O.nf4_codebook_from_quantiles()
+    assert len(pub) == 16 and np.all(np.diff(pub) > 0)
+    assert pub[0] == -1.0 and pub[15] == 1.0 and pub[7] == 0.0
+    # the published table was computed in fp32 (values normalised to 1): agree to 2 ulp of 1.0
+    assert np.all(np.abs(pub.astype(np.float64) - der) <= 2 * 2.0 ** -23), np.abs(pub - der)
+
+
+def test_nf4_quantizer_brute_force_and_properties():
+    rng = np.random.default_rng(27)
+    W = (rng.standard_normal((6, 128)) * 0.02).astype(np.float32).astype(np.float64)
+    W[2, 64:] = 0.0                                       # one all-zero block
+    W[3, :64] = np.asarray(O.NF4_CODEBOOK * 4, dtype=np.float32) * 0.5   # codebook values x a
+    codes, a = O.quantize_nf4_blocks(W)
+    assert codes.shape == (6, 128) and a.shape == (6, 2) and codes.dtype == np.uint8
+    cb = [float(np.float32(c)) for c in O.NF4_CODEBOOK]
+    for r in range(6):
+        for j in range(128):
+            amax = max(abs(float(v)) for v in W[r, (j // 64) * 64:(j // 64) * 64 + 64])
+            if amax == 0.0:
+                assert codes[r, j] == 7
+                continue
+            assert a[r, j // 64] == np.float32(amax)
+            x = float(W[r, j]) / amax
+            best = min(range(16), key=lambda i: (abs(x - cb[i]), i))     # brute force, Python floats
+            assert codes[r, j] == best, (r, j)
+    assert codes[3, :64].tolist() == list(range(16)) * 4  # codebook points are fixed points
+    deq = O.dequantize_nf4_blocks(codes, a)
+    assert np.all(deq[2, 64:] == 0.0)
+    gaps = np.diff(np.asarray(cb))
+    half_gap = np.max(gaps) / 2
+    assert np.all(np.abs(deq - W) <= half_gap * np.repeat(a.astype(np.float64), 64, axis=1) + 1e-12)
+    # an exact midpoint between codes 7 (0.0) and 8 goes to the lower index
+    m = cb[8] / 2
+    c2, _ = O.quantize_nf4_blocks(np.array([[1.0, m] + [0.0] * 62]))
+    assert c2[0, 1] == 7 and c2[0, 0] == 15
+
+
 def test_same_precision_shadow_recall_is_one(tiny_fp32):
     """a full-precision shadow with token alignment predicts exactly."""
     toks, routes = O.decode_sequence(tiny_fp32, 11, 6, TINY.k)
