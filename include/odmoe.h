@@ -64,8 +64,11 @@ typedef enum {
   ODMOE_PRED_SHADOW_SAME = 4, /* shadow with the main model's own weights (recall must be exactly 1.0)   */
   ODMOE_PRED_GATE_REUSE = 5,  /* prior work: after the main router of layer l,
                                  apply the gates of layers l+1..l+D to layer l's normalised input   */
-  ODMOE_PRED_SHADOW_BF16 = 6  /* SEP with a BF16 shadow of an FP32 main model: the B200 analogue of the
+  ODMOE_PRED_SHADOW_BF16 = 6, /* SEP with a BF16 shadow of an FP32 main model: the B200 analogue of the
                                  paper's FP16 shadow (99.94 % recall); needs dtype FP32 */
+  ODMOE_PRED_SHADOW_NF4 = 7   /* SEP with an NF4 shadow (95.67 % recall; reading Q27):
+                                 expert matrices NF4 in 64-weight blocks, embedding/routers int8-row;
+                                 needs d, F multiples of 64 */
 } odmoe_predictor;
 
 typedef struct {
@@ -187,6 +190,14 @@ odmoe_status odmoe_shadow_expert_ffn(const int8_t* q13, const float* s13, const 
                                      int gate_idx, int d, int F, float* a_scratch, float* y,
                                      void* stream);
 
+/* NF4 shadow expert FFN (reading Q27): like odmoe_shadow_expert_ffn with W = c[code] * absmax.
+ * q13: codes of W13 [2F][d/2] bytes (two codes per byte, low nibble = even column), a13: fp32
+ * absmax [2F][d/64]; q2 [d][F/2], a2 [d][F/64]; u bf16 [d]. d, F multiples of 64 (the flat
+ * kernel needs multiples of 1024; other shapes take a warp-per-row kernel). */
+odmoe_status odmoe_shadow_expert_ffn_nf4(const uint8_t* q13, const float* a13, const uint8_t* q2,
+                                         const float* a2, const void* u, const float* gate_w, int gate_idx,
+                                         int d, int F, float* a_scratch, float* y, void* stream);
+
 /* Router over INT8-row weights (shadow gating): like odmoe_route_topk with w_gate = s_e*q_e,
  * gamma = 1, u_out bf16. */
 odmoe_status odmoe_shadow_route_topk(float* h, const float* const* y_add, int n_add,
@@ -228,6 +239,13 @@ odmoe_status odmoe_lm_head_argmax(const float* h, const void* lm_head, int V, in
  * s = fl32(m_r/127); zero rows -> q = 0, s = 1.  w [R,C] dt -> q [R,C] int8, s [R] fp32. */
 odmoe_status odmoe_quantize_int8_rows(const void* w, int64_t R, int64_t C, int dt, int8_t* q,
                                       float* s, void* stream);
+
+/* NF4 blockwise quantiser (reading Q27; QLoRA's codebook): per block of 64 consecutive weights
+ * of a row, absmax[r][b] = max|w| (fp32), code = nearest codebook entry to w/absmax compared in
+ * fp64 (lower index on a tie; zero block -> code 7). w [R][C] of dtype dt (device), q [R][C/2]
+ * bytes (low nibble = even column), absmax [R][C/64]. C % 64 == 0 else E_CONFIG. */
+odmoe_status odmoe_quantize_nf4(const void* w, int64_t R, int64_t C, int dt, uint8_t* q, float* absmax,
+                                void* stream);
 
 /* Synthetic weight generator: out[i] = dt(fl32(v_i * fl32(1/sqrt(fan_in)))),
  * v_i from splitmix64(seed, tensor_id, i). kind: 1 emb, 2 router, 3 W1, 4 W3, 5 W2, 6 LM head;

@@ -141,4 +141,59 @@ cudaError_t launch_quantize(const void* w, int64_t R, int64_t C, WType wt, int8_
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- NF4 blockwise quantiser
+// Reading Q27 (QLoRA NF4, blocks of 64 along a row, fp32 absmax): one warp per block, two weights
+// per lane; x = w / absmax in fp64 and the nearest code by |x - c_i| in fp64 (lower index on an
+// exact tie), so the decision is the oracle's bit for bit. Zero block -> code 7 (0.0).
+__constant__ float kNF4Q[16] = {
+    -1.0f, -0.6961928009986877f, -0.5250730514526367f, -0.39491748809814453f,
+    -0.28444138169288635f, -0.18477343022823334f, -0.09105003625154495f, 0.0f,
+    0.07958029955625534f, 0.16093020141124725f, 0.24611230194568634f, 0.33791524171829224f,
+    0.44070982933044434f, 0.5626170039176941f, 0.7229568362236023f, 1.0f};
+
+__device__ __forceinline__ uint32_t nf4_code(double x) {
+  uint32_t best = 0;
+  double bd = fabs(x - (double)kNF4Q[0]);
+#pragma unroll
+  for (int i = 1; i < 16; ++i) {
+    const double di = fabs(x - (double)kNF4Q[i]);
+    if (di < bd) { bd = di; best = (uint32_t)i; }
+  }
+  return best;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) quantize_nf4_kernel(const T* __restrict__ w, long long R, long long C,
+                                                           uint8_t* __restrict__ q, float* __restrict__ absmax) {
+  const long long nb = R * (C / 64);
+  const int lane = threadIdx.x & 31;
+  for (long long blk = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; blk < nb;
+       blk += ((long long)gridDim.x * blockDim.x) >> 5) {
+    const long long r = blk / (C / 64), cb = blk - r * (C / 64);
+    const long long o = r * C + cb * 64 + 2 * lane;
+    const float v0 = ld_f<T>(w, o), v1 = ld_f<T>(w, o + 1);
+    float m = fmaxf(fabsf(v0), fabsf(v1));
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, s));
+    uint32_t c0 = 7, c1 = 7;
+    if (m > 0.f) {
+      c0 = nf4_code((double)v0 / (double)m);
+      c1 = nf4_code((double)v1 / (double)m);
+    }
+    q[o >> 1] = (uint8_t)(c0 | (c1 << 4));
+    if (lane == 0) absmax[blk] = m;
+  }
+}
+
+cudaError_t launch_quantize_nf4(const void* w, int64_t R, int64_t C, WType wt, uint8_t* q, float* absmax,
+                                cudaStream_t s) {
+  if (R <= 0) return cudaSuccess;
+  if (C % 64) return cudaErrorInvalidValue;
+  const int grid = num_sms() * 8;
+  if (wt == W_BF16) quantize_nf4_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)w, R, C, q, absmax);
+  else if (wt == W_F32) quantize_nf4_kernel<float><<<grid, 256, 0, s>>>((const float*)w, R, C, q, absmax);
+  else return cudaErrorInvalidValue;
+  return cudaGetLastError();
+}
+
 }  // namespace odmoe

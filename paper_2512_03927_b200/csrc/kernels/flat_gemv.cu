@@ -10,6 +10,8 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <cuda_fp16.h>
+
 #include <cstdlib>
 
 namespace odmoe {
@@ -34,20 +36,12 @@ constexpr int kFG_UNROLL = 8;
 #endif
 constexpr int kFG_THREADS = kFG_WARPS * 32;
 
+// FDot<WT, XT>::run(w, xp): one 16-byte weight granule (kN weights) . its kN activations.
+// Activations live in shared memory in a lane-interleaved ("swizzled") order: a granule's kN
+// activations are Q = kN*sizeof(XT)/16 uint4 words, and word q of lane L for granule column g
+// sits at uint4 index (g*Q + q)*32 + L. A warp's q-th loads are then 512 contiguous bytes (no bank
+// conflicts) for every weight/activation type; xp = word 0 of this lane, word q at xp[32*q].
 template <typename WT, typename XT> struct FDot;
-template <> struct FDot<__nv_bfloat16, float> {
-  static constexpr int kN = 8;
-  __device__ __forceinline__ static float run(const uint4& w, const float* x) { return dot16<__nv_bfloat16>(w, x); }
-};
-template <> struct FDot<float, float> {
-  static constexpr int kN = 4;
-  __device__ __forceinline__ static float run(const uint4& w, const float* x) { return dot16<float>(w, x); }
-};
-template <> struct FDot<int8_t, float> {
-  static constexpr int kN = 16;
-  __device__ __forceinline__ static float run(const uint4& w, const float* x) { return dot16<int8_t>(w, x); }
-};
-#ifdef FG_F32X2
 // Packed fp32x2 arithmetic (sm_100 FFMA2 / FADD2): one instruction per element PAIR.
 typedef unsigned long long f2_t;
 __device__ __forceinline__ f2_t f2_pack(float lo, float hi) {
@@ -71,7 +65,113 @@ __device__ __forceinline__ float f2_sum(f2_t a) {
   return lo + hi;
 }
 __device__ __forceinline__ f2_t bf2_unpack(uint32_t v) { return f2_pack(bf16_lo(v), bf16_hi(v)); }
-#endif
+__device__ __forceinline__ f2_t f2_of(uint32_t lo, uint32_t hi) { return f2_pack(__uint_as_float(lo), __uint_as_float(hi)); }
+
+template <> struct FDot<__nv_bfloat16, float> {
+  static constexpr int kN = 8;
+  __device__ __forceinline__ static float run(const uint4& w, const uint4* xp) {
+    const uint4 x0 = xp[0], x1 = xp[32];
+    f2_t s = f2_fma(bf2_unpack(w.x), f2_of(x0.x, x0.y), 0ull);
+    s = f2_fma(bf2_unpack(w.y), f2_of(x0.z, x0.w), s);
+    s = f2_fma(bf2_unpack(w.z), f2_of(x1.x, x1.y), s);
+    s = f2_fma(bf2_unpack(w.w), f2_of(x1.z, x1.w), s);
+    return f2_sum(s);
+  }
+};
+template <> struct FDot<float, float> {
+  static constexpr int kN = 4;
+  __device__ __forceinline__ static float run(const uint4& w, const uint4* xp) {
+    const uint4 x0 = xp[0];
+    f2_t s = f2_fma(f2_of(w.x, w.y), f2_of(x0.x, x0.y), 0ull);
+    s = f2_fma(f2_of(w.z, w.w), f2_of(x0.z, x0.w), s);
+    return f2_sum(s);
+  }
+};
+// 4 int8 of one word -> two exact fp32 pairs (byte into the mantissa of 2^23, one FADD2 per pair)
+__device__ __forceinline__ void i8x4_unpack(uint32_t word, f2_t& q01, f2_t& q23) {
+  const uint32_t b = word ^ 0x80808080u;
+  const f2_t m = f2_pack(-8388736.0f, -8388736.0f);
+  q01 = f2_add(f2_pack(__uint_as_float(__byte_perm(b, 0x4B000000u, 0x7540)),
+                       __uint_as_float(__byte_perm(b, 0x4B000000u, 0x7541))), m);
+  q23 = f2_add(f2_pack(__uint_as_float(__byte_perm(b, 0x4B000000u, 0x7542)),
+                       __uint_as_float(__byte_perm(b, 0x4B000000u, 0x7543))), m);
+}
+template <> struct FDot<int8_t, float> {
+  static constexpr int kN = 16;
+  __device__ __forceinline__ static float run(const uint4& w, const uint4* xp) {
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+    f2_t s = 0ull;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint4 xq = xp[32 * q];
+      f2_t q01, q23;
+      i8x4_unpack(ws[q], q01, q23);
+      s = f2_fma(q01, f2_of(xq.x, xq.y), s);
+      s = f2_fma(q23, f2_of(xq.z, xq.w), s);
+    }
+    return f2_sum(s);
+  }
+};
+
+
+// ---------------------------------------------------------------- NF4 (shadow, reading Q27)
+// Two NF4 codes per byte (low nibble = even column); one fp32 absmax per 64 weights of a row,
+// stored row-major [R][C/64]. A 16-byte granule (32 weights) lies inside one block, and since C/32
+// is even the block of granule n of the matrix is n/2: the scale address needs no division.
+struct nf4x2 { uint8_t v; };
+template <typename WT> struct FTraits { static constexpr int bits = 8 * (int)sizeof(WT); static constexpr bool nf4 = false; };
+template <> struct FTraits<nf4x2> { static constexpr int bits = 4; static constexpr bool nf4 = true; };
+template <> struct FDot<nf4x2, uint16_t> { static constexpr int kN = 32; };
+template <> struct FDot<nf4x2, float> { static constexpr int kN = 32; };
+
+// QLoRA's published NF4 codebook (Dettmers et al. 2023)
+__constant__ float kNF4Code[16] = {
+    -1.0f, -0.6961928009986877f, -0.5250730514526367f, -0.39491748809814453f,
+    -0.28444138169288635f, -0.18477343022823334f, -0.09105003625154495f, 0.0f,
+    0.07958029955625534f, 0.16093020141124725f, 0.24611230194568634f, 0.33791524171829224f,
+    0.44070982933044434f, 0.5626170039176941f, 0.7229568362236023f, 1.0f};
+constexpr int kNF4LutWords = 256 * 32;  // byte -> f16x2(code lo, code hi), one copy per lane (no bank conflicts)
+
+__device__ __forceinline__ f2_t h2_unpack(uint32_t v) {
+  float lo, hi;
+  asm("{.reg .f16 l, h;\n mov.b32 {l, h}, %2;\n cvt.f32.f16 %0, l;\n cvt.f32.f16 %1, h;}"
+      : "=f"(lo), "=f"(hi) : "r"(v));
+  return f2_pack(lo, hi);
+}
+__device__ __forceinline__ void nf4_build_lut(uint32_t* lut, int tid, int nthreads) {
+  for (int i = tid; i < kNF4LutWords; i += nthreads) {
+    const int b = i >> 5;
+    const __half2 h = __floats2half2_rn(kNF4Code[b & 15], kNF4Code[b >> 4]);
+    lut[i] = *reinterpret_cast<const uint32_t*>(&h);
+  }
+}
+// 32 weights (one granule) . 32 activations; `lut` already offset by the lane.
+__device__ __forceinline__ float nf4_dot(const uint4& w, const uint4* xp, const uint32_t* lut, uint16_t) {
+  const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+  f2_t s = 0ull;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint4 xq = xp[32 * k];
+    const uint32_t xw[4] = {xq.x, xq.y, xq.z, xq.w};
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+      s = f2_fma(h2_unpack(lut[((ws[k] >> (8 * b)) & 0xFFu) * 32]), bf2_unpack(xw[b]), s);
+  }
+  return f2_sum(s);
+}
+__device__ __forceinline__ float nf4_dot(const uint4& w, const uint4* xp, const uint32_t* lut, float) {
+  const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+  f2_t s = 0ull;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint4 xq = xp[32 * (2 * k + h)];  // activations 8k+4h .. 8k+4h+3
+      s = f2_fma(h2_unpack(lut[((ws[k] >> (16 * h)) & 0xFFu) * 32]), f2_of(xq.x, xq.y), s);
+      s = f2_fma(h2_unpack(lut[((ws[k] >> (16 * h + 8)) & 0xFFu) * 32]), f2_of(xq.z, xq.w), s);
+    }
+  return f2_sum(s);
+}
 
 __device__ __forceinline__ float fbf2(uint32_t w, uint32_t x, float s) {
   s = fmaf(bf16_lo(w), bf16_lo(x), s);
@@ -79,8 +179,8 @@ __device__ __forceinline__ float fbf2(uint32_t w, uint32_t x, float s) {
 }
 template <> struct FDot<__nv_bfloat16, uint16_t> {
   static constexpr int kN = 8;
-  __device__ __forceinline__ static float run(const uint4& w, const uint16_t* x) {
-    const uint4 xv = *reinterpret_cast<const uint4*>(x);
+  __device__ __forceinline__ static float run(const uint4& w, const uint4* xp) {
+    const uint4 xv = xp[0];
 #ifdef FG_F32X2
     f2_t s = f2_fma(bf2_unpack(w.x), bf2_unpack(xv.x), 0ull);
     s = f2_fma(bf2_unpack(w.y), bf2_unpack(xv.y), s);
@@ -120,9 +220,9 @@ __device__ __forceinline__ f2_t i8x4_dot2(uint32_t word, uint32_t x01, uint32_t 
 #endif
 template <> struct FDot<int8_t, uint16_t> {
   static constexpr int kN = 16;
-  __device__ __forceinline__ static float run(const uint4& w, const uint16_t* x) {
-    const uint4 x0 = *reinterpret_cast<const uint4*>(x);
-    const uint4 x1 = *reinterpret_cast<const uint4*>(x + 8);
+  __device__ __forceinline__ static float run(const uint4& w, const uint4* xp) {
+    const uint4 x0 = xp[0];
+    const uint4 x1 = xp[32];
 #ifdef FG_F32X2
     f2_t s = i8x4_dot2(w.x, x0.x, x0.y, 0ull);
     s = i8x4_dot2(w.y, x0.z, x0.w, s);
@@ -173,8 +273,17 @@ template <typename WT, typename XT, int MODE, int UNROLL, typename WaitFn>
 __device__ __forceinline__ void flat_phase(const FlatArgs& a, uint8_t* sm, const WaitFn& wait_dep,
                                            bool ids_ready = false) {
   constexpr int N = FDot<WT, XT>::kN;
+  constexpr int Q = N * (int)sizeof(XT) / 16;       // uint4 activation words per granule
+  constexpr int EPU = 16 / (int)sizeof(XT);         // activations per uint4
+  static_assert(Q >= 1 && (Q & (Q - 1)) == 0, "Q must be a power of two");
+  // natural uint4 index o of the activation vector -> its swizzled slot (see FDot)
+  auto swz4 = [](int o) { const int q = o & (Q - 1), t = o / Q; return ((t >> 5) * Q + q) * 32 + (t & 31); };
+  auto swz = [&](int e) { return swz4(e / EPU) * EPU + (e & (EPU - 1)); };
+  constexpr bool kNF4 = FTraits<WT>::nf4;
+  static_assert(!kNF4 || FG_PIPE == 0, "NF4 is implemented for the default pipeline");
   float* part = reinterpret_cast<float*>(sm);                          // [warps][rows_cap]
   XT* xs = reinterpret_cast<XT*>(part + kFG_WARPS * a.rows_cap);       // [C]
+  uint32_t* lut = reinterpret_cast<uint32_t*>(xs + a.C);               // NF4 only: [256][32]
   __shared__ float red[kFG_WARPS + 1];
   __shared__ unsigned long long kbest[kFG_WARPS];
   __shared__ bool is_last;
@@ -203,8 +312,10 @@ __device__ __forceinline__ void flat_phase(const FlatArgs& a, uint8_t* sm, const
         }
       }
       const int id = ex.base + ex.ids[gate_idx];
-      W = reinterpret_cast<const WT*>(ex.tbl[id]) + (a.second ? 2LL * a.F_full * a.d_full : 0LL);
-      sc = ex.stbl ? ex.stbl[id] + (a.second ? 2 * a.F_full : 0) : nullptr;
+      W = reinterpret_cast<const WT*>(reinterpret_cast<const char*>(ex.tbl[id]) +
+                                      (a.second ? 2LL * a.F_full * a.d_full * FTraits<WT>::bits / 8 : 0LL));
+      sc = ex.stbl ? ex.stbl[id] + (a.second ? (kNF4 ? 2LL * a.F_full * a.d_full / 64 : 2LL * a.F_full) : 0LL)
+                   : nullptr;
     }
   }
   long long rb, re;
@@ -225,18 +336,24 @@ __device__ __forceinline__ void flat_phase(const FlatArgs& a, uint8_t* sm, const
 #else
   const long long g_begin = G * warp / kFG_WARPS, g_end = G * (warp + 1) / kFG_WARPS;
 #endif
-  const uint4* base = reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(W) + rb * (long long)a.C * sizeof(WT));
+  const uint4* base = reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(W) +
+                                                     rb * (long long)a.C * FTraits<WT>::bits / 8);
+  const float* scb = kNF4 ? sc + ((rb * Cg) >> 1) : nullptr;  // block absmax of this CTA's first row
 
   // The weights do not depend on the previous kernel: issue this warp's first batch before the
   // programmatic-dependent-launch wait (no-op without PDL), then stage the activations.
   const uint64_t pol = l2_policy(a.evict_first != 0);
   uint4 wa[UNROLL], wb[UNROLL];
+  float sa[UNROLL], sb[UNROLL];  // NF4 block scales of the batch (unused otherwise)
 #if FG_PIPE == 2
   uint4 wc[UNROLL];
 #endif
 #pragma unroll
   for (int i = 0; i < UNROLL; ++i)
-    if (g_begin + i < g_end) wa[i] = ld_stream_pol(base + (g_begin + i) * 32 + lane, pol);
+    if (g_begin + i < g_end) {
+      wa[i] = ld_stream_pol(base + (g_begin + i) * 32 + lane, pol);
+      if constexpr (kNF4) sa[i] = __ldg(scb + (((g_begin + i) * 32 + lane) >> 1));
+    }
 #if FG_PIPE >= 1
 #pragma unroll
   for (int i = 0; i < UNROLL; ++i)
@@ -268,18 +385,18 @@ __device__ __forceinline__ void flat_phase(const FlatArgs& a, uint8_t* sm, const
       const float v = a.h[j] * rstd;
       if constexpr (std::is_same<XT, uint16_t>::value) {
         const __nv_bfloat16 b = __float2bfloat16_rn(v);
-        xs[j] = *reinterpret_cast<const uint16_t*>(&b);
+        xs[swz(j)] = *reinterpret_cast<const uint16_t*>(&b);
       } else {
-        xs[j] = v;
+        xs[swz(j)] = v;
       }
     }
   } else if constexpr (std::is_same<XT, uint16_t>::value) {
     const uint4* s4 = reinterpret_cast<const uint4*>(a.x);
-    for (int i = tid; i < a.C / 8; i += kFG_THREADS) reinterpret_cast<uint4*>(xs)[i] = s4[i];
+    for (int i = tid; i < a.C / 8; i += kFG_THREADS) reinterpret_cast<uint4*>(xs)[swz4(i)] = s4[i];
   } else {
     if (a.x_bf16) {
       const uint16_t* s16 = reinterpret_cast<const uint16_t*>(a.x);
-      for (int i = tid; i < a.C; i += kFG_THREADS) xs[i] = __uint_as_float((uint32_t)s16[i] << 16);
+      for (int i = tid; i < a.C; i += kFG_THREADS) xs[swz(i)] = __uint_as_float((uint32_t)s16[i] << 16);
     } else {
       // all loads of a thread first (latency-bound otherwise: 57 KB per CTA for W2)
       const float4* s4 = reinterpret_cast<const float4*>(a.x);
@@ -291,22 +408,28 @@ __device__ __forceinline__ void flat_phase(const FlatArgs& a, uint8_t* sm, const
           if (i0 + u * kFG_THREADS < n4) v[u] = s4[i0 + u * kFG_THREADS];
 #pragma unroll
         for (int u = 0; u < 8; ++u)
-          if (i0 + u * kFG_THREADS < n4) reinterpret_cast<float4*>(xs)[i0 + u * kFG_THREADS] = v[u];
+          if (i0 + u * kFG_THREADS < n4) reinterpret_cast<float4*>(xs)[swz4(i0 + u * kFG_THREADS)] = v[u];
       }
     }
   }
   for (int i = tid; i < kFG_WARPS * a.rows_cap; i += kFG_THREADS) part[i] = 0.f;
+  if constexpr (kNF4) nf4_build_lut(lut, tid, kFG_THREADS);
   __syncthreads();
+  const uint32_t* lut_l = lut + lane;
 
   int row = (int)(g_begin / Gr);
   int gcol = (int)(g_begin - (long long)row * Gr);   // group index within the row
   float acc = 0.f;
   // consume one register batch (rows are whole groups: a boundary is one compare)
-  auto consume = [&](const uint4 (&wv)[UNROLL], long long g0) {
+  auto consume = [&](const uint4 (&wv)[UNROLL], const float (&sv)[UNROLL], long long g0) {
 #pragma unroll
     for (int i = 0; i < UNROLL; ++i) {
       if (g0 + i < g_end) {
-        acc += FDot<WT, XT>::run(wv[i], xs + (size_t)(gcol * 32 + lane) * N);
+        const uint4* xp = reinterpret_cast<const uint4*>(xs) + (size_t)gcol * Q * 32 + lane;
+        if constexpr (kNF4)
+          acc = fmaf(sv[i], nf4_dot(wv[i], xp, lut_l, XT{}), acc);
+        else
+          acc += FDot<WT, XT>::run(wv[i], xp);
         if (++gcol == Gr) {  // row complete (warp-uniform)
           const float t = warp_sum(acc);
           if (lane == 0) part[warp * a.rows_cap + row] += t;
@@ -324,7 +447,7 @@ __device__ __forceinline__ void flat_phase(const FlatArgs& a, uint8_t* sm, const
     auto consume_at = [&](const uint4 (&wv)[UNROLL], long long g0) {
       row = (int)(g0 / Gr);
       gcol = (int)(g0 - (long long)row * Gr);
-      consume(wv, g0);
+      consume(wv, sa, g0);
       if (gcol != 0) {  // batch ended inside a row: flush the partial now (rows are shared by warps)
         const float t = warp_sum(acc);
         if (lane == 0) part[warp * a.rows_cap + row] += t;
@@ -350,22 +473,28 @@ __device__ __forceinline__ void flat_phase(const FlatArgs& a, uint8_t* sm, const
     const long long g1 = g0 + UNROLL, g2 = g0 + 2 * UNROLL;
 #pragma unroll
     for (int i = 0; i < UNROLL; ++i)
-      if (g1 + i < g_end) wb[i] = ld_stream_pol(base + (g1 + i) * 32 + lane, pol);
-    consume(wa, g0);
+      if (g1 + i < g_end) {
+        wb[i] = ld_stream_pol(base + (g1 + i) * 32 + lane, pol);
+        if constexpr (kNF4) sb[i] = __ldg(scb + (((g1 + i) * 32 + lane) >> 1));
+      }
+    consume(wa, sa, g0);
 #pragma unroll
     for (int i = 0; i < UNROLL; ++i)
-      if (g2 + i < g_end) wa[i] = ld_stream_pol(base + (g2 + i) * 32 + lane, pol);
-    if (g1 < g_end) consume(wb, g1);
+      if (g2 + i < g_end) {
+        wa[i] = ld_stream_pol(base + (g2 + i) * 32 + lane, pol);
+        if constexpr (kNF4) sa[i] = __ldg(scb + (((g2 + i) * 32 + lane) >> 1));
+      }
+    if (g1 < g_end) consume(wb, sb, g1);
   }
 #elif FG_PIPE == 1
   // both batches issued before the dependency wait; consume one, re-issue it two batches ahead
   for (long long g0 = g_begin; g0 < g_end; g0 += 2 * UNROLL) {
     const long long g1 = g0 + UNROLL, g2 = g0 + 2 * UNROLL, g3 = g0 + 3 * UNROLL;
-    consume(wa, g0);
+    consume(wa, sa, g0);
 #pragma unroll
     for (int i = 0; i < UNROLL; ++i)
       if (g2 + i < g_end) wa[i] = ld_stream_pol(base + (g2 + i) * 32 + lane, pol);
-    if (g1 < g_end) consume(wb, g1);
+    if (g1 < g_end) consume(wb, sb, g1);
 #pragma unroll
     for (int i = 0; i < UNROLL; ++i)
       if (g3 + i < g_end) wb[i] = ld_stream_pol(base + (g3 + i) * 32 + lane, pol);
@@ -374,15 +503,15 @@ __device__ __forceinline__ void flat_phase(const FlatArgs& a, uint8_t* sm, const
   // three register batches: two stay in flight while one is consumed
   for (long long g0 = g_begin; g0 < g_end; g0 += 3 * UNROLL) {
     const long long g1 = g0 + UNROLL, g2 = g0 + 2 * UNROLL;
-    consume(wa, g0);
+    consume(wa, sa, g0);
 #pragma unroll
     for (int i = 0; i < UNROLL; ++i)
       if (g0 + 3 * UNROLL + i < g_end) wa[i] = ld_stream_pol(base + (g0 + 3 * UNROLL + i) * 32 + lane, pol);
-    if (g1 < g_end) consume(wb, g1);
+    if (g1 < g_end) consume(wb, sb, g1);
 #pragma unroll
     for (int i = 0; i < UNROLL; ++i)
       if (g0 + 4 * UNROLL + i < g_end) wb[i] = ld_stream_pol(base + (g0 + 4 * UNROLL + i) * 32 + lane, pol);
-    if (g2 < g_end) consume(wc, g2);
+    if (g2 < g_end) consume(wc, sa, g2);
 #pragma unroll
     for (int i = 0; i < UNROLL; ++i)
       if (g0 + 5 * UNROLL + i < g_end) wc[i] = ld_stream_pol(base + (g0 + 5 * UNROLL + i) * 32 + lane, pol);
@@ -402,7 +531,7 @@ __device__ __forceinline__ void flat_phase(const FlatArgs& a, uint8_t* sm, const
         g += part[w * a.rows_cap + 2 * p];
         v += part[w * a.rows_cap + 2 * p + 1];
       }
-      if (sc != nullptr) { g *= sc[rb + 2 * p]; v *= sc[rb + 2 * p + 1]; }
+      if (!kNF4 && sc != nullptr) { g *= sc[rb + 2 * p]; v *= sc[rb + 2 * p + 1]; }
       a.out[rb / 2 + p] = silu_mul(g, v);
     }
   } else if (MODE == 1) {
@@ -411,7 +540,7 @@ __device__ __forceinline__ void flat_phase(const FlatArgs& a, uint8_t* sm, const
       float s = 0.f;
 #pragma unroll
       for (int w = 0; w < kFG_WARPS; ++w) s += part[w * a.rows_cap + r];
-      if (sc != nullptr) s *= sc[rb + r];
+      if (!kNF4 && sc != nullptr) s *= sc[rb + r];
       a.out[rb + r] = gw * s;
     }
   } else {
@@ -502,7 +631,8 @@ static cudaError_t fg_launch(FlatArgs a, cudaStream_t s, bool pdl) {
   const long long units = MODE == 0 ? a.R / 2 : a.R;
   const int grid = (int)(units < sms ? (units > 0 ? units : 1) : sms);
   a.rows_cap = (int)((units + grid - 1) / grid) * (MODE == 0 ? 2 : 1) + 2;
-  const size_t smem = (size_t)kFG_WARPS * a.rows_cap * sizeof(float) + (size_t)a.C * sizeof(XT) + 16;
+  const size_t smem = (size_t)kFG_WARPS * a.rows_cap * sizeof(float) + (size_t)a.C * sizeof(XT) + 16 +
+                      (FTraits<WT>::nf4 ? kNF4LutWords * 4 : 0);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   auto kern = flat_gemv_kernel<WT, XT, MODE, UNROLL>;
   if (smem > 40 * 1024) {
@@ -531,6 +661,7 @@ cudaError_t launch_w13_flat(ExpertRef ex, WType wt, const void* u, int u_f32, fl
     case W_BF16: return fg_launch<__nv_bfloat16, uint16_t, 0>(a, s, pdl);
     case W_F32: return fg_launch<float, float, 0>(a, s, pdl);
     case W_I8: return fg_launch<int8_t, uint16_t, 0>(a, s, pdl);
+    case W_NF4: return fg_launch<nf4x2, uint16_t, 0>(a, s, pdl);
   }
   return cudaErrorInvalidValue;
 }
@@ -544,6 +675,7 @@ cudaError_t launch_w2_flat(ExpertRef ex, WType wt, const float* act, const float
     case W_BF16: return fg_launch<__nv_bfloat16, float, 1>(a, s, pdl);
     case W_F32: return fg_launch<float, float, 1>(a, s, pdl);
     case W_I8: return fg_launch<int8_t, float, 1>(a, s, pdl);
+    case W_NF4: return fg_launch<nf4x2, float, 1>(a, s, pdl);
   }
   return cudaErrorInvalidValue;
 }
@@ -589,8 +721,9 @@ static cudaError_t fused_launch(FlatArgs a13, FlatArgs a2, cudaStream_t s, bool 
   const int grid = (int)(units < sms ? (units > 0 ? units : 1) : sms);
   a13.rows_cap = (int)((a13.R / 2 + grid - 1) / grid) * 2 + 2;
   a2.rows_cap = (int)((a2.R + grid - 1) / grid) + 2;
-  const size_t s1 = (size_t)kFG_WARPS * a13.rows_cap * sizeof(float) + (size_t)a13.C * sizeof(XT) + 16;
-  const size_t s2 = (size_t)kFG_WARPS * a2.rows_cap * sizeof(float) + (size_t)a2.C * sizeof(float) + 16;
+  const size_t lut = FTraits<WT>::nf4 ? kNF4LutWords * 4 : 0;
+  const size_t s1 = (size_t)kFG_WARPS * a13.rows_cap * sizeof(float) + (size_t)a13.C * sizeof(XT) + 16 + lut;
+  const size_t s2 = (size_t)kFG_WARPS * a2.rows_cap * sizeof(float) + (size_t)a2.C * sizeof(float) + 16 + lut;
   const size_t smem = s1 > s2 ? s1 : s2;
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   auto kern = flat_expert_kernel<WT, XT, UNROLL>;
@@ -633,8 +766,72 @@ cudaError_t launch_expert_fused(ExpertRef ex, const void* w2_direct, const float
     case W_BF16: return fused_launch<__nv_bfloat16, uint16_t>(a13, a2, s, pdl);
     case W_F32: return fused_launch<float, float>(a13, a2, s, pdl);
     case W_I8: return fused_launch<int8_t, uint16_t>(a13, a2, s, pdl);
+    case W_NF4: return fused_launch<nf4x2, uint16_t>(a13, a2, s, pdl);
   }
   return cudaErrorInvalidValue;
+}
+
+// ---------------------------------------------------------------- NF4, small shapes
+// Rows shorter than one 512-byte group (C % 1024 != 0) cannot use the flat stream: one warp per
+// output unit (a W1/W3 row pair, or a W2 row), one byte (two weights) per lane step. Test sizes
+// and odd shapes only; the Mixtral shapes take the flat kernel above.
+template <int MODE>
+__global__ void __launch_bounds__(256) nf4_rowwarp_kernel(ExpertRef ex, int second, const void* x, int x_f32,
+                                                         int R, int C, int d_full, int F_full,
+                                                         const float* gate_w, float* out) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int lane = threadIdx.x & 31;
+  const int unit = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const uint8_t* Wb;
+  const float* sc;
+  int gate_idx = ex.sel;
+  if (ex.tbl == nullptr) {
+    Wb = reinterpret_cast<const uint8_t*>(ex.blob);
+    sc = ex.scales;
+  } else {
+    if (ex.sorted) {
+      for (int j = 0; j < ex.k; ++j) {
+        int rank = 0;
+        for (int i = 0; i < ex.k; ++i) rank += ex.ids[i] < ex.ids[j];
+        if (rank == ex.sel) gate_idx = j;
+      }
+    }
+    const int id = ex.base + ex.ids[gate_idx];
+    Wb = reinterpret_cast<const uint8_t*>(ex.tbl[id]) + (second ? (size_t)F_full * d_full : 0);
+    sc = ex.stbl[id] + (second ? (size_t)2 * F_full * d_full / 64 : 0);
+  }
+  const int nunits = MODE == 0 ? R / 2 : R;
+  if (unit >= nunits) return;
+  auto xv = [&](int j) -> float {
+    return x_f32 ? reinterpret_cast<const float*>(x)[j]
+                 : __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(x)[j] << 16);
+  };
+  float acc[2] = {0.f, 0.f};
+  for (int q = 0; q < (MODE == 0 ? 2 : 1); ++q) {
+    const int r = MODE == 0 ? 2 * unit + q : unit;
+    float t = 0.f;
+    for (int jb = lane; jb < C / 2; jb += 32) {
+      const uint8_t b = Wb[(size_t)r * (C / 2) + jb];
+      const float a = sc[(size_t)r * (C / 64) + (2 * jb) / 64];
+      t = fmaf(a, kNF4Code[b & 15] * xv(2 * jb) + kNF4Code[b >> 4] * xv(2 * jb + 1), t);
+    }
+    acc[q] = warp_sum(t);
+  }
+  if (lane == 0) {
+    if (MODE == 0) out[unit] = silu_mul(acc[0], acc[1]);
+    else out[unit] = (gate_w ? gate_w[gate_idx] : 1.f) * acc[0];
+  }
+}
+
+cudaError_t launch_nf4_small(ExpertRef ex, int second, const void* x, int x_f32, int d, int F, const float* gate_w,
+                             float* out, cudaStream_t s) {
+  const int R = second ? d : 2 * F, C = second ? F : d;
+  if (C % 64) return cudaErrorInvalidValue;
+  const int units = second ? R : R / 2;
+  const int grid = (units + 7) / 8;
+  if (second) nf4_rowwarp_kernel<1><<<grid, 256, 0, s>>>(ex, 1, x, 1, R, C, d, F, gate_w, out);
+  else nf4_rowwarp_kernel<0><<<grid, 256, 0, s>>>(ex, 0, x, x_f32, R, C, d, F, gate_w, out);
+  return cudaGetLastError();
 }
 
 }  // namespace odmoe

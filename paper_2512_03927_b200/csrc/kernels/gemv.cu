@@ -191,6 +191,9 @@ int gemv_engine() {
 
 cudaError_t launch_w13(ExpertRef ex, WType wt, const void* u, int u_f32, float* a, int d, int F,
                        cudaStream_t s, bool pdl) {
+  if (wt == W_NF4)
+    return stream_ok(wt, d) ? launch_w13_flat(ex, wt, u, u_f32, a, d, F, s, pdl)
+                            : launch_nf4_small(ex, 0, u, u_f32, d, F, nullptr, a, s);
   if (stream_ok(wt, d)) {
     if (gemv_engine() == 2) return launch_w13_flat(ex, wt, u, u_f32, a, d, F, s, pdl);
     if (gemv_engine() == 1) return launch_w13_stream(ex, wt, u, u_f32, a, d, F, s);
@@ -199,12 +202,16 @@ cudaError_t launch_w13(ExpertRef ex, WType wt, const void* u, int u_f32, float* 
     case W_BF16: return w13_impl<__nv_bfloat16>(ex, u, u_f32, a, d, F, s);
     case W_F32: return w13_impl<float>(ex, u, u_f32, a, d, F, s);
     case W_I8: return w13_impl<int8_t>(ex, u, u_f32, a, d, F, s);
+    default: break;
   }
   return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_w2(ExpertRef ex, WType wt, const float* a, const float* gate_w, float* y, int d,
                       int F, cudaStream_t s, bool pdl) {
+  if (wt == W_NF4)
+    return stream_ok(wt, F) ? launch_w2_flat(ex, wt, a, gate_w, y, d, F, s, pdl)
+                            : launch_nf4_small(ex, 1, a, 1, d, F, gate_w, y, s);
   if (stream_ok(wt, F)) {
     if (gemv_engine() == 2) return launch_w2_flat(ex, wt, a, gate_w, y, d, F, s, pdl);
     if (gemv_engine() == 1) return launch_w2_stream(ex, wt, a, gate_w, y, d, F, s);
@@ -213,6 +220,7 @@ cudaError_t launch_w2(ExpertRef ex, WType wt, const float* a, const float* gate_
     case W_BF16: return w2_impl<__nv_bfloat16>(ex, a, gate_w, y, d, F, s);
     case W_F32: return w2_impl<float>(ex, a, gate_w, y, d, F, s);
     case W_I8: return w2_impl<int8_t>(ex, a, gate_w, y, d, F, s);
+    default: break;
   }
   return cudaErrorInvalidValue;
 }

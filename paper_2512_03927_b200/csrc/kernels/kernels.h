@@ -5,7 +5,10 @@
 
 namespace odmoe {
 
-enum WType { W_BF16 = 0, W_F32 = 1, W_I8 = 2 };
+enum WType { W_BF16 = 0, W_F32 = 1, W_I8 = 2, W_NF4 = 3 };
+// W_NF4 (shadow experts only, reading Q27): two 4-bit codes per byte (low nibble = even column),
+// "scales" = fp32 absmax per 64-weight block of a row, [R][C/64]; expert blob = codes of W13 then
+// W2 (3dF/2 bytes), scale array = W13 blocks then W2 blocks.
 
 int num_sms();  // cached SM count of the current device
 
@@ -55,6 +58,12 @@ cudaError_t launch_w2_flat(ExpertRef ex, WType wt, const float* act, const float
 cudaError_t launch_lm_head_flat(const float* h, const void* W, WType wt, int V, int d, float eps,
                                 int32_t* token_out, float* logits, void* scratch, cudaStream_t s, bool pdl);
 bool use_fused_expert();  // env ODMOE_FUSED=0 disables (A/B)
+// NF4 rows shorter than one flat group: warp-per-row kernel (x: bf16 unless x_f32; W2 x = fp32)
+cudaError_t launch_nf4_small(ExpertRef ex, int second, const void* x, int x_f32, int d, int F, const float* gate_w,
+                             float* out, cudaStream_t s);
+// NF4 blockwise quantiser (reading Q27): codes [R][C/2] bytes, absmax [R][C/64]; C % 64 == 0
+cudaError_t launch_quantize_nf4(const void* w, int64_t R, int64_t C, WType wt, uint8_t* q, float* absmax,
+                                cudaStream_t s);
 // Fused expert FFN (flat engine): W13+SwiGLU -> grid barrier -> W2+gate in ONE cooperative
 // launch. Direct mode: ex.blob/ex.scales = W13 (+ scales), w2_direct/s2_direct = W2 (+ scales);
 // indirect mode: the expert table entries (whole blobs). a_buf: fp32 [F] scratch.

@@ -177,6 +177,7 @@ cudaError_t launch_embed(const void* emb, const float* emb_scale, WType wt, cons
     case W_BF16: embed_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)emb, nullptr, token, d, h); break;
     case W_F32: embed_kernel<float><<<grid, 256, 0, s>>>((const float*)emb, nullptr, token, d, h); break;
     case W_I8: embed_kernel<int8_t><<<grid, 256, 0, s>>>((const int8_t*)emb, emb_scale, token, d, h); break;
+    default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
 }

@@ -246,6 +246,7 @@ cudaError_t launch_router(float* h, const float* const* y_add, int n_add, const 
     case W_I8:
       return router_impl<int8_t>(h, y_add, n_add, nullptr, w_gate, wg_scale, m, E, d, k, eps, u_out, ids, w,
                                  logits, flag, s, pdl);
+    default: break;
   }
   return cudaErrorInvalidValue;
 }

@@ -362,6 +362,7 @@ static cudaError_t sg_launch(StreamArgs a, cudaStream_t s) {
 // Whether the streaming engine handles a [R, C] matrix of type wt (rows must be whole 512-byte
 // groups; activations must fit in shared memory next to the ring).
 bool stream_ok(WType wt, int C) {
+  if (wt == W_NF4) return C % 1024 == 0 && (long long)C * 4 <= 64 * 1024;  // flat engine only
   const int esz = wt == W_F32 ? 4 : (wt == W_BF16 ? 2 : 1);
   return ((long long)C * esz) % 512 == 0 && (long long)C * 4 <= 64 * 1024;
 }
@@ -375,6 +376,7 @@ cudaError_t launch_w13_stream(ExpertRef ex, WType wt, const void* u, int u_f32, 
     case W_BF16: return sg_launch<__nv_bfloat16, uint16_t, 0>(a, s);
     case W_F32: return sg_launch<float, float, 0>(a, s);
     case W_I8: return sg_launch<int8_t, uint16_t, 0>(a, s);
+    default: break;
   }
   return cudaErrorInvalidValue;
 }
@@ -388,6 +390,7 @@ cudaError_t launch_w2_stream(ExpertRef ex, WType wt, const float* act, const flo
     case W_BF16: return sg_launch<__nv_bfloat16, float, 1>(a, s);
     case W_F32: return sg_launch<float, float, 1>(a, s);
     case W_I8: return sg_launch<int8_t, float, 1>(a, s);
+    default: break;
   }
   return cudaErrorInvalidValue;
 }

@@ -48,7 +48,8 @@ struct Ctx {
 
   // shadow model (rank 0)
   bool has_shadow = false;
-  WType sh_wt = W_I8;
+  WType sh_wt = W_I8;    // shadow embedding / router weights
+  WType sh_ewt = W_I8;   // shadow expert weights (W_NF4 for the NF4 shadow)
   void* sh_emb = nullptr;      // int8 [V,d] (or main dtype for SHADOW_SAME)
   float* sh_semb = nullptr;    // [V]
   void* sh_router = nullptr;   // [L][E][d]

@@ -66,7 +66,8 @@ odmoe_status guard(Ctx* c, F&& f) {
 
 inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 inline bool is_shadow(int p) {
-  return p == ODMOE_PRED_SHADOW_INT8 || p == ODMOE_PRED_SHADOW_SAME || p == ODMOE_PRED_SHADOW_BF16;
+  return p == ODMOE_PRED_SHADOW_INT8 || p == ODMOE_PRED_SHADOW_SAME || p == ODMOE_PRED_SHADOW_BF16 ||
+         p == ODMOE_PRED_SHADOW_NF4;
 }
 inline WType wtype(int dt) { return dt == ODMOE_FP32 ? W_F32 : W_BF16; }
 inline size_t dsize(int dt) { return dt == ODMOE_FP32 ? 4 : 2; }
@@ -190,7 +191,8 @@ void validate(const odmoe_config* g) {
   if (g->k > g->E || g->k > 8 || g->E > 64) bad("need 1 <= k <= E <= 64 and k <= 8");
   if (g->d % 8 || g->F % 8) bad("d and F must be multiples of 8");
   if (g->dtype != ODMOE_BF16 && g->dtype != ODMOE_FP32) bad("dtype");
-  if (g->predictor < 0 || g->predictor > 6) bad("predictor");
+  if (g->predictor < 0 || g->predictor > 7) bad("predictor");
+  if (g->predictor == ODMOE_PRED_SHADOW_NF4 && (g->d % 64 || g->F % 64)) bad("the NF4 shadow needs d, F multiples of 64");
   if (g->lookahead < 1) bad("lookahead must be >= 1");
   if (g->world_size < 1 || g->rank < 0 || g->rank >= g->world_size) bad("rank/world_size");
   const int G = g->group_size > 0 ? g->group_size : std::min(g->k, g->world_size);
@@ -223,7 +225,7 @@ void build_shadow(Ctx* c, char* staging) {
   const int L = c->L, E = c->E, d = c->d, V = c->V, F = c->F;
   if (c->cfg.predictor == ODMOE_PRED_SHADOW_SAME) {
     // The shadow runs the main model's own weights (recall must be exactly 1.0).
-    c->sh_wt = c->wt;
+    c->sh_wt = c->sh_ewt = c->wt;
     c->sh_emb = c->d_emb;
     c->sh_router = c->d_router;
     c->d_sh_tbl = c->d_res_tbl;
@@ -232,7 +234,7 @@ void build_shadow(Ctx* c, char* staging) {
   }
   if (c->cfg.predictor == ODMOE_PRED_SHADOW_BF16) {
     // BF16 copy of the FP32 main model (round to nearest even), no scales
-    c->sh_wt = W_BF16;
+    c->sh_wt = c->sh_ewt = W_BF16;
     c->sh_emb = dmalloc<char>(c, (size_t)V * d * 2, "shadow emb bf16");
     c->sh_router = dmalloc<char>(c, (size_t)L * E * d * 2, "shadow router bf16");
     CUDA_OK(c, launch_f32_to_bf16((const float*)c->d_emb, c->sh_emb, (int64_t)V * d, c->s_main));
@@ -255,7 +257,9 @@ void build_shadow(Ctx* c, char* staging) {
     CUDA_OK(c, cudaStreamSynchronize(c->s_main));
     return;
   }
+  const bool nf4 = c->cfg.predictor == ODMOE_PRED_SHADOW_NF4;
   c->sh_wt = W_I8;
+  c->sh_ewt = nf4 ? W_NF4 : W_I8;
   c->sh_emb = dmalloc<int8_t>(c, (size_t)V * d, "shadow emb");
   c->sh_semb = dmalloc<float>(c, V, "shadow emb scales");
   c->sh_router = dmalloc<int8_t>(c, (size_t)L * E * d, "shadow router");
@@ -267,14 +271,25 @@ void build_shadow(Ctx* c, char* staging) {
   for (int l = 0; l < L; ++l)
     for (int e = 0; e < E; ++e) {
       const size_t i = (size_t)l * E + e;
-      int8_t* q = dmalloc<int8_t>(c, (size_t)3 * F * d, "shadow expert");
-      float* s = dmalloc<float>(c, (size_t)2 * F + d, "shadow scales");
       const char* src = staging;
       if (!c->res_blob.empty() && c->res_blob[i]) {
         src = c->res_blob[i];
       } else {
         CUDA_OK(c, launch_gen(staging, 0, l, e, 0, 0, 0, d, F, c->cfg.weight_seed, c->wt, c->s_main));
       }
+      if (nf4) {  // codes W13 [2F][d/2] then W2 [d][F/2]; absmax W13 [2F][d/64] then W2 [d][F/64]
+        uint8_t* q = dmalloc<uint8_t>(c, (size_t)3 * F * d / 2, "shadow expert nf4");
+        float* s = dmalloc<float>(c, (size_t)3 * F * d / 64, "shadow nf4 absmax");
+        CUDA_OK(c, launch_quantize_nf4(src, 2LL * F, d, c->wt, q, s, c->s_main));
+        CUDA_OK(c, launch_quantize_nf4(src + (size_t)2 * F * d * c->esz, d, F, c->wt, q + (size_t)F * d,
+                                       s + (size_t)2 * F * d / 64, c->s_main));
+        c->sh_blob[i] = q;
+        c->sh_sc[i] = s;
+        c->stats.shadow_bytes += (int64_t)3 * F * d / 2 + (int64_t)3 * F * d / 64 * 4;
+        continue;
+      }
+      int8_t* q = dmalloc<int8_t>(c, (size_t)3 * F * d, "shadow expert");
+      float* s = dmalloc<float>(c, (size_t)2 * F + d, "shadow scales");
       CUDA_OK(c, launch_quantize(src, 2LL * F, d, c->wt, q, s, c->s_main));
       CUDA_OK(c, launch_quantize(src + (size_t)2 * F * d * c->esz, d, F, c->wt, q + (size_t)2 * F * d, s + 2 * F, c->s_main));
       c->sh_blob[i] = q;
@@ -499,11 +514,11 @@ void enqueue_shadow(Ctx* c, const int32_t* token_dev) {
                    c->sh_ids + (size_t)l * k, j, l * E, k, 0};
       {
         KTimer t(c, K_SHADOW, s);
-        CUDA_OK(c, launch_w13(ex, swt, c->sh_u, u_f32, c->sh_a + (size_t)j * F, d, F, s, true));
+        CUDA_OK(c, launch_w13(ex, c->sh_ewt, c->sh_u, u_f32, c->sh_a + (size_t)j * F, d, F, s, true));
       }
       {
         KTimer t(c, K_SHADOW, s);
-        CUDA_OK(c, launch_w2(ex, swt, c->sh_a + (size_t)j * F, c->sh_w + (size_t)l * k, c->sh_y + (size_t)j * d, d, F, s, true));
+        CUDA_OK(c, launch_w2(ex, c->sh_ewt, c->sh_a + (size_t)j * F, c->sh_w + (size_t)l * k, c->sh_y + (size_t)j * d, d, F, s, true));
       }
     }
   }
@@ -606,8 +621,8 @@ void enqueue_refine(Ctx* c, int j) {
   for (int i = 0; i < k; ++i) {
     ExpertRef ex{nullptr, nullptr, (const void* const*)c->d_sh_tbl, (const float* const*)c->d_sh_stbl,
                  (const int32_t*)(pkt + c->pkt_ids_off), i, j * E, k, 0};
-    { KTimer t(c, K_SHADOW, s); CUDA_OK(c, launch_w13(ex, swt, pkt, 0, c->rf_a + (size_t)i * F, d, F, s)); }
-    { KTimer t(c, K_SHADOW, s); CUDA_OK(c, launch_w2(ex, swt, c->rf_a + (size_t)i * F, (const float*)(pkt + c->pkt_w_off), c->rf_y + (size_t)i * d, d, F, s, true)); }
+    { KTimer t(c, K_SHADOW, s); CUDA_OK(c, launch_w13(ex, c->sh_ewt, pkt, 0, c->rf_a + (size_t)i * F, d, F, s)); }
+    { KTimer t(c, K_SHADOW, s); CUDA_OK(c, launch_w2(ex, c->sh_ewt, c->rf_a + (size_t)i * F, (const float*)(pkt + c->pkt_w_off), c->rf_y + (size_t)i * d, d, F, s, true)); }
   }
   for (int r = 1; r <= R && j + r < L; ++r) {
     const int m = j + r;
@@ -621,8 +636,8 @@ void enqueue_refine(Ctx* c, int j) {
       for (int i = 0; i < k; ++i) {
         ExpertRef ex{nullptr, nullptr, (const void* const*)c->d_sh_tbl, (const float* const*)c->d_sh_stbl,
                      out + (size_t)(r - 1) * k, i, m * E, k, 0};
-        { KTimer t(c, K_SHADOW, s); CUDA_OK(c, launch_w13(ex, swt, c->rf_u, 0, c->rf_a + (size_t)i * F, d, F, s, true)); }
-        { KTimer t(c, K_SHADOW, s); CUDA_OK(c, launch_w2(ex, swt, c->rf_a + (size_t)i * F, c->rf_w + (size_t)(r - 1) * k, c->rf_y + (size_t)i * d, d, F, s, true)); }
+        { KTimer t(c, K_SHADOW, s); CUDA_OK(c, launch_w13(ex, c->sh_ewt, c->rf_u, 0, c->rf_a + (size_t)i * F, d, F, s, true)); }
+        { KTimer t(c, K_SHADOW, s); CUDA_OK(c, launch_w2(ex, c->sh_ewt, c->rf_a + (size_t)i * F, c->rf_w + (size_t)(r - 1) * k, c->rf_y + (size_t)i * d, d, F, s, true)); }
       }
     }
   }
@@ -1538,7 +1553,7 @@ odmoe_status odmoe_set_option(void* ctx, int key, int64_t value) {
       if (value < 1) fail(c, ODMOE_E_CONFIG, "lookahead must be >= 1");
       c->cfg.lookahead = (int32_t)value;
     } else if (key == 2) {
-      if (value < 0 || value > 6) fail(c, ODMOE_E_CONFIG, "predictor");
+      if (value < 0 || value > 7) fail(c, ODMOE_E_CONFIG, "predictor");
       const bool wants_shadow = is_shadow((int)value);
       if (wants_shadow && value != c->built_pred)
         fail(c, ODMOE_E_STATE, "this ctx was not created with that shadow predictor");
@@ -1759,6 +1774,21 @@ odmoe_status odmoe_shadow_expert_ffn(const int8_t* q13, const float* s13, const 
   return ODMOE_OK;
 }
 
+odmoe_status odmoe_shadow_expert_ffn_nf4(const uint8_t* q13, const float* a13, const uint8_t* q2,
+                                         const float* a2, const void* u, const float* gate_w, int gate_idx,
+                                         int d, int F, float* a_scratch, float* y, void* stream) {
+  if (!q13 || !a13 || !q2 || !a2 || !u || !a_scratch || !y || d < 64 || F < 64 || d % 64 || F % 64 || gate_idx < 0)
+    return ODMOE_E_CONFIG;
+  if (use_fused_expert() && stream_ok(W_NF4, d) && stream_ok(W_NF4, F))
+    return launch_expert_fused(direct_ref(q13, a13, gate_idx), q2, a2, W_NF4, u, 0, a_scratch, gate_w, y, d, F,
+                               S(stream), false) == cudaSuccess ? ODMOE_OK : ODMOE_E_CUDA;
+  if (launch_w13(direct_ref(q13, a13, gate_idx), W_NF4, u, 0, a_scratch, d, F, S(stream)) != cudaSuccess)
+    return ODMOE_E_CUDA;
+  if (launch_w2(direct_ref(q2, a2, gate_idx), W_NF4, a_scratch, gate_w, y, d, F, S(stream)) != cudaSuccess)
+    return ODMOE_E_CUDA;
+  return ODMOE_OK;
+}
+
 odmoe_status odmoe_lm_head_argmax(const float* h, const void* lm_head, int V, int d, int dt, float eps,
                                   int32_t* token_out, float* logits, void* scratch, void* stream) {
   if (!h || !lm_head || !token_out || !scratch || V < 1 || d < 8 || d % 8 || (dt != ODMOE_BF16 && dt != ODMOE_FP32))
@@ -1773,6 +1803,13 @@ odmoe_status odmoe_quantize_int8_rows(const void* w, int64_t R, int64_t C, int d
                                       void* stream) {
   if (!w || !q || !s || R < 0 || C < 1 || (dt != ODMOE_BF16 && dt != ODMOE_FP32)) return ODMOE_E_CONFIG;
   return launch_quantize(w, R, C, wtype(dt), q, s, S(stream)) == cudaSuccess ? ODMOE_OK : ODMOE_E_CUDA;
+}
+
+odmoe_status odmoe_quantize_nf4(const void* w, int64_t R, int64_t C, int dt, uint8_t* q, float* absmax,
+                                void* stream) {
+  if (!w || !q || !absmax || R < 0 || C < 64 || C % 64 || (dt != ODMOE_BF16 && dt != ODMOE_FP32))
+    return ODMOE_E_CONFIG;
+  return launch_quantize_nf4(w, R, C, wtype(dt), q, absmax, S(stream)) == cudaSuccess ? ODMOE_OK : ODMOE_E_CUDA;
 }
 
 odmoe_status odmoe_gen_weights(void* out, int kind, int layer, int expert, int64_t rows, int64_t cols,

@@ -399,3 +399,34 @@ def test_bf16_shadow_of_fp32_model(od):
     assert r_bf16 >= 0.95, r_bf16
     with pytest.raises(od.OdmoeError):
         engine(od, TINY, "bf16", predictor=od.PRED_SHADOW_BF16)   # BF16 shadow needs an FP32 main model
+
+
+@pytest.mark.parametrize("dims", [(256, 512), (1024, 2048)])
+def test_nf4_shadow_predictor(od, dims):
+    """SEP with the NF4 shadow (reading Q27). TINY rows take the warp-per-row NF4
+    kernel, d=1024/F=2048 the flat one. Shadow routing teacher-forced against the oracle's NF4
+    model (ids from the GPU's own shadow state), outputs identical to the no-predictor run,
+    recall accounting exact."""
+    d, F = dims
+    shape = type(TINY)(TINY.L, TINY.E, TINY.k, d, F, TINY.V)
+    W = gen_model_weights(shape, SEED, dtype="bf16")
+    SW = O.quantize_model_nf4(W)
+    eng = engine(od, shape, "bf16", predictor=od.PRED_SHADOW_NF4, slots_per_gpu=2, debug_capture=1)
+    tok = int(gen_prompt(shape, 4, 1)[0])
+    first, toks, excused = tok, [], 0
+    for _ in range(10):
+        nxt, recs = eng.decode_step(tok)
+        excused += check_step_teacher_forced(eng, W, shape, "bf16", tok, nxt, SW)
+        for l in range(shape.L):
+            assert recs[l].correct == len(set(recs[l].true_ids[:2]) & set(recs[l].pred_ids[:2]))
+        toks.append(nxt)
+        tok = nxt
+    assert excused <= 3
+    st = eng.stats()
+    expert_bytes = shape.L * shape.E * 3 * d * F
+    assert st["shadow_bytes"] < 0.6 * expert_bytes + 4 * shape.V * d   # ~0.56 B per weight
+    eng.close()
+    en, toksn, _, _ = _run(od, shape, 10, first, predictor=od.PRED_NONE, slots_per_gpu=2)
+    en.close()
+    assert toks == toksn
+    print("nf4 shadow recall", dims, st["correct"] / st["predicted_total"])

@@ -186,6 +186,54 @@ def test_shadow_expert_ffn_parity(od, shape):
     assert l2rel(host(y), ref) <= 1e-5
 
 
+# ------------------------------------------------------------------ NF4 shadow (reading Q27)
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+@pytest.mark.parametrize("shape", [(40, 256), (96, 4096 + 192), (28672, 4096)])
+def test_nf4_quantizer_bit_exact(od, shape, dtype):
+    """Codes and absmax identical to the oracle (integer decisions taken in fp64 on both sides)."""
+    t = torch()
+    R, C = shape
+    Wf = stored(weight_fp32(SEED, tensor_id(KIND_W2, 1, R % 5), R, C, C), dtype).reshape(R, C).copy()
+    Wf[1, 64:128] = 0.0                                    # an all-zero block -> code 7
+    cb = np.asarray(O.NF4_CODEBOOK, dtype=np.float32)
+    Wf[2, :64] = np.tile(cb, 4) * np.float32(0.25)         # codebook points (exact in bf16? kept as stored)
+    Wf[2, :64] = stored(Wf[2, :64], dtype)
+    q_ref, a_ref = O.quantize_nf4_blocks(Wf.astype(np.float64))
+    packed_ref = (q_ref[:, 0::2] | (q_ref[:, 1::2] << 4)).astype(np.uint8)
+    q = t.empty((R, C // 2), dtype=t.uint8, device="cuda")
+    a = t.empty((R, C // 64), dtype=t.float32, device="cuda")
+    od.quantize_nf4(to_dev(Wf, dtype), q, a, dtype=od.BF16 if dtype == "bf16" else od.FP32)
+    t.cuda.synchronize()
+    assert np.array_equal(a.cpu().numpy(), a_ref)
+    assert np.array_equal(q.cpu().numpy(), packed_ref)
+
+
+@pytest.mark.parametrize("dF", [(256, 512), (1024, 2048), (4096, 14336)])
+def test_nf4_shadow_expert_ffn_parity(od, dF):
+    """NF4 expert FFN vs the oracle's dequantised weights. (256, 512): warp-per-row kernel (fp32
+    codebook, tol 1e-5); flat kernel: the codebook is held as fp16 pairs in shared memory
+    (relative error <= 2^-11 per weight), tol 2^-10 on the l2-relative output."""
+    t = torch()
+    d, F = dF
+    shape = type(TINY)(1, 8, 2, d, F, 1024)
+    W1, W3, W2 = gen_expert(shape, SEED, 0, 3, "bf16")
+    W13 = w13_interleaved(W1, W3).reshape(2 * F, d)
+    q13, a13 = O.quantize_nf4_blocks(W13)
+    q2, a2 = O.quantize_nf4_blocks(W2)
+    pk = lambda q: np.ascontiguousarray((q[:, 0::2] | (q[:, 1::2] << 4)).astype(np.uint8))  # noqa: E731
+    u_f = stored(O.rms_norm(gen_hidden(78, 1, d)[0]).astype(np.float32), "bf16")
+    a = t.empty(F, dtype=t.float32, device="cuda")
+    y = t.empty(d, dtype=t.float32, device="cuda")
+    gw = t.tensor([0.75, 0.25], dtype=t.float32, device="cuda")
+    cu = lambda x: t.from_numpy(np.ascontiguousarray(x)).cuda()  # noqa: E731
+    od.shadow_expert_ffn_nf4(cu(pk(q13)), cu(a13), cu(pk(q2)), cu(a2), to_dev(u_f, "bf16"), a, y, gate_w=gw, gate_idx=1)
+    t.cuda.synchronize()
+    dq13 = O.dequantize_nf4_blocks(q13, a13)
+    ref = 0.25 * O.expert_ffn(dq13[0::2], dq13[1::2], O.dequantize_nf4_blocks(q2, a2), u_f)
+    tol = 1e-5 if d % 1024 else 2.0 ** -10
+    assert l2rel(host(y), ref) <= tol, l2rel(host(y), ref)
+
+
 def test_shadow_router_parity(od):
     t = torch()
     E, d, k = 8, 4096, 2

@@ -91,7 +91,18 @@ def main():
         nb = 3 * F * d + (2 * F + d) * 4
         out["expert_ffn_int8"] = dict(us_median=med * 1e6, us_best=best * 1e6, GBps=nb / med / 1e9,
                                       frac_hbm=nb / med / 1e9 / pk["hbm_gbs"], bytes=nb)
-        del blob, q
+        # NF4 shadow expert (reading Q27): codes + block absmax
+        q4 = torch.empty((3 * F * d // 2,), dtype=torch.uint8, device=dev)
+        a4 = torch.empty(3 * F * d // 64, device=dev)
+        odmoe.quantize_nf4(w13.view(2 * F, d), q4[: F * d].view(2 * F, d // 2), a4[: 2 * F * d // 64].view(2 * F, d // 64))
+        odmoe.quantize_nf4(w2, q4[F * d:].view(d, F // 2), a4[2 * F * d // 64:].view(d, F // 64))
+        med, best = timeit(lambda: odmoe.shadow_expert_ffn_nf4(q4[: F * d].view(2 * F, d // 2), a4[: 2 * F * d // 64],
+                                                               q4[F * d:].view(d, F // 2), a4[2 * F * d // 64:],
+                                                               u, a, y, gate_w=gw), args.iters, flush)
+        nb = 3 * F * d // 2 + 3 * F * d // 64 * 4
+        out["expert_ffn_nf4"] = dict(us_median=med * 1e6, us_best=best * 1e6, GBps=nb / med / 1e9,
+                                     frac_hbm=nb / med / 1e9 / pk["hbm_gbs"], bytes=nb)
+        del blob, q, q4
     if args.only in ("", "lm"):
         W = torch.empty((V, d), dtype=bf, device=dev)
         odmoe.gen_weights(W, 6, rows=V, cols=d, fan_in=d, seed=2512)
