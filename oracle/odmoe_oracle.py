@@ -27,6 +27,9 @@ Parity pins (tests/test_oracle_pins.py, -m "not gpu"):
   quantize_nf4_blocks pinned: brute-force nearest-code search with Python floats; codes of the
                       codebook values themselves map to themselves; midpoint ties; zero blocks;
                       dequantised error <= half the local codebook gap x absmax.
+  round_e4m3 / quantize_fp8_rows
+                      pinned: torch.float8_e4m3fn casts (library) on random data incl. ties and
+                      subnormals; value table endpoints (448, 2^-9); row max -> +-448 exactly.
   shadow_predict      pinned: same-precision shadow => recall exactly 1.0.
   plan_* / misprediction_reloads / max_load_budget
                       pinned: SPEC examples S:271-273.
@@ -48,7 +51,8 @@ __all__ = [
     "expert_ffn", "moe_layer", "final_logits", "greedy_argmax", "decode_token", "decode_sequence",
     "quantize_int8_rows", "dequantize_int8_rows", "quantize_model_int8", "shadow_predict",
     "round_bf16", "shadow_model_bf16", "NF4_CODEBOOK", "NF4_BLOCK", "nf4_codebook_from_quantiles",
-    "quantize_nf4_blocks", "dequantize_nf4_blocks", "quantize_model_nf4",
+    "quantize_nf4_blocks", "dequantize_nf4_blocks", "quantize_model_nf4", "e4m3_values", "round_e4m3",
+    "quantize_fp8_rows", "dequantize_fp8_rows", "quantize_model_fp8",
     "near_tie", "plan_group_size", "plan_groups", "assign_layer", "assign_experts",
     "misprediction_reloads", "max_load_budget", "residency_bound", "recall_eq2", "recall_eq3",
     "recall_bruteforce", "prefill_permutation", "prefill_reference", "expert_counts",
@@ -313,6 +317,63 @@ def dequantize_nf4_blocks(codes, absmax, block: int = NF4_BLOCK):
     return cb[codes] * a
 
 
+# ---------------------------------------------------------------- FP8 (E4M3) row shadow (reading Q28)
+def e4m3_values():
+    """The 127 non-negative finite E4M3 ("fn": no infinities, S.1111.111 = NaN) values in code
+    order 0x00..0x7E, from the format: exponent bias 7, 3 mantissa bits, subnormals at e = 0."""
+    vals = []
+    for e in range(16):
+        for m in range(8):
+            if e == 15 and m == 7:
+                continue
+            vals.append(m / 8.0 * 2.0 ** -6 if e == 0 else (1.0 + m / 8.0) * 2.0 ** (e - 7))
+    return np.asarray(vals)
+
+
+def round_e4m3(x):
+    """Round to the nearest E4M3 value, ties to the even code, saturating at +-448 (satfinite).
+    Returns (values fp64, codes uint8 with the sign in bit 7)."""
+    x = np.asarray(x, dtype=np.float64)
+    V = e4m3_values()
+    a = np.abs(x)
+    i = np.clip(np.searchsorted(V, a, side="left"), 1, len(V) - 1)
+    lo, hi = V[i - 1], V[i]
+    dlo, dhi = a - lo, hi - a
+    pick_hi = (dhi < dlo) | ((dhi == dlo) & (i % 2 == 0))
+    idx = np.where(pick_hi, i, i - 1)
+    idx = np.where(a >= V[-1], len(V) - 1, idx)
+    idx = np.where(a == 0, 0, idx)
+    neg = np.signbit(x)
+    vals = np.where(neg, -V[idx], V[idx])
+    codes = (idx | (neg.astype(np.int64) << 7)).astype(np.uint8)
+    return vals, codes
+
+
+def quantize_fp8_rows(W):
+    """FP8 row shadow (reading Q28): per row r, m_r = max|w|, s_r = fl32(m_r / 448) (fp64 quotient
+    rounded to fp32); x = fl32(w / s_r) (fp64 quotient rounded to fp32); q = E4M3(x) (RNE,
+    satfinite). A zero row gives q = 0, s = 1. Returns (codes uint8 [R, C], s float32 [R])."""
+    W = np.asarray(W, dtype=np.float64)
+    if W.ndim == 1:
+        W = W[None, :]
+    m = np.max(np.abs(W), axis=1)
+    s = np.ones(W.shape[0], dtype=np.float32)
+    nz = m > 0
+    s[nz] = (m[nz] / 448.0).astype(np.float32)
+    x = (W / s.astype(np.float64)[:, None]).astype(np.float32)
+    _, codes = round_e4m3(x)
+    codes[~nz] = 0
+    return codes, s
+
+
+def dequantize_fp8_rows(codes, s):
+    V = e4m3_values()
+    codes = np.asarray(codes)
+    mag = V[np.minimum(codes & 0x7F, len(V) - 1)]
+    val = np.where(codes & 0x80, -mag, mag)
+    return np.asarray(s, dtype=np.float64)[:, None] * val
+
+
 def quantize_model_nf4(weights):
     """The NF4 shadow (reading Q27): every expert matrix NF4-blockwise; the embedding and the
     routers int8-row as in the INT8 shadow (0.3 % of the bytes). Dequantised fp64, same structure."""
@@ -322,6 +383,18 @@ def quantize_model_nf4(weights):
     for l, Wg in weights["router"].items():
         out["router"][l] = dq8(Wg)
         out["experts"][l] = {e: tuple(dq4(M) for M in mats) for e, mats in weights["experts"][l].items()}
+    return out
+
+
+def quantize_model_fp8(weights):
+    """The FP8 shadow (reading Q28): expert matrices E4M3 row-scaled; embedding and routers
+    int8-row as in the INT8 shadow. Dequantised fp64, same structure."""
+    dq8 = lambda W: dequantize_int8_rows(*quantize_int8_rows(W))  # noqa: E731
+    dqf = lambda W: dequantize_fp8_rows(*quantize_fp8_rows(W))  # noqa: E731
+    out = {"emb": dq8(weights["emb"]), "router": {}, "experts": {}}
+    for l, Wg in weights["router"].items():
+        out["router"][l] = dq8(Wg)
+        out["experts"][l] = {e: tuple(dqf(M) for M in mats) for e, mats in weights["experts"][l].items()}
     return out
 
 

@@ -298,6 +298,39 @@ def test_nf4_quantizer_brute_force_and_properties():
     assert c2[0, 1] == 7 and c2[0, 0] == 15
 
 
+def test_e4m3_rounding_matches_library_cast():
+    import torch
+    V = O.e4m3_values()
+    assert len(V) == 127 and V[-1] == 448.0 and V[1] == 2.0 ** -9 and np.all(np.diff(V) > 0)
+    lib_tbl = torch.arange(127, dtype=torch.uint8).view(torch.float8_e4m3fn).to(torch.float64).numpy()
+    assert np.array_equal(V, lib_tbl)
+    rng = np.random.default_rng(28)
+    x = np.concatenate([rng.standard_normal(20000) * 50, rng.standard_normal(2000) * 1e-3,
+                        (V[:-1] + V[1:]) / 2, -(V[:-1] + V[1:]) / 2,            # exact midpoints (ties)
+                        [0.0, 448.0, 447.9, 449.0, 500.0, -600.0]]).astype(np.float32)
+    vals, codes = O.round_e4m3(x)
+    lib = torch.from_numpy(x).to(torch.float8_e4m3fn)
+    inr = np.abs(x) < 464.0            # torch's cast gives NaN past the last rounding boundary
+    assert np.array_equal(codes[inr], lib.view(torch.uint8).numpy()[inr])
+    assert np.array_equal(vals[inr], lib.to(torch.float64).numpy()[inr])
+    assert np.all(np.abs(vals[~inr]) == 448.0)   # satfinite (the quantiser never gets there)
+
+
+def test_fp8_row_quantizer_properties():
+    rng = np.random.default_rng(29)
+    W = (rng.standard_normal((16, 256)) * 0.02).astype(np.float32).astype(np.float64)
+    W[4] = 0.0
+    codes, s = O.quantize_fp8_rows(W)
+    deq = O.dequantize_fp8_rows(codes, s)
+    assert np.all(codes[4] == 0) and s[4] == 1.0
+    rows = [r for r in range(16) if r != 4]
+    # the row maximum maps to +-448 (code 0x7E / 0xFE) and the error is within half an E4M3 step
+    for r in rows:
+        j = int(np.argmax(np.abs(W[r])))
+        assert codes[r, j] & 0x7F == 0x7E
+        assert np.all(np.abs(deq[r] - W[r]) <= np.abs(W[r]) * 2.0 ** -4 + s[r] * 2.0 ** -10)
+
+
 def test_same_precision_shadow_recall_is_one(tiny_fp32):
     """a full-precision shadow with token alignment predicts exactly."""
     toks, routes = O.decode_sequence(tiny_fp32, 11, 6, TINY.k)
