@@ -66,9 +66,11 @@ typedef enum {
                                  apply the gates of layers l+1..l+D to layer l's normalised input   */
   ODMOE_PRED_SHADOW_BF16 = 6, /* SEP with a BF16 shadow of an FP32 main model: the B200 analogue of the
                                  paper's FP16 shadow (99.94 % recall); needs dtype FP32 */
-  ODMOE_PRED_SHADOW_NF4 = 7   /* SEP with an NF4 shadow (95.67 % recall; reading Q27):
+  ODMOE_PRED_SHADOW_NF4 = 7,  /* SEP with an NF4 shadow (95.67 % recall; reading Q27):
                                  expert matrices NF4 in 64-weight blocks, embedding/routers int8-row;
                                  needs d, F multiples of 64 */
+  ODMOE_PRED_SHADOW_FP8 = 8   /* SEP with an FP8 (E4M3, row-scaled) shadow: the precision axis between
+                                 INT8 and BF16 (reading Q28); embedding/routers int8 */
 } odmoe_predictor;
 
 typedef struct {
@@ -198,6 +200,12 @@ odmoe_status odmoe_shadow_expert_ffn_nf4(const uint8_t* q13, const float* a13, c
                                          const float* a2, const void* u, const float* gate_w, int gate_idx,
                                          int d, int F, float* a_scratch, float* y, void* stream);
 
+/* FP8 shadow expert FFN (reading Q28): like odmoe_shadow_expert_ffn with W = s_r * e4m3(q_rj):
+ * q13 E4M3 codes [2F][d], s13 [2F]; q2 [d][F], s2 [d]; u bf16 [d]. */
+odmoe_status odmoe_shadow_expert_ffn_fp8(const uint8_t* q13, const float* s13, const uint8_t* q2,
+                                         const float* s2, const void* u, const float* gate_w, int gate_idx,
+                                         int d, int F, float* a_scratch, float* y, void* stream);
+
 /* Router over INT8-row weights (shadow gating): like odmoe_route_topk with w_gate = s_e*q_e,
  * gamma = 1, u_out bf16. */
 odmoe_status odmoe_shadow_route_topk(float* h, const float* const* y_add, int n_add,
@@ -246,6 +254,11 @@ odmoe_status odmoe_quantize_int8_rows(const void* w, int64_t R, int64_t C, int d
  * bytes (low nibble = even column), absmax [R][C/64]. C % 64 == 0 else E_CONFIG. */
 odmoe_status odmoe_quantize_nf4(const void* w, int64_t R, int64_t C, int dt, uint8_t* q, float* absmax,
                                 void* stream);
+
+/* FP8 row quantiser (reading Q28): s_r = fl32(max|w_r|/448), code = E4M3(RNE, satfinite) of
+ * fl32(w/s_r) (fp64 quotient); zero row -> codes 0, s = 1. q [R][C] bytes, s [R] (device). */
+odmoe_status odmoe_quantize_fp8_rows(const void* w, int64_t R, int64_t C, int dt, uint8_t* q, float* s,
+                                     void* stream);
 
 /* Synthetic weight generator: out[i] = dt(fl32(v_i * fl32(1/sqrt(fan_in)))),
  * v_i from splitmix64(seed, tensor_id, i). kind: 1 emb, 2 router, 3 W1, 4 W3, 5 W2, 6 LM head;

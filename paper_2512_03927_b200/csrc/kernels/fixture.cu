@@ -10,6 +10,8 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <cuda_fp8.h>
+
 namespace odmoe {
 
 constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;
@@ -192,6 +194,48 @@ cudaError_t launch_quantize_nf4(const void* w, int64_t R, int64_t C, WType wt, u
   const int grid = num_sms() * 8;
   if (wt == W_BF16) quantize_nf4_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)w, R, C, q, absmax);
   else if (wt == W_F32) quantize_nf4_kernel<float><<<grid, 256, 0, s>>>((const float*)w, R, C, q, absmax);
+  else return cudaErrorInvalidValue;
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- FP8 (E4M3) row quantiser
+// Reading Q28: s = fl32(max|w| / 448) (fp64 quotient), x = fl32(w / s) (fp64 quotient), code =
+// E4M3 RNE with saturation (the hardware conversion); zero row -> codes 0, s = 1.
+template <typename T>
+__global__ void __launch_bounds__(256) quantize_fp8_kernel(const T* __restrict__ w, long long C,
+                                                           uint8_t* __restrict__ q, float* __restrict__ sc) {
+  __shared__ float red[8];
+  const long long r = blockIdx.x;
+  const T* wr = w + r * C;
+  float m = 0.f;
+  for (long long j = threadIdx.x; j < C; j += blockDim.x) m = fmaxf(m, fabsf(ld_f<T>(wr, j)));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t = fmaxf(t, red[i]);
+    red[0] = t;
+  }
+  __syncthreads();
+  m = red[0];
+  const float s = m > 0.f ? __double2float_rn((double)m / 448.0) : 1.0f;
+  if (threadIdx.x == 0) sc[r] = s;
+  for (long long j = threadIdx.x; j < C; j += blockDim.x) {
+    uint8_t code = 0;
+    if (m > 0.f) {
+      const float x = __double2float_rn((double)ld_f<T>(wr, j) / (double)s);
+      code = (uint8_t)__nv_cvt_float_to_fp8(x, __NV_SATFINITE, __NV_E4M3);
+    }
+    q[r * C + j] = code;
+  }
+}
+
+cudaError_t launch_quantize_fp8(const void* w, int64_t R, int64_t C, WType wt, uint8_t* q, float* s, cudaStream_t st) {
+  if (R <= 0) return cudaSuccess;
+  if (wt == W_BF16) quantize_fp8_kernel<__nv_bfloat16><<<(unsigned)R, 256, 0, st>>>((const __nv_bfloat16*)w, C, q, s);
+  else if (wt == W_F32) quantize_fp8_kernel<float><<<(unsigned)R, 256, 0, st>>>((const float*)w, C, q, s);
   else return cudaErrorInvalidValue;
   return cudaGetLastError();
 }

@@ -11,6 +11,7 @@
 #include "kernels.h"
 
 #include <cuda_fp16.h>
+#include <cuda_fp8.h>
 
 #include <cstdlib>
 
@@ -122,6 +123,7 @@ struct nf4x2 { uint8_t v; };
 template <typename WT> struct FTraits { static constexpr int bits = 8 * (int)sizeof(WT); static constexpr bool nf4 = false; };
 template <> struct FTraits<nf4x2> { static constexpr int bits = 4; static constexpr bool nf4 = true; };
 template <> struct FDot<nf4x2, uint16_t> { static constexpr int kN = 32; };
+struct fp8e4 { uint8_t v; };  // E4M3 code (FP8 shadow, reading Q28); row scales like int8
 template <> struct FDot<nf4x2, float> { static constexpr int kN = 32; };
 
 // QLoRA's published NF4 codebook (Dettmers et al. 2023)
@@ -172,6 +174,42 @@ __device__ __forceinline__ float nf4_dot(const uint4& w, const uint4* xp, const 
     }
   return f2_sum(s);
 }
+
+// ---------------------------------------------------------------- FP8 E4M3 (shadow, reading Q28)
+__device__ __forceinline__ uint32_t e4m3x2_to_h2(uint32_t v16) {
+  uint32_t r;
+  asm("{.reg .b16 t;\n cvt.u16.u32 t, %1;\n cvt.rn.f16x2.e4m3x2 %0, t;}" : "=r"(r) : "r"(v16));
+  return r;
+}
+template <> struct FDot<fp8e4, uint16_t> {
+  static constexpr int kN = 16;
+  __device__ __forceinline__ static float run(const uint4& w, const uint4* xp) {
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+    const uint4 x0 = xp[0], x1 = xp[32];
+    const uint32_t xw[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+    f2_t s = 0ull;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      s = f2_fma(h2_unpack(e4m3x2_to_h2(ws[k] & 0xFFFFu)), bf2_unpack(xw[2 * k]), s);
+      s = f2_fma(h2_unpack(e4m3x2_to_h2(ws[k] >> 16)), bf2_unpack(xw[2 * k + 1]), s);
+    }
+    return f2_sum(s);
+  }
+};
+template <> struct FDot<fp8e4, float> {
+  static constexpr int kN = 16;
+  __device__ __forceinline__ static float run(const uint4& w, const uint4* xp) {
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+    f2_t s = 0ull;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint4 xq = xp[32 * k];
+      s = f2_fma(h2_unpack(e4m3x2_to_h2(ws[k] & 0xFFFFu)), f2_of(xq.x, xq.y), s);
+      s = f2_fma(h2_unpack(e4m3x2_to_h2(ws[k] >> 16)), f2_of(xq.z, xq.w), s);
+    }
+    return f2_sum(s);
+  }
+};
 
 __device__ __forceinline__ float fbf2(uint32_t w, uint32_t x, float s) {
   s = fmaf(bf16_lo(w), bf16_lo(x), s);
@@ -652,6 +690,18 @@ static cudaError_t fg_launch(FlatArgs a, cudaStream_t s, bool pdl) {
   return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
+// Low-bit weights (int8 / NF4 / FP8) with fp32 activations in shared memory: the dot products then
+// skip the bf16 -> fp32 unpack of every activation pair (ALU-bound kernels). ODMOE_LOWBIT_X=bf16
+// keeps bf16 activations (A/B).
+static bool lowbit_xf32() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ODMOE_LOWBIT_X");
+    v = (e && e[0] == 'b') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 cudaError_t launch_w13_flat(ExpertRef ex, WType wt, const void* u, int u_f32, float* a_out, int d, int F,
                             cudaStream_t s, bool pdl) {
   FlatArgs a{};
@@ -660,8 +710,9 @@ cudaError_t launch_w13_flat(ExpertRef ex, WType wt, const void* u, int u_f32, fl
   switch (wt) {
     case W_BF16: return fg_launch<__nv_bfloat16, uint16_t, 0>(a, s, pdl);
     case W_F32: return fg_launch<float, float, 0>(a, s, pdl);
-    case W_I8: return fg_launch<int8_t, uint16_t, 0>(a, s, pdl);
-    case W_NF4: return fg_launch<nf4x2, uint16_t, 0>(a, s, pdl);
+    case W_I8: return lowbit_xf32() ? fg_launch<int8_t, float, 0>(a, s, pdl) : fg_launch<int8_t, uint16_t, 0>(a, s, pdl);
+    case W_NF4: return lowbit_xf32() ? fg_launch<nf4x2, float, 0>(a, s, pdl) : fg_launch<nf4x2, uint16_t, 0>(a, s, pdl);
+    case W_F8: return lowbit_xf32() ? fg_launch<fp8e4, float, 0>(a, s, pdl) : fg_launch<fp8e4, uint16_t, 0>(a, s, pdl);
   }
   return cudaErrorInvalidValue;
 }
@@ -676,6 +727,7 @@ cudaError_t launch_w2_flat(ExpertRef ex, WType wt, const float* act, const float
     case W_F32: return fg_launch<float, float, 1>(a, s, pdl);
     case W_I8: return fg_launch<int8_t, float, 1>(a, s, pdl);
     case W_NF4: return fg_launch<nf4x2, float, 1>(a, s, pdl);
+    case W_F8: return fg_launch<fp8e4, float, 1>(a, s, pdl);
   }
   return cudaErrorInvalidValue;
 }
@@ -765,20 +817,21 @@ cudaError_t launch_expert_fused(ExpertRef ex, const void* w2_direct, const float
   switch (wt) {
     case W_BF16: return fused_launch<__nv_bfloat16, uint16_t>(a13, a2, s, pdl);
     case W_F32: return fused_launch<float, float>(a13, a2, s, pdl);
-    case W_I8: return fused_launch<int8_t, uint16_t>(a13, a2, s, pdl);
-    case W_NF4: return fused_launch<nf4x2, uint16_t>(a13, a2, s, pdl);
+    case W_I8: return lowbit_xf32() ? fused_launch<int8_t, float>(a13, a2, s, pdl) : fused_launch<int8_t, uint16_t>(a13, a2, s, pdl);
+    case W_NF4: return lowbit_xf32() ? fused_launch<nf4x2, float>(a13, a2, s, pdl) : fused_launch<nf4x2, uint16_t>(a13, a2, s, pdl);
+    case W_F8: return lowbit_xf32() ? fused_launch<fp8e4, float>(a13, a2, s, pdl) : fused_launch<fp8e4, uint16_t>(a13, a2, s, pdl);
   }
   return cudaErrorInvalidValue;
 }
 
-// ---------------------------------------------------------------- NF4, small shapes
-// Rows shorter than one 512-byte group (C % 1024 != 0) cannot use the flat stream: one warp per
-// output unit (a W1/W3 row pair, or a W2 row), one byte (two weights) per lane step. Test sizes
-// and odd shapes only; the Mixtral shapes take the flat kernel above.
-template <int MODE>
-__global__ void __launch_bounds__(256) nf4_rowwarp_kernel(ExpertRef ex, int second, const void* x, int x_f32,
-                                                         int R, int C, int d_full, int F_full,
-                                                         const float* gate_w, float* out) {
+// ---------------------------------------------------------------- NF4 / FP8, small shapes
+// Rows shorter than one 512-byte group cannot use the flat stream: one warp per output unit (a
+// W1/W3 row pair, or a W2 row). Test sizes and odd shapes only; Mixtral shapes take the flat
+// kernel above. FMT 0 = NF4 (block absmax), 1 = FP8 E4M3 (row scale).
+template <int MODE, int FMT>
+__global__ void __launch_bounds__(256) lowbit_rowwarp_kernel(ExpertRef ex, int second, const void* x, int x_f32,
+                                                            int R, int C, int d_full, int F_full,
+                                                            const float* gate_w, float* out) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const int lane = threadIdx.x & 31;
   const int unit = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -797,8 +850,9 @@ __global__ void __launch_bounds__(256) nf4_rowwarp_kernel(ExpertRef ex, int seco
       }
     }
     const int id = ex.base + ex.ids[gate_idx];
-    Wb = reinterpret_cast<const uint8_t*>(ex.tbl[id]) + (second ? (size_t)F_full * d_full : 0);
-    sc = ex.stbl[id] + (second ? (size_t)2 * F_full * d_full / 64 : 0);
+    Wb = reinterpret_cast<const uint8_t*>(ex.tbl[id]) +
+         (second ? (size_t)2 * F_full * d_full / (FMT == 0 ? 2 : 1) : 0);
+    sc = ex.stbl[id] + (second ? (FMT == 0 ? (size_t)2 * F_full * d_full / 64 : (size_t)2 * F_full) : 0);
   }
   const int nunits = MODE == 0 ? R / 2 : R;
   if (unit >= nunits) return;
@@ -810,10 +864,19 @@ __global__ void __launch_bounds__(256) nf4_rowwarp_kernel(ExpertRef ex, int seco
   for (int q = 0; q < (MODE == 0 ? 2 : 1); ++q) {
     const int r = MODE == 0 ? 2 * unit + q : unit;
     float t = 0.f;
-    for (int jb = lane; jb < C / 2; jb += 32) {
-      const uint8_t b = Wb[(size_t)r * (C / 2) + jb];
-      const float a = sc[(size_t)r * (C / 64) + (2 * jb) / 64];
-      t = fmaf(a, kNF4Code[b & 15] * xv(2 * jb) + kNF4Code[b >> 4] * xv(2 * jb + 1), t);
+    if (FMT == 0) {
+      for (int jb = lane; jb < C / 2; jb += 32) {
+        const uint8_t b = Wb[(size_t)r * (C / 2) + jb];
+        const float a = sc[(size_t)r * (C / 64) + (2 * jb) / 64];
+        t = fmaf(a, kNF4Code[b & 15] * xv(2 * jb) + kNF4Code[b >> 4] * xv(2 * jb + 1), t);
+      }
+    } else {
+      for (int j = lane; j < C; j += 32) {
+        __nv_fp8_e4m3 f;
+        f.__x = Wb[(size_t)r * C + j];
+        t = fmaf(float(f), xv(j), t);
+      }
+      t *= sc[r];
     }
     acc[q] = warp_sum(t);
   }
@@ -823,14 +886,21 @@ __global__ void __launch_bounds__(256) nf4_rowwarp_kernel(ExpertRef ex, int seco
   }
 }
 
-cudaError_t launch_nf4_small(ExpertRef ex, int second, const void* x, int x_f32, int d, int F, const float* gate_w,
-                             float* out, cudaStream_t s) {
+cudaError_t launch_lowbit_small(ExpertRef ex, WType wt, int second, const void* x, int x_f32, int d, int F,
+                                const float* gate_w, float* out, cudaStream_t s) {
   const int R = second ? d : 2 * F, C = second ? F : d;
-  if (C % 64) return cudaErrorInvalidValue;
+  if (wt == W_NF4 && C % 64) return cudaErrorInvalidValue;
   const int units = second ? R : R / 2;
   const int grid = (units + 7) / 8;
-  if (second) nf4_rowwarp_kernel<1><<<grid, 256, 0, s>>>(ex, 1, x, 1, R, C, d, F, gate_w, out);
-  else nf4_rowwarp_kernel<0><<<grid, 256, 0, s>>>(ex, 0, x, x_f32, R, C, d, F, gate_w, out);
+  if (wt == W_NF4) {
+    if (second) lowbit_rowwarp_kernel<1, 0><<<grid, 256, 0, s>>>(ex, 1, x, 1, R, C, d, F, gate_w, out);
+    else lowbit_rowwarp_kernel<0, 0><<<grid, 256, 0, s>>>(ex, 0, x, x_f32, R, C, d, F, gate_w, out);
+  } else if (wt == W_F8) {
+    if (second) lowbit_rowwarp_kernel<1, 1><<<grid, 256, 0, s>>>(ex, 1, x, 1, R, C, d, F, gate_w, out);
+    else lowbit_rowwarp_kernel<0, 1><<<grid, 256, 0, s>>>(ex, 0, x, x_f32, R, C, d, F, gate_w, out);
+  } else {
+    return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }
 

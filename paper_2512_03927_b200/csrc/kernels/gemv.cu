@@ -191,9 +191,9 @@ int gemv_engine() {
 
 cudaError_t launch_w13(ExpertRef ex, WType wt, const void* u, int u_f32, float* a, int d, int F,
                        cudaStream_t s, bool pdl) {
-  if (wt == W_NF4)
+  if (wt == W_NF4 || wt == W_F8)
     return stream_ok(wt, d) ? launch_w13_flat(ex, wt, u, u_f32, a, d, F, s, pdl)
-                            : launch_nf4_small(ex, 0, u, u_f32, d, F, nullptr, a, s);
+                            : launch_lowbit_small(ex, wt, 0, u, u_f32, d, F, nullptr, a, s);
   if (stream_ok(wt, d)) {
     if (gemv_engine() == 2) return launch_w13_flat(ex, wt, u, u_f32, a, d, F, s, pdl);
     if (gemv_engine() == 1) return launch_w13_stream(ex, wt, u, u_f32, a, d, F, s);
@@ -209,9 +209,9 @@ cudaError_t launch_w13(ExpertRef ex, WType wt, const void* u, int u_f32, float* 
 
 cudaError_t launch_w2(ExpertRef ex, WType wt, const float* a, const float* gate_w, float* y, int d,
                       int F, cudaStream_t s, bool pdl) {
-  if (wt == W_NF4)
+  if (wt == W_NF4 || wt == W_F8)
     return stream_ok(wt, F) ? launch_w2_flat(ex, wt, a, gate_w, y, d, F, s, pdl)
-                            : launch_nf4_small(ex, 1, a, 1, d, F, gate_w, y, s);
+                            : launch_lowbit_small(ex, wt, 1, a, 1, d, F, gate_w, y, s);
   if (stream_ok(wt, F)) {
     if (gemv_engine() == 2) return launch_w2_flat(ex, wt, a, gate_w, y, d, F, s, pdl);
     if (gemv_engine() == 1) return launch_w2_stream(ex, wt, a, gate_w, y, d, F, s);

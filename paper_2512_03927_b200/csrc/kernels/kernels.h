@@ -5,7 +5,8 @@
 
 namespace odmoe {
 
-enum WType { W_BF16 = 0, W_F32 = 1, W_I8 = 2, W_NF4 = 3 };
+enum WType { W_BF16 = 0, W_F32 = 1, W_I8 = 2, W_NF4 = 3, W_F8 = 4 };
+// W_F8 (shadow experts only, reading Q28): E4M3 codes, one fp32 scale per row (int8's layout).
 // W_NF4 (shadow experts only, reading Q27): two 4-bit codes per byte (low nibble = even column),
 // "scales" = fp32 absmax per 64-weight block of a row, [R][C/64]; expert blob = codes of W13 then
 // W2 (3dF/2 bytes), scale array = W13 blocks then W2 blocks.
@@ -58,9 +59,11 @@ cudaError_t launch_w2_flat(ExpertRef ex, WType wt, const float* act, const float
 cudaError_t launch_lm_head_flat(const float* h, const void* W, WType wt, int V, int d, float eps,
                                 int32_t* token_out, float* logits, void* scratch, cudaStream_t s, bool pdl);
 bool use_fused_expert();  // env ODMOE_FUSED=0 disables (A/B)
-// NF4 rows shorter than one flat group: warp-per-row kernel (x: bf16 unless x_f32; W2 x = fp32)
-cudaError_t launch_nf4_small(ExpertRef ex, int second, const void* x, int x_f32, int d, int F, const float* gate_w,
-                             float* out, cudaStream_t s);
+// NF4 / FP8 rows shorter than one flat group: warp-per-row kernel (x: bf16 unless x_f32; W2 x = fp32)
+cudaError_t launch_lowbit_small(ExpertRef ex, WType wt, int second, const void* x, int x_f32, int d, int F,
+                                const float* gate_w, float* out, cudaStream_t s);
+// FP8 row quantiser (reading Q28): codes [R][C] E4M3, s [R]
+cudaError_t launch_quantize_fp8(const void* w, int64_t R, int64_t C, WType wt, uint8_t* q, float* s, cudaStream_t st);
 // NF4 blockwise quantiser (reading Q27): codes [R][C/2] bytes, absmax [R][C/64]; C % 64 == 0
 cudaError_t launch_quantize_nf4(const void* w, int64_t R, int64_t C, WType wt, uint8_t* q, float* absmax,
                                 cudaStream_t s);

@@ -67,7 +67,7 @@ odmoe_status guard(Ctx* c, F&& f) {
 inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 inline bool is_shadow(int p) {
   return p == ODMOE_PRED_SHADOW_INT8 || p == ODMOE_PRED_SHADOW_SAME || p == ODMOE_PRED_SHADOW_BF16 ||
-         p == ODMOE_PRED_SHADOW_NF4;
+         p == ODMOE_PRED_SHADOW_NF4 || p == ODMOE_PRED_SHADOW_FP8;
 }
 inline WType wtype(int dt) { return dt == ODMOE_FP32 ? W_F32 : W_BF16; }
 inline size_t dsize(int dt) { return dt == ODMOE_FP32 ? 4 : 2; }
@@ -191,7 +191,7 @@ void validate(const odmoe_config* g) {
   if (g->k > g->E || g->k > 8 || g->E > 64) bad("need 1 <= k <= E <= 64 and k <= 8");
   if (g->d % 8 || g->F % 8) bad("d and F must be multiples of 8");
   if (g->dtype != ODMOE_BF16 && g->dtype != ODMOE_FP32) bad("dtype");
-  if (g->predictor < 0 || g->predictor > 7) bad("predictor");
+  if (g->predictor < 0 || g->predictor > 8) bad("predictor");
   if (g->predictor == ODMOE_PRED_SHADOW_NF4 && (g->d % 64 || g->F % 64)) bad("the NF4 shadow needs d, F multiples of 64");
   if (g->lookahead < 1) bad("lookahead must be >= 1");
   if (g->world_size < 1 || g->rank < 0 || g->rank >= g->world_size) bad("rank/world_size");
@@ -258,8 +258,9 @@ void build_shadow(Ctx* c, char* staging) {
     return;
   }
   const bool nf4 = c->cfg.predictor == ODMOE_PRED_SHADOW_NF4;
+  const bool fp8 = c->cfg.predictor == ODMOE_PRED_SHADOW_FP8;
   c->sh_wt = W_I8;
-  c->sh_ewt = nf4 ? W_NF4 : W_I8;
+  c->sh_ewt = nf4 ? W_NF4 : (fp8 ? W_F8 : W_I8);
   c->sh_emb = dmalloc<int8_t>(c, (size_t)V * d, "shadow emb");
   c->sh_semb = dmalloc<float>(c, V, "shadow emb scales");
   c->sh_router = dmalloc<int8_t>(c, (size_t)L * E * d, "shadow router");
@@ -290,8 +291,14 @@ void build_shadow(Ctx* c, char* staging) {
       }
       int8_t* q = dmalloc<int8_t>(c, (size_t)3 * F * d, "shadow expert");
       float* s = dmalloc<float>(c, (size_t)2 * F + d, "shadow scales");
-      CUDA_OK(c, launch_quantize(src, 2LL * F, d, c->wt, q, s, c->s_main));
-      CUDA_OK(c, launch_quantize(src + (size_t)2 * F * d * c->esz, d, F, c->wt, q + (size_t)2 * F * d, s + 2 * F, c->s_main));
+      if (fp8) {  // E4M3 codes, int8's layout (rows of W13 then W2; row scales s13 then s2)
+        CUDA_OK(c, launch_quantize_fp8(src, 2LL * F, d, c->wt, (uint8_t*)q, s, c->s_main));
+        CUDA_OK(c, launch_quantize_fp8(src + (size_t)2 * F * d * c->esz, d, F, c->wt, (uint8_t*)q + (size_t)2 * F * d,
+                                       s + 2 * F, c->s_main));
+      } else {
+        CUDA_OK(c, launch_quantize(src, 2LL * F, d, c->wt, q, s, c->s_main));
+        CUDA_OK(c, launch_quantize(src + (size_t)2 * F * d * c->esz, d, F, c->wt, q + (size_t)2 * F * d, s + 2 * F, c->s_main));
+      }
       c->sh_blob[i] = q;
       c->sh_sc[i] = s;
       c->stats.shadow_bytes += (int64_t)3 * F * d + (int64_t)(2 * F + d) * 4;
@@ -1553,7 +1560,7 @@ odmoe_status odmoe_set_option(void* ctx, int key, int64_t value) {
       if (value < 1) fail(c, ODMOE_E_CONFIG, "lookahead must be >= 1");
       c->cfg.lookahead = (int32_t)value;
     } else if (key == 2) {
-      if (value < 0 || value > 7) fail(c, ODMOE_E_CONFIG, "predictor");
+      if (value < 0 || value > 8) fail(c, ODMOE_E_CONFIG, "predictor");
       const bool wants_shadow = is_shadow((int)value);
       if (wants_shadow && value != c->built_pred)
         fail(c, ODMOE_E_STATE, "this ctx was not created with that shadow predictor");
@@ -1789,6 +1796,21 @@ odmoe_status odmoe_shadow_expert_ffn_nf4(const uint8_t* q13, const float* a13, c
   return ODMOE_OK;
 }
 
+odmoe_status odmoe_shadow_expert_ffn_fp8(const uint8_t* q13, const float* s13, const uint8_t* q2,
+                                         const float* s2, const void* u, const float* gate_w, int gate_idx,
+                                         int d, int F, float* a_scratch, float* y, void* stream) {
+  if (!q13 || !s13 || !q2 || !s2 || !u || !a_scratch || !y || d < 16 || F < 16 || d % 16 || F % 16 || gate_idx < 0)
+    return ODMOE_E_CONFIG;
+  if (use_fused_expert() && stream_ok(W_F8, d) && stream_ok(W_F8, F))
+    return launch_expert_fused(direct_ref(q13, s13, gate_idx), q2, s2, W_F8, u, 0, a_scratch, gate_w, y, d, F,
+                               S(stream), false) == cudaSuccess ? ODMOE_OK : ODMOE_E_CUDA;
+  if (launch_w13(direct_ref(q13, s13, gate_idx), W_F8, u, 0, a_scratch, d, F, S(stream)) != cudaSuccess)
+    return ODMOE_E_CUDA;
+  if (launch_w2(direct_ref(q2, s2, gate_idx), W_F8, a_scratch, gate_w, y, d, F, S(stream)) != cudaSuccess)
+    return ODMOE_E_CUDA;
+  return ODMOE_OK;
+}
+
 odmoe_status odmoe_lm_head_argmax(const float* h, const void* lm_head, int V, int d, int dt, float eps,
                                   int32_t* token_out, float* logits, void* scratch, void* stream) {
   if (!h || !lm_head || !token_out || !scratch || V < 1 || d < 8 || d % 8 || (dt != ODMOE_BF16 && dt != ODMOE_FP32))
@@ -1810,6 +1832,12 @@ odmoe_status odmoe_quantize_nf4(const void* w, int64_t R, int64_t C, int dt, uin
   if (!w || !q || !absmax || R < 0 || C < 64 || C % 64 || (dt != ODMOE_BF16 && dt != ODMOE_FP32))
     return ODMOE_E_CONFIG;
   return launch_quantize_nf4(w, R, C, wtype(dt), q, absmax, S(stream)) == cudaSuccess ? ODMOE_OK : ODMOE_E_CUDA;
+}
+
+odmoe_status odmoe_quantize_fp8_rows(const void* w, int64_t R, int64_t C, int dt, uint8_t* q, float* s,
+                                     void* stream) {
+  if (!w || !q || !s || R < 0 || C < 1 || (dt != ODMOE_BF16 && dt != ODMOE_FP32)) return ODMOE_E_CONFIG;
+  return launch_quantize_fp8(w, R, C, wtype(dt), q, s, S(stream)) == cudaSuccess ? ODMOE_OK : ODMOE_E_CUDA;
 }
 
 odmoe_status odmoe_gen_weights(void* out, int kind, int layer, int expert, int64_t rows, int64_t cols,

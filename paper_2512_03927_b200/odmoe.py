@@ -15,9 +15,9 @@ LIB_PATH = os.environ.get("ODMOE_LIB") or os.path.join(_HERE, "libodmoe.so")
 
 BF16, FP32 = 0, 1
 (PRED_SHADOW_INT8, PRED_NONE, PRED_RANDOM, PRED_PERFECT, PRED_SHADOW_SAME, PRED_GATE_REUSE, PRED_SHADOW_BF16,
- PRED_SHADOW_NF4) = range(8)
+ PRED_SHADOW_NF4, PRED_SHADOW_FP8) = range(9)
 PREDICTORS = {"shadow_int8": 0, "none": 1, "random": 2, "perfect": 3, "shadow_same": 4, "gate_reuse": 5,
-              "shadow_bf16": 6, "shadow_nf4": 7}
+              "shadow_bf16": 6, "shadow_nf4": 7, "shadow_fp8": 8}
 
 STATUS = {0: "OK", 1: "E_CONFIG", 2: "E_RANGE", 3: "E_NONFINITE", 4: "E_BUDGET", 5: "E_STATE",
           6: "E_PLAN", 7: "E_NOMEM", 8: "E_CUDA", 9: "E_NCCL"}
@@ -106,6 +106,8 @@ _lm = _sig("odmoe_lm_head_argmax", [_P, _P, _I, _I, _I, _F, _P, _P, _P, _P])
 _quant = _sig("odmoe_quantize_int8_rows", [_P, _I64, _I64, _I, _P, _P, _P])
 _sh_ffn_nf4 = _sig("odmoe_shadow_expert_ffn_nf4", [_P, _P, _P, _P, _P, _P, _I, _I, _I, _P, _P, _P])
 _quant_nf4 = _sig("odmoe_quantize_nf4", [_P, _I64, _I64, _I, _P, _P, _P])
+_sh_ffn_fp8 = _sig("odmoe_shadow_expert_ffn_fp8", [_P, _P, _P, _P, _P, _P, _I, _I, _I, _P, _P, _P])
+_quant_fp8 = _sig("odmoe_quantize_fp8_rows", [_P, _I64, _I64, _I, _P, _P, _P])
 _gen = _sig("odmoe_gen_weights", [_P, _I, _I, _I, _I64, _I64, _I64, _I, _I, ctypes.c_uint64, _I, _P])
 _load_ = _sig("odmoe_load", [_P, _I, _I])
 _load_wait = _sig("odmoe_load_wait", [_P, _I, _I, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p)])
@@ -129,7 +131,8 @@ EXPORTED = ["odmoe_set_option", "odmoe_expert_ffn_grouped", "odmoe_prefill_group
             "odmoe_shadow_expert_ffn", "odmoe_shadow_route_topk", "odmoe_lm_head_argmax",
             "odmoe_quantize_int8_rows", "odmoe_gen_weights", "odmoe_load", "odmoe_load_wait",
             "odmoe_evict", "odmoe_predict_ahead", "odmoe_decode_step", "odmoe_prefill",
-            "odmoe_debug_read", "odmoe_tensor_ptr", "odmoe_shadow_expert_ffn_nf4", "odmoe_quantize_nf4"]
+            "odmoe_debug_read", "odmoe_tensor_ptr", "odmoe_shadow_expert_ffn_nf4", "odmoe_quantize_nf4",
+            "odmoe_shadow_expert_ffn_fp8", "odmoe_quantize_fp8_rows"]
 
 
 def abi_version() -> int:
@@ -201,6 +204,13 @@ def shadow_expert_ffn_nf4(q13, a13, q2, a2, u, a_scratch, y, gate_w=None, gate_i
                        _ptr(a_scratch), _ptr(y), _stream(stream)))
 
 
+def shadow_expert_ffn_fp8(q13, s13, q2, s2, u, a_scratch, y, gate_w=None, gate_idx=0, stream=None):
+    """FP8 shadow expert: q13 uint8 E4M3 [2F, d], s13 [2F], q2 [d, F], s2 [d]."""
+    d, F = q2.shape
+    _check(_sh_ffn_fp8(_ptr(q13), _ptr(s13), _ptr(q2), _ptr(s2), _ptr(u), _ptr(gate_w), gate_idx, d, F,
+                       _ptr(a_scratch), _ptr(y), _stream(stream)))
+
+
 def prefill_group(ids, w, E: int, offsets, src_pair, inv, gate_perm, stream=None):
     """ids [T,k] int32, w [T,k] fp32 -> offsets [E+1], src_pair/inv [T*k] int32, gate_perm [T*k]."""
     T, k = ids.shape
@@ -237,6 +247,12 @@ def quantize_nf4(w, q, absmax, dtype=BF16, stream=None):
     """w [R, C] -> q uint8 [R, C/2] (two codes per byte, low nibble = even column), absmax [R, C/64]."""
     R, C = w.shape
     _check(_quant_nf4(_ptr(w), R, C, dtype, _ptr(q), _ptr(absmax), _stream(stream)))
+
+
+def quantize_fp8_rows(w, q, s, dtype=BF16, stream=None):
+    """w [R, C] -> q uint8 E4M3 codes [R, C], s [R]."""
+    R, C = w.shape
+    _check(_quant_fp8(_ptr(w), R, C, dtype, _ptr(q), _ptr(s), _stream(stream)))
 
 
 def gen_weights(out, kind, layer=0, expert=0, rows=0, cols=0, fan_in=1, d=0, F=0, seed=2512, dtype=BF16,

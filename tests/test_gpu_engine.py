@@ -401,17 +401,19 @@ def test_bf16_shadow_of_fp32_model(od):
         engine(od, TINY, "bf16", predictor=od.PRED_SHADOW_BF16)   # BF16 shadow needs an FP32 main model
 
 
+@pytest.mark.parametrize("fmt", ["nf4", "fp8"])
 @pytest.mark.parametrize("dims", [(256, 512), (1024, 2048)])
-def test_nf4_shadow_predictor(od, dims):
-    """SEP with the NF4 shadow (reading Q27). TINY rows take the warp-per-row NF4
-    kernel, d=1024/F=2048 the flat one. Shadow routing teacher-forced against the oracle's NF4
-    model (ids from the GPU's own shadow state), outputs identical to the no-predictor run,
-    recall accounting exact."""
+def test_lowbit_shadow_predictor(od, dims, fmt):
+    """SEP with the NF4 shadow (reading Q27) and the FP8 shadow (Q28). TINY rows take
+    the warp-per-row kernel, d=1024/F=2048 the flat one. Shadow routing teacher-forced against the
+    oracle's quantised model (ids from the GPU's own shadow state), outputs identical to the
+    no-predictor run, recall accounting exact."""
     d, F = dims
     shape = type(TINY)(TINY.L, TINY.E, TINY.k, d, F, TINY.V)
     W = gen_model_weights(shape, SEED, dtype="bf16")
-    SW = O.quantize_model_nf4(W)
-    eng = engine(od, shape, "bf16", predictor=od.PRED_SHADOW_NF4, slots_per_gpu=2, debug_capture=1)
+    SW = O.quantize_model_nf4(W) if fmt == "nf4" else O.quantize_model_fp8(W)
+    pred = od.PRED_SHADOW_NF4 if fmt == "nf4" else od.PRED_SHADOW_FP8
+    eng = engine(od, shape, "bf16", predictor=pred, slots_per_gpu=2, debug_capture=1)
     tok = int(gen_prompt(shape, 4, 1)[0])
     first, toks, excused = tok, [], 0
     for _ in range(10):
@@ -424,9 +426,10 @@ def test_nf4_shadow_predictor(od, dims):
     assert excused <= 3
     st = eng.stats()
     expert_bytes = shape.L * shape.E * 3 * d * F
-    assert st["shadow_bytes"] < 0.6 * expert_bytes + 4 * shape.V * d   # ~0.56 B per weight
+    per_weight = 0.6 if fmt == "nf4" else 1.01                          # ~0.56 / ~1.0 B per weight
+    assert st["shadow_bytes"] < per_weight * expert_bytes + 8 * shape.V * d
     eng.close()
     en, toksn, _, _ = _run(od, shape, 10, first, predictor=od.PRED_NONE, slots_per_gpu=2)
     en.close()
     assert toks == toksn
-    print("nf4 shadow recall", dims, st["correct"] / st["predicted_total"])
+    print(fmt, "shadow recall", dims, st["correct"] / st["predicted_total"])

@@ -234,6 +234,44 @@ def test_nf4_shadow_expert_ffn_parity(od, dF):
     assert l2rel(host(y), ref) <= tol, l2rel(host(y), ref)
 
 
+# ------------------------------------------------------------------ FP8 shadow (reading Q28)
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+@pytest.mark.parametrize("shape", [(37, 256), (64, 4096), (4096, 14336)])
+def test_fp8_quantizer_bit_exact(od, shape, dtype):
+    t = torch()
+    R, C = shape
+    Wf = stored(weight_fp32(SEED, tensor_id(KIND_W1, 2, R % 3), R, C, C), dtype).reshape(R, C).copy()
+    Wf[1] = 0.0
+    q_ref, s_ref = O.quantize_fp8_rows(Wf.astype(np.float64))
+    q = t.empty((R, C), dtype=t.uint8, device="cuda")
+    s = t.empty(R, dtype=t.float32, device="cuda")
+    od.quantize_fp8_rows(to_dev(Wf, dtype), q, s, dtype=od.BF16 if dtype == "bf16" else od.FP32)
+    t.cuda.synchronize()
+    assert np.array_equal(s.cpu().numpy(), s_ref)
+    assert np.array_equal(q.cpu().numpy(), q_ref)
+
+
+@pytest.mark.parametrize("dF", [(256, 512), (4096, 14336)])
+def test_fp8_shadow_expert_ffn_parity(od, dF):
+    """E4M3 values are exact in fp16, so the dequantisation is exact on both kernels: tol 1e-5."""
+    t = torch()
+    d, F = dF
+    shape = type(TINY)(1, 8, 2, d, F, 1024)
+    W1, W3, W2 = gen_expert(shape, SEED, 0, 5, "bf16")
+    W13 = w13_interleaved(W1, W3).reshape(2 * F, d)
+    q13, s13 = O.quantize_fp8_rows(W13)
+    q2, s2 = O.quantize_fp8_rows(W2)
+    u_f = stored(O.rms_norm(gen_hidden(79, 1, d)[0]).astype(np.float32), "bf16")
+    a = t.empty(F, dtype=t.float32, device="cuda")
+    y = t.empty(d, dtype=t.float32, device="cuda")
+    cu = lambda x: t.from_numpy(np.ascontiguousarray(x)).cuda()  # noqa: E731
+    od.shadow_expert_ffn_fp8(cu(q13), cu(s13), cu(q2), cu(s2), to_dev(u_f, "bf16"), a, y)
+    t.cuda.synchronize()
+    dq13 = O.dequantize_fp8_rows(q13, s13)
+    ref = O.expert_ffn(dq13[0::2], dq13[1::2], O.dequantize_fp8_rows(q2, s2), u_f)
+    assert l2rel(host(y), ref) <= 1e-5, l2rel(host(y), ref)
+
+
 def test_shadow_router_parity(od):
     t = torch()
     E, d, k = 8, 4096, 2

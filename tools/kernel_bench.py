@@ -102,7 +102,16 @@ def main():
         nb = 3 * F * d // 2 + 3 * F * d // 64 * 4
         out["expert_ffn_nf4"] = dict(us_median=med * 1e6, us_best=best * 1e6, GBps=nb / med / 1e9,
                                      frac_hbm=nb / med / 1e9 / pk["hbm_gbs"], bytes=nb)
-        del blob, q, q4
+        # FP8 shadow expert (reading Q28)
+        q8 = torch.empty((3 * F * d,), dtype=torch.uint8, device=dev)
+        odmoe.quantize_fp8_rows(w13.view(2 * F, d), q8[: 2 * F * d].view(2 * F, d), sc[: 2 * F])
+        odmoe.quantize_fp8_rows(w2, q8[2 * F * d:].view(d, F), sc[2 * F:])
+        med, best = timeit(lambda: odmoe.shadow_expert_ffn_fp8(q8[: 2 * F * d], sc[: 2 * F], q8[2 * F * d:].view(d, F),
+                                                               sc[2 * F:], u, a, y, gate_w=gw), args.iters, flush)
+        nb = 3 * F * d + (2 * F + d) * 4
+        out["expert_ffn_fp8"] = dict(us_median=med * 1e6, us_best=best * 1e6, GBps=nb / med / 1e9,
+                                     frac_hbm=nb / med / 1e9 / pk["hbm_gbs"], bytes=nb)
+        del blob, q, q4, q8
     if args.only in ("", "lm"):
         W = torch.empty((V, d), dtype=bf, device=dev)
         odmoe.gen_weights(W, 6, rows=V, cols=d, fan_in=d, seed=2512)

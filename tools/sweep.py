@@ -30,6 +30,8 @@ def main():
     ap.add_argument("--slots", type=int, default=2)
     ap.add_argument("--refine", default="0", help="comma list of SEP refinement depths (shadow predictor only)")
     ap.add_argument("--out", default="")
+    ap.add_argument("--build-predictor", default="shadow_int8",
+                    help="predictor the engine is created with (its shadow is the one shadow predictors use)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -45,7 +47,8 @@ def main():
         obj = [odmoe.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
-    eng = odmoe.Engine(device=local, rank=rank, world_size=world, nccl_id=uid, predictor=odmoe.PRED_SHADOW_INT8,
+    eng = odmoe.Engine(device=local, rank=rank, world_size=world, nccl_id=uid,
+                       predictor=odmoe.PREDICTORS[args.build_predictor],
                        slots_per_gpu=args.slots, lookahead=1, weight_seed=2512, **SHAPE)
     lines = []
     combos = []
@@ -86,6 +89,8 @@ def main():
             if rank == 0:
                 rec = st["correct"] / st["predicted_total"] if st["predicted_total"] else None
                 recb = st["refine_correct"] / st["refine_total"] if st["refine_total"] else None
+                if pname.startswith("shadow"):
+                    pname = args.build_predictor
                 line = {"n_gpus": world, "predictor": pname, "lookahead": D, "refine_depth": R,
                         "recall_refined": recb, "refine_corrections_per_token": st["refine_corrections"] / args.steps,
                         "tok_s": args.steps / s,
