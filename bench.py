@@ -40,10 +40,13 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--predictor", default="shadow_int8")
-    ap.add_argument("--slots", type=int, default=2)
+    ap.add_argument("--slots", type=int, default=0,
+                    help="device expert slots per GPU; 0 => 2 (groups: whole experts) or 2k (sliced: 1/N slices)")
+    ap.add_argument("--placement", default="groups", choices=["groups", "sliced"],
+                    help="N > 1: the paper's worker groups (P:104) or sliced loading (SURVEY §8(f)3)")
     ap.add_argument("--refine", type=int, default=2,
                     help="SEP refinement depth R (DESIGN.md §7); 0 = the paper's token-aligned shadow only")
-    ap.add_argument("--lookahead", type=int, default=0, help="0 => max(1, N/2)")
+    ap.add_argument("--lookahead", type=int, default=0, help="0 => max(1, N/2) (groups) or 1 (sliced)")
     ap.add_argument("--no-resident", action="store_true", help="skip the fully-resident baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--first-token", type=int, default=-1)
@@ -241,15 +244,34 @@ def run_reference(args):
     return 0
 
 
+def sliced(args, n):
+    return args.placement == "sliced" and n > 1
+
+
+def n_slots(args, n):
+    return args.slots or (2 * SHAPE["k"] if sliced(args, n) else 2)
+
+
+def lookahead(args, n):
+    return args.lookahead or (1 if sliced(args, n) else max(1, n // 2))
+
+
 def workload_config(args, n):
     ng = max(1, n // 2)
-    return {"workload": ("configs[1]: Mixtral-8x7B shape (L=32, E=8, top-2, d=4096, F=14336, V=32000), "
-                         "bf16, batch-1 decode, on-demand expert loading" if n == 1 else
-                         f"configs[2]/[3]: Mixtral-8x7B shape, bf16, batch-1 decode, experts round-robin "
-                         f"over {ng} groups of 2 GPUs, lookahead {args.lookahead or ng}"),
-            "predictor": args.predictor, "slots_per_gpu": args.slots, "refine_depth": args.refine,
-            "expert_bytes_per_gpu": args.slots * EXPERT_BYTES,
-            "lookahead": args.lookahead or max(1, n // 2), "weight_seed": SEED,
+    if n == 1:
+        wl = ("configs[1]: Mixtral-8x7B shape (L=32, E=8, top-2, d=4096, F=14336, V=32000), "
+              "bf16, batch-1 decode, on-demand expert loading")
+    elif sliced(args, n):
+        wl = (f"configs[2]/[3]: Mixtral-8x7B shape, bf16, batch-1 decode, sliced loading: each of {n} GPUs "
+              f"loads and computes 1/{n} of every routed expert, partials reduced on GPU 0, lookahead {lookahead(args, n)}")
+    else:
+        wl = (f"configs[2]/[3]: Mixtral-8x7B shape, bf16, batch-1 decode, experts round-robin "
+              f"over {ng} groups of 2 GPUs, lookahead {lookahead(args, n)}")
+    per_slot = EXPERT_BYTES // n if sliced(args, n) else EXPERT_BYTES
+    return {"workload": wl, "placement": args.placement if n > 1 else "single",
+            "predictor": args.predictor, "slots_per_gpu": n_slots(args, n), "refine_depth": args.refine,
+            "expert_bytes_per_gpu": n_slots(args, n) * per_slot,
+            "lookahead": lookahead(args, n), "weight_seed": SEED,
             "attention": "none on the hot path (reading Q22)",
             "l2": "inputs larger than L2: every step streams 64 distinct 352 MB experts"}
 
@@ -287,14 +309,14 @@ def main():
         obj = [odmoe.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
-    D = args.lookahead or max(1, n // 2)
+    D = lookahead(args, n)
     pred = odmoe.PREDICTORS[args.predictor]
     log(rank, "create engine")
     t_create = time.time()
     refine = args.refine if args.predictor.startswith("shadow") else 0
     eng = odmoe.Engine(device=local, rank=rank, world_size=world, nccl_id=uid, predictor=pred,
-                       slots_per_gpu=args.slots, lookahead=D, time_kernels=1, weight_seed=SEED,
-                       refine_depth=refine, **SHAPE)
+                       slots_per_gpu=n_slots(args, n), lookahead=D, time_kernels=1, weight_seed=SEED,
+                       refine_depth=refine, placement=int(sliced(args, n)), **SHAPE)
     t_create = time.time() - t_create
     def barrier():
         if dist is not None:
@@ -367,7 +389,8 @@ def main():
     if rank == 0:
         n_exp = max(1, st["n_w13"])
         gemv_ms = (st["ms_w13"] + st["ms_w2"]) / n_exp
-        achieved = EXPERT_BYTES / (gemv_ms * 1e-3) / 1e9
+        blob = EXPERT_BYTES // n if sliced(args, n) else EXPERT_BYTES   # bytes one launch pair streams
+        achieved = blob / (gemv_ms * 1e-3) / 1e9
         traffic = None
         prof = os.path.join(ROOT, "profiles", "ncu_expert_gemv_r01.json")
         if os.path.exists(prof):
@@ -393,7 +416,7 @@ def main():
             "roofline": {"bound": "hbm", "kernel": "expert SwiGLU GEMV (W13+SwiGLU, W2+gate)",
                          "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
-                         "peak_source": peak_src, "bytes_per_launch_pair": EXPERT_BYTES,
+                         "peak_source": peak_src, "bytes_per_launch_pair": blob,
                          "avg_us_per_expert": gemv_ms * 1e3, "w13_us": st["ms_w13"] / n_exp * 1e3,
                          "w2_us": st["ms_w2"] / n_exp * 1e3},
             "host_link": {"bound": "pcie_h2d", "achieved": bytes_all / dev_s / 1e9,
@@ -417,10 +440,11 @@ def main():
         }
         # Eq. 1 (reading Q12): t_maxload = N_G t^M + (N_G - 1) t^W; the method is I/O-bound
         # when one expert's load takes longer ("compare it with t^maxload")
-        ng = max(1, n // 2)
+        ng = 1 if sliced(args, n) else max(1, n // 2)
+        per_layer = 2 if (n == 1 or sliced(args, n)) else 1     # launch pairs one GPU runs per layer
         t_M = st["ms_router"] / max(1, st["n_router"]) * 1e3
-        t_W = gemv_ms * 1e3 * (2 if n == 1 else 1)
-        t_load = EXPERT_BYTES / (link_all / n * 1e9) * 1e6 * (2 if n == 1 else 1)
+        t_W = gemv_ms * 1e3 * per_layer
+        t_load = blob / (link_all / n * 1e9) * 1e6 * per_layer
         t_max = ng * t_M + (ng - 1) * t_W
         line["eq1"] = {"N_G": ng, "t_M_us": t_M, "t_W_us": t_W, "t_load_us": t_load, "t_maxload_us": t_max,
                        "io_bottlenecked": t_load > t_max,
@@ -466,7 +490,8 @@ def resident_baseline(odmoe, torch, args, dev, rank, world, dist):
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
     eng = odmoe.Engine(device=dev, rank=rank, world_size=world, nccl_id=uid, predictor=odmoe.PRED_NONE,
-                       slots_per_gpu=-1, time_kernels=1, weight_seed=SEED, **SHAPE)
+                       slots_per_gpu=-1, time_kernels=1, weight_seed=SEED, placement=int(sliced(args, world)),
+                       **SHAPE)
     tok = 1
     for _ in range(args.warmup):
         tok, _ = eng.decode_step(tok, records=False)
@@ -490,8 +515,9 @@ def resident_baseline(odmoe, torch, args, dev, rank, world, dist):
         s = float(t[0])
     n_exp = max(1, st["n_w13"])
     gemv_ms = (st["ms_w13"] + st["ms_w2"]) / n_exp
+    blob = EXPERT_BYTES // world if sliced(args, world) else EXPERT_BYTES
     return {"value": args.steps / s, "unit": UNIT, "ms_per_step": s / args.steps * 1e3,
-            "expert_gemv_us": gemv_ms * 1e3, "expert_gemv_GBps": EXPERT_BYTES / (gemv_ms * 1e-3) / 1e9,
+            "expert_gemv_us": gemv_ms * 1e3, "expert_gemv_GBps": blob / (gemv_ms * 1e-3) / 1e9,
             "resident_expert_bytes_per_gpu": st["resident_bytes"],
             "hbm_roofline_tok_s_1gpu": 6541.5e9 / (64 * EXPERT_BYTES + SHAPE["V"] * SHAPE["d"] * 2)}
 

@@ -73,6 +73,17 @@ typedef enum {
                                  INT8 and BF16 (reading Q28); embedding/routers int8 */
 } odmoe_predictor;
 
+/* Where expert work goes at N > 1 GPUs. */
+typedef enum {
+  ODMOE_PLACE_GROUPS = 0,  /* the paper's placement: G = min(k, N) GPUs per group, layer l on
+                              group l mod N_G, sorted experts <-> sorted GPUs; one whole expert per GPU   */
+  ODMOE_PLACE_SLICED = 1   /* SURVEY §8(f)3 "sliced loading": every GPU holds, loads and computes 1/N of
+                              every expert (W13 rows of its F/N gate/up pairs, the matching W2 columns),
+                              sums its k gated partials and the N partials are reduced on GPU 0. All N host
+                              links serve every layer, so lookahead 1 suffices. Needs F % (16 N) == 0; not
+                              with SHADOW_SAME; slots_per_gpu counts slice slots (>= k)                */
+} odmoe_placement;
+
 typedef struct {
   int32_t L, E, k, d, F, V;  /* Mixtral 32,8,2,4096,14336,32000; tiny 4,8,2,256,512,1024           */
   int32_t dtype;             /* odmoe_dtype of the main model's weights and of the normalised input u */
@@ -92,7 +103,8 @@ typedef struct {
   int32_t refine_depth;      /* R >= 0: SEP refinement ("Mode B"): after the main router of
                                 layer l the shadow re-runs layers l..l+R-1 from the main model's exact
                                 state and corrects the loads of layers l+1..l+R; 0 = off (paper's Mode A) */
-  int32_t reserved[6];
+  int32_t placement;         /* odmoe_placement: 0 = the paper's worker groups, 1 = sliced      */
+  int32_t reserved[5];
   const void* nccl_id;       /* 128-byte ncclUniqueId from rank 0 (NULL when world_size == 1)          */
 } odmoe_config;
 

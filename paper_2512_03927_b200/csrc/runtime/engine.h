@@ -36,6 +36,9 @@ struct Ctx {
   size_t esz = 2;
   int64_t blob_elems = 0, blob_bytes = 0, w13_bytes = 0;
   int world = 1, rank = 0, G = 1, NG = 1, my_group = 0, my_pos = 0;
+  bool sliced = false;    // ODMOE_PLACE_SLICED: this rank's experts are F/N-wide slices
+  int Fs = 0;             // F of the blobs this rank holds (F, or F / world when sliced)
+  int64_t full_bytes = 0; // one whole expert blob (generator output)
   bool resident = false;
   int built_pred = -1;           // predictor the ctx was created with (decides whether a shadow exists)
   int dev = 0;
@@ -80,6 +83,7 @@ struct Ctx {
   float* d_y = nullptr;          // [k][d] per-expert outputs (this GPU)
   float* d_yred = nullptr;       // [d] reduced output (rank 0, N > 1)
   float* d_zero = nullptr;       // [d] zeros (idle ranks' reduce contribution)
+  float* d_ysum = nullptr;       // [d] sliced placement: sum of this rank's k gated partials
   const float** d_yptr = nullptr;    // [k] -> d_y parts (N = 1)
   const float** d_yredptr = nullptr; // [1] -> d_yred
   int32_t* d_tok_in = nullptr;

@@ -167,6 +167,7 @@ int plan_layer(int k, int world, int G, int l, const int32_t* S, int rank, int32
 // distinct ids for i in [p*k/G, (p+1)*k/G), so it needs >= p*k/G smaller and >= (G-1-p)*k/G larger
 // ids among E experts.
 bool plan_pool_holds(int E, int k, int world, int G, int l, int e, int rank) {
+  if (G == 0) return true;  // sliced placement: every rank holds a slice of every expert
   const int NG = world / G;
   if ((l % NG) != rank / G) return false;
   const int pos = rank % G;
@@ -176,6 +177,7 @@ bool plan_pool_holds(int E, int k, int world, int G, int l, int e, int rank) {
 }
 
 std::vector<int> my_experts(const Ctx* c, int l, const int32_t* S) {
+  if (c->sliced) return std::vector<int>(S, S + c->k);  // every rank: its slice of all k experts
   int32_t buf[8];
   const int n = plan_layer(c->k, c->world, c->G, l, S, c->rank, buf);
   return std::vector<int>(buf, buf + n);
@@ -192,6 +194,13 @@ void validate(const odmoe_config* g) {
   if (g->d % 8 || g->F % 8) bad("d and F must be multiples of 8");
   if (g->dtype != ODMOE_BF16 && g->dtype != ODMOE_FP32) bad("dtype");
   if (g->predictor < 0 || g->predictor > 8) bad("predictor");
+  if (g->placement != ODMOE_PLACE_GROUPS && g->placement != ODMOE_PLACE_SLICED) bad("placement");
+  if (g->placement == ODMOE_PLACE_SLICED && g->world_size > 1) {
+    if (g->F % (16 * g->world_size)) bad("sliced placement needs F % (16 N) == 0");
+    if (g->predictor == ODMOE_PRED_SHADOW_SAME) bad("sliced placement: SHADOW_SAME keeps whole experts");
+    if (g->group_size != 0) bad("sliced placement: group_size must be 0");
+    if (g->slots_per_gpu != -1 && g->slots_per_gpu < g->k) bad("sliced placement needs slots_per_gpu >= k");
+  }
   if (g->predictor == ODMOE_PRED_SHADOW_NF4 && (g->d % 64 || g->F % 64)) bad("the NF4 shadow needs d, F multiples of 64");
   if (g->lookahead < 1) bad("lookahead must be >= 1");
   if (g->world_size < 1 || g->rank < 0 || g->rank >= g->world_size) bad("rank/world_size");
@@ -313,7 +322,23 @@ void build_shadow(Ctx* c, char* staging) {
 
 // Which (layer, expert) blobs this rank may ever need.
 bool rank_may_need(const Ctx* c, int l, int e) {
-  return plan_pool_holds(c->E, c->k, c->world, c->G, l, e, c->rank);
+  return plan_pool_holds(c->E, c->k, c->world, c->sliced ? 0 : c->G, l, e, c->rank);
+}
+
+// Generate expert (l, e) into dst: the whole blob, or (sliced placement) this rank's slice: W13
+// gate/up pairs [f0, f0 + Fs) (contiguous rows of the interleaved W13) and W2 columns [f0, f0 + Fs)
+// (a pitched copy), laid out as a blob of an expert with F = Fs. `full` is whole-blob scratch.
+void gen_blob(Ctx* c, int l, int e, char* dst, char* full) {
+  const int d = c->d, F = c->F;
+  if (!c->sliced) {
+    CUDA_OK(c, launch_gen(dst, 0, l, e, 0, 0, 0, d, F, c->cfg.weight_seed, c->wt, c->s_main));
+    return;
+  }
+  CUDA_OK(c, launch_gen(full, 0, l, e, 0, 0, 0, d, F, c->cfg.weight_seed, c->wt, c->s_main));
+  const size_t es = c->esz, f0 = (size_t)c->rank * c->Fs;
+  CUDA_OK(c, cudaMemcpyAsync(dst, full + 2 * f0 * d * es, (size_t)c->w13_bytes, cudaMemcpyDeviceToDevice, c->s_main));
+  CUDA_OK(c, cudaMemcpy2DAsync(dst + c->w13_bytes, (size_t)c->Fs * es, full + (size_t)2 * F * d * es + f0 * es,
+                               (size_t)F * es, (size_t)c->Fs * es, (size_t)d, cudaMemcpyDeviceToDevice, c->s_main));
 }
 
 void build_pool(Ctx* c, char* staging) {
@@ -332,7 +357,7 @@ void build_pool(Ctx* c, char* staging) {
       for (int e = 0; e < E; ++e)
         if (c->pool_off[(size_t)l * E + e] >= 0 || (c->rank == 0 && c->cfg.predictor == ODMOE_PRED_SHADOW_SAME)) {
           char* p = dmalloc<char>(c, c->blob_bytes, "resident expert");
-          CUDA_OK(c, launch_gen(p, 0, l, e, 0, 0, 0, d, F, c->cfg.weight_seed, c->wt, c->s_main));
+          gen_blob(c, l, e, p, staging);
           c->res_blob[(size_t)l * E + e] = p;
           c->stats.resident_bytes += c->blob_bytes;
         }
@@ -350,7 +375,7 @@ void build_pool(Ctx* c, char* staging) {
     }
     c->pool = hmalloc<char>(c, (size_t)c->pool_bytes, "expert pool");
     // Fill the pool: generate each blob on the GPU, copy D2H into its pinned slot.
-    char* stg[2] = {staging, staging + c->blob_bytes};
+    char* stg[2] = {staging + c->full_bytes, staging + c->full_bytes + c->blob_bytes};
     cudaEvent_t done[2];
     CUDA_OK(c, cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming));
     CUDA_OK(c, cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming));
@@ -362,7 +387,7 @@ void build_pool(Ctx* c, char* staging) {
         if (off < 0) continue;
         const int b = i++ & 1;
         if (used[b]) CUDA_OK(c, cudaEventSynchronize(done[b]));
-        CUDA_OK(c, launch_gen(stg[b], 0, l, e, 0, 0, 0, d, F, c->cfg.weight_seed, c->wt, c->s_main));
+        gen_blob(c, l, e, stg[b], staging);
         CUDA_OK(c, cudaMemcpyAsync(c->pool + off, stg[b], c->blob_bytes, cudaMemcpyDeviceToHost, c->s_main));
         CUDA_OK(c, cudaEventRecord(done[b], c->s_main));
         used[b] = true;
@@ -405,6 +430,7 @@ void build_buffers(Ctx* c) {
   c->d_y = dmalloc<float>(c, (size_t)k * d, "y");
   c->d_yred = dmalloc<float>(c, d, "yred");
   c->d_zero = dmalloc<float>(c, d, "zero");
+  c->d_ysum = dmalloc<float>(c, d, "ysum");
   CUDA_OK(c, cudaMemset(c->d_zero, 0, sizeof(float) * d));
   CUDA_OK(c, cudaMemset(c->d_y, 0, sizeof(float) * k * d));
   c->d_yptr = dmalloc<const float*>(c, k, "yptr");
@@ -890,17 +916,18 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
     if (c->resident) {
       // routing consumed on the device: no host round trip per layer
       if (in_group) {
-        const int mine = k / c->G;
+        const int mine = c->sliced ? k : k / c->G;
         for (int j = 0; j < mine; ++j) {
+          const bool own = c->world == 1 || c->sliced;  // this rank computes (a slice of) every expert
           ExpertRef ex{nullptr, nullptr, (const void* const*)c->d_res_tbl, nullptr, ids_dev,
-                       c->world == 1 ? j : c->my_pos, l * E, k, c->world == 1 ? 0 : 1};
+                       own ? j : c->my_pos, l * E, k, own ? 0 : 1};
           float* y = c->d_y + (size_t)j * d;
           if (fused) {
             KTimer t(c, K_W13, s);
-            CUDA_OK(c, launch_expert_fused(ex, nullptr, nullptr, c->wt, pkt, u_f32, c->d_a + (size_t)j * F, w_dev, y, d, F, s, true));
+            CUDA_OK(c, launch_expert_fused(ex, nullptr, nullptr, c->wt, pkt, u_f32, c->d_a + (size_t)j * F, w_dev, y, d, c->Fs, s, true));
           } else {
-            { KTimer t(c, K_W13, s); CUDA_OK(c, launch_w13(ex, c->wt, pkt, u_f32, c->d_a + (size_t)j * F, d, F, s, true)); }
-            { KTimer t(c, K_W2, s); CUDA_OK(c, launch_w2(ex, c->wt, c->d_a + (size_t)j * F, w_dev, y, d, F, s, true)); }
+            { KTimer t(c, K_W13, s); CUDA_OK(c, launch_w13(ex, c->wt, pkt, u_f32, c->d_a + (size_t)j * F, d, c->Fs, s, true)); }
+            { KTimer t(c, K_W2, s); CUDA_OK(c, launch_w2(ex, c->wt, c->d_a + (size_t)j * F, w_dev, y, d, c->Fs, s, true)); }
           }
           if (c->dbg_ypart) CUDA_OK(c, cudaMemcpyAsync(c->dbg_ypart + ((size_t)l * k + j) * d, y, sizeof(float) * d, cudaMemcpyDeviceToDevice, s));
         }
@@ -960,7 +987,7 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
             if (c->loader.error() != cudaSuccess) CUDA_OK(c, c->loader.error());
             fail(c, ODMOE_E_STATE, "load was cancelled before compute");
           }
-          const int ypos = c->world == 1 ? j : jj;
+          const int ypos = (c->world == 1 || c->sliced) ? j : jj;
           float* y = c->d_y + (size_t)ypos * d;
           ExpertRef e13 = direct_ref(sl.dev, nullptr, j);
           ExpertRef e2 = direct_ref(sl.dev + c->w13_bytes, nullptr, j);
@@ -968,12 +995,12 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
             CUDA_OK(c, cudaStreamWaitEvent(s, sl.ev_done, 0));
             KTimer t(c, K_W13, s);
             CUDA_OK(c, launch_expert_fused(e13, sl.dev + c->w13_bytes, nullptr, c->wt, pkt, u_f32, c->d_a + (size_t)ypos * F,
-                                           w_dev, y, d, F, s, false));
+                                           w_dev, y, d, c->Fs, s, false));
           } else {  // W13 starts as soon as its part has landed, W2 after the rest
             CUDA_OK(c, cudaStreamWaitEvent(s, sl.ev_w13, 0));
-            { KTimer t(c, K_W13, s); CUDA_OK(c, launch_w13(e13, c->wt, pkt, u_f32, c->d_a + (size_t)ypos * F, d, F, s)); }
+            { KTimer t(c, K_W13, s); CUDA_OK(c, launch_w13(e13, c->wt, pkt, u_f32, c->d_a + (size_t)ypos * F, d, c->Fs, s)); }
             CUDA_OK(c, cudaStreamWaitEvent(s, sl.ev_done, 0));
-            { KTimer t(c, K_W2, s); CUDA_OK(c, launch_w2(e2, c->wt, c->d_a + (size_t)ypos * F, w_dev, y, d, F, s)); }
+            { KTimer t(c, K_W2, s); CUDA_OK(c, launch_w2(e2, c->wt, c->d_a + (size_t)ypos * F, w_dev, y, d, c->Fs, s)); }
           }
           // evict right after use: the slot is reusable once this event fires (Q16)
           CUDA_OK(c, cudaEventRecord(sl.ev_free, s));
@@ -1000,6 +1027,12 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
     }
     if (c->world > 1) {
       const float* send = (in_group ? c->d_y : c->d_zero);
+      if (c->sliced) {  // this rank's k gated partials, summed in router rank order
+        CUDA_OK(c, cudaMemsetAsync(c->d_ysum, 0, sizeof(float) * d, s));
+        CUDA_OK(c, launch_combine(c->d_ysum, c->d_yptr, k, d, s));
+        c->stats.kernel_launches++;
+        send = c->d_ysum;
+      }
       NCCL_OK(c, ncclReduce(send, c->d_yred, d, ncclFloat32, ncclSum, 0, c->comm, s));
       if (c->dbg_yred && r0) CUDA_OK(c, cudaMemcpyAsync(c->dbg_yred + (size_t)l * d, c->d_yred, sizeof(float) * d, cudaMemcpyDeviceToDevice, s));
     }
@@ -1134,13 +1167,14 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
 // layer"; with fewer GPUs it keeps the decode pool placement and round-robins the loads over the
 // groups, so group g loads layer l + 1 while another group computes layer l.
 bool prefill_mine(const Ctx* c, int l, int e) {
+  if (c->sliced) return true;  // every rank: its slice of every expert
   return (l % c->NG) == c->my_group && e * c->G / c->E == c->my_pos;
 }
 
 void ensure_prefill(Ctx* c, int T) {
   const int E = c->E, k = c->k, d = c->d, F = c->F;
   if (c->pslots.empty() && !c->resident) {
-    c->pslots.resize((size_t)2 * std::max(1, E / c->G));
+    c->pslots.resize((size_t)2 * (c->sliced ? E : std::max(1, E / c->G)));
     for (auto& s : c->pslots) {
       s.dev = dmalloc<char>(c, c->blob_bytes, "prefill slot");
       CUDA_OK(c, cudaEventCreateWithFlags(&s.ev_w13, cudaEventDisableTiming));
@@ -1168,7 +1202,7 @@ void ensure_prefill(Ctx* c, int T) {
   c->p_a2 = dmalloc<char>(c, (size_t)M * F * 2, "p_a2");
   c->p_y = dmalloc<float>(c, (size_t)M * d, "p_y");
   c->p_part = dmalloc<float>(c, (size_t)T * d, "p_part");
-  c->tiles_cap = (int)(((M + 127) / 128 + E) * (2 * F / grouped_gemm_bn(0) + d / grouped_gemm_bn(1)));
+  c->tiles_cap = (int)(((M + 127) / 128 + E) * (2 * c->Fs / grouped_gemm_bn(0) + d / grouped_gemm_bn(1)));
   c->p_tiles = dmalloc<int4>(c, (size_t)c->tiles_cap, "p_tiles");
   c->T_cap = T;
 }
@@ -1185,10 +1219,10 @@ void build_tiles(const std::vector<int32_t>& off, const std::vector<int>& mine, 
 }
 
 void prefill_impl(Ctx* c, const int32_t* tokens, int T, int32_t* token_out, int32_t* counts_out) {
-  const int L = c->L, E = c->E, k = c->k, d = c->d, F = c->F;
+  const int L = c->L, E = c->E, k = c->k, d = c->d;
   if (c->wt != W_BF16) fail(c, ODMOE_E_CONFIG, "prefill runs the bf16 tensor-core GEMM: needs dtype BF16");
   if (E > kMaxGGExperts) fail(c, ODMOE_E_CONFIG, "prefill supports E <= 8");
-  if (d % 256 || F % 128) fail(c, ODMOE_E_CONFIG, "prefill needs d % 256 == 0 and F % 128 == 0");
+  if (d % 256 || c->Fs % 128) fail(c, ODMOE_E_CONFIG, "prefill needs d % 256 == 0 and F (per rank) % 128 == 0");
   if (T < 1 || !tokens) fail(c, ODMOE_E_CONFIG, "empty prompt (S:108)");
   for (int t = 0; t < T; ++t)
     if (tokens[t] < 0 || tokens[t] >= c->V) fail(c, ODMOE_E_RANGE, "token out of range");
@@ -1263,7 +1297,7 @@ void prefill_impl(Ctx* c, const int32_t* tokens, int T, int32_t* token_out, int3
         if (prefill_mine(c, l, e)) mine.push_back(e);
       CUDA_OK(c, launch_gather_rows(u, c->p_src, k, (int)M, d, c->p_x, s));
       tiles.clear();
-      build_tiles(off, mine, 2 * F, grouped_gemm_bn(0), tiles);
+      build_tiles(off, mine, 2 * c->Fs, grouped_gemm_bn(0), tiles);
       const int n1 = (int)tiles.size();
       build_tiles(off, mine, d, grouped_gemm_bn(1), tiles);
       const int n2 = (int)tiles.size() - n1;
@@ -1292,9 +1326,9 @@ void prefill_impl(Ctx* c, const int32_t* tokens, int T, int32_t* token_out, int3
         g1.b[e] = blob;
         g2.b[e] = blob + c->w13_bytes;
       }
-      g1.a = c->p_x; g1.tiles = c->p_tiles; g1.n_tiles = n1; g1.M = (int)M; g1.N = 2 * F; g1.K = d;
+      g1.a = c->p_x; g1.tiles = c->p_tiles; g1.n_tiles = n1; g1.M = (int)M; g1.N = 2 * c->Fs; g1.K = d;
       g1.mode = 0; g1.out = c->p_a2; g1.gate = nullptr;
-      g2.a = c->p_a2; g2.tiles = c->p_tiles + n1; g2.n_tiles = n2; g2.M = (int)M; g2.N = d; g2.K = F;
+      g2.a = c->p_a2; g2.tiles = c->p_tiles + n1; g2.n_tiles = n2; g2.M = (int)M; g2.N = d; g2.K = c->Fs;
       g2.mode = 1; g2.out = c->p_y; g2.gate = c->p_gate;
       if (c->world > 1) CUDA_OK(c, cudaMemsetAsync(c->p_y, 0, sizeof(float) * M * d, s));
       { KTimer t(c, K_W13, s); CUDA_OK(c, launch_grouped_gemm(g1, s)); }
@@ -1447,12 +1481,15 @@ odmoe_status odmoe_create(const odmoe_config* cfg, void** ctx_out) {
     c->L = cfg->L; c->E = cfg->E; c->k = cfg->k; c->d = cfg->d; c->F = cfg->F; c->V = cfg->V;
     c->wt = wtype(cfg->dtype);
     c->esz = dsize(cfg->dtype);
-    c->blob_elems = 3LL * c->F * c->d;
-    c->blob_bytes = c->blob_elems * (int64_t)c->esz;
-    c->w13_bytes = 2LL * c->F * c->d * (int64_t)c->esz;
     c->world = cfg->world_size;
     c->rank = cfg->rank;
-    c->G = cfg->group_size > 0 ? cfg->group_size : std::min(c->k, c->world);
+    c->sliced = cfg->placement == ODMOE_PLACE_SLICED && c->world > 1;
+    c->Fs = c->sliced ? c->F / c->world : c->F;
+    c->full_bytes = 3LL * c->F * c->d * (int64_t)c->esz;
+    c->blob_elems = 3LL * c->Fs * c->d;
+    c->blob_bytes = c->blob_elems * (int64_t)c->esz;
+    c->w13_bytes = 2LL * c->Fs * c->d * (int64_t)c->esz;
+    c->G = c->sliced ? c->world : (cfg->group_size > 0 ? cfg->group_size : std::min(c->k, c->world));
     c->NG = c->world / c->G;
     c->my_group = c->rank / c->G;
     c->my_pos = c->rank % c->G;
@@ -1472,7 +1509,7 @@ odmoe_status odmoe_create(const odmoe_config* cfg, void** ctx_out) {
         NCCL_OK(c, ncclCommInitRank(&c->comm, c->world, id, c->rank));
         NCCL_OK(c, ncclCommSplit(c->comm, 0, c->rank, &c->comm_pred, nullptr));
       }
-      char* staging = dmalloc<char>(c, (size_t)c->blob_bytes * 2, "staging");
+      char* staging = dmalloc<char>(c, (size_t)(c->full_bytes + 2 * c->blob_bytes), "staging");
       if (c->rank == 0) build_nonexpert(c);
       build_pool(c, staging);
       if (c->has_shadow) build_shadow(c, staging);

@@ -16,6 +16,7 @@ LIB_PATH = os.environ.get("ODMOE_LIB") or os.path.join(_HERE, "libodmoe.so")
 BF16, FP32 = 0, 1
 (PRED_SHADOW_INT8, PRED_NONE, PRED_RANDOM, PRED_PERFECT, PRED_SHADOW_SAME, PRED_GATE_REUSE, PRED_SHADOW_BF16,
  PRED_SHADOW_NF4, PRED_SHADOW_FP8) = range(9)
+PLACE_GROUPS, PLACE_SLICED = 0, 1
 PREDICTORS = {"shadow_int8": 0, "none": 1, "random": 2, "perfect": 3, "shadow_same": 4, "gate_reuse": 5,
               "shadow_bf16": 6, "shadow_nf4": 7, "shadow_fp8": 8}
 
@@ -53,7 +54,7 @@ class Config(ctypes.Structure):
                 ("device", ctypes.c_int32), ("chunk_bytes", ctypes.c_int64),
                 ("debug_capture", ctypes.c_int32), ("time_kernels", ctypes.c_int32),
                 ("pool_threads", ctypes.c_int32), ("refine_depth", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 6),
+                ("placement", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5),
                 ("nccl_id", ctypes.c_void_p)]
 
 
@@ -290,13 +291,13 @@ class Engine:
     def __init__(self, L, E, k, d, F, V, dtype=BF16, predictor=PRED_SHADOW_INT8, lookahead=1,
                  slots_per_gpu=2, rms_eps=1e-5, weight_seed=2512, aux_seed=1, rank=0, world_size=1,
                  group_size=0, device=0, chunk_bytes=0, debug_capture=0, time_kernels=0,
-                 nccl_id: Optional[bytes] = None, refine_depth=0):
+                 nccl_id: Optional[bytes] = None, refine_depth=0, placement=0):
         self.cfg = Config(L=L, E=E, k=k, d=d, F=F, V=V, dtype=dtype, predictor=predictor,
                           lookahead=lookahead, slots_per_gpu=slots_per_gpu, rms_eps=rms_eps,
                           weight_seed=weight_seed, aux_seed=aux_seed, rank=rank, world_size=world_size,
                           group_size=group_size, device=device, chunk_bytes=chunk_bytes,
                           debug_capture=debug_capture, time_kernels=time_kernels, pool_threads=0,
-                          refine_depth=refine_depth)
+                          refine_depth=refine_depth, placement=placement)
         self._uid = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
         self.cfg.nccl_id = ctypes.cast(self._uid, ctypes.c_void_p) if self._uid is not None else None
         self.L, self.E, self.k, self.d, self.F, self.V = L, E, k, d, F, V

@@ -14,7 +14,7 @@ SEED = 2512
 N_TOK = 10
 
 
-def _run_rank(rank, world, port, q, predictor, slots, lookahead, prompt, refine=0):
+def _run_rank(rank, world, port, q, predictor, slots, lookahead, prompt, refine=0, placement=0):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     import torch as t
@@ -27,7 +27,7 @@ def _run_rank(rank, world, port, q, predictor, slots, lookahead, prompt, refine=
     try:
         eng = odmoe.Engine(TINY.L, TINY.E, TINY.k, TINY.d, TINY.F, TINY.V, dtype=odmoe.BF16, predictor=predictor,
                            slots_per_gpu=slots, lookahead=lookahead, weight_seed=SEED, rank=rank, world_size=world,
-                           device=rank, nccl_id=obj[0], refine_depth=refine)
+                           device=rank, nccl_id=obj[0], refine_depth=refine, placement=placement)
         toks, routes = [], []
         pf = None
         if prompt:
@@ -47,12 +47,14 @@ def _run_rank(rank, world, port, q, predictor, slots, lookahead, prompt, refine=
     dist.destroy_process_group()
 
 
-def _multi(world, predictor, slots=2, lookahead=1, prompt=None, refine=0):
+def _multi(world, predictor, slots=2, lookahead=1, prompt=None, refine=0, placement=0):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29600 + world * 11 + predictor * 3 + refine * 2 + (5 if slots == -1 else 0) + os.getpid() % 50
-    ps = [ctx.Process(target=_run_rank, args=(r, world, port, q, predictor, slots, lookahead, prompt, refine))
+    port = (29600 + world * 11 + predictor * 3 + refine * 2 + (5 if slots == -1 else 0) + 7 * placement
+            + os.getpid() % 50)
+    ps = [ctx.Process(target=_run_rank, args=(r, world, port, q, predictor, slots, lookahead, prompt, refine,
+                                              placement))
           for r in range(world)]
     for p in ps:
         p.start()
@@ -99,5 +101,32 @@ def test_multi_gpu_bitwise_invariance(world):
         assert r[2] == base_toks
     # fully resident at N GPUs (device-side routing, no host sync per layer)
     res = _multi(world, odmoe.PRED_NONE, slots=-1)
+    for r in res:
+        assert r[2] == base_toks
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_multi_gpu_sliced_placement(world):
+    """Sliced loading: every GPU holds/loads/computes 1/N of every expert and the
+    N partial outputs are reduced on GPU 0. Values change only by the split of the F-sum (within
+    fp32 rounding), so greedy tokens and routing match the 1-GPU run on TINY; two runs are
+    bitwise identical (fixed reduction order); prefill (tensor-core grouped GEMM on F/N slices)
+    gives the same token and expert counts."""
+    t = torch()
+    if t.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    from paper_2512_03927_b200 import odmoe
+    prompt = [int(x) for x in gen_prompt(TINY, 5, 24)]
+    base_toks, base_routes, base_pf = _single(odmoe.PRED_NONE, prompt=prompt)
+    runs = []
+    for pred, refine in ((odmoe.PRED_SHADOW_INT8, 0), (odmoe.PRED_SHADOW_INT8, 1), (odmoe.PRED_NONE, 0)):
+        res = _multi(world, pred, slots=4, lookahead=1, prompt=prompt, refine=refine, placement=odmoe.PLACE_SLICED)
+        for r in res:
+            assert r[2] == base_toks, (world, pred, r[0])
+            assert r[4] == base_pf, (world, pred, r[0])
+            assert r[5] <= 4
+        assert res[0][3] == base_routes
+        runs.append(res[0][2])
+    res = _multi(world, odmoe.PRED_NONE, slots=-1, placement=odmoe.PLACE_SLICED)   # resident, sliced
     for r in res:
         assert r[2] == base_toks

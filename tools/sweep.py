@@ -27,7 +27,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--lookaheads", default="1,2,3,4")
     ap.add_argument("--predictors", default="shadow_int8,perfect,gate_reuse,none,random")
-    ap.add_argument("--slots", type=int, default=2)
+    ap.add_argument("--slots", type=int, default=0, help="0 => 2 (groups) or 2k (sliced)")
+    ap.add_argument("--placement", default="groups", choices=["groups", "sliced"])
     ap.add_argument("--refine", default="0", help="comma list of SEP refinement depths (shadow predictor only)")
     ap.add_argument("--out", default="")
     ap.add_argument("--build-predictor", default="shadow_int8",
@@ -49,7 +50,8 @@ def main():
         uid = obj[0]
     eng = odmoe.Engine(device=local, rank=rank, world_size=world, nccl_id=uid,
                        predictor=odmoe.PREDICTORS[args.build_predictor],
-                       slots_per_gpu=args.slots, lookahead=1, weight_seed=2512, **SHAPE)
+                       slots_per_gpu=args.slots or (4 if args.placement == "sliced" and world > 1 else 2),
+                       lookahead=1, weight_seed=2512, placement=int(args.placement == "sliced"), **SHAPE)
     lines = []
     combos = []
     for pname in args.predictors.split(","):
@@ -91,7 +93,7 @@ def main():
                 recb = st["refine_correct"] / st["refine_total"] if st["refine_total"] else None
                 if pname.startswith("shadow"):
                     pname = args.build_predictor
-                line = {"n_gpus": world, "predictor": pname, "lookahead": D, "refine_depth": R,
+                line = {"n_gpus": world, "placement": args.placement, "predictor": pname, "lookahead": D, "refine_depth": R,
                         "recall_refined": recb, "refine_corrections_per_token": st["refine_corrections"] / args.steps,
                         "tok_s": args.steps / s,
                         "ms_per_token": s / args.steps * 1e3, "recall_eq3": rec,
