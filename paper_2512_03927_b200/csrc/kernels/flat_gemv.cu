@@ -690,9 +690,10 @@ static cudaError_t fg_launch(FlatArgs a, cudaStream_t s, bool pdl) {
   return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
-// Low-bit weights (int8 / NF4 / FP8) with fp32 activations in shared memory: the dot products then
-// skip the bf16 -> fp32 unpack of every activation pair (ALU-bound kernels). ODMOE_LOWBIT_X=bf16
-// keeps bf16 activations (A/B).
+// INT8 / FP8 weights with fp32 activations in shared memory: the dot products then skip the
+// bf16 -> fp32 unpack of every activation pair (ALU-bound kernels; INT8 expert 57.4 -> 53.3 us,
+// FP8 55.3 -> 54.1 us, profiles/kb_r01_lowbit_*.json; NF4 is faster with bf16 activations, whose
+// 64-byte-per-lane footprint keeps shared-memory traffic lower). ODMOE_LOWBIT_X=bf16: A/B.
 static bool lowbit_xf32() {
   static int v = -1;
   if (v < 0) {
@@ -711,7 +712,7 @@ cudaError_t launch_w13_flat(ExpertRef ex, WType wt, const void* u, int u_f32, fl
     case W_BF16: return fg_launch<__nv_bfloat16, uint16_t, 0>(a, s, pdl);
     case W_F32: return fg_launch<float, float, 0>(a, s, pdl);
     case W_I8: return lowbit_xf32() ? fg_launch<int8_t, float, 0>(a, s, pdl) : fg_launch<int8_t, uint16_t, 0>(a, s, pdl);
-    case W_NF4: return lowbit_xf32() ? fg_launch<nf4x2, float, 0>(a, s, pdl) : fg_launch<nf4x2, uint16_t, 0>(a, s, pdl);
+    case W_NF4: return fg_launch<nf4x2, uint16_t, 0>(a, s, pdl);  // bf16 x measured faster for NF4
     case W_F8: return lowbit_xf32() ? fg_launch<fp8e4, float, 0>(a, s, pdl) : fg_launch<fp8e4, uint16_t, 0>(a, s, pdl);
   }
   return cudaErrorInvalidValue;
@@ -818,7 +819,7 @@ cudaError_t launch_expert_fused(ExpertRef ex, const void* w2_direct, const float
     case W_BF16: return fused_launch<__nv_bfloat16, uint16_t>(a13, a2, s, pdl);
     case W_F32: return fused_launch<float, float>(a13, a2, s, pdl);
     case W_I8: return lowbit_xf32() ? fused_launch<int8_t, float>(a13, a2, s, pdl) : fused_launch<int8_t, uint16_t>(a13, a2, s, pdl);
-    case W_NF4: return lowbit_xf32() ? fused_launch<nf4x2, float>(a13, a2, s, pdl) : fused_launch<nf4x2, uint16_t>(a13, a2, s, pdl);
+    case W_NF4: return fused_launch<nf4x2, uint16_t>(a13, a2, s, pdl);
     case W_F8: return lowbit_xf32() ? fused_launch<fp8e4, float>(a13, a2, s, pdl) : fused_launch<fp8e4, uint16_t>(a13, a2, s, pdl);
   }
   return cudaErrorInvalidValue;
