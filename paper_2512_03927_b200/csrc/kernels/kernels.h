@@ -127,6 +127,13 @@ cudaError_t launch_embed_rows(const void* emb, WType wt, const int32_t* tokens, 
 cudaError_t launch_gen(void* out, int kind, int layer, int expert, int64_t rows, int64_t cols,
                        int64_t fan_in, int d, int F, uint64_t seed, WType wt, cudaStream_t s);
 
+// P2P combine over NVLink (p2p.cu): sender sums its n partials into its row of GPU 0's buffer and
+// releases `epoch` in its flag; GPU 0 waits for the flags in `mask` and sums the rows in rank order.
+cudaError_t launch_p2p_send(const float* const* y, int n, int d, float* dst, uint32_t* flag, uint32_t epoch,
+                            cudaStream_t s);
+cudaError_t launch_p2p_gather(const float* part, const uint32_t* flags, uint32_t mask, int d, uint32_t epoch,
+                              float* out, int32_t* err_flag, cudaStream_t s);
+
 // BF16 (round to nearest even) copy of an fp32 tensor: the BF16 shadow of an FP32 main model.
 cudaError_t launch_f32_to_bf16(const float* in, void* out, int64_t n, cudaStream_t s);
 

@@ -84,6 +84,14 @@ struct Ctx {
   float* d_yred = nullptr;       // [d] reduced output (rank 0, N > 1)
   float* d_zero = nullptr;       // [d] zeros (idle ranks' reduce contribution)
   float* d_ysum = nullptr;       // [d] sliced placement: sum of this rank's k gated partials
+  // P2P combine (N > 1): GPU 0 owns part [world][d] + flags [world]; every rank maps them (CUDA IPC)
+  bool p2p = false;
+  float* p2p_part = nullptr;     // GPU 0's receive rows (local on rank 0, IPC-mapped elsewhere)
+  uint32_t* p2p_flag = nullptr;
+  float* p2p_own_part = nullptr; // rank 0: the allocation (freed at destroy)
+  uint32_t* p2p_own_flag = nullptr;
+  uint32_t p2p_seq = 0;          // epoch of the next layer combine (same sequence on every rank)
+  const float** d_y1ptr = nullptr;  // device array {d_y} (one partial)
   const float** d_yptr = nullptr;    // [k] -> d_y parts (N = 1)
   const float** d_yredptr = nullptr; // [1] -> d_yred
   int32_t* d_tok_in = nullptr;

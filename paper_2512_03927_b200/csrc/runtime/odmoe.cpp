@@ -815,6 +815,60 @@ void pump(Ctx* c) {
   }
 }
 
+// ------------------------------------------------------------------ P2P combine setup
+// GPU 0 allocates the receive rows and flags, exports them with CUDA IPC and broadcasts the handles
+// over NCCL; the other ranks map them (NVLink peer access). ODMOE_P2P=0 keeps the NCCL reduce.
+void setup_p2p(Ctx* c) {
+  const char* e = getenv("ODMOE_P2P");
+  if ((e && e[0] == '0') || c->world > 32) return;
+  struct Handles { cudaIpcMemHandle_t part, flag; int ok; };
+  Handles h{};
+  if (c->rank == 0) {
+    c->p2p_own_part = dmalloc<float>(c, (size_t)c->world * c->d, "p2p part");
+    c->p2p_own_flag = dmalloc<uint32_t>(c, 32, "p2p flags");
+    CUDA_OK(c, cudaMemset(c->p2p_own_flag, 0, 32 * sizeof(uint32_t)));
+    h.ok = cudaIpcGetMemHandle(&h.part, c->p2p_own_part) == cudaSuccess &&
+           cudaIpcGetMemHandle(&h.flag, c->p2p_own_flag) == cudaSuccess;
+  }
+  char* dbuf = dmalloc<char>(c, sizeof(Handles), "p2p handles");
+  CUDA_OK(c, cudaMemcpy(dbuf, &h, sizeof(h), cudaMemcpyHostToDevice));
+  NCCL_OK(c, ncclBroadcast(dbuf, dbuf, sizeof(Handles), ncclChar, 0, c->comm, c->s_main));
+  CUDA_OK(c, cudaStreamSynchronize(c->s_main));
+  CUDA_OK(c, cudaMemcpy(&h, dbuf, sizeof(h), cudaMemcpyDeviceToHost));
+  cudaFree(dbuf);
+  int ok = h.ok;
+  if (c->rank == 0) {
+    c->p2p_part = c->p2p_own_part;
+    c->p2p_flag = c->p2p_own_flag;
+  } else if (ok) {
+    void* pp = nullptr;
+    void* pf = nullptr;
+    ok = cudaIpcOpenMemHandle(&pp, h.part, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess &&
+         cudaIpcOpenMemHandle(&pf, h.flag, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
+    if (!ok) cudaGetLastError();
+    c->p2p_part = (float*)pp;
+    c->p2p_flag = (uint32_t*)pf;
+  }
+  // every rank must agree (a rank that could not map falls back with everyone else)
+  int32_t* dok = dmalloc<int32_t>(c, 1, "p2p ok");
+  CUDA_OK(c, cudaMemcpy(dok, &ok, 4, cudaMemcpyHostToDevice));
+  NCCL_OK(c, ncclAllReduce(dok, dok, 1, ncclInt32, ncclMin, c->comm, c->s_main));
+  CUDA_OK(c, cudaStreamSynchronize(c->s_main));
+  CUDA_OK(c, cudaMemcpy(&ok, dok, 4, cudaMemcpyDeviceToHost));
+  cudaFree(dok);
+  c->p2p = ok != 0;
+  c->p2p_seq = 1;
+}
+
+// Ranks whose expert work feeds layer l's combine (bit r = rank r).
+uint32_t p2p_mask(const Ctx* c, int l) {
+  if (c->sliced) return c->world >= 32 ? 0xffffffffu : ((1u << c->world) - 1u);
+  const int g = l % c->NG;
+  uint32_t m = 0;
+  for (int p = 0; p < c->G; ++p) m |= 1u << (g * c->G + p);
+  return m;
+}
+
 // ------------------------------------------------------------------ one decode step
 void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_record* rec) {
   const int L = c->L, E = c->E, k = c->k, d = c->d, F = c->F;
@@ -896,6 +950,11 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
     char* pkt = c->d_pkt + (size_t)l * c->pkt_bytes;
     int32_t* ids_dev = (int32_t*)(pkt + c->pkt_ids_off);
     float* w_dev = (float*)(pkt + c->pkt_w_off);
+    if (r0 && c->p2p && l > 0) {  // layer l-1's partials from the peers (NVLink) -> d_yred
+      CUDA_OK(c, launch_p2p_gather(c->p2p_part, c->p2p_flag, p2p_mask(c, l - 1), d, c->p2p_seq - 1, c->d_yred,
+                                   c->d_flag, s));
+      c->stats.kernel_launches++;
+    }
     if (r0) {
       KTimer t(c, K_ROUTER, s);
       CUDA_OK(c, launch_router(c->d_h, yadd, n_add, nullptr, (const char*)c->d_router + (size_t)l * E * d * c->esz,
@@ -1025,7 +1084,16 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
         c->stats.wait_us += wait_us;
       }
     }
-    if (c->world > 1) {
+    if (c->world > 1 && c->p2p) {
+      // this rank's gated partials, summed in router rank order, stored into its row of GPU 0's
+      // buffer over NVLink and published with a release flag (one kernel; no NCCL reduce)
+      const uint32_t ep = c->p2p_seq++;
+      if (in_group) {
+        CUDA_OK(c, launch_p2p_send(c->d_yptr, c->sliced ? k : k / c->G, d, c->p2p_part + (size_t)c->rank * d,
+                                   c->p2p_flag + c->rank, ep, s));
+        c->stats.kernel_launches++;
+      }
+    } else if (c->world > 1) {
       const float* send = (in_group ? c->d_y : c->d_zero);
       if (c->sliced) {  // this rank's k gated partials, summed in router rank order
         CUDA_OK(c, cudaMemsetAsync(c->d_ysum, 0, sizeof(float) * d, s));
@@ -1040,6 +1108,11 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
 
   // final combine + LM head + argmax (rank 0)
   if (r0) {
+    if (c->p2p) {
+      CUDA_OK(c, launch_p2p_gather(c->p2p_part, c->p2p_flag, p2p_mask(c, L - 1), d, c->p2p_seq - 1, c->d_yred,
+                                   c->d_flag, s));
+      c->stats.kernel_launches++;
+    }
     CUDA_OK(c, launch_combine(c->d_h, yadd, n_add, d, s));
     c->stats.kernel_launches++;
     if (c->dbg_hfinal) CUDA_OK(c, cudaMemcpyAsync(c->dbg_hfinal, c->d_h, sizeof(float) * d, cudaMemcpyDeviceToDevice, s));
@@ -1057,6 +1130,7 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
   }
   CUDA_OK(c, cudaStreamSynchronize(s));
   if (!c->resident && (shadow_pred || gate_reuse) && (r0 || c->world > 1)) CUDA_OK(c, cudaStreamSynchronize(c->s_shadow));
+  if (c->h_flag[0] == 2) fail(c, ODMOE_E_STATE, "peer partials did not arrive (P2P combine timeout)");
   if (c->h_flag[0]) fail(c, ODMOE_E_NONFINITE, "non-finite router logits");
   if (c->resident) std::copy(c->h_ids, c->h_ids + (size_t)L * k, true_ids.begin());
 
@@ -1429,6 +1503,13 @@ void destroy_ctx(Ctx* c) {
   for (auto e : {c->ev_ids, c->ev_tok, c->ev_shadow_done, c->ev_step}) if (e) cudaEventDestroy(e);
   for (auto& t : c->timed) { c->tev_pool.push_back(t.a); c->tev_pool.push_back(t.b); }
   for (auto e : c->tev_pool) cudaEventDestroy(e);
+  if (c->rank != 0) {
+    if (c->p2p_part) cudaIpcCloseMemHandle(c->p2p_part);
+    if (c->p2p_flag) cudaIpcCloseMemHandle(c->p2p_flag);
+  } else {
+    if (c->p2p_own_part) cudaFree(c->p2p_own_part);
+    if (c->p2p_own_flag) cudaFree(c->p2p_own_flag);
+  }
   if (c->comm_pred) ncclCommDestroy(c->comm_pred);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->s_main) cudaStreamDestroy(c->s_main);
@@ -1500,14 +1581,19 @@ odmoe_status odmoe_create(const odmoe_config* cfg, void** ctx_out) {
                     is_shadow(cfg->predictor);
     try {
       CUDA_OK(c, cudaSetDevice(c->dev));
-      CUDA_OK(c, cudaStreamCreateWithFlags(&c->s_main, cudaStreamNonBlocking));
-      CUDA_OK(c, cudaStreamCreateWithFlags(&c->s_shadow, cudaStreamNonBlocking));
+      // The main model's stream gets the highest priority: when a shadow kernel (SEP, refinement)
+      // and a main-model kernel are both pending, the block scheduler hands freed SMs to the main one.
+      int prio_lo = 0, prio_hi = 0;
+      CUDA_OK(c, cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+      CUDA_OK(c, cudaStreamCreateWithPriority(&c->s_main, cudaStreamNonBlocking, prio_hi));
+      CUDA_OK(c, cudaStreamCreateWithPriority(&c->s_shadow, cudaStreamNonBlocking, prio_lo));
       CUDA_OK(c, cudaStreamCreateWithFlags(&c->s_copy, cudaStreamNonBlocking));
       if (c->world > 1) {
         ncclUniqueId id;
         std::memcpy(&id, cfg->nccl_id, sizeof(id));
         NCCL_OK(c, ncclCommInitRank(&c->comm, c->world, id, c->rank));
         NCCL_OK(c, ncclCommSplit(c->comm, 0, c->rank, &c->comm_pred, nullptr));
+        setup_p2p(c);
       }
       char* staging = dmalloc<char>(c, (size_t)(c->full_bytes + 2 * c->blob_bytes), "staging");
       if (c->rank == 0) build_nonexpert(c);
