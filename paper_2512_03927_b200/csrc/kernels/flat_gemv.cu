@@ -309,7 +309,7 @@ struct PdlWait {
 // barrier for the W2 phase of the fused expert kernel. Weights are prefetched before it.
 template <typename WT, typename XT, int MODE, int UNROLL, typename WaitFn>
 __device__ __forceinline__ void flat_phase(const FlatArgs& a, uint8_t* sm, const WaitFn& wait_dep,
-                                           bool ids_ready = false) {
+                                           bool ids_ready = false, long long rb_ovr = -1, long long re_ovr = -1) {
   constexpr int N = FDot<WT, XT>::kN;
   constexpr int Q = N * (int)sizeof(XT) / 16;       // uint4 activation words per granule
   constexpr int EPU = 16 / (int)sizeof(XT);         // activations per uint4
@@ -357,7 +357,9 @@ __device__ __forceinline__ void flat_phase(const FlatArgs& a, uint8_t* sm, const
     }
   }
   long long rb, re;
-  if (MODE == 0) {
+  if (rb_ovr >= 0) {  // the caller assigns this CTA's rows (multi-expert kernel)
+    rb = rb_ovr; re = re_ovr;
+  } else if (MODE == 0) {
     split_range(a.R / 2, gridDim.x, blockIdx.x, rb, re);
     rb *= 2; re *= 2;
   } else {
@@ -656,6 +658,9 @@ flat_expert_kernel(const FlatArgs a13, const FlatArgs a2, unsigned int* counter,
   flat_phase<WT, float, 1, UNROLL>(a2, sm, GridBarrier{counter, target}, /*ids_ready=*/true);
 }
 
+// Rows must be whole 512-byte groups (the flat stream's unit), else the launch is refused.
+template <typename WT> static bool flat_row_ok(long long C) { return C > 0 && (C * FTraits<WT>::bits / 8) % 512 == 0; }
+
 template <typename WT, typename XT, int MODE>
 static cudaError_t fg_launch(FlatArgs a, cudaStream_t s, bool pdl) {
   constexpr int UNROLL = kFG_UNROLL;
@@ -665,6 +670,7 @@ static cudaError_t fg_launch(FlatArgs a, cudaStream_t s, bool pdl) {
     ef = (e && e[0] == '0') ? 0 : 1;
   }
   a.evict_first = ef;
+  if (!flat_row_ok<WT>(a.C)) return cudaErrorInvalidValue;
   const int sms = num_sms();
   const long long units = MODE == 0 ? a.R / 2 : a.R;
   const int grid = (int)(units < sms ? (units > 0 ? units : 1) : sms);
@@ -748,27 +754,155 @@ cudaError_t launch_lm_head_flat(const float* h, const void* W, WType wt, int V, 
 }
 
 // ---------------------------------------------------------------- fused expert FFN launcher
+// Multi-expert fused FFN: the n (<= 4) experts of one layer that this GPU computes, in ONE
+// cooperative launch: W13 of all n (the CTAs split the n*F gate/up pairs evenly, so a CTA may own
+// the end of one expert and the start of the next), one grid barrier, W2 of all n (n*d rows). One
+// launch, ramp, barrier and tail per layer instead of per expert.
+constexpr int kMaxMulti = 4;
+struct MultiArgs {
+  FlatArgs a13[kMaxMulti], a2[kMaxMulti];
+  int n;
+};
+struct NoWait {
+  __device__ __forceinline__ void operator()() const {}
+};
+
+template <typename WT, typename XT, int UNROLL>
+__global__ void __launch_bounds__(kFG_THREADS, 1)
+flat_experts_kernel(const __grid_constant__ MultiArgs m, unsigned int* counter, unsigned int target) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  const int n = m.n;
+  // phase 1: pairs [p0, p1) of the concatenated n*F pair space
+  const long long F = m.a13[0].R / 2;
+  long long p0, p1;
+  split_range((long long)n * F, gridDim.x, blockIdx.x, p0, p1);
+  bool first = true;
+  for (int e = 0; e < n; ++e) {
+    const long long lo = p0 > e * F ? p0 : e * F, hi = p1 < (e + 1) * F ? p1 : (e + 1) * F;
+    if (lo >= hi) continue;
+    if (first) flat_phase<WT, XT, 0, UNROLL>(m.a13[e], sm, PdlWait{}, false, 2 * (lo - e * F), 2 * (hi - e * F));
+    else flat_phase<WT, XT, 0, UNROLL>(m.a13[e], sm, NoWait{}, true, 2 * (lo - e * F), 2 * (hi - e * F));
+    first = false;
+    __syncthreads();
+  }
+  // phase 2: rows [r0, r1) of the concatenated n*d row space; the first segment waits at the barrier
+  const long long D = m.a2[0].R;
+  long long r0, r1;
+  split_range((long long)n * D, gridDim.x, blockIdx.x, r0, r1);
+  first = true;
+  for (int e = 0; e < n; ++e) {
+    const long long lo = r0 > e * D ? r0 : e * D, hi = r1 < (e + 1) * D ? r1 : (e + 1) * D;
+    if (lo >= hi) continue;
+    if (first) flat_phase<WT, float, 1, UNROLL>(m.a2[e], sm, GridBarrier{counter, target}, true, lo - e * D, hi - e * D);
+    else flat_phase<WT, float, 1, UNROLL>(m.a2[e], sm, NoWait{}, true, lo - e * D, hi - e * D);
+    first = false;
+    __syncthreads();
+  }
+  if (first) GridBarrier{counter, target}();  // (a CTA without W2 rows still arrives)
+}
+
+// Grid-barrier arrival counter of this device (one per device; see fused_launch).
+static unsigned int g_epochs[64] = {0};
+static unsigned int* g_counters[64] = {nullptr};
+static cudaError_t barrier_counter(int dev) {
+  if (g_counters[dev]) return cudaSuccess;
+  cudaError_t e = cudaMalloc(&g_counters[dev], sizeof(unsigned int));
+  if (e != cudaSuccess) return e;
+  return cudaMemset(g_counters[dev], 0, sizeof(unsigned int));
+}
+
+template <typename WT, typename XT>
+static cudaError_t multi_launch(MultiArgs m, cudaStream_t s, bool pdl) {
+  constexpr int UNROLL = kFG_UNROLL;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaError_t e = barrier_counter(dev);
+  if (e != cudaSuccess) return e;
+  static int ef = -1;
+  if (ef < 0) {
+    const char* v = getenv("ODMOE_L2_EVICT_FIRST");
+    ef = (v && v[0] == '0') ? 0 : 1;
+  }
+  const int n = m.n;
+  const long long F = m.a13[0].R / 2, D = m.a2[0].R;
+  if (!flat_row_ok<WT>(m.a13[0].C) || !flat_row_ok<WT>(m.a2[0].C)) return cudaErrorInvalidValue;
+  const int sms = num_sms();
+  const long long units = (long long)n * (F < D ? F : D);
+  const int grid = (int)(units < sms ? units : sms);
+  const int cap13 = (int)(((long long)n * F + grid - 1) / grid) * 2 + 2;
+  const int cap2 = (int)(((long long)n * D + grid - 1) / grid) + 2;
+  for (int i = 0; i < n; ++i) {
+    m.a13[i].evict_first = m.a2[i].evict_first = ef;
+    m.a13[i].rows_cap = cap13;
+    m.a2[i].rows_cap = cap2;
+  }
+  const size_t lut = FTraits<WT>::nf4 ? kNF4LutWords * 4 : 0;
+  const size_t s1 = (size_t)kFG_WARPS * cap13 * sizeof(float) + (size_t)m.a13[0].C * sizeof(XT) + 16 + lut;
+  const size_t s2 = (size_t)kFG_WARPS * cap2 * sizeof(float) + (size_t)m.a2[0].C * sizeof(float) + 16 + lut;
+  const size_t smem = s1 > s2 ? s1 : s2;
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  auto kern = flat_experts_kernel<WT, XT, UNROLL>;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const unsigned int target = g_epochs[dev] + (unsigned int)grid;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kFG_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 2 : 1;
+  e = cudaLaunchKernelEx(&cfg, kern, m, g_counters[dev], target);
+  if (e == cudaSuccess) g_epochs[dev] = target;
+  return e;
+}
+
+cudaError_t launch_experts_fused(int n, const ExpertRef* ex, const void* const* w2_direct, const float* const* s2_direct,
+                                 WType wt, const void* u, int u_f32, float* a_buf, const float* gate_w,
+                                 float* const* y, int d, int F, cudaStream_t s, bool pdl) {
+  if (n < 1 || n > kMaxMulti) return cudaErrorInvalidValue;
+  MultiArgs m{};
+  m.n = n;
+  for (int i = 0; i < n; ++i) {
+    FlatArgs& a13 = m.a13[i];
+    FlatArgs& a2 = m.a2[i];
+    a13.ex = ex[i]; a13.second = 0; a13.x = u; a13.x_bf16 = !u_f32; a13.R = 2 * F; a13.C = d;
+    a13.out = a_buf + (size_t)i * F; a13.d_full = d; a13.F_full = F;
+    a2.ex = ex[i]; a2.second = 1; a2.x = a_buf + (size_t)i * F; a2.x_bf16 = 0; a2.R = d; a2.C = F;
+    a2.gate_w = gate_w; a2.out = y[i]; a2.d_full = d; a2.F_full = F;
+    if (ex[i].tbl == nullptr) {
+      a2.ex.blob = w2_direct[i];
+      a2.ex.scales = s2_direct ? s2_direct[i] : nullptr;
+    }
+  }
+  switch (wt) {
+    case W_BF16: return multi_launch<__nv_bfloat16, uint16_t>(m, s, pdl);
+    case W_F32: return multi_launch<float, float>(m, s, pdl);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 template <typename WT, typename XT>
 static cudaError_t fused_launch(FlatArgs a13, FlatArgs a2, cudaStream_t s, bool pdl) {
   constexpr int UNROLL = kFG_UNROLL;
-  static unsigned int* counters = nullptr;  // one per device
-  static unsigned int epochs[64] = {0};
-  static unsigned int* dev_counters[64] = {nullptr};
   int dev = 0;
   cudaGetDevice(&dev);
-  if (!dev_counters[dev]) {
-    cudaError_t e = cudaMalloc(&dev_counters[dev], sizeof(unsigned int));
-    if (e != cudaSuccess) return e;
-    e = cudaMemset(dev_counters[dev], 0, sizeof(unsigned int));
+  {
+    cudaError_t e = barrier_counter(dev);
     if (e != cudaSuccess) return e;
   }
-  (void)counters;
   static int ef = -1;
   if (ef < 0) {
     const char* e = getenv("ODMOE_L2_EVICT_FIRST");
     ef = (e && e[0] == '0') ? 0 : 1;
   }
   a13.evict_first = a2.evict_first = ef;
+  if (!flat_row_ok<WT>(a13.C) || !flat_row_ok<WT>(a2.C)) return cudaErrorInvalidValue;
   const int sms = num_sms();
   long long units = a13.R / 2 < a2.R ? a13.R / 2 : a2.R;
   const int grid = (int)(units < sms ? (units > 0 ? units : 1) : sms);
@@ -785,7 +919,7 @@ static cudaError_t fused_launch(FlatArgs a13, FlatArgs a2, cudaStream_t s, bool 
   // Stream-ordered launches on this device use increasing barrier targets. Only ONE stream may
   // run these kernels (the engine's compute stream): two cooperative kernels spinning on barriers
   // on different streams could hold each other's SMs.
-  const unsigned int target = epochs[dev] + (unsigned int)grid;
+  const unsigned int target = g_epochs[dev] + (unsigned int)grid;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kFG_THREADS);
@@ -798,8 +932,8 @@ static cudaError_t fused_launch(FlatArgs a13, FlatArgs a2, cudaStream_t s, bool 
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 2 : 1;
-  e = cudaLaunchKernelEx(&cfg, kern, a13, a2, dev_counters[dev], target);
-  if (e == cudaSuccess) epochs[dev] = target;
+  e = cudaLaunchKernelEx(&cfg, kern, a13, a2, g_counters[dev], target);
+  if (e == cudaSuccess) g_epochs[dev] = target;
   return e;
 }
 

@@ -70,6 +70,11 @@ cudaError_t launch_quantize_nf4(const void* w, int64_t R, int64_t C, WType wt, u
 // Fused expert FFN (flat engine): W13+SwiGLU -> grid barrier -> W2+gate in ONE cooperative
 // launch. Direct mode: ex.blob/ex.scales = W13 (+ scales), w2_direct/s2_direct = W2 (+ scales);
 // indirect mode: the expert table entries (whole blobs). a_buf: fp32 [F] scratch.
+// The n (<= 4) experts one GPU computes for a layer in ONE cooperative launch (W13 of all, one grid
+// barrier, W2 of all); a_buf: fp32 [n][F]; y[i]: output of expert i (gate-weighted). bf16 / fp32.
+cudaError_t launch_experts_fused(int n, const ExpertRef* ex, const void* const* w2_direct, const float* const* s2_direct,
+                                 WType wt, const void* u, int u_f32, float* a_buf, const float* gate_w,
+                                 float* const* y, int d, int F, cudaStream_t s, bool pdl);
 cudaError_t launch_expert_fused(ExpertRef ex, const void* w2_direct, const float* s2_direct, WType wt,
                                 const void* u, int u_f32, float* a_buf, const float* gate_w, float* y, int d,
                                 int F, cudaStream_t s, bool pdl);

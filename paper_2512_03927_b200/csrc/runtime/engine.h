@@ -156,7 +156,7 @@ struct Ctx {
   int32_t predict_cache_token = -1;
 
   // kernel timing (time_kernels)
-  struct Timed { int fam; cudaEvent_t a, b; };
+  struct Timed { int fam; cudaEvent_t a, b; int units; };  // units: experts covered by one launch
   std::vector<Timed> timed;
   std::vector<cudaEvent_t> tev_pool;
 

@@ -99,7 +99,8 @@ struct KTimer {
   int fam;
   cudaStream_t s;
   cudaEvent_t a = nullptr, b = nullptr;
-  KTimer(Ctx* c_, int fam_, cudaStream_t s_) : c(c_), fam(fam_), s(s_) {
+  int units;
+  KTimer(Ctx* c_, int fam_, cudaStream_t s_, int units_ = 1) : c(c_), fam(fam_), s(s_), units(units_) {
     c->stats.kernel_launches++;
     if (!c->cfg.time_kernels) return;
     a = get();
@@ -109,7 +110,7 @@ struct KTimer {
   ~KTimer() {
     if (!a) return;
     cudaEventRecord(b, s);
-    c->timed.push_back(Ctx::Timed{fam, a, b});
+    c->timed.push_back(Ctx::Timed{fam, a, b, units});
   }
   cudaEvent_t get() {
     if (!c->tev_pool.empty()) {
@@ -129,7 +130,7 @@ void harvest_timers(Ctx* c) {
     if (cudaEventElapsedTime(&ms, t.a, t.b) == cudaSuccess) {
       switch (t.fam) {
         case K_ROUTER: c->stats.ms_router += ms; c->stats.n_router++; break;
-        case K_W13: c->stats.ms_w13 += ms; c->stats.n_w13++; break;
+        case K_W13: c->stats.ms_w13 += ms; c->stats.n_w13 += t.units; break;
         case K_W2: c->stats.ms_w2 += ms; c->stats.n_w2++; break;
         case K_SHADOW: c->stats.ms_shadow += ms; c->stats.n_shadow++; break;
         case K_LM: c->stats.ms_lm_head += ms; c->stats.n_lm_head++; break;
@@ -882,7 +883,7 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
   // prediction communicator is idle). At N > 1 the prediction broadcasts spin on the shadow
   // stream; a cooperative grid that cannot become fully resident would wait at its barrier for
   // SMs held by a kernel that waits for a peer that waits for us.
-  const bool fused = use_fused_expert() && stream_ok(c->wt, d) && stream_ok(c->wt, F) &&
+  const bool fused = use_fused_expert() && stream_ok(c->wt, d) && stream_ok(c->wt, c->Fs) &&
                      (c->world == 1 || c->resident);
 
   // token in (pinned -> device); the previous step's shadow must be done with d_tok_in
@@ -976,12 +977,27 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
       // routing consumed on the device: no host round trip per layer
       if (in_group) {
         const int mine = c->sliced ? k : k / c->G;
+        const bool own = c->world == 1 || c->sliced;  // this rank computes (a slice of) every expert
+        if (fused && mine <= 4) {
+          // all of this GPU's experts of the layer in one cooperative launch
+          ExpertRef exs[4];
+          float* ys[4];
+          for (int j = 0; j < mine; ++j) {
+            exs[j] = ExpertRef{nullptr, nullptr, (const void* const*)c->d_res_tbl, nullptr, ids_dev,
+                               own ? j : c->my_pos * mine + j, l * E, k, own ? 0 : 1};
+            ys[j] = c->d_y + (size_t)j * d;
+          }
+          KTimer t(c, K_W13, s, mine);
+          CUDA_OK(c, launch_experts_fused(mine, exs, nullptr, nullptr, c->wt, pkt, u_f32, c->d_a, w_dev, ys, d,
+                                          c->Fs, s, true));
+        }
         for (int j = 0; j < mine; ++j) {
-          const bool own = c->world == 1 || c->sliced;  // this rank computes (a slice of) every expert
           ExpertRef ex{nullptr, nullptr, (const void* const*)c->d_res_tbl, nullptr, ids_dev,
-                       own ? j : c->my_pos, l * E, k, own ? 0 : 1};
+                       own ? j : c->my_pos * mine + j, l * E, k, own ? 0 : 1};
           float* y = c->d_y + (size_t)j * d;
-          if (fused) {
+          if (fused && mine <= 4) {
+            // launched above
+          } else if (fused) {
             KTimer t(c, K_W13, s);
             CUDA_OK(c, launch_expert_fused(ex, nullptr, nullptr, c->wt, pkt, u_f32, c->d_a + (size_t)j * F, w_dev, y, d, c->Fs, s, true));
           } else {
