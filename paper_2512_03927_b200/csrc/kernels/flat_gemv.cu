@@ -755,9 +755,10 @@ cudaError_t launch_lm_head_flat(const float* h, const void* W, WType wt, int V, 
 
 // ---------------------------------------------------------------- fused expert FFN launcher
 // Multi-expert fused FFN: the n (<= 4) experts of one layer that this GPU computes, in ONE
-// cooperative launch: W13 of all n (the CTAs split the n*F gate/up pairs evenly, so a CTA may own
-// the end of one expert and the start of the next), one grid barrier, W2 of all n (n*d rows). One
-// launch, ramp, barrier and tail per layer instead of per expert.
+// cooperative launch: W13 of all n, one grid barrier, W2 of all n. Every CTA takes the same row
+// range of each expert as the one-expert kernel would (so each output is computed with the same
+// per-warp split and is bitwise identical to it), one expert after the other. One launch, ramp,
+// barrier and tail per layer instead of per expert.
 constexpr int kMaxMulti = 4;
 struct MultiArgs {
   FlatArgs a13[kMaxMulti], a2[kMaxMulti];
@@ -772,33 +773,19 @@ __global__ void __launch_bounds__(kFG_THREADS, 1)
 flat_experts_kernel(const __grid_constant__ MultiArgs m, unsigned int* counter, unsigned int target) {
   extern __shared__ __align__(128) uint8_t sm[];
   const int n = m.n;
-  // phase 1: pairs [p0, p1) of the concatenated n*F pair space
-  const long long F = m.a13[0].R / 2;
-  long long p0, p1;
-  split_range((long long)n * F, gridDim.x, blockIdx.x, p0, p1);
-  bool first = true;
+  long long p0, p1, r0, r1;
+  split_range(m.a13[0].R / 2, gridDim.x, blockIdx.x, p0, p1);  // gate/up pairs of each expert
+  split_range(m.a2[0].R, gridDim.x, blockIdx.x, r0, r1);       // W2 rows of each expert
   for (int e = 0; e < n; ++e) {
-    const long long lo = p0 > e * F ? p0 : e * F, hi = p1 < (e + 1) * F ? p1 : (e + 1) * F;
-    if (lo >= hi) continue;
-    if (first) flat_phase<WT, XT, 0, UNROLL>(m.a13[e], sm, PdlWait{}, false, 2 * (lo - e * F), 2 * (hi - e * F));
-    else flat_phase<WT, XT, 0, UNROLL>(m.a13[e], sm, NoWait{}, true, 2 * (lo - e * F), 2 * (hi - e * F));
-    first = false;
+    if (e == 0) flat_phase<WT, XT, 0, UNROLL>(m.a13[e], sm, PdlWait{}, false, 2 * p0, 2 * p1);
+    else flat_phase<WT, XT, 0, UNROLL>(m.a13[e], sm, NoWait{}, true, 2 * p0, 2 * p1);
     __syncthreads();
   }
-  // phase 2: rows [r0, r1) of the concatenated n*d row space; the first segment waits at the barrier
-  const long long D = m.a2[0].R;
-  long long r0, r1;
-  split_range((long long)n * D, gridDim.x, blockIdx.x, r0, r1);
-  first = true;
   for (int e = 0; e < n; ++e) {
-    const long long lo = r0 > e * D ? r0 : e * D, hi = r1 < (e + 1) * D ? r1 : (e + 1) * D;
-    if (lo >= hi) continue;
-    if (first) flat_phase<WT, float, 1, UNROLL>(m.a2[e], sm, GridBarrier{counter, target}, true, lo - e * D, hi - e * D);
-    else flat_phase<WT, float, 1, UNROLL>(m.a2[e], sm, NoWait{}, true, lo - e * D, hi - e * D);
-    first = false;
+    if (e == 0) flat_phase<WT, float, 1, UNROLL>(m.a2[e], sm, GridBarrier{counter, target}, true, r0, r1);
+    else flat_phase<WT, float, 1, UNROLL>(m.a2[e], sm, NoWait{}, true, r0, r1);
     __syncthreads();
   }
-  if (first) GridBarrier{counter, target}();  // (a CTA without W2 rows still arrives)
 }
 
 // Grid-barrier arrival counter of this device (one per device; see fused_launch).
@@ -827,10 +814,10 @@ static cudaError_t multi_launch(MultiArgs m, cudaStream_t s, bool pdl) {
   const long long F = m.a13[0].R / 2, D = m.a2[0].R;
   if (!flat_row_ok<WT>(m.a13[0].C) || !flat_row_ok<WT>(m.a2[0].C)) return cudaErrorInvalidValue;
   const int sms = num_sms();
-  const long long units = (long long)n * (F < D ? F : D);
-  const int grid = (int)(units < sms ? units : sms);
-  const int cap13 = (int)(((long long)n * F + grid - 1) / grid) * 2 + 2;
-  const int cap2 = (int)(((long long)n * D + grid - 1) / grid) + 2;
+  const long long units = F < D ? F : D;   // the one-expert kernel's grid (same per-CTA rows)
+  const int grid = (int)(units < sms ? (units > 0 ? units : 1) : sms);
+  const int cap13 = (int)((F + grid - 1) / grid) * 2 + 2;
+  const int cap2 = (int)((D + grid - 1) / grid) + 2;
   for (int i = 0; i < n; ++i) {
     m.a13[i].evict_first = m.a2[i].evict_first = ef;
     m.a13[i].rows_cap = cap13;
