@@ -112,6 +112,14 @@ def main():
         out["expert_ffn_fp8"] = dict(us_median=med * 1e6, us_best=best * 1e6, GBps=nb / med / 1e9,
                                      frac_hbm=nb / med / 1e9 / pk["hbm_gbs"], bytes=nb)
         del blob, q, q4, q8
+    if args.only in ("read",):
+        # read-only ceiling: torch's reduction over the same byte counts (one and two experts)
+        for nb in (3 * F * d * 2, 6 * F * d * 2, 1 << 30):
+            t = torch.empty(nb // 2, dtype=bf, device=dev).normal_()
+            med, best = timeit(lambda: t.sum(dtype=torch.float32), args.iters, flush)
+            out[f"torch_sum_{nb >> 20}MiB"] = dict(us_median=med * 1e6, GBps=nb / med / 1e9,
+                                                   frac_hbm=nb / med / 1e9 / pk["hbm_gbs"], bytes=nb)
+            del t
     if args.only in ("", "lm"):
         W = torch.empty((V, d), dtype=bf, device=dev)
         odmoe.gen_weights(W, 6, rows=V, cols=d, fan_in=d, seed=2512)
