@@ -12,5 +12,6 @@ from .fixture import (  # noqa: F401
     GOLDEN, KIND_EMB, KIND_ROUTER, KIND_W1, KIND_W3, KIND_W2, KIND_LM_HEAD, KIND_PROMPT,
     ModelShape, TINY, MIXTRAL, splitmix64, stream_u24, uniform_pm1, tensor_id, weight_fp32,
     weight_bf16_bits, bf16_bits_to_f32, f32_to_bf16_bits, fan_in_scale, gen_model_weights,
-    gen_expert, gen_prompt, gen_hidden,
+    gen_expert, gen_prompt, gen_hidden, gen_attention, KIND_WQ, KIND_WK, KIND_WV, KIND_WO, TINY_ATTN,
+    MIXTRAL_ATTN,
 )

@@ -35,6 +35,10 @@ KIND_W2 = 5
 KIND_LM_HEAD = 6
 KIND_PROMPT = 7
 KIND_HIDDEN = 8  # random test hidden states (router / expert unit tests)
+KIND_WQ = 9      # attention projections (reading Q29): fan_in = d for all four
+KIND_WK = 10
+KIND_WV = 11
+KIND_WO = 12
 
 
 @dataclasses.dataclass(frozen=True)
@@ -45,12 +49,17 @@ class ModelShape:
     d: int
     F: int
     V: int
+    H: int = 0    # attention query heads (0 = no attention block, the round-1 hot path)
+    Hkv: int = 0  # key/value heads (GQA); head_dim = d / H
 
 
 # BASELINE.json configs[0] (V=1024 is SURVEY.md's proposal; BASELINE gives no vocab)
 TINY = ModelShape(L=4, E=8, k=2, d=256, F=512, V=1024)
 # Mixtral-8x7B shape (SURVEY.md §0 "Mixtral shape")
 MIXTRAL = ModelShape(L=32, E=8, k=2, d=4096, F=14336, V=32000)
+# with Mixtral's attention block (32 query heads, 8 KV heads, head_dim 128; reading Q29)
+TINY_ATTN = ModelShape(L=4, E=8, k=2, d=256, F=512, V=1024, H=4, Hkv=2)
+MIXTRAL_ATTN = ModelShape(L=32, E=8, k=2, d=4096, F=14336, V=32000, H=32, Hkv=8)
 
 
 def splitmix64(z):
@@ -174,9 +183,20 @@ def gen_expert(shape: ModelShape, seed: int, layer: int, expert: int, dtype: str
     return W1, W3, W2
 
 
+def gen_attention(shape: ModelShape, seed: int, layer: int, dtype: str = "bf16"):
+    """(Wq [H*hd, d], Wk [Hkv*hd, d], Wv [Hkv*hd, d], Wo [d, H*hd]) stored values, hd = d / H."""
+    d, hd = shape.d, shape.d // shape.H
+    Wq = _stored(seed, tensor_id(KIND_WQ, layer), shape.H * hd, d, d, dtype)
+    Wk = _stored(seed, tensor_id(KIND_WK, layer), shape.Hkv * hd, d, d, dtype)
+    Wv = _stored(seed, tensor_id(KIND_WV, layer), shape.Hkv * hd, d, d, dtype)
+    Wo = _stored(seed, tensor_id(KIND_WO, layer), d, shape.H * hd, d, dtype)
+    return Wq, Wk, Wv, Wo
+
+
 def gen_model_weights(shape: ModelShape, seed: int, dtype: str = "bf16", layers=None):
     """Dict of stored weights (float32 arrays): emb [V,d], router[l] [E,d],
-    experts[l][e] = (W1, W3, W2), lm_head [V,d]. gamma is 1 (reading Q7)."""
+    experts[l][e] = (W1, W3, W2), lm_head [V,d]; with shape.H > 0 also attn[l] = (Wq, Wk, Wv, Wo).
+    gamma is 1 (reading Q7)."""
     d = shape.d
     layers = range(shape.L) if layers is None else layers
     w = {
@@ -188,6 +208,9 @@ def gen_model_weights(shape: ModelShape, seed: int, dtype: str = "bf16", layers=
     for l in layers:
         w["router"][l] = _stored(seed, tensor_id(KIND_ROUTER, l), shape.E, d, d, dtype)
         w["experts"][l] = {e: gen_expert(shape, seed, l, e, dtype) for e in range(shape.E)}
+    if shape.H > 0:
+        w["attn"] = {l: gen_attention(shape, seed, l, dtype) for l in layers}
+        w["heads"] = (shape.H, shape.Hkv)
     return w
 
 

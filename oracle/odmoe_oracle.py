@@ -30,6 +30,11 @@ Parity pins (tests/test_oracle_pins.py, -m "not gpu"):
   round_e4m3 / quantize_fp8_rows
                       pinned: torch.float8_e4m3fn casts (library) on random data incl. ties and
                       subnormals; value table endpoints (448, 2^-9); row max -> +-448 exactly.
+  rope                pinned: position 0 = identity; norm preserved; relative-position identity
+                      <rope(q,m), rope(k,n)> = <rope(q,m+j), rope(k,n+j)>; hd = 2 rotation by pos rad.
+  attention_decode    pinned: one position -> v; equal keys -> mean of values; torch's
+                      scaled_dot_product_attention (library, GQA by repeat) on random data.
+  attn_block          pinned: W_o = 0 -> h unchanged; one position with selector W_v, W_o -> closed form.
   shadow_predict      pinned: same-precision shadow => recall exactly 1.0.
   plan_* / misprediction_reloads / max_load_budget
                       pinned: SPEC examples S:271-273.
@@ -50,7 +55,8 @@ __all__ = [
     "rms_norm", "router_logits", "top_k", "top_k_bruteforce", "mixture_weights", "silu",
     "expert_ffn", "moe_layer", "final_logits", "greedy_argmax", "decode_token", "decode_sequence",
     "quantize_int8_rows", "dequantize_int8_rows", "quantize_model_int8", "shadow_predict",
-    "round_bf16", "shadow_model_bf16", "NF4_CODEBOOK", "NF4_BLOCK", "nf4_codebook_from_quantiles",
+    "round_bf16", "shadow_model_bf16", "ROPE_THETA", "rope", "attention_decode", "attn_block", "new_cache",
+    "decode_token_attn", "NF4_CODEBOOK", "NF4_BLOCK", "nf4_codebook_from_quantiles",
     "quantize_nf4_blocks", "dequantize_nf4_blocks", "quantize_model_nf4", "e4m3_values", "round_e4m3",
     "quantize_fp8_rows", "dequantize_fp8_rows", "quantize_model_fp8",
     "near_tie", "plan_group_size", "plan_groups", "assign_layer", "assign_experts",
@@ -204,6 +210,86 @@ def decode_sequence(weights, first_token: int, n_tokens: int, k: int, eps: float
         toks.append(t_next)
         t = t_next
     return toks, routes
+
+
+# ---------------------------------------------------------------- attention block (Q29)
+# The paper's main node runs "attention layers ... and normalization networks" of
+# Mixtral-8x7B; it prints no formula. Reading Q29: Mixtral's block -- pre-RMSNorm (gamma = 1), GQA
+# with H query and Hkv key/value heads of head_dim = d/H, rotary embedding (rotate-half form,
+# theta = 1e6), causal softmax(q k^T / sqrt(head_dim)) v, output projection, residual add.
+ROPE_THETA = 1.0e6
+
+
+def rope(x, pos: int, theta: float = ROPE_THETA):
+    """Rotary embedding of x [..., hd] at position pos: with half = hd/2, f_i = theta^(-2i/hd),
+    a_i = pos * f_i: (x1, x2) -> (x1 cos a - x2 sin a, x2 cos a + x1 sin a) on the two halves."""
+    x = np.asarray(x, dtype=np.float64)
+    hd = x.shape[-1]
+    half = hd // 2
+    ang = pos * theta ** (-np.arange(half, dtype=np.float64) * 2.0 / hd)
+    c, s = np.cos(ang), np.sin(ang)
+    x1, x2 = x[..., :half], x[..., half:]
+    return np.concatenate([x1 * c - x2 * s, x2 * c + x1 * s], axis=-1)
+
+
+def attention_decode(q, K, V):
+    """One query position against T cached positions (GQA): q [H, hd], K, V [T, Hkv, hd].
+    Query head i reads key/value head i // (H / Hkv). o_i = softmax(K_g q_i / sqrt(hd)) V_g."""
+    q = np.asarray(q, dtype=np.float64)
+    K = np.asarray(K, dtype=np.float64)
+    V = np.asarray(V, dtype=np.float64)
+    H, hd = q.shape
+    rep = H // K.shape[1]
+    o = np.zeros((H, hd))
+    for i in range(H):
+        g = i // rep
+        s = K[:, g, :] @ q[i] / math.sqrt(hd)
+        p = np.exp(s - np.max(s))
+        p /= np.sum(p)
+        o[i] = p @ V[:, g, :]
+    return o
+
+
+def attn_block(h, attn_w, heads, cache_l, pos: int, eps: float = 1e-5):
+    """h + W_o attention(RMSNorm(h)) at position pos; appends this position's k, v (after RoPE for
+    k) to cache_l = {"K": [...], "V": [...]} (positions 0..pos-1 already there). Returns
+    (h_out, dict with x, q, k, v, o)."""
+    Wq, Wk, Wv, Wo = attn_w
+    H, Hkv = heads
+    d = Wq.shape[1]
+    hd = d // H
+    h = np.asarray(h, dtype=np.float64)
+    x = rms_norm(h, eps=eps)
+    q = rope((np.asarray(Wq, dtype=np.float64) @ x).reshape(H, hd), pos)
+    k = rope((np.asarray(Wk, dtype=np.float64) @ x).reshape(Hkv, hd), pos)
+    v = (np.asarray(Wv, dtype=np.float64) @ x).reshape(Hkv, hd)
+    assert len(cache_l["K"]) == pos
+    cache_l["K"].append(k)
+    cache_l["V"].append(v)
+    o = attention_decode(q, np.stack(cache_l["K"]), np.stack(cache_l["V"]))
+    return h + np.asarray(Wo, dtype=np.float64) @ o.reshape(-1), {"x": x, "q": q, "k": k, "v": v, "o": o}
+
+
+def new_cache(L):
+    return {l: {"K": [], "V": []} for l in L}
+
+
+def decode_token_attn(weights, token: int, pos: int, cache, k: int, eps: float = 1e-5):
+    """One decode iteration with the attention block (Q29): h0 = Emb[t]; for l: h = attn_block(h),
+    h = moe_layer(h); t' = argmax(LM head). `cache` (new_cache) gains position pos."""
+    L = sorted(weights["router"].keys())
+    h = np.asarray(weights["emb"][token], dtype=np.float64)
+    recs = []
+    for l in L:
+        h_att, arec = attn_block(h, weights["attn"][l], weights["heads"], cache[l], pos, eps)
+        out = moe_layer(h_att, weights["router"][l], weights["experts"][l], k, eps)
+        out["h_in"] = h
+        out["h_att"] = h_att
+        out["attn"] = arec
+        recs.append(out)
+        h = out["h_next"]
+    z = final_logits(weights["lm_head"], h, eps)
+    return greedy_argmax(z), recs, z
 
 
 # ---------------------------------------------------------------- O8 shadow / SEP (P:43, P:84-86, P:143-147)

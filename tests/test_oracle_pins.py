@@ -331,6 +331,62 @@ def test_fp8_row_quantizer_properties():
         assert np.all(np.abs(deq[r] - W[r]) <= np.abs(W[r]) * 2.0 ** -4 + s[r] * 2.0 ** -10)
 
 
+# ------------------------------------------------------------------ attention block (Q29)
+def test_rope_closed_forms():
+    rng = np.random.default_rng(30)
+    x = rng.standard_normal((3, 64))
+    assert np.allclose(O.rope(x, 0), x, rtol=0, atol=0)
+    assert np.allclose(np.linalg.norm(O.rope(x, 17), axis=-1), np.linalg.norm(x, axis=-1), rtol=1e-12)
+    q, k = rng.standard_normal(64), rng.standard_normal(64)
+    a = O.rope(q, 9) @ O.rope(k, 4)
+    b = O.rope(q, 9 + 123) @ O.rope(k, 4 + 123)
+    assert abs(a - b) < 1e-9 * max(1.0, abs(a))
+    # hd = 2: a plane rotation by pos radians (frequency theta^0 = 1)
+    r = O.rope(np.array([1.0, 0.0]), 3)
+    assert np.allclose(r, [math.cos(3), math.sin(3)], rtol=0, atol=1e-15)
+
+
+def test_attention_decode_special_cases_and_library():
+    import torch
+    rng = np.random.default_rng(31)
+    H, Hkv, hd, T = 8, 2, 16, 11
+    q = rng.standard_normal((H, hd))
+    K, V = rng.standard_normal((T, Hkv, hd)), rng.standard_normal((T, Hkv, hd))
+    o1 = O.attention_decode(q, K[:1], V[:1])                     # one position -> its value
+    assert np.allclose(o1, np.repeat(V[0], H // Hkv, axis=0), rtol=0, atol=1e-15)
+    Ke = np.repeat(K[:1], T, axis=0)                               # equal keys -> mean of values
+    assert np.allclose(O.attention_decode(q, Ke, V), np.repeat(V.mean(axis=0), H // Hkv, axis=0), atol=1e-12)
+    o = O.attention_decode(q, K, V)
+    tq = torch.from_numpy(q)[None, :, None, :]                    # [1, H, 1, hd]
+    tk = torch.from_numpy(K).permute(1, 0, 2).repeat_interleave(H // Hkv, dim=0)[None]
+    tv = torch.from_numpy(V).permute(1, 0, 2).repeat_interleave(H // Hkv, dim=0)[None]
+    ref = torch.nn.functional.scaled_dot_product_attention(tq, tk, tv)[0, :, 0, :].numpy()
+    assert np.allclose(o, ref, rtol=1e-10, atol=1e-12)
+
+
+def test_attn_block_closed_forms():
+    rng = np.random.default_rng(32)
+    d, H, Hkv = 16, 4, 2
+    hd = d // H
+    Wq, Wk = rng.standard_normal((d, d)), rng.standard_normal((Hkv * hd, d))
+    Wv = rng.standard_normal((Hkv * hd, d))
+    h = rng.standard_normal(d)
+    cache = O.new_cache([0])
+    out, _ = O.attn_block(h, (Wq, Wk, Wv, np.zeros((d, d))), (H, Hkv), cache[0], 0)
+    assert np.array_equal(out, h)                                  # W_o = 0: residual only
+    # one position: attention returns v of the query head's group; W_v selects coordinates
+    sel = np.zeros((Hkv * hd, d))
+    for i in range(Hkv * hd):
+        sel[i, i] = 1.0
+    Wo = np.zeros((d, d))
+    Wo[0, 0] = 2.0                                                 # out_0 = 2 * o[head 0][0]
+    cache = O.new_cache([0])
+    out, rec = O.attn_block(h, (Wq, Wk, sel, Wo), (H, Hkv), cache[0], 0)
+    x = O.rms_norm(h)
+    assert np.allclose(out[0], h[0] + 2.0 * x[0], rtol=1e-12) and np.allclose(out[1:], h[1:])
+    assert len(cache[0]["K"]) == 1
+
+
 def test_same_precision_shadow_recall_is_one(tiny_fp32):
     """a full-precision shadow with token alignment predicts exactly."""
     toks, routes = O.decode_sequence(tiny_fp32, 11, 6, TINY.k)
