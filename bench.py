@@ -52,6 +52,10 @@ def parse():
     ap.add_argument("--first-token", type=int, default=-1)
     ap.add_argument("--prefill", type=int, default=512,
                     help="prompt tokens prefilled (configs[4]: TTFT + grouped GEMM) before the decode warm-up; 0 = skip")
+    ap.add_argument("--attention", action="store_true",
+                    help="with Mixtral's attention block (32 q / 8 kv heads, RoPE; SURVEY §8(f)4, reading Q29)")
+    ap.add_argument("--context", type=int, default=512,
+                    help="--attention: decode starts at this KV-cache position (rows before it zero: synthetic context)")
     ap.add_argument("--out", default="")
     return ap.parse_args()
 
@@ -244,6 +248,10 @@ def run_reference(args):
     return 0
 
 
+def attn_kw(args):
+    return dict(n_heads=32, n_kv_heads=8, max_seq=args.context + args.warmup + args.steps + 8) if args.attention else {}
+
+
 def sliced(args, n):
     return args.placement == "sliced" and n > 1
 
@@ -272,7 +280,9 @@ def workload_config(args, n):
             "predictor": args.predictor, "slots_per_gpu": n_slots(args, n), "refine_depth": args.refine,
             "expert_bytes_per_gpu": n_slots(args, n) * per_slot,
             "lookahead": lookahead(args, n), "weight_seed": SEED,
-            "attention": "none on the hot path (reading Q22)",
+            "attention": (f"Mixtral GQA 32q/8kv, head_dim 128, RoPE 1e6, bf16 KV cache; decode from position "
+                          f"{args.context} (earlier cache rows zero: synthetic context)" if args.attention
+                          else "none on the hot path (reading Q22)"),
             "l2": "inputs larger than L2: every step streams 64 distinct 352 MB experts"}
 
 
@@ -316,7 +326,9 @@ def main():
     refine = args.refine if args.predictor.startswith("shadow") else 0
     eng = odmoe.Engine(device=local, rank=rank, world_size=world, nccl_id=uid, predictor=pred,
                        slots_per_gpu=n_slots(args, n), lookahead=D, time_kernels=1, weight_seed=SEED,
-                       refine_depth=refine, placement=int(sliced(args, n)), **SHAPE)
+                       refine_depth=refine, placement=int(sliced(args, n)), **SHAPE, **attn_kw(args))
+    if args.attention:
+        eng.set_position(args.context)
     t_create = time.time() - t_create
     def barrier():
         if dist is not None:
@@ -327,7 +339,7 @@ def main():
 
     tok = args.first_token if args.first_token >= 0 else 1
     prefill = None
-    if args.prefill > 0:
+    if args.prefill > 0 and not args.attention:
         log(rank, f"prefill {args.prefill}")
         from inputs import MIXTRAL, gen_prompt
         prompt = [int(x) for x in gen_prompt(MIXTRAL, 1, args.prefill)]
@@ -436,7 +448,8 @@ def main():
                        "loads_cancelled": st["loads_cancelled"], "max_resident": st["max_resident"],
                        "ms_router": st["ms_router"] / max(1, st["n_router"]) * 1e3,
                        "us_shadow_per_step": st["ms_shadow"] / args.steps * 1e3,
-                       "us_lm_head": st["ms_lm_head"] / max(1, st["n_lm_head"]) * 1e3},
+                       "us_lm_head": st["ms_lm_head"] / max(1, st["n_lm_head"]) * 1e3,
+                       "us_attention_per_step": st["ms_attn"] / args.steps * 1e3},
         }
         # Eq. 1 (reading Q12): t_maxload = N_G t^M + (N_G - 1) t^W; the method is I/O-bound
         # when one expert's load takes longer ("compare it with t^maxload")
@@ -491,7 +504,9 @@ def resident_baseline(odmoe, torch, args, dev, rank, world, dist):
         uid = obj[0]
     eng = odmoe.Engine(device=dev, rank=rank, world_size=world, nccl_id=uid, predictor=odmoe.PRED_NONE,
                        slots_per_gpu=-1, time_kernels=1, weight_seed=SEED, placement=int(sliced(args, world)),
-                       **SHAPE)
+                       **SHAPE, **attn_kw(args))
+    if args.attention:
+        eng.set_position(args.context)
     tok = 1
     for _ in range(args.warmup):
         tok, _ = eng.decode_step(tok, records=False)

@@ -104,7 +104,11 @@ typedef struct {
                                 layer l the shadow re-runs layers l..l+R-1 from the main model's exact
                                 state and corrects the loads of layers l+1..l+R; 0 = off (paper's Mode A) */
   int32_t placement;         /* odmoe_placement: 0 = the paper's worker groups, 1 = sliced      */
-  int32_t reserved[5];
+  int32_t n_heads;           /* attention block (reading Q29): query heads H, 0 = no
+                                attention (the MoE-only hot path); head_dim = d / H in {32, 64, 128}     */
+  int32_t n_kv_heads;        /* key/value heads (GQA), H % Hkv == 0, H / Hkv <= 8                       */
+  int32_t max_seq;           /* KV-cache capacity in tokens (0 => 4096 when n_heads > 0)                */
+  int32_t reserved[2];
   const void* nccl_id;       /* 128-byte ncclUniqueId from rank 0 (NULL when world_size == 1)          */
 } odmoe_config;
 
@@ -139,6 +143,8 @@ typedef struct {
   int64_t correct, predicted_total; /* Σc and Σ k over layers with a prediction (rank 0)              */
   int64_t refine_corrections;        /* layer predictions changed by the SEP refinement                */
   int64_t refine_correct, refine_total; /* Σc, Σk of the refined predictions (rank 0)                  */
+  double ms_attn;                    /* attention block kernels (QKV, RoPE, attention, W_o), rank 0     */
+  int64_t n_attn;
 } odmoe_stats;
 
 /* ------------------------------------------------------------------ lifecycle */
@@ -296,7 +302,8 @@ odmoe_status odmoe_evict(void* ctx, int layer, int expert);
 /* Runtime options (take effect at the next decode step; every rank must set the same value):
  *   key 1 = lookahead D (>= 1, Q11); key 2 = predictor (odmoe_predictor; the shadow predictors
  *   need a ctx created with a shadow predictor: E_STATE otherwise); key 3 = refine_depth R (0..4;
- *   only with a shadow predictor). E_CONFIG on a bad key/value. */
+ *   only with a shadow predictor); key 4 = KV-cache position of the next decode step (attention
+ *   ctx only; 0 starts a new sequence; E_RANGE outside [0, max_seq)). E_CONFIG on a bad key/value. */
 odmoe_status odmoe_set_option(void* ctx, int key, int64_t value);
 
 /* SEP Mode A (Q10): run the shadow from the main model's token `token`

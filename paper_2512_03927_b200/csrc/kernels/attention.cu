@@ -1,0 +1,151 @@
+// Attention block of the main node (reading Q29: Mixtral's GQA with rotary
+// embedding). The projections run on the flat GEMV (decode) / tcgen05 grouped GEMM (prefill);
+// this file holds what sits between them:
+//   rope_kv   : rotate q and k of the current position(s) (rotate-half form, theta = 1e6), store k, v
+//               (bf16) into the KV cache rows (or a caller buffer), q stays fp32;
+//   attn_split: flash-decoding over the cached positions: CTA = (kv head g, position split s), one
+//               warp per query head of the group; per split a running max, sum and un-normalised
+//               output; scores q.k / sqrt(hd) in fp32 with k, v read as bf16;
+//   attn_merge: merges the splits with their log-sum-exp weights into o (fp32 or bf16).
+// Decode reads at most pos+1 rows per KV head: the work is tiny next to the weight GEMVs and is
+// latency-bound; splits of 128 positions spread it over Hkv * ceil((pos+1)/128) CTAs.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace odmoe {
+
+constexpr int kAttnSplit = 128;  // positions per split
+constexpr int kMaxHd = 128;
+
+__device__ __forceinline__ float bf16_to_f(uint16_t b) { return __uint_as_float((uint32_t)b << 16); }
+
+// grid = (T tokens, H + Hkv heads), block = hd/2 threads: one rotation pair per thread.
+__global__ void rope_kv_kernel(float* __restrict__ qkv, int qkv_stride, int H, int Hkv, int hd, int pos0,
+                               uint16_t* __restrict__ kc, uint16_t* __restrict__ vc, int kv_stride,
+                               float log2_theta) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int t = blockIdx.x, head = blockIdx.y, i = threadIdx.x, half = hd / 2;
+  const int pos = pos0 + t;
+  float* row = qkv + (size_t)t * qkv_stride;
+  // angle = pos * theta^(-2i/hd), in fp64 so the rotation is exact to fp32 output precision
+  const double ang = (double)pos * exp2(-(double)log2_theta * (2.0 * i) / hd);
+  double sd, cd;
+  sincos(ang, &sd, &cd);
+  const float c = (float)cd, s = (float)sd;
+  if (head < H) {
+    float* q = row + head * hd;
+    const float x1 = q[i], x2 = q[i + half];
+    __syncthreads();
+    q[i] = x1 * c - x2 * s;
+    q[i + half] = x2 * c + x1 * s;
+  } else {
+    const int g = head - H;
+    const float* k = row + H * hd + g * hd;
+    const float* v = row + (H + Hkv) * hd + g * hd;
+    const float x1 = k[i], x2 = k[i + half];
+    uint16_t* kd = kc + (size_t)t * kv_stride + g * hd;
+    uint16_t* vd = vc + (size_t)t * kv_stride + g * hd;
+    const __nv_bfloat16 r1 = __float2bfloat16_rn(x1 * c - x2 * s), r2 = __float2bfloat16_rn(x2 * c + x1 * s);
+    kd[i] = *reinterpret_cast<const uint16_t*>(&r1);
+    kd[i + half] = *reinterpret_cast<const uint16_t*>(&r2);
+    const __nv_bfloat16 v1 = __float2bfloat16_rn(v[i]), v2 = __float2bfloat16_rn(v[i + half]);
+    vd[i] = *reinterpret_cast<const uint16_t*>(&v1);
+    vd[i + half] = *reinterpret_cast<const uint16_t*>(&v2);
+  }
+}
+
+cudaError_t launch_rope_kv(float* qkv, int qkv_stride, int T, int H, int Hkv, int hd, int pos0, void* kc, void* vc,
+                           int kv_stride, cudaStream_t s) {
+  if (hd % 2 || hd > kMaxHd || T < 1) return cudaErrorInvalidValue;
+  rope_kv_kernel<<<dim3(T, H + Hkv), hd / 2, 0, s>>>(qkv, qkv_stride, H, Hkv, hd, pos0, (uint16_t*)kc, (uint16_t*)vc,
+                                                     kv_stride, (float)19.931568569324174);  // log2(1e6)
+  return cudaGetLastError();
+}
+
+// Partials: part[((t * H + head) * nsplit + s) * (hd + 2)] = {o[0..hd), m, l}.
+// Query t (of T) sits at position pos0 + t and attends to positions [0, pos0 + t] (causal).
+// K rows for positions < pos0 come from kc_past (the cache); rows >= pos0 from kc_cur
+// (the rows written by rope_kv for these queries: the cache itself for the main model, a private
+// buffer for the shadow, which reads the main model's cache for the past: KV alignment).
+__global__ void __launch_bounds__(32 * 8) attn_split_kernel(const float* __restrict__ q, int q_stride, int H, int Hkv,
+                                                           int hd, int pos0, const uint16_t* __restrict__ kc_past,
+                                                           const uint16_t* __restrict__ vc_past,
+                                                           const uint16_t* __restrict__ kc_cur,
+                                                           const uint16_t* __restrict__ vc_cur, int kv_stride,
+                                                           int nsplit, float* __restrict__ part) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int t = blockIdx.z, g = blockIdx.x, sp = blockIdx.y;
+  const int rep = H / Hkv;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp >= rep) return;
+  const int head = g * rep + warp;
+  const int pos = pos0 + t;
+  const int p_begin = sp * kAttnSplit;
+  const int p_end = min(pos + 1, p_begin + kAttnSplit);
+  float* out = part + ((size_t)(t * H + head) * nsplit + sp) * (hd + 2);
+  const int per = hd / 32;  // elements per lane (hd = 32, 64 or 128)
+  float qv[4];
+  const float* qh = q + (size_t)t * q_stride + head * hd;
+  const float scale = rsqrtf((float)hd);
+  for (int j = 0; j < per; ++j) qv[j] = qh[lane * per + j] * scale;
+  float m = -INFINITY, l = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int p = p_begin; p < p_end; ++p) {
+    const uint16_t* kr = p < pos0 ? kc_past + (size_t)p * kv_stride : kc_cur + (size_t)(p - pos0) * kv_stride;
+    const uint16_t* vr = p < pos0 ? vc_past + (size_t)p * kv_stride : vc_cur + (size_t)(p - pos0) * kv_stride;
+    kr += g * hd + lane * per;
+    vr += g * hd + lane * per;
+    float sdot = 0.f;
+    for (int j = 0; j < per; ++j) sdot = fmaf(qv[j], bf16_to_f(kr[j]), sdot);
+    sdot = warp_sum(sdot);
+    const float mn = fmaxf(m, sdot);
+    const float corr = __expf(m - mn), w = __expf(sdot - mn);
+    l = l * corr + w;
+    for (int j = 0; j < per; ++j) acc[j] = fmaf(w, bf16_to_f(vr[j]), acc[j] * corr);
+    m = mn;
+  }
+  for (int j = 0; j < per; ++j) out[lane * per + j] = acc[j];
+  if (lane == 0) {
+    out[hd] = m;
+    out[hd + 1] = l;
+  }
+}
+
+// o[t][head*hd + i] = sum_s e^{m_s - M} acc_s[i] / sum_s e^{m_s - M} l_s; grid (T, H), block hd.
+__global__ void attn_merge_kernel(const float* __restrict__ part, int H, int hd, int nsplit, int pos0,
+                                  float* __restrict__ o_f32, uint16_t* __restrict__ o_bf16, int o_stride) {
+  const int t = blockIdx.x, head = blockIdx.y, i = threadIdx.x;
+  const int used = (pos0 + t) / kAttnSplit + 1;  // splits that saw at least one position
+  const float* p0 = part + (size_t)(t * H + head) * nsplit * (hd + 2);
+  float M = -INFINITY;
+  for (int s = 0; s < used; ++s) M = fmaxf(M, p0[s * (hd + 2) + hd]);
+  float num = 0.f, den = 0.f;
+  for (int s = 0; s < used; ++s) {
+    const float w = __expf(p0[s * (hd + 2) + hd] - M);
+    num = fmaf(w, p0[s * (hd + 2) + i], num);
+    den = fmaf(w, p0[s * (hd + 2) + hd + 1], den);
+  }
+  const float v = num / den;
+  if (o_f32) o_f32[(size_t)t * o_stride + head * hd + i] = v;
+  if (o_bf16) {
+    const __nv_bfloat16 b = __float2bfloat16_rn(v);
+    o_bf16[(size_t)t * o_stride + head * hd + i] = *reinterpret_cast<const uint16_t*>(&b);
+  }
+}
+
+int attn_splits(int max_pos) { return max_pos / kAttnSplit + 1; }
+
+cudaError_t launch_attention(const float* q, int q_stride, int T, int H, int Hkv, int hd, int pos0, const void* kc_past,
+                             const void* vc_past, const void* kc_cur, const void* vc_cur, int kv_stride, float* part,
+                             float* o_f32, void* o_bf16, int o_stride, cudaStream_t s) {
+  if (hd % 32 || hd > kMaxHd || H % Hkv || H / Hkv > 8 || T < 1) return cudaErrorInvalidValue;
+  const int nsplit = attn_splits(pos0 + T - 1);
+  attn_split_kernel<<<dim3(Hkv, nsplit, T), 32 * (H / Hkv), 0, s>>>(
+      q, q_stride, H, Hkv, hd, pos0, (const uint16_t*)kc_past, (const uint16_t*)vc_past, (const uint16_t*)kc_cur,
+      (const uint16_t*)vc_cur, kv_stride, nsplit, part);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  attn_merge_kernel<<<dim3(T, H), hd, 0, s>>>(part, H, hd, nsplit, pos0, o_f32, (uint16_t*)o_bf16, o_stride);
+  return cudaGetLastError();
+}
+
+}  // namespace odmoe

@@ -298,6 +298,7 @@ struct FlatArgs {
   int rows_cap;
   int d_full, F_full;
   int evict_first;       // L2 policy of the weight stream
+  int accumulate;        // MODE 1/3: out[r] += result instead of out[r] = result
 };
 
 struct PdlWait {
@@ -408,7 +409,7 @@ __device__ __forceinline__ void flat_phase(const FlatArgs& a, uint8_t* sm, const
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   // stage activations (MODE 2: RMSNorm of h first) and zero the partials
-  if (MODE == 2) {
+  if (MODE == 2 || MODE == 3) {
     float ss = 0.f;
     for (int j = tid; j < a.C; j += kFG_THREADS) { const float v = a.h[j]; ss = fmaf(v, v, ss); }
     ss = warp_sum(ss);
@@ -574,14 +575,14 @@ __device__ __forceinline__ void flat_phase(const FlatArgs& a, uint8_t* sm, const
       if (!kNF4 && sc != nullptr) { g *= sc[rb + 2 * p]; v *= sc[rb + 2 * p + 1]; }
       a.out[rb / 2 + p] = silu_mul(g, v);
     }
-  } else if (MODE == 1) {
+  } else if (MODE == 1 || MODE == 3) {
     const float gw = a.gate_w ? a.gate_w[gate_idx] : 1.f;
     for (int r = tid; r < nrows; r += kFG_THREADS) {
       float s = 0.f;
 #pragma unroll
       for (int w = 0; w < kFG_WARPS; ++w) s += part[w * a.rows_cap + r];
       if (!kNF4 && sc != nullptr) s *= sc[rb + r];
-      a.out[rb + r] = gw * s;
+      a.out[rb + r] = a.accumulate ? a.out[rb + r] + gw * s : gw * s;
     }
   } else {
     unsigned long long best = 0ull;
@@ -739,6 +740,105 @@ cudaError_t launch_w2_flat(ExpertRef ex, WType wt, const float* act, const float
   return cudaErrorInvalidValue;
 }
 
+// Rows shorter than one flat group (small test shapes): one warp per row. NORM: x = RMSNorm(h)
+// (rounded to bf16 unless the weights are fp32), else x = fp32 input; out = or += (row-scaled).
+template <typename WT, bool NORM>
+__global__ void __launch_bounds__(256) gemv_rows_small_kernel(const float* __restrict__ xin, const WT* __restrict__ W,
+                                                              const float* __restrict__ sc, int R, int C, float eps,
+                                                              float* out, int accumulate) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  extern __shared__ float xs_small[];
+  __shared__ float red[9];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  float rstd = 1.f;
+  if (NORM) {
+    float ss = 0.f;
+    for (int j = tid; j < C; j += blockDim.x) ss = fmaf(xin[j], xin[j], ss);
+    ss = warp_sum(ss);
+    if (lane == 0) red[warp] = ss;
+    __syncthreads();
+    if (tid == 0) {
+      float t = 0.f;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+      red[8] = t;
+    }
+    __syncthreads();
+    rstd = 1.0f / sqrtf(red[8] / (float)C + eps);
+  }
+  for (int j = tid; j < C; j += blockDim.x) {
+    float v = xin[j] * rstd;
+    if (NORM && !std::is_same<WT, float>::value) v = __bfloat162float(__float2bfloat16_rn(v));
+    xs_small[j] = v;
+  }
+  __syncthreads();
+  const int r = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (r >= R) return;
+  float acc = 0.f;
+  for (int j = lane; j < C; j += 32) {
+    float w;
+    if constexpr (std::is_same<WT, __nv_bfloat16>::value) w = __bfloat162float(W[(size_t)r * C + j]);
+    else w = (float)W[(size_t)r * C + j];
+    acc = fmaf(w, xs_small[j], acc);
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) {
+    if (sc) acc *= sc[r];
+    out[r] = accumulate ? out[r] + acc : acc;
+  }
+}
+
+template <typename WT, bool NORM>
+static cudaError_t small_rows(const float* x, const void* W, const float* sc, int R, int C, float eps, float* out,
+                              int acc, cudaStream_t s) {
+  gemv_rows_small_kernel<WT, NORM><<<(R + 7) / 8, 256, (size_t)C * 4, s>>>(x, (const WT*)W, sc, R, C, eps, out, acc);
+  return cudaGetLastError();
+}
+
+// Attention projections (reading Q29). QKV: out = W RMSNorm(h) (activations rounded to bf16 for
+// bf16 / int8 weights, as for u), R rows of C = d columns. O: h += W o with o fp32.
+cudaError_t launch_gemv_rmsnorm(const float* h, const void* W, const float* scales, WType wt, int R, int C, float eps,
+                                float* out, cudaStream_t s, bool pdl) {
+  const bool flat = wt == W_BF16 ? flat_row_ok<__nv_bfloat16>(C) : (wt == W_F32 ? flat_row_ok<float>(C) : flat_row_ok<int8_t>(C));
+  if (!flat) {
+    switch (wt) {
+      case W_BF16: return small_rows<__nv_bfloat16, true>(h, W, scales, R, C, eps, out, 0, s);
+      case W_F32: return small_rows<float, true>(h, W, scales, R, C, eps, out, 0, s);
+      case W_I8: return small_rows<int8_t, true>(h, W, scales, R, C, eps, out, 0, s);
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  FlatArgs a{};
+  a.ex = direct_ref(W, scales, 0); a.second = 0; a.R = R; a.C = C; a.out = out; a.h = h; a.eps = eps;
+  switch (wt) {
+    case W_BF16: return fg_launch<__nv_bfloat16, uint16_t, 3>(a, s, pdl);
+    case W_F32: return fg_launch<float, float, 3>(a, s, pdl);
+    case W_I8: return fg_launch<int8_t, uint16_t, 3>(a, s, pdl);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_gemv_acc(const void* W, const float* scales, WType wt, int R, int C, const float* x, float* out,
+                            cudaStream_t s, bool pdl) {
+  const bool flat = wt == W_BF16 ? flat_row_ok<__nv_bfloat16>(C) : (wt == W_F32 ? flat_row_ok<float>(C) : flat_row_ok<int8_t>(C));
+  if (!flat) {
+    switch (wt) {
+      case W_BF16: return small_rows<__nv_bfloat16, false>(x, W, scales, R, C, 0.f, out, 1, s);
+      case W_F32: return small_rows<float, false>(x, W, scales, R, C, 0.f, out, 1, s);
+      case W_I8: return small_rows<int8_t, false>(x, W, scales, R, C, 0.f, out, 1, s);
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  FlatArgs a{};
+  a.ex = direct_ref(W, scales, 0); a.second = 0; a.x = x; a.x_bf16 = 0; a.R = R; a.C = C; a.out = out;
+  a.accumulate = 1;
+  switch (wt) {
+    case W_BF16: return fg_launch<__nv_bfloat16, float, 1>(a, s, pdl);
+    case W_F32: return fg_launch<float, float, 1>(a, s, pdl);
+    case W_I8: return fg_launch<int8_t, float, 1>(a, s, pdl);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 cudaError_t launch_lm_head_flat(const float* h, const void* W, WType wt, int V, int d, float eps,
                                 int32_t* token_out, float* logits, void* scratch, cudaStream_t s, bool pdl) {
   FlatArgs a{};
@@ -768,23 +868,27 @@ struct NoWait {
   __device__ __forceinline__ void operator()() const {}
 };
 
-template <typename WT, typename XT, int UNROLL>
+// NE (experts) is a template parameter: every m.a13[e] / m.a2[e] is then a compile-time index into
+// the parameter space (a runtime index made the compiler copy the argument structs to local memory).
+template <typename WT, typename XT, int UNROLL, int NE>
 __global__ void __launch_bounds__(kFG_THREADS, 1)
 flat_experts_kernel(const __grid_constant__ MultiArgs m, unsigned int* counter, unsigned int target) {
   extern __shared__ __align__(128) uint8_t sm[];
-  const int n = m.n;
   long long p0, p1, r0, r1;
   split_range(m.a13[0].R / 2, gridDim.x, blockIdx.x, p0, p1);  // gate/up pairs of each expert
   split_range(m.a2[0].R, gridDim.x, blockIdx.x, r0, r1);       // W2 rows of each expert
-  for (int e = 0; e < n; ++e) {
-    if (e == 0) flat_phase<WT, XT, 0, UNROLL>(m.a13[e], sm, PdlWait{}, false, 2 * p0, 2 * p1);
-    else flat_phase<WT, XT, 0, UNROLL>(m.a13[e], sm, NoWait{}, true, 2 * p0, 2 * p1);
+  flat_phase<WT, XT, 0, UNROLL>(m.a13[0], sm, PdlWait{}, false, 2 * p0, 2 * p1);
+#pragma unroll
+  for (int e = 1; e < NE; ++e) {
     __syncthreads();
+    flat_phase<WT, XT, 0, UNROLL>(m.a13[e], sm, NoWait{}, true, 2 * p0, 2 * p1);
   }
-  for (int e = 0; e < n; ++e) {
-    if (e == 0) flat_phase<WT, float, 1, UNROLL>(m.a2[e], sm, GridBarrier{counter, target}, true, r0, r1);
-    else flat_phase<WT, float, 1, UNROLL>(m.a2[e], sm, NoWait{}, true, r0, r1);
+  __syncthreads();
+  flat_phase<WT, float, 1, UNROLL>(m.a2[0], sm, GridBarrier{counter, target}, true, r0, r1);
+#pragma unroll
+  for (int e = 1; e < NE; ++e) {
     __syncthreads();
+    flat_phase<WT, float, 1, UNROLL>(m.a2[e], sm, NoWait{}, true, r0, r1);
   }
 }
 
@@ -828,7 +932,10 @@ static cudaError_t multi_launch(MultiArgs m, cudaStream_t s, bool pdl) {
   const size_t s2 = (size_t)kFG_WARPS * cap2 * sizeof(float) + (size_t)m.a2[0].C * sizeof(float) + 16 + lut;
   const size_t smem = s1 > s2 ? s1 : s2;
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  auto kern = flat_experts_kernel<WT, XT, UNROLL>;
+  void (*kern)(const MultiArgs, unsigned int*, unsigned int) =
+      n == 1 ? flat_experts_kernel<WT, XT, UNROLL, 1>
+             : (n == 2 ? flat_experts_kernel<WT, XT, UNROLL, 2>
+                       : (n == 3 ? flat_experts_kernel<WT, XT, UNROLL, 3> : flat_experts_kernel<WT, XT, UNROLL, 4>));
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const unsigned int target = g_epochs[dev] + (unsigned int)grid;

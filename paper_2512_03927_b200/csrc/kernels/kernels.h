@@ -132,6 +132,25 @@ cudaError_t launch_embed_rows(const void* emb, WType wt, const int32_t* tokens, 
 cudaError_t launch_gen(void* out, int kind, int layer, int expert, int64_t rows, int64_t cols,
                        int64_t fan_in, int d, int F, uint64_t seed, WType wt, cudaStream_t s);
 
+// ---- attention block (reading Q29; attention.cu + flat_gemv.cu)
+// out[R] = W RMSNorm(h) (flat GEMV, RMSNorm fused in the prologue); needs (C * elem) % 512 == 0
+cudaError_t launch_gemv_rmsnorm(const float* h, const void* W, const float* scales, WType wt, int R, int C, float eps,
+                                float* out, cudaStream_t s, bool pdl);
+// out[R] += W x (x fp32 [C])
+cudaError_t launch_gemv_acc(const void* W, const float* scales, WType wt, int R, int C, const float* x, float* out,
+                            cudaStream_t s, bool pdl);
+// rotate q, k of T positions pos0.. in qkv rows ([q H*hd | k Hkv*hd | v Hkv*hd], fp32, stride
+// qkv_stride); k (rotated) and v stored as bf16 rows of kv_stride elements at kc / vc (row t)
+cudaError_t launch_rope_kv(float* qkv, int qkv_stride, int T, int H, int Hkv, int hd, int pos0, void* kc, void* vc,
+                           int kv_stride, cudaStream_t s);
+// causal GQA attention of T queries at positions pos0..: keys/values < pos0 from *_past (rows by
+// position), >= pos0 from *_cur (row t = position pos0 + t); part: attn_part_floats(...) fp32;
+// o [T][H*hd] as fp32 and/or bf16 (either may be NULL)
+int attn_splits(int max_pos);
+cudaError_t launch_attention(const float* q, int q_stride, int T, int H, int Hkv, int hd, int pos0, const void* kc_past,
+                             const void* vc_past, const void* kc_cur, const void* vc_cur, int kv_stride, float* part,
+                             float* o_f32, void* o_bf16, int o_stride, cudaStream_t s);
+
 // P2P combine over NVLink (p2p.cu): sender sums its n partials into its row of GPU 0's buffer and
 // releases `epoch` in its flag; GPU 0 waits for the flags in `mask` and sums the rows in rank order.
 cudaError_t launch_p2p_send(const float* const* y, int n, int d, float* dst, uint32_t* flag, uint32_t epoch,

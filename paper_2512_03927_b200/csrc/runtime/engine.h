@@ -15,7 +15,7 @@
 
 namespace odmoe {
 
-enum Family { K_ROUTER = 0, K_W13, K_W2, K_SHADOW, K_LM, K_EMBED, K_NFAM };
+enum Family { K_ROUTER = 0, K_W13, K_W2, K_SHADOW, K_LM, K_EMBED, K_ATTN, K_NFAM };
 
 struct Slot {
   char* dev = nullptr;
@@ -48,6 +48,29 @@ struct Ctx {
   void* d_emb = nullptr;
   void* d_lm = nullptr;
   void* d_router = nullptr;
+
+  // attention block (rank 0; reading Q29): fused QKV [L][(H+2Hkv)*hd][d], W_o [L][d][H*hd] in the
+  // main dtype; KV cache [L][max_seq][Hkv*hd] bf16; pos = tokens already in the cache
+  int H = 0, Hkv = 0, hd = 0, qkv_rows = 0, kvd = 0, max_seq = 0;
+  int64_t pos = 0;
+  void* d_wqkv = nullptr;
+  void* d_wo = nullptr;
+  void* d_kc = nullptr;
+  void* d_vc = nullptr;
+  float* d_qkv = nullptr;       // [qkv_rows]
+  float* d_attn_o = nullptr;    // [H*hd]
+  float* d_attn_part = nullptr; // split partials
+  float* dbg_hpre = nullptr;    // [L][d] h before the attention block (debug capture)
+  // shadow attention: int8-row copies, its own current-position k/v (past from the main cache)
+  void* sh_wqkv = nullptr;
+  float* sh_sqkv = nullptr;
+  void* sh_wo = nullptr;
+  float* sh_so = nullptr;
+  float* sh_qkv = nullptr;
+  float* sh_attn_o = nullptr;
+  float* sh_attn_part = nullptr;
+  void* sh_kcur = nullptr;
+  void* sh_vcur = nullptr;
 
   // shadow model (rank 0)
   bool has_shadow = false;
@@ -152,7 +175,8 @@ struct Ctx {
 
   // PERFECT predictor: routing recorded per input token (Mode A: routing is a function of the
   // token only, there is no KV state on the hot path)
-  std::map<int32_t, std::vector<int32_t>> route_cache;
+  // PERFECT predictor: routing recorded per input token (and position, with attention)
+  std::map<int64_t, std::vector<int32_t>> route_cache;
   int32_t predict_cache_token = -1;
 
   // kernel timing (time_kernels)

@@ -135,6 +135,7 @@ void harvest_timers(Ctx* c) {
         case K_SHADOW: c->stats.ms_shadow += ms; c->stats.n_shadow++; break;
         case K_LM: c->stats.ms_lm_head += ms; c->stats.n_lm_head++; break;
         case K_EMBED: c->stats.ms_embed += ms; c->stats.n_embed++; break;
+        case K_ATTN: c->stats.ms_attn += ms; c->stats.n_attn++; break;
       }
     }
     c->tev_pool.push_back(t.a);
@@ -216,6 +217,15 @@ void validate(const odmoe_config* g) {
   if (g->predictor == ODMOE_PRED_SHADOW_BF16 && g->dtype != ODMOE_FP32)
     bad("the BF16 shadow is for an FP32 main model");
   if (g->refine_depth > 0 && g->dtype != ODMOE_BF16) bad("refine_depth needs the bf16 model");
+  if (g->n_heads < 0 || g->n_kv_heads < 0 || g->max_seq < 0) bad("attention sizes");
+  if (g->n_heads > 0) {
+    const int hd = g->d / g->n_heads;
+    if (g->d % g->n_heads || (hd != 32 && hd != 64 && hd != 128)) bad("attention: head_dim = d / n_heads must be 32, 64 or 128");
+    if (g->n_kv_heads < 1 || g->n_heads % g->n_kv_heads || g->n_heads / g->n_kv_heads > 8)
+      bad("attention: n_heads % n_kv_heads == 0 and n_heads / n_kv_heads <= 8");
+    if (g->predictor == ODMOE_PRED_SHADOW_BF16) bad("attention: the BF16 shadow has no attention weights yet");
+    if (((int64_t)g->d * (g->dtype == ODMOE_FP32 ? 4 : 2)) % 512) bad("attention: d * sizeof(dtype) % 512 == 0");
+  }
 }
 
 // ------------------------------------------------------------------ setup
@@ -229,6 +239,67 @@ void build_nonexpert(Ctx* c) {
   CUDA_OK(c, launch_gen(c->d_lm, 6, 0, 0, V, d, d, d, c->F, seed, c->wt, c->s_main));
   for (int l = 0; l < L; ++l)
     CUDA_OK(c, launch_gen((char*)c->d_router + (size_t)l * E * d * c->esz, 2, l, 0, E, d, d, d, c->F, seed, c->wt, c->s_main));
+  if (c->H > 0) {
+    // fused QKV rows [q H*hd | k Hkv*hd | v Hkv*hd] x d and W_o [d][H*hd] per layer; KV cache
+    const size_t qkv = (size_t)c->qkv_rows * d * c->esz, wo = (size_t)d * c->H * c->hd * c->esz;
+    c->d_wqkv = dmalloc<char>(c, qkv * L, "wqkv");
+    c->d_wo = dmalloc<char>(c, wo * L, "wo");
+    for (int l = 0; l < L; ++l) {
+      char* b = (char*)c->d_wqkv + qkv * l;
+      const int64_t qr = (int64_t)c->H * c->hd, kr = (int64_t)c->kvd;
+      CUDA_OK(c, launch_gen(b, 9, l, 0, qr, d, d, d, c->F, seed, c->wt, c->s_main));
+      CUDA_OK(c, launch_gen(b + qr * d * c->esz, 10, l, 0, kr, d, d, d, c->F, seed, c->wt, c->s_main));
+      CUDA_OK(c, launch_gen(b + (qr + kr) * d * c->esz, 11, l, 0, kr, d, d, d, c->F, seed, c->wt, c->s_main));
+      CUDA_OK(c, launch_gen((char*)c->d_wo + wo * l, 12, l, 0, d, qr, d, d, c->F, seed, c->wt, c->s_main));
+    }
+    const size_t kv = (size_t)L * c->max_seq * c->kvd * 2;
+    c->d_kc = dmalloc<char>(c, kv, "k cache");
+    c->d_vc = dmalloc<char>(c, kv, "v cache");
+    CUDA_OK(c, cudaMemsetAsync(c->d_kc, 0, kv, c->s_main));
+    CUDA_OK(c, cudaMemsetAsync(c->d_vc, 0, kv, c->s_main));
+  }
+}
+
+// Attention block of layer l at position c->pos on stream s: h += W_o attn(RMSNorm(h)) (Q29).
+// Main model: its weights, k/v of this position written into the cache. Shadow: int8-row weights,
+// this position's k/v in a private buffer, earlier positions from the MAIN model's cache (KV
+// alignment).
+void enqueue_attention(Ctx* c, int l, cudaStream_t s, float* h, bool shadow) {
+  const int d = c->d, hq = c->H * c->hd;
+  const size_t kv_l = (size_t)l * c->max_seq * c->kvd * 2;
+  char* kc = (char*)c->d_kc + kv_l;
+  char* vc = (char*)c->d_vc + kv_l;
+  const size_t cur = (size_t)c->pos * c->kvd * 2;
+  if (!shadow) {
+    const size_t qkv = (size_t)c->qkv_rows * d * c->esz, wo = (size_t)d * hq * c->esz;
+    { KTimer t(c, K_ATTN, s);
+      CUDA_OK(c, launch_gemv_rmsnorm(h, (const char*)c->d_wqkv + qkv * l, nullptr, c->wt, c->qkv_rows, d,
+                                     c->cfg.rms_eps, c->d_qkv, s, true)); }
+    { KTimer t(c, K_ATTN, s);
+      CUDA_OK(c, launch_rope_kv(c->d_qkv, c->qkv_rows, 1, c->H, c->Hkv, c->hd, (int)c->pos, kc + cur, vc + cur,
+                                c->kvd, s)); }
+    { KTimer t(c, K_ATTN, s);
+      CUDA_OK(c, launch_attention(c->d_qkv, c->qkv_rows, 1, c->H, c->Hkv, c->hd, (int)c->pos, kc, vc, kc + cur,
+                                  vc + cur, c->kvd, c->d_attn_part, c->d_attn_o, nullptr, hq, s)); }
+    { KTimer t(c, K_ATTN, s);
+      CUDA_OK(c, launch_gemv_acc((const char*)c->d_wo + wo * l, nullptr, c->wt, d, hq, c->d_attn_o, h, s, true)); }
+    return;
+  }
+  const bool same = c->sh_wt != W_I8;  // SHADOW_SAME: the main weights
+  const size_t qkv = (size_t)c->qkv_rows * d * (same ? c->esz : 1), wo = (size_t)d * hq * (same ? c->esz : 1);
+  { KTimer t(c, K_SHADOW, s);
+    CUDA_OK(c, launch_gemv_rmsnorm(h, (const char*)c->sh_wqkv + qkv * l,
+                                   same ? nullptr : c->sh_sqkv + (size_t)l * c->qkv_rows, c->sh_wt, c->qkv_rows, d,
+                                   c->cfg.rms_eps, c->sh_qkv, s, true)); }
+  { KTimer t(c, K_SHADOW, s);
+    CUDA_OK(c, launch_rope_kv(c->sh_qkv, c->qkv_rows, 1, c->H, c->Hkv, c->hd, (int)c->pos, c->sh_kcur, c->sh_vcur,
+                              c->kvd, s)); }
+  { KTimer t(c, K_SHADOW, s);
+    CUDA_OK(c, launch_attention(c->sh_qkv, c->qkv_rows, 1, c->H, c->Hkv, c->hd, (int)c->pos, kc, vc, c->sh_kcur,
+                                c->sh_vcur, c->kvd, c->sh_attn_part, c->sh_attn_o, nullptr, hq, s)); }
+  { KTimer t(c, K_SHADOW, s);
+    CUDA_OK(c, launch_gemv_acc((const char*)c->sh_wo + wo * l, same ? nullptr : c->sh_so + (size_t)l * d, c->sh_wt,
+                               d, hq, c->sh_attn_o, h, s, true)); }
 }
 
 void build_shadow(Ctx* c, char* staging) {
@@ -238,6 +309,8 @@ void build_shadow(Ctx* c, char* staging) {
     c->sh_wt = c->sh_ewt = c->wt;
     c->sh_emb = c->d_emb;
     c->sh_router = c->d_router;
+    c->sh_wqkv = c->d_wqkv;
+    c->sh_wo = c->d_wo;
     c->d_sh_tbl = c->d_res_tbl;
     c->d_sh_stbl = nullptr;
     return;
@@ -277,6 +350,16 @@ void build_shadow(Ctx* c, char* staging) {
   c->sh_srouter = dmalloc<float>(c, (size_t)L * E, "shadow router scales");
   CUDA_OK(c, launch_quantize(c->d_emb, V, d, c->wt, (int8_t*)c->sh_emb, c->sh_semb, c->s_main));
   CUDA_OK(c, launch_quantize(c->d_router, (int64_t)L * E, d, c->wt, (int8_t*)c->sh_router, c->sh_srouter, c->s_main));
+  if (c->H > 0) {  // attention projections: int8-row like the routers (reading Q29)
+    const int64_t hq = (int64_t)c->H * c->hd;
+    c->sh_wqkv = dmalloc<int8_t>(c, (size_t)L * c->qkv_rows * d, "shadow wqkv");
+    c->sh_sqkv = dmalloc<float>(c, (size_t)L * c->qkv_rows, "shadow sqkv");
+    c->sh_wo = dmalloc<int8_t>(c, (size_t)L * d * hq, "shadow wo");
+    c->sh_so = dmalloc<float>(c, (size_t)L * d, "shadow so");
+    CUDA_OK(c, launch_quantize(c->d_wqkv, (int64_t)L * c->qkv_rows, d, c->wt, (int8_t*)c->sh_wqkv, c->sh_sqkv, c->s_main));
+    CUDA_OK(c, launch_quantize(c->d_wo, (int64_t)L * d, hq, c->wt, (int8_t*)c->sh_wo, c->sh_so, c->s_main));
+    c->stats.shadow_bytes += (int64_t)L * (c->qkv_rows * d + d * hq) + (int64_t)L * (c->qkv_rows + d) * 4;
+  }
   c->sh_blob.assign((size_t)L * E, nullptr);
   c->sh_sc.assign((size_t)L * E, nullptr);
   for (int l = 0; l < L; ++l)
@@ -496,6 +579,20 @@ void build_buffers(Ctx* c) {
       CUDA_OK(c, cudaMemcpy(c->rf_yptr, yp.data(), sizeof(float*) * k, cudaMemcpyHostToDevice));
     }
   }
+  if (c->H > 0 && c->rank == 0) {
+    const size_t part = (size_t)c->H * attn_splits(c->max_seq - 1) * (c->hd + 2);
+    c->d_qkv = dmalloc<float>(c, c->qkv_rows, "qkv");
+    c->d_attn_o = dmalloc<float>(c, (size_t)c->H * c->hd, "attn o");
+    c->d_attn_part = dmalloc<float>(c, part, "attn part");
+    if (c->has_shadow) {
+      c->sh_qkv = dmalloc<float>(c, c->qkv_rows, "sh qkv");
+      c->sh_attn_o = dmalloc<float>(c, (size_t)c->H * c->hd, "sh attn o");
+      c->sh_attn_part = dmalloc<float>(c, part, "sh attn part");
+      c->sh_kcur = dmalloc<char>(c, (size_t)c->kvd * 2, "sh kcur");
+      c->sh_vcur = dmalloc<char>(c, (size_t)c->kvd * 2, "sh vcur");
+    }
+    if (c->cfg.debug_capture) c->dbg_hpre = dmalloc<float>(c, (size_t)L * d, "dbg_hpre");
+  }
   c->predA_tbl.assign((size_t)L * k, -1);
   c->predA_ready.assign(L, 0);
   c->predB_tbl.assign((size_t)L * k, -1);
@@ -526,9 +623,15 @@ void enqueue_shadow(Ctx* c, const int32_t* token_dev) {
     CUDA_OK(c, launch_embed(c->sh_emb, c->sh_semb, swt, token_dev, d, c->sh_h, s));
   }
   for (int l = 0; l < L; ++l) {
+    int n_add = l > 0 ? k : 0;
+    if (c->H > 0) {  // the shadow's own attention block (past keys/values from the main cache)
+      if (n_add > 0) CUDA_OK(c, launch_combine(c->sh_h, c->sh_yptr, n_add, d, s));
+      n_add = 0;
+      enqueue_attention(c, l, s, c->sh_h, true);
+    }
     {
       KTimer t(c, K_SHADOW, s);
-      CUDA_OK(c, launch_router(c->sh_h, c->sh_yptr, l > 0 ? k : 0, nullptr,
+      CUDA_OK(c, launch_router(c->sh_h, c->sh_yptr, n_add, nullptr,
                                (const char*)c->sh_router + (size_t)l * E * d * sesz,
                                same ? nullptr : c->sh_srouter + (size_t)l * E, swt, 1, E, d, k,
                                c->cfg.rms_eps, c->sh_u, c->sh_ids + (size_t)l * k,
@@ -660,9 +763,15 @@ void enqueue_refine(Ctx* c, int j) {
   }
   for (int r = 1; r <= R && j + r < L; ++r) {
     const int m = j + r;
+    int n_add = k;
+    if (c->H > 0) {
+      CUDA_OK(c, launch_combine(c->rf_h, c->rf_yptr, k, d, s));
+      n_add = 0;
+      enqueue_attention(c, m, s, c->rf_h, true);
+    }
     {
       KTimer t(c, K_SHADOW, s);
-      CUDA_OK(c, launch_router(c->rf_h, c->rf_yptr, k, nullptr, (const char*)c->sh_router + (size_t)m * E * d * sesz,
+      CUDA_OK(c, launch_router(c->rf_h, c->rf_yptr, n_add, nullptr, (const char*)c->sh_router + (size_t)m * E * d * sesz,
                                same ? nullptr : c->sh_srouter + (size_t)m * E, swt, 1, E, d, k, c->cfg.rms_eps,
                                c->rf_u, out + (size_t)(r - 1) * k, c->rf_w + (size_t)(r - 1) * k, nullptr, nullptr, s, true));
     }
@@ -874,6 +983,9 @@ uint32_t p2p_mask(const Ctx* c, int l) {
 void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_record* rec) {
   const int L = c->L, E = c->E, k = c->k, d = c->d, F = c->F;
   if (token_in < 0 || token_in >= c->V) fail(c, ODMOE_E_RANGE, "token out of range");
+  if (c->H > 0 && c->pos >= c->max_seq) fail(c, ODMOE_E_RANGE, "KV cache full (max_seq)");
+  // a step is a function of its token (no attention) or of (token, position) over a replayed context
+  const int64_t route_key = c->H > 0 ? ((int64_t)c->pos << 32) | (uint32_t)token_in : (int64_t)token_in;
   cudaStream_t s = c->s_main;
   const int p = c->cfg.predictor;
   const bool r0 = c->rank == 0;
@@ -920,7 +1032,7 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
       std::fill(c->pred_ready.begin(), c->pred_ready.end(), 1);
       c->pred_valid = true;
     } else if (p == ODMOE_PRED_PERFECT) {
-      auto it = c->route_cache.find(token_in);
+      auto it = c->route_cache.find(route_key);
       if (it != c->route_cache.end()) {
         std::copy(it->second.begin(), it->second.end(), c->pred_tbl.begin());
         c->predA_tbl = c->pred_tbl;
@@ -955,6 +1067,16 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
       CUDA_OK(c, launch_p2p_gather(c->p2p_part, c->p2p_flag, p2p_mask(c, l - 1), d, c->p2p_seq - 1, c->d_yred,
                                    c->d_flag, s));
       c->stats.kernel_launches++;
+    }
+    if (r0 && c->H > 0) {
+      // attention block of layer l (Q29): h += y_{l-1}; h += W_o attn(RMSNorm(h)); router sees that h
+      if (n_add > 0) {
+        CUDA_OK(c, launch_combine(c->d_h, yadd, n_add, d, s));
+        c->stats.kernel_launches++;
+        n_add = 0;
+      }
+      if (c->dbg_hpre) CUDA_OK(c, cudaMemcpyAsync(c->dbg_hpre + (size_t)l * d, c->d_h, sizeof(float) * d, cudaMemcpyDeviceToDevice, s));
+      enqueue_attention(c, l, s, c->d_h, false);
     }
     if (r0) {
       KTimer t(c, K_ROUTER, s);
@@ -1193,10 +1315,11 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
         for (int j = 0; j < k; ++j) rec[l].weights[j] = wv[(size_t)l * k + j];
     }
   }
-  c->route_cache[token_in] = true_ids;
+  c->route_cache[route_key] = true_ids;
   *token_out = c->h_tok[1];
   c->stats.tokens++;
   c->step++;
+  if (c->H > 0) c->pos++;
   if (c->cfg.time_kernels) harvest_timers(c);
   // loader statistics
   c->stats.loads_issued = c->loader.loads_issued.load();
@@ -1248,6 +1371,7 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
     }
     add(11, c->dbg_hfinal, (int64_t)d * 4, 1);
     add(12, c->d_lmlogits, (int64_t)c->V * 4, 1);
+    if (c->dbg_hpre) add(13, c->dbg_hpre, (int64_t)d * 4, L);
   }
 }
 
@@ -1311,6 +1435,7 @@ void build_tiles(const std::vector<int32_t>& off, const std::vector<int>& mine, 
 void prefill_impl(Ctx* c, const int32_t* tokens, int T, int32_t* token_out, int32_t* counts_out) {
   const int L = c->L, E = c->E, k = c->k, d = c->d;
   if (c->wt != W_BF16) fail(c, ODMOE_E_CONFIG, "prefill runs the bf16 tensor-core GEMM: needs dtype BF16");
+  if (c->H > 0) fail(c, ODMOE_E_CONFIG, "prefill with the attention block: not built yet (decode only)");
   if (E > kMaxGGExperts) fail(c, ODMOE_E_CONFIG, "prefill supports E <= 8");
   if (d % 256 || c->Fs % 128) fail(c, ODMOE_E_CONFIG, "prefill needs d % 256 == 0 and F (per rank) % 128 == 0");
   if (T < 1 || !tokens) fail(c, ODMOE_E_CONFIG, "empty prompt (S:108)");
@@ -1481,7 +1606,10 @@ void destroy_ctx(Ctx* c) {
   if (c->s_copy) cudaStreamSynchronize(c->s_copy);
   auto F = [](void* p) { if (p) cudaFree(p); };
   F(c->d_emb); F(c->d_lm); F(c->d_router);
+  F(c->d_wqkv); F(c->d_wo); F(c->d_kc); F(c->d_vc); F(c->d_qkv); F(c->d_attn_o); F(c->d_attn_part); F(c->dbg_hpre);
+  F(c->sh_qkv); F(c->sh_attn_o); F(c->sh_attn_part); F(c->sh_kcur); F(c->sh_vcur);
   if (c->built_pred != ODMOE_PRED_SHADOW_SAME) {
+    F(c->sh_wqkv); F(c->sh_sqkv); F(c->sh_wo); F(c->sh_so);
     F(c->sh_emb); F(c->sh_semb); F(c->sh_router); F(c->sh_srouter);
     for (auto p : c->sh_blob) F(p);
     for (auto p : c->sh_sc) F(p);
@@ -1591,6 +1719,14 @@ odmoe_status odmoe_create(const odmoe_config* cfg, void** ctx_out) {
     c->my_group = c->rank / c->G;
     c->my_pos = c->rank % c->G;
     c->resident = cfg->slots_per_gpu == -1;
+    if (cfg->n_heads > 0) {
+      c->H = cfg->n_heads;
+      c->Hkv = cfg->n_kv_heads;
+      c->hd = c->d / c->H;
+      c->kvd = c->Hkv * c->hd;
+      c->qkv_rows = (c->H + 2 * c->Hkv) * c->hd;
+      c->max_seq = cfg->max_seq > 0 ? cfg->max_seq : 4096;
+    }
     c->built_pred = cfg->predictor;
     c->dev = cfg->device;
     c->has_shadow = c->rank == 0 && !c->resident &&
@@ -1712,6 +1848,9 @@ odmoe_status odmoe_set_option(void* ctx, int key, int64_t value) {
       if (value > 0 && (c->ev_ref.empty() || c->wt != W_BF16))
         fail(c, ODMOE_E_STATE, "refinement needs a bf16 ctx created with a shadow predictor");
       c->cfg.refine_depth = (int32_t)value;
+    } else if (key == 4) {
+      if (value < 0 || value >= c->max_seq || c->H == 0) fail(c, ODMOE_E_RANGE, "position outside the KV cache");
+      c->pos = value;
     } else {
       fail(c, ODMOE_E_CONFIG, "unknown option key");
     }
@@ -1790,7 +1929,7 @@ odmoe_status odmoe_debug_read(const void* ctx, int what, int layer, void* dst, i
   if (!c || !dst) return ODMOE_E_STATE;
   auto it = c->hdbg_index.find(what);
   if (it == c->hdbg_index.end()) return ODMOE_E_STATE;
-  const int64_t off = it->second.first + (int64_t)(what >= 11 ? 0 : layer) * it->second.second;
+  const int64_t off = it->second.first + (int64_t)((what == 11 || what == 12) ? 0 : layer) * it->second.second;
   if (layer < 0 || layer >= c->L || bytes > it->second.second || off + bytes > (int64_t)c->hdbg.size()) return ODMOE_E_RANGE;
   std::memcpy(dst, c->hdbg.data() + off, (size_t)bytes);
   return ODMOE_OK;
