@@ -249,7 +249,8 @@ def run_reference(args):
 
 
 def attn_kw(args):
-    return dict(n_heads=32, n_kv_heads=8, max_seq=args.context + args.warmup + args.steps + 8) if args.attention else {}
+    ctx = max(args.context, args.prefill)
+    return dict(n_heads=32, n_kv_heads=8, max_seq=ctx + args.warmup + args.steps + 8) if args.attention else {}
 
 
 def sliced(args, n):
@@ -280,9 +281,10 @@ def workload_config(args, n):
             "predictor": args.predictor, "slots_per_gpu": n_slots(args, n), "refine_depth": args.refine,
             "expert_bytes_per_gpu": n_slots(args, n) * per_slot,
             "lookahead": lookahead(args, n), "weight_seed": SEED,
-            "attention": (f"Mixtral GQA 32q/8kv, head_dim 128, RoPE 1e6, bf16 KV cache; decode from position "
-                          f"{args.context} (earlier cache rows zero: synthetic context)" if args.attention
-                          else "none on the hot path (reading Q22)"),
+            "attention": (("Mixtral GQA 32q/8kv, head_dim 128, RoPE 1e6, bf16 KV cache; " +
+                           (f"decode after the {args.prefill}-token prefill" if args.prefill > 0 else
+                            f"decode from position {args.context} (earlier cache rows zero: synthetic context)"))
+                          if args.attention else "none on the hot path (reading Q22)"),
             "l2": "inputs larger than L2: every step streams 64 distinct 352 MB experts"}
 
 
@@ -327,8 +329,8 @@ def main():
     eng = odmoe.Engine(device=local, rank=rank, world_size=world, nccl_id=uid, predictor=pred,
                        slots_per_gpu=n_slots(args, n), lookahead=D, time_kernels=1, weight_seed=SEED,
                        refine_depth=refine, placement=int(sliced(args, n)), **SHAPE, **attn_kw(args))
-    if args.attention:
-        eng.set_position(args.context)
+    if args.attention and args.prefill <= 0:
+        eng.set_position(args.context)  # no prompt: decode over a zero-filled synthetic context
     t_create = time.time() - t_create
     def barrier():
         if dist is not None:
@@ -339,7 +341,7 @@ def main():
 
     tok = args.first_token if args.first_token >= 0 else 1
     prefill = None
-    if args.prefill > 0 and not args.attention:
+    if args.prefill > 0:
         log(rank, f"prefill {args.prefill}")
         from inputs import MIXTRAL, gen_prompt
         prompt = [int(x) for x in gen_prompt(MIXTRAL, 1, args.prefill)]

@@ -134,6 +134,35 @@ __global__ void attn_merge_kernel(const float* __restrict__ part, int H, int hd,
 
 int attn_splits(int max_pos) { return max_pos / kAttnSplit + 1; }
 
+// x[t] = bf16(RMSNorm(h[t])) for T rows (prefill: the A operand of the QKV GEMM); block per row.
+__global__ void __launch_bounds__(256) rmsnorm_rows_kernel(const float* __restrict__ h, int d, float eps,
+                                                           uint16_t* __restrict__ x) {
+  __shared__ float red[9];
+  const int t = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const float* hr = h + (size_t)t * d;
+  float ss = 0.f;
+  for (int j = tid; j < d; j += blockDim.x) ss = fmaf(hr[j], hr[j], ss);
+  ss = warp_sum(ss);
+  if (lane == 0) red[warp] = ss;
+  __syncthreads();
+  if (tid == 0) {
+    float s = 0.f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+    red[8] = s;
+  }
+  __syncthreads();
+  const float rstd = 1.0f / sqrtf(red[8] / (float)d + eps);
+  for (int j = tid; j < d; j += blockDim.x) {
+    const __nv_bfloat16 b = __float2bfloat16_rn(hr[j] * rstd);
+    x[(size_t)t * d + j] = *reinterpret_cast<const uint16_t*>(&b);
+  }
+}
+
+cudaError_t launch_rmsnorm_rows(const float* h, int T, int d, float eps, void* x_bf16, cudaStream_t s) {
+  rmsnorm_rows_kernel<<<T, 256, 0, s>>>(h, d, eps, (uint16_t*)x_bf16);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_attention(const float* q, int q_stride, int T, int H, int Hkv, int hd, int pos0, const void* kc_past,
                              const void* vc_past, const void* kc_cur, const void* vc_cur, int kv_stride, float* part,
                              float* o_f32, void* o_bf16, int o_stride, cudaStream_t s) {

@@ -182,7 +182,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_cons
       const int r = hh * kGG_BM + q * 32 + lane;
       const bool valid = r < rows;
       const long long grow = (long long)row0 + r;
-      const float g = (MODE == 1 && valid) ? gate[grow] : 0.f;
+      const float g = (MODE == 1 && valid) ? (gate ? gate[grow] : 1.f) : 0.f;  // no gate: plain GEMM
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 16) {
         uint32_t v[16];

@@ -147,6 +147,7 @@ cudaError_t launch_rope_kv(float* qkv, int qkv_stride, int T, int H, int Hkv, in
 // position), >= pos0 from *_cur (row t = position pos0 + t); part: attn_part_floats(...) fp32;
 // o [T][H*hd] as fp32 and/or bf16 (either may be NULL)
 int attn_splits(int max_pos);
+cudaError_t launch_rmsnorm_rows(const float* h, int T, int d, float eps, void* x_bf16, cudaStream_t s);
 cudaError_t launch_attention(const float* q, int q_stride, int T, int H, int Hkv, int hd, int pos0, const void* kc_past,
                              const void* vc_past, const void* kc_cur, const void* vc_cur, int kv_stride, float* part,
                              float* o_f32, void* o_bf16, int o_stride, cudaStream_t s);

@@ -61,6 +61,12 @@ struct Ctx {
   float* d_attn_o = nullptr;    // [H*hd]
   float* d_attn_part = nullptr; // split partials
   float* dbg_hpre = nullptr;    // [L][d] h before the attention block (debug capture)
+  // prefill attention buffers (T_cap rows)
+  void* pa_x = nullptr;         // bf16 [T][d] RMSNorm(h) / attention output o
+  float* pa_qkv = nullptr;      // fp32 [T][qkv_rows]
+  float* pa_part = nullptr;     // split partials
+  float* pa_out = nullptr;      // fp32 [T][d] W_o o
+  int4* pa_tiles = nullptr;
   // shadow attention: int8-row copies, its own current-position k/v (past from the main cache)
   void* sh_wqkv = nullptr;
   float* sh_sqkv = nullptr;

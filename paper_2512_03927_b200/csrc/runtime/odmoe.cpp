@@ -1418,6 +1418,14 @@ void ensure_prefill(Ctx* c, int T) {
   c->p_part = dmalloc<float>(c, (size_t)T * d, "p_part");
   c->tiles_cap = (int)(((M + 127) / 128 + E) * (2 * c->Fs / grouped_gemm_bn(0) + d / grouped_gemm_bn(1)));
   c->p_tiles = dmalloc<int4>(c, (size_t)c->tiles_cap, "p_tiles");
+  if (c->H > 0 && c->rank == 0) {
+    F_(c->pa_x); F_(c->pa_qkv); F_(c->pa_part); F_(c->pa_out); F_(c->pa_tiles);
+    c->pa_x = dmalloc<char>(c, (size_t)T * d * 2, "pa_x");
+    c->pa_qkv = dmalloc<float>(c, (size_t)T * c->qkv_rows, "pa_qkv");
+    c->pa_part = dmalloc<float>(c, (size_t)T * c->H * attn_splits(T - 1) * (c->hd + 2), "pa_part");
+    c->pa_out = dmalloc<float>(c, (size_t)T * d, "pa_out");
+    c->pa_tiles = dmalloc<int4>(c, (size_t)((T + 255) / 256 + 1) * (c->qkv_rows / 128 + d / 128 + 2), "pa_tiles");
+  }
   c->T_cap = T;
 }
 
@@ -1432,10 +1440,41 @@ void build_tiles(const std::vector<int32_t>& off, const std::vector<int>& mine, 
   }
 }
 
+// Prefill attention of layer l for positions 0..T-1 (rank 0): x = RMSNorm(h) (bf16), QKV = x W^T on
+// the tcgen05 GEMM, RoPE + KV cache rows, causal GQA attention, h += o W_o^T (GEMM + row add).
+void prefill_attention(Ctx* c, int l, int T, cudaStream_t s) {
+  const int d = c->d, hq = c->H * c->hd;
+  const size_t qkv_b = (size_t)c->qkv_rows * d * c->esz, wo_b = (size_t)d * hq * c->esz;
+  const size_t kv_l = (size_t)l * c->max_seq * c->kvd * 2;
+  char* kc = (char*)c->d_kc + kv_l;
+  char* vc = (char*)c->d_vc + kv_l;
+  auto gemm = [&](const void* a, const void* w, int N, int K, float* out) {
+    std::vector<int4> tiles;
+    const int BM = grouped_gemm_bm(), BN = grouped_gemm_bn(1);
+    for (int m0 = 0; m0 < T; m0 += BM)
+      for (int n0 = 0; n0 < N; n0 += BN) tiles.push_back(make_int4(0, m0, std::min(BM, T - m0), n0));
+    CUDA_OK(c, cudaMemcpyAsync(c->pa_tiles, tiles.data(), sizeof(int4) * tiles.size(), cudaMemcpyHostToDevice, s));
+    GroupedGemmArgs g{};
+    g.a = a; g.b[0] = w; g.n_experts = 1; g.tiles = c->pa_tiles; g.n_tiles = (int)tiles.size();
+    g.M = T; g.N = N; g.K = K; g.mode = 1; g.out = out; g.gate = nullptr;
+    CUDA_OK(c, launch_grouped_gemm(g, s));
+    CUDA_OK(c, cudaStreamSynchronize(s));  // the host tile list is reused by the next GEMM
+  };
+  KTimer t(c, K_ATTN, s);
+  CUDA_OK(c, launch_rmsnorm_rows(c->p_h, T, d, c->cfg.rms_eps, c->pa_x, s));
+  gemm(c->pa_x, (const char*)c->d_wqkv + qkv_b * l, c->qkv_rows, d, c->pa_qkv);
+  CUDA_OK(c, launch_rope_kv(c->pa_qkv, c->qkv_rows, T, c->H, c->Hkv, c->hd, 0, kc, vc, c->kvd, s));
+  CUDA_OK(c, launch_attention(c->pa_qkv, c->qkv_rows, T, c->H, c->Hkv, c->hd, 0, kc, vc, kc, vc, c->kvd, c->pa_part,
+                              nullptr, c->pa_x, hq, s));
+  gemm(c->pa_x, (const char*)c->d_wo + wo_b * l, d, hq, c->pa_out);
+  CUDA_OK(c, launch_add_rows(c->p_h, c->pa_out, (long long)T * d, s));
+  c->stats.kernel_launches += 6;
+}
+
 void prefill_impl(Ctx* c, const int32_t* tokens, int T, int32_t* token_out, int32_t* counts_out) {
   const int L = c->L, E = c->E, k = c->k, d = c->d;
   if (c->wt != W_BF16) fail(c, ODMOE_E_CONFIG, "prefill runs the bf16 tensor-core GEMM: needs dtype BF16");
-  if (c->H > 0) fail(c, ODMOE_E_CONFIG, "prefill with the attention block: not built yet (decode only)");
+  if (c->H > 0 && T > c->max_seq) fail(c, ODMOE_E_RANGE, "prompt longer than the KV cache (max_seq)");
   if (E > kMaxGGExperts) fail(c, ODMOE_E_CONFIG, "prefill supports E <= 8");
   if (d % 256 || c->Fs % 128) fail(c, ODMOE_E_CONFIG, "prefill needs d % 256 == 0 and F (per rank) % 128 == 0");
   if (T < 1 || !tokens) fail(c, ODMOE_E_CONFIG, "empty prompt (S:108)");
@@ -1483,7 +1522,9 @@ void prefill_impl(Ctx* c, const int32_t* tokens, int T, int32_t* token_out, int3
   char* u = c->p_pkt;
   int32_t* ids = (int32_t*)(c->p_pkt + c->p_ids_off);
   float* w = (float*)(c->p_pkt + c->p_w_off);
+  if (c->H > 0) c->pos = 0;  // a prompt starts a new sequence
   for (int l = 0; l < L; ++l) {
+    if (r0 && c->H > 0) prefill_attention(c, l, T, s);
     if (r0) {
       KTimer t(c, K_ROUTER, s);
       CUDA_OK(c, launch_router(c->p_h, nullptr, 0, nullptr, (const char*)c->d_router + (size_t)l * E * d * c->esz,
@@ -1581,6 +1622,7 @@ void prefill_impl(Ctx* c, const int32_t* tokens, int T, int32_t* token_out, int3
   CUDA_OK(c, cudaMemcpyAsync(c->h_flag, c->d_flag, 4, cudaMemcpyDeviceToHost, s));
   CUDA_OK(c, cudaStreamSynchronize(s));
   if (c->h_flag[0]) fail(c, ODMOE_E_NONFINITE, "non-finite router logits");
+  if (c->H > 0) c->pos = T;
   if (c->cfg.time_kernels) harvest_timers(c);
   c->stats.bytes_h2d = c->loader.bytes_h2d.load();
   c->stats.loads_issued = c->loader.loads_issued.load();
@@ -1608,6 +1650,7 @@ void destroy_ctx(Ctx* c) {
   F(c->d_emb); F(c->d_lm); F(c->d_router);
   F(c->d_wqkv); F(c->d_wo); F(c->d_kc); F(c->d_vc); F(c->d_qkv); F(c->d_attn_o); F(c->d_attn_part); F(c->dbg_hpre);
   F(c->sh_qkv); F(c->sh_attn_o); F(c->sh_attn_part); F(c->sh_kcur); F(c->sh_vcur);
+  F(c->pa_x); F(c->pa_qkv); F(c->pa_part); F(c->pa_out); F(c->pa_tiles);
   if (c->built_pred != ODMOE_PRED_SHADOW_SAME) {
     F(c->sh_wqkv); F(c->sh_sqkv); F(c->sh_wo); F(c->sh_so);
     F(c->sh_emb); F(c->sh_semb); F(c->sh_router); F(c->sh_srouter);

@@ -131,8 +131,30 @@ def test_attention_config_errors(od):
     eng.set_position(0)
     eng.decode_step(t)
     with pytest.raises(od.OdmoeError):
-        eng.prefill([1, 2, 3])                               # prefill with attention: not built yet
+        eng.prefill([1, 2, 3, 4])                            # prompt longer than the cache
     eng.close()
+
+
+def test_attention_prefill_matches_token_by_token_decode(od):
+    """Prefill (tcgen05 GEMM projections, causal attention over the prompt) leaves the same KV
+    cache and next token as feeding the prompt one decode step at a time (within bf16 rounding:
+    the prefill's attention output enters W_o as bf16); decoding then continues identically."""
+    shape = TINY_ATTN
+    prompt = [int(x) for x in gen_prompt(shape, 8, 40)]
+    a = engine(od, shape, predictor=od.PRED_NONE, slots_per_gpu=2)
+    tok_a, counts = a.prefill(prompt)
+    b = engine(od, shape, predictor=od.PRED_NONE, slots_per_gpu=2)
+    for t in prompt:
+        tok_b, _ = b.decode_step(t)
+    assert tok_a == tok_b
+    ta, tb = tok_a, tok_b
+    for _ in range(6):
+        ta, _ = a.decode_step(ta)
+        tb, _ = b.decode_step(tb)
+        assert ta == tb
+    assert sum(counts) == shape.L * shape.k * len(prompt)
+    a.close()
+    b.close()
 
 
 @pytest.mark.slow
