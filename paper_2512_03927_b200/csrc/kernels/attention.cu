@@ -18,11 +18,19 @@ constexpr int kAttnSplit = 128;  // positions per split
 constexpr int kMaxHd = 128;
 
 __device__ __forceinline__ float bf16_to_f(uint16_t b) { return __uint_as_float((uint32_t)b << 16); }
+// KV-cache element: bf16 for the bf16 model, fp32 for the fp32 model (P:260's 8 KB fp32 per token)
+__device__ __forceinline__ float kv_ld(const uint16_t* p) { return bf16_to_f(*p); }
+__device__ __forceinline__ float kv_ld(const float* p) { return *p; }
+__device__ __forceinline__ void kv_st(uint16_t* p, float v) {
+  const __nv_bfloat16 b = __float2bfloat16_rn(v);
+  *p = *reinterpret_cast<const uint16_t*>(&b);
+}
+__device__ __forceinline__ void kv_st(float* p, float v) { *p = v; }
 
 // grid = (T tokens, H + Hkv heads), block = hd/2 threads: one rotation pair per thread.
+template <typename KT>
 __global__ void rope_kv_kernel(float* __restrict__ qkv, int qkv_stride, int H, int Hkv, int hd, int pos0,
-                               uint16_t* __restrict__ kc, uint16_t* __restrict__ vc, int kv_stride,
-                               float log2_theta) {
+                               KT* __restrict__ kc, KT* __restrict__ vc, int kv_stride, float log2_theta) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const int t = blockIdx.x, head = blockIdx.y, i = threadIdx.x, half = hd / 2;
   const int pos = pos0 + t;
@@ -43,22 +51,25 @@ __global__ void rope_kv_kernel(float* __restrict__ qkv, int qkv_stride, int H, i
     const float* k = row + H * hd + g * hd;
     const float* v = row + (H + Hkv) * hd + g * hd;
     const float x1 = k[i], x2 = k[i + half];
-    uint16_t* kd = kc + (size_t)t * kv_stride + g * hd;
-    uint16_t* vd = vc + (size_t)t * kv_stride + g * hd;
-    const __nv_bfloat16 r1 = __float2bfloat16_rn(x1 * c - x2 * s), r2 = __float2bfloat16_rn(x2 * c + x1 * s);
-    kd[i] = *reinterpret_cast<const uint16_t*>(&r1);
-    kd[i + half] = *reinterpret_cast<const uint16_t*>(&r2);
-    const __nv_bfloat16 v1 = __float2bfloat16_rn(v[i]), v2 = __float2bfloat16_rn(v[i + half]);
-    vd[i] = *reinterpret_cast<const uint16_t*>(&v1);
-    vd[i + half] = *reinterpret_cast<const uint16_t*>(&v2);
+    KT* kd = kc + (size_t)t * kv_stride + g * hd;
+    KT* vd = vc + (size_t)t * kv_stride + g * hd;
+    kv_st(kd + i, x1 * c - x2 * s);
+    kv_st(kd + i + half, x2 * c + x1 * s);
+    kv_st(vd + i, v[i]);
+    kv_st(vd + i + half, v[i + half]);
   }
 }
 
 cudaError_t launch_rope_kv(float* qkv, int qkv_stride, int T, int H, int Hkv, int hd, int pos0, void* kc, void* vc,
-                           int kv_stride, cudaStream_t s) {
+                           int kv_stride, int kv_f32, cudaStream_t s) {
   if (hd % 2 || hd > kMaxHd || T < 1) return cudaErrorInvalidValue;
-  rope_kv_kernel<<<dim3(T, H + Hkv), hd / 2, 0, s>>>(qkv, qkv_stride, H, Hkv, hd, pos0, (uint16_t*)kc, (uint16_t*)vc,
-                                                     kv_stride, (float)19.931568569324174);  // log2(1e6)
+  const float lt = (float)19.931568569324174;  // log2(1e6)
+  if (kv_f32)
+    rope_kv_kernel<float><<<dim3(T, H + Hkv), hd / 2, 0, s>>>(qkv, qkv_stride, H, Hkv, hd, pos0, (float*)kc, (float*)vc,
+                                                              kv_stride, lt);
+  else
+    rope_kv_kernel<uint16_t><<<dim3(T, H + Hkv), hd / 2, 0, s>>>(qkv, qkv_stride, H, Hkv, hd, pos0, (uint16_t*)kc,
+                                                                 (uint16_t*)vc, kv_stride, lt);
   return cudaGetLastError();
 }
 
@@ -67,13 +78,50 @@ cudaError_t launch_rope_kv(float* qkv, int qkv_stride, int T, int H, int Hkv, in
 // K rows for positions < pos0 come from kc_past (the cache); rows >= pos0 from kc_cur
 // (the rows written by rope_kv for these queries: the cache itself for the main model, a private
 // buffer for the shadow, which reads the main model's cache for the past: KV alignment).
+template <typename KT>
+__device__ __forceinline__ float dot_row(const float* __restrict__ q, const KT* __restrict__ k, int hd);
+template <>
+__device__ __forceinline__ float dot_row<uint16_t>(const float* __restrict__ q, const uint16_t* __restrict__ k, int hd) {
+  float s0 = 0.f, s1 = 0.f;
+  const uint4* k4 = reinterpret_cast<const uint4*>(k);
+#pragma unroll 4
+  for (int c = 0; c < hd / 8; ++c) {
+    const uint4 w = k4[c];
+    const float* qc = q + 8 * c;
+    s0 = fmaf(qc[0], bf16_lo(w.x), s0); s1 = fmaf(qc[1], bf16_hi(w.x), s1);
+    s0 = fmaf(qc[2], bf16_lo(w.y), s0); s1 = fmaf(qc[3], bf16_hi(w.y), s1);
+    s0 = fmaf(qc[4], bf16_lo(w.z), s0); s1 = fmaf(qc[5], bf16_hi(w.z), s1);
+    s0 = fmaf(qc[6], bf16_lo(w.w), s0); s1 = fmaf(qc[7], bf16_hi(w.w), s1);
+  }
+  return s0 + s1;
+}
+template <>
+__device__ __forceinline__ float dot_row<float>(const float* __restrict__ q, const float* __restrict__ k, int hd) {
+  float s0 = 0.f, s1 = 0.f;
+  const float4* k4 = reinterpret_cast<const float4*>(k);
+#pragma unroll 4
+  for (int c = 0; c < hd / 4; ++c) {
+    const float4 w = k4[c];
+    const float* qc = q + 4 * c;
+    s0 = fmaf(qc[0], w.x, s0); s1 = fmaf(qc[1], w.y, s1);
+    s0 = fmaf(qc[2], w.z, s0); s1 = fmaf(qc[3], w.w, s1);
+  }
+  return s0 + s1;
+}
+
+// One warp per query head of the group: (1) lanes score different positions (each lane a whole
+// q.k over hd, many independent loads in flight), (2) softmax statistics by warp reductions,
+// (3) lanes own head dimensions and accumulate p_t v_t over the split's positions.
+template <typename KT>
 __global__ void __launch_bounds__(32 * 8) attn_split_kernel(const float* __restrict__ q, int q_stride, int H, int Hkv,
-                                                           int hd, int pos0, const uint16_t* __restrict__ kc_past,
-                                                           const uint16_t* __restrict__ vc_past,
-                                                           const uint16_t* __restrict__ kc_cur,
-                                                           const uint16_t* __restrict__ vc_cur, int kv_stride,
+                                                           int hd, int pos0, const KT* __restrict__ kc_past,
+                                                           const KT* __restrict__ vc_past,
+                                                           const KT* __restrict__ kc_cur,
+                                                           const KT* __restrict__ vc_cur, int kv_stride,
                                                            int nsplit, float* __restrict__ part) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  __shared__ float qs[8][kMaxHd];
+  __shared__ float ps[8][kAttnSplit];
   const int t = blockIdx.z, g = blockIdx.x, sp = blockIdx.y;
   const int rep = H / Hkv;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -81,31 +129,45 @@ __global__ void __launch_bounds__(32 * 8) attn_split_kernel(const float* __restr
   const int head = g * rep + warp;
   const int pos = pos0 + t;
   const int p_begin = sp * kAttnSplit;
-  const int p_end = min(pos + 1, p_begin + kAttnSplit);
+  const int n = max(0, min(pos + 1, p_begin + kAttnSplit) - p_begin);
   float* out = part + ((size_t)(t * H + head) * nsplit + sp) * (hd + 2);
-  const int per = hd / 32;  // elements per lane (hd = 32, 64 or 128)
-  float qv[4];
-  const float* qh = q + (size_t)t * q_stride + head * hd;
   const float scale = rsqrtf((float)hd);
-  for (int j = 0; j < per; ++j) qv[j] = qh[lane * per + j] * scale;
-  float m = -INFINITY, l = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int p = p_begin; p < p_end; ++p) {
-    const uint16_t* kr = p < pos0 ? kc_past + (size_t)p * kv_stride : kc_cur + (size_t)(p - pos0) * kv_stride;
-    const uint16_t* vr = p < pos0 ? vc_past + (size_t)p * kv_stride : vc_cur + (size_t)(p - pos0) * kv_stride;
-    kr += g * hd + lane * per;
-    vr += g * hd + lane * per;
-    float sdot = 0.f;
-    for (int j = 0; j < per; ++j) sdot = fmaf(qv[j], bf16_to_f(kr[j]), sdot);
-    sdot = warp_sum(sdot);
-    const float mn = fmaxf(m, sdot);
-    const float corr = __expf(m - mn), w = __expf(sdot - mn);
-    l = l * corr + w;
-    for (int j = 0; j < per; ++j) acc[j] = fmaf(w, bf16_to_f(vr[j]), acc[j] * corr);
-    m = mn;
+  const float* qh = q + (size_t)t * q_stride + head * hd;
+  for (int j = lane; j < hd; j += 32) qs[warp][j] = qh[j] * scale;
+  __syncwarp();
+  auto krow = [&](int p) -> const KT* {
+    return (p < pos0 ? kc_past + (size_t)p * kv_stride : kc_cur + (size_t)(p - pos0) * kv_stride) + g * hd;
+  };
+  auto vrow = [&](int p) -> const KT* {
+    return (p < pos0 ? vc_past + (size_t)p * kv_stride : vc_cur + (size_t)(p - pos0) * kv_stride) + g * hd;
+  };
+  float m = -INFINITY;
+  for (int i = lane; i < n; i += 32) {
+    const float sdot = dot_row<KT>(qs[warp], krow(p_begin + i), hd);
+    ps[warp][i] = sdot;
+    m = fmaxf(m, sdot);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  float l = 0.f;
+  for (int i = lane; i < n; i += 32) {
+    const float w = __expf(ps[warp][i] - m);
+    ps[warp][i] = w;
+    l += w;
+  }
+  l = warp_sum(l);
+  __syncwarp();
+  const int per = hd / 32;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+  for (int i = 0; i < n; ++i) {
+    const float w = ps[warp][i];
+    const KT* vr = vrow(p_begin + i) + lane * per;
+    for (int j = 0; j < per; ++j) acc[j] = fmaf(w, kv_ld(vr + j), acc[j]);
   }
   for (int j = 0; j < per; ++j) out[lane * per + j] = acc[j];
   if (lane == 0) {
-    out[hd] = m;
+    out[hd] = n > 0 ? m : -INFINITY;
     out[hd + 1] = l;
   }
 }
@@ -164,13 +226,19 @@ cudaError_t launch_rmsnorm_rows(const float* h, int T, int d, float eps, void* x
 }
 
 cudaError_t launch_attention(const float* q, int q_stride, int T, int H, int Hkv, int hd, int pos0, const void* kc_past,
-                             const void* vc_past, const void* kc_cur, const void* vc_cur, int kv_stride, float* part,
-                             float* o_f32, void* o_bf16, int o_stride, cudaStream_t s) {
+                             const void* vc_past, const void* kc_cur, const void* vc_cur, int kv_stride, int kv_f32,
+                             float* part, float* o_f32, void* o_bf16, int o_stride, cudaStream_t s) {
   if (hd % 32 || hd > kMaxHd || H % Hkv || H / Hkv > 8 || T < 1) return cudaErrorInvalidValue;
   const int nsplit = attn_splits(pos0 + T - 1);
-  attn_split_kernel<<<dim3(Hkv, nsplit, T), 32 * (H / Hkv), 0, s>>>(
-      q, q_stride, H, Hkv, hd, pos0, (const uint16_t*)kc_past, (const uint16_t*)vc_past, (const uint16_t*)kc_cur,
-      (const uint16_t*)vc_cur, kv_stride, nsplit, part);
+  const dim3 grid(Hkv, nsplit, T);
+  if (kv_f32)
+    attn_split_kernel<float><<<grid, 32 * (H / Hkv), 0, s>>>(q, q_stride, H, Hkv, hd, pos0, (const float*)kc_past,
+                                                             (const float*)vc_past, (const float*)kc_cur,
+                                                             (const float*)vc_cur, kv_stride, nsplit, part);
+  else
+    attn_split_kernel<uint16_t><<<grid, 32 * (H / Hkv), 0, s>>>(q, q_stride, H, Hkv, hd, pos0, (const uint16_t*)kc_past,
+                                                                (const uint16_t*)vc_past, (const uint16_t*)kc_cur,
+                                                                (const uint16_t*)vc_cur, kv_stride, nsplit, part);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   attn_merge_kernel<<<dim3(T, H), hd, 0, s>>>(part, H, hd, nsplit, pos0, o_f32, (uint16_t*)o_bf16, o_stride);

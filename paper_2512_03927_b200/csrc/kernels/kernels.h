@@ -140,17 +140,18 @@ cudaError_t launch_gemv_rmsnorm(const float* h, const void* W, const float* scal
 cudaError_t launch_gemv_acc(const void* W, const float* scales, WType wt, int R, int C, const float* x, float* out,
                             cudaStream_t s, bool pdl);
 // rotate q, k of T positions pos0.. in qkv rows ([q H*hd | k Hkv*hd | v Hkv*hd], fp32, stride
-// qkv_stride); k (rotated) and v stored as bf16 rows of kv_stride elements at kc / vc (row t)
+// qkv_stride); k (rotated) and v stored as rows of kv_stride elements at kc / vc (row t), bf16 or
+// (kv_f32) fp32
 cudaError_t launch_rope_kv(float* qkv, int qkv_stride, int T, int H, int Hkv, int hd, int pos0, void* kc, void* vc,
-                           int kv_stride, cudaStream_t s);
+                           int kv_stride, int kv_f32, cudaStream_t s);
 // causal GQA attention of T queries at positions pos0..: keys/values < pos0 from *_past (rows by
 // position), >= pos0 from *_cur (row t = position pos0 + t); part: attn_part_floats(...) fp32;
 // o [T][H*hd] as fp32 and/or bf16 (either may be NULL)
 int attn_splits(int max_pos);
 cudaError_t launch_rmsnorm_rows(const float* h, int T, int d, float eps, void* x_bf16, cudaStream_t s);
 cudaError_t launch_attention(const float* q, int q_stride, int T, int H, int Hkv, int hd, int pos0, const void* kc_past,
-                             const void* vc_past, const void* kc_cur, const void* vc_cur, int kv_stride, float* part,
-                             float* o_f32, void* o_bf16, int o_stride, cudaStream_t s);
+                             const void* vc_past, const void* kc_cur, const void* vc_cur, int kv_stride, int kv_f32,
+                             float* part, float* o_f32, void* o_bf16, int o_stride, cudaStream_t s);
 
 // P2P combine over NVLink (p2p.cu): sender sums its n partials into its row of GPU 0's buffer and
 // releases `epoch` in its flag; GPU 0 waits for the flags in `mask` and sums the rows in rank order.

@@ -52,6 +52,7 @@ struct Ctx {
   // attention block (rank 0; reading Q29): fused QKV [L][(H+2Hkv)*hd][d], W_o [L][d][H*hd] in the
   // main dtype; KV cache [L][max_seq][Hkv*hd] bf16; pos = tokens already in the cache
   int H = 0, Hkv = 0, hd = 0, qkv_rows = 0, kvd = 0, max_seq = 0;
+  int kv_esz = 2;               // KV-cache element: bf16 (bf16 model) or fp32 (fp32 model)
   int64_t pos = 0;
   void* d_wqkv = nullptr;
   void* d_wo = nullptr;

@@ -252,7 +252,7 @@ void build_nonexpert(Ctx* c) {
       CUDA_OK(c, launch_gen(b + (qr + kr) * d * c->esz, 11, l, 0, kr, d, d, d, c->F, seed, c->wt, c->s_main));
       CUDA_OK(c, launch_gen((char*)c->d_wo + wo * l, 12, l, 0, d, qr, d, d, c->F, seed, c->wt, c->s_main));
     }
-    const size_t kv = (size_t)L * c->max_seq * c->kvd * 2;
+    const size_t kv = (size_t)L * c->max_seq * c->kvd * c->kv_esz;
     c->d_kc = dmalloc<char>(c, kv, "k cache");
     c->d_vc = dmalloc<char>(c, kv, "v cache");
     CUDA_OK(c, cudaMemsetAsync(c->d_kc, 0, kv, c->s_main));
@@ -266,10 +266,11 @@ void build_nonexpert(Ctx* c) {
 // alignment).
 void enqueue_attention(Ctx* c, int l, cudaStream_t s, float* h, bool shadow) {
   const int d = c->d, hq = c->H * c->hd;
-  const size_t kv_l = (size_t)l * c->max_seq * c->kvd * 2;
+  const size_t kv_l = (size_t)l * c->max_seq * c->kvd * c->kv_esz;
   char* kc = (char*)c->d_kc + kv_l;
   char* vc = (char*)c->d_vc + kv_l;
-  const size_t cur = (size_t)c->pos * c->kvd * 2;
+  const size_t cur = (size_t)c->pos * c->kvd * c->kv_esz;
+  const int kvf = c->kv_esz == 4;
   if (!shadow) {
     const size_t qkv = (size_t)c->qkv_rows * d * c->esz, wo = (size_t)d * hq * c->esz;
     { KTimer t(c, K_ATTN, s);
@@ -277,10 +278,10 @@ void enqueue_attention(Ctx* c, int l, cudaStream_t s, float* h, bool shadow) {
                                      c->cfg.rms_eps, c->d_qkv, s, true)); }
     { KTimer t(c, K_ATTN, s);
       CUDA_OK(c, launch_rope_kv(c->d_qkv, c->qkv_rows, 1, c->H, c->Hkv, c->hd, (int)c->pos, kc + cur, vc + cur,
-                                c->kvd, s)); }
+                                c->kvd, kvf, s)); }
     { KTimer t(c, K_ATTN, s);
       CUDA_OK(c, launch_attention(c->d_qkv, c->qkv_rows, 1, c->H, c->Hkv, c->hd, (int)c->pos, kc, vc, kc + cur,
-                                  vc + cur, c->kvd, c->d_attn_part, c->d_attn_o, nullptr, hq, s)); }
+                                  vc + cur, c->kvd, kvf, c->d_attn_part, c->d_attn_o, nullptr, hq, s)); }
     { KTimer t(c, K_ATTN, s);
       CUDA_OK(c, launch_gemv_acc((const char*)c->d_wo + wo * l, nullptr, c->wt, d, hq, c->d_attn_o, h, s, true)); }
     return;
@@ -293,10 +294,10 @@ void enqueue_attention(Ctx* c, int l, cudaStream_t s, float* h, bool shadow) {
                                    c->cfg.rms_eps, c->sh_qkv, s, true)); }
   { KTimer t(c, K_SHADOW, s);
     CUDA_OK(c, launch_rope_kv(c->sh_qkv, c->qkv_rows, 1, c->H, c->Hkv, c->hd, (int)c->pos, c->sh_kcur, c->sh_vcur,
-                              c->kvd, s)); }
+                              c->kvd, kvf, s)); }
   { KTimer t(c, K_SHADOW, s);
     CUDA_OK(c, launch_attention(c->sh_qkv, c->qkv_rows, 1, c->H, c->Hkv, c->hd, (int)c->pos, kc, vc, c->sh_kcur,
-                                c->sh_vcur, c->kvd, c->sh_attn_part, c->sh_attn_o, nullptr, hq, s)); }
+                                c->sh_vcur, c->kvd, kvf, c->sh_attn_part, c->sh_attn_o, nullptr, hq, s)); }
   { KTimer t(c, K_SHADOW, s);
     CUDA_OK(c, launch_gemv_acc((const char*)c->sh_wo + wo * l, same ? nullptr : c->sh_so + (size_t)l * d, c->sh_wt,
                                d, hq, c->sh_attn_o, h, s, true)); }
@@ -588,8 +589,8 @@ void build_buffers(Ctx* c) {
       c->sh_qkv = dmalloc<float>(c, c->qkv_rows, "sh qkv");
       c->sh_attn_o = dmalloc<float>(c, (size_t)c->H * c->hd, "sh attn o");
       c->sh_attn_part = dmalloc<float>(c, part, "sh attn part");
-      c->sh_kcur = dmalloc<char>(c, (size_t)c->kvd * 2, "sh kcur");
-      c->sh_vcur = dmalloc<char>(c, (size_t)c->kvd * 2, "sh vcur");
+      c->sh_kcur = dmalloc<char>(c, (size_t)c->kvd * c->kv_esz, "sh kcur");
+      c->sh_vcur = dmalloc<char>(c, (size_t)c->kvd * c->kv_esz, "sh vcur");
     }
     if (c->cfg.debug_capture) c->dbg_hpre = dmalloc<float>(c, (size_t)L * d, "dbg_hpre");
   }
@@ -1445,9 +1446,10 @@ void build_tiles(const std::vector<int32_t>& off, const std::vector<int>& mine, 
 void prefill_attention(Ctx* c, int l, int T, cudaStream_t s) {
   const int d = c->d, hq = c->H * c->hd;
   const size_t qkv_b = (size_t)c->qkv_rows * d * c->esz, wo_b = (size_t)d * hq * c->esz;
-  const size_t kv_l = (size_t)l * c->max_seq * c->kvd * 2;
+  const size_t kv_l = (size_t)l * c->max_seq * c->kvd * c->kv_esz;
   char* kc = (char*)c->d_kc + kv_l;
   char* vc = (char*)c->d_vc + kv_l;
+  const int kvf = c->kv_esz == 4;
   auto gemm = [&](const void* a, const void* w, int N, int K, float* out) {
     std::vector<int4> tiles;
     const int BM = grouped_gemm_bm(), BN = grouped_gemm_bn(1);
@@ -1463,8 +1465,8 @@ void prefill_attention(Ctx* c, int l, int T, cudaStream_t s) {
   KTimer t(c, K_ATTN, s);
   CUDA_OK(c, launch_rmsnorm_rows(c->p_h, T, d, c->cfg.rms_eps, c->pa_x, s));
   gemm(c->pa_x, (const char*)c->d_wqkv + qkv_b * l, c->qkv_rows, d, c->pa_qkv);
-  CUDA_OK(c, launch_rope_kv(c->pa_qkv, c->qkv_rows, T, c->H, c->Hkv, c->hd, 0, kc, vc, c->kvd, s));
-  CUDA_OK(c, launch_attention(c->pa_qkv, c->qkv_rows, T, c->H, c->Hkv, c->hd, 0, kc, vc, kc, vc, c->kvd, c->pa_part,
+  CUDA_OK(c, launch_rope_kv(c->pa_qkv, c->qkv_rows, T, c->H, c->Hkv, c->hd, 0, kc, vc, c->kvd, kvf, s));
+  CUDA_OK(c, launch_attention(c->pa_qkv, c->qkv_rows, T, c->H, c->Hkv, c->hd, 0, kc, vc, kc, vc, c->kvd, kvf, c->pa_part,
                               nullptr, c->pa_x, hq, s));
   gemm(c->pa_x, (const char*)c->d_wo + wo_b * l, d, hq, c->pa_out);
   CUDA_OK(c, launch_add_rows(c->p_h, c->pa_out, (long long)T * d, s));
@@ -1769,6 +1771,7 @@ odmoe_status odmoe_create(const odmoe_config* cfg, void** ctx_out) {
       c->kvd = c->Hkv * c->hd;
       c->qkv_rows = (c->H + 2 * c->Hkv) * c->hd;
       c->max_seq = cfg->max_seq > 0 ? cfg->max_seq : 4096;
+      c->kv_esz = cfg->dtype == ODMOE_FP32 ? 4 : 2;
     }
     c->built_pred = cfg->predictor;
     c->dev = cfg->device;
