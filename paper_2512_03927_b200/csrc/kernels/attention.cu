@@ -8,13 +8,13 @@
 //               output; scores q.k / sqrt(hd) in fp32 with k, v read as bf16;
 //   attn_merge: merges the splits with their log-sum-exp weights into o (fp32 or bf16).
 // Decode reads at most pos+1 rows per KV head: the work is tiny next to the weight GEMVs and is
-// latency-bound; splits of 128 positions spread it over Hkv * ceil((pos+1)/128) CTAs.
+// latency-bound; splits of 32 positions spread it over Hkv * ceil((pos+1)/32) CTAs.
 #include "common.cuh"
 #include "kernels.h"
 
 namespace odmoe {
 
-constexpr int kAttnSplit = 128;  // positions per split
+constexpr int kAttnSplit = 32;  // positions per split (one per lane in the scoring pass)
 constexpr int kMaxHd = 128;
 
 __device__ __forceinline__ float bf16_to_f(uint16_t b) { return __uint_as_float((uint32_t)b << 16); }
@@ -78,49 +78,73 @@ cudaError_t launch_rope_kv(float* qkv, int qkv_stride, int T, int H, int Hkv, in
 // K rows for positions < pos0 come from kc_past (the cache); rows >= pos0 from kc_cur
 // (the rows written by rope_kv for these queries: the cache itself for the main model, a private
 // buffer for the shadow, which reads the main model's cache for the past: KV alignment).
-template <typename KT>
-__device__ __forceinline__ float dot_row(const float* __restrict__ q, const KT* __restrict__ k, int hd);
-template <>
-__device__ __forceinline__ float dot_row<uint16_t>(const float* __restrict__ q, const uint16_t* __restrict__ k, int hd) {
+// q . k over HD (q pre-scaled, in shared memory; all of the row's loads issued at once)
+template <typename KT, int HD>
+__device__ __forceinline__ float dot_row(const float* __restrict__ q, const KT* __restrict__ k) {
   float s0 = 0.f, s1 = 0.f;
-  const uint4* k4 = reinterpret_cast<const uint4*>(k);
-#pragma unroll 4
-  for (int c = 0; c < hd / 8; ++c) {
-    const uint4 w = k4[c];
-    const float* qc = q + 8 * c;
-    s0 = fmaf(qc[0], bf16_lo(w.x), s0); s1 = fmaf(qc[1], bf16_hi(w.x), s1);
-    s0 = fmaf(qc[2], bf16_lo(w.y), s0); s1 = fmaf(qc[3], bf16_hi(w.y), s1);
-    s0 = fmaf(qc[4], bf16_lo(w.z), s0); s1 = fmaf(qc[5], bf16_hi(w.z), s1);
-    s0 = fmaf(qc[6], bf16_lo(w.w), s0); s1 = fmaf(qc[7], bf16_hi(w.w), s1);
-  }
-  return s0 + s1;
-}
-template <>
-__device__ __forceinline__ float dot_row<float>(const float* __restrict__ q, const float* __restrict__ k, int hd) {
-  float s0 = 0.f, s1 = 0.f;
-  const float4* k4 = reinterpret_cast<const float4*>(k);
-#pragma unroll 4
-  for (int c = 0; c < hd / 4; ++c) {
-    const float4 w = k4[c];
-    const float* qc = q + 4 * c;
-    s0 = fmaf(qc[0], w.x, s0); s1 = fmaf(qc[1], w.y, s1);
-    s0 = fmaf(qc[2], w.z, s0); s1 = fmaf(qc[3], w.w, s1);
+  if constexpr (std::is_same<KT, uint16_t>::value) {
+    const uint4* k4 = reinterpret_cast<const uint4*>(k);
+    uint4 w[HD / 8];
+#pragma unroll
+    for (int c = 0; c < HD / 8; ++c) w[c] = k4[c];
+#pragma unroll
+    for (int c = 0; c < HD / 8; ++c) {
+      const float* qc = q + 8 * c;
+      s0 = fmaf(qc[0], bf16_lo(w[c].x), s0); s1 = fmaf(qc[1], bf16_hi(w[c].x), s1);
+      s0 = fmaf(qc[2], bf16_lo(w[c].y), s0); s1 = fmaf(qc[3], bf16_hi(w[c].y), s1);
+      s0 = fmaf(qc[4], bf16_lo(w[c].z), s0); s1 = fmaf(qc[5], bf16_hi(w[c].z), s1);
+      s0 = fmaf(qc[6], bf16_lo(w[c].w), s0); s1 = fmaf(qc[7], bf16_hi(w[c].w), s1);
+    }
+  } else {
+    const float4* k4 = reinterpret_cast<const float4*>(k);
+    float4 w[HD / 4];
+#pragma unroll
+    for (int c = 0; c < HD / 4; ++c) w[c] = k4[c];
+#pragma unroll
+    for (int c = 0; c < HD / 4; ++c) {
+      const float* qc = q + 4 * c;
+      s0 = fmaf(qc[0], w[c].x, s0); s1 = fmaf(qc[1], w[c].y, s1);
+      s0 = fmaf(qc[2], w[c].z, s0); s1 = fmaf(qc[3], w[c].w, s1);
+    }
   }
   return s0 + s1;
 }
 
-// One warp per query head of the group: (1) lanes score different positions (each lane a whole
-// q.k over hd, many independent loads in flight), (2) softmax statistics by warp reductions,
-// (3) lanes own head dimensions and accumulate p_t v_t over the split's positions.
-template <typename KT>
+// HD/32 consecutive elements of a value row owned by one lane
+template <int PER> struct VecBf16;
+template <> struct VecBf16<1> { using T = uint16_t; };
+template <> struct VecBf16<2> { using T = uint32_t; };
+template <> struct VecBf16<4> { using T = uint2; };
+template <typename KT, int PER>
+__device__ __forceinline__ void ld_vals(const KT* p, float (&v)[PER]) {
+  if constexpr (std::is_same<KT, float>::value) {
+#pragma unroll
+    for (int j = 0; j < PER; ++j) v[j] = p[j];
+  } else if constexpr (PER == 4) {
+    const uint2 u = *reinterpret_cast<const uint2*>(p);
+    v[0] = bf16_lo(u.x); v[1] = bf16_hi(u.x); v[2] = bf16_lo(u.y); v[3] = bf16_hi(u.y);
+  } else if constexpr (PER == 2) {
+    const uint32_t u = *reinterpret_cast<const uint32_t*>(p);
+    v[0] = bf16_lo(u); v[1] = bf16_hi(u);
+  } else {
+    v[0] = bf16_to_f(*p);
+  }
+}
+
+// CTA = (kv head g, split of kAttnSplit positions, query t); one warp per query head of the group.
+// (1) each lane scores one position (its whole q.k: HD/8 16-byte loads in flight), (2) softmax
+// statistics by warp reductions, (3) lanes own HD/32 dimensions and accumulate p_t v_t with eight
+// positions' loads in flight.
+template <typename KT, int HD>
 __global__ void __launch_bounds__(32 * 8) attn_split_kernel(const float* __restrict__ q, int q_stride, int H, int Hkv,
-                                                           int hd, int pos0, const KT* __restrict__ kc_past,
+                                                           int pos0, const KT* __restrict__ kc_past,
                                                            const KT* __restrict__ vc_past,
                                                            const KT* __restrict__ kc_cur,
                                                            const KT* __restrict__ vc_cur, int kv_stride,
                                                            int nsplit, float* __restrict__ part) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  __shared__ float qs[8][kMaxHd];
+  constexpr int PER = HD / 32;
+  __shared__ float qs[8][HD];
   __shared__ float ps[8][kAttnSplit];
   const int t = blockIdx.z, g = blockIdx.x, sp = blockIdx.y;
   const int rep = H / Hkv;
@@ -130,45 +154,46 @@ __global__ void __launch_bounds__(32 * 8) attn_split_kernel(const float* __restr
   const int pos = pos0 + t;
   const int p_begin = sp * kAttnSplit;
   const int n = max(0, min(pos + 1, p_begin + kAttnSplit) - p_begin);
-  float* out = part + ((size_t)(t * H + head) * nsplit + sp) * (hd + 2);
-  const float scale = rsqrtf((float)hd);
-  const float* qh = q + (size_t)t * q_stride + head * hd;
-  for (int j = lane; j < hd; j += 32) qs[warp][j] = qh[j] * scale;
+  float* out = part + ((size_t)(t * H + head) * nsplit + sp) * (HD + 2);
+  const float scale = rsqrtf((float)HD);
+  const float* qh = q + (size_t)t * q_stride + head * HD;
+  for (int j = lane; j < HD; j += 32) qs[warp][j] = qh[j] * scale;
   __syncwarp();
-  auto krow = [&](int p) -> const KT* {
-    return (p < pos0 ? kc_past + (size_t)p * kv_stride : kc_cur + (size_t)(p - pos0) * kv_stride) + g * hd;
+  auto row = [&](const KT* past, const KT* cur, int p) -> const KT* {
+    return (p < pos0 ? past + (size_t)p * kv_stride : cur + (size_t)(p - pos0) * kv_stride) + g * HD;
   };
-  auto vrow = [&](int p) -> const KT* {
-    return (p < pos0 ? vc_past + (size_t)p * kv_stride : vc_cur + (size_t)(p - pos0) * kv_stride) + g * hd;
-  };
-  float m = -INFINITY;
-  for (int i = lane; i < n; i += 32) {
-    const float sdot = dot_row<KT>(qs[warp], krow(p_begin + i), hd);
-    ps[warp][i] = sdot;
-    m = fmaxf(m, sdot);
+  float m = -INFINITY, sdot = -INFINITY;
+  if (lane < n) {
+    sdot = dot_row<KT, HD>(qs[warp], row(kc_past, kc_cur, p_begin + lane));
+    m = sdot;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  float l = 0.f;
-  for (int i = lane; i < n; i += 32) {
-    const float w = __expf(ps[warp][i] - m);
-    ps[warp][i] = w;
-    l += w;
-  }
-  l = warp_sum(l);
+  const float w = lane < n ? __expf(sdot - m) : 0.f;
+  ps[warp][lane] = w;
+  const float l = warp_sum(w);
   __syncwarp();
-  const int per = hd / 32;
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 4
-  for (int i = 0; i < n; ++i) {
-    const float w = ps[warp][i];
-    const KT* vr = vrow(p_begin + i) + lane * per;
-    for (int j = 0; j < per; ++j) acc[j] = fmaf(w, kv_ld(vr + j), acc[j]);
+  float acc[PER];
+#pragma unroll
+  for (int j = 0; j < PER; ++j) acc[j] = 0.f;
+  for (int i0 = 0; i0 < n; i0 += 8) {
+    float v[8][PER];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (i0 + u < n) ld_vals<KT, PER>(row(vc_past, vc_cur, p_begin + i0 + u) + lane * PER, v[u]);
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (i0 + u < n) {
+        const float pw = ps[warp][i0 + u];
+#pragma unroll
+        for (int j = 0; j < PER; ++j) acc[j] = fmaf(pw, v[u][j], acc[j]);
+      }
   }
-  for (int j = 0; j < per; ++j) out[lane * per + j] = acc[j];
+#pragma unroll
+  for (int j = 0; j < PER; ++j) out[lane * PER + j] = acc[j];
   if (lane == 0) {
-    out[hd] = n > 0 ? m : -INFINITY;
-    out[hd + 1] = l;
+    out[HD] = n > 0 ? m : -INFINITY;
+    out[HD + 1] = l;
   }
 }
 
@@ -231,14 +256,21 @@ cudaError_t launch_attention(const float* q, int q_stride, int T, int H, int Hkv
   if (hd % 32 || hd > kMaxHd || H % Hkv || H / Hkv > 8 || T < 1) return cudaErrorInvalidValue;
   const int nsplit = attn_splits(pos0 + T - 1);
   const dim3 grid(Hkv, nsplit, T);
-  if (kv_f32)
-    attn_split_kernel<float><<<grid, 32 * (H / Hkv), 0, s>>>(q, q_stride, H, Hkv, hd, pos0, (const float*)kc_past,
-                                                             (const float*)vc_past, (const float*)kc_cur,
-                                                             (const float*)vc_cur, kv_stride, nsplit, part);
-  else
-    attn_split_kernel<uint16_t><<<grid, 32 * (H / Hkv), 0, s>>>(q, q_stride, H, Hkv, hd, pos0, (const uint16_t*)kc_past,
-                                                                (const uint16_t*)vc_past, (const uint16_t*)kc_cur,
-                                                                (const uint16_t*)vc_cur, kv_stride, nsplit, part);
+  const int threads = 32 * (H / Hkv);
+#define ODMOE_ATTN_LAUNCH(KT, HD)                                                                              \
+  attn_split_kernel<KT, HD><<<grid, threads, 0, s>>>(q, q_stride, H, Hkv, pos0, (const KT*)kc_past,           \
+                                                     (const KT*)vc_past, (const KT*)kc_cur, (const KT*)vc_cur, \
+                                                     kv_stride, nsplit, part)
+  if (kv_f32) {
+    if (hd == 32) ODMOE_ATTN_LAUNCH(float, 32);
+    else if (hd == 64) ODMOE_ATTN_LAUNCH(float, 64);
+    else ODMOE_ATTN_LAUNCH(float, 128);
+  } else {
+    if (hd == 32) ODMOE_ATTN_LAUNCH(uint16_t, 32);
+    else if (hd == 64) ODMOE_ATTN_LAUNCH(uint16_t, 64);
+    else ODMOE_ATTN_LAUNCH(uint16_t, 128);
+  }
+#undef ODMOE_ATTN_LAUNCH
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   attn_merge_kernel<<<dim3(T, H), hd, 0, s>>>(part, H, hd, nsplit, pos0, o_f32, (uint16_t*)o_bf16, o_stride);

@@ -1386,6 +1386,8 @@ bool prefill_mine(const Ctx* c, int l, int e) {
   return (l % c->NG) == c->my_group && e * c->G / c->E == c->my_pos;
 }
 
+constexpr int kPrefillQChunk = 256;  // prefill attention queries per launch
+
 void ensure_prefill(Ctx* c, int T) {
   const int E = c->E, k = c->k, d = c->d, F = c->F;
   if (c->pslots.empty() && !c->resident) {
@@ -1423,7 +1425,8 @@ void ensure_prefill(Ctx* c, int T) {
     F_(c->pa_x); F_(c->pa_qkv); F_(c->pa_part); F_(c->pa_out); F_(c->pa_tiles);
     c->pa_x = dmalloc<char>(c, (size_t)T * d * 2, "pa_x");
     c->pa_qkv = dmalloc<float>(c, (size_t)T * c->qkv_rows, "pa_qkv");
-    c->pa_part = dmalloc<float>(c, (size_t)T * c->H * attn_splits(T - 1) * (c->hd + 2), "pa_part");
+    c->pa_part = dmalloc<float>(c, (size_t)std::min(T, kPrefillQChunk) * c->H * attn_splits(T - 1) * (c->hd + 2),
+                                "pa_part");
     c->pa_out = dmalloc<float>(c, (size_t)T * d, "pa_out");
     c->pa_tiles = dmalloc<int4>(c, (size_t)((T + 255) / 256 + 1) * (c->qkv_rows / 128 + d / 128 + 2), "pa_tiles");
   }
@@ -1466,8 +1469,13 @@ void prefill_attention(Ctx* c, int l, int T, cudaStream_t s) {
   CUDA_OK(c, launch_rmsnorm_rows(c->p_h, T, d, c->cfg.rms_eps, c->pa_x, s));
   gemm(c->pa_x, (const char*)c->d_wqkv + qkv_b * l, c->qkv_rows, d, c->pa_qkv);
   CUDA_OK(c, launch_rope_kv(c->pa_qkv, c->qkv_rows, T, c->H, c->Hkv, c->hd, 0, kc, vc, c->kvd, kvf, s));
-  CUDA_OK(c, launch_attention(c->pa_qkv, c->qkv_rows, T, c->H, c->Hkv, c->hd, 0, kc, vc, kc, vc, c->kvd, kvf, c->pa_part,
-                              nullptr, c->pa_x, hq, s));
+  for (int t0 = 0; t0 < T; t0 += kPrefillQChunk) {  // query chunks bound the split-partial buffer
+    const int tc = std::min(kPrefillQChunk, T - t0);
+    const size_t cur = (size_t)t0 * c->kvd * c->kv_esz;
+    CUDA_OK(c, launch_attention(c->pa_qkv + (size_t)t0 * c->qkv_rows, c->qkv_rows, tc, c->H, c->Hkv, c->hd, t0, kc, vc,
+                                kc + cur, vc + cur, c->kvd, kvf, c->pa_part, nullptr,
+                                (char*)c->pa_x + (size_t)t0 * hq * 2, hq, s));
+  }
   gemm(c->pa_x, (const char*)c->d_wo + wo_b * l, d, hq, c->pa_out);
   CUDA_OK(c, launch_add_rows(c->p_h, c->pa_out, (long long)T * d, s));
   c->stats.kernel_launches += 6;
