@@ -14,7 +14,7 @@ SEED = 2512
 N_TOK = 10
 
 
-def _run_rank(rank, world, port, q, predictor, slots, lookahead, prompt, refine=0, placement=0):
+def _run_rank(rank, world, port, q, predictor, slots, lookahead, prompt, refine=0, placement=0, heads=(0, 0)):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     import torch as t
@@ -27,7 +27,8 @@ def _run_rank(rank, world, port, q, predictor, slots, lookahead, prompt, refine=
     try:
         eng = odmoe.Engine(TINY.L, TINY.E, TINY.k, TINY.d, TINY.F, TINY.V, dtype=odmoe.BF16, predictor=predictor,
                            slots_per_gpu=slots, lookahead=lookahead, weight_seed=SEED, rank=rank, world_size=world,
-                           device=rank, nccl_id=obj[0], refine_depth=refine, placement=placement)
+                           device=rank, nccl_id=obj[0], refine_depth=refine, placement=placement,
+                           n_heads=heads[0], n_kv_heads=heads[1], max_seq=128 if heads[0] else 0)
         toks, routes = [], []
         pf = None
         if prompt:
@@ -47,14 +48,14 @@ def _run_rank(rank, world, port, q, predictor, slots, lookahead, prompt, refine=
     dist.destroy_process_group()
 
 
-def _multi(world, predictor, slots=2, lookahead=1, prompt=None, refine=0, placement=0):
+def _multi(world, predictor, slots=2, lookahead=1, prompt=None, refine=0, placement=0, heads=(0, 0)):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = (29600 + world * 11 + predictor * 3 + refine * 2 + (5 if slots == -1 else 0) + 7 * placement
-            + os.getpid() % 50)
+            + 13 * (heads[0] > 0) + os.getpid() % 50)
     ps = [ctx.Process(target=_run_rank, args=(r, world, port, q, predictor, slots, lookahead, prompt, refine,
-                                              placement))
+                                              placement, heads))
           for r in range(world)]
     for p in ps:
         p.start()
@@ -66,10 +67,11 @@ def _multi(world, predictor, slots=2, lookahead=1, prompt=None, refine=0, placem
     return res
 
 
-def _single(predictor, slots=2, lookahead=1, prompt=None):
+def _single(predictor, slots=2, lookahead=1, prompt=None, heads=(0, 0)):
     from paper_2512_03927_b200 import odmoe
     eng = odmoe.Engine(TINY.L, TINY.E, TINY.k, TINY.d, TINY.F, TINY.V, dtype=odmoe.BF16, predictor=predictor,
-                       slots_per_gpu=slots, lookahead=lookahead, weight_seed=SEED)
+                       slots_per_gpu=slots, lookahead=lookahead, weight_seed=SEED, n_heads=heads[0],
+                       n_kv_heads=heads[1], max_seq=128 if heads[0] else 0)
     pf = eng.prefill(prompt) if prompt else None
     toks, routes, t_ = [], [], 9
     for _ in range(N_TOK):
@@ -130,3 +132,22 @@ def test_multi_gpu_sliced_placement(world):
     res = _multi(world, odmoe.PRED_NONE, slots=-1, placement=odmoe.PLACE_SLICED)   # resident, sliced
     for r in res:
         assert r[2] == base_toks
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_multi_gpu_attention(world):
+    """Attention block (rank 0, the main node) at N GPUs: prefill + decode tokens equal the 1-GPU
+    run for the paper's groups (bitwise path) and the sliced placement (within fp32 rounding)."""
+    t = torch()
+    if t.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    from paper_2512_03927_b200 import odmoe
+    heads = (4, 2)
+    prompt = [int(x) for x in gen_prompt(TINY, 9, 20)]
+    base_toks, _, base_pf = _single(odmoe.PRED_NONE, prompt=prompt, heads=heads)
+    for placement, pred, refine in ((0, odmoe.PRED_SHADOW_INT8, 2), (1, odmoe.PRED_SHADOW_INT8, 1)):
+        res = _multi(world, pred, slots=4, lookahead=1, prompt=prompt, refine=refine, placement=placement,
+                     heads=heads)
+        for r in res:
+            assert r[2] == base_toks, (world, placement, r[0])
+            assert r[4] == base_pf, (world, placement, r[0])
