@@ -78,6 +78,11 @@ struct Ctx {
   float* sh_attn_part = nullptr;
   void* sh_kcur = nullptr;
   void* sh_vcur = nullptr;
+  // KV alignment (Fig. 3 "KV1"): 1 = the shadow attends over the MAIN model's cache;
+  // 0 ("KV0") = the shadow keeps its own cache, filled by its own token-aligned passes
+  int kv_align = 1;
+  void* sh_kc = nullptr;
+  void* sh_vc = nullptr;
 
   // shadow model (rank 0)
   bool has_shadow = false;

@@ -264,7 +264,7 @@ void build_nonexpert(Ctx* c) {
 // Main model: its weights, k/v of this position written into the cache. Shadow: int8-row weights,
 // this position's k/v in a private buffer, earlier positions from the MAIN model's cache (KV
 // alignment).
-void enqueue_attention(Ctx* c, int l, cudaStream_t s, float* h, bool shadow) {
+void enqueue_attention(Ctx* c, int l, cudaStream_t s, float* h, bool shadow, bool mode_a = false) {
   const int d = c->d, hq = c->H * c->hd;
   const size_t kv_l = (size_t)l * c->max_seq * c->kvd * c->kv_esz;
   char* kc = (char*)c->d_kc + kv_l;
@@ -288,16 +288,28 @@ void enqueue_attention(Ctx* c, int l, cudaStream_t s, float* h, bool shadow) {
   }
   const bool same = c->sh_wt != W_I8;  // SHADOW_SAME: the main weights
   const size_t qkv = (size_t)c->qkv_rows * d * (same ? c->esz : 1), wo = (size_t)d * hq * (same ? c->esz : 1);
+  // KV0: past positions from the shadow's own cache; its token-aligned pass (Mode A) appends this
+  // position there, the refinement passes use the private buffer
+  void* kcur = c->sh_kcur;
+  void* vcur = c->sh_vcur;
+  if (!c->kv_align) {
+    kc = (char*)c->sh_kc + kv_l;
+    vc = (char*)c->sh_vc + kv_l;
+    if (mode_a) {
+      kcur = kc + cur;
+      vcur = vc + cur;
+    }
+  }
   { KTimer t(c, K_SHADOW, s);
     CUDA_OK(c, launch_gemv_rmsnorm(h, (const char*)c->sh_wqkv + qkv * l,
                                    same ? nullptr : c->sh_sqkv + (size_t)l * c->qkv_rows, c->sh_wt, c->qkv_rows, d,
                                    c->cfg.rms_eps, c->sh_qkv, s, true)); }
   { KTimer t(c, K_SHADOW, s);
-    CUDA_OK(c, launch_rope_kv(c->sh_qkv, c->qkv_rows, 1, c->H, c->Hkv, c->hd, (int)c->pos, c->sh_kcur, c->sh_vcur,
+    CUDA_OK(c, launch_rope_kv(c->sh_qkv, c->qkv_rows, 1, c->H, c->Hkv, c->hd, (int)c->pos, kcur, vcur,
                               c->kvd, kvf, s)); }
   { KTimer t(c, K_SHADOW, s);
-    CUDA_OK(c, launch_attention(c->sh_qkv, c->qkv_rows, 1, c->H, c->Hkv, c->hd, (int)c->pos, kc, vc, c->sh_kcur,
-                                c->sh_vcur, c->kvd, kvf, c->sh_attn_part, c->sh_attn_o, nullptr, hq, s)); }
+    CUDA_OK(c, launch_attention(c->sh_qkv, c->qkv_rows, 1, c->H, c->Hkv, c->hd, (int)c->pos, kc, vc, kcur,
+                                vcur, c->kvd, kvf, c->sh_attn_part, c->sh_attn_o, nullptr, hq, s)); }
   { KTimer t(c, K_SHADOW, s);
     CUDA_OK(c, launch_gemv_acc((const char*)c->sh_wo + wo * l, same ? nullptr : c->sh_so + (size_t)l * d, c->sh_wt,
                                d, hq, c->sh_attn_o, h, s, true)); }
@@ -628,7 +640,7 @@ void enqueue_shadow(Ctx* c, const int32_t* token_dev) {
     if (c->H > 0) {  // the shadow's own attention block (past keys/values from the main cache)
       if (n_add > 0) CUDA_OK(c, launch_combine(c->sh_h, c->sh_yptr, n_add, d, s));
       n_add = 0;
-      enqueue_attention(c, l, s, c->sh_h, true);
+      enqueue_attention(c, l, s, c->sh_h, true, true);
     }
     {
       KTimer t(c, K_SHADOW, s);
@@ -1633,6 +1645,14 @@ void prefill_impl(Ctx* c, const int32_t* tokens, int T, int32_t* token_out, int3
   CUDA_OK(c, cudaStreamSynchronize(s));
   if (c->h_flag[0]) fail(c, ODMOE_E_NONFINITE, "non-finite router logits");
   if (c->H > 0) c->pos = T;
+  if (c->H > 0 && c->sh_kc) {  // KV0 shadow: it shares the prompt's keys/values once, then keeps its own
+    const size_t row = (size_t)c->kvd * c->kv_esz, layer = (size_t)c->max_seq * row;
+    for (int l = 0; l < L; ++l) {
+      CUDA_OK(c, cudaMemcpyAsync((char*)c->sh_kc + l * layer, (char*)c->d_kc + l * layer, row * T, cudaMemcpyDeviceToDevice, s));
+      CUDA_OK(c, cudaMemcpyAsync((char*)c->sh_vc + l * layer, (char*)c->d_vc + l * layer, row * T, cudaMemcpyDeviceToDevice, s));
+    }
+    CUDA_OK(c, cudaStreamSynchronize(s));
+  }
   if (c->cfg.time_kernels) harvest_timers(c);
   c->stats.bytes_h2d = c->loader.bytes_h2d.load();
   c->stats.loads_issued = c->loader.loads_issued.load();
@@ -1660,7 +1680,7 @@ void destroy_ctx(Ctx* c) {
   F(c->d_emb); F(c->d_lm); F(c->d_router);
   F(c->d_wqkv); F(c->d_wo); F(c->d_kc); F(c->d_vc); F(c->d_qkv); F(c->d_attn_o); F(c->d_attn_part); F(c->dbg_hpre);
   F(c->sh_qkv); F(c->sh_attn_o); F(c->sh_attn_part); F(c->sh_kcur); F(c->sh_vcur);
-  F(c->pa_x); F(c->pa_qkv); F(c->pa_part); F(c->pa_out); F(c->pa_tiles);
+  F(c->pa_x); F(c->pa_qkv); F(c->pa_part); F(c->pa_out); F(c->pa_tiles); F(c->sh_kc); F(c->sh_vc);
   if (c->built_pred != ODMOE_PRED_SHADOW_SAME) {
     F(c->sh_wqkv); F(c->sh_sqkv); F(c->sh_wo); F(c->sh_so);
     F(c->sh_emb); F(c->sh_semb); F(c->sh_router); F(c->sh_srouter);
@@ -1902,6 +1922,17 @@ odmoe_status odmoe_set_option(void* ctx, int key, int64_t value) {
       if (value > 0 && (c->ev_ref.empty() || c->wt != W_BF16))
         fail(c, ODMOE_E_STATE, "refinement needs a bf16 ctx created with a shadow predictor");
       c->cfg.refine_depth = (int32_t)value;
+    } else if (key == 5) {
+      if (value != 0 && value != 1) fail(c, ODMOE_E_CONFIG, "kv_align is 0 or 1");
+      if (c->H == 0 || !c->has_shadow) fail(c, ODMOE_E_STATE, "kv_align needs an attention ctx with a shadow");
+      if (value == 0 && !c->sh_kc) {  // the shadow's own cache (zero: nothing seen yet)
+        const size_t kv = (size_t)c->L * c->max_seq * c->kvd * c->kv_esz;
+        c->sh_kc = dmalloc<char>(c, kv, "shadow k cache");
+        c->sh_vc = dmalloc<char>(c, kv, "shadow v cache");
+        CUDA_OK(c, cudaMemset(c->sh_kc, 0, kv));
+        CUDA_OK(c, cudaMemset(c->sh_vc, 0, kv));
+      }
+      c->kv_align = (int)value;
     } else if (key == 4) {
       if (value < 0 || value >= c->max_seq || c->H == 0) fail(c, ODMOE_E_RANGE, "position outside the KV cache");
       c->pos = value;

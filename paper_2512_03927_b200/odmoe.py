@@ -348,6 +348,10 @@ class Engine:
     def set_refine_depth(self, R: int):
         self._ck(_set_option(self.ctx, 3, int(R)))
 
+    def set_kv_align(self, on: bool):
+        """Attention + shadow ctx: 1 = the shadow reads the main model's KV cache (KV1), 0 = its own (KV0)."""
+        self._ck(_set_option(self.ctx, 5, int(bool(on))))
+
     def set_position(self, pos: int):
         """Attention ctx: KV-cache position of the next decode step (0 = new sequence)."""
         self._ck(_set_option(self.ctx, 4, int(pos)))

@@ -29,6 +29,8 @@ def main():
     ap.add_argument("--predictors", default="shadow_int8,perfect,gate_reuse,none,random")
     ap.add_argument("--slots", type=int, default=0, help="0 => 2 (groups) or 2k (sliced)")
     ap.add_argument("--placement", default="groups", choices=["groups", "sliced"])
+    ap.add_argument("--attention", action="store_true", help="Mixtral attention block (32/8 heads) + 512-token prefill")
+    ap.add_argument("--kv-align", default="1", help="comma list of shadow KV alignment (1 = main cache, 0 = own)")
     ap.add_argument("--refine", default="0", help="comma list of SEP refinement depths (shadow predictor only)")
     ap.add_argument("--out", default="")
     ap.add_argument("--build-predictor", default="shadow_int8",
@@ -51,19 +53,31 @@ def main():
     eng = odmoe.Engine(device=local, rank=rank, world_size=world, nccl_id=uid,
                        predictor=odmoe.PREDICTORS[args.build_predictor],
                        slots_per_gpu=args.slots or (4 if args.placement == "sliced" and world > 1 else 2),
-                       lookahead=1, weight_seed=2512, placement=int(args.placement == "sliced"), **SHAPE)
+                       lookahead=1, weight_seed=2512, placement=int(args.placement == "sliced"), **SHAPE,
+                       **(dict(n_heads=32, n_kv_heads=8, max_seq=2048) if args.attention else {}))
     lines = []
     combos = []
+    aligns = [int(x) for x in args.kv_align.split(",")] if args.attention else [1]
     for pname in args.predictors.split(","):
         for D in [int(x) for x in args.lookaheads.split(",")]:
             for R in ([int(x) for x in args.refine.split(",")] if pname.startswith("shadow") else [0]):
-                combos.append((pname, D, R))
-    for pname, D, R in combos:
+                for A in (aligns if pname.startswith("shadow") else [1]):
+                    combos.append((pname, D, R, A))
+    prompt = None
+    if args.attention:
+        from inputs import MIXTRAL, gen_prompt
+        prompt = [int(x) for x in gen_prompt(MIXTRAL, 1, 512)]
+    for pname, D, R, A in combos:
         if True:
             eng.set_predictor(odmoe.PREDICTORS[pname])
             eng.set_lookahead(D)
             eng.set_refine_depth(R)
-            tok = 1
+            if args.attention:
+                if pname.startswith("shadow"):
+                    eng.set_kv_align(A)
+                tok, _ = eng.prefill(prompt)  # same context for every configuration
+            else:
+                tok = 1
             for _ in range(args.warmup):
                 tok, _ = eng.decode_step(tok, records=False)
             eng.reset_stats()
@@ -93,7 +107,8 @@ def main():
                 recb = st["refine_correct"] / st["refine_total"] if st["refine_total"] else None
                 if pname.startswith("shadow"):
                     pname = args.build_predictor
-                line = {"n_gpus": world, "placement": args.placement, "predictor": pname, "lookahead": D, "refine_depth": R,
+                line = {"n_gpus": world, "placement": args.placement, "attention": args.attention,
+                        "kv_align": A, "predictor": pname, "lookahead": D, "refine_depth": R,
                         "recall_refined": recb, "refine_corrections_per_token": st["refine_corrections"] / args.steps,
                         "tok_s": args.steps / s,
                         "ms_per_token": s / args.steps * 1e3, "recall_eq3": rec,
