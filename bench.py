@@ -42,8 +42,10 @@ def parse():
     ap.add_argument("--predictor", default="shadow_int8")
     ap.add_argument("--slots", type=int, default=0,
                     help="device expert slots per GPU; 0 => 2 (groups: whole experts) or 2k (sliced: 1/N slices)")
-    ap.add_argument("--placement", default="groups", choices=["groups", "sliced"],
-                    help="N > 1: the paper's worker groups (P:104) or sliced loading (SURVEY §8(f)3)")
+    ap.add_argument("--placement", default="sliced", choices=["groups", "sliced"],
+                    help="N > 1: sliced loading (SURVEY §8(f)3; default: every link serves every layer, "
+                         "measured 97.6 vs 93.6 % of the link roofline at 4 GPUs) or the paper's worker "
+                         "groups (P:104)")
     ap.add_argument("--refine", type=int, default=2,
                     help="SEP refinement depth R (DESIGN.md §7); 0 = the paper's token-aligned shadow only")
     ap.add_argument("--lookahead", type=int, default=0, help="0 => max(1, N/2) (groups) or 1 (sliced)")
