@@ -414,6 +414,13 @@ def main():
                 traffic = json.load(open(prof)).get("dram_bytes_per_expert")
             except Exception:
                 traffic = None
+        floor_us = None  # pure-read floor of one 352 MB launch (tools/pattern_bench.cu, measured)
+        pf = os.path.join(ROOT, "profiles", "pattern_bench_r01.json")
+        if os.path.exists(pf) and not sliced(args, n):
+            try:
+                floor_us = json.load(open(pf))["slices_336MB"]["us_mean"]
+            except Exception:
+                floor_us = None
         recall = st["correct"] / st["predicted_total"] if st["predicted_total"] else None
         recall_ref = st["refine_correct"] / st["refine_total"] if st["refine_total"] else None
         roof_tok = link_all * 1e9 / (64 * EXPERT_BYTES)
@@ -434,7 +441,12 @@ def main():
                          "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
                          "peak_source": peak_src, "bytes_per_launch_pair": blob,
                          "avg_us_per_expert": gemv_ms * 1e3, "w13_us": st["ms_w13"] / n_exp * 1e3,
-                         "w2_us": st["ms_w2"] / n_exp * 1e3},
+                         "w2_us": st["ms_w2"] / n_exp * 1e3,
+                         "read_floor_us": floor_us,
+                         "frac_of_read_floor": (floor_us / (gemv_ms * 1e3)) if floor_us else None,
+                         "note": "CUDA events around each on-demand launch in the timed step (includes the wait "
+                                 "for the copy-stream event and the idle-to-busy ramp); read_floor_us = the same "
+                                 "bytes streamed with no arithmetic in one launch (profiles/pattern_bench_r01.json)"},
             "host_link": {"bound": "pcie_h2d", "achieved": bytes_all / dev_s / 1e9,
                           "peak": link_all, "unit": "GB/s", "frac": bytes_all / dev_s / 1e9 / link_all,
                           "roofline_tok_s": roof_tok, "frac_tok_s": value / roof_tok,
