@@ -14,6 +14,8 @@
 #include <cuda_fp8.h>
 
 #include <cstdlib>
+#include <map>
+#include <mutex>
 
 namespace odmoe {
 
@@ -893,13 +895,25 @@ flat_experts_kernel(const __grid_constant__ MultiArgs m, unsigned int* counter, 
 }
 
 // Grid-barrier arrival counter of this device (one per device; see fused_launch).
-static unsigned int g_epochs[64] = {0};
-static unsigned int* g_counters[64] = {nullptr};
-static cudaError_t barrier_counter(int dev) {
-  if (g_counters[dev]) return cudaSuccess;
-  cudaError_t e = cudaMalloc(&g_counters[dev], sizeof(unsigned int));
-  if (e != cudaSuccess) return e;
-  return cudaMemset(g_counters[dev], 0, sizeof(unsigned int));
+// One arrival counter per (device, stream): launches on one stream are ordered, so their targets
+// can simply keep growing; two streams (e.g. two engines in one process) never share a counter.
+struct BarrierState {
+  unsigned int* counter = nullptr;
+  unsigned int epoch = 0;
+};
+static std::mutex g_barrier_mu;
+static std::map<std::pair<int, cudaStream_t>, BarrierState> g_barriers;
+static cudaError_t barrier_counter(int dev, cudaStream_t s, BarrierState*& out) {
+  std::lock_guard<std::mutex> lk(g_barrier_mu);
+  BarrierState& b = g_barriers[{dev, s}];
+  if (!b.counter) {
+    cudaError_t e = cudaMalloc(&b.counter, sizeof(unsigned int));
+    if (e != cudaSuccess) return e;
+    e = cudaMemset(b.counter, 0, sizeof(unsigned int));
+    if (e != cudaSuccess) return e;
+  }
+  out = &b;
+  return cudaSuccess;
 }
 
 template <typename WT, typename XT>
@@ -907,7 +921,8 @@ static cudaError_t multi_launch(MultiArgs m, cudaStream_t s, bool pdl) {
   constexpr int UNROLL = kFG_UNROLL;
   int dev = 0;
   cudaGetDevice(&dev);
-  cudaError_t e = barrier_counter(dev);
+  BarrierState* bs = nullptr;
+  cudaError_t e = barrier_counter(dev, s, bs);
   if (e != cudaSuccess) return e;
   static int ef = -1;
   if (ef < 0) {
@@ -938,7 +953,7 @@ static cudaError_t multi_launch(MultiArgs m, cudaStream_t s, bool pdl) {
                        : (n == 3 ? flat_experts_kernel<WT, XT, UNROLL, 3> : flat_experts_kernel<WT, XT, UNROLL, 4>));
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const unsigned int target = g_epochs[dev] + (unsigned int)grid;
+  const unsigned int target = bs->epoch + (unsigned int)grid;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kFG_THREADS);
@@ -951,8 +966,8 @@ static cudaError_t multi_launch(MultiArgs m, cudaStream_t s, bool pdl) {
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 2 : 1;
-  e = cudaLaunchKernelEx(&cfg, kern, m, g_counters[dev], target);
-  if (e == cudaSuccess) g_epochs[dev] = target;
+  e = cudaLaunchKernelEx(&cfg, kern, m, bs->counter, target);
+  if (e == cudaSuccess) bs->epoch = target;
   return e;
 }
 
@@ -986,8 +1001,9 @@ static cudaError_t fused_launch(FlatArgs a13, FlatArgs a2, cudaStream_t s, bool 
   constexpr int UNROLL = kFG_UNROLL;
   int dev = 0;
   cudaGetDevice(&dev);
+  BarrierState* bs = nullptr;
   {
-    cudaError_t e = barrier_counter(dev);
+    cudaError_t e = barrier_counter(dev, s, bs);
     if (e != cudaSuccess) return e;
   }
   static int ef = -1;
@@ -1010,10 +1026,10 @@ static cudaError_t fused_launch(FlatArgs a13, FlatArgs a2, cudaStream_t s, bool 
   auto kern = flat_expert_kernel<WT, XT, UNROLL>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  // Stream-ordered launches on this device use increasing barrier targets. Only ONE stream may
-  // run these kernels (the engine's compute stream): two cooperative kernels spinning on barriers
-  // on different streams could hold each other's SMs.
-  const unsigned int target = g_epochs[dev] + (unsigned int)grid;
+  // Stream-ordered launches use increasing barrier targets on their stream's own counter; a
+  // cooperative grid becomes resident only as a whole, so grids of two streams serialise instead
+  // of holding each other's SMs.
+  const unsigned int target = bs->epoch + (unsigned int)grid;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kFG_THREADS);
@@ -1026,8 +1042,8 @@ static cudaError_t fused_launch(FlatArgs a13, FlatArgs a2, cudaStream_t s, bool 
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 2 : 1;
-  e = cudaLaunchKernelEx(&cfg, kern, a13, a2, g_counters[dev], target);
-  if (e == cudaSuccess) g_epochs[dev] = target;
+  e = cudaLaunchKernelEx(&cfg, kern, a13, a2, bs->counter, target);
+  if (e == cudaSuccess) bs->epoch = target;
   return e;
 }
 
