@@ -15,6 +15,23 @@
 namespace odmoe {
 
 constexpr int kAttnSplit = 32;  // positions per split (one per lane in the scoring pass)
+
+// Programmatic dependent launch for the small kernels of the block: each waits for its predecessor
+// (griddepcontrol.wait) and lets its successor's launch start right away (launch_dependents), so the
+// chain QKV -> RoPE -> split -> merge -> W_o pays one launch latency instead of five.
+template <typename K, typename... Args>
+static cudaError_t pdl_launch(K kern, dim3 grid, dim3 block, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
 constexpr int kMaxHd = 128;
 
 __device__ __forceinline__ float bf16_to_f(uint16_t b) { return __uint_as_float((uint32_t)b << 16); }
@@ -32,6 +49,7 @@ template <typename KT>
 __global__ void rope_kv_kernel(float* __restrict__ qkv, int qkv_stride, int H, int Hkv, int hd, int pos0,
                                KT* __restrict__ kc, KT* __restrict__ vc, int kv_stride, float log2_theta) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int t = blockIdx.x, head = blockIdx.y, i = threadIdx.x, half = hd / 2;
   const int pos = pos0 + t;
   float* row = qkv + (size_t)t * qkv_stride;
@@ -65,12 +83,10 @@ cudaError_t launch_rope_kv(float* qkv, int qkv_stride, int T, int H, int Hkv, in
   if (hd % 2 || hd > kMaxHd || T < 1) return cudaErrorInvalidValue;
   const float lt = (float)19.931568569324174;  // log2(1e6)
   if (kv_f32)
-    rope_kv_kernel<float><<<dim3(T, H + Hkv), hd / 2, 0, s>>>(qkv, qkv_stride, H, Hkv, hd, pos0, (float*)kc, (float*)vc,
-                                                              kv_stride, lt);
-  else
-    rope_kv_kernel<uint16_t><<<dim3(T, H + Hkv), hd / 2, 0, s>>>(qkv, qkv_stride, H, Hkv, hd, pos0, (uint16_t*)kc,
-                                                                 (uint16_t*)vc, kv_stride, lt);
-  return cudaGetLastError();
+    return pdl_launch(rope_kv_kernel<float>, dim3(T, H + Hkv), dim3(hd / 2), s, qkv, qkv_stride, H, Hkv, hd, pos0,
+                      (float*)kc, (float*)vc, kv_stride, lt);
+  return pdl_launch(rope_kv_kernel<uint16_t>, dim3(T, H + Hkv), dim3(hd / 2), s, qkv, qkv_stride, H, Hkv, hd, pos0,
+                    (uint16_t*)kc, (uint16_t*)vc, kv_stride, lt);
 }
 
 // Partials: part[((t * H + head) * nsplit + s) * (hd + 2)] = {o[0..hd), m, l}.
@@ -143,6 +159,7 @@ __global__ void __launch_bounds__(32 * 8) attn_split_kernel(const float* __restr
                                                            const KT* __restrict__ vc_cur, int kv_stride,
                                                            int nsplit, float* __restrict__ part) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   constexpr int PER = HD / 32;
   __shared__ float qs[8][HD];
   __shared__ float ps[8][kAttnSplit];
@@ -200,6 +217,8 @@ __global__ void __launch_bounds__(32 * 8) attn_split_kernel(const float* __restr
 // o[t][head*hd + i] = sum_s e^{m_s - M} acc_s[i] / sum_s e^{m_s - M} l_s; grid (T, H), block hd.
 __global__ void attn_merge_kernel(const float* __restrict__ part, int H, int hd, int nsplit, int pos0,
                                   float* __restrict__ o_f32, uint16_t* __restrict__ o_bf16, int o_stride) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int t = blockIdx.x, head = blockIdx.y, i = threadIdx.x;
   const int used = (pos0 + t) / kAttnSplit + 1;  // splits that saw at least one position
   const float* p0 = part + (size_t)(t * H + head) * nsplit * (hd + 2);
@@ -257,10 +276,10 @@ cudaError_t launch_attention(const float* q, int q_stride, int T, int H, int Hkv
   const int nsplit = attn_splits(pos0 + T - 1);
   const dim3 grid(Hkv, nsplit, T);
   const int threads = 32 * (H / Hkv);
-#define ODMOE_ATTN_LAUNCH(KT, HD)                                                                              \
-  attn_split_kernel<KT, HD><<<grid, threads, 0, s>>>(q, q_stride, H, Hkv, pos0, (const KT*)kc_past,           \
-                                                     (const KT*)vc_past, (const KT*)kc_cur, (const KT*)vc_cur, \
-                                                     kv_stride, nsplit, part)
+  cudaError_t e = cudaSuccess;
+#define ODMOE_ATTN_LAUNCH(KT, HD)                                                                         \
+  e = pdl_launch(attn_split_kernel<KT, HD>, grid, dim3(threads), s, q, q_stride, H, Hkv, pos0, (const KT*)kc_past, \
+                 (const KT*)vc_past, (const KT*)kc_cur, (const KT*)vc_cur, kv_stride, nsplit, part)
   if (kv_f32) {
     if (hd == 32) ODMOE_ATTN_LAUNCH(float, 32);
     else if (hd == 64) ODMOE_ATTN_LAUNCH(float, 64);
@@ -271,10 +290,9 @@ cudaError_t launch_attention(const float* q, int q_stride, int T, int H, int Hkv
     else ODMOE_ATTN_LAUNCH(uint16_t, 128);
   }
 #undef ODMOE_ATTN_LAUNCH
-  cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  attn_merge_kernel<<<dim3(T, H), hd, 0, s>>>(part, H, hd, nsplit, pos0, o_f32, (uint16_t*)o_bf16, o_stride);
-  return cudaGetLastError();
+  return pdl_launch(attn_merge_kernel, dim3(T, H), dim3(hd), s, (const float*)part, H, hd, nsplit, pos0, o_f32,
+                    (uint16_t*)o_bf16, o_stride);
 }
 
 }  // namespace odmoe

@@ -181,6 +181,7 @@ __global__ void __launch_bounds__(kRouterThreads) router_kernel(
 
 // Residual combine only (after the last layer): h += (y_0 + y_1 + ...), same order as the router.
 __global__ void combine_kernel(float* __restrict__ h, const float* const* __restrict__ y_add, int n_add, int d) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the next kernel may prefetch its weights
   for (int j = (blockIdx.x * blockDim.x + threadIdx.x) * 4; j < d; j += gridDim.x * blockDim.x * 4) {
     float4 hv = *reinterpret_cast<const float4*>(h + j);
     float4 s = *reinterpret_cast<const float4*>(y_add[0] + j);
