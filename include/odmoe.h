@@ -338,10 +338,12 @@ odmoe_status odmoe_prefill_debug_read(const void* ctx, int what, int layer, void
 
 /* Parity capture (cfg.debug_capture == 1), rank 0, last decode step. Copies `bytes` bytes of
  * field `what` for `layer` into host `dst`. Fields and sizes:
- *   0 H_IN fp32[d]  1 U dt[d]  2 LOGITS fp32[E]  3 IDS int32[k]  4 W fp32[k]
+ *   0 H_IN fp32[d] (the MoE input: after the attention block when n_heads > 0)  1 U dt[d]
+ *   2 LOGITS fp32[E]  3 IDS int32[k]  4 W fp32[k]
  *   5 Y fp32[d] (combined)  6 Y_PART fp32[k][d] (N=1: per selected expert, rank order)
  *   7 SH_H_IN fp32[d]  8 SH_U bf16[d]  9 SH_LOGITS fp32[E]  10 SH_IDS int32[k]
- *   11 H_FINAL fp32[d] (layer ignored)  12 LM_LOGITS fp32[V] (layer ignored) */
+ *   11 H_FINAL fp32[d] (layer ignored)  12 LM_LOGITS fp32[V] (layer ignored)
+ *   13 H_PRE fp32[d] (n_heads > 0: h before the attention block of the layer) */
 odmoe_status odmoe_debug_read(const void* ctx, int what, int layer, void* dst, int64_t bytes);
 
 /* Device pointers of ctx-owned tensors (tests): 0 emb, 1 lm_head, 2 router[layer],
