@@ -329,7 +329,7 @@ def main():
     t_create = time.time()
     refine = args.refine if args.predictor.startswith("shadow") else 0
     eng = odmoe.Engine(device=local, rank=rank, world_size=world, nccl_id=uid, predictor=pred,
-                       slots_per_gpu=n_slots(args, n), lookahead=D, time_kernels=1, weight_seed=SEED,
+                       slots_per_gpu=n_slots(args, n), lookahead=D, time_kernels=2, weight_seed=SEED,
                        refine_depth=refine, placement=int(sliced(args, n)), **SHAPE, **attn_kw(args))
     if args.attention and args.prefill <= 0:
         eng.set_position(args.context)  # no prompt: decode over a zero-filled synthetic context

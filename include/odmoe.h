@@ -98,7 +98,9 @@ typedef struct {
   int32_t device;            /* CUDA device ordinal of this rank                                       */
   int64_t chunk_bytes;       /* H2D copy chunk (0 => 32 MiB)                                            */
   int32_t debug_capture;     /* 1 => keep every per-layer intermediate on the host (parity tests)      */
-  int32_t time_kernels;      /* 1 => CUDA events around every kernel (bench roofline)                  */
+  int32_t time_kernels;      /* CUDA events around kernels: 1 => expert FFN launches only (the roofline
+                                kernel; keeps the PDL chains of the other kernels intact), 2 => every
+                                kernel family (per-family stats)                                        */
   int32_t pool_threads;      /* host threads used to build the pool (0 => all)                         */
   int32_t refine_depth;      /* R >= 0: SEP refinement ("Mode B"): after the main router of
                                 layer l the shadow re-runs layers l..l+R-1 from the main model's exact

@@ -94,7 +94,7 @@ cudaError_t launch_rope_kv(float* qkv, int qkv_stride, int T, int H, int Hkv, in
 // K rows for positions < pos0 come from kc_past (the cache); rows >= pos0 from kc_cur
 // (the rows written by rope_kv for these queries: the cache itself for the main model, a private
 // buffer for the shadow, which reads the main model's cache for the past: KV alignment).
-// q . k over HD (q pre-scaled, in shared memory; all of the row's loads issued at once)
+// q . k over HD (q pre-scaled; both operands in shared memory)
 template <typename KT, int HD>
 __device__ __forceinline__ float dot_row(const float* __restrict__ q, const KT* __restrict__ k) {
   float s0 = 0.f, s1 = 0.f;
@@ -127,10 +127,6 @@ __device__ __forceinline__ float dot_row(const float* __restrict__ q, const KT* 
 }
 
 // HD/32 consecutive elements of a value row owned by one lane
-template <int PER> struct VecBf16;
-template <> struct VecBf16<1> { using T = uint16_t; };
-template <> struct VecBf16<2> { using T = uint32_t; };
-template <> struct VecBf16<4> { using T = uint2; };
 template <typename KT, int PER>
 __device__ __forceinline__ void ld_vals(const KT* p, float (&v)[PER]) {
   if constexpr (std::is_same<KT, float>::value) {
@@ -148,9 +144,11 @@ __device__ __forceinline__ void ld_vals(const KT* p, float (&v)[PER]) {
 }
 
 // CTA = (kv head g, split of kAttnSplit positions, query t); one warp per query head of the group.
-// (1) each lane scores one position (its whole q.k: HD/8 16-byte loads in flight), (2) softmax
-// statistics by warp reductions, (3) lanes own HD/32 dimensions and accumulate p_t v_t with eight
-// positions' loads in flight.
+// The split's key and value rows of head g (32 x HD each) are staged into shared memory with
+// cp.async first -- every load in flight at once, shared by the group's query heads -- then
+// (1) each lane scores one position, (2) softmax statistics by warp reductions, (3) lanes own HD/32
+// dimensions and accumulate p_t v_t from shared memory. Rows are padded by 16 B so a warp reading
+// 32 different rows at the same offset hits distinct banks.
 template <typename KT, int HD>
 __global__ void __launch_bounds__(32 * 8) attn_split_kernel(const float* __restrict__ q, int q_stride, int H, int Hkv,
                                                            int pos0, const KT* __restrict__ kc_past,
@@ -158,30 +156,49 @@ __global__ void __launch_bounds__(32 * 8) attn_split_kernel(const float* __restr
                                                            const KT* __restrict__ kc_cur,
                                                            const KT* __restrict__ vc_cur, int kv_stride,
                                                            int nsplit, float* __restrict__ part) {
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   constexpr int PER = HD / 32;
+  constexpr int ROWB = HD * (int)sizeof(KT) + 16;      // padded row bytes in shared memory
+  constexpr int CH = HD * (int)sizeof(KT) / 16;        // 16-byte chunks per row
   __shared__ float qs[8][HD];
   __shared__ float ps[8][kAttnSplit];
+  __shared__ __align__(16) uint8_t ks[kAttnSplit * ROWB];
+  __shared__ __align__(16) uint8_t vs[kAttnSplit * ROWB];
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int t = blockIdx.z, g = blockIdx.x, sp = blockIdx.y;
   const int rep = H / Hkv;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (warp >= rep) return;
-  const int head = g * rep + warp;
   const int pos = pos0 + t;
   const int p_begin = sp * kAttnSplit;
   const int n = max(0, min(pos + 1, p_begin + kAttnSplit) - p_begin);
-  float* out = part + ((size_t)(t * H + head) * nsplit + sp) * (HD + 2);
-  const float scale = rsqrtf((float)HD);
-  const float* qh = q + (size_t)t * q_stride + head * HD;
-  for (int j = lane; j < HD; j += 32) qs[warp][j] = qh[j] * scale;
-  __syncwarp();
   auto row = [&](const KT* past, const KT* cur, int p) -> const KT* {
     return (p < pos0 ? past + (size_t)p * kv_stride : cur + (size_t)(p - pos0) * kv_stride) + g * HD;
   };
+  // stage K and V rows of this split (all threads of the CTA)
+  for (int i = threadIdx.x; i < n * CH; i += blockDim.x) {
+    const int r = i / CH, c = i - r * CH;
+    const uint32_t dk = (uint32_t)__cvta_generic_to_shared(ks + r * ROWB + c * 16);
+    const uint32_t dv = (uint32_t)__cvta_generic_to_shared(vs + r * ROWB + c * 16);
+    const char* sk = reinterpret_cast<const char*>(row(kc_past, kc_cur, p_begin + r)) + c * 16;
+    const char* sv = reinterpret_cast<const char*>(row(vc_past, vc_cur, p_begin + r)) + c * 16;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dk), "l"(sk) : "memory");
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dv), "l"(sv) : "memory");
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  const bool active = warp < rep;
+  const int head = g * rep + (active ? warp : 0);
+  const float scale = rsqrtf((float)HD);
+  if (active) {
+    const float* qh = q + (size_t)t * q_stride + head * HD;
+    for (int j = lane; j < HD; j += 32) qs[warp][j] = qh[j] * scale;
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  if (!active) return;
+  float* out = part + ((size_t)(t * H + head) * nsplit + sp) * (HD + 2);
   float m = -INFINITY, sdot = -INFINITY;
   if (lane < n) {
-    sdot = dot_row<KT, HD>(qs[warp], row(kc_past, kc_cur, p_begin + lane));
+    sdot = dot_row<KT, HD>(qs[warp], reinterpret_cast<const KT*>(ks + lane * ROWB));
     m = sdot;
   }
 #pragma unroll
@@ -193,18 +210,12 @@ __global__ void __launch_bounds__(32 * 8) attn_split_kernel(const float* __restr
   float acc[PER];
 #pragma unroll
   for (int j = 0; j < PER; ++j) acc[j] = 0.f;
-  for (int i0 = 0; i0 < n; i0 += 8) {
-    float v[8][PER];
+  for (int u = 0; u < n; ++u) {
+    const float pw = ps[warp][u];
+    float v[PER];
+    ld_vals<KT, PER>(reinterpret_cast<const KT*>(vs + u * ROWB) + lane * PER, v);
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (i0 + u < n) ld_vals<KT, PER>(row(vc_past, vc_cur, p_begin + i0 + u) + lane * PER, v[u]);
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (i0 + u < n) {
-        const float pw = ps[warp][i0 + u];
-#pragma unroll
-        for (int j = 0; j < PER; ++j) acc[j] = fmaf(pw, v[u][j], acc[j]);
-      }
+    for (int j = 0; j < PER; ++j) acc[j] = fmaf(pw, v[j], acc[j]);
   }
 #pragma unroll
   for (int j = 0; j < PER; ++j) out[lane * PER + j] = acc[j];
