@@ -916,6 +916,16 @@ static cudaError_t barrier_counter(int dev, cudaStream_t s, BarrierState*& out) 
   return cudaSuccess;
 }
 
+unsigned int* barrier_capture_reset(cudaStream_t s) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  BarrierState* bs = nullptr;
+  if (barrier_counter(dev, s, bs) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lk(g_barrier_mu);
+  bs->epoch = 0;
+  return bs->counter;
+}
+
 template <typename WT, typename XT>
 static cudaError_t multi_launch(MultiArgs m, cudaStream_t s, bool pdl) {
   constexpr int UNROLL = kFG_UNROLL;

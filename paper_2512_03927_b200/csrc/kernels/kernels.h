@@ -59,6 +59,9 @@ cudaError_t launch_w2_flat(ExpertRef ex, WType wt, const float* act, const float
 cudaError_t launch_lm_head_flat(const float* h, const void* W, WType wt, int V, int d, float eps,
                                 int32_t* token_out, float* logits, void* scratch, cudaStream_t s, bool pdl);
 bool use_fused_expert();  // env ODMOE_FUSED=0 disables (A/B)
+// Graph capture of cooperative kernels: restart the grid-barrier targets of stream s at 0 and return
+// its arrival counter (the captured step memsets it to 0 first, so every replay sees the same targets).
+unsigned int* barrier_capture_reset(cudaStream_t s);
 // NF4 / FP8 rows shorter than one flat group: warp-per-row kernel (x: bf16 unless x_f32; W2 x = fp32)
 cudaError_t launch_lowbit_small(ExpertRef ex, WType wt, int second, const void* x, int x_f32, int d, int F,
                                 const float* gate_w, float* out, cudaStream_t s);

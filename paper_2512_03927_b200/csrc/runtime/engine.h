@@ -192,7 +192,10 @@ struct Ctx {
   int32_t predict_cache_token = -1;
 
   // kernel timing (time_kernels)
-  struct Timed { int fam; cudaEvent_t a, b; int units; };  // units: experts covered by one launch
+  struct Timed { int fam; cudaEvent_t a, b; int units; bool graph = false; };  // units: experts per launch
+  cudaGraphExec_t graph_exec = nullptr;  // fully-resident 1-GPU step (captured once, replayed)
+  int64_t graph_launches = 0;
+  std::vector<Timed> graph_timers;
   std::vector<Timed> timed;
   std::vector<cudaEvent_t> tev_pool;
 

@@ -112,7 +112,7 @@ struct KTimer {
   ~KTimer() {
     if (!a) return;
     cudaEventRecord(b, s);
-    c->timed.push_back(Ctx::Timed{fam, a, b, units});
+    c->timed.push_back(Ctx::Timed{fam, a, b, units, false});
   }
   cudaEvent_t get() {
     if (!c->tev_pool.empty()) {
@@ -140,8 +140,10 @@ void harvest_timers(Ctx* c) {
         case K_ATTN: c->stats.ms_attn += ms; c->stats.n_attn++; break;
       }
     }
-    c->tev_pool.push_back(t.a);
-    c->tev_pool.push_back(t.b);
+    if (!t.graph) {  // graph-owned events stay with the graph
+      c->tev_pool.push_back(t.a);
+      c->tev_pool.push_back(t.b);
+    }
   }
   c->timed.clear();
 }
@@ -995,6 +997,15 @@ uint32_t p2p_mask(const Ctx* c, int l) {
 }
 
 // ------------------------------------------------------------------ one decode step
+bool graph_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ODMOE_GRAPH");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_record* rec) {
   const int L = c->L, E = c->E, k = c->k, d = c->d, F = c->F;
   if (token_in < 0 || token_in >= c->V) fail(c, ODMOE_E_RANGE, "token out of range");
@@ -1013,11 +1024,28 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
   const bool fused = use_fused_expert() && stream_ok(c->wt, d) && stream_ok(c->wt, c->Fs) &&
                      (c->world == 1 || c->resident);
 
+  // Fully-resident 1-GPU steps (no attention, no debug capture) are the same sequence of launches
+  // every token: the second step is captured into a CUDA graph (token H2D ... token D2H) and later
+  // steps replay it -- one launch per token instead of ~200 (ODMOE_GRAPH=0 disables).
+  const bool graphable = c->resident && c->world == 1 && c->H == 0 && !c->cfg.debug_capture && graph_enabled();
+  const bool replay = graphable && c->graph_exec != nullptr;
+  const bool capture = graphable && !replay && c->step >= 1;
+  const int64_t launches0 = c->stats.kernel_launches;
+  const size_t timers0 = c->timed.size();
+  if (capture) {
+    unsigned int* counter = barrier_capture_reset(s);  // grid-barrier targets restart at 0 in every replay
+    if (!counter) fail(c, ODMOE_E_CUDA, "barrier counter");
+    CUDA_OK(c, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    CUDA_OK(c, cudaMemsetAsync(counter, 0, sizeof(unsigned int), s));
+  }
+
   // token in (pinned -> device); the previous step's shadow must be done with d_tok_in
   c->h_tok[0] = token_in;
-  CUDA_OK(c, cudaStreamWaitEvent(s, c->ev_shadow_done, 0));
-  CUDA_OK(c, cudaMemcpyAsync(c->d_tok_in, c->h_tok, 4, cudaMemcpyHostToDevice, s));
-  CUDA_OK(c, cudaEventRecord(c->ev_tok, s));
+  if (!replay) {
+    if (!c->resident) CUDA_OK(c, cudaStreamWaitEvent(s, c->ev_shadow_done, 0));
+    CUDA_OK(c, cudaMemcpyAsync(c->d_tok_in, c->h_tok, 4, cudaMemcpyHostToDevice, s));
+    if (!c->resident) CUDA_OK(c, cudaEventRecord(c->ev_tok, s));
+  }
 
   // predictions for this step
   std::fill(c->pred_ready.begin(), c->pred_ready.end(), 0);
@@ -1060,13 +1088,14 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
   c->l_cur = 0;
   pump(c);
 
+  std::vector<int32_t> true_ids((size_t)L * k);
+  if (!replay) {
   // embedding (rank 0)
   if (r0) {
     KTimer t(c, K_EMBED, s);
     CUDA_OK(c, launch_embed(c->d_emb, nullptr, c->wt, c->d_tok_in, d, c->d_h, s));
   }
 
-  std::vector<int32_t> true_ids((size_t)L * k);
   const float* const* yadd = c->world == 1 ? c->d_yptr : c->d_yredptr;
   int n_add = 0;
   for (int l = 0; l < L; ++l) {
@@ -1280,6 +1309,23 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
   if (c->resident && r0) {
     for (int l = 0; l < L; ++l)
       CUDA_OK(c, cudaMemcpyAsync(c->h_ids + (size_t)l * k, c->d_pkt + (size_t)l * c->pkt_bytes + c->pkt_ids_off, 4 * k, cudaMemcpyDeviceToHost, s));
+  }
+  }  // !replay
+  if (capture) {
+    cudaGraph_t graph = nullptr;
+    CUDA_OK(c, cudaStreamEndCapture(s, &graph));
+    const cudaError_t ie = cudaGraphInstantiate(&c->graph_exec, graph, 0);
+    cudaGraphDestroy(graph);
+    CUDA_OK(c, ie);
+    c->graph_launches = c->stats.kernel_launches - launches0;
+    c->graph_timers.assign(c->timed.begin() + timers0, c->timed.end());  // events owned by the graph
+    for (auto& t : c->graph_timers) t.graph = true;
+    c->timed.resize(timers0);
+  }
+  if (capture || replay) {
+    CUDA_OK(c, cudaGraphLaunch(c->graph_exec, s));
+    if (replay) c->stats.kernel_launches += c->graph_launches;
+    c->timed.insert(c->timed.end(), c->graph_timers.begin(), c->graph_timers.end());
   }
   CUDA_OK(c, cudaStreamSynchronize(s));
   if (!c->resident && (shadow_pred || gate_reuse) && (r0 || c->world > 1)) CUDA_OK(c, cudaStreamSynchronize(c->s_shadow));
@@ -1722,6 +1768,11 @@ void destroy_ctx(Ctx* c) {
   for (auto e : {c->ev_ids, c->ev_tok, c->ev_shadow_done, c->ev_step}) if (e) cudaEventDestroy(e);
   for (auto& t : c->timed) { c->tev_pool.push_back(t.a); c->tev_pool.push_back(t.b); }
   for (auto e : c->tev_pool) cudaEventDestroy(e);
+  if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
+  for (auto& t : c->graph_timers) {
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
   if (c->rank != 0) {
     if (c->p2p_part) cudaIpcCloseMemHandle(c->p2p_part);
     if (c->p2p_flag) cudaIpcCloseMemHandle(c->p2p_flag);
