@@ -107,12 +107,20 @@ struct KTimer {
     if (!c->cfg.time_kernels || (c->cfg.time_kernels == 1 && fam != K_W13 && fam != K_W2)) return;
     a = get();
     b = get();
-    cudaEventRecord(a, s);
+    record(a);
   }
   ~KTimer() {
     if (!a) return;
-    cudaEventRecord(b, s);
+    record(b);
     c->timed.push_back(Ctx::Timed{fam, a, b, units, false});
+  }
+  // inside a stream capture a plain record is only a dependency marker; External makes it a
+  // timestamp node of the graph
+  void record(cudaEvent_t e) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &st);
+    if (st == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+    else cudaEventRecord(e, s);
   }
   cudaEvent_t get() {
     if (!c->tev_pool.empty()) {
