@@ -406,7 +406,7 @@ def main():
         n_exp = max(1, st["n_w13"])
         gemv_ms = (st["ms_w13"] + st["ms_w2"]) / n_exp
         blob = EXPERT_BYTES // n if sliced(args, n) else EXPERT_BYTES   # bytes one launch pair streams
-        achieved = blob / (gemv_ms * 1e-3) / 1e9
+        achieved = blob / (gemv_ms * 1e-3) / 1e9 if gemv_ms > 0 else None
         traffic = None
         prof = os.path.join(ROOT, "profiles", "ncu_expert_gemv_r01.json")
         if os.path.exists(prof):
@@ -438,12 +438,12 @@ def main():
                            "(refine_depth, DESIGN.md §7), which drive the loads when enabled",
             "roofline": {"bound": "hbm", "kernel": "expert SwiGLU GEMV (W13+SwiGLU, W2+gate)",
                          "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                         "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                         "frac": achieved / peaks["hbm_gbs"] if achieved else None, "traffic": traffic,
                          "peak_source": peak_src, "bytes_per_launch_pair": blob,
                          "avg_us_per_expert": gemv_ms * 1e3, "w13_us": st["ms_w13"] / n_exp * 1e3,
                          "w2_us": st["ms_w2"] / n_exp * 1e3,
                          "read_floor_us": floor_us,
-                         "frac_of_read_floor": (floor_us / (gemv_ms * 1e3)) if floor_us else None,
+                         "frac_of_read_floor": (floor_us / (gemv_ms * 1e3)) if (floor_us and gemv_ms > 0) else None,
                          "note": "CUDA events around each on-demand launch in the timed step (includes the wait "
                                  "for the copy-stream event and the idle-to-busy ramp); read_floor_us = the same "
                                  "bytes streamed with no arithmetic in one launch (profiles/pattern_bench_r01.json)"},
@@ -488,7 +488,9 @@ def main():
             # (back-to-back launches with PDL; no idle-to-busy ramp per expert)
             line["roofline_resident"] = {"bound": "hbm", "kernel": line["roofline"]["kernel"],
                                          "achieved": res["expert_gemv_GBps"], "peak": peaks["hbm_gbs"],
-                                         "unit": "GB/s", "frac": res["expert_gemv_GBps"] / peaks["hbm_gbs"],
+                                         "unit": "GB/s",
+                                         "frac": (res["expert_gemv_GBps"] / peaks["hbm_gbs"]
+                                                  if res["expert_gemv_GBps"] else None),
                                          "traffic": traffic, "avg_us_per_expert": res["expert_gemv_us"]}
         if not args.no_cpu_baseline and n == 1:
             log(rank, "cpu baseline (oracle sample)")
@@ -548,7 +550,8 @@ def resident_baseline(odmoe, torch, args, dev, rank, world, dist):
     gemv_ms = (st["ms_w13"] + st["ms_w2"]) / n_exp
     blob = EXPERT_BYTES // world if sliced(args, world) else EXPERT_BYTES
     return {"value": args.steps / s, "unit": UNIT, "ms_per_step": s / args.steps * 1e3,
-            "expert_gemv_us": gemv_ms * 1e3, "expert_gemv_GBps": blob / (gemv_ms * 1e-3) / 1e9,
+            "expert_gemv_us": gemv_ms * 1e3,
+            "expert_gemv_GBps": blob / (gemv_ms * 1e-3) / 1e9 if gemv_ms > 0 else None,
             "resident_expert_bytes_per_gpu": st["resident_bytes"],
             "hbm_roofline_tok_s_1gpu": 6541.5e9 / (64 * EXPERT_BYTES + SHAPE["V"] * SHAPE["d"] * 2)}
 
