@@ -307,7 +307,8 @@ odmoe_status odmoe_evict(void* ctx, int layer, int expert);
  *   only with a shadow predictor); key 4 = KV-cache position of the next decode step (attention
  *   ctx only; 0 starts a new sequence; E_RANGE outside [0, max_seq)); key 5 = KV alignment of the
  *   shadow (Fig. 3: 1 = attend over the main model's cache (default), 0 = the shadow keeps
- *   its own cache from its own passes; attention ctx with a shadow). E_CONFIG on a bad key/value. */
+ *   its own cache from its own passes; attention ctx with a shadow); key 6 = time_kernels level (0..2,
+ *   see odmoe_config). E_CONFIG on a bad key/value. */
 odmoe_status odmoe_set_option(void* ctx, int key, int64_t value);
 
 /* SEP Mode A (Q10): run the shadow from the main model's token `token`

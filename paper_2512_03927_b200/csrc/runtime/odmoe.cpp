@@ -1994,6 +1994,20 @@ odmoe_status odmoe_set_option(void* ctx, int key, int64_t value) {
         CUDA_OK(c, cudaMemset(c->sh_vc, 0, kv));
       }
       c->kv_align = (int)value;
+    } else if (key == 6) {
+      if (value < 0 || value > 2) fail(c, ODMOE_E_CONFIG, "time_kernels is 0, 1 or 2");
+      CUDA_OK(c, cudaStreamSynchronize(c->s_main));
+      if (c->cfg.time_kernels) harvest_timers(c);
+      c->cfg.time_kernels = (int32_t)value;
+      if (c->graph_exec) {  // its timestamp nodes follow the old level: capture again
+        cudaGraphExecDestroy(c->graph_exec);
+        c->graph_exec = nullptr;
+        for (auto& t : c->graph_timers) {
+          cudaEventDestroy(t.a);
+          cudaEventDestroy(t.b);
+        }
+        c->graph_timers.clear();
+      }
     } else if (key == 4) {
       if (value < 0 || value >= c->max_seq || c->H == 0) fail(c, ODMOE_E_RANGE, "position outside the KV cache");
       c->pos = value;

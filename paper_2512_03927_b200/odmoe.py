@@ -352,6 +352,10 @@ class Engine:
         """Attention + shadow ctx: 1 = the shadow reads the main model's KV cache (KV1), 0 = its own (KV0)."""
         self._ck(_set_option(self.ctx, 5, int(bool(on))))
 
+    def set_time_kernels(self, level: int):
+        """0 = no CUDA events, 1 = around the expert launches, 2 = around every kernel family."""
+        self._ck(_set_option(self.ctx, 6, int(level)))
+
     def set_position(self, pos: int):
         """Attention ctx: KV-cache position of the next decode step (0 = new sequence)."""
         self._ck(_set_option(self.ctx, 4, int(pos)))
