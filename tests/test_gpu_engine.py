@@ -433,3 +433,24 @@ def test_lowbit_shadow_predictor(od, dims, fmt):
     en.close()
     assert toks == toksn
     print(fmt, "shadow recall", dims, st["correct"] / st["predicted_total"])
+
+
+def test_resident_graph_replay_and_timer_levels(od):
+    """The fully-resident 1-GPU step is captured into a CUDA graph on its second call and replayed;
+    switching the timer level drops and recaptures it. Tokens equal the on-demand run throughout,
+    and level 1 times exactly the expert launches (k per layer)."""
+    first = 11
+    ref_eng, ref, _, _ = _run(od, TINY, 10, first, predictor=od.PRED_NONE, slots_per_gpu=2)
+    ref_eng.close()
+    eng = engine(od, TINY, predictor=od.PRED_NONE, slots_per_gpu=-1, time_kernels=1)
+    t, toks = first, []
+    for i in range(10):
+        if i == 5:
+            st = eng.stats()
+            assert st["n_w13"] == 5 * TINY.L * TINY.k and st["n_router"] == 0  # level 1: experts only
+            eng.set_time_kernels(2)
+        t, _ = eng.decode_step(t)
+        toks.append(t)
+    assert toks == ref
+    assert eng.stats()["n_router"] > 0                                      # level 2: every family
+    eng.close()
