@@ -26,6 +26,11 @@ constexpr int kFG_WARPS = FG_WARPS;
 #ifndef FG_NO_F32X2
 #define FG_F32X2 1  // packed fp32x2 FMA/ADD (sm_100 FFMA2/FADD2) in the bf16-x and INT8 dot products
 #endif
+#ifndef FG_SLOW
+#define FG_FAST 1  // branch-free consume of whole batches (at most one row boundary per batch)
+#else
+#define FG_FAST 0
+#endif
 #ifndef FG_PIPE
 #define FG_PIPE 0  // register pipeline variant (0: 2 batches, load-then-consume; 1: 2 batches
                    // prefetched before the wait; 2: 3 batches of UNROLL 6), see profiles/kbench_r01_*
@@ -465,6 +470,38 @@ __device__ __forceinline__ void flat_phase(const FlatArgs& a, uint8_t* sm, const
   float acc = 0.f;
   // consume one register batch (rows are whole groups: a boundary is one compare)
   auto consume = [&](const uint4 (&wv)[UNROLL], const float (&sv)[UNROLL], long long g0) {
+#if FG_FAST
+    // Fast path: a whole batch inside the slice of a row at least UNROLL groups long crosses at
+    // most one row boundary. Granules before it add to acc, the rest to acc1 (predicated adds, no
+    // branch per granule); the order of every row's sum is the one of the general path below.
+    if (Gr >= UNROLL && g0 + UNROLL <= g_end) {
+      const int b = Gr - gcol;  // granules left in the current row (>= 1)
+      const uint4* x0 = reinterpret_cast<const uint4*>(xs) + lane;
+      float acc1 = 0.f;
+#pragma unroll
+      for (int i = 0; i < UNROLL; ++i) {
+        const int c = gcol + i < Gr ? gcol + i : gcol + i - Gr;
+        const uint4* xp = x0 + (size_t)c * Q * 32;
+        if constexpr (kNF4) {
+          const float t = nf4_dot(wv[i], xp, lut_l, XT{});
+          if (i < b) acc = fmaf(sv[i], t, acc); else acc1 = fmaf(sv[i], t, acc1);
+        } else {
+          const float t = FDot<WT, XT>::run(wv[i], xp);
+          if (i < b) acc += t; else acc1 += t;
+        }
+      }
+      if (b <= UNROLL) {  // the row completed inside this batch
+        const float t = warp_sum(acc);
+        if (lane == 0) part[warp * a.rows_cap + row] += t;
+        acc = acc1;
+        ++row;
+        gcol = UNROLL - b;
+      } else {
+        gcol += UNROLL;
+      }
+      return;
+    }
+#endif
 #pragma unroll
     for (int i = 0; i < UNROLL; ++i) {
       if (g0 + i < g_end) {
@@ -1004,6 +1041,132 @@ cudaError_t launch_experts_fused(int n, const ExpertRef* ex, const void* const* 
     case W_F32: return multi_launch<float, float>(m, s, pdl);
     default: return cudaErrorInvalidValue;
   }
+}
+
+// One phase (MODE 0: W13+SwiGLU, MODE 1: W2+gate) of the NE experts of one layer in ONE
+// non-cooperative launch (the shadow's k experts). Every CTA takes the one-expert
+// kernel's row range of each expert in turn, so each expert's sums are those of its own launch
+// (bitwise), and one launch + ramp + tail is paid per phase instead of per expert. No grid barrier:
+// it may share the GPU with the compute stream's cooperative grid.
+template <typename WT, typename XT, int MODE, int UNROLL, int NE>
+__global__ void __launch_bounds__(kFG_THREADS, 1) flat_gemv_multi_kernel(const __grid_constant__ MultiArgs m) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  long long r0, r1;
+  if (MODE == 0) {
+    split_range(m.a13[0].R / 2, gridDim.x, blockIdx.x, r0, r1);
+    r0 *= 2; r1 *= 2;
+  } else {
+    split_range(m.a2[0].R, gridDim.x, blockIdx.x, r0, r1);
+  }
+  flat_phase<WT, XT, MODE, UNROLL>(MODE == 0 ? m.a13[0] : m.a2[0], sm, PdlWait{}, false, r0, r1);
+#pragma unroll
+  for (int e = 1; e < NE; ++e) {
+    __syncthreads();
+    flat_phase<WT, XT, MODE, UNROLL>(MODE == 0 ? m.a13[e] : m.a2[e], sm, NoWait{}, true, r0, r1);
+  }
+}
+
+template <typename WT, typename XT, int MODE>
+static cudaError_t fg_multi_launch(MultiArgs m, cudaStream_t s, bool pdl) {
+  constexpr int UNROLL = kFG_UNROLL;
+  static int ef = -1;
+  if (ef < 0) {
+    const char* e = getenv("ODMOE_L2_EVICT_FIRST");
+    ef = (e && e[0] == '0') ? 0 : 1;
+  }
+  FlatArgs* as = MODE == 0 ? m.a13 : m.a2;
+  if (!flat_row_ok<WT>(as[0].C)) return cudaErrorInvalidValue;
+  const int sms = num_sms();
+  const long long units = MODE == 0 ? as[0].R / 2 : as[0].R;   // fg_launch's grid and rows_cap
+  const int grid = (int)(units < sms ? (units > 0 ? units : 1) : sms);
+  const int cap = (int)((units + grid - 1) / grid) * (MODE == 0 ? 2 : 1) + 2;
+  for (int i = 0; i < m.n; ++i) {
+    as[i].evict_first = ef;
+    as[i].rows_cap = cap;
+  }
+  const size_t smem = (size_t)kFG_WARPS * cap * sizeof(float) + (size_t)as[0].C * sizeof(XT) + 16 +
+                      (FTraits<WT>::nf4 ? kNF4LutWords * 4 : 0);
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  void (*kern)(const MultiArgs) =
+      m.n == 1 ? flat_gemv_multi_kernel<WT, XT, MODE, UNROLL, 1>
+               : (m.n == 2 ? flat_gemv_multi_kernel<WT, XT, MODE, UNROLL, 2>
+                           : (m.n == 3 ? flat_gemv_multi_kernel<WT, XT, MODE, UNROLL, 3>
+                                       : flat_gemv_multi_kernel<WT, XT, MODE, UNROLL, 4>));
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kFG_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, m);
+}
+
+// the shapes on which launch_w13 / launch_w2 take the flat engine (same decision, same kernels)
+bool multi_flat_ok(int n, WType wt, int d, int F) {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("ODMOE_MULTI");  // ODMOE_MULTI=0: one launch per expert (A/B)
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on && n >= 1 && n <= kMaxMulti && gemv_engine() == 2 && stream_ok(wt, d) && stream_ok(wt, F);
+}
+
+cudaError_t launch_w13_multi(int n, const ExpertRef* ex, WType wt, const void* u, int u_f32, float* a_buf, int d,
+                             int F, cudaStream_t s, bool pdl) {
+  if (!multi_flat_ok(n, wt, d, F)) {  // small shapes / other engines: one launch per expert
+    for (int i = 0; i < n; ++i) {
+      const cudaError_t e = launch_w13(ex[i], wt, u, u_f32, a_buf + (size_t)i * F, d, F, s, pdl);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
+  MultiArgs m{};
+  m.n = n;
+  for (int i = 0; i < n; ++i) {
+    FlatArgs& a = m.a13[i];
+    a.ex = ex[i]; a.second = 0; a.x = u; a.x_bf16 = !u_f32; a.R = 2 * F; a.C = d; a.out = a_buf + (size_t)i * F;
+    a.d_full = d; a.F_full = F;
+  }
+  switch (wt) {
+    case W_BF16: return fg_multi_launch<__nv_bfloat16, uint16_t, 0>(m, s, pdl);
+    case W_F32: return fg_multi_launch<float, float, 0>(m, s, pdl);
+    case W_I8: return lowbit_xf32() ? fg_multi_launch<int8_t, float, 0>(m, s, pdl) : fg_multi_launch<int8_t, uint16_t, 0>(m, s, pdl);
+    case W_NF4: return fg_multi_launch<nf4x2, uint16_t, 0>(m, s, pdl);
+    case W_F8: return lowbit_xf32() ? fg_multi_launch<fp8e4, float, 0>(m, s, pdl) : fg_multi_launch<fp8e4, uint16_t, 0>(m, s, pdl);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_w2_multi(int n, const ExpertRef* ex, WType wt, const float* a_buf, const float* gate_w, float* y_buf,
+                            int d, int F, cudaStream_t s, bool pdl) {
+  if (!multi_flat_ok(n, wt, d, F)) {
+    for (int i = 0; i < n; ++i) {
+      const cudaError_t e = launch_w2(ex[i], wt, a_buf + (size_t)i * F, gate_w, y_buf + (size_t)i * d, d, F, s, pdl);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
+  MultiArgs m{};
+  m.n = n;
+  for (int i = 0; i < n; ++i) {
+    FlatArgs& a = m.a2[i];
+    a.ex = ex[i]; a.second = 1; a.x = a_buf + (size_t)i * F; a.x_bf16 = 0; a.R = d; a.C = F; a.gate_w = gate_w;
+    a.out = y_buf + (size_t)i * d; a.d_full = d; a.F_full = F;
+  }
+  switch (wt) {
+    case W_BF16: return fg_multi_launch<__nv_bfloat16, float, 1>(m, s, pdl);
+    case W_F32: return fg_multi_launch<float, float, 1>(m, s, pdl);
+    case W_I8: return fg_multi_launch<int8_t, float, 1>(m, s, pdl);
+    case W_NF4: return fg_multi_launch<nf4x2, float, 1>(m, s, pdl);
+    case W_F8: return fg_multi_launch<fp8e4, float, 1>(m, s, pdl);
+  }
+  return cudaErrorInvalidValue;
 }
 
 template <typename WT, typename XT>

@@ -78,6 +78,14 @@ cudaError_t launch_quantize_nf4(const void* w, int64_t R, int64_t C, WType wt, u
 cudaError_t launch_experts_fused(int n, const ExpertRef* ex, const void* const* w2_direct, const float* const* s2_direct,
                                  WType wt, const void* u, int u_f32, float* a_buf, const float* gate_w,
                                  float* const* y, int d, int F, cudaStream_t s, bool pdl);
+// The n (<= 4) experts of one layer, one phase per launch, not cooperative (the shadow's k experts):
+// W13+SwiGLU of all -> a_buf [n][F]; W2+gate of all -> y_buf [n][d]. Each expert's result is bitwise
+// that of launch_w13 / launch_w2; shapes the flat engine does not take fall back to those launches.
+bool multi_flat_ok(int n, WType wt, int d, int F);  // one launch per phase for these shapes
+cudaError_t launch_w13_multi(int n, const ExpertRef* ex, WType wt, const void* u, int u_f32, float* a_buf, int d,
+                             int F, cudaStream_t s, bool pdl);
+cudaError_t launch_w2_multi(int n, const ExpertRef* ex, WType wt, const float* a_buf, const float* gate_w, float* y_buf,
+                            int d, int F, cudaStream_t s, bool pdl);
 cudaError_t launch_expert_fused(ExpertRef ex, const void* w2_direct, const float* s2_direct, WType wt,
                                 const void* u, int u_f32, float* a_buf, const float* gate_w, float* y, int d,
                                 int F, cudaStream_t s, bool pdl);

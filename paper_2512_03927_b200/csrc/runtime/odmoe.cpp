@@ -633,12 +633,24 @@ void build_buffers(Ctx* c) {
   }
 }
 
+// The shadow's k experts of one layer (a8 on the quantised weights): W13+SwiGLU of all k in one
+// launch, W2+gate of all k in a second one (launch_w13_multi / launch_w2_multi; bitwise the
+// per-expert launches). a: [k][F] scratch, y: [k][d] gate-weighted outputs.
+void shadow_experts(Ctx* c, const ExpertRef* ex, const void* u, int u_f32, float* a, const float* gate_w, float* y,
+                    bool pdl_first, cudaStream_t s) {
+  const int k = c->k, d = c->d, F = c->F;
+  // shapes the flat engine does not take run one launch per expert (count them all)
+  if (!multi_flat_ok(k, c->sh_ewt, d, F)) c->stats.kernel_launches += 2 * (k - 1);
+  { KTimer t(c, K_SHADOW, s, k); CUDA_OK(c, launch_w13_multi(k, ex, c->sh_ewt, u, u_f32, a, d, F, s, pdl_first)); }
+  { KTimer t(c, K_SHADOW, s, k); CUDA_OK(c, launch_w2_multi(k, ex, c->sh_ewt, a, gate_w, y, d, F, s, true)); }
+}
+
 // ------------------------------------------------------------------ shadow forward (SEP, Mode A)
 // Enqueue the shadow pass for `token_dev` on s_shadow: embed, then L x [router, k expert FFNs]
 // with the shadow's own routing chosen on the device (Q10). Predictions land
 // in sh_ids [L][k]; at N = 1 each layer's ids are copied to h_pred with event ev_pred[l].
 void enqueue_shadow(Ctx* c, const int32_t* token_dev) {
-  const int L = c->L, E = c->E, k = c->k, d = c->d, F = c->F;
+  const int L = c->L, E = c->E, k = c->k, d = c->d;
   cudaStream_t s = c->s_shadow;
   const WType swt = c->sh_wt;
   const bool same = swt != W_I8;  // no row scales (main-dtype or BF16 shadow)
@@ -671,18 +683,11 @@ void enqueue_shadow(Ctx* c, const int32_t* token_dev) {
       CUDA_OK(c, cudaEventRecord(c->ev_pred[l], s));
     }
     const int u_f32 = swt == W_F32;
-    for (int j = 0; j < k; ++j) {
-      ExpertRef ex{nullptr, nullptr, (const void* const*)c->d_sh_tbl, (const float* const*)c->d_sh_stbl,
-                   c->sh_ids + (size_t)l * k, j, l * E, k, 0};
-      {
-        KTimer t(c, K_SHADOW, s);
-        CUDA_OK(c, launch_w13(ex, c->sh_ewt, c->sh_u, u_f32, c->sh_a + (size_t)j * F, d, F, s, true));
-      }
-      {
-        KTimer t(c, K_SHADOW, s);
-        CUDA_OK(c, launch_w2(ex, c->sh_ewt, c->sh_a + (size_t)j * F, c->sh_w + (size_t)l * k, c->sh_y + (size_t)j * d, d, F, s, true));
-      }
-    }
+    std::vector<ExpertRef> ex(k);
+    for (int j = 0; j < k; ++j)
+      ex[j] = ExpertRef{nullptr, nullptr, (const void* const*)c->d_sh_tbl, (const float* const*)c->d_sh_stbl,
+                        c->sh_ids + (size_t)l * k, j, l * E, k, 0};
+    shadow_experts(c, ex.data(), c->sh_u, u_f32, c->sh_a, c->sh_w + (size_t)l * k, c->sh_y, true, s);
   }
   CUDA_OK(c, cudaEventRecord(c->ev_shadow_done, s));
 }
@@ -769,7 +774,7 @@ void enqueue_gate_reuse(Ctx* c, int j) {
 
 void enqueue_refine(Ctx* c, int j) {
   if (c->cfg.predictor == ODMOE_PRED_GATE_REUSE) return enqueue_gate_reuse(c, j);
-  const int L = c->L, E = c->E, k = c->k, d = c->d, F = c->F, R = c->R;
+  const int L = c->L, E = c->E, k = c->k, d = c->d, R = c->R;
   cudaStream_t s = c->s_shadow;
   const WType swt = c->sh_wt;
   const size_t sesz = swt == W_I8 ? 1 : (swt == W_BF16 ? 2 : 4);
@@ -780,12 +785,11 @@ void enqueue_refine(Ctx* c, int j) {
   CUDA_OK(c, cudaMemcpyAsync(c->rf_h, c->h_hist + (size_t)j * d, sizeof(float) * d, cudaMemcpyDeviceToDevice, s));
   CUDA_OK(c, cudaMemsetAsync(out, 0xff, sizeof(int32_t) * 4 * k, s));
   // layer j with the main's u_j and true ids
-  for (int i = 0; i < k; ++i) {
-    ExpertRef ex{nullptr, nullptr, (const void* const*)c->d_sh_tbl, (const float* const*)c->d_sh_stbl,
-                 (const int32_t*)(pkt + c->pkt_ids_off), i, j * E, k, 0};
-    { KTimer t(c, K_SHADOW, s); CUDA_OK(c, launch_w13(ex, c->sh_ewt, pkt, 0, c->rf_a + (size_t)i * F, d, F, s)); }
-    { KTimer t(c, K_SHADOW, s); CUDA_OK(c, launch_w2(ex, c->sh_ewt, c->rf_a + (size_t)i * F, (const float*)(pkt + c->pkt_w_off), c->rf_y + (size_t)i * d, d, F, s, true)); }
-  }
+  std::vector<ExpertRef> ex(k);
+  for (int i = 0; i < k; ++i)
+    ex[i] = ExpertRef{nullptr, nullptr, (const void* const*)c->d_sh_tbl, (const float* const*)c->d_sh_stbl,
+                      (const int32_t*)(pkt + c->pkt_ids_off), i, j * E, k, 0};
+  shadow_experts(c, ex.data(), pkt, 0, c->rf_a, (const float*)(pkt + c->pkt_w_off), c->rf_y, false, s);
   for (int r = 1; r <= R && j + r < L; ++r) {
     const int m = j + r;
     int n_add = k;
@@ -801,12 +805,10 @@ void enqueue_refine(Ctx* c, int j) {
                                c->rf_u, out + (size_t)(r - 1) * k, c->rf_w + (size_t)(r - 1) * k, nullptr, nullptr, s, true));
     }
     if (r < R && m + 1 < L) {
-      for (int i = 0; i < k; ++i) {
-        ExpertRef ex{nullptr, nullptr, (const void* const*)c->d_sh_tbl, (const float* const*)c->d_sh_stbl,
-                     out + (size_t)(r - 1) * k, i, m * E, k, 0};
-        { KTimer t(c, K_SHADOW, s); CUDA_OK(c, launch_w13(ex, c->sh_ewt, c->rf_u, 0, c->rf_a + (size_t)i * F, d, F, s, true)); }
-        { KTimer t(c, K_SHADOW, s); CUDA_OK(c, launch_w2(ex, c->sh_ewt, c->rf_a + (size_t)i * F, c->rf_w + (size_t)(r - 1) * k, c->rf_y + (size_t)i * d, d, F, s, true)); }
-      }
+      for (int i = 0; i < k; ++i)
+        ex[i] = ExpertRef{nullptr, nullptr, (const void* const*)c->d_sh_tbl, (const float* const*)c->d_sh_stbl,
+                          out + (size_t)(r - 1) * k, i, m * E, k, 0};
+      shadow_experts(c, ex.data(), c->rf_u, 0, c->rf_a, c->rf_w + (size_t)(r - 1) * k, c->rf_y, true, s);
     }
   }
 }

@@ -69,7 +69,7 @@ def main():
     pk = peaks()
     out = {}
     bf = torch.bfloat16
-    if args.only in ("", "gemv"):
+    if args.only in ("", "gemv", "shadow"):
         blob = torch.empty(3 * F * d, dtype=bf, device=dev)
         odmoe.gen_weights(blob, 0, layer=0, expert=0, d=d, F=F, seed=2512)
         w13, w2 = blob[: 2 * F * d], blob[2 * F * d:].view(d, F)
@@ -77,10 +77,11 @@ def main():
         a = torch.empty(F, device=dev)
         y = torch.empty(d, device=dev)
         gw = torch.ones(2, device=dev)
-        med, best = timeit(lambda: odmoe.expert_ffn(w13, w2, u, a, y, gate_w=gw), args.iters, flush)
-        nbytes = 3 * F * d * 2
-        out["expert_ffn_bf16"] = dict(us_median=med * 1e6, us_best=best * 1e6, GBps=nbytes / med / 1e9,
-                                      frac_hbm=nbytes / med / 1e9 / pk["hbm_gbs"], bytes=nbytes)
+        if args.only != "shadow":  # --only shadow: the low-bit shadow experts alone (ncu target)
+            med, best = timeit(lambda: odmoe.expert_ffn(w13, w2, u, a, y, gate_w=gw), args.iters, flush)
+            nbytes = 3 * F * d * 2
+            out["expert_ffn_bf16"] = dict(us_median=med * 1e6, us_best=best * 1e6, GBps=nbytes / med / 1e9,
+                                          frac_hbm=nbytes / med / 1e9 / pk["hbm_gbs"], bytes=nbytes)
         # int8 shadow expert
         q = torch.empty((3 * F * d,), dtype=torch.int8, device=dev)
         sc = torch.empty(2 * F + d, device=dev)
