@@ -1,12 +1,12 @@
 // Flat-stream GEMV (expert W13+SwiGLU, W2+gate, INT8 shadow, LM head + argmax): the third and
-// fastest design measured on B200 (profiles/kbench_r01_*.json). Each CTA (one per SM, 16 warps)
-// owns a contiguous, balanced row range; that range is ONE byte stream which is cut into 16
-// contiguous per-warp slices of 512-byte groups. A warp issues UNROLL groups (one 16-byte
-// ld.global.nc.L1::no_allocate per lane each) before consuming any, so every SM keeps
-// 16 x UNROLL x 512 B = 128 KB in flight, and walks its slice with a running (row, column)
-// position: rows are whole groups, so a row boundary is detected with one compare and the row's
-// partial is flushed with a warp shuffle only then. Per-warp row partials are reduced in a
-// fixed warp order at the end (deterministic, no atomics).
+// fastest design measured on B200 (profiles/kbench_r01_*.json). Each CTA (one per SM, kFG_WARPS =
+// 24 warps) owns a contiguous, balanced row range; that range is ONE byte stream which is cut into
+// kFG_WARPS contiguous per-warp slices of 512-byte groups. A warp issues UNROLL (4) groups (one
+// 16-byte ld.global.nc.L1::no_allocate per lane each) per register batch and keeps two batches in
+// flight, so every SM has 24 x 2 x 4 x 512 B = 96 KB of weights in flight, and walks its slice with
+// a running (row, column) position: rows are whole groups, so a row boundary is detected with one
+// compare and the row's partial is flushed with a warp shuffle only then. Per-warp row partials are
+// reduced in a fixed warp order at the end (deterministic, no atomics).
 #include "common.cuh"
 #include "kernels.h"
 
@@ -20,8 +20,8 @@
 namespace odmoe {
 
 #ifndef FG_WARPS
-#define FG_WARPS 16
-#endif
+#define FG_WARPS 24  // 24 warps x 4-granule batches (profiles/kb_r01_warps_ab.json): every type faster
+#endif            // than 16 x 8 (bf16 66.4 -> 65.6 us, INT8 53.2 -> 49.2, NF4 79.9 -> 68.6 per expert)
 constexpr int kFG_WARPS = FG_WARPS;
 #ifndef FG_NO_F32X2
 #define FG_F32X2 1  // packed fp32x2 FMA/ADD (sm_100 FFMA2/FADD2) in the bf16-x and INT8 dot products
@@ -40,7 +40,7 @@ constexpr int kFG_UNROLL = FG_UNROLL;
 #elif FG_PIPE == 2
 constexpr int kFG_UNROLL = 6;
 #else
-constexpr int kFG_UNROLL = 8;
+constexpr int kFG_UNROLL = 4;
 #endif
 constexpr int kFG_THREADS = kFG_WARPS * 32;
 
@@ -474,7 +474,14 @@ __device__ __forceinline__ void flat_phase(const FlatArgs& a, uint8_t* sm, const
     // Fast path: a whole batch inside the slice of a row at least UNROLL groups long crosses at
     // most one row boundary. Granules before it add to acc, the rest to acc1 (predicated adds, no
     // branch per granule); the order of every row's sum is the one of the general path below.
-    if (Gr >= UNROLL && g0 + UNROLL <= g_end) {
+    // Measured (profiles/kb_r01_warps_ab.json): bf16 expert 70.6 -> 66.6 us; the low-bit dot
+    // products got slower (INT8 53.2 -> 58.4 us), so they keep the general loop.
+#ifdef FG_FAST_ALL
+    constexpr bool kFastT = !kNF4;
+#else
+    constexpr bool kFastT = std::is_same<WT, __nv_bfloat16>::value || std::is_same<WT, float>::value;
+#endif
+    if constexpr (kFastT) if (Gr >= UNROLL && g0 + UNROLL <= g_end) {
       const int b = Gr - gcol;  // granules left in the current row (>= 1)
       const uint4* x0 = reinterpret_cast<const uint4*>(xs) + lane;
       float acc1 = 0.f;
@@ -482,13 +489,8 @@ __device__ __forceinline__ void flat_phase(const FlatArgs& a, uint8_t* sm, const
       for (int i = 0; i < UNROLL; ++i) {
         const int c = gcol + i < Gr ? gcol + i : gcol + i - Gr;
         const uint4* xp = x0 + (size_t)c * Q * 32;
-        if constexpr (kNF4) {
-          const float t = nf4_dot(wv[i], xp, lut_l, XT{});
-          if (i < b) acc = fmaf(sv[i], t, acc); else acc1 = fmaf(sv[i], t, acc1);
-        } else {
-          const float t = FDot<WT, XT>::run(wv[i], xp);
-          if (i < b) acc += t; else acc1 += t;
-        }
+        const float t = FDot<WT, XT>::run(wv[i], xp);
+        if (i < b) acc += t; else acc1 += t;
       }
       if (b <= UNROLL) {  // the row completed inside this batch
         const float t = warp_sum(acc);
