@@ -247,7 +247,7 @@ odmoe_status odmoe_prefill_group(const int32_t* ids, const float* w, int T, int 
  *   a2[r] = bf16(silu(W1_e x[r]) * (W3_e x[r]))   and   y[r] = gate_perm[r] * (W2_e a2[r]).
  * w13[e], w2[e]: HOST arrays of DEVICE pointers (bf16 [F][2][d] and [d][F]); x_perm [M,d] bf16,
  * gate_perm [M] fp32, a2_scratch [M,F] bf16, y_perm [M,d] fp32 (device); offsets [n_experts+1]
- * HOST int32, M = offsets[n_experts]; tiles_scratch device >= 16*(M/128 + n_experts)*(2F/256 +
+ * HOST int32, M = offsets[n_experts]; tiles_scratch device >= 16*(M/128 + n_experts)*(2F/224 +
  * d/128) bytes. Limits: n_experts <= 8, d % 256 == 0, F % 128 == 0, bf16 only. Synchronous on
  * `stream` (returns after the GEMMs complete). */
 odmoe_status odmoe_expert_ffn_grouped(const void* const* w13, const void* const* w2, int n_experts,

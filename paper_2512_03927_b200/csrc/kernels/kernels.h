@@ -124,7 +124,7 @@ struct GroupedGemmArgs {
   const float* gate;
 };
 cudaError_t launch_grouped_gemm(const GroupedGemmArgs& g, cudaStream_t s);
-int grouped_gemm_bn(int mode);  // output-tile width for the mode (tile n0 step)
+int grouped_gemm_bn(int mode, int N);  // output-tile width for the mode and N (tile n0 step)
 int grouped_gemm_bm();          // rows per tile (tile row0 step, <= 256)
 
 // Prefill permutation: stable counting sort of the T*k pairs by expert.

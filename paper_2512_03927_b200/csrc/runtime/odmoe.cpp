@@ -1489,7 +1489,7 @@ void ensure_prefill(Ctx* c, int T) {
   c->p_a2 = dmalloc<char>(c, (size_t)M * F * 2, "p_a2");
   c->p_y = dmalloc<float>(c, (size_t)M * d, "p_y");
   c->p_part = dmalloc<float>(c, (size_t)T * d, "p_part");
-  c->tiles_cap = (int)(((M + 127) / 128 + E) * (2 * c->Fs / grouped_gemm_bn(0) + d / grouped_gemm_bn(1)));
+  c->tiles_cap = (int)(((M + 127) / 128 + E) * (2 * c->Fs / grouped_gemm_bn(0, 2 * c->Fs) + d / grouped_gemm_bn(1, d)));
   c->p_tiles = dmalloc<int4>(c, (size_t)c->tiles_cap, "p_tiles");
   if (c->H > 0 && c->rank == 0) {
     F_(c->pa_x); F_(c->pa_qkv); F_(c->pa_part); F_(c->pa_out); F_(c->pa_tiles);
@@ -1525,7 +1525,7 @@ void prefill_attention(Ctx* c, int l, int T, cudaStream_t s) {
   const int kvf = c->kv_esz == 4;
   auto gemm = [&](const void* a, const void* w, int N, int K, float* out) {
     std::vector<int4> tiles;
-    const int BM = grouped_gemm_bm(), BN = grouped_gemm_bn(1);
+    const int BM = grouped_gemm_bm(), BN = grouped_gemm_bn(1, N);
     for (int m0 = 0; m0 < T; m0 += BM)
       for (int n0 = 0; n0 < N; n0 += BN) tiles.push_back(make_int4(0, m0, std::min(BM, T - m0), n0));
     CUDA_OK(c, cudaMemcpyAsync(c->pa_tiles, tiles.data(), sizeof(int4) * tiles.size(), cudaMemcpyHostToDevice, s));
@@ -1633,9 +1633,9 @@ void prefill_impl(Ctx* c, const int32_t* tokens, int T, int32_t* token_out, int3
         if (prefill_mine(c, l, e)) mine.push_back(e);
       CUDA_OK(c, launch_gather_rows(u, c->p_src, k, (int)M, d, c->p_x, s));
       tiles.clear();
-      build_tiles(off, mine, 2 * c->Fs, grouped_gemm_bn(0), tiles);
+      build_tiles(off, mine, 2 * c->Fs, grouped_gemm_bn(0, 2 * c->Fs), tiles);
       const int n1 = (int)tiles.size();
-      build_tiles(off, mine, d, grouped_gemm_bn(1), tiles);
+      build_tiles(off, mine, d, grouped_gemm_bn(1, d), tiles);
       const int n2 = (int)tiles.size() - n1;
       if ((int)tiles.size() > c->tiles_cap) fail(c, ODMOE_E_STATE, "tile list overflow");
       if (!tiles.empty())
@@ -2175,9 +2175,9 @@ odmoe_status odmoe_expert_ffn_grouped(const void* const* w13, const void* const*
   std::vector<int> all(n_experts);
   for (int e = 0; e < n_experts; ++e) all[e] = e;
   std::vector<int4> tiles;
-  build_tiles(off, all, 2 * F, grouped_gemm_bn(0), tiles);
+  build_tiles(off, all, 2 * F, grouped_gemm_bn(0, 2 * F), tiles);
   const int n1 = (int)tiles.size();
-  build_tiles(off, all, d, grouped_gemm_bn(1), tiles);
+  build_tiles(off, all, d, grouped_gemm_bn(1, d), tiles);
   if ((int64_t)(tiles.size() * sizeof(int4)) > tiles_scratch_bytes) return ODMOE_E_CONFIG;
   const int M = off[n_experts];
   if (M == 0) return ODMOE_OK;
