@@ -231,6 +231,15 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        # torchrun pins OMP_NUM_THREADS=1 per rank; rank 0 runs alone here, so give the oracle the
+        # host cores it has at N = 1
+        try:
+            import numpy  # noqa: F401  (threadpoolctl only sees BLAS libraries already loaded)
+            from threadpoolctl import threadpool_limits
+            threadpool_limits(limits=len(os.sched_getaffinity(0)))
+        except Exception:
+            pass
     walk = OracleWalk()
     for _ in range(args.warmup):
         walk.step()
