@@ -454,3 +454,63 @@ def test_resident_graph_replay_and_timer_levels(od):
     assert toks == ref
     assert eng.stats()["n_router"] > 0                                      # level 2: every family
     eng.close()
+
+
+MID = type(TINY)(L=4, E=8, k=2, d=1024, F=2048, V=2048)   # rows of whole 512-byte groups: flat engine
+
+
+def test_mid_shape_flat_engine_teacher_forced(od):
+    """A shape whose rows are whole 512-byte groups, so every expert GEMV takes the flat engine:
+    the fused cooperative bf16 expert kernel, the INT8 shadow's one-launch-per-phase multi-expert
+    kernel, the refinement. Teacher-forced per layer vs the oracle, main and shadow."""
+    W = gen_model_weights(MID, SEED, dtype="bf16")
+    SW = O.quantize_model_int8(W)
+    eng = engine(od, MID, "bf16", predictor=od.PRED_SHADOW_INT8, slots_per_gpu=2, refine_depth=2,
+                 debug_capture=1)
+    tok = int(gen_prompt(MID, 2, 1)[0])
+    excused = 0
+    for _ in range(4):
+        nxt, recs = eng.decode_step(tok)
+        excused += check_step_teacher_forced(eng, W, MID, "bf16", tok, nxt, SW)
+        for l in range(MID.L):
+            assert recs[l].correct == len(set(recs[l].true_ids[: MID.k]) & set(recs[l].pred_ids[: MID.k]))
+        tok = nxt
+    assert excused <= 2
+    eng.close()
+
+
+_MULTI_PROBE = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+from paper_2512_03927_b200 import odmoe as od
+from inputs import gen_prompt
+L, E, k, d, F, V = 4, 8, 2, 1024, 2048, 2048
+eng = od.Engine(L, E, k, d, F, V, dtype=od.BF16, weight_seed=2512, predictor=od.PRED_SHADOW_INT8,
+                slots_per_gpu=2, refine_depth=2, debug_capture=1)
+tok, out = 7, []
+for _ in range(3):
+    tok, recs = eng.decode_step(tok)
+    out.append(str(tok))
+    for l in range(L):
+        out.append(eng.debug_read("SH_LOGITS", l, 4 * E).hex())
+        out.append(",".join(str(x) for x in recs[l].pred_ids[:k]))
+eng.close()
+print("|".join(out))
+"""
+
+
+def test_shadow_multi_launch_bitwise_equals_per_expert_launches(od):
+    """ODMOE_MULTI=0 (one launch per shadow expert) and the default multi-expert launch give
+    bitwise-identical shadow logits and predictions (each CTA takes the one-expert row range)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for multi in ("0", "1"):
+        env = dict(os.environ, ODMOE_MULTI=multi)
+        p = subprocess.run([sys.executable, "-c", _MULTI_PROBE.format(root=root)], env=env, capture_output=True,
+                           text=True, timeout=600)
+        assert p.returncode == 0, p.stderr[-2000:]
+        res[multi] = p.stdout.strip().splitlines()[-1]
+    assert res["0"] == res["1"]
