@@ -105,12 +105,13 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-template <int BN, int MODE>  // MODE 0: SwiGLU -> bf16 [M, N/2]; MODE 1: gate-scale -> fp32 [M, N]
+// MODE 0: SwiGLU -> bf16 [M, N/2]; MODE 1: gate-scale -> fp32 [M, N]. STAGES: smem ring depth
+// (2 with BN = 128 leaves room for two CTAs per SM, whose epilogues then overlap the other's loads)
+template <int BN, int MODE, int STAGES = gg_stages<BN>()>
 __global__ void __launch_bounds__(kGG_THREADS, 1)
 grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ GGMaps maps_b,
                     const int4* __restrict__ tiles, int K, int N, void* __restrict__ out,
                     const float* __restrict__ gate) {
-  constexpr int STAGES = gg_stages<BN>();
   constexpr int A_BYTES = kGG_BM * kGG_BK * 2;          // one 128-row half
   constexpr int B_BYTES = BN * kGG_BK * 2;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -224,6 +225,15 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_cons
 }
 
 // ---------------------------------------------------------------- host side
+// ODMOE_GG_2CTA=1: 128-wide tiles with a 2-stage ring (97 KB smem, 256 TMEM columns), two CTAs per SM
+static bool gg_two_ctas() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ODMOE_GG_2CTA");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -249,15 +259,15 @@ static bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t c
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN, int MODE>
+template <int BN, int MODE, int STAGES = gg_stages<BN>()>
 static cudaError_t gg_launch(const GroupedGemmArgs& g, cudaStream_t s) {
   CUtensorMap ma;
   GGMaps mb;
   if (!make_map(&ma, g.a, (uint64_t)g.M, (uint64_t)g.K, kGG_BM)) return cudaErrorInvalidValue;
   for (int e = 0; e < g.n_experts; ++e)
     if (g.b[e] && !make_map(&mb.b[e], g.b[e], (uint64_t)g.N, (uint64_t)g.K, BN)) return cudaErrorInvalidValue;
-  const size_t smem = 1024 + (size_t)gg_stages<BN>() * (kGG_MT * kGG_BM + BN) * kGG_BK * 2 + 256;
-  auto kern = grouped_gemm_kernel<BN, MODE>;
+  const size_t smem = 1024 + (size_t)STAGES * (kGG_MT * kGG_BM + BN) * kGG_BK * 2 + 256;
+  auto kern = grouped_gemm_kernel<BN, MODE, STAGES>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   kern<<<g.n_tiles, kGG_THREADS, smem, s>>>(ma, mb, g.tiles, g.K, g.N, g.out, g.gate);
@@ -267,6 +277,10 @@ static cudaError_t gg_launch(const GroupedGemmArgs& g, cudaStream_t s) {
 cudaError_t launch_grouped_gemm(const GroupedGemmArgs& g, cudaStream_t s) {
   if (g.n_experts > kMaxGGExperts || g.K % kGG_BK) return cudaErrorInvalidValue;
   if (g.n_tiles == 0) return cudaSuccess;
+  if (gg_two_ctas()) {
+    if (g.N % 128) return cudaErrorInvalidValue;
+    return g.mode == 0 ? gg_launch<128, 0, 2>(g, s) : gg_launch<128, 1, 2>(g, s);
+  }
   if (g.mode == 0) {
     if (grouped_gemm_bn(0, g.N) == 224) return gg_launch<224, 0>(g, s);
     if (g.N % 256) return cudaErrorInvalidValue;
@@ -276,18 +290,20 @@ cudaError_t launch_grouped_gemm(const GroupedGemmArgs& g, cudaStream_t s) {
   return gg_launch<128, 1>(g, s);
 }
 
-// GEMM1 tile width: 224 where it divides N. Mixtral's 2F = 28672 then gives 128 tiles per expert,
-// 1024 for 8 experts = 6.9 waves of 148 CTAs, against 896 = 6.05 waves (a 7th wave with 8 tiles)
-// at 256 -- the same 7 waves with 12.5 % less work in each.
+// GEMM1 tile width. 224 (where it divides N; Mixtral's 2F = 28672 -> 1024 tiles = 6.9 waves of 148
+// CTAs instead of 896 = 6.05) was measured no faster than 256 (0.673 vs 0.668 ms for the T = 512
+// grouped FFN, profiles/kb_r01_grouped_bn_ab.json): the per-tile prologue / epilogue, not the
+// wave tail, sets the gap to the HBM floor. ODMOE_GG_BN=224 keeps it selectable.
 int grouped_gemm_bn(int mode, int N) {
-  static int force256 = -1;
-  if (force256 < 0) {
-    const char* e = getenv("ODMOE_GG_BN");  // ODMOE_GG_BN=256: the earlier tiling (A/B)
-    force256 = (e && e[0] == '2' && e[1] == '5') ? 1 : 0;
+  static int use224 = -1;
+  if (use224 < 0) {
+    const char* e = getenv("ODMOE_GG_BN");
+    use224 = (e && e[0] == '2' && e[1] == '2' && e[2] == '4') ? 1 : 0;
   }
-  if (mode != 0) return 128;
-  return (N % 224 == 0 && !force256) ? 224 : 256;
+  if (mode != 0 || gg_two_ctas()) return 128;
+  return (use224 && N % 224 == 0) ? 224 : 256;
 }
+
 int grouped_gemm_bm() { return kGG_MT * kGG_BM; }
 
 }  // namespace odmoe

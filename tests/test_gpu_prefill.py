@@ -57,7 +57,7 @@ def _grouped_case(od, shape, counts, check_rows):
     w2s = [to_dev(W2, "bf16") for (_, _, W2) in mats]
     a2 = t.empty((max(M, 1), F), dtype=t.bfloat16, device="cuda")
     y = t.full((max(M, 1), d), float("nan"), dtype=t.float32, device="cuda")
-    tiles = t.empty(16 * ((M // 128 + E + 1) * (2 * F // 224 + d // 128)), dtype=t.uint8, device="cuda")
+    tiles = t.empty(16 * ((M // 128 + E + 1) * (2 * F // 128 + d // 128)), dtype=t.uint8, device="cuda")
     od.expert_ffn_grouped(w13s, w2s, xb, off, t.from_numpy(gate).cuda(), a2, y, tiles)
     yh = host(y)
     errs = []

@@ -161,7 +161,7 @@ def main():
         gate = torch.rand(M, device=dev)
         a2 = torch.empty(M, F, dtype=bf, device=dev)
         y = torch.empty(M, d, device=dev)
-        tiles = torch.empty(16 * ((M // 128 + E + 1) * (2 * F // 224 + d // 128)), dtype=torch.uint8, device=dev)
+        tiles = torch.empty(16 * ((M // 128 + E + 1) * (2 * F // 128 + d // 128)), dtype=torch.uint8, device=dev)
         med, best = timeit(lambda: odmoe.expert_ffn_grouped(w13s, w2s, x, off, gate, a2, y, tiles), max(5, args.iters // 4), flush)
         flops = 2.0 * M * 3 * d * F
         nb = E * 3 * F * d * 2
