@@ -302,6 +302,39 @@ def test_mixtral_decode_sampled_layers(od):
     eng.close()
 
 
+@pytest.mark.slow
+def test_mixtral_shadow_sampled_layers(od):
+    """The INT8 shadow at BASELINE.json configs[1] shape in the bench's launch configuration (the
+    one-launch-per-phase multi-expert kernel over the quantised experts): on sampled layers its
+    router input, routing and expert output (h_{l+1} - h_l of the shadow's own residual stream)
+    vs the oracle's int8-row shadow (quantize_model_int8 applied to the regenerated weights)."""
+    from inputs import KIND_ROUTER, tensor_id, weight_fp32, bf16_bits_to_f32, f32_to_bf16_bits
+    shape = MIXTRAL
+    d, k, E = shape.d, shape.k, shape.E
+    dq = lambda M: O.dequantize_int8_rows(*O.quantize_int8_rows(M))  # noqa: E731
+    eng = engine(od, shape, "bf16", predictor=od.PRED_SHADOW_INT8, slots_per_gpu=2, debug_capture=1)
+    tok = int(gen_prompt(shape, 2, 1)[0])
+    eng.decode_step(tok)
+    for l in (0, 13):
+        Wg = bf16_bits_to_f32(f32_to_bf16_bits(weight_fp32(SEED, tensor_id(KIND_ROUTER, l), E, d, d))).reshape(E, d)
+        sh = read_f32(eng, "SH_H_IN", l, d)
+        su = read_u(eng, "SH_U", l, d, "bf16")
+        assert np.all(np.abs(su - O.rms_norm(sh)) <= 2.0 ** -8 * np.abs(O.rms_norm(sh)) + 1e-6)
+        sr_ref = O.router_logits(dq(Wg), su)
+        sl = read_f32(eng, "SH_LOGITS", l, E)
+        assert np.allclose(sl, sr_ref, rtol=0, atol=1e-5 * np.abs(sr_ref).max() + 1e-7), l
+        sids = read_i32(eng, "SH_IDS", l, k)
+        assert ids_match(sids, sr_ref, k)[0], (l, sids, sr_ref)
+        w = O.mixture_weights(sr_ref, [int(i) for i in sids])
+        y_ref = np.zeros(d)
+        for j in range(k):
+            W1, W3, W2 = gen_expert(shape, SEED, l, int(sids[j]), "bf16")
+            y_ref += w[j] * O.expert_ffn(dq(W1), dq(W3), dq(W2), su)
+        y = read_f32(eng, "SH_H_IN", l + 1, d) - sh
+        assert l2rel(y, y_ref) <= 1e-4, (l, l2rel(y, y_ref))
+    eng.close()
+
+
 def test_runtime_options_switch_predictor_and_lookahead(od):
     """odmoe_set_option: switching predictor / lookahead between steps changes time and recall
     accounting only; tokens stay identical."""
