@@ -713,7 +713,7 @@ static cudaError_t fg_launch(FlatArgs a, cudaStream_t s, bool pdl) {
   }
   a.evict_first = ef;
   if (!flat_row_ok<WT>(a.C)) return cudaErrorInvalidValue;
-  const int sms = num_sms();
+  const int sms = stream_grid_sms();
   const long long units = MODE == 0 ? a.R / 2 : a.R;
   const int grid = (int)(units < sms ? (units > 0 ? units : 1) : sms);
   a.rows_cap = (int)((units + grid - 1) / grid) * (MODE == 0 ? 2 : 1) + 2;
@@ -981,7 +981,7 @@ static cudaError_t multi_launch(MultiArgs m, cudaStream_t s, bool pdl) {
   const int n = m.n;
   const long long F = m.a13[0].R / 2, D = m.a2[0].R;
   if (!flat_row_ok<WT>(m.a13[0].C) || !flat_row_ok<WT>(m.a2[0].C)) return cudaErrorInvalidValue;
-  const int sms = num_sms();
+  const int sms = stream_grid_sms();
   const long long units = F < D ? F : D;   // the one-expert kernel's grid (same per-CTA rows)
   const int grid = (int)(units < sms ? (units > 0 ? units : 1) : sms);
   const int cap13 = (int)((F + grid - 1) / grid) * 2 + 2;
@@ -1078,7 +1078,7 @@ static cudaError_t fg_multi_launch(MultiArgs m, cudaStream_t s, bool pdl) {
   }
   FlatArgs* as = MODE == 0 ? m.a13 : m.a2;
   if (!flat_row_ok<WT>(as[0].C)) return cudaErrorInvalidValue;
-  const int sms = num_sms();
+  const int sms = stream_grid_sms();
   const long long units = MODE == 0 ? as[0].R / 2 : as[0].R;   // fg_launch's grid and rows_cap
   const int grid = (int)(units < sms ? (units > 0 ? units : 1) : sms);
   const int cap = (int)((units + grid - 1) / grid) * (MODE == 0 ? 2 : 1) + 2;
@@ -1188,7 +1188,7 @@ static cudaError_t fused_launch(FlatArgs a13, FlatArgs a2, cudaStream_t s, bool 
   }
   a13.evict_first = a2.evict_first = ef;
   if (!flat_row_ok<WT>(a13.C) || !flat_row_ok<WT>(a2.C)) return cudaErrorInvalidValue;
-  const int sms = num_sms();
+  const int sms = stream_grid_sms();
   long long units = a13.R / 2 < a2.R ? a13.R / 2 : a2.R;
   const int grid = (int)(units < sms ? (units > 0 ? units : 1) : sms);
   a13.rows_cap = (int)((a13.R / 2 + grid - 1) / grid) * 2 + 2;

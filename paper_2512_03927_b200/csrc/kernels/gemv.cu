@@ -234,6 +234,23 @@ bool use_fused_expert() {
   return v == 1 && gemv_engine() == 2;
 }
 
+// SMs a one-CTA-per-SM streaming grid may count on (flat engine). At N > 1 the engine reserves one:
+// the prediction communicator's broadcasts (one CTA, maxCTAs = 1) spin on the shadow stream, and a
+// grid of all 148 CTAs would leave one CTA waiting for that SM until the broadcast completes.
+static int g_sm_reserve[64] = {0};
+void set_stream_sm_reserve(int n) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64) g_sm_reserve[dev] = n < 0 ? 0 : n;
+}
+int stream_grid_sms() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int r = (dev >= 0 && dev < 64) ? g_sm_reserve[dev] : 0;
+  const int n = num_sms() - r;
+  return n > 0 ? n : 1;
+}
+
 int num_sms() {
   static int cached[64] = {0};
   int dev = 0;

@@ -12,6 +12,8 @@ enum WType { W_BF16 = 0, W_F32 = 1, W_I8 = 2, W_NF4 = 3, W_F8 = 4 };
 // W2 (3dF/2 bytes), scale array = W13 blocks then W2 blocks.
 
 int num_sms();  // cached SM count of the current device
+int stream_grid_sms();            // num_sms() minus the reserve below (grid of the flat engine)
+void set_stream_sm_reserve(int n);  // SMs the flat engine leaves free on the current device
 
 // a2+a3: h += sum(y_add); u = RMSNorm(h) (rounded to u's dtype); logits = W_g u; top-k; softmax.
 // wt: weight type of w_gate (W_I8 uses wg_scale[E]); u dtype = fp32 iff wt == W_F32, else bf16.

@@ -1007,6 +1007,15 @@ uint32_t p2p_mask(const Ctx* c, int l) {
 }
 
 // ------------------------------------------------------------------ one decode step
+bool fused_ngpu_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ODMOE_FUSED_NGPU");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 bool graph_enabled() {
   static int v = -1;
   if (v < 0) {
@@ -1031,8 +1040,10 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
   // prediction communicator is idle). At N > 1 the prediction broadcasts spin on the shadow
   // stream; a cooperative grid that cannot become fully resident would wait at its barrier for
   // SMs held by a kernel that waits for a peer that waits for us.
+  // ODMOE_FUSED_NGPU=1 also allows it at N > 1: the prediction communicator is limited to one CTA
+  // and the grid leaves one SM free, so the grid can always become resident beside it.
   const bool fused = use_fused_expert() && stream_ok(c->wt, d) && stream_ok(c->wt, c->Fs) &&
-                     (c->world == 1 || c->resident);
+                     (c->world == 1 || c->resident || fused_ngpu_enabled());
 
   // Fully-resident 1-GPU steps (no attention, no debug capture) are the same sequence of launches
   // every token: the second step is captured into a CUDA graph (token H2D ... token D2H) and later
@@ -1881,7 +1892,13 @@ odmoe_status odmoe_create(const odmoe_config* cfg, void** ctx_out) {
         ncclUniqueId id;
         std::memcpy(&id, cfg->nccl_id, sizeof(id));
         NCCL_OK(c, ncclCommInitRank(&c->comm, c->world, id, c->rank));
-        NCCL_OK(c, ncclCommSplit(c->comm, 0, c->rank, &c->comm_pred, nullptr));
+        // the prediction communicator moves a few hundred bytes at a time and its receives spin on
+        // the shadow stream beside the expert kernels: one CTA, and the flat engine leaves one SM
+        ncclConfig_t pcfg = NCCL_CONFIG_INITIALIZER;
+        pcfg.minCTAs = 1;
+        pcfg.maxCTAs = 1;
+        NCCL_OK(c, ncclCommSplit(c->comm, 0, c->rank, &c->comm_pred, &pcfg));
+        set_stream_sm_reserve(1);
         setup_p2p(c);
       }
       char* staging = dmalloc<char>(c, (size_t)(c->full_bytes + 2 * c->blob_bytes), "staging");
