@@ -1,4 +1,4 @@
-"""N > 1 host logic on CPU (gloo, world_size 2 and 4): every rank computes its placement with
+"""N > 1 host logic on CPU (gloo, world_size 2, 4 and 8): every rank computes its placement with
 the library's host-only plan functions; the union over ranks must assign each routed expert to
 exactly one GPU of the layer's group (P:104 one-to-one; S:288 sorted pairing; l mod N_G round
 robin) and every rank's pool must hold whatever it can be assigned."""
@@ -54,7 +54,7 @@ def _worker(rank, world, port, q):
     q.put((rank, bool(ok)))
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_multirank_placement_gloo(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
