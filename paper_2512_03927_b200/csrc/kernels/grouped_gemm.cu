@@ -39,7 +39,9 @@ template <int BN> __host__ __device__ constexpr uint32_t gg_tmem_cols() {
 
 struct GGMaps {
   CUtensorMap b[kMaxGGExperts];
+  int dyn_stages;  // 1: ring depth per tile (more B stages when the tile has one A half)
 };
+constexpr int kGG_MAX_ST = 8;  // barrier slots
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -114,13 +116,12 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_cons
                     const float* __restrict__ gate) {
   constexpr int A_BYTES = kGG_BM * kGG_BK * 2;          // one 128-row half
   constexpr int B_BYTES = BN * kGG_BK * 2;
+  constexpr int RING = STAGES * (kGG_MT * A_BYTES + B_BYTES);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;                                   // [STAGES][2 halves]
-  uint8_t* sB = smem + STAGES * kGG_MT * A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* acc_ready = empty + STAGES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + RING);
+  uint64_t* empty = full + kGG_MAX_ST;
+  uint64_t* acc_ready = empty + kGG_MAX_ST;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_ready + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -128,9 +129,17 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_cons
   const int expert = tile.x, row0 = tile.y, rows = tile.z, n0 = tile.w;
   const int halves = rows > kGG_BM ? 2 : 1;
   const int KB = K / kGG_BK;
+  // The loads are latency-bound (ncu: the MMA issuer waits on "full"), so the weight bytes in flight
+  // set the rate. A stage is [A halves][B]; a tile with one A half packs more stages into the same
+  // ring (GEMM1: 4 x 48 KB instead of 3 x 64 KB -> 128 KB of weights in flight instead of 96).
+  const int stage_bytes = halves * A_BYTES + B_BYTES;
+  int nst = maps_b.dyn_stages ? RING / stage_bytes : STAGES;
+  nst = nst > kGG_MAX_ST ? kGG_MAX_ST : nst;
+  auto sA_of = [&](int s, int hh) { return smem + s * stage_bytes + hh * A_BYTES; };
+  auto sB_of = [&](int s) { return smem + s * stage_bytes + halves * A_BYTES; };
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < nst; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     mbar_init(acc_ready, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
@@ -149,33 +158,31 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_cons
   if (warp == 0) {
     if (lane == 0) {
       const uint32_t tx = (uint32_t)(halves * A_BYTES + B_BYTES);
-      for (int kb = 0; kb < KB; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t ph = (uint32_t)(kb / STAGES) & 1u;
-        mbar_wait(&empty[s], ph ^ 1u);
+      for (int kb = 0, s = 0, ph = 0; kb < KB; ++kb) {
+        mbar_wait(&empty[s], (uint32_t)ph ^ 1u);
         mbar_expect_tx(&full[s], tx);
         for (int hh = 0; hh < halves; ++hh)
-          tma_load_2d(sA + (s * kGG_MT + hh) * A_BYTES, &map_a, &full[s], kb * kGG_BK, row0 + hh * kGG_BM);
-        tma_load_2d(sB + s * B_BYTES, &maps_b.b[expert], &full[s], kb * kGG_BK, n0);
+          tma_load_2d(sA_of(s, hh), &map_a, &full[s], kb * kGG_BK, row0 + hh * kGG_BM);
+        tma_load_2d(sB_of(s), &maps_b.b[expert], &full[s], kb * kGG_BK, n0);
+        if (++s == nst) { s = 0; ph ^= 1; }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = umma_idesc_bf16(kGG_BM, BN);
-      for (int kb = 0; kb < KB; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t ph = (uint32_t)(kb / STAGES) & 1u;
-        mbar_wait(&full[s], ph);
+      for (int kb = 0, s = 0, ph = 0; kb < KB; ++kb) {
+        mbar_wait(&full[s], (uint32_t)ph);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t b0 = smem_u32(sB + s * B_BYTES);
+        const uint32_t b0 = smem_u32(sB_of(s));
         for (int hh = 0; hh < halves; ++hh) {
-          const uint32_t a0 = smem_u32(sA + (s * kGG_MT + hh) * A_BYTES);
+          const uint32_t a0 = smem_u32(sA_of(s, hh));
 #pragma unroll
           for (int k = 0; k < kGG_BK / 16; ++k)
             umma_bf16(tmem + (uint32_t)(hh * BN), umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32),
                       idesc, (kb | k) != 0);
         }
         umma_commit(&empty[s]);  // smem slot free once these MMAs have read it
+        if (++s == nst) { s = 0; ph ^= 1; }
       }
       umma_commit(acc_ready);
     }
@@ -263,6 +270,12 @@ template <int BN, int MODE, int STAGES = gg_stages<BN>()>
 static cudaError_t gg_launch(const GroupedGemmArgs& g, cudaStream_t s) {
   CUtensorMap ma;
   GGMaps mb;
+  static int dyn = -1;
+  if (dyn < 0) {
+    const char* e = getenv("ODMOE_GG_DYN");  // ODMOE_GG_DYN=0: the fixed ring (A/B)
+    dyn = (e && e[0] == '0') ? 0 : 1;
+  }
+  mb.dyn_stages = dyn;
   if (!make_map(&ma, g.a, (uint64_t)g.M, (uint64_t)g.K, kGG_BM)) return cudaErrorInvalidValue;
   for (int e = 0; e < g.n_experts; ++e)
     if (g.b[e] && !make_map(&mb.b[e], g.b[e], (uint64_t)g.N, (uint64_t)g.K, BN)) return cudaErrorInvalidValue;
