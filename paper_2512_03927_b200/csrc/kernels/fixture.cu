@@ -102,7 +102,7 @@ template <typename T> __device__ __forceinline__ float ld_f(const T* p, long lon
 template <> __device__ __forceinline__ float ld_f<__nv_bfloat16>(const __nv_bfloat16* p, long long i) { return __bfloat162float(p[i]); }
 template <> __device__ __forceinline__ float ld_f<float>(const float* p, long long i) { return p[i]; }
 
-template <typename T>
+template <typename T, bool BIASED = false>
 __global__ void __launch_bounds__(256) quantize_rows_kernel(const T* __restrict__ w, long long C,
                                                             int8_t* __restrict__ q, float* __restrict__ sc) {
   __shared__ float red[8];
@@ -130,15 +130,17 @@ __global__ void __launch_bounds__(256) quantize_rows_kernel(const T* __restrict_
       qi = qi > 127 ? 127 : (qi < -127 ? -127 : qi);
       code = (int8_t)qi;
     }
-    q[r * C + j] = code;
+    q[r * C + j] = BIASED ? (int8_t)(uint8_t)(code + 128) : code;
   }
 }
 
 cudaError_t launch_quantize(const void* w, int64_t R, int64_t C, WType wt, int8_t* q, float* sc,
-                            cudaStream_t s) {
+                            cudaStream_t s, bool biased) {
   if (R <= 0) return cudaSuccess;
-  if (wt == W_BF16) quantize_rows_kernel<__nv_bfloat16><<<(unsigned)R, 256, 0, s>>>((const __nv_bfloat16*)w, C, q, sc);
-  else if (wt == W_F32) quantize_rows_kernel<float><<<(unsigned)R, 256, 0, s>>>((const float*)w, C, q, sc);
+  if (wt == W_BF16 && !biased) quantize_rows_kernel<__nv_bfloat16><<<(unsigned)R, 256, 0, s>>>((const __nv_bfloat16*)w, C, q, sc);
+  else if (wt == W_BF16) quantize_rows_kernel<__nv_bfloat16, true><<<(unsigned)R, 256, 0, s>>>((const __nv_bfloat16*)w, C, q, sc);
+  else if (wt == W_F32 && !biased) quantize_rows_kernel<float><<<(unsigned)R, 256, 0, s>>>((const float*)w, C, q, sc);
+  else if (wt == W_F32) quantize_rows_kernel<float, true><<<(unsigned)R, 256, 0, s>>>((const float*)w, C, q, sc);
   else return cudaErrorInvalidValue;
   return cudaGetLastError();
 }

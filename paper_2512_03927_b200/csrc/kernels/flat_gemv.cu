@@ -131,6 +131,7 @@ template <typename WT> struct FTraits { static constexpr int bits = 8 * (int)siz
 template <> struct FTraits<nf4x2> { static constexpr int bits = 4; static constexpr bool nf4 = true; };
 template <> struct FDot<nf4x2, uint16_t> { static constexpr int kN = 32; };
 struct fp8e4 { uint8_t v; };  // E4M3 code (FP8 shadow, reading Q28); row scales like int8
+struct u8b { uint8_t v; };    // INT8-row code stored as q + 128 (W_U8)
 template <> struct FDot<nf4x2, float> { static constexpr int kN = 32; };
 
 // QLoRA's published NF4 codebook (Dettmers et al. 2023)
@@ -263,6 +264,48 @@ __device__ __forceinline__ f2_t i8x4_dot2(uint32_t word, uint32_t x01, uint32_t 
   return f2_fma(q23, bf2_unpack(x23), s);
 }
 #endif
+// W_U8: the byte already is q + 128, so it goes into the mantissa of 2^23 without the sign flip
+__device__ __forceinline__ f2_t u8x4_dot2(uint32_t b, uint32_t x01, uint32_t x23, f2_t s) {
+  const f2_t m = f2_pack(-8388736.0f, -8388736.0f);
+  const f2_t q01 = f2_add(f2_pack(__uint_as_float(__byte_perm(b, 0x4B000000u, 0x7540)),
+                                  __uint_as_float(__byte_perm(b, 0x4B000000u, 0x7541))), m);
+  const f2_t q23 = f2_add(f2_pack(__uint_as_float(__byte_perm(b, 0x4B000000u, 0x7542)),
+                                  __uint_as_float(__byte_perm(b, 0x4B000000u, 0x7543))), m);
+  s = f2_fma(q01, bf2_unpack(x01), s);
+  return f2_fma(q23, bf2_unpack(x23), s);
+}
+template <> struct FDot<u8b, float> {
+  static constexpr int kN = 16;
+  __device__ __forceinline__ static float run(const uint4& w, const uint4* xp) {
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+    const f2_t m = f2_pack(-8388736.0f, -8388736.0f);
+    f2_t s = 0ull;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint4 xq = xp[32 * q];
+      const uint32_t b = ws[q];
+      const f2_t q01 = f2_add(f2_pack(__uint_as_float(__byte_perm(b, 0x4B000000u, 0x7540)),
+                                      __uint_as_float(__byte_perm(b, 0x4B000000u, 0x7541))), m);
+      const f2_t q23 = f2_add(f2_pack(__uint_as_float(__byte_perm(b, 0x4B000000u, 0x7542)),
+                                      __uint_as_float(__byte_perm(b, 0x4B000000u, 0x7543))), m);
+      s = f2_fma(q01, f2_of(xq.x, xq.y), s);
+      s = f2_fma(q23, f2_of(xq.z, xq.w), s);
+    }
+    return f2_sum(s);
+  }
+};
+template <> struct FDot<u8b, uint16_t> {
+  static constexpr int kN = 16;
+  __device__ __forceinline__ static float run(const uint4& w, const uint4* xp) {
+    const uint4 x0 = xp[0];
+    const uint4 x1 = xp[32];
+    f2_t s = u8x4_dot2(w.x, x0.x, x0.y, 0ull);
+    s = u8x4_dot2(w.y, x0.z, x0.w, s);
+    s = u8x4_dot2(w.z, x1.x, x1.y, s);
+    s = u8x4_dot2(w.w, x1.z, x1.w, s);
+    return f2_sum(s);
+  }
+};
 template <> struct FDot<int8_t, uint16_t> {
   static constexpr int kN = 16;
   __device__ __forceinline__ static float run(const uint4& w, const uint4* xp) {
@@ -760,6 +803,7 @@ cudaError_t launch_w13_flat(ExpertRef ex, WType wt, const void* u, int u_f32, fl
     case W_BF16: return fg_launch<__nv_bfloat16, uint16_t, 0>(a, s, pdl);
     case W_F32: return fg_launch<float, float, 0>(a, s, pdl);
     case W_I8: return lowbit_xf32() ? fg_launch<int8_t, float, 0>(a, s, pdl) : fg_launch<int8_t, uint16_t, 0>(a, s, pdl);
+    case W_U8: return lowbit_xf32() ? fg_launch<u8b, float, 0>(a, s, pdl) : fg_launch<u8b, uint16_t, 0>(a, s, pdl);
     case W_NF4: return fg_launch<nf4x2, uint16_t, 0>(a, s, pdl);  // bf16 x measured faster for NF4
     case W_F8: return lowbit_xf32() ? fg_launch<fp8e4, float, 0>(a, s, pdl) : fg_launch<fp8e4, uint16_t, 0>(a, s, pdl);
   }
@@ -775,6 +819,7 @@ cudaError_t launch_w2_flat(ExpertRef ex, WType wt, const float* act, const float
     case W_BF16: return fg_launch<__nv_bfloat16, float, 1>(a, s, pdl);
     case W_F32: return fg_launch<float, float, 1>(a, s, pdl);
     case W_I8: return fg_launch<int8_t, float, 1>(a, s, pdl);
+    case W_U8: return fg_launch<u8b, float, 1>(a, s, pdl);
     case W_NF4: return fg_launch<nf4x2, float, 1>(a, s, pdl);
     case W_F8: return fg_launch<fp8e4, float, 1>(a, s, pdl);
   }
@@ -1139,6 +1184,7 @@ cudaError_t launch_w13_multi(int n, const ExpertRef* ex, WType wt, const void* u
     case W_BF16: return fg_multi_launch<__nv_bfloat16, uint16_t, 0>(m, s, pdl);
     case W_F32: return fg_multi_launch<float, float, 0>(m, s, pdl);
     case W_I8: return lowbit_xf32() ? fg_multi_launch<int8_t, float, 0>(m, s, pdl) : fg_multi_launch<int8_t, uint16_t, 0>(m, s, pdl);
+    case W_U8: return lowbit_xf32() ? fg_multi_launch<u8b, float, 0>(m, s, pdl) : fg_multi_launch<u8b, uint16_t, 0>(m, s, pdl);
     case W_NF4: return fg_multi_launch<nf4x2, uint16_t, 0>(m, s, pdl);
     case W_F8: return lowbit_xf32() ? fg_multi_launch<fp8e4, float, 0>(m, s, pdl) : fg_multi_launch<fp8e4, uint16_t, 0>(m, s, pdl);
   }
@@ -1165,6 +1211,7 @@ cudaError_t launch_w2_multi(int n, const ExpertRef* ex, WType wt, const float* a
     case W_BF16: return fg_multi_launch<__nv_bfloat16, float, 1>(m, s, pdl);
     case W_F32: return fg_multi_launch<float, float, 1>(m, s, pdl);
     case W_I8: return fg_multi_launch<int8_t, float, 1>(m, s, pdl);
+    case W_U8: return fg_multi_launch<u8b, float, 1>(m, s, pdl);
     case W_NF4: return fg_multi_launch<nf4x2, float, 1>(m, s, pdl);
     case W_F8: return fg_multi_launch<fp8e4, float, 1>(m, s, pdl);
   }
@@ -1238,6 +1285,7 @@ cudaError_t launch_expert_fused(ExpertRef ex, const void* w2_direct, const float
     case W_BF16: return fused_launch<__nv_bfloat16, uint16_t>(a13, a2, s, pdl);
     case W_F32: return fused_launch<float, float>(a13, a2, s, pdl);
     case W_I8: return lowbit_xf32() ? fused_launch<int8_t, float>(a13, a2, s, pdl) : fused_launch<int8_t, uint16_t>(a13, a2, s, pdl);
+    case W_U8: return lowbit_xf32() ? fused_launch<u8b, float>(a13, a2, s, pdl) : fused_launch<u8b, uint16_t>(a13, a2, s, pdl);
     case W_NF4: return fused_launch<nf4x2, uint16_t>(a13, a2, s, pdl);
     case W_F8: return lowbit_xf32() ? fused_launch<fp8e4, float>(a13, a2, s, pdl) : fused_launch<fp8e4, uint16_t>(a13, a2, s, pdl);
   }

@@ -191,6 +191,8 @@ int gemv_engine() {
 
 cudaError_t launch_w13(ExpertRef ex, WType wt, const void* u, int u_f32, float* a, int d, int F,
                        cudaStream_t s, bool pdl) {
+  if (wt == W_U8)  // flat engine only (the engine picks W_U8 only where it applies)
+    return stream_ok(wt, d) ? launch_w13_flat(ex, wt, u, u_f32, a, d, F, s, pdl) : cudaErrorInvalidValue;
   if (wt == W_NF4 || wt == W_F8)
     return stream_ok(wt, d) ? launch_w13_flat(ex, wt, u, u_f32, a, d, F, s, pdl)
                             : launch_lowbit_small(ex, wt, 0, u, u_f32, d, F, nullptr, a, s);
@@ -209,6 +211,8 @@ cudaError_t launch_w13(ExpertRef ex, WType wt, const void* u, int u_f32, float* 
 
 cudaError_t launch_w2(ExpertRef ex, WType wt, const float* a, const float* gate_w, float* y, int d,
                       int F, cudaStream_t s, bool pdl) {
+  if (wt == W_U8)
+    return stream_ok(wt, F) ? launch_w2_flat(ex, wt, a, gate_w, y, d, F, s, pdl) : cudaErrorInvalidValue;
   if (wt == W_NF4 || wt == W_F8)
     return stream_ok(wt, F) ? launch_w2_flat(ex, wt, a, gate_w, y, d, F, s, pdl)
                             : launch_lowbit_small(ex, wt, 1, a, 1, d, F, gate_w, y, s);

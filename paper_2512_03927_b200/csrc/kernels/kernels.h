@@ -5,7 +5,9 @@
 
 namespace odmoe {
 
-enum WType { W_BF16 = 0, W_F32 = 1, W_I8 = 2, W_NF4 = 3, W_F8 = 4 };
+enum WType { W_BF16 = 0, W_F32 = 1, W_I8 = 2, W_NF4 = 3, W_F8 = 4, W_U8 = 5 };
+// W_U8 (shadow experts on the flat engine only): the INT8-row codes q stored as the byte q + 128,
+// same row scales; the dot product then widens a byte without flipping its sign bit first.
 // W_F8 (shadow experts only, reading Q28): E4M3 codes, one fp32 scale per row (int8's layout).
 // W_NF4 (shadow experts only, reading Q27): two 4-bit codes per byte (low nibble = even column),
 // "scales" = fp32 absmax per 64-weight block of a row, [R][C/64]; expert blob = codes of W13 then
@@ -178,6 +180,7 @@ cudaError_t launch_f32_to_bf16(const float* in, void* out, int64_t n, cudaStream
 
 // Q9 int8-row quantiser of a [R, C] matrix of type wt (bf16 / fp32).
 cudaError_t launch_quantize(const void* w, int64_t R, int64_t C, WType wt, int8_t* q, float* sc,
-                            cudaStream_t s);
+                            cudaStream_t s,
+                            bool biased = false);  // biased: store q + 128 (W_U8)
 
 }  // namespace odmoe

@@ -368,7 +368,12 @@ void build_shadow(Ctx* c, char* staging) {
   const bool nf4 = c->cfg.predictor == ODMOE_PRED_SHADOW_NF4;
   const bool fp8 = c->cfg.predictor == ODMOE_PRED_SHADOW_FP8;
   c->sh_wt = W_I8;
-  c->sh_ewt = nf4 ? W_NF4 : (fp8 ? W_F8 : W_I8);
+  // INT8 experts on the flat engine are stored biased (W_U8: q + 128), which saves the sign flip of
+  // every weight word in the dot product; other shapes keep signed codes (ODMOE_SHADOW_U8=0: A/B)
+  const char* u8e = getenv("ODMOE_SHADOW_U8");
+  const bool u8 = !nf4 && !fp8 && !(u8e && u8e[0] == '0') && gemv_engine() == 2 && stream_ok(W_U8, d) &&
+                  stream_ok(W_U8, F);
+  c->sh_ewt = nf4 ? W_NF4 : (fp8 ? W_F8 : (u8 ? W_U8 : W_I8));
   c->sh_emb = dmalloc<int8_t>(c, (size_t)V * d, "shadow emb");
   c->sh_semb = dmalloc<float>(c, V, "shadow emb scales");
   c->sh_router = dmalloc<int8_t>(c, (size_t)L * E * d, "shadow router");
@@ -414,8 +419,9 @@ void build_shadow(Ctx* c, char* staging) {
         CUDA_OK(c, launch_quantize_fp8(src + (size_t)2 * F * d * c->esz, d, F, c->wt, (uint8_t*)q + (size_t)2 * F * d,
                                        s + 2 * F, c->s_main));
       } else {
-        CUDA_OK(c, launch_quantize(src, 2LL * F, d, c->wt, q, s, c->s_main));
-        CUDA_OK(c, launch_quantize(src + (size_t)2 * F * d * c->esz, d, F, c->wt, q + (size_t)2 * F * d, s + 2 * F, c->s_main));
+        CUDA_OK(c, launch_quantize(src, 2LL * F, d, c->wt, q, s, c->s_main, u8));
+        CUDA_OK(c, launch_quantize(src + (size_t)2 * F * d * c->esz, d, F, c->wt, q + (size_t)2 * F * d, s + 2 * F,
+                                   c->s_main, u8));
       }
       c->sh_blob[i] = q;
       c->sh_sc[i] = s;
