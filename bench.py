@@ -312,6 +312,11 @@ def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    # stdout carries the JSON line alone: native banners written to fd 1 (NCCL's version line under
+    # torchrun) go to stderr; the line itself is written to the saved descriptor.
+    sys.stdout.flush()
+    json_out = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     import faulthandler
     faulthandler.dump_traceback_later(480, repeat=True, file=sys.stderr)  # stack dump if a phase stalls
     import torch
@@ -508,7 +513,7 @@ def main():
             except Exception as e:  # report, never hide
                 line["cpu_baseline"] = {"value": None, "error": repr(e)}
         out = json.dumps(line)
-        print(out, flush=True)
+        print(out, file=json_out, flush=True)
         if args.out:
             with open(args.out, "w") as f:
                 f.write(out + "\n")
