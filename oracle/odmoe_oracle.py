@@ -59,7 +59,8 @@ __all__ = [
     "decode_token_attn", "NF4_CODEBOOK", "NF4_BLOCK", "nf4_codebook_from_quantiles",
     "quantize_nf4_blocks", "dequantize_nf4_blocks", "quantize_model_nf4", "e4m3_values", "round_e4m3",
     "quantize_fp8_rows", "dequantize_fp8_rows", "quantize_model_fp8",
-    "near_tie", "plan_group_size", "plan_groups", "assign_layer", "assign_experts",
+    "near_tie", "tied_run", "ids_excusable", "expected_loads", "shadow_greedy_token", "shadow_decode",
+    "plan_group_size", "plan_groups", "assign_layer", "assign_experts",
     "misprediction_reloads", "max_load_budget", "residency_bound", "recall_eq2", "recall_eq3",
     "recall_bruteforce", "prefill_permutation", "prefill_reference", "expert_counts",
 ]
@@ -319,10 +320,13 @@ def dequantize_int8_rows(q, s):
 
 
 def quantize_model_int8(weights):
-    """Q(W) for every matrix of the model: embedding, routers, experts. Returns a
-    weights dict of the same structure holding the dequantised fp64 values."""
+    """Q(W) for every matrix of the model: embedding, routers, experts and (when present) the
+    LM head, which the shadow needs only to take its own greedy token (cross-token speculation,
+    P:188-203). Returns a weights dict of the same structure holding the dequantised fp64 values."""
     dq = lambda W: dequantize_int8_rows(*quantize_int8_rows(W))  # noqa: E731
     out = {"emb": dq(weights["emb"]), "router": {}, "experts": {}}
+    if "lm_head" in weights:
+        out["lm_head"] = dq(weights["lm_head"])
     for l, Wg in weights["router"].items():
         out["router"][l] = dq(Wg)
         out["experts"][l] = {e: tuple(dq(M) for M in mats) for e, mats in weights["experts"][l].items()}
@@ -503,6 +507,34 @@ def shadow_predict(shadow_weights, main_token: int, k: int, eps: float = 1e-5):
     return P, recs
 
 
+def shadow_greedy_token(shadow_weights, h_L, eps: float = 1e-5) -> int:
+    """The shadow's own next token: greedy argmax of its quantised LM head on RMSNorm(h_L) (the
+    paper's "the quantized model may generate a different token"; lowest id on ties)."""
+    return greedy_argmax(final_logits(shadow_weights["lm_head"], h_L, eps))
+
+
+def shadow_decode(shadow_weights, main_tokens, k: int, period: int, eps: float = 1e-5):
+    """SEP with token alignment period T_p ("align the tokens ... once every few
+    autoregression iterations"; Fig. 6 T_i; S:165-173 shadow_decode_step). Iteration n (0-based)
+    predicts the main model's iteration n, whose input is main_tokens[n]. If n mod T_p == 0 the
+    shadow's input is the main token (token alignment); otherwise it is the shadow's OWN greedy
+    token from iteration n-1. Each iteration runs all L layers (no attention: no KV state, so only
+    the token axis of alignment exists, reading Q22). Returns (P [N][L] lists of k ids in rank
+    order, shadow input tokens [N], shadow output tokens [N])."""
+    if period < 1:
+        raise ValueError("alignment period must be >= 1")
+    P, t_in, t_out = [], [], []
+    own = None
+    for n, tm in enumerate(main_tokens):
+        t = int(tm) if (n % period == 0 or own is None) else own
+        preds, recs = shadow_predict(shadow_weights, t, k, eps)
+        own = shadow_greedy_token(shadow_weights, recs[-1]["h_next"], eps)
+        P.append(preds)
+        t_in.append(t)
+        t_out.append(own)
+    return P, t_in, t_out
+
+
 def near_tie(r, k: int, rel: float = 1e-3) -> bool:
     """North-star excuse window (reading Q4): the oracle's k-th and (k+1)-th largest logits
     differ by less than rel * max(|r_(k)|, |r_(k+1)|); both zero counts as a tie."""
@@ -513,6 +545,44 @@ def near_tie(r, k: int, rel: float = 1e-3) -> bool:
     if a == 0.0 and b == 0.0:
         return True
     return abs(a - b) < rel * max(abs(a), abs(b))
+
+
+def _close(a: float, b: float, rel: float) -> bool:
+    return (a == 0.0 and b == 0.0) or abs(a - b) < rel * max(abs(a), abs(b))
+
+
+def tied_run(r, k: int, rel: float = 1e-3):
+    """The tied run at the selection boundary (reading Q4; SURVEY §8(c) Parity 2): every index whose
+    logit lies inside the near-tie window of the k-th largest logit r_(k), i.e.
+    |r_e - r_(k)| < rel * max(|r_e|, |r_(k)|) (both zero counts). Contains the k-th itself."""
+    r = [float(x) for x in np.asarray(r).ravel()]
+    kth = sorted(r, reverse=True)[k - 1]
+    return {e for e, x in enumerate(r) if _close(x, kth, rel)}
+
+
+def ids_excusable(ids, r, k: int, rel: float = 1e-3):
+    """Parity protocol 2 (north_star: "Selected expert IDs must match the oracle exactly, except
+    where the oracle's k-th and (k+1)-th logits differ by less than 1e-3 relative").
+    `ids` (k ids in rank order) is accepted iff
+      (a) they are k distinct indices;
+      (b) as a set they equal top_k(r, k), or near_tie(r, k) holds and the symmetric difference with
+          top_k lies inside tied_run(r, k) (only members of the tied run were swapped);
+      (c) the rank order is by descending oracle logit, except between two near-equal logits.
+    Returns (ok, excused) with excused = (ids != top_k(r, k))."""
+    ids = [int(x) for x in ids]
+    ref = top_k(r, k)
+    if ids == ref:
+        return True, False
+    rr = [float(x) for x in np.asarray(r).ravel()]
+    if len(set(ids)) != k or any(e < 0 or e >= len(rr) for e in ids):
+        return False, True
+    diff = set(ids) ^ set(ref)
+    if diff and not (near_tie(r, k, rel) and diff <= tied_run(r, k, rel)):
+        return False, True
+    for a, b in zip(ids, ids[1:]):
+        if rr[b] > rr[a] and not _close(rr[a], rr[b], rel):
+            return False, True
+    return True, True
 
 
 # ---------------------------------------------------------------- O9 placement (P:104-139)
@@ -557,6 +627,20 @@ def misprediction_reloads(true_S, resident):
     if len(stale_workers) < len(missing):
         raise ValueError("not enough stale workers for the reload set")
     return list(zip(missing, stale_workers[: len(missing)]))
+
+
+def expected_loads(true_S, issued) -> int:
+    r"""Expert loads of one decode token ("minimal I/O bandwidth waste"; "waits for the
+    completion of expert reloading"; SURVEY §8(c) "Loader accounting (a6 <-> a12)"). Per layer l the
+    loader performs the loads issued from the prediction before the router ran, I_l, and after the
+    router the reloads S_l \ I_l (handle_misprediction): |I_l| + |S_l \ I_l| =
+    k + |I_l \ S_l|. Summed over layers: L*k + (number of issued loads that were wrong). `true_S`,
+    `issued`: per-layer id collections. Bytes = loads x blob bytes."""
+    total = 0
+    for S, I in zip(true_S, issued):
+        S, I = set(int(x) for x in S), set(int(x) for x in I)
+        total += len(I) + len(S - I)
+    return total
 
 
 def max_load_budget(t_M: float, t_W: float, n_groups: int) -> float:

@@ -535,3 +535,123 @@ def test_paper_constants_shapes():
     assert expert_fp32 < g["worker_GB_max"] * 1e9
     assert abs(E * L * expert_fp32 / 1e9 - g["fully_cached_GB"]) < 1.0
     assert abs(E * L * 3 * d * F / 1e9 - g["shadow_GB"]) < 0.5
+
+
+# ------------------------------------------------------------------ parity protocol (north_star; Q4)
+def test_near_tie_and_tied_run_golden_cases():
+    """The excuse window of the parity protocol, pinned case by case: k-th vs (k+1)-th (not
+    k-1 / k), relative not absolute, both zero, negatives, just inside / just outside."""
+    for c in gold("near_tie_cases.json")["near_tie"]:
+        assert O.near_tie(c["r"], c["k"]) == c["tie"], c
+        assert O.tied_run(c["r"], c["k"]) == set(c["run"]), c
+
+
+def test_ids_excusable_golden_cases():
+    """A GPU set may differ from the oracle's only by swapping members of the tied run; rank order
+    must follow the oracle logits except between near-equal ones."""
+    for c in gold("near_tie_cases.json")["ids"]:
+        assert O.ids_excusable(c["ids"], c["r"], c["k"]) == (c["ok"], c["excused"]), c
+
+
+def test_ids_excusable_bruteforce_small():
+    """Brute force over every ordered k-tuple on small integer logits with ties: accepted tuples
+    are exactly those whose sorted logit vector equals the top-k's (exact ties only, so the
+    window reduces to equality) and that are ordered by non-increasing logit."""
+    rng = np.random.default_rng(21)
+    for _ in range(200):
+        E, k = int(rng.integers(2, 6)), int(rng.integers(1, 4))
+        k = min(k, E)
+        r = rng.integers(-2, 3, size=E).astype(float) * 4.0  # ties or gaps >= 4 (far outside 1e-3)
+        want = sorted(r, reverse=True)[:k]
+        for ids in permutations(range(E), k):
+            vals = [r[i] for i in ids]
+            expect = sorted(vals, reverse=True) == want and vals == sorted(vals, reverse=True)
+            ok, _ = O.ids_excusable(list(ids), r, k)
+            assert ok == expect, (r, k, ids)
+
+
+def test_final_logits_apply_the_rmsnorm():
+    """z = W_o RMSNorm(h): with W_o = I and h = [3, 4], z = h / sqrt(12.5 + 1e-5) (closed form); a
+    missing or doubled norm is off by >= 4e-6 relative."""
+    z = O.final_logits(np.eye(2), np.array([3.0, 4.0]))
+    want = np.array([3.0, 4.0]) / math.sqrt(12.5 + 1e-5)
+    assert np.allclose(z, want, rtol=1e-14, atol=0)
+    assert not np.allclose(z, np.array([3.0, 4.0]), rtol=1e-6)
+    assert not np.allclose(z, O.rms_norm(want), rtol=1e-6, atol=0)
+
+
+# ------------------------------------------------------------------ loader accounting (a6 <-> a12)
+def test_expected_loads_spec_examples():
+    for c in gold("loads_S311.json")["cases"]:
+        assert O.expected_loads(c["S"], c["I"]) == c["loads"], c
+
+
+def test_expected_loads_recall_identity_on_random_records():
+    """when every layer's k predicted experts were issued before its router,
+    loads = L*k*(2 - recall(n)) exactly (recall from Eq. 2 over one token); PERFECT => L*k."""
+    rng = np.random.default_rng(22)
+    for _ in range(300):
+        L, k = int(rng.integers(1, 9)), int(rng.integers(1, 4))
+        E = k + int(rng.integers(0, 5))
+        S = [list(rng.choice(E, size=k, replace=False)) for _ in range(L)]
+        P = [list(rng.choice(E, size=k, replace=False)) for _ in range(L)]
+        c = np.array([[[len(set(s) & set(p)) for s, p in zip(S, P)]]])
+        rec = O.recall_eq2(c, np.ones((1, 1), dtype=int), k)[0]
+        assert Fraction(O.expected_loads(S, P)) == L * k * (2 - rec)
+        assert O.expected_loads(S, S) == L * k
+        assert O.expected_loads(S, [[] for _ in S]) == L * k
+
+
+def test_misprediction_reload_set_is_true_minus_issued():
+    """the reload set is exactly true \\ resident, one reload per stale worker."""
+    rng = np.random.default_rng(23)
+    for _ in range(300):
+        E, k = 8, 2
+        S = list(rng.choice(E, size=k, replace=False))
+        I = list(rng.choice(E, size=k, replace=False))
+        rel = O.misprediction_reloads(S, {int(e): 0 for e in I})
+        assert sorted(e for e, _ in rel) == sorted(set(int(x) for x in S) - set(int(x) for x in I))
+        assert len(rel) + len(set(I)) == O.expected_loads([S], [I])
+
+
+# ------------------------------------------------------------------ cross-token speculation (P:188-203)
+@pytest.fixture(scope="module")
+def tiny_shadow(tiny_fp32):
+    return O.quantize_model_int8(tiny_fp32)
+
+
+def test_shadow_decode_period_one_is_mode_a(tiny_fp32, tiny_shadow):
+    """T_p = 1 aligns every iteration: identical to the token-aligned shadow (Mode A) per token."""
+    toks, _ = O.decode_sequence(tiny_fp32, 11, 6, TINY.k)
+    main_in = [11] + toks[:-1]
+    P, t_in, _ = O.shadow_decode(tiny_shadow, main_in, TINY.k, period=1)
+    assert t_in == main_in
+    for n, t in enumerate(main_in):
+        assert P[n] == O.shadow_predict(tiny_shadow, t, TINY.k)[0]
+
+
+def test_shadow_decode_same_precision_recall_one_for_every_period(tiny_fp32):
+    """S:171/S:217 generalised: a shadow identical to the main model generates the main model's
+    own tokens, so its predictions are exact for every alignment period."""
+    toks, routes = O.decode_sequence(tiny_fp32, 11, 8, TINY.k)
+    main_in = [11] + toks[:-1]
+    for period in (1, 2, 4, 8):
+        P, t_in, t_out = O.shadow_decode(tiny_fp32, main_in, TINY.k, period)
+        assert t_in == main_in and t_out == toks
+        assert all(sorted(P[n][l]) == routes[n][l] for n in range(8) for l in range(TINY.L))
+
+
+def test_shadow_decode_unaligned_iterations_ignore_the_main_token(tiny_fp32, tiny_shadow):
+    """At n mod T_p != 0 the shadow consumes its own previous token: the main token there has no
+    influence, and t_in[n] = t_out[n-1]."""
+    toks, _ = O.decode_sequence(tiny_fp32, 5, 6, TINY.k)
+    main_in = [5] + toks[:-1]
+    P, t_in, t_out = O.shadow_decode(tiny_shadow, main_in, TINY.k, period=3)
+    scrambled = [t if n % 3 == 0 else (t + 101) % TINY.V for n, t in enumerate(main_in)]
+    P2, t_in2, _ = O.shadow_decode(tiny_shadow, scrambled, TINY.k, period=3)
+    assert P2 == P and t_in2 == t_in
+    for n in range(1, 6):
+        if n % 3:
+            assert t_in[n] == t_out[n - 1]
+        else:
+            assert t_in[n] == main_in[n]
