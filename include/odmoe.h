@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define ODMOE_ABI_VERSION 1
+#define ODMOE_ABI_VERSION 2
 
 typedef enum {
   ODMOE_OK = 0,
@@ -114,15 +114,27 @@ typedef struct {
   const void* nccl_id;       /* 128-byte ncclUniqueId from rank 0 (NULL when world_size == 1)          */
 } odmoe_config;
 
-/* One per layer per decode step (S:154-157 RoutingRecord). k <= 8. */
+/* One per layer per decode step (S:154-157 RoutingRecord). k <= 8. Filled on every rank that passes
+ * a non-NULL rec; true_ids / pred_ids / weights / correct are the same on every rank, the load fields
+ * (issued_ids, reload_ids, n_reloads, load_wait_us) describe THIS rank's loads. */
 typedef struct {
   int32_t true_ids[8];       /* main-router top-k, rank order                                          */
-  int32_t pred_ids[8];       /* predictor's ids for this layer (-1 = none)                             */
+  int32_t pred_ids[8];       /* the predictor's ids for this layer (Mode A for the shadows; -1 = none) */
   float weights[8];          /* mixture weights, aligned with true_ids                                 */
-  int32_t pred_available;    /* 0 => no prediction existed when the router ran (c = 0)          */
+  int32_t pred_available;    /* 1 => the predictor produced ids for this layer in this step (Eq. 3
+                                counts them: prediction accuracy); 0 => none (c = 0)     */
   int32_t correct;           /* c(n, l) = |true ∩ pred| (Eq. 2 numerator term)                   */
   int32_t n_reloads;         /* experts loaded after the router because the prediction missed  */
-  float load_wait_us;        /* host-observed wait for this layer's experts                            */
+  float load_wait_us;        /* host-observed wait for this layer's router ids                         */
+  int32_t pred_in_time;      /* 1 => pred_ids had reached the host BEFORE this layer's router ids did
+                                (the prediction could drive the loads: "prediction
+                                available at decision time")                                          */
+  int32_t correct_in_time;   /* correct if pred_in_time else 0 (the conservative c of S:197)           */
+  int32_t issued_ids[8];     /* experts of this layer whose loads THIS rank issued before the router ids
+                                reached the host (predicted loads, incl. ones later stopped), ascending,
+                                -1 padded                                                             */
+  int32_t reload_ids[8];     /* experts of this layer THIS rank loaded after the router (misprediction
+                                fallback), ascending, -1 padded                    */
 } odmoe_layer_record;
 
 typedef struct {
@@ -147,6 +159,10 @@ typedef struct {
   int64_t refine_correct, refine_total; /* Σc, Σk of the refined predictions (rank 0)                  */
   double ms_attn;                    /* attention block kernels (QKV, RoPE, attention, W_o), rank 0     */
   int64_t n_attn;
+  int64_t correct_in_time;           /* Σc over layers whose prediction arrived before the router */
+  int64_t spec_steps;                /* decode steps whose predictions came from a speculative shadow pass
+                                        (token alignment period > 1, the shadow's own token)            */
+  int64_t early_loads;               /* loads issued for the NEXT token while this one was decoding     */
 } odmoe_stats;
 
 /* ------------------------------------------------------------------ lifecycle */
@@ -301,6 +317,46 @@ odmoe_status odmoe_load_wait(void* ctx, int layer, int expert, void** w13, void*
  * it afterward"; Q16). E_STATE if the expert is not resident/loading. */
 odmoe_status odmoe_evict(void* ctx, int layer, int expert);
 
+/* Event trace of the decode engine (S:350-358 event schema; Eq. 1 analysis). Enabled with
+ * odmoe_set_option(ctx, 7, 1); every decode step then appends events on this rank. Times are device
+ * times in microseconds since the trace was enabled (CUDA events on the compute and copy streams of
+ * this GPU); host-only events carry t_us = NaN. */
+typedef enum {
+  ODMOE_EV_STEP_START = 0,    /* compute stream reached the start of decode step `step`            */
+  ODMOE_EV_LOAD_ISSUE = 1,    /* host: load of (layer, expert) submitted to the loader; l_cur = the
+                                 main layer the host was at (the lookahead window, Q11: layer (counted
+                                 from this step's layer 0; L + m for layer m of the next token) must
+                                 be <= l_cur + D); aux = 0 predicted, 1 reload after the router,
+                                 2 refined prediction, 3 next-token (cross-token speculation)       */
+  ODMOE_EV_LOAD_START = 2,    /* copy engine began the first chunk (after the slot's free event)   */
+  ODMOE_EV_LOAD_END = 3,      /* copy engine finished the last chunk it issued; bytes = bytes copied */
+  ODMOE_EV_LOAD_CANCEL = 4,   /* host: a mispredicted load was stopped                      */
+  ODMOE_EV_ROUTER_DONE = 5,   /* layer's routing known on this GPU (router kernel, or the packet
+                                 broadcast at N > 1)                                                  */
+  ODMOE_EV_COMPUTE_START = 6, /* expert kernel of (layer, expert) may start: its load has landed and
+                                 the compute stream reached it                                        */
+  ODMOE_EV_COMPUTE_END = 7,   /* expert kernel of (layer, expert) finished                          */
+  ODMOE_EV_MISPREDICT = 8,    /* host: (layer, expert) was routed but not loaded -> reload   */
+  ODMOE_EV_STEP_END = 9       /* compute stream finished the step (token on the host next)          */
+} odmoe_event_type;
+
+typedef struct {
+  int32_t type;              /* odmoe_event_type                                                      */
+  int32_t step;              /* decode step (ctx-local counter) the event belongs to                  */
+  int32_t layer, expert;     /* -1 when not applicable                                                */
+  int32_t slot;              /* device expert slot, -1 when not applicable                            */
+  int32_t l_cur;             /* LOAD_ISSUE: main layer at issue time (-1 = before layer 0's router)    */
+  int32_t aux;               /* LOAD_ISSUE kind (see above)                                           */
+  int32_t rank;              /* this rank                                                              */
+  int64_t bytes;             /* LOAD_END / LOAD_CANCEL: bytes copied for this load                    */
+  double t_us;               /* device time (µs since the trace was enabled), NaN for host-only events */
+} odmoe_trace_event;
+
+/* Move up to `cap` resolved trace events (in emission order) into `out` (host, caller-owned) and
+ * set *n_out; events whose device times are not final yet (loads still in flight) stay queued.
+ * E_STATE if tracing was never enabled. */
+odmoe_status odmoe_trace_read(void* ctx, odmoe_trace_event* out, int32_t cap, int32_t* n_out);
+
 /* Runtime options (take effect at the next decode step; every rank must set the same value):
  *   key 1 = lookahead D (>= 1, Q11); key 2 = predictor (odmoe_predictor; the shadow predictors
  *   need a ctx created with a shadow predictor: E_STATE otherwise); key 3 = refine_depth R (0..4;
@@ -308,7 +364,14 @@ odmoe_status odmoe_evict(void* ctx, int layer, int expert);
  *   ctx only; 0 starts a new sequence; E_RANGE outside [0, max_seq)); key 5 = KV alignment of the
  *   shadow (Fig. 3: 1 = attend over the main model's cache (default), 0 = the shadow keeps
  *   its own cache from its own passes; attention ctx with a shadow); key 6 = time_kernels level (0..2,
- *   see odmoe_config). E_CONFIG on a bad key/value. */
+ *   see odmoe_config); key 7 = event trace (0 off, 1 on; odmoe_trace_read); key 8 = token alignment
+ *   period T_p of the shadow (Fig. 6 "T_i": 1 = the main model's token every iteration
+ *   (Mode A, default); T_p > 1 = at iterations n with n mod T_p != 0 (n counted from the first step
+ *   or the last key-8 / key-4 call) the shadow decodes with its OWN greedy token from its INT8 LM
+ *   head, so its pass for token n+1 starts right after its pass for n, before the main model has
+ *   finished n, and loads for layers 0.. of n+1 may be issued inside the lookahead window (cross-
+ *   token speculation); shadow predictors only, T_p in 1..64). E_CONFIG on a bad
+ *   key/value. */
 odmoe_status odmoe_set_option(void* ctx, int key, int64_t value);
 
 /* SEP Mode A (Q10): run the shadow from the main model's token `token`

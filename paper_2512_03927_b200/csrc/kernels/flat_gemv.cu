@@ -674,6 +674,7 @@ __device__ __forceinline__ void flat_phase(const FlatArgs& a, uint8_t* sm, const
       float s = 0.f;
 #pragma unroll
       for (int w = 0; w < kFG_WARPS; ++w) s += part[w * a.rows_cap + r];
+      if (!kNF4 && sc != nullptr) s *= sc[rb + r];  // int8-row LM head (the shadow's own token)
       if (a.out) a.out[rb + r] = s;
       const unsigned long long key = fg_argmax_key(s, (int)(rb + r));
       best = key > best ? key : best;
@@ -926,15 +927,17 @@ cudaError_t launch_gemv_acc(const void* W, const float* scales, WType wt, int R,
 }
 
 cudaError_t launch_lm_head_flat(const float* h, const void* W, WType wt, int V, int d, float eps,
-                                int32_t* token_out, float* logits, void* scratch, cudaStream_t s, bool pdl) {
+                                int32_t* token_out, float* logits, void* scratch, cudaStream_t s, bool pdl,
+                                const float* scales) {
   FlatArgs a{};
-  a.ex = direct_ref(W, nullptr, 0); a.second = 0; a.R = V; a.C = d; a.out = logits; a.h = h; a.eps = eps;
+  a.ex = direct_ref(W, scales, 0); a.second = 0; a.R = V; a.C = d; a.out = logits; a.h = h; a.eps = eps;
   a.partial = reinterpret_cast<unsigned long long*>(scratch);
   a.ticket = reinterpret_cast<unsigned int*>(a.partial + 1024);
   a.token_out = token_out;
   switch (wt) {
     case W_BF16: return fg_launch<__nv_bfloat16, uint16_t, 2>(a, s, pdl);
     case W_F32: return fg_launch<float, float, 2>(a, s, pdl);
+    case W_I8: return fg_launch<int8_t, uint16_t, 2>(a, s, pdl);
     default: return cudaErrorInvalidValue;
   }
 }

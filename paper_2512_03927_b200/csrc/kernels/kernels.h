@@ -61,7 +61,8 @@ cudaError_t launch_w13_flat(ExpertRef ex, WType wt, const void* u, int u_f32, fl
 cudaError_t launch_w2_flat(ExpertRef ex, WType wt, const float* act, const float* gate_w, float* y, int d,
                            int F, cudaStream_t s, bool pdl);
 cudaError_t launch_lm_head_flat(const float* h, const void* W, WType wt, int V, int d, float eps,
-                                int32_t* token_out, float* logits, void* scratch, cudaStream_t s, bool pdl);
+                                int32_t* token_out, float* logits, void* scratch, cudaStream_t s, bool pdl,
+                                const float* scales = nullptr);
 bool use_fused_expert();  // env ODMOE_FUSED=0 disables (A/B)
 // Graph capture of cooperative kernels: restart the grid-barrier targets of stream s at 0 and return
 // its arrival counter (the captured step memsets it to 0 first, so every replay sees the same targets).
@@ -103,9 +104,10 @@ cudaError_t launch_lm_head_stream(const float* h, const void* W, WType wt, int V
                                   int32_t* token_out, float* logits, void* scratch, cudaStream_t s);
 
 // a10: token = argmax_v (W_o RMSNorm(h))_v, lowest id on ties. scratch >= 8*(grid+2) bytes.
+// W_I8 (the shadow's LM head, cross-token speculation): logit_v = scales[v] * (q_v . bf16(RMSNorm(h))).
 cudaError_t launch_lm_head(const float* h, const void* W, WType wt, int V, int d, float eps,
                            int32_t* token_out, float* logits, void* scratch, cudaStream_t s,
-                           bool pdl = false);
+                           bool pdl = false, const float* scales = nullptr);
 
 // a1: h = Emb[token] (fp32); int8 rows use emb_scale.
 cudaError_t launch_embed(const void* emb, const float* emb_scale, WType wt, const int32_t* token,

@@ -23,8 +23,8 @@ __device__ __forceinline__ unsigned long long argmax_key(float v, int id) {
 
 template <typename WT, int U>
 __global__ void __launch_bounds__(kLmThreads, 1)
-lm_head_kernel(const float* __restrict__ h, const WT* __restrict__ W, int V, int d, float eps,
-               float* __restrict__ logits, unsigned long long* __restrict__ partial,
+lm_head_kernel(const float* __restrict__ h, const WT* __restrict__ W, const float* __restrict__ sc, int V, int d,
+               float eps, float* __restrict__ logits, unsigned long long* __restrict__ partial,
                unsigned int* __restrict__ ticket, int32_t* __restrict__ token_out) {
   extern __shared__ __align__(16) float us[];
   __shared__ float red[kLmWarps];
@@ -78,6 +78,7 @@ lm_head_kernel(const float* __restrict__ h, const WT* __restrict__ W, int V, int
     }
     acc = warp_sum(acc);
     if (lane == 0) {
+      if (sc) acc *= sc[r];
       if (logits) logits[r] = acc;
       const unsigned long long key = argmax_key(acc, (int)r);
       best = key > best ? key : best;
@@ -107,7 +108,7 @@ lm_head_kernel(const float* __restrict__ h, const WT* __restrict__ W, int V, int
 }
 
 template <typename WT>
-static cudaError_t lm_impl(const float* h, const void* W, int V, int d, float eps,
+static cudaError_t lm_impl(const float* h, const void* W, const float* sc, int V, int d, float eps,
                            int32_t* token_out, float* logits, void* scratch, cudaStream_t s) {
   constexpr int U = 16;
   const int sms = num_sms();
@@ -117,19 +118,22 @@ static cudaError_t lm_impl(const float* h, const void* W, int V, int d, float ep
   const size_t smem = (size_t)d * sizeof(float);
   auto kern = lm_head_kernel<WT, U>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<grid, kLmThreads, smem, s>>>(h, (const WT*)W, V, d, eps, logits, partial, ticket, token_out);
+  kern<<<grid, kLmThreads, smem, s>>>(h, (const WT*)W, sc, V, d, eps, logits, partial, ticket, token_out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_lm_head(const float* h, const void* W, WType wt, int V, int d, float eps,
-                           int32_t* token_out, float* logits, void* scratch, cudaStream_t s, bool pdl) {
+                           int32_t* token_out, float* logits, void* scratch, cudaStream_t s, bool pdl,
+                           const float* scales) {
   if (stream_ok(wt, d)) {
-    if (gemv_engine() == 2) return launch_lm_head_flat(h, W, wt, V, d, eps, token_out, logits, scratch, s, pdl);
+    if (gemv_engine() == 2 || wt == W_I8)
+      return launch_lm_head_flat(h, W, wt, V, d, eps, token_out, logits, scratch, s, pdl, scales);
     if (gemv_engine() == 1) return launch_lm_head_stream(h, W, wt, V, d, eps, token_out, logits, scratch, s);
   }
   switch (wt) {
-    case W_BF16: return lm_impl<__nv_bfloat16>(h, W, V, d, eps, token_out, logits, scratch, s);
-    case W_F32: return lm_impl<float>(h, W, V, d, eps, token_out, logits, scratch, s);
+    case W_BF16: return lm_impl<__nv_bfloat16>(h, W, nullptr, V, d, eps, token_out, logits, scratch, s);
+    case W_F32: return lm_impl<float>(h, W, nullptr, V, d, eps, token_out, logits, scratch, s);
+    case W_I8: return lm_impl<int8_t>(h, W, scales, V, d, eps, token_out, logits, scratch, s);
     default: return cudaErrorInvalidValue;
   }
 }

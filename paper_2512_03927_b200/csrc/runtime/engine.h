@@ -152,8 +152,38 @@ struct Ctx {
   int32_t* h_tok = nullptr;      // [2]: in, out
   int32_t* h_flag = nullptr;
   cudaEvent_t ev_ids = nullptr, ev_tok = nullptr, ev_shadow_done = nullptr, ev_step = nullptr;
-  std::vector<cudaEvent_t> ev_pred;  // [L] (per layer at N = 1; per chunk at N > 1)
+  cudaEvent_t* ev_pred = nullptr;    // [L] view of ev_pred_all for this step's buffer (per layer at N = 1;
+                                     // per chunk at N > 1)
   int pred_chunk = 4;
+
+  // Prediction buffers: the shadow pass of step n writes buffer n & 1 (so a speculative pass for
+  // n + 1 can run while step n still reads its own); buffer 2 belongs to odmoe_predict_ahead.
+  // sh_ids / h_pred / sh_logits / dbg_sh_h / dbg_sh_u / ev_pred are views of this step's buffer.
+  static constexpr int kPredBufs = 3;
+  int32_t* sh_ids_all = nullptr;        // device [3][L][k]
+  int32_t* h_pred_all = nullptr;        // pinned [3][L][k]
+  float* sh_logits_all = nullptr;       // device [3][L][E]
+  float* dbg_sh_h_all = nullptr;        // device [3][L][d] (debug capture)
+  char* dbg_sh_u_all = nullptr;         // device [3][L][d*4] (debug capture)
+  float* dbg_sh_hf_all = nullptr;       // device [3][d]: the shadow's final hidden state (debug capture)
+  std::vector<cudaEvent_t> ev_pred_all; // [3][L]
+  int cur_buf = 0;
+
+  // Cross-token speculation (token alignment period T_p > 1): at iterations
+  // n with n mod T_p != 0 the shadow decodes with its own greedy token (INT8-row LM head), so its pass
+  // for n + 1 is enqueued right after the pass for n and loads of the next token's first layers may
+  // be issued inside the lookahead window while the main model still decodes n.
+  void* sh_lm = nullptr;                // shadow LM head [V][d] (int8-row; main / bf16 weights for SAME / BF16)
+  float* sh_slm = nullptr;              // its row scales [V] (int8)
+  int32_t* sh_tok = nullptr;            // device [3]: the shadow's own greedy token of each buffer's pass
+  void* sh_lmscratch = nullptr;         // argmax scratch of the shadow LM head (own ticket)
+  float* sh_lmlogits = nullptr;         // device [V] (debug capture)
+  int align_period = 1;                 // T_p
+  int64_t align_n = 0;                  // iteration index since the last alignment reset
+  int64_t spec_step = -1;               // the step whose shadow pass is already enqueued (speculative)
+  int next_plan_nx = 0;                 // next layer of the NEXT token whose predicted loads are unplanned
+  std::vector<char> nx_ready;           // [L] next token's prediction of layer m on the host
+  std::vector<int32_t> nx_tbl;          // [L][k]
 
   ncclComm_t comm = nullptr, comm_pred = nullptr;
 
@@ -200,6 +230,26 @@ struct Ctx {
   std::vector<cudaEvent_t> tev_pool;
 
   odmoe_stats stats{};
+
+  // event trace (option key 7; odmoe_trace_read). Entries are kept in emission order; an entry is
+  // resolved when its device event (if any) has completed and, for load entries, its request settled.
+  struct TraceRec {
+    odmoe_trace_event ev;
+    cudaEvent_t e = nullptr;               // timing event (nullptr: host-only entry)
+    std::shared_ptr<LoadReq> req;          // load entries: bytes + settled state
+    bool own_event = true;                 // return `e` to the pool on resolution
+  };
+  int trace = 0;
+  cudaEvent_t tr_origin = nullptr;
+  std::vector<TraceRec> tr_pending;
+  std::vector<odmoe_trace_event> tr_done;
+  std::vector<cudaEvent_t> tr_pool;
+
+  // per-step load bookkeeping for the layer records (this rank): experts whose loads were issued
+  // before the router ids reached the host / loaded after them (misprediction fallback)
+  std::vector<std::vector<int>> issued_pre, reloaded;   // [L]
+  std::vector<std::vector<int>> issued_nx;              // [L] the next token's early loads
+  std::vector<char> in_time;                            // [L] prediction on the host before the router ids
 
   // prefill: batch buffers sized for T_cap tokens, E/G expert slots x 2 (double buffer)
   int T_cap = 0;

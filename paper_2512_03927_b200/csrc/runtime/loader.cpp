@@ -62,10 +62,28 @@ bool Loader::is_done(const std::shared_ptr<LoadReq>& r) {
   return r->done;
 }
 
+bool Loader::settled(const std::shared_ptr<LoadReq>& r, int64_t* bytes) {
+  std::lock_guard<std::mutex> lk(mu_);
+  if (bytes) *bytes = r->issued;
+  return r->fully_issued || r->cancelled || err_.load() != cudaSuccess || !started_;
+}
+
 void Loader::run() {
   cudaSetDevice(device_);
   std::unique_lock<std::mutex> lk(mu_);
   for (;;) {
+    // After a copy-stream error nothing more will land: hand the chunk events back, drop every
+    // request (waiters see err_) and leave as soon as stop() asks, without waiting for inflight_.
+    if (err_.load() != cudaSuccess) {
+      for (auto& c : inflight_) ev_pool_.push_back(c.ev);
+      inflight_.clear();
+      for (auto& r : pending_) r->cancelled = true;
+      pending_.clear();
+      cv_issued_.notify_all();
+      if (stop_) break;
+      cv_work_.wait(lk, [&] { return stop_ || !pending_.empty(); });
+      continue;
+    }
     // Retire completed chunks (FIFO on one stream: completion is in order).
     while (!inflight_.empty()) {
       const cudaError_t q = cudaEventQuery(inflight_.front().ev);
@@ -85,12 +103,14 @@ void Loader::run() {
       std::shared_ptr<LoadReq> r = pending_[bi];
       cudaError_t e = cudaSuccess;
       if (r->issued == 0 && r->wait_ev != nullptr) e = cudaStreamWaitEvent(copy_, r->wait_ev, 0);
+      if (e == cudaSuccess && r->issued == 0 && r->tr_start) e = cudaEventRecord(r->tr_start, copy_);
       int64_t n = std::min(chunk_, r->bytes - r->issued);
       if (r->issued < r->w13_bytes && r->issued + n > r->w13_bytes) n = r->w13_bytes - r->issued;
       if (e == cudaSuccess)
         e = cudaMemcpyAsync(r->dst + r->issued, r->src + r->issued, (size_t)n, cudaMemcpyHostToDevice, copy_);
       r->issued += n;
       bytes_h2d += n;
+      if (e == cudaSuccess && r->tr_end) e = cudaEventRecord(r->tr_end, copy_);  // end of the last chunk issued
       if (e == cudaSuccess && r->issued == r->w13_bytes && r->ev_w13) e = cudaEventRecord(r->ev_w13, copy_);
       const bool last = r->issued == r->bytes;
       if (e == cudaSuccess && last) e = cudaEventRecord(r->ev_done, copy_);

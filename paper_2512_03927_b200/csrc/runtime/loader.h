@@ -34,6 +34,8 @@ struct LoadReq {
   int64_t bytes = 0, w13_bytes = 0;
   cudaEvent_t ev_w13 = nullptr, ev_done = nullptr;  // owned by the slot
   cudaEvent_t wait_ev = nullptr;   // optional: copy stream waits on it before the first chunk
+  cudaEvent_t tr_start = nullptr, tr_end = nullptr;  // optional timing events (event trace): before the
+                                   // first chunk / after every chunk (the last record = end of the copy)
   // loader-owned state (guarded by Loader::mu_)
   int64_t issued = 0;
   bool cancelled = false, fully_issued = false, done = false;
@@ -52,6 +54,9 @@ class Loader {
   // Block until every chunk of r is queued (its events are recorded). Returns false on error.
   bool wait_issued(const std::shared_ptr<LoadReq>& r);
   bool is_done(const std::shared_ptr<LoadReq>& r);
+  // No further chunk of r will be issued (fully issued, cancelled or the loader failed); *bytes =
+  // bytes issued for it.
+  bool settled(const std::shared_ptr<LoadReq>& r, int64_t* bytes);
   cudaError_t error() const { return err_.load(); }
 
   std::atomic<int64_t> bytes_h2d{0}, loads_issued{0}, loads_completed{0}, loads_cancelled{0};

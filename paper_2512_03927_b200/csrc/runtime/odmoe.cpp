@@ -156,6 +156,72 @@ void harvest_timers(Ctx* c) {
   c->timed.clear();
 }
 
+// ------------------------------------------------------------------ event trace
+cudaEvent_t tr_event(Ctx* c) {
+  if (!c->tr_pool.empty()) {
+    cudaEvent_t e = c->tr_pool.back();
+    c->tr_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  CUDA_OK(c, cudaEventCreate(&e));
+  return e;
+}
+
+odmoe_trace_event tr_make(const Ctx* c, int type, int layer, int expert, int slot, int l_cur, int aux, int64_t step) {
+  odmoe_trace_event ev{};
+  ev.type = type;
+  ev.step = (int32_t)step;
+  ev.layer = layer;
+  ev.expert = expert;
+  ev.slot = slot;
+  ev.l_cur = l_cur;
+  ev.aux = aux;
+  ev.rank = c->rank;
+  ev.bytes = 0;
+  ev.t_us = std::nan("");
+  return ev;
+}
+
+// host-only entry (t_us = NaN); `req` makes it wait for that load to settle (bytes copied)
+void tr_host(Ctx* c, int type, int layer, int expert, int slot, int aux, std::shared_ptr<LoadReq> req = nullptr) {
+  if (!c->trace) return;
+  Ctx::TraceRec r;
+  r.ev = tr_make(c, type, layer, expert, slot, c->l_cur, aux, c->step);
+  r.req = std::move(req);
+  c->tr_pending.push_back(std::move(r));
+}
+
+// device-timed entry: an event recorded on `s` now
+void tr_dev(Ctx* c, int type, cudaStream_t s, int layer, int expert = -1, int slot = -1) {
+  if (!c->trace) return;
+  Ctx::TraceRec r;
+  r.ev = tr_make(c, type, layer, expert, slot, c->l_cur, 0, c->step);
+  r.e = tr_event(c);
+  CUDA_OK(c, cudaEventRecord(r.e, s));
+  c->tr_pending.push_back(std::move(r));
+}
+
+// Move every resolvable entry (in order) to tr_done.
+void tr_resolve(Ctx* c) {
+  std::vector<Ctx::TraceRec> keep;
+  for (auto& r : c->tr_pending) {
+    int64_t bytes = 0;
+    if (r.req && !c->loader.settled(r.req, &bytes)) { keep.push_back(std::move(r)); continue; }
+    if (r.e) {
+      const cudaError_t q = cudaEventQuery(r.e);
+      if (q == cudaErrorNotReady) { keep.push_back(std::move(r)); continue; }
+      float ms = 0.f;
+      if (q == cudaSuccess && cudaEventElapsedTime(&ms, c->tr_origin, r.e) == cudaSuccess) r.ev.t_us = 1e3 * (double)ms;
+      cudaGetLastError();  // never-recorded events (a load stopped before its first chunk) leave NaN
+      if (r.own_event) c->tr_pool.push_back(r.e);
+    }
+    if (r.req) r.ev.bytes = bytes;
+    c->tr_done.push_back(r.ev);
+  }
+  c->tr_pending.swap(keep);
+}
+
 // ------------------------------------------------------------------ placement
 // Pure placement functions (also exported as odmoe_plan_* for host-side tests).
 // Experts of layer l that `rank` computes for routing S (k ids): none unless the rank is in group
@@ -333,6 +399,7 @@ void build_shadow(Ctx* c, char* staging) {
     // The shadow runs the main model's own weights (recall must be exactly 1.0).
     c->sh_wt = c->sh_ewt = c->wt;
     c->sh_emb = c->d_emb;
+    c->sh_lm = c->d_lm;
     c->sh_router = c->d_router;
     c->sh_wqkv = c->d_wqkv;
     c->sh_wo = c->d_wo;
@@ -345,7 +412,9 @@ void build_shadow(Ctx* c, char* staging) {
     c->sh_wt = c->sh_ewt = W_BF16;
     c->sh_emb = dmalloc<char>(c, (size_t)V * d * 2, "shadow emb bf16");
     c->sh_router = dmalloc<char>(c, (size_t)L * E * d * 2, "shadow router bf16");
+    c->sh_lm = dmalloc<char>(c, (size_t)V * d * 2, "shadow lm head bf16");
     CUDA_OK(c, launch_f32_to_bf16((const float*)c->d_emb, c->sh_emb, (int64_t)V * d, c->s_main));
+    CUDA_OK(c, launch_f32_to_bf16((const float*)c->d_lm, c->sh_lm, (int64_t)V * d, c->s_main));
     CUDA_OK(c, launch_f32_to_bf16((const float*)c->d_router, c->sh_router, (int64_t)L * E * d, c->s_main));
     c->sh_blob.assign((size_t)L * E, nullptr);
     c->sh_sc.assign((size_t)L * E, nullptr);
@@ -358,7 +427,7 @@ void build_shadow(Ctx* c, char* staging) {
         c->sh_blob[i] = q;
         c->stats.shadow_bytes += (int64_t)3 * F * d * 2;
       }
-    c->stats.shadow_bytes += (int64_t)V * d * 2 + (int64_t)L * E * d * 2;
+    c->stats.shadow_bytes += (int64_t)2 * V * d * 2 + (int64_t)L * E * d * 2;
     c->d_sh_tbl = dmalloc<void*>(c, (size_t)L * E, "shadow tbl");
     c->d_sh_stbl = nullptr;
     CUDA_OK(c, cudaMemcpyAsync(c->d_sh_tbl, c->sh_blob.data(), sizeof(void*) * L * E, cudaMemcpyHostToDevice, c->s_main));
@@ -379,6 +448,10 @@ void build_shadow(Ctx* c, char* staging) {
   c->sh_router = dmalloc<int8_t>(c, (size_t)L * E * d, "shadow router");
   c->sh_srouter = dmalloc<float>(c, (size_t)L * E, "shadow router scales");
   CUDA_OK(c, launch_quantize(c->d_emb, V, d, c->wt, (int8_t*)c->sh_emb, c->sh_semb, c->s_main));
+  // int8-row LM head: the shadow's own greedy token (cross-token speculation)
+  c->sh_lm = dmalloc<int8_t>(c, (size_t)V * d, "shadow lm head");
+  c->sh_slm = dmalloc<float>(c, V, "shadow lm head scales");
+  CUDA_OK(c, launch_quantize(c->d_lm, V, d, c->wt, (int8_t*)c->sh_lm, c->sh_slm, c->s_main));
   CUDA_OK(c, launch_quantize(c->d_router, (int64_t)L * E, d, c->wt, (int8_t*)c->sh_router, c->sh_srouter, c->s_main));
   if (c->H > 0) {  // attention projections: int8-row like the routers (reading Q29)
     const int64_t hq = (int64_t)c->H * c->hd;
@@ -427,7 +500,7 @@ void build_shadow(Ctx* c, char* staging) {
       c->sh_sc[i] = s;
       c->stats.shadow_bytes += (int64_t)3 * F * d + (int64_t)(2 * F + d) * 4;
     }
-  c->stats.shadow_bytes += (int64_t)V * d + V * 4 + (int64_t)L * E * d + L * E * 4;
+  c->stats.shadow_bytes += 2 * ((int64_t)V * d + V * 4) + (int64_t)L * E * d + L * E * 4;
   c->d_sh_tbl = dmalloc<void*>(c, (size_t)L * E, "shadow tbl");
   c->d_sh_stbl = dmalloc<float*>(c, (size_t)L * E, "shadow stbl");
   CUDA_OK(c, cudaMemcpyAsync(c->d_sh_tbl, c->sh_blob.data(), sizeof(void*) * L * E, cudaMemcpyHostToDevice, c->s_main));
@@ -533,6 +606,18 @@ void build_slots(Ctx* c) {
   c->stats.resident_bytes = (int64_t)n * c->blob_bytes;
 }
 
+// Point the per-step prediction views (sh_ids, h_pred, sh_logits, dbg_sh_*, ev_pred) at buffer b.
+void select_buf(Ctx* c, int b) {
+  const size_t L = c->L, k = c->k, E = c->E, d = c->d;
+  c->cur_buf = b;
+  c->sh_ids = c->sh_ids_all ? c->sh_ids_all + b * L * k : nullptr;
+  c->h_pred = c->h_pred_all + b * L * k;
+  c->sh_logits = c->sh_logits_all ? c->sh_logits_all + b * L * E : nullptr;
+  c->dbg_sh_h = c->dbg_sh_h_all ? c->dbg_sh_h_all + b * L * d : nullptr;
+  c->dbg_sh_u = c->dbg_sh_u_all ? c->dbg_sh_u_all + b * L * d * 4 : nullptr;
+  c->ev_pred = c->ev_pred_all.data() + b * L;
+}
+
 void build_buffers(Ctx* c) {
   const int L = c->L, E = c->E, k = c->k, d = c->d, F = c->F, V = c->V;
   c->pkt_ids_off = (int64_t)d * c->esz;
@@ -564,30 +649,37 @@ void build_buffers(Ctx* c) {
   c->d_lmlogits = dmalloc<float>(c, V, "lm logits");
   c->h_ids = hmalloc<int32_t>(c, (size_t)L * k, "h_ids");
   c->h_w = hmalloc<float>(c, (size_t)L * k, "h_w");
-  c->h_pred = hmalloc<int32_t>(c, (size_t)L * k, "h_pred");
+  c->h_pred_all = hmalloc<int32_t>(c, (size_t)Ctx::kPredBufs * L * k, "h_pred");
   c->h_tok = hmalloc<int32_t>(c, 2, "h_tok");
   c->h_flag = hmalloc<int32_t>(c, 1, "h_flag");
   CUDA_OK(c, cudaEventCreateWithFlags(&c->ev_ids, cudaEventDisableTiming));
   CUDA_OK(c, cudaEventCreateWithFlags(&c->ev_tok, cudaEventDisableTiming));
   CUDA_OK(c, cudaEventCreateWithFlags(&c->ev_shadow_done, cudaEventDisableTiming));
   CUDA_OK(c, cudaEventCreateWithFlags(&c->ev_step, cudaEventDisableTiming));
-  c->ev_pred.resize(L);
-  for (auto& e : c->ev_pred) CUDA_OK(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  c->ev_pred_all.assign((size_t)Ctx::kPredBufs * L, nullptr);
+  for (auto& e : c->ev_pred_all) CUDA_OK(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  c->nx_ready.assign(L, 0);
+  c->nx_tbl.assign((size_t)L * k, -1);
+  c->issued_nx.assign(L, {});
   c->pred_ready.assign(L, 0);
   c->pred_tbl.assign((size_t)L * k, -1);
   if (c->has_shadow) {
     c->sh_h = dmalloc<float>(c, d, "sh_h");
     c->sh_u = dmalloc<char>(c, (size_t)d * 4, "sh_u");
-    c->sh_ids = dmalloc<int32_t>(c, (size_t)L * k, "sh_ids");
+    c->sh_ids_all = dmalloc<int32_t>(c, (size_t)Ctx::kPredBufs * L * k, "sh_ids");
     c->sh_w = dmalloc<float>(c, (size_t)L * k, "sh_w");
-    c->sh_logits = dmalloc<float>(c, (size_t)L * E, "sh_logits");
+    c->sh_logits_all = dmalloc<float>(c, (size_t)Ctx::kPredBufs * L * E, "sh_logits");
+    c->sh_tok = dmalloc<int32_t>(c, Ctx::kPredBufs, "sh_tok");
+    c->sh_lmscratch = dmalloc<char>(c, 16 * 4096, "shadow lm scratch");
+    CUDA_OK(c, cudaMemset(c->sh_lmscratch, 0, 16 * 4096));
+    CUDA_OK(c, cudaMemset(c->sh_tok, 0, sizeof(int32_t) * Ctx::kPredBufs));
     c->sh_a = dmalloc<float>(c, (size_t)k * F, "sh_a");
     c->sh_y = dmalloc<float>(c, (size_t)k * d, "sh_y");
     c->sh_yptr = dmalloc<const float*>(c, k, "sh_yptr");
     for (int j = 0; j < k; ++j) yp[j] = c->sh_y + (size_t)j * d;
     CUDA_OK(c, cudaMemcpy(c->sh_yptr, yp.data(), sizeof(float*) * k, cudaMemcpyHostToDevice));
   } else if (c->world > 1) {
-    c->sh_ids = dmalloc<int32_t>(c, (size_t)L * k, "sh_ids");  // receive buffer for P
+    c->sh_ids_all = dmalloc<int32_t>(c, (size_t)Ctx::kPredBufs * L * k, "sh_ids");  // receive buffers for P
   }
   // SEP refinement buffers (allocated for any shadow ctx so the depth can be switched at run time)
   if (is_shadow(c->built_pred) || c->built_pred == ODMOE_PRED_GATE_REUSE) {
@@ -626,13 +718,19 @@ void build_buffers(Ctx* c) {
   }
   c->predA_tbl.assign((size_t)L * k, -1);
   c->predA_ready.assign(L, 0);
+  c->issued_pre.assign(L, {});
+  c->reloaded.assign(L, {});
+  c->in_time.assign(L, 0);
+  select_buf(c, 0);
   c->predB_tbl.assign((size_t)L * k, -1);
   if (c->cfg.debug_capture && c->rank == 0) {
     c->dbg_h = dmalloc<float>(c, (size_t)L * d, "dbg_h");
     c->dbg_ypart = dmalloc<float>(c, (size_t)L * k * d, "dbg_ypart");
     c->dbg_yred = dmalloc<float>(c, (size_t)L * d, "dbg_yred");
-    c->dbg_sh_h = dmalloc<float>(c, (size_t)L * d, "dbg_sh_h");
-    c->dbg_sh_u = dmalloc<char>(c, (size_t)L * d * 4, "dbg_sh_u");
+    c->dbg_sh_h_all = dmalloc<float>(c, (size_t)Ctx::kPredBufs * L * d, "dbg_sh_h");
+    c->dbg_sh_u_all = dmalloc<char>(c, (size_t)Ctx::kPredBufs * L * d * 4, "dbg_sh_u");
+    c->dbg_sh_hf_all = dmalloc<float>(c, (size_t)Ctx::kPredBufs * d, "dbg_sh_hf");
+    if (c->has_shadow) c->sh_lmlogits = dmalloc<float>(c, (size_t)Ctx::kPredBufs * V, "shadow lm logits");
     c->dbg_hfinal = dmalloc<float>(c, d, "dbg_hfinal");
     CUDA_OK(c, cudaMemset(c->dbg_ypart, 0, sizeof(float) * L * k * d));
     CUDA_OK(c, cudaMemset(c->dbg_yred, 0, sizeof(float) * L * d));
@@ -652,19 +750,30 @@ void shadow_experts(Ctx* c, const ExpertRef* ex, const void* u, int u_f32, float
 }
 
 // ------------------------------------------------------------------ shadow forward (SEP, Mode A)
-// Enqueue the shadow pass for `token_dev` on s_shadow: embed, then L x [router, k expert FFNs]
-// with the shadow's own routing chosen on the device (Q10). Predictions land
-// in sh_ids [L][k]; at N = 1 each layer's ids are copied to h_pred with event ev_pred[l].
-void enqueue_shadow(Ctx* c, const int32_t* token_dev) {
+// Enqueue one shadow pass on s_shadow into prediction buffer b: embed the token at token_dev (the
+// main model's token, Mode A / token alignment, or the shadow's own previous token at an unaligned
+// iteration), then L x [router, k expert FFNs] with the shadow's own routing chosen on the device
+// (Q10). Predictions land in sh_ids_all[b] [L][k]; at N = 1 each layer's ids are
+// copied to h_pred_all[b] with event ev_pred_all[b][l]; at N > 1 rank 0 broadcasts them in chunks of
+// pred_chunk layers as soon as each chunk's last router has run. want_token: also run the shadow's
+// final norm + INT8-row LM head + argmax into sh_tok[b] (its own next token).
+void enqueue_shadow(Ctx* c, const int32_t* token_dev, int b, bool want_token) {
   const int L = c->L, E = c->E, k = c->k, d = c->d;
   cudaStream_t s = c->s_shadow;
   const WType swt = c->sh_wt;
   const bool same = swt != W_I8;  // no row scales (main-dtype or BF16 shadow)
   const size_t sesz = swt == W_I8 ? 1 : (swt == W_BF16 ? 2 : 4);
+  int32_t* ids = c->sh_ids_all + (size_t)b * L * k;
+  float* logits = c->sh_logits_all + (size_t)b * L * E;
+  int32_t* hp = c->h_pred_all + (size_t)b * L * k;
+  cudaEvent_t* evp = c->ev_pred_all.data() + (size_t)b * L;
+  float* dh = c->dbg_sh_h_all ? c->dbg_sh_h_all + (size_t)b * L * d : nullptr;
+  char* du = c->dbg_sh_u_all ? c->dbg_sh_u_all + (size_t)b * L * d * 4 : nullptr;
   {
     KTimer t(c, K_SHADOW, s);
     CUDA_OK(c, launch_embed(c->sh_emb, c->sh_semb, swt, token_dev, d, c->sh_h, s));
   }
+  if (token_dev == c->d_tok_in) CUDA_OK(c, cudaEventRecord(c->ev_shadow_done, s));  // d_tok_in consumed
   for (int l = 0; l < L; ++l) {
     int n_add = l > 0 ? k : 0;
     if (c->H > 0) {  // the shadow's own attention block (past keys/values from the main cache)
@@ -677,38 +786,74 @@ void enqueue_shadow(Ctx* c, const int32_t* token_dev) {
       CUDA_OK(c, launch_router(c->sh_h, c->sh_yptr, n_add, nullptr,
                                (const char*)c->sh_router + (size_t)l * E * d * sesz,
                                same ? nullptr : c->sh_srouter + (size_t)l * E, swt, 1, E, d, k,
-                               c->cfg.rms_eps, c->sh_u, c->sh_ids + (size_t)l * k,
-                               c->sh_w + (size_t)l * k, c->sh_logits + (size_t)l * E, nullptr, s, true));
+                               c->cfg.rms_eps, c->sh_u, ids + (size_t)l * k,
+                               c->sh_w + (size_t)l * k, logits + (size_t)l * E, nullptr, s, true));
     }
-    if (c->dbg_sh_h) {
-      CUDA_OK(c, cudaMemcpyAsync(c->dbg_sh_h + (size_t)l * d, c->sh_h, sizeof(float) * d, cudaMemcpyDeviceToDevice, s));
-      CUDA_OK(c, cudaMemcpyAsync((char*)c->dbg_sh_u + (size_t)l * d * 4, c->sh_u, (size_t)d * (swt == W_F32 ? 4 : 2), cudaMemcpyDeviceToDevice, s));
+    if (dh) {
+      CUDA_OK(c, cudaMemcpyAsync(dh + (size_t)l * d, c->sh_h, sizeof(float) * d, cudaMemcpyDeviceToDevice, s));
+      CUDA_OK(c, cudaMemcpyAsync(du + (size_t)l * d * 4, c->sh_u, (size_t)d * (swt == W_F32 ? 4 : 2), cudaMemcpyDeviceToDevice, s));
     }
     if (c->world == 1) {
-      CUDA_OK(c, cudaMemcpyAsync(c->h_pred + (size_t)l * k, c->sh_ids + (size_t)l * k, 4 * k, cudaMemcpyDeviceToHost, s));
-      CUDA_OK(c, cudaEventRecord(c->ev_pred[l], s));
+      CUDA_OK(c, cudaMemcpyAsync(hp + (size_t)l * k, ids + (size_t)l * k, 4 * k, cudaMemcpyDeviceToHost, s));
+      CUDA_OK(c, cudaEventRecord(evp[l], s));
+    } else if ((l + 1) % c->pred_chunk == 0 || l == L - 1) {
+      // this chunk's predictions go out now, not after the whole pass (receivers post the same
+      // broadcasts in the same comm_pred order: enqueue_pred_broadcast)
+      const int l0 = l / c->pred_chunk * c->pred_chunk, n = l + 1 - l0;
+      NCCL_OK(c, ncclBroadcast(ids + (size_t)l0 * k, ids + (size_t)l0 * k, (size_t)n * k, ncclInt32, 0, c->comm_pred, s));
+      CUDA_OK(c, cudaMemcpyAsync(hp + (size_t)l0 * k, ids + (size_t)l0 * k, 4 * n * k, cudaMemcpyDeviceToHost, s));
+      CUDA_OK(c, cudaEventRecord(evp[l0], s));
     }
     const int u_f32 = swt == W_F32;
     std::vector<ExpertRef> ex(k);
     for (int j = 0; j < k; ++j)
       ex[j] = ExpertRef{nullptr, nullptr, (const void* const*)c->d_sh_tbl, (const float* const*)c->d_sh_stbl,
-                        c->sh_ids + (size_t)l * k, j, l * E, k, 0};
+                        ids + (size_t)l * k, j, l * E, k, 0};
     shadow_experts(c, ex.data(), c->sh_u, u_f32, c->sh_a, c->sh_w + (size_t)l * k, c->sh_y, true, s);
   }
-  CUDA_OK(c, cudaEventRecord(c->ev_shadow_done, s));
+  if (want_token) {  // h_L = h_{L-1} + y_{L-1}; own greedy token (lowest id on ties)
+    CUDA_OK(c, launch_combine(c->sh_h, c->sh_yptr, k, d, s));
+    if (c->dbg_sh_hf_all)
+      CUDA_OK(c, cudaMemcpyAsync(c->dbg_sh_hf_all + (size_t)b * d, c->sh_h, sizeof(float) * d, cudaMemcpyDeviceToDevice, s));
+    KTimer t(c, K_SHADOW, s);
+    CUDA_OK(c, launch_lm_head(c->sh_h, c->sh_lm, swt, c->V, d, c->cfg.rms_eps, c->sh_tok + b,
+                              c->sh_lmlogits ? c->sh_lmlogits + (size_t)b * c->V : nullptr, c->sh_lmscratch, s,
+                              false, same ? nullptr : c->sh_slm));
+  }
 }
 
-// At N > 1 rank 0 broadcasts the prediction table in chunks of pred_chunk layers over comm_pred
-// on s_shadow; every rank copies each chunk to h_pred and records ev_pred[first layer of chunk].
-void enqueue_pred_broadcast(Ctx* c) {
+// At N > 1 the non-zero ranks receive rank 0's prediction table of buffer b in chunks of pred_chunk
+// layers over comm_pred on s_shadow, copy each chunk to h_pred_all[b] and record its event.
+void enqueue_pred_broadcast(Ctx* c, int b) {
   const int L = c->L, k = c->k;
   cudaStream_t s = c->s_shadow;
+  int32_t* ids = c->sh_ids_all + (size_t)b * L * k;
+  int32_t* hp = c->h_pred_all + (size_t)b * L * k;
+  cudaEvent_t* evp = c->ev_pred_all.data() + (size_t)b * L;
   for (int l0 = 0; l0 < L; l0 += c->pred_chunk) {
     const int n = std::min(c->pred_chunk, L - l0);
-    NCCL_OK(c, ncclBroadcast(c->sh_ids + (size_t)l0 * k, c->sh_ids + (size_t)l0 * k, (size_t)n * k, ncclInt32, 0, c->comm_pred, s));
-    CUDA_OK(c, cudaMemcpyAsync(c->h_pred + (size_t)l0 * k, c->sh_ids + (size_t)l0 * k, 4 * n * k, cudaMemcpyDeviceToHost, s));
-    CUDA_OK(c, cudaEventRecord(c->ev_pred[l0], s));
+    NCCL_OK(c, ncclBroadcast(ids + (size_t)l0 * k, ids + (size_t)l0 * k, (size_t)n * k, ncclInt32, 0, c->comm_pred, s));
+    CUDA_OK(c, cudaMemcpyAsync(hp + (size_t)l0 * k, ids + (size_t)l0 * k, 4 * n * k, cudaMemcpyDeviceToHost, s));
+    CUDA_OK(c, cudaEventRecord(evp[l0], s));
   }
+}
+
+// The NEXT token's prediction for layer m (speculative pass, buffer (step + 1) & 1) on the host?
+bool next_pred_available(Ctx* c, int m) {
+  if (c->spec_step != c->step + 1) return false;
+  if (c->nx_ready[m]) return true;
+  const int b = (int)((c->step + 1) & 1), L = c->L, k = c->k;
+  const int evl = c->world == 1 ? m : (m / c->pred_chunk) * c->pred_chunk;
+  const cudaError_t q = cudaEventQuery(c->ev_pred_all[(size_t)b * L + evl]);
+  if (q == cudaErrorNotReady) return false;
+  CUDA_OK(c, q);
+  const int hi = c->world == 1 ? m + 1 : std::min(L, evl + c->pred_chunk);
+  const int32_t* hp = c->h_pred_all + (size_t)b * L * k;
+  for (int l = evl; l < hi; ++l) {
+    c->nx_ready[l] = 1;
+    std::copy(hp + (size_t)l * k, hp + (size_t)(l + 1) * k, c->nx_tbl.begin() + (size_t)l * k);
+  }
+  return true;
 }
 
 // Prediction for layer m available on the host? (non-blocking). Mode A (token-start shadow)
@@ -849,7 +994,11 @@ int occupied_count(const Ctx* c) {
   return n;
 }
 
-void submit_into(Ctx* c, Slot& s, int slot, int64_t tok, int l, int e, int64_t key) {
+// kind: 0 predicted, 1 reload after the router, 2 refined prediction, 3 next-token
+// (cross-token speculation), 4 user load (odmoe_load), 5 prefill
+enum LoadKind { LK_PRED = 0, LK_RELOAD = 1, LK_REFINE = 2, LK_NEXT = 3, LK_USER = 4, LK_PREFILL = 5 };
+
+void submit_into(Ctx* c, Slot& s, int slot, int64_t tok, int l, int e, int64_t key, int kind) {
   if (!holds_expert(c, l, e)) fail(c, ODMOE_E_RANGE, "expert not in this rank's pool");
   s.occupied = true;
   s.token = tok;
@@ -867,18 +1016,41 @@ void submit_into(Ctx* c, Slot& s, int slot, int64_t tok, int l, int e, int64_t k
   r->ev_w13 = s.ev_w13;
   r->ev_done = s.ev_done;
   r->wait_ev = s.free_recorded ? s.ev_free : nullptr;
+  if (c->trace) {
+    r->tr_start = tr_event(c);
+    r->tr_end = tr_event(c);
+    // the window position of the load: layer m of the next token is L + m (Q11)
+    const int pos = (int)((tok > c->step ? (tok - c->step) * c->L : 0) + l);
+    Ctx::TraceRec a, b, i;
+    i.ev = tr_make(c, ODMOE_EV_LOAD_ISSUE, pos, e, slot, c->l_cur, kind, tok < 0 ? c->step : tok);
+    a.ev = tr_make(c, ODMOE_EV_LOAD_START, l, e, slot, c->l_cur, kind, tok < 0 ? c->step : tok);
+    a.e = r->tr_start;
+    a.req = r;
+    b.ev = tr_make(c, ODMOE_EV_LOAD_END, l, e, slot, c->l_cur, kind, tok < 0 ? c->step : tok);
+    b.e = r->tr_end;
+    b.req = r;
+    c->tr_pending.push_back(std::move(i));
+    c->tr_pending.push_back(std::move(a));
+    c->tr_pending.push_back(std::move(b));
+  }
+  if (tok == c->step && l >= 0 && l < c->L && !c->issued_pre.empty()) {
+    if (kind == LK_RELOAD) c->reloaded[l].push_back(e);
+    else if (kind != LK_USER && kind != LK_PREFILL) c->issued_pre[l].push_back(e);
+  } else if (tok == c->step + 1 && kind == LK_NEXT && l >= 0 && l < c->L) {
+    c->issued_nx[l].push_back(e);
+  }
   s.req = r;
   c->loader.submit(r);
 }
 
-void submit_load(Ctx* c, int slot, int64_t tok, int l, int e, int64_t key) {
-  submit_into(c, c->slots[slot], slot, tok, l, e, key);
+void submit_load(Ctx* c, int slot, int64_t tok, int l, int e, int64_t key, int kind) {
+  submit_into(c, c->slots[slot], slot, tok, l, e, key, kind);
   c->stats.max_resident = std::max<int64_t>(c->stats.max_resident, occupied_count(c));
 }
 
 void release_slot(Ctx* c, int slot) {
   Slot& s = c->slots[slot];
-  if (s.req) c->loader.cancel(s.req);
+  if (s.req && c->loader.cancel(s.req)) tr_host(c, ODMOE_EV_LOAD_CANCEL, s.layer, s.expert, slot, 0, s.req);
   s.occupied = false;
   s.layer = s.expert = -1;
   s.token = -1;
@@ -931,7 +1103,7 @@ void apply_refinements(Ctx* c) {
           c->next_plan = std::min(c->next_plan, m);
           break;
         }
-        submit_load(c, fs, c->step, m, mine[jj], load_key(c, c->step, m, 1 + (int)jj));
+        submit_load(c, fs, c->step, m, mine[jj], load_key(c, c->step, m, 1 + (int)jj), LK_REFINE);
       }
     }
   }
@@ -953,8 +1125,30 @@ void pump(Ctx* c) {
     for (auto& s : c->slots) nfree += !s.occupied;
     if (nfree < (int)todo.size()) break;
     for (size_t j = 0; j < todo.size(); ++j)
-      submit_load(c, free_slot(c), c->step, m, todo[j], load_key(c, c->step, m, 1 + (int)j));
+      submit_load(c, free_slot(c), c->step, m, todo[j], load_key(c, c->step, m, 1 + (int)j), LK_PRED);
     c->next_plan++;
+  }
+  // Cross-token speculation: once every layer of this token is planned, the next
+  // token's layers m whose window position L + m <= l_cur + D are loaded from the speculative
+  // shadow pass's predictions while the main model is still finishing this token.
+  if (c->next_plan < c->L || c->spec_step != c->step + 1) return;
+  const int64_t tn = c->step + 1;
+  while (c->next_plan_nx < c->L) {
+    const int m = c->next_plan_nx;
+    if (c->L + m > c->l_cur + c->cfg.lookahead) break;
+    if (!next_pred_available(c, m)) break;
+    std::vector<int> mine = my_experts(c, m, c->nx_tbl.data() + (size_t)m * c->k);
+    std::vector<int> todo;
+    for (int e : mine)
+      if (find_slot(c, tn, m, e) < 0) todo.push_back(e);
+    int nfree = 0;
+    for (auto& s : c->slots) nfree += !s.occupied;
+    if (nfree < (int)todo.size()) break;
+    for (size_t j = 0; j < todo.size(); ++j) {
+      submit_load(c, free_slot(c), tn, m, todo[j], load_key(c, tn, m, 1 + (int)j), LK_NEXT);
+      c->stats.early_loads++;
+    }
+    c->next_plan_nx++;
   }
 }
 
@@ -1054,7 +1248,13 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
   // Fully-resident 1-GPU steps (no attention, no debug capture) are the same sequence of launches
   // every token: the second step is captured into a CUDA graph (token H2D ... token D2H) and later
   // steps replay it -- one launch per token instead of ~200 (ODMOE_GRAPH=0 disables).
-  const bool graphable = c->resident && c->world == 1 && c->H == 0 && !c->cfg.debug_capture && graph_enabled();
+  const bool graphable = c->resident && c->world == 1 && c->H == 0 && !c->cfg.debug_capture && !c->trace && graph_enabled();
+  c->predict_cache_token = -1;  // this step's shadow pass overwrites sh_ids (odmoe_predict_ahead's cache)
+  for (int l = 0; l < L; ++l) {
+    c->issued_pre[l].clear();
+    c->reloaded[l].clear();
+    c->in_time[l] = 0;
+  }
   const bool replay = graphable && c->graph_exec != nullptr;
   const bool capture = graphable && !replay && c->step >= 1;
   const int64_t launches0 = c->stats.kernel_launches;
@@ -1073,6 +1273,8 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
     CUDA_OK(c, cudaMemcpyAsync(c->d_tok_in, c->h_tok, 4, cudaMemcpyHostToDevice, s));
     if (!c->resident) CUDA_OK(c, cudaEventRecord(c->ev_tok, s));
   }
+  c->l_cur = -1;
+  tr_dev(c, ODMOE_EV_STEP_START, s, -1);
 
   // predictions for this step
   std::fill(c->pred_ready.begin(), c->pred_ready.end(), 0);
@@ -1086,14 +1288,35 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
   c->ref_next = 0;
   std::fill(c->ref_enq.begin(), c->ref_enq.end(), 0);
   c->pred_valid = false;
+  // Prediction buffer of this step; cross-token speculation state (token alignment period T_p):
+  // this step's shadow pass may already have run during the previous step from the shadow's own
+  // token (have_spec); the next step's pass is speculative iff iteration align_n + 1 is unaligned.
+  const int pb = (int)(c->step & 1);
+  select_buf(c, pb);
+  const bool have_spec = shadow_pred && !c->resident && c->spec_step == c->step;
+  const bool next_spec = shadow_pred && !c->resident && c->align_period > 1 &&
+                         ((c->align_n + 1) % c->align_period) != 0;
+  if (!have_spec) {  // early loads of an abandoned speculation (options changed in between) are dropped
+    for (int i = 0; i < (int)c->slots.size(); ++i)
+      if (c->slots[i].occupied && c->slots[i].token == c->step) release_slot(c, i);
+  } else {
+    for (int l = 0; l < L; ++l) c->issued_pre[l] = c->issued_nx[l];
+  }
+  for (int l = 0; l < L; ++l) c->issued_nx[l].clear();
   if (!c->resident) {
     if (shadow_pred) {
       if (r0) {
-        CUDA_OK(c, cudaStreamWaitEvent(c->s_shadow, c->ev_tok, 0));
-        enqueue_shadow(c, c->d_tok_in);
+        if (!have_spec) {
+          CUDA_OK(c, cudaStreamWaitEvent(c->s_shadow, c->ev_tok, 0));
+          enqueue_shadow(c, c->d_tok_in, pb, c->align_period > 1);
+        }
+        if (next_spec) enqueue_shadow(c, c->sh_tok + pb, pb ^ 1, true);  // the shadow's own token
+      } else if (c->world > 1) {
+        if (!have_spec) enqueue_pred_broadcast(c, pb);
+        if (next_spec) enqueue_pred_broadcast(c, pb ^ 1);
       }
-      if (c->world > 1) enqueue_pred_broadcast(c);
       c->pred_valid = true;
+      if (have_spec) c->stats.spec_steps++;
     } else if (gate_reuse) {
       c->pred_valid = true;  // predictions arrive per layer through the refinement path
     } else if (p == ODMOE_PRED_RANDOM) {
@@ -1111,8 +1334,12 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
       }
     }
   }
-  c->next_plan = 0;
+  c->next_plan = have_spec ? c->next_plan_nx : 0;
+  c->spec_step = next_spec ? c->step + 1 : -1;
+  c->next_plan_nx = 0;
+  std::fill(c->nx_ready.begin(), c->nx_ready.end(), 0);
   c->l_cur = 0;
+  for (int m = 0; m < c->next_plan; ++m) pred_available(c, m);  // early-loaded layers: predictions on the host
   pump(c);
 
   std::vector<int32_t> true_ids((size_t)L * k);
@@ -1163,6 +1390,7 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
       }
     }
     if (c->world > 1) NCCL_OK(c, ncclBroadcast(pkt, pkt, c->pkt_bytes, ncclChar, 0, c->comm, s));
+    tr_dev(c, ODMOE_EV_ROUTER_DONE, s, l);
     n_add = c->world == 1 ? k : 1;
 
     const bool in_group = (l % c->NG) == c->my_group;
@@ -1216,6 +1444,8 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
       const double wait_us = (now_s() - tw) * 1e6;
       const int32_t* S = c->h_ids + (size_t)l * k;
       std::copy(S, S + k, true_ids.begin() + (size_t)l * k);
+      // the prediction that could drive this layer's loads had reached the host before the ids did
+      c->in_time[l] = c->pred_valid && (shadow_pred ? c->predA_ready[l] : c->pred_ready[l]);
       pred_available(c, l);  // refresh (shadow may have finished meanwhile)
       int reloads = 0;
       if (in_group) {
@@ -1234,14 +1464,18 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
           if (fs < 0) {
             // every slot holds a future prefetch: drop the furthest one and re-plan it later
             int far = -1;
+            // (never a slot held by odmoe_load, token -2; the next token's early loads are furthest)
+            auto wpos = [&](const Slot& q) { return (q.token - c->step) * (int64_t)L + q.layer; };
             for (int i = 0; i < (int)c->slots.size(); ++i)
-              if (c->slots[i].occupied && (far < 0 || c->slots[i].layer > c->slots[far].layer)) far = i;
-            if (far < 0 || c->slots[far].layer <= l) fail(c, ODMOE_E_BUDGET, "no slot for a reload");
-            c->next_plan = std::min(c->next_plan, c->slots[far].layer);
+              if (c->slots[i].occupied && c->slots[i].token >= c->step && (far < 0 || wpos(c->slots[i]) > wpos(c->slots[far]))) far = i;
+            if (far < 0 || wpos(c->slots[far]) <= l) fail(c, ODMOE_E_BUDGET, "no slot for a reload");
+            if (c->slots[far].token == c->step) c->next_plan = std::min(c->next_plan, c->slots[far].layer);
+            else c->next_plan_nx = std::min(c->next_plan_nx, c->slots[far].layer);
             release_slot(c, far);
             fs = far;
           }
-          submit_load(c, fs, c->step, l, e, load_key(c, c->step, l, 0));
+          tr_host(c, ODMOE_EV_MISPREDICT, l, e, fs, 0);
+          submit_load(c, fs, c->step, l, e, load_key(c, c->step, l, 0), LK_RELOAD);
           reloads++;
           c->stats.reloads++;
         }
@@ -1261,15 +1495,18 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
           ExpertRef e2 = direct_ref(sl.dev + c->w13_bytes, nullptr, j);
           if (fused) {  // one launch once the whole blob has landed
             CUDA_OK(c, cudaStreamWaitEvent(s, sl.ev_done, 0));
+            tr_dev(c, ODMOE_EV_COMPUTE_START, s, l, S[j], si);
             KTimer t(c, K_W13, s);
             CUDA_OK(c, launch_expert_fused(e13, sl.dev + c->w13_bytes, nullptr, c->wt, pkt, u_f32, c->d_a + (size_t)ypos * F,
                                            w_dev, y, d, c->Fs, s, false));
           } else {  // W13 starts as soon as its part has landed, W2 after the rest
             CUDA_OK(c, cudaStreamWaitEvent(s, sl.ev_w13, 0));
+            tr_dev(c, ODMOE_EV_COMPUTE_START, s, l, S[j], si);
             { KTimer t(c, K_W13, s); CUDA_OK(c, launch_w13(e13, c->wt, pkt, u_f32, c->d_a + (size_t)ypos * F, d, c->Fs, s)); }
             CUDA_OK(c, cudaStreamWaitEvent(s, sl.ev_done, 0));
             { KTimer t(c, K_W2, s); CUDA_OK(c, launch_w2(e2, c->wt, c->d_a + (size_t)ypos * F, w_dev, y, d, c->Fs, s)); }
           }
+          tr_dev(c, ODMOE_EV_COMPUTE_END, s, l, S[j], si);
           // evict right after use: the slot is reusable once this event fires (Q16)
           CUDA_OK(c, cudaEventRecord(sl.ev_free, s));
           sl.free_recorded = true;
@@ -1283,15 +1520,15 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
       }
       if (c->next_plan <= l) c->next_plan = l + 1;
       pump(c);
-      if (rec && r0) {
+      if (rec) {
         odmoe_layer_record& R = rec[l];
         std::memset(&R, 0, sizeof(R));
-        for (int j = 0; j < 8; ++j) { R.true_ids[j] = -1; R.pred_ids[j] = -1; }
+        for (int j = 0; j < 8; ++j) { R.true_ids[j] = -1; R.pred_ids[j] = -1; R.issued_ids[j] = -1; R.reload_ids[j] = -1; }
         for (int j = 0; j < k; ++j) R.true_ids[j] = S[j];
         R.n_reloads = reloads;
         R.load_wait_us = (float)wait_us;
-        c->stats.wait_us += wait_us;
       }
+      c->stats.wait_us += wait_us;
     }
     if (c->world > 1 && c->p2p) {
       // this rank's gated partials, summed in router rank order, stored into its row of GPU 0's
@@ -1332,6 +1569,8 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
   if (c->world > 1) NCCL_OK(c, ncclBroadcast(c->d_tok_out, c->d_tok_out, 1, ncclInt32, 0, c->comm, s));
   CUDA_OK(c, cudaMemcpyAsync(c->h_tok + 1, c->d_tok_out, 4, cudaMemcpyDeviceToHost, s));
   CUDA_OK(c, cudaMemcpyAsync(c->h_flag, c->d_flag, 4, cudaMemcpyDeviceToHost, s));
+  c->l_cur = L;  // the window now reaches into the next token (positions <= L + D)
+  tr_dev(c, ODMOE_EV_STEP_END, s, -1);
   if (c->resident) CUDA_OK(c, cudaMemcpyAsync(c->h_ids, c->d_pkt + c->pkt_ids_off, 4 * k, cudaMemcpyDeviceToHost, s));
   if (c->resident && r0) {
     for (int l = 0; l < L; ++l)
@@ -1354,8 +1593,20 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
     if (replay) c->stats.kernel_launches += c->graph_launches;
     c->timed.insert(c->timed.end(), c->graph_timers.begin(), c->graph_timers.end());
   }
+  if (c->spec_step == c->step + 1 && !replay) {
+    // keep issuing the next token's early loads while the LM head and the token copy finish
+    for (;;) {
+      const cudaError_t q = cudaStreamQuery(s);
+      if (q == cudaSuccess) break;
+      if (q != cudaErrorNotReady) CUDA_OK(c, q);
+      pump(c);
+      if (c->loader.error() != cudaSuccess) CUDA_OK(c, c->loader.error());
+      std::this_thread::sleep_for(std::chrono::microseconds(5));
+    }
+  }
   CUDA_OK(c, cudaStreamSynchronize(s));
   if (!c->resident && (shadow_pred || gate_reuse) && (r0 || c->world > 1)) CUDA_OK(c, cudaStreamSynchronize(c->s_shadow));
+  if (c->spec_step == c->step + 1) pump(c);  // the speculative pass has finished: plan what fits now
   if (c->h_flag[0] == 2) fail(c, ODMOE_E_STATE, "peer partials did not arrive (P2P combine timeout)");
   if (c->h_flag[0]) fail(c, ODMOE_E_NONFINITE, "non-finite router logits");
   if (c->resident) std::copy(c->h_ids, c->h_ids + (size_t)L * k, true_ids.begin());
@@ -1365,7 +1616,7 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
   for (int l = 0; l < L; ++l) pred_available(c, l);
   if (c->R > 0) apply_refinements(c);
   if (gate_reuse) c->predA_tbl = c->predB_tbl;  // the gate-reuse predictions are this predictor's output
-  if (r0) {
+  {
     for (int l = 0; l < L; ++l) {
       const int32_t* S = true_ids.data() + (size_t)l * k;
       const int32_t* P = c->predA_tbl.data() + (size_t)l * k;
@@ -1374,9 +1625,10 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
       if (have)
         for (int a = 0; a < k; ++a)
           for (int b = 0; b < k; ++b) corr += S[a] == P[b];
-      if (have) { c->stats.correct += corr; c->stats.predicted_total += k; }
+      const int corr_t = c->in_time[l] ? corr : 0;
+      if (have && r0) { c->stats.correct += corr; c->stats.predicted_total += k; c->stats.correct_in_time += corr_t; }
       const int32_t* PB = c->predB_tbl.data() + (size_t)l * k;
-      if (PB[0] >= 0) {
+      if (PB[0] >= 0 && r0) {
         int cb = 0;
         for (int a = 0; a < k; ++a)
           for (int b = 0; b < k; ++b) cb += S[a] == PB[b];
@@ -1387,12 +1639,19 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
         odmoe_layer_record& R = rec[l];
         if (c->resident) {
           std::memset(&R, 0, sizeof(R));
-          for (int j = 0; j < 8; ++j) { R.true_ids[j] = -1; R.pred_ids[j] = -1; }
+          for (int j = 0; j < 8; ++j) { R.true_ids[j] = -1; R.pred_ids[j] = -1; R.issued_ids[j] = -1; R.reload_ids[j] = -1; }
           for (int j = 0; j < k; ++j) R.true_ids[j] = S[j];
         }
         for (int j = 0; j < k; ++j) R.pred_ids[j] = have ? P[j] : -1;
         R.pred_available = have;
         R.correct = corr;
+        R.pred_in_time = c->in_time[l];
+        R.correct_in_time = corr_t;
+        std::vector<int> a = c->issued_pre[l], b = c->reloaded[l];
+        std::sort(a.begin(), a.end());
+        std::sort(b.begin(), b.end());
+        for (int j = 0; j < (int)a.size() && j < 8; ++j) R.issued_ids[j] = a[j];
+        for (int j = 0; j < (int)b.size() && j < 8; ++j) R.reload_ids[j] = b[j];
       }
     }
     if (rec) {
@@ -1407,8 +1666,10 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
   *token_out = c->h_tok[1];
   c->stats.tokens++;
   c->step++;
+  c->align_n++;
   if (c->H > 0) c->pos++;
   if (c->cfg.time_kernels) harvest_timers(c);
+  if (c->trace) tr_resolve(c);
   // loader statistics
   c->stats.loads_issued = c->loader.loads_issued.load();
   c->stats.loads_completed = c->loader.loads_completed.load();
@@ -1456,6 +1717,11 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
       add(8, c->dbg_sh_u, (int64_t)d * 4, L);
       add(9, c->sh_logits, (int64_t)E * 4, L);
       add(10, c->sh_ids, (int64_t)k * 4, L);
+      if (c->align_period > 1) {  // the pass that produced this step's predictions: its final state + own token
+        add(14, c->dbg_sh_hf_all + (size_t)pb * d, (int64_t)d * 4, 1);
+        add(15, c->sh_tok + pb, 4, 1);
+        add(16, c->sh_lmlogits + (size_t)pb * c->V, (int64_t)c->V * 4, 1);
+      }
     }
     add(11, c->dbg_hfinal, (int64_t)d * 4, 1);
     add(12, c->d_lmlogits, (int64_t)c->V * 4, 1);
@@ -1575,6 +1841,9 @@ void prefill_impl(Ctx* c, const int32_t* tokens, int T, int32_t* token_out, int3
   if (E > kMaxGGExperts) fail(c, ODMOE_E_CONFIG, "prefill supports E <= 8");
   if (d % 256 || c->Fs % 128) fail(c, ODMOE_E_CONFIG, "prefill needs d % 256 == 0 and F (per rank) % 128 == 0");
   if (T < 1 || !tokens) fail(c, ODMOE_E_CONFIG, "empty prompt (S:108)");
+  c->predict_cache_token = -1;  // the KV position changes (odmoe_predict_ahead's cache)
+  c->align_n = 0;                // a new sequence starts aligned
+  c->spec_step = -1;
   for (int t = 0; t < T; ++t)
     if (tokens[t] < 0 || tokens[t] >= c->V) fail(c, ODMOE_E_RANGE, "token out of range");
   ensure_prefill(c, T);
@@ -1604,7 +1873,7 @@ void prefill_impl(Ctx* c, const int32_t* tokens, int T, int32_t* token_out, int3
       for (int i = 0; i < (int)c->pslots.size(); ++i)
         if (!c->pslots[i].occupied) { fs = i; break; }
       if (fs < 0) break;
-      submit_into(c, c->pslots[fs], fs, -3, need[next].first, need[next].second, (int64_t)need[next].first * 16);
+      submit_into(c, c->pslots[fs], fs, -3, need[next].first, need[next].second, (int64_t)need[next].first * 16, LK_PREFILL);
       next++;
     }
   };
@@ -1752,13 +2021,17 @@ void destroy_ctx(Ctx* c) {
   if (c->s_shadow) cudaStreamSynchronize(c->s_shadow);
   if (c->s_copy) cudaStreamSynchronize(c->s_copy);
   auto F = [](void* p) { if (p) cudaFree(p); };
+  for (auto& r : c->tr_pending)
+    if (r.e) cudaEventDestroy(r.e);
+  for (auto e : c->tr_pool) cudaEventDestroy(e);
+  if (c->tr_origin) cudaEventDestroy(c->tr_origin);
   F(c->d_emb); F(c->d_lm); F(c->d_router);
   F(c->d_wqkv); F(c->d_wo); F(c->d_kc); F(c->d_vc); F(c->d_qkv); F(c->d_attn_o); F(c->d_attn_part); F(c->dbg_hpre);
   F(c->sh_qkv); F(c->sh_attn_o); F(c->sh_attn_part); F(c->sh_kcur); F(c->sh_vcur);
   F(c->pa_x); F(c->pa_qkv); F(c->pa_part); F(c->pa_out); F(c->pa_tiles); F(c->sh_kc); F(c->sh_vc);
   if (c->built_pred != ODMOE_PRED_SHADOW_SAME) {
     F(c->sh_wqkv); F(c->sh_sqkv); F(c->sh_wo); F(c->sh_so);
-    F(c->sh_emb); F(c->sh_semb); F(c->sh_router); F(c->sh_srouter);
+    F(c->sh_emb); F(c->sh_semb); F(c->sh_router); F(c->sh_srouter); F(c->sh_lm); F(c->sh_slm);
     for (auto p : c->sh_blob) F(p);
     for (auto p : c->sh_sc) F(p);
     F(c->d_sh_tbl); F(c->d_sh_stbl);
@@ -1774,8 +2047,9 @@ void destroy_ctx(Ctx* c) {
   F(c->d_h); F(c->d_pkt); F(c->d_logits); F(c->d_a); F(c->d_y); F(c->d_yred); F(c->d_zero);
   F((void*)c->d_yptr); F((void*)c->d_yredptr); F(c->d_tok_in); F(c->d_tok_out); F(c->d_flag);
   F(c->d_lmscratch); F(c->d_lmlogits);
-  F(c->sh_h); F(c->sh_u); F(c->sh_ids); F(c->sh_w); F(c->sh_logits); F(c->sh_a); F(c->sh_y); F((void*)c->sh_yptr);
-  F(c->dbg_h); F(c->dbg_ypart); F(c->dbg_yred); F(c->dbg_sh_h); F(c->dbg_sh_u); F(c->dbg_hfinal);
+  F(c->sh_h); F(c->sh_u); F(c->sh_ids_all); F(c->sh_w); F(c->sh_logits_all); F(c->sh_a); F(c->sh_y); F((void*)c->sh_yptr);
+  F(c->sh_tok); F(c->sh_lmscratch); F(c->sh_lmlogits);
+  F(c->dbg_h); F(c->dbg_ypart); F(c->dbg_yred); F(c->dbg_sh_h_all); F(c->dbg_sh_u_all); F(c->dbg_sh_hf_all); F(c->dbg_hfinal);
   F(c->p_h); F(c->p_pkt); F(c->p_tok); F(c->p_off); F(c->p_src); F(c->p_inv); F(c->p_gate);
   F(c->p_x); F(c->p_a2); F(c->p_y); F(c->p_part); F(c->p_tiles);
   for (auto& s : c->pslots) {
@@ -1790,8 +2064,8 @@ void destroy_ctx(Ctx* c) {
   for (auto e : c->ev_router) cudaEventDestroy(e);
   for (auto e : c->ev_ref) cudaEventDestroy(e);
   auto FH = [](void* p) { if (p) cudaFreeHost(p); };
-  FH(c->pool); FH(c->h_ids); FH(c->h_w); FH(c->h_pred); FH(c->h_tok); FH(c->h_flag);
-  for (auto e : c->ev_pred) cudaEventDestroy(e);
+  FH(c->pool); FH(c->h_ids); FH(c->h_w); FH(c->h_pred_all); FH(c->h_tok); FH(c->h_flag);
+  for (auto e : c->ev_pred_all) cudaEventDestroy(e);
   for (auto e : {c->ev_ids, c->ev_tok, c->ev_shadow_done, c->ev_step}) if (e) cudaEventDestroy(e);
   for (auto& t : c->timed) { c->tev_pool.push_back(t.a); c->tev_pool.push_back(t.b); }
   for (auto e : c->tev_pool) cudaEventDestroy(e);
@@ -1972,18 +2246,20 @@ odmoe_status odmoe_predict_ahead(void* ctx, int32_t token, int from_layer, int d
   CTX_GUARD(ctx);
   return guard(c, [&] {
     if (!c->has_shadow) fail(c, ODMOE_E_STATE, "no shadow on this rank");
+    CUDA_OK(c, cudaStreamSynchronize(c->s_shadow));  // a previous step's shadow work is done with sh_ids
     if (token < 0 || token >= c->V || from_layer < 0 || depth < 0 || from_layer + depth > c->L)
       fail(c, ODMOE_E_RANGE, "range");
+    const int pbuf = Ctx::kPredBufs - 1;  // its own prediction buffer: a speculative pass may hold the others
     if (c->predict_cache_token != token) {
       c->h_tok[0] = token;
       CUDA_OK(c, cudaMemcpyAsync(c->d_tok_in, c->h_tok, 4, cudaMemcpyHostToDevice, c->s_shadow));
-      enqueue_shadow(c, c->d_tok_in);
+      enqueue_shadow(c, c->d_tok_in, pbuf, false);
       CUDA_OK(c, cudaStreamSynchronize(c->s_shadow));
       if (c->cfg.time_kernels) harvest_timers(c);
       c->predict_cache_token = token;
     }
     std::vector<int32_t> P((size_t)c->L * c->k);
-    CUDA_OK(c, cudaMemcpy(P.data(), c->sh_ids, 4 * P.size(), cudaMemcpyDeviceToHost));
+    CUDA_OK(c, cudaMemcpy(P.data(), c->sh_ids_all + (size_t)pbuf * c->L * c->k, 4 * P.size(), cudaMemcpyDeviceToHost));
     std::copy(P.begin() + (size_t)from_layer * c->k, P.begin() + (size_t)(from_layer + depth) * c->k, pred_ids);
   });
 }
@@ -2036,9 +2312,38 @@ odmoe_status odmoe_set_option(void* ctx, int key, int64_t value) {
     } else if (key == 4) {
       if (value < 0 || value >= c->max_seq || c->H == 0) fail(c, ODMOE_E_RANGE, "position outside the KV cache");
       c->pos = value;
+      c->predict_cache_token = -1;
+    } else if (key == 7) {
+      if (value != 0 && value != 1) fail(c, ODMOE_E_CONFIG, "trace is 0 or 1");
+      if (value && !c->tr_origin) {
+        CUDA_OK(c, cudaEventCreate(&c->tr_origin));
+        CUDA_OK(c, cudaEventRecord(c->tr_origin, c->s_main));
+        CUDA_OK(c, cudaStreamSynchronize(c->s_main));
+      }
+      c->trace = (int)value;
+    } else if (key == 8) {
+      if (value < 1 || value > 64) fail(c, ODMOE_E_CONFIG, "token alignment period must be in 1..64");
+      if (value > 1 && (!is_shadow(c->built_pred) || c->resident || c->H > 0))
+        fail(c, ODMOE_E_STATE, "cross-token speculation needs an on-demand shadow ctx without attention");
+      c->align_period = (int)value;
+      c->align_n = 0;
+      c->spec_step = -1;
     } else {
       fail(c, ODMOE_E_CONFIG, "unknown option key");
     }
+  });
+}
+
+odmoe_status odmoe_trace_read(void* ctx, odmoe_trace_event* out, int32_t cap, int32_t* n_out) {
+  CTX_GUARD(ctx);
+  return guard(c, [&] {
+    if (!c->tr_origin) fail(c, ODMOE_E_STATE, "trace was never enabled");
+    if (!n_out || cap < 0 || (cap > 0 && !out)) fail(c, ODMOE_E_CONFIG, "bad output buffer");
+    tr_resolve(c);
+    const int n = std::min<int>(cap, (int)c->tr_done.size());
+    std::copy(c->tr_done.begin(), c->tr_done.begin() + n, out);
+    c->tr_done.erase(c->tr_done.begin(), c->tr_done.begin() + n);
+    *n_out = n;
   });
 }
 
@@ -2051,7 +2356,7 @@ odmoe_status odmoe_load(void* ctx, int layer, int expert) {
     if (find_slot(c, -2, layer, expert) >= 0) return;
     const int fs = free_slot(c);
     if (fs < 0) fail(c, ODMOE_E_BUDGET, "all slots occupied");
-    submit_load(c, fs, -2, layer, expert, -1);
+    submit_load(c, fs, -2, layer, expert, -1, LK_USER);
   });
 }
 
@@ -2074,7 +2379,9 @@ odmoe_status odmoe_evict(void* ctx, int layer, int expert) {
     const int si = find_slot(c, -2, layer, expert);
     if (si < 0) fail(c, ODMOE_E_STATE, "expert not resident");
     Slot& s = c->slots[si];
-    CUDA_OK(c, cudaEventRecord(s.ev_free, c->s_main));  // after work already on the compute stream
+    // after work already on the compute stream: kernels a caller ran on its own streams on the
+    // slot's pointers must be ordered before this call by the caller (header contract)
+    CUDA_OK(c, cudaEventRecord(s.ev_free, c->s_main));
     s.free_recorded = true;
     release_slot(c, si);
   });
@@ -2114,7 +2421,8 @@ odmoe_status odmoe_debug_read(const void* ctx, int what, int layer, void* dst, i
   if (!c || !dst) return ODMOE_E_STATE;
   auto it = c->hdbg_index.find(what);
   if (it == c->hdbg_index.end()) return ODMOE_E_STATE;
-  const int64_t off = it->second.first + (int64_t)((what == 11 || what == 12) ? 0 : layer) * it->second.second;
+  const bool single = what == 11 || what == 12 || what == 14 || what == 15 || what == 16;
+  const int64_t off = it->second.first + (int64_t)(single ? 0 : layer) * it->second.second;
   if (layer < 0 || layer >= c->L || bytes > it->second.second || off + bytes > (int64_t)c->hdbg.size()) return ODMOE_E_RANGE;
   std::memcpy(dst, c->hdbg.data() + off, (size_t)bytes);
   return ODMOE_OK;

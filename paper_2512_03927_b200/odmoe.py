@@ -63,7 +63,20 @@ class LayerRecord(ctypes.Structure):
     _fields_ = [("true_ids", ctypes.c_int32 * 8), ("pred_ids", ctypes.c_int32 * 8),
                 ("weights", ctypes.c_float * 8), ("pred_available", ctypes.c_int32),
                 ("correct", ctypes.c_int32), ("n_reloads", ctypes.c_int32),
-                ("load_wait_us", ctypes.c_float)]
+                ("load_wait_us", ctypes.c_float), ("pred_in_time", ctypes.c_int32),
+                ("correct_in_time", ctypes.c_int32), ("issued_ids", ctypes.c_int32 * 8),
+                ("reload_ids", ctypes.c_int32 * 8)]
+
+
+class TraceEvent(ctypes.Structure):
+    _fields_ = [("type", ctypes.c_int32), ("step", ctypes.c_int32), ("layer", ctypes.c_int32),
+                ("expert", ctypes.c_int32), ("slot", ctypes.c_int32), ("l_cur", ctypes.c_int32),
+                ("aux", ctypes.c_int32), ("rank", ctypes.c_int32), ("bytes", ctypes.c_int64),
+                ("t_us", ctypes.c_double)]
+
+
+EV_NAMES = ["StepStart", "LoadIssue", "LoadStart", "LoadEnd", "LoadCancel", "RouterDone", "ComputeStart",
+            "ComputeEnd", "Mispredict", "StepEnd"]
 
 
 class Stats(ctypes.Structure):
@@ -75,7 +88,8 @@ class Stats(ctypes.Structure):
         (n, ctypes.c_int64) for n in ("n_router", "n_w13", "n_w2", "n_shadow", "n_lm_head", "n_embed")] + [
         ("wait_us", ctypes.c_double), ("correct", ctypes.c_int64), ("predicted_total", ctypes.c_int64),
         ("refine_corrections", ctypes.c_int64), ("refine_correct", ctypes.c_int64), ("refine_total", ctypes.c_int64),
-        ("ms_attn", ctypes.c_double), ("n_attn", ctypes.c_int64)]
+        ("ms_attn", ctypes.c_double), ("n_attn", ctypes.c_int64), ("correct_in_time", ctypes.c_int64),
+        ("spec_steps", ctypes.c_int64), ("early_loads", ctypes.c_int64)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
@@ -125,6 +139,7 @@ _ffn_grouped = _sig("odmoe_expert_ffn_grouped", [_P, _P, _I, _P, _P, _P, _I, _I,
 _prefill_group = _sig("odmoe_prefill_group", [_P, _P, _I, _I, _I, _P, _P, _P, _P, _P])
 _prefill_dbg = _sig("odmoe_prefill_debug_read", [_P, _I, _I, _P, _I64])
 _set_option = _sig("odmoe_set_option", [_P, _I, _I64])
+_trace_read = _sig("odmoe_trace_read", [_P, _P, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32)])
 _plan_layer = _sig("odmoe_plan_layer", [_I, _I, _I, _I, _P, _I, _P, ctypes.POINTER(ctypes.c_int32)])
 _plan_pool = _sig("odmoe_plan_pool_holds", [_I, _I, _I, _I, _I, _I, _I], ctypes.c_int32)
 
@@ -135,7 +150,7 @@ EXPORTED = ["odmoe_set_option", "odmoe_expert_ffn_grouped", "odmoe_prefill_group
             "odmoe_quantize_int8_rows", "odmoe_gen_weights", "odmoe_load", "odmoe_load_wait",
             "odmoe_evict", "odmoe_predict_ahead", "odmoe_decode_step", "odmoe_prefill",
             "odmoe_debug_read", "odmoe_tensor_ptr", "odmoe_shadow_expert_ffn_nf4", "odmoe_quantize_nf4",
-            "odmoe_shadow_expert_ffn_fp8", "odmoe_quantize_fp8_rows"]
+            "odmoe_shadow_expert_ffn_fp8", "odmoe_quantize_fp8_rows", "odmoe_trace_read"]
 
 
 def abi_version() -> int:
@@ -355,6 +370,28 @@ class Engine:
     def set_time_kernels(self, level: int):
         """0 = no CUDA events, 1 = around the expert launches, 2 = around every kernel family."""
         self._ck(_set_option(self.ctx, 6, int(level)))
+
+    def set_trace(self, on: bool):
+        """Event trace on/off (LoadIssue/Start/End/Cancel, RouterDone, ComputeStart/End, Mispredict)."""
+        self._ck(_set_option(self.ctx, 7, int(bool(on))))
+
+    def set_align_period(self, period: int):
+        """Token alignment period T_p of the shadow (1 = Mode A; > 1 = cross-token speculation)."""
+        self._ck(_set_option(self.ctx, 8, int(period)))
+
+    def trace(self, cap: int = 1 << 16):
+        """Resolved trace events since the last call, as dicts (t_us = device µs, NaN = host-only)."""
+        out = []
+        buf = (TraceEvent * cap)()
+        while True:
+            n = ctypes.c_int32(0)
+            self._ck(_trace_read(self.ctx, buf, cap, ctypes.byref(n)))
+            for i in range(n.value):
+                e = buf[i]
+                out.append(dict(type=EV_NAMES[e.type], step=e.step, layer=e.layer, expert=e.expert, slot=e.slot,
+                                l_cur=e.l_cur, aux=e.aux, rank=e.rank, bytes=e.bytes, t_us=e.t_us))
+            if n.value < cap:
+                return out
 
     def set_position(self, pos: int):
         """Attention ctx: KV-cache position of the next decode step (0 = new sequence)."""

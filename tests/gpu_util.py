@@ -48,22 +48,35 @@ def l2rel(x, ref):
 
 
 def ids_match(gpu_ids, ref_logits, k):
-    """True if the GPU's top-k equals the oracle's, or differs only inside a near-tie window."""
-    ref = O.top_k(ref_logits, k)
-    if list(gpu_ids) == list(ref):
-        return True, False
-    if set(gpu_ids) == set(ref):
-        # same set, different order among equal-ish logits
-        return _order_tie_ok(gpu_ids, ref_logits), True
-    return O.near_tie(ref_logits, k), True
+    """(ok, excused): the GPU's top-k equals the oracle's, or differs from it only by swapping
+    members of the tied run at the k/k+1 boundary (O.ids_excusable, pinned by
+    tests/golden/near_tie_cases.json)."""
+    return O.ids_excusable([int(x) for x in gpu_ids], ref_logits, k)
 
 
-def _order_tie_ok(gpu_ids, ref_logits):
-    r = [float(ref_logits[i]) for i in gpu_ids]
-    for a, b in zip(r, r[1:]):
-        if b > a and abs(a - b) >= 1e-3 * max(abs(a), abs(b)):
-            return False
-    return True
+def token_match(gpu_token, ref_logits):
+    """Greedy token: the oracle's argmax, or a member of the tied run at the top (k = 1 rule)."""
+    return O.ids_excusable([int(gpu_token)], ref_logits, 1)
+
+
+def maxabs_rel(x, ref):
+    """max |x - ref| / max |ref| (SURVEY §8(c) Parity 3, reported beside the l2 error)."""
+    x = np.asarray(x, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    m = np.max(np.abs(ref))
+    return float(np.max(np.abs(x - ref)) / (m if m > 0 else 1.0))
+
+
+# Element-wise bound for vectors whose inputs are teacher-forced bit for bit (bf16 or fp32 weights
+# and u identical on both sides; the GPU accumulates in fp32 in another order): fp32 rounding only.
+# One wrong output element out of d = 4096 moves max-abs by O(1), l2 only by 1/64.
+TOL_ELEM = 1e-4
+
+
+def assert_close(x, ref, tol_l2, tol_max=TOL_ELEM, what=""):
+    e2, em = l2rel(x, ref), maxabs_rel(x, ref)
+    assert e2 <= tol_l2 and em <= tol_max, (what, e2, em)
+    return e2, em
 
 
 def d2h(ptr: int, nbytes: int) -> bytes:

@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
     missing = [n for n in declared() if not hasattr(lib, n)]
     assert not missing, missing
     assert set(declared()) == set(odmoe.EXPORTED)
-    assert odmoe.abi_version() == 1
+    assert odmoe.abi_version() == 2
 
 
 def test_library_is_sm100a_and_has_no_cpu_path():
