@@ -58,6 +58,12 @@ def parse():
                     help="with Mixtral's attention block (32 q / 8 kv heads, RoPE; SURVEY §8(f)4, reading Q29)")
     ap.add_argument("--context", type=int, default=512,
                     help="--attention: decode starts at this KV-cache position (rows before it zero: synthetic context)")
+    ap.add_argument("--align-period", type=int, default=1,
+                    help="token alignment period T_p of the shadow (1 = every token, the paper's optimum "
+                         "P:277; > 1 = cross-token speculation, SURVEY §8(f)2)")
+    ap.add_argument("--group-size", type=int, default=0, help="groups placement: G (0 => min(k, N))")
+    ap.add_argument("--no-r0", action="store_true", help="skip the paper-only SEP (refine 0) leg")
+    ap.add_argument("--trace-steps", type=int, default=2, help="steps traced for the Eq. 1 analysis (0 = skip)")
     ap.add_argument("--out", default="")
     return ap.parse_args()
 
@@ -226,8 +232,9 @@ def oracle_sample(n_layers=8):
 
 def run_reference(args):
     """--impl reference: the CPU oracle as the reference arm, on our arm's metric/config. Each step
-    is a bounded sample: one layer of the decode token (the steps walk the token's layers);
-    tokens/s = 1 / (mean layer time x 32 + LM head)."""
+    is a bounded sample: ONE of the 32 MoE layers of a decode token (the steps walk the token's
+    layers), so ms_per_step is the measured time of that sample and the timed region is
+    steps x ms_per_step; the metric (tok/s) = 1 / (mean layer time x 32 + LM head)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
@@ -248,7 +255,8 @@ def run_reference(args):
     s_tok = statistics.mean(times) * walk.shape.L + t_lm
     v = 1.0 / s_tok
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": s_tok * 1e3,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": statistics.mean(times) * 1e3,
+            "step": "one of the 32 MoE layers of a decode token (1/32 of a token; the LM head timed once)",
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": workload_config(args, 1),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": _blas_threads(), "kind": "oracle",
@@ -344,7 +352,10 @@ def main():
     refine = args.refine if args.predictor.startswith("shadow") else 0
     eng = odmoe.Engine(device=local, rank=rank, world_size=world, nccl_id=uid, predictor=pred,
                        slots_per_gpu=n_slots(args, n), lookahead=D, time_kernels=2, weight_seed=SEED,
-                       refine_depth=refine, placement=int(sliced(args, n)), **SHAPE, **attn_kw(args))
+                       refine_depth=refine, placement=int(sliced(args, n)), group_size=args.group_size,
+                       **SHAPE, **attn_kw(args))
+    if args.align_period > 1:
+        eng.set_align_period(args.align_period)
     if args.attention and args.prefill <= 0:
         eng.set_position(args.context)  # no prompt: decode over a zero-filled synthetic context
     t_create = time.time() - t_create
@@ -397,6 +408,22 @@ def main():
     clk = clocks.stop()
     dev_s = ev0.elapsed_time(ev1) * 1e-3
     st = eng.stats()
+    # paper-only SEP (refinement off: the token-aligned shadow alone) beside the default
+    r0 = None
+    if refine > 0 and not args.no_r0:
+        log(rank, "SEP refine 0 leg")
+        r0 = leg(eng, torch, barrier, dist, tok, min(args.steps, 8), refine=0, restore=refine)
+        tok = r0.pop("tok")
+    # Eq. 1 from a per-layer event trace of a few more steps
+    trace_ev = None
+    if args.trace_steps > 0:
+        log(rank, "traced steps")
+        eng.set_trace(True)
+        for _ in range(args.trace_steps):
+            tok, _ = eng.decode_step(tok, records=False)
+        time.sleep(0.05)
+        trace_ev = eng.trace()
+        eng.set_trace(False)
     if dist is not None:
         tt = torch.tensor([dev_s, wall], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -421,9 +448,9 @@ def main():
         gemv_ms = (st["ms_w13"] + st["ms_w2"]) / n_exp
         blob = EXPERT_BYTES // n if sliced(args, n) else EXPERT_BYTES   # bytes one launch pair streams
         achieved = blob / (gemv_ms * 1e-3) / 1e9 if gemv_ms > 0 else None
-        traffic = None
+        traffic = None  # ncu dram bytes of one launch pair, captured at this slice size only
         prof = os.path.join(ROOT, "profiles", "ncu_expert_gemv_r01.json")
-        if os.path.exists(prof):
+        if os.path.exists(prof) and not sliced(args, n):
             try:
                 traffic = json.load(open(prof)).get("dram_bytes_per_expert")
             except Exception:
@@ -436,6 +463,7 @@ def main():
             except Exception:
                 floor_us = None
         recall = st["correct"] / st["predicted_total"] if st["predicted_total"] else None
+        recall_it = st["correct_in_time"] / st["predicted_total"] if st["predicted_total"] else None
         recall_ref = st["refine_correct"] / st["refine_total"] if st["refine_total"] else None
         roof_tok = link_all * 1e9 / (64 * EXPERT_BYTES)
         line = {
@@ -446,10 +474,13 @@ def main():
                     "greedy token feedback)",
             "config": workload_config(args, n),
             "recall_eq3": recall,
+            "recall_in_time": recall_it,
             "recall_refined": recall_ref,
-            "recall_note": "recall_eq3 = Eq. 3 of the token-aligned INT8 shadow (the paper's SEP); "
-                           "recall_refined = predictions re-anchored at the main model's state each layer "
-                           "(refine_depth, DESIGN.md §7), which drive the loads when enabled",
+            "recall_note": "recall_eq3 = Eq. 3 of the token-aligned INT8 shadow (the paper's SEP, prediction "
+                           "accuracy); recall_in_time = the same with predictions that reached the host after "
+                           "their layer's router scored 0 (S:197); recall_refined = predictions re-anchored at "
+                           "the main model's state each layer (refine_depth, DESIGN.md §7), which drive the "
+                           "loads when enabled",
             "roofline": {"bound": "hbm", "kernel": "expert SwiGLU GEMV (W13+SwiGLU, W2+gate)",
                          "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / peaks["hbm_gbs"] if achieved else None, "traffic": traffic,
@@ -476,23 +507,22 @@ def main():
                        "pool_bytes": st["pool_bytes"], "resident_expert_bytes": st["resident_bytes"],
                        "shadow_bytes": st["shadow_bytes"], "reloads": st["reloads"],
                        "loads_cancelled": st["loads_cancelled"], "max_resident": st["max_resident"],
-                       "ms_router": st["ms_router"] / max(1, st["n_router"]) * 1e3,
+                       "us_router": st["ms_router"] / max(1, st["n_router"]) * 1e3,
                        "us_shadow_per_step": st["ms_shadow"] / args.steps * 1e3,
                        "us_lm_head": st["ms_lm_head"] / max(1, st["n_lm_head"]) * 1e3,
                        "us_attention_per_step": st["ms_attn"] / args.steps * 1e3},
         }
-        # Eq. 1 (reading Q12): t_maxload = N_G t^M + (N_G - 1) t^W; the method is I/O-bound
-        # when one expert's load takes longer ("compare it with t^maxload")
-        ng = 1 if sliced(args, n) else max(1, n // 2)
-        per_layer = 2 if (n == 1 or sliced(args, n)) else 1     # launch pairs one GPU runs per layer
-        t_M = st["ms_router"] / max(1, st["n_router"]) * 1e3
-        t_W = gemv_ms * 1e3 * per_layer
-        t_load = blob / (link_all / n * 1e9) * 1e6 * per_layer
-        t_max = ng * t_M + (ng - 1) * t_W
-        line["eq1"] = {"N_G": ng, "t_M_us": t_M, "t_W_us": t_W, "t_load_us": t_load, "t_maxload_us": t_max,
-                       "io_bottlenecked": t_load > t_max,
-                       "note": "t^M = router kernel, t^W = expert GEMVs of one GPU for one layer (CUDA events); "
-                               "t_load = that GPU's expert bytes per layer / measured H2D GB/s"}
+        # Eq. 1 (reading Q12): t_maxload = N_G t^M + (N_G - 1) t^W, validated per layer
+        # against the event trace of the traced steps
+        G = args.group_size or min(SHAPE["k"], n)
+        ng = 1 if sliced(args, n) else max(1, n // G)
+        if trace_ev is not None:
+            line["eq1"] = eq1_from_trace(trace_ev, ng, SHAPE["L"])
+        sh_rf = shadow_roofline(st, args.steps, peaks["hbm_gbs"])
+        if sh_rf is not None:
+            line["roofline_shadow"] = sh_rf
+        if r0 is not None:
+            line["sep_refine0"] = r0
         if prefill is not None:
             line["prefill"] = prefill
         if res is not None:
@@ -523,6 +553,116 @@ def main():
     faulthandler.cancel_dump_traceback_later()
     log(rank, "done")
     return 0
+
+
+def leg(eng, torch, barrier, dist, tok, steps, refine, restore):
+    """A short extra on-demand leg on the same engine with another refinement depth (time_kernels
+    stays on; CUDA-event time, max over ranks). Returns tokens/s, recall and the shadow's GPU time."""
+    eng.set_refine_depth(refine)
+    tok, _ = eng.decode_step(tok, records=False)
+    eng.reset_stats()
+    barrier()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        tok, _ = eng.decode_step(tok, records=False)
+    b.record()
+    barrier()
+    sec = a.elapsed_time(b) * 1e-3
+    if dist is not None:
+        t = torch.tensor([sec], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        sec = float(t[0])
+    st = eng.stats()
+    out = {"refine_depth": refine, "steps": steps, "value": steps / sec, "unit": UNIT,
+           "recall_eq3": st["correct"] / st["predicted_total"] if st["predicted_total"] else None,
+           "recall_in_time": st["correct_in_time"] / st["predicted_total"] if st["predicted_total"] else None,
+           "reloads_per_step": st["reloads"] / steps, "us_shadow_per_step": st["ms_shadow"] / steps * 1e3,
+           "bytes_h2d_per_step": st["bytes_h2d"] / steps, "tok": tok}
+    eng.set_refine_depth(restore)
+    return out
+
+
+def shadow_roofline(st, steps, peak):
+    """The INT8 shadow's expert phases (one launch per phase for the k experts of a layer) against
+    the HBM peak: algorithmic bytes = int8 codes + fp32 row scales of the k experts."""
+    if not st.get("n_sh_w13") or not st.get("n_sh_w2"):
+        return None
+    k, d, F = SHAPE["k"], SHAPE["d"], SHAPE["F"]
+    b13 = k * (2 * F * d + 2 * F * 4)
+    b2 = k * (d * F + d * 4)
+    us13 = st["ms_sh_w13"] / (st["n_sh_w13"] / k) * 1e3
+    us2 = st["ms_sh_w2"] / (st["n_sh_w2"] / k) * 1e3
+    out = {"bound": "hbm", "kernel": "INT8 shadow experts, one launch per phase for the layer's k experts",
+           "w13": {"bytes": b13, "us": us13, "GBps": b13 / us13 / 1e3, "frac": b13 / us13 / 1e3 / peak},
+           "w2": {"bytes": b2, "us": us2, "GBps": b2 / us2 / 1e3, "frac": b2 / us2 / 1e3 / peak},
+           "peak": peak, "unit": "GB/s", "us_shadow_per_step": st["ms_shadow"] / steps * 1e3}
+    out["frac"] = (b13 + b2) / (us13 + us2) / 1e3 / peak
+    return out
+
+
+def eq1_from_trace(ev, ng, L):
+    """Eq. 1 (worked example P:137; reading Q12) against the measured per-layer trace of this
+    rank: t^M_l = main-node time of layer l (previous layer's last expert end -> this layer's routing
+    known), t^W_l = expert computation of layer l on this GPU, t_load = one expert load (LoadStart ->
+    LoadEnd, landed loads). Eq. 1 predicts an I/O stall at layer l iff t_load > t^maxload = N_G t^M +
+    (N_G - 1) t^W; the trace measures one when the expert start waited for its load (ComputeStart -
+    RouterDone > 5 us)."""
+    import math
+    by = {}
+    for e in ev:
+        by.setdefault(e["type"], []).append(e)
+    full = max((e["bytes"] for e in by.get("LoadEnd", [])), default=0)
+    starts = {}
+    for e in by.get("LoadStart", []):
+        starts.setdefault((e["step"], e["layer"], e["expert"]), []).append(e["t_us"])
+    loads = []
+    for e in by.get("LoadEnd", []):
+        key = (e["step"], e["layer"], e["expert"])
+        if e["bytes"] == full and key in starts and not math.isnan(e["t_us"]):
+            loads.append(e["t_us"] - max(starts[key]))
+    router = {(e["step"], e["layer"]): e["t_us"] for e in by.get("RouterDone", [])}
+    cs, ce, cw = {}, {}, {}
+    cstart = {(e["step"], e["layer"], e["expert"]): e["t_us"] for e in by.get("ComputeStart", [])}
+    for e in by.get("ComputeStart", []):
+        cs.setdefault((e["step"], e["layer"]), []).append(e["t_us"])
+    for e in by.get("ComputeEnd", []):
+        ce.setdefault((e["step"], e["layer"]), []).append(e["t_us"])
+        key = (e["step"], e["layer"], e["expert"])
+        if key in cstart:  # this expert's kernel time (its start event fires once its load has landed)
+            cw[(e["step"], e["layer"])] = cw.get((e["step"], e["layer"]), 0.0) + e["t_us"] - cstart[key]
+    step0 = {e["step"]: e["t_us"] for e in by.get("StepStart", [])}
+    tM, tW, stalls = [], [], []
+    for (s, l), tr in sorted(router.items()):
+        prev = None
+        for j in range(l - 1, -1, -1):
+            if (s, j) in ce:
+                prev = max(ce[(s, j)])
+                break
+        if prev is None:
+            prev = step0.get(s)
+        if prev is not None:
+            tM.append(tr - prev)
+        if (s, l) in cs and (s, l) in cw:
+            tW.append(cw[(s, l)])
+            # time the layer's expert work spent waiting for its loads once the routing was known
+            stalls.append(max(ce[(s, l)]) - tr - cw[(s, l)])
+    if not loads or not tM or not tW:
+        return {"N_G": ng, "note": "trace incomplete on this rank"}
+    mean = lambda v: sum(v) / len(v)  # noqa: E731
+    t_M, t_W, t_load = mean(tM), mean(tW), mean(loads)
+    t_max = ng * t_M + (ng - 1) * t_W
+    pred_stall = t_load > t_max
+    n_stall = sum(1 for x in stalls if x > 5.0)
+    return {"N_G": ng, "t_M_us": t_M, "t_W_us": t_W, "t_load_us": t_load, "t_maxload_us": t_max,
+            "io_bottlenecked": pred_stall, "layers_traced": len(stalls),
+            "stalled_layers_measured": n_stall, "stalled_layers_predicted": len(stalls) if pred_stall else 0,
+            "mean_stall_us": mean(stalls), "loads_traced": len(loads),
+            "note": "this rank's layers; t^M = previous layer's last expert end -> routing known; t^W = this "
+                    "GPU's expert kernel time of the layer; stall = (last expert end - routing known) - t^W, "
+                    "the time the layer's expert work waited for its loads (P:124, Fig. 4); CUDA events, "
+                    "S:350-358 trace"}
 
 
 def resident_baseline(odmoe, torch, args, dev, rank, world, dist):
@@ -579,7 +719,7 @@ def resident_baseline(odmoe, torch, args, dev, rank, world, dist):
             "expert_gemv_us": gemv_ms * 1e3,
             "expert_gemv_GBps": blob / (gemv_ms * 1e-3) / 1e9 if gemv_ms > 0 else None,
             "resident_expert_bytes_per_gpu": st["resident_bytes"],
-            "hbm_roofline_tok_s_1gpu": 6541.5e9 / (64 * EXPERT_BYTES + SHAPE["V"] * SHAPE["d"] * 2)}
+            "hbm_roofline_tok_s_1gpu": measured_peaks()[0]["hbm_gbs"] * 1e9 / (64 * EXPERT_BYTES + SHAPE["V"] * SHAPE["d"] * 2)}
 
 
 if __name__ == "__main__":

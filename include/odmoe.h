@@ -110,7 +110,16 @@ typedef struct {
                                 attention (the MoE-only hot path); head_dim = d / H in {32, 64, 128}     */
   int32_t n_kv_heads;        /* key/value heads (GQA), H % Hkv == 0, H / Hkv <= 8                       */
   int32_t max_seq;           /* KV-cache capacity in tokens (0 => 4096 when n_heads > 0)                */
-  int32_t reserved[2];
+  int32_t emulate_world;     /* 0/1 = off; N in {2, 4, 8} with world_size == 1: run the expert arithmetic
+                                of an N-GPU run of `placement` on this one GPU -- SLICED: each routed
+                                expert as N F/N slices computed with the kernels and grid a real rank
+                                uses, each emulated rank's k gated partials summed in router rank order,
+                                the N partials summed in rank order (the P2P combine's order); GROUPS:
+                                the experts summed per emulated rank of layer l's group (sorted pairing)
+                                then over the group's ranks in rank order. Values are bitwise those of
+                                the real N-GPU run (parity of the multi-GPU arithmetic on one GPU; time
+                                is NOT emulated). On-demand decode only (no prefill)                   */
+  int32_t reserved[1];
   const void* nccl_id;       /* 128-byte ncclUniqueId from rank 0 (NULL when world_size == 1)          */
 } odmoe_config;
 
@@ -163,6 +172,10 @@ typedef struct {
   int64_t spec_steps;                /* decode steps whose predictions came from a speculative shadow pass
                                         (token alignment period > 1, the shadow's own token)            */
   int64_t early_loads;               /* loads issued for the NEXT token while this one was decoding     */
+  /* time_kernels = 2: the shadow's expert phases (one launch per phase for its k experts; also in
+     ms_shadow): W13 + SwiGLU, W2 + gate; n_* count experts */
+  double ms_sh_w13, ms_sh_w2;
+  int64_t n_sh_w13, n_sh_w2;
 } odmoe_stats;
 
 /* ------------------------------------------------------------------ lifecycle */
@@ -409,7 +422,13 @@ odmoe_status odmoe_prefill_debug_read(const void* ctx, int what, int layer, void
  *   5 Y fp32[d] (combined)  6 Y_PART fp32[k][d] (N=1: per selected expert, rank order)
  *   7 SH_H_IN fp32[d]  8 SH_U bf16[d]  9 SH_LOGITS fp32[E]  10 SH_IDS int32[k]
  *   11 H_FINAL fp32[d] (layer ignored)  12 LM_LOGITS fp32[V] (layer ignored)
- *   13 H_PRE fp32[d] (n_heads > 0: h before the attention block of the layer) */
+ *   13 H_PRE fp32[d] (n_heads > 0: h before the attention block of the layer)
+ *   with a token alignment period > 1, the shadow pass that produced this step's predictions:
+ *   14 SH_H_FINAL fp32[d] (its h_L)  15 SH_TOK int32[1] (its own greedy token)
+ *   16 SH_LM_LOGITS fp32[V] (its INT8-row LM head logits)   (layer ignored for 11, 12, 14-16)
+ *   with emulate_world = N: 5 Y fp32[d] = the combined output of the N emulated ranks;
+ *   17 Y_RANK fp32[N][d] = each emulated rank's partial (sliced: its F/N slices of the k experts,
+ *   summed in router rank order; groups: its experts) */
 odmoe_status odmoe_debug_read(const void* ctx, int what, int layer, void* dst, int64_t bytes);
 
 /* Device pointers of ctx-owned tensors (tests): 0 emb, 1 lm_head, 2 router[layer],

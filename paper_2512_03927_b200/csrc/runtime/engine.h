@@ -15,7 +15,7 @@
 
 namespace odmoe {
 
-enum Family { K_ROUTER = 0, K_W13, K_W2, K_SHADOW, K_LM, K_EMBED, K_ATTN, K_NFAM };
+enum Family { K_ROUTER = 0, K_W13, K_W2, K_SHADOW, K_LM, K_EMBED, K_ATTN, K_SH_W13, K_SH_W2, K_NFAM };
 
 struct Slot {
   char* dev = nullptr;
@@ -39,6 +39,16 @@ struct Ctx {
   bool sliced = false;    // ODMOE_PLACE_SLICED: this rank's experts are F/N-wide slices
   int Fs = 0;             // F of the blobs this rank holds (F, or F / world when sliced)
   int64_t full_bytes = 0; // one whole expert blob (generator output)
+  // emulate_world (world 1): the expert arithmetic of an N-GPU run on this GPU (odmoe.h)
+  int emu = 0;                   // emulated ranks (0 = off)
+  bool emu_sliced = false;       // SLICED: blob = N slice blobs (slice r laid out as rank r's pool blob)
+  int emu_G = 1, emu_NG = 1;     // GROUPS: group size and number of groups of the emulated run
+  int64_t emu_slice_bytes = 0, emu_w13s = 0;
+  float* d_yemu = nullptr;       // [N][k][d] sliced: expert j's partial of slice r
+  float* d_prank = nullptr;      // [N][d] each emulated rank's partial
+  const float** d_emu_ptr = nullptr;   // device pointer arrays [L][N + N*k]
+  const float** h_emu_ptr = nullptr;   // pinned staging of the same
+  float* dbg_yrank = nullptr;    // [L][N][d] (debug capture)
   bool resident = false;
   int built_pred = -1;           // predictor the ctx was created with (decides whether a shadow exists)
   int dev = 0;

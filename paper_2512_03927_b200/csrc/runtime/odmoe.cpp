@@ -146,6 +146,10 @@ void harvest_timers(Ctx* c) {
         case K_LM: c->stats.ms_lm_head += ms; c->stats.n_lm_head++; break;
         case K_EMBED: c->stats.ms_embed += ms; c->stats.n_embed++; break;
         case K_ATTN: c->stats.ms_attn += ms; c->stats.n_attn++; break;
+        case K_SH_W13:  // the shadow's expert phases also count in ms_shadow
+          c->stats.ms_shadow += ms; c->stats.n_shadow++; c->stats.ms_sh_w13 += ms; c->stats.n_sh_w13 += t.units; break;
+        case K_SH_W2:
+          c->stats.ms_shadow += ms; c->stats.n_shadow++; c->stats.ms_sh_w2 += ms; c->stats.n_sh_w2 += t.units; break;
       }
     }
     if (!t.graph) {  // graph-owned events stay with the graph
@@ -282,10 +286,23 @@ void validate(const odmoe_config* g) {
     if (g->slots_per_gpu != -1 && g->slots_per_gpu < g->k) bad("sliced placement needs slots_per_gpu >= k");
   }
   if (g->predictor == ODMOE_PRED_SHADOW_NF4 && (g->d % 64 || g->F % 64)) bad("the NF4 shadow needs d, F multiples of 64");
+  if (g->emulate_world > 1) {
+    const int N = g->emulate_world;
+    if (N != 2 && N != 4 && N != 8) bad("emulate_world must be 0, 1, 2, 4 or 8");
+    if (g->world_size != 1) bad("emulate_world runs on one GPU (world_size 1)");
+    if (g->slots_per_gpu == -1) bad("emulate_world: on-demand decode only");
+    if (g->placement == ODMOE_PLACE_SLICED && g->F % (16 * N)) bad("emulated sliced placement needs F % (16 N) == 0");
+    if (g->placement == ODMOE_PLACE_GROUPS) {
+      const int Ge = g->group_size > 0 ? g->group_size : std::min(g->k, N);
+      if (N % Ge || g->k % Ge) bad("emulate_world: N and k must be divisible by the group size");
+    }
+  } else if (g->emulate_world < 0) {
+    bad("emulate_world must be 0, 1, 2, 4 or 8");
+  }
   if (g->lookahead < 1) bad("lookahead must be >= 1");
   if (g->world_size < 1 || g->rank < 0 || g->rank >= g->world_size) bad("rank/world_size");
   const int G = g->group_size > 0 ? g->group_size : std::min(g->k, g->world_size);
-  if (g->world_size % G) bad("world_size must be divisible by the group size (S:251, S:269)");
+  if (g->world_size % G && g->emulate_world <= 1) bad("world_size must be divisible by the group size (S:251, S:269)");
   if (g->k % G) bad("k must be divisible by the group size");
   if (g->world_size > 1 && G != g->k) bad("multi-GPU needs group_size == k (one expert per GPU per layer)");
   if (g->slots_per_gpu != -1 && g->slots_per_gpu < g->k / G) bad("slots_per_gpu must be >= k/G or -1");
@@ -518,6 +535,18 @@ bool rank_may_need(const Ctx* c, int l, int e) {
 // (a pitched copy), laid out as a blob of an expert with F = Fs. `full` is whole-blob scratch.
 void gen_blob(Ctx* c, int l, int e, char* dst, char* full) {
   const int d = c->d, F = c->F;
+  if (c->emu > 1 && c->emu_sliced) {  // N slice blobs back to back, slice r as rank r would hold it
+    CUDA_OK(c, launch_gen(full, 0, l, e, 0, 0, 0, d, F, c->cfg.weight_seed, c->wt, c->s_main));
+    const size_t es = c->esz;
+    for (int r = 0; r < c->emu; ++r) {
+      char* o = dst + (size_t)r * c->emu_slice_bytes;
+      const size_t f0 = (size_t)r * c->Fs;
+      CUDA_OK(c, cudaMemcpyAsync(o, full + 2 * f0 * d * es, (size_t)c->emu_w13s, cudaMemcpyDeviceToDevice, c->s_main));
+      CUDA_OK(c, cudaMemcpy2DAsync(o + c->emu_w13s, (size_t)c->Fs * es, full + (size_t)2 * F * d * es + f0 * es,
+                                   (size_t)F * es, (size_t)c->Fs * es, (size_t)d, cudaMemcpyDeviceToDevice, c->s_main));
+    }
+    return;
+  }
   if (!c->sliced) {
     CUDA_OK(c, launch_gen(dst, 0, l, e, 0, 0, 0, d, F, c->cfg.weight_seed, c->wt, c->s_main));
     return;
@@ -722,6 +751,14 @@ void build_buffers(Ctx* c) {
   c->reloaded.assign(L, {});
   c->in_time.assign(L, 0);
   select_buf(c, 0);
+  if (c->emu > 1) {
+    const int N = c->emu;
+    c->d_yemu = dmalloc<float>(c, (size_t)N * k * d, "emulated slice outputs");
+    c->d_prank = dmalloc<float>(c, (size_t)N * d, "emulated rank partials");
+    c->d_emu_ptr = dmalloc<const float*>(c, (size_t)L * (N + N * k), "emulation pointer arrays");
+    c->h_emu_ptr = hmalloc<const float*>(c, (size_t)L * (N + N * k), "emulation pointer arrays (host)");
+    if (c->cfg.debug_capture) c->dbg_yrank = dmalloc<float>(c, (size_t)L * N * d, "dbg_yrank");
+  }
   c->predB_tbl.assign((size_t)L * k, -1);
   if (c->cfg.debug_capture && c->rank == 0) {
     c->dbg_h = dmalloc<float>(c, (size_t)L * d, "dbg_h");
@@ -745,8 +782,8 @@ void shadow_experts(Ctx* c, const ExpertRef* ex, const void* u, int u_f32, float
   const int k = c->k, d = c->d, F = c->F;
   // shapes the flat engine does not take run one launch per expert (count them all)
   if (!multi_flat_ok(k, c->sh_ewt, d, F)) c->stats.kernel_launches += 2 * (k - 1);
-  { KTimer t(c, K_SHADOW, s, k); CUDA_OK(c, launch_w13_multi(k, ex, c->sh_ewt, u, u_f32, a, d, F, s, pdl_first)); }
-  { KTimer t(c, K_SHADOW, s, k); CUDA_OK(c, launch_w2_multi(k, ex, c->sh_ewt, a, gate_w, y, d, F, s, true)); }
+  { KTimer t(c, K_SH_W13, s, k); CUDA_OK(c, launch_w13_multi(k, ex, c->sh_ewt, u, u_f32, a, d, F, s, pdl_first)); }
+  { KTimer t(c, K_SH_W2, s, k); CUDA_OK(c, launch_w2_multi(k, ex, c->sh_ewt, a, gate_w, y, d, F, s, true)); }
 }
 
 // ------------------------------------------------------------------ shadow forward (SEP, Mode A)
@@ -1207,6 +1244,55 @@ uint32_t p2p_mask(const Ctx* c, int l) {
 }
 
 // ------------------------------------------------------------------ one decode step
+// emulate_world: layer l's combine as an N-GPU run performs it (odmoe.h): each emulated rank sums its
+// gated partials in router rank order (p2p_send's order), then the ranks' partials are summed in rank
+// order into d_yred (p2p_gather's order); the next router adds d_yred (n_add = 1).
+void emu_combine(Ctx* c, int l, const int32_t* S, cudaStream_t s) {
+  const int N = c->emu, k = c->k, d = c->d;
+  const float** hp = c->h_emu_ptr + (size_t)l * (N + N * k);
+  const float** dp = c->d_emu_ptr + (size_t)l * (N + N * k);
+  std::vector<int> nrank(N, 0);
+  int r0 = 0, nr = N;
+  if (c->emu_sliced) {
+    for (int r = 0; r < N; ++r) {
+      for (int j = 0; j < k; ++j) hp[N + r * k + j] = c->d_yemu + ((size_t)r * k + j) * d;
+      nrank[r] = k;
+    }
+  } else {  // layer l's group; each rank's experts by the sorted pairing
+    r0 = (l % c->emu_NG) * c->emu_G;
+    nr = c->emu_G;
+    for (int r = r0; r < r0 + nr; ++r) {
+      int32_t mine[8];
+      const int n = plan_layer(k, N, c->emu_G, l, S, r, mine);
+      for (int j = 0; j < k; ++j)
+        for (int i = 0; i < n; ++i)
+          if (S[j] == mine[i]) hp[N + r * k + nrank[r]++] = c->d_y + (size_t)j * d;
+    }
+  }
+  int np = 0;
+  for (int r = r0; r < r0 + nr; ++r)
+    if (nrank[r] > 0) hp[np++] = c->d_prank + (size_t)r * d;
+  CUDA_OK(c, cudaMemcpyAsync(dp, hp, sizeof(float*) * (N + N * k), cudaMemcpyHostToDevice, s));
+  for (int r = r0; r < r0 + nr; ++r) {
+    if (nrank[r] == 0) continue;
+    float* pr = c->d_prank + (size_t)r * d;
+    CUDA_OK(c, cudaMemsetAsync(pr, 0, sizeof(float) * d, s));
+    CUDA_OK(c, launch_combine(pr, dp + N + r * k, nrank[r], d, s));
+    c->stats.kernel_launches++;
+  }
+  CUDA_OK(c, cudaMemsetAsync(c->d_yred, 0, sizeof(float) * d, s));
+  CUDA_OK(c, launch_combine(c->d_yred, dp, np, d, s));
+  c->stats.kernel_launches++;
+  if (c->dbg_yrank) {
+    CUDA_OK(c, cudaMemsetAsync(c->dbg_yrank + (size_t)l * N * d, 0, sizeof(float) * N * d, s));
+    for (int r = r0; r < r0 + nr; ++r)
+      if (nrank[r] > 0)
+        CUDA_OK(c, cudaMemcpyAsync(c->dbg_yrank + ((size_t)l * N + r) * d, c->d_prank + (size_t)r * d, sizeof(float) * d,
+                                   cudaMemcpyDeviceToDevice, s));
+  }
+  if (c->dbg_yred) CUDA_OK(c, cudaMemcpyAsync(c->dbg_yred + (size_t)l * d, c->d_yred, sizeof(float) * d, cudaMemcpyDeviceToDevice, s));
+}
+
 bool fused_ngpu_enabled() {
   static int v = -1;
   if (v < 0) {
@@ -1242,7 +1328,7 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
   // SMs held by a kernel that waits for a peer that waits for us.
   // ODMOE_FUSED_NGPU=1 also allows it at N > 1: the prediction communicator is limited to one CTA
   // and the grid leaves one SM free, so the grid can always become resident beside it.
-  const bool fused = use_fused_expert() && stream_ok(c->wt, d) && stream_ok(c->wt, c->Fs) &&
+  const bool fused = use_fused_expert() && stream_ok(c->wt, d) && stream_ok(c->wt, c->Fs) && c->emu <= 1 &&
                      (c->world == 1 || c->resident || fused_ngpu_enabled());
 
   // Fully-resident 1-GPU steps (no attention, no debug capture) are the same sequence of launches
@@ -1350,7 +1436,8 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
     CUDA_OK(c, launch_embed(c->d_emb, nullptr, c->wt, c->d_tok_in, d, c->d_h, s));
   }
 
-  const float* const* yadd = c->world == 1 ? c->d_yptr : c->d_yredptr;
+  const bool multi = c->world > 1 || c->emu > 1;  // the next router adds one reduced partial
+  const float* const* yadd = multi ? c->d_yredptr : c->d_yptr;
   int n_add = 0;
   for (int l = 0; l < L; ++l) {
     c->l_cur = l;
@@ -1391,7 +1478,7 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
     }
     if (c->world > 1) NCCL_OK(c, ncclBroadcast(pkt, pkt, c->pkt_bytes, ncclChar, 0, c->comm, s));
     tr_dev(c, ODMOE_EV_ROUTER_DONE, s, l);
-    n_add = c->world == 1 ? k : 1;
+    n_add = multi ? 1 : k;
 
     const bool in_group = (l % c->NG) == c->my_group;
     if (c->resident) {
@@ -1493,7 +1580,18 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
           float* y = c->d_y + (size_t)ypos * d;
           ExpertRef e13 = direct_ref(sl.dev, nullptr, j);
           ExpertRef e2 = direct_ref(sl.dev + c->w13_bytes, nullptr, j);
-          if (fused) {  // one launch once the whole blob has landed
+          if (c->emu > 1) {  // the N-GPU run's launches on this GPU (split W13 / W2, reserve-1 grid)
+            CUDA_OK(c, cudaStreamWaitEvent(s, sl.ev_done, 0));
+            tr_dev(c, ODMOE_EV_COMPUTE_START, s, l, S[j], si);
+            const int nsl = c->emu_sliced ? c->emu : 1;
+            for (int r = 0; r < nsl; ++r) {
+              const char* base = sl.dev + (size_t)r * c->emu_slice_bytes;
+              const char* b2 = c->emu_sliced ? base + c->emu_w13s : sl.dev + c->w13_bytes;
+              float* yo = c->emu_sliced ? c->d_yemu + ((size_t)r * k + j) * d : y;
+              { KTimer t(c, K_W13, s); CUDA_OK(c, launch_w13(direct_ref(base, nullptr, j), c->wt, pkt, u_f32, c->d_a + (size_t)ypos * F, d, c->Fs, s)); }
+              { KTimer t(c, K_W2, s); CUDA_OK(c, launch_w2(direct_ref(b2, nullptr, j), c->wt, c->d_a + (size_t)ypos * F, w_dev, yo, d, c->Fs, s)); }
+            }
+          } else if (fused) {  // one launch once the whole blob has landed
             CUDA_OK(c, cudaStreamWaitEvent(s, sl.ev_done, 0));
             tr_dev(c, ODMOE_EV_COMPUTE_START, s, l, S[j], si);
             KTimer t(c, K_W13, s);
@@ -1518,6 +1616,7 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
           jj++;
         }
       }
+      if (c->emu > 1) emu_combine(c, l, S, s);
       if (c->next_plan <= l) c->next_plan = l + 1;
       pump(c);
       if (rec) {
@@ -1724,6 +1823,7 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
       }
     }
     add(11, c->dbg_hfinal, (int64_t)d * 4, 1);
+    if (c->dbg_yrank) add(17, c->dbg_yrank, (int64_t)c->emu * d * 4, L);
     add(12, c->d_lmlogits, (int64_t)c->V * 4, 1);
     if (c->dbg_hpre) add(13, c->dbg_hpre, (int64_t)d * 4, L);
   }
@@ -1841,6 +1941,7 @@ void prefill_impl(Ctx* c, const int32_t* tokens, int T, int32_t* token_out, int3
   if (E > kMaxGGExperts) fail(c, ODMOE_E_CONFIG, "prefill supports E <= 8");
   if (d % 256 || c->Fs % 128) fail(c, ODMOE_E_CONFIG, "prefill needs d % 256 == 0 and F (per rank) % 128 == 0");
   if (T < 1 || !tokens) fail(c, ODMOE_E_CONFIG, "empty prompt (S:108)");
+  if (c->emu > 1) fail(c, ODMOE_E_CONFIG, "emulate_world emulates the decode step only");
   c->predict_cache_token = -1;  // the KV position changes (odmoe_predict_ahead's cache)
   c->align_n = 0;                // a new sequence starts aligned
   c->spec_step = -1;
@@ -2049,6 +2150,8 @@ void destroy_ctx(Ctx* c) {
   F(c->d_lmscratch); F(c->d_lmlogits);
   F(c->sh_h); F(c->sh_u); F(c->sh_ids_all); F(c->sh_w); F(c->sh_logits_all); F(c->sh_a); F(c->sh_y); F((void*)c->sh_yptr);
   F(c->sh_tok); F(c->sh_lmscratch); F(c->sh_lmlogits);
+  F(c->d_yemu); F(c->d_prank); F((void*)c->d_emu_ptr); F(c->dbg_yrank);
+  if (c->h_emu_ptr) cudaFreeHost((void*)c->h_emu_ptr);
   F(c->dbg_h); F(c->dbg_ypart); F(c->dbg_yred); F(c->dbg_sh_h_all); F(c->dbg_sh_u_all); F(c->dbg_sh_hf_all); F(c->dbg_hfinal);
   F(c->p_h); F(c->p_pkt); F(c->p_tok); F(c->p_off); F(c->p_src); F(c->p_inv); F(c->p_gate);
   F(c->p_x); F(c->p_a2); F(c->p_y); F(c->p_part); F(c->p_tiles);
@@ -2141,6 +2244,19 @@ odmoe_status odmoe_create(const odmoe_config* cfg, void** ctx_out) {
     c->blob_elems = 3LL * c->Fs * c->d;
     c->blob_bytes = c->blob_elems * (int64_t)c->esz;
     c->w13_bytes = 2LL * c->Fs * c->d * (int64_t)c->esz;
+    if (cfg->emulate_world > 1) {
+      c->emu = cfg->emulate_world;
+      c->emu_sliced = cfg->placement == ODMOE_PLACE_SLICED;
+      if (c->emu_sliced) {
+        c->Fs = c->F / c->emu;  // every kernel launch runs one F/N slice, as on a real rank
+        c->emu_slice_bytes = 3LL * c->Fs * c->d * (int64_t)c->esz;
+        c->emu_w13s = 2LL * c->Fs * c->d * (int64_t)c->esz;
+        c->w13_bytes = c->blob_bytes;  // no W13 prefix in a blob of N slices: compute waits for all of it
+      } else {
+        c->emu_G = cfg->group_size > 0 ? cfg->group_size : std::min(c->k, c->emu);
+        c->emu_NG = c->emu / c->emu_G;
+      }
+    }
     c->G = c->sliced ? c->world : (cfg->group_size > 0 ? cfg->group_size : std::min(c->k, c->world));
     c->NG = c->world / c->G;
     c->my_group = c->rank / c->G;
@@ -2168,6 +2284,7 @@ odmoe_status odmoe_create(const odmoe_config* cfg, void** ctx_out) {
       CUDA_OK(c, cudaStreamCreateWithPriority(&c->s_main, cudaStreamNonBlocking, prio_hi));
       CUDA_OK(c, cudaStreamCreateWithPriority(&c->s_shadow, cudaStreamNonBlocking, prio_lo));
       CUDA_OK(c, cudaStreamCreateWithFlags(&c->s_copy, cudaStreamNonBlocking));
+      if (c->emu > 1) set_stream_sm_reserve(1);  // the flat engine's grid of a rank of a multi-GPU run
       if (c->world > 1) {
         ncclUniqueId id;
         std::memcpy(&id, cfg->nccl_id, sizeof(id));
@@ -2231,10 +2348,13 @@ odmoe_status odmoe_reset_stats(void* ctx) {
   return ODMOE_OK;
 }
 
+// Every ctx entry re-applies its flat-engine grid (a multi-GPU rank, real or emulated, leaves one SM
+// free); several ctxs may share a device within one process.
 #define CTX_GUARD(ctxp)                                                   \
   Ctx* c = reinterpret_cast<Ctx*>(ctxp);                                  \
   if (!c || c->poisoned) return ODMOE_E_STATE;                            \
-  cudaSetDevice(c->dev);
+  cudaSetDevice(c->dev);                                                  \
+  set_stream_sm_reserve((c->world > 1 || c->emu > 1) ? 1 : 0);
 
 odmoe_status odmoe_decode_step(void* ctx, int32_t token_in, int32_t* token_out, odmoe_layer_record* rec) {
   CTX_GUARD(ctx);

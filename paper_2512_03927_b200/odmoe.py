@@ -25,7 +25,7 @@ STATUS = {0: "OK", 1: "E_CONFIG", 2: "E_RANGE", 3: "E_NONFINITE", 4: "E_BUDGET",
 
 # debug_read fields
 DBG = dict(H_IN=0, U=1, LOGITS=2, IDS=3, W=4, Y=5, Y_PART=6, SH_H_IN=7, SH_U=8, SH_LOGITS=9,
-           SH_IDS=10, H_FINAL=11, LM_LOGITS=12, H_PRE=13)
+           SH_IDS=10, H_FINAL=11, LM_LOGITS=12, H_PRE=13, SH_H_FINAL=14, SH_TOK=15, SH_LM_LOGITS=16, Y_RANK=17)
 
 
 class OdmoeError(RuntimeError):
@@ -55,7 +55,7 @@ class Config(ctypes.Structure):
                 ("debug_capture", ctypes.c_int32), ("time_kernels", ctypes.c_int32),
                 ("pool_threads", ctypes.c_int32), ("refine_depth", ctypes.c_int32),
                 ("placement", ctypes.c_int32), ("n_heads", ctypes.c_int32), ("n_kv_heads", ctypes.c_int32),
-                ("max_seq", ctypes.c_int32), ("reserved", ctypes.c_int32 * 2),
+                ("max_seq", ctypes.c_int32), ("emulate_world", ctypes.c_int32), ("reserved", ctypes.c_int32 * 1),
                 ("nccl_id", ctypes.c_void_p)]
 
 
@@ -89,7 +89,8 @@ class Stats(ctypes.Structure):
         ("wait_us", ctypes.c_double), ("correct", ctypes.c_int64), ("predicted_total", ctypes.c_int64),
         ("refine_corrections", ctypes.c_int64), ("refine_correct", ctypes.c_int64), ("refine_total", ctypes.c_int64),
         ("ms_attn", ctypes.c_double), ("n_attn", ctypes.c_int64), ("correct_in_time", ctypes.c_int64),
-        ("spec_steps", ctypes.c_int64), ("early_loads", ctypes.c_int64)]
+        ("spec_steps", ctypes.c_int64), ("early_loads", ctypes.c_int64), ("ms_sh_w13", ctypes.c_double),
+        ("ms_sh_w2", ctypes.c_double), ("n_sh_w13", ctypes.c_int64), ("n_sh_w2", ctypes.c_int64)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
@@ -309,14 +310,14 @@ class Engine:
                  slots_per_gpu=2, rms_eps=1e-5, weight_seed=2512, aux_seed=1, rank=0, world_size=1,
                  group_size=0, device=0, chunk_bytes=0, debug_capture=0, time_kernels=0,
                  nccl_id: Optional[bytes] = None, refine_depth=0, placement=0, n_heads=0, n_kv_heads=0,
-                 max_seq=0):
+                 max_seq=0, emulate_world=0):
         self.cfg = Config(L=L, E=E, k=k, d=d, F=F, V=V, dtype=dtype, predictor=predictor,
                           lookahead=lookahead, slots_per_gpu=slots_per_gpu, rms_eps=rms_eps,
                           weight_seed=weight_seed, aux_seed=aux_seed, rank=rank, world_size=world_size,
                           group_size=group_size, device=device, chunk_bytes=chunk_bytes,
                           debug_capture=debug_capture, time_kernels=time_kernels, pool_threads=0,
                           refine_depth=refine_depth, placement=placement, n_heads=n_heads,
-                          n_kv_heads=n_kv_heads, max_seq=max_seq)
+                          n_kv_heads=n_kv_heads, max_seq=max_seq, emulate_world=emulate_world)
         self._uid = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
         self.cfg.nccl_id = ctypes.cast(self._uid, ctypes.c_void_p) if self._uid is not None else None
         self.L, self.E, self.k, self.d, self.F, self.V = L, E, k, d, F, V
