@@ -59,7 +59,7 @@ __all__ = [
     "decode_token_attn", "NF4_CODEBOOK", "NF4_BLOCK", "nf4_codebook_from_quantiles",
     "quantize_nf4_blocks", "dequantize_nf4_blocks", "quantize_model_nf4", "e4m3_values", "round_e4m3",
     "quantize_fp8_rows", "dequantize_fp8_rows", "quantize_model_fp8",
-    "near_tie", "tied_run", "ids_excusable", "expected_loads", "shadow_greedy_token", "shadow_decode",
+    "sliced_expert_partials", "near_tie", "tied_run", "ids_excusable", "expected_loads", "shadow_greedy_token", "shadow_decode",
     "plan_group_size", "plan_groups", "assign_layer", "assign_experts",
     "misprediction_reloads", "max_load_budget", "residency_bound", "recall_eq2", "recall_eq3",
     "recall_bruteforce", "prefill_permutation", "prefill_reference", "expert_counts",
@@ -143,6 +143,27 @@ def expert_ffn(W1, W3, W2, u):
     v = np.asarray(W3, dtype=np.float64) @ u
     a = silu(g) * v
     return np.asarray(W2, dtype=np.float64) @ a
+
+
+def sliced_expert_partials(W1, W3, W2, u, n: int):
+    """Sliced loading (the B200 generalisation of P:126's "(N_W - k)-fold" I/O
+    multiplication): the expert's F intermediate units are split into n contiguous blocks
+    B_r = [r F/n, (r+1) F/n); GPU r holds rows B_r of W1 and W3 and columns B_r of W2 and computes
+    partial_r = W2[:, B_r] (silu(W1[B_r] u) * (W3[B_r] u)). The F-sum of O5 regrouped: sum_r
+    partial_r = expert_ffn(W1, W3, W2, u). Returns the list of n partials [d]."""
+    W1 = np.asarray(W1, dtype=np.float64)
+    W3 = np.asarray(W3, dtype=np.float64)
+    W2 = np.asarray(W2, dtype=np.float64)
+    u = np.asarray(u, dtype=np.float64)
+    F = W1.shape[0]
+    if F % n:
+        raise ValueError("F must be divisible by the number of slices")
+    out = []
+    for r in range(n):
+        B = slice(r * F // n, (r + 1) * F // n)
+        a = silu(W1[B] @ u) * (W3[B] @ u)
+        out.append(W2[:, B] @ a)
+    return out
 
 
 # ---------------------------------------------------------------- O6 one MoE layer (P:113-124)

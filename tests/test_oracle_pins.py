@@ -655,3 +655,30 @@ def test_shadow_decode_unaligned_iterations_ignore_the_main_token(tiny_fp32, tin
             assert t_in[n] == t_out[n - 1]
         else:
             assert t_in[n] == main_in[n]
+
+
+# ------------------------------------------------------------------ sliced loading
+def test_sliced_partials_closed_form_and_sum():
+    """W1 = W3 = W2 = I (F = d = 4, n = 2): expert_ffn(u) = silu(u) * u; slice 0 owns units 0-1 and
+    writes only outputs 0-1 through W2's COLUMNS 0-1, slice 1 the rest (closed form). On random
+    weights the partials sum to expert_ffn and n = 1 is expert_ffn itself."""
+    u = np.array([0.5, -1.0, 2.0, 0.25])
+    I = np.eye(4)
+    p = O.sliced_expert_partials(I, I, I, u, 2)
+    s = u / (1.0 + np.exp(-u)) * u
+    assert np.allclose(p[0], [s[0], s[1], 0, 0], rtol=0, atol=1e-15)
+    assert np.allclose(p[1], [0, 0, s[2], s[3]], rtol=0, atol=1e-15)
+    W2 = np.arange(16.0).reshape(4, 4)   # distinguishes columns from rows
+    p = O.sliced_expert_partials(I, I, W2, u, 2)
+    assert np.allclose(p[0], W2[:, :2] @ s[:2], rtol=1e-15) and np.allclose(p[1], W2[:, 2:] @ s[2:], rtol=1e-15)
+    rng = np.random.default_rng(24)
+    W1, W3 = rng.normal(size=(64, 16)), rng.normal(size=(64, 16))
+    W2r = rng.normal(size=(16, 64))
+    x = rng.normal(size=16)
+    full = O.expert_ffn(W1, W3, W2r, x)
+    for n in (1, 2, 4, 8):
+        parts = O.sliced_expert_partials(W1, W3, W2r, x, n)
+        assert len(parts) == n and np.allclose(np.sum(parts, axis=0), full, rtol=1e-12, atol=1e-12)
+    assert np.array_equal(O.sliced_expert_partials(W1, W3, W2r, x, 1)[0], full)
+    with pytest.raises(ValueError):
+        O.sliced_expert_partials(W1, W3, W2r, x, 3)
