@@ -807,6 +807,7 @@ cudaError_t launch_w13_flat(ExpertRef ex, WType wt, const void* u, int u_f32, fl
     case W_U8: return lowbit_xf32() ? fg_launch<u8b, float, 0>(a, s, pdl) : fg_launch<u8b, uint16_t, 0>(a, s, pdl);
     case W_NF4: return fg_launch<nf4x2, uint16_t, 0>(a, s, pdl);  // bf16 x measured faster for NF4
     case W_F8: return lowbit_xf32() ? fg_launch<fp8e4, float, 0>(a, s, pdl) : fg_launch<fp8e4, uint16_t, 0>(a, s, pdl);
+    default: break;  // W_I8P: mma_gemv.cu
   }
   return cudaErrorInvalidValue;
 }
@@ -823,6 +824,7 @@ cudaError_t launch_w2_flat(ExpertRef ex, WType wt, const float* act, const float
     case W_U8: return fg_launch<u8b, float, 1>(a, s, pdl);
     case W_NF4: return fg_launch<nf4x2, float, 1>(a, s, pdl);
     case W_F8: return fg_launch<fp8e4, float, 1>(a, s, pdl);
+    default: break;  // W_I8P: mma_gemv.cu
   }
   return cudaErrorInvalidValue;
 }
@@ -1164,6 +1166,7 @@ bool multi_flat_ok(int n, WType wt, int d, int F) {
     const char* e = getenv("ODMOE_MULTI");  // ODMOE_MULTI=0: one launch per expert (A/B)
     on = (e && e[0] == '0') ? 0 : 1;
   }
+  if (wt == W_I8P) return on && n >= 1 && n <= kMaxMulti && mma_shadow_ok(d, F);
   return on && n >= 1 && n <= kMaxMulti && gemv_engine() == 2 && stream_ok(wt, d) && stream_ok(wt, F);
 }
 
@@ -1176,6 +1179,7 @@ cudaError_t launch_w13_multi(int n, const ExpertRef* ex, WType wt, const void* u
     }
     return cudaSuccess;
   }
+  if (wt == W_I8P) return launch_mma_shadow(n, ex, 0, u, nullptr, a_buf, d, F, s, pdl);
   MultiArgs m{};
   m.n = n;
   for (int i = 0; i < n; ++i) {
@@ -1190,6 +1194,7 @@ cudaError_t launch_w13_multi(int n, const ExpertRef* ex, WType wt, const void* u
     case W_U8: return lowbit_xf32() ? fg_multi_launch<u8b, float, 0>(m, s, pdl) : fg_multi_launch<u8b, uint16_t, 0>(m, s, pdl);
     case W_NF4: return fg_multi_launch<nf4x2, uint16_t, 0>(m, s, pdl);
     case W_F8: return lowbit_xf32() ? fg_multi_launch<fp8e4, float, 0>(m, s, pdl) : fg_multi_launch<fp8e4, uint16_t, 0>(m, s, pdl);
+    default: break;  // W_I8P: mma_gemv.cu
   }
   return cudaErrorInvalidValue;
 }
@@ -1203,6 +1208,7 @@ cudaError_t launch_w2_multi(int n, const ExpertRef* ex, WType wt, const float* a
     }
     return cudaSuccess;
   }
+  if (wt == W_I8P) return launch_mma_shadow(n, ex, 1, a_buf, gate_w, y_buf, d, F, s, pdl);
   MultiArgs m{};
   m.n = n;
   for (int i = 0; i < n; ++i) {
@@ -1217,6 +1223,7 @@ cudaError_t launch_w2_multi(int n, const ExpertRef* ex, WType wt, const float* a
     case W_U8: return fg_multi_launch<u8b, float, 1>(m, s, pdl);
     case W_NF4: return fg_multi_launch<nf4x2, float, 1>(m, s, pdl);
     case W_F8: return fg_multi_launch<fp8e4, float, 1>(m, s, pdl);
+    default: break;  // W_I8P: mma_gemv.cu
   }
   return cudaErrorInvalidValue;
 }
@@ -1291,6 +1298,7 @@ cudaError_t launch_expert_fused(ExpertRef ex, const void* w2_direct, const float
     case W_U8: return lowbit_xf32() ? fused_launch<u8b, float>(a13, a2, s, pdl) : fused_launch<u8b, uint16_t>(a13, a2, s, pdl);
     case W_NF4: return fused_launch<nf4x2, uint16_t>(a13, a2, s, pdl);
     case W_F8: return lowbit_xf32() ? fused_launch<fp8e4, float>(a13, a2, s, pdl) : fused_launch<fp8e4, uint16_t>(a13, a2, s, pdl);
+    default: break;  // W_I8P: mma_gemv.cu
   }
   return cudaErrorInvalidValue;
 }

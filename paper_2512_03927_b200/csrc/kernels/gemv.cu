@@ -191,6 +191,7 @@ int gemv_engine() {
 
 cudaError_t launch_w13(ExpertRef ex, WType wt, const void* u, int u_f32, float* a, int d, int F,
                        cudaStream_t s, bool pdl) {
+  if (wt == W_I8P) return launch_mma_shadow(1, &ex, 0, u, nullptr, a, d, F, s, pdl);
   if (wt == W_U8)  // flat engine only (the engine picks W_U8 only where it applies)
     return stream_ok(wt, d) ? launch_w13_flat(ex, wt, u, u_f32, a, d, F, s, pdl) : cudaErrorInvalidValue;
   if (wt == W_NF4 || wt == W_F8)
@@ -211,6 +212,7 @@ cudaError_t launch_w13(ExpertRef ex, WType wt, const void* u, int u_f32, float* 
 
 cudaError_t launch_w2(ExpertRef ex, WType wt, const float* a, const float* gate_w, float* y, int d,
                       int F, cudaStream_t s, bool pdl) {
+  if (wt == W_I8P) return launch_mma_shadow(1, &ex, 1, a, gate_w, y, d, F, s, pdl);
   if (wt == W_U8)
     return stream_ok(wt, F) ? launch_w2_flat(ex, wt, a, gate_w, y, d, F, s, pdl) : cudaErrorInvalidValue;
   if (wt == W_NF4 || wt == W_F8)

@@ -5,7 +5,10 @@
 
 namespace odmoe {
 
-enum WType { W_BF16 = 0, W_F32 = 1, W_I8 = 2, W_NF4 = 3, W_F8 = 4, W_U8 = 5 };
+enum WType { W_BF16 = 0, W_F32 = 1, W_I8 = 2, W_NF4 = 3, W_F8 = 4, W_U8 = 5, W_I8P = 6 };
+// W_I8P (INT8 shadow experts, mma_gemv.cu): the biased codes q + 128 in the fragment-packed layout of
+// mma.sync m16n8k16 (16-row tiles x 32-column blocks of 512 B; W13 tiles pair gate/up rows), same
+// natural-order row scales; expert blob = packed W13 (2Fd bytes) then packed W2 (dF bytes).
 // W_U8 (shadow experts on the flat engine only): the INT8-row codes q stored as the byte q + 128,
 // same row scales; the dot product then widens a byte without flipping its sign bit first.
 // W_F8 (shadow experts only, reading Q28): E4M3 codes, one fp32 scale per row (int8's layout).
@@ -176,6 +179,14 @@ cudaError_t launch_p2p_send(const float* const* y, int n, int d, float* dst, uin
                             cudaStream_t s);
 cudaError_t launch_p2p_gather(const float* part, const uint32_t* flags, uint32_t mask, int d, uint32_t epoch,
                               float* out, int32_t* err_flag, cudaStream_t s);
+
+// INT8 shadow experts on the tensor cores (mma_gemv.cu): one phase (mode 0 = W13 + SwiGLU -> out
+// [n][F], x = bf16 u; mode 1 = W2 + gate -> out [n][d], x = fp32 a [n][F]) of n <= 4 W_I8P experts.
+bool mma_shadow_ok(int d, int F);
+cudaError_t launch_mma_shadow(int n, const ExpertRef* ex, int mode, const void* x, const float* gate_w,
+                              float* out, int d, int F, cudaStream_t s, bool pdl);
+// biased codes [R][C] (row-major) -> W_I8P layout; pair_rows: W13's gate/up pairing
+cudaError_t launch_pack_i8_frag(const uint8_t* q_biased, uint8_t* out, int R, int C, int pair_rows, cudaStream_t s);
 
 // BF16 (round to nearest even) copy of an fp32 tensor: the BF16 shadow of an FP32 main model.
 cudaError_t launch_f32_to_bf16(const float* in, void* out, int64_t n, cudaStream_t s);

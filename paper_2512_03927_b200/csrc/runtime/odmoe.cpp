@@ -459,7 +459,11 @@ void build_shadow(Ctx* c, char* staging) {
   const char* u8e = getenv("ODMOE_SHADOW_U8");
   const bool u8 = !nf4 && !fp8 && !(u8e && u8e[0] == '0') && gemv_engine() == 2 && stream_ok(W_U8, d) &&
                   stream_ok(W_U8, F);
-  c->sh_ewt = nf4 ? W_NF4 : (fp8 ? W_F8 : (u8 ? W_U8 : W_I8));
+  // INT8 experts on the tensor cores (mma_gemv.cu): biased codes in the fragment-packed layout;
+  // ODMOE_SHADOW_MMA=0 keeps the CUDA-core flat engine (A/B)
+  const char* mme = getenv("ODMOE_SHADOW_MMA");
+  const bool mma = !nf4 && !fp8 && !(mme && mme[0] == '0') && mma_shadow_ok(d, F);
+  c->sh_ewt = nf4 ? W_NF4 : (fp8 ? W_F8 : (mma ? W_I8P : (u8 ? W_U8 : W_I8)));
   c->sh_emb = dmalloc<int8_t>(c, (size_t)V * d, "shadow emb");
   c->sh_semb = dmalloc<float>(c, V, "shadow emb scales");
   c->sh_router = dmalloc<int8_t>(c, (size_t)L * E * d, "shadow router");
@@ -508,6 +512,14 @@ void build_shadow(Ctx* c, char* staging) {
         CUDA_OK(c, launch_quantize_fp8(src, 2LL * F, d, c->wt, (uint8_t*)q, s, c->s_main));
         CUDA_OK(c, launch_quantize_fp8(src + (size_t)2 * F * d * c->esz, d, F, c->wt, (uint8_t*)q + (size_t)2 * F * d,
                                        s + 2 * F, c->s_main));
+      } else if (mma) {  // biased codes row-major into scratch, then the fragment-packed layout
+        int8_t* qs = reinterpret_cast<int8_t*>(staging + c->full_bytes);
+        CUDA_OK(c, launch_quantize(src, 2LL * F, d, c->wt, qs, s, c->s_main, true));
+        CUDA_OK(c, launch_quantize(src + (size_t)2 * F * d * c->esz, d, F, c->wt, qs + (size_t)2 * F * d, s + 2 * F,
+                                   c->s_main, true));
+        CUDA_OK(c, launch_pack_i8_frag((const uint8_t*)qs, (uint8_t*)q, 2 * F, d, 1, c->s_main));
+        CUDA_OK(c, launch_pack_i8_frag((const uint8_t*)qs + (size_t)2 * F * d, (uint8_t*)q + (size_t)2 * F * d, d, F, 0,
+                                       c->s_main));
       } else {
         CUDA_OK(c, launch_quantize(src, 2LL * F, d, c->wt, q, s, c->s_main, u8));
         CUDA_OK(c, launch_quantize(src + (size_t)2 * F * d * c->esz, d, F, c->wt, q + (size_t)2 * F * d, s + 2 * F,
@@ -1452,6 +1464,7 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
       CUDA_OK(c, launch_p2p_gather(c->p2p_part, c->p2p_flag, p2p_mask(c, l - 1), d, c->p2p_seq - 1, c->d_yred,
                                    c->d_flag, s));
       c->stats.kernel_launches++;
+      if (c->dbg_yred) CUDA_OK(c, cudaMemcpyAsync(c->dbg_yred + (size_t)(l - 1) * d, c->d_yred, sizeof(float) * d, cudaMemcpyDeviceToDevice, s));
     }
     if (r0 && c->H > 0) {
       // attention block of layer l (Q29): h += y_{l-1}; h += W_o attn(RMSNorm(h)); router sees that h
@@ -1657,6 +1670,7 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
       CUDA_OK(c, launch_p2p_gather(c->p2p_part, c->p2p_flag, p2p_mask(c, L - 1), d, c->p2p_seq - 1, c->d_yred,
                                    c->d_flag, s));
       c->stats.kernel_launches++;
+      if (c->dbg_yred) CUDA_OK(c, cudaMemcpyAsync(c->dbg_yred + (size_t)(L - 1) * d, c->d_yred, sizeof(float) * d, cudaMemcpyDeviceToDevice, s));
     }
     CUDA_OK(c, launch_combine(c->d_h, yadd, n_add, d, s));
     c->stats.kernel_launches++;
@@ -2257,7 +2271,9 @@ odmoe_status odmoe_create(const odmoe_config* cfg, void** ctx_out) {
         c->emu_NG = c->emu / c->emu_G;
       }
     }
-    c->G = c->sliced ? c->world : (cfg->group_size > 0 ? cfg->group_size : std::min(c->k, c->world));
+    // (an emulated multi-GPU run keeps this process's own placement: one GPU holds everything)
+    c->G = c->sliced ? c->world
+                     : (cfg->emulate_world > 1 ? 1 : (cfg->group_size > 0 ? cfg->group_size : std::min(c->k, c->world)));
     c->NG = c->world / c->G;
     c->my_group = c->rank / c->G;
     c->my_pos = c->rank % c->G;

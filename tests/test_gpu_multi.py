@@ -111,9 +111,9 @@ def test_multi_gpu_bitwise_invariance(world):
 def test_multi_gpu_sliced_placement(world):
     """Sliced loading: every GPU holds/loads/computes 1/N of every expert and the
     N partial outputs are reduced on GPU 0. Values change only by the split of the F-sum (within
-    fp32 rounding), so greedy tokens and routing match the 1-GPU run on TINY; two runs are
-    bitwise identical (fixed reduction order); prefill (tensor-core grouped GEMM on F/N slices)
-    gives the same token and expert counts."""
+    fp32 rounding), so greedy tokens and routing match the 1-GPU run on TINY (bitwise repeatability
+    and equality with the one-GPU emulation: test_multi_gpu_matches_one_gpu_emulation); prefill
+    (tensor-core grouped GEMM on F/N slices) gives the same token and expert counts."""
     t = torch()
     if t.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
@@ -129,6 +129,7 @@ def test_multi_gpu_sliced_placement(world):
             assert r[5] <= 4
         assert res[0][3] == base_routes
         runs.append(res[0][2])
+    assert all(r == runs[0] for r in runs)   # predictors change time, never values
     res = _multi(world, odmoe.PRED_NONE, slots=-1, placement=odmoe.PLACE_SLICED)   # resident, sliced
     for r in res:
         assert r[2] == base_toks
@@ -151,3 +152,89 @@ def test_multi_gpu_attention(world):
         for r in res:
             assert r[2] == base_toks, (world, placement, r[0])
             assert r[4] == base_pf, (world, placement, r[0])
+
+
+def _run_rank_capture(rank, world, port, q, placement, p2p):
+    """One rank of a real N-GPU decode with the debug capture on rank 0: per step the token, the
+    final hidden state and every layer's combined expert output (bytes)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ["ODMOE_P2P"] = "1" if p2p else "0"
+    import torch as t
+    import torch.distributed as dist
+    t.cuda.set_device(rank)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2512_03927_b200 import odmoe
+    obj = [odmoe.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    try:
+        eng = odmoe.Engine(TINY.L, TINY.E, TINY.k, TINY.d, TINY.F, TINY.V, dtype=odmoe.BF16,
+                           predictor=odmoe.PRED_NONE, slots_per_gpu=4, lookahead=1, weight_seed=SEED, rank=rank,
+                           world_size=world, device=rank, nccl_id=obj[0], placement=placement, debug_capture=1)
+        out, t_ = [], 9
+        for _ in range(6):
+            t_, _ = eng.decode_step(t_)
+            if rank == 0:
+                out.append((t_, eng.debug_read("H_FINAL", 0, 4 * TINY.d),
+                            [eng.debug_read("Y", l, 4 * TINY.d) for l in range(TINY.L)]))
+        eng.close()
+        q.put((rank, "ok", out))
+    except Exception as e:
+        q.put((rank, "err", repr(e)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _capture_multi(world, placement, p2p):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29900 + world * 7 + placement * 3 + int(p2p) + os.getpid() % 50
+    ps = [ctx.Process(target=_run_rank_capture, args=(r, world, port, q, placement, p2p)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = sorted([q.get(timeout=600) for _ in ps], key=lambda x: x[0])
+    for p in ps:
+        p.join(timeout=120)
+    for r in res:
+        assert r[1] == "ok", r
+    return res[0][2]
+
+
+def _capture_emulated(world, placement):
+    from paper_2512_03927_b200 import odmoe
+    eng = odmoe.Engine(TINY.L, TINY.E, TINY.k, TINY.d, TINY.F, TINY.V, dtype=odmoe.BF16, predictor=odmoe.PRED_NONE,
+                       slots_per_gpu=4, lookahead=1, weight_seed=SEED, placement=placement, debug_capture=1,
+                       emulate_world=world)
+    out, t_ = [], 9
+    for _ in range(6):
+        t_, _ = eng.decode_step(t_)
+        out.append((t_, eng.debug_read("H_FINAL", 0, 4 * TINY.d),
+                    [eng.debug_read("Y", l, 4 * TINY.d) for l in range(TINY.L)]))
+    eng.close()
+    return out
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_multi_gpu_matches_one_gpu_emulation(world):
+    """The real N-GPU data path (sliced slices + P2P rank-order combine; the paper's groups) gives
+    bit for bit the states of its one-GPU emulation (emulate_world), whose arithmetic
+    tests/test_gpu_emulate.py checks element by element against the oracle on the driver's 1-GPU
+    box. Two real runs are bitwise identical; the NCCL-reduce fallback (ODMOE_P2P=0) agrees
+    within fp32 rounding (its reduction order is NCCL's)."""
+    t = torch()
+    if t.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    import numpy as np
+    from paper_2512_03927_b200 import odmoe
+    for placement in (odmoe.PLACE_SLICED, odmoe.PLACE_GROUPS):
+        emu = _capture_emulated(world, placement)
+        real = _capture_multi(world, placement, p2p=True)
+        assert real == emu, (world, placement)
+        assert _capture_multi(world, placement, p2p=True) == real
+        nccl = _capture_multi(world, placement, p2p=False)
+        for (ta, ha, ya), (tb, hb, yb) in zip(nccl, real):
+            assert ta == tb
+            a = np.frombuffer(ha, dtype=np.float32)
+            b = np.frombuffer(hb, dtype=np.float32)
+            assert np.max(np.abs(a - b)) <= 1e-5 * np.max(np.abs(b))
