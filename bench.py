@@ -424,6 +424,27 @@ def main():
         time.sleep(0.05)
         trace_ev = eng.trace()
         eng.set_trace(False)
+    # the shadow's whole token-aligned pass alone (SEP Mode A, a4): one event pair per pass on the
+    # shadow stream, 8 passes for distinct tokens (N = 1: at N > 1 a pass broadcasts its predictions)
+    sh_pass = None
+    if n == 1 and args.predictor.startswith("shadow") and args.attention is False:
+        eng.set_time_kernels(0)
+        eng.set_pass_timing(True)
+        eng.predict_ahead(7)
+        eng.reset_stats()
+        for t in range(8):
+            eng.predict_ahead(1000 + t)
+        pst = eng.stats()
+        eng.set_pass_timing(False)
+        if pst["n_sh_pass"]:
+            k_, d_, F_ = SHAPE["k"], SHAPE["d"], SHAPE["F"]
+            sh_bytes = SHAPE["L"] * k_ * (3 * F_ * d_ + (2 * F_ + d_) * 4)
+            us = pst["ms_sh_pass"] / pst["n_sh_pass"] * 1e3
+            sh_pass = {"bound": "hbm", "kernel": "whole INT8 shadow pass (32 x [router, k expert W13+SwiGLU, W2+gate])",
+                       "algorithmic_bytes": sh_bytes, "us": us, "GBps": sh_bytes / us / 1e3,
+                       "peak": peaks["hbm_gbs"], "frac": sh_bytes / us / 1e3 / peaks["hbm_gbs"], "passes": pst["n_sh_pass"],
+                       "note": "odmoe_predict_ahead for 8 distinct tokens, alone on the GPU; CUDA events around each "
+                               "pass on the shadow stream; bytes = the k experts' int8 codes + row scales of 32 layers"}
     if dist is not None:
         tt = torch.tensor([dev_s, wall], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -520,7 +541,11 @@ def main():
             line["eq1"] = eq1_from_trace(trace_ev, ng, SHAPE["L"])
         sh_rf = shadow_roofline(st, args.steps, peaks["hbm_gbs"])
         if sh_rf is not None:
+            sh_rf["note"] = ("per-phase CUDA events inside the decode step (the shadow stream shares the GPU with "
+                             "the main model's kernels and copies; each event pair also cuts the PDL chain)")
             line["roofline_shadow"] = sh_rf
+        if sh_pass is not None:
+            line["roofline_shadow_pass"] = sh_pass
         if r0 is not None:
             line["sep_refine0"] = r0
         if prefill is not None:

@@ -176,6 +176,10 @@ typedef struct {
      ms_shadow): W13 + SwiGLU, W2 + gate; n_* count experts */
   double ms_sh_w13, ms_sh_w2;
   int64_t n_sh_w13, n_sh_w2;
+  /* option 9: device time of whole shadow passes (embed .. last expert; one event pair per pass, so
+     the kernels inside keep their PDL chains) and their count */
+  double ms_sh_pass;
+  int64_t n_sh_pass;
 } odmoe_stats;
 
 /* ------------------------------------------------------------------ lifecycle */
@@ -240,6 +244,21 @@ odmoe_status odmoe_shadow_expert_ffn(const int8_t* q13, const float* s13, const 
                                      const float* s2, const void* u, const float* gate_w,
                                      int gate_idx, int d, int F, float* a_scratch, float* y,
                                      void* stream);
+
+/* The same INT8 shadow expert on the tensor cores (reading Q32; the engine's default shadow path):
+ * q13p / q2p are the codes in the fragment-packed layout written by odmoe_pack_int8_frag (W13 with
+ * pair_rows = 1, W2 with pair_rows = 0), s13 / s2 natural-order row scales as above. d, F multiples
+ * of 32. Same math as odmoe_shadow_expert_ffn (fp32 accumulation in the tensor cores' order);
+ * a_scratch (4F bytes) receives the SwiGLU activation in the tensor cores' B-fragment form (f16 hi +
+ * lo per element), not as fp32. */
+odmoe_status odmoe_shadow_expert_ffn_packed(const uint8_t* q13p, const float* s13, const uint8_t* q2p,
+                                            const float* s2, const void* u, const float* gate_w, int gate_idx,
+                                            int d, int F, float* a_scratch, float* y, void* stream);
+/* int8 codes q [R][C] (row-major, signed) -> the fragment-packed layout of mma.sync m16n8k16
+ * (16-row tiles x 32-column blocks of 512 B; each lane's 16 B = its A fragments of two k-blocks, the
+ * codes stored biased q + 128). pair_rows = 1: tile row g / g+8 = rows 2(8t+g) / 2(8t+g)+1 (W13's
+ * gate/up pairs). R % 16 == 0, C % 32 == 0 else E_CONFIG. out: R*C bytes (device). */
+odmoe_status odmoe_pack_int8_frag(const int8_t* q, int64_t R, int64_t C, int pair_rows, uint8_t* out, void* stream);
 
 /* NF4 shadow expert FFN (reading Q27): like odmoe_shadow_expert_ffn with W = c[code] * absmax.
  * q13: codes of W13 [2F][d/2] bytes (two codes per byte, low nibble = even column), a13: fp32
@@ -383,8 +402,8 @@ odmoe_status odmoe_trace_read(void* ctx, odmoe_trace_event* out, int32_t cap, in
  *   or the last key-8 / key-4 call) the shadow decodes with its OWN greedy token from its INT8 LM
  *   head, so its pass for token n+1 starts right after its pass for n, before the main model has
  *   finished n, and loads for layers 0.. of n+1 may be issued inside the lookahead window (cross-
- *   token speculation); shadow predictors only, T_p in 1..64). E_CONFIG on a bad
- *   key/value. */
+ *   token speculation); shadow predictors only, T_p in 1..64); key 9 = shadow-pass
+ *   timing (0/1: odmoe_stats.ms_sh_pass / n_sh_pass). E_CONFIG on a bad key/value. */
 odmoe_status odmoe_set_option(void* ctx, int key, int64_t value);
 
 /* SEP Mode A (Q10): run the shadow from the main model's token `token`

@@ -186,7 +186,12 @@ bool mma_shadow_ok(int d, int F);
 cudaError_t launch_mma_shadow(int n, const ExpertRef* ex, int mode, const void* x, const float* gate_w,
                               float* out, int d, int F, cudaStream_t s, bool pdl);
 // biased codes [R][C] (row-major) -> W_I8P layout; pair_rows: W13's gate/up pairing
-cudaError_t launch_pack_i8_frag(const uint8_t* q_biased, uint8_t* out, int R, int C, int pair_rows, cudaStream_t s);
+cudaError_t launch_pack_i8_frag(const uint8_t* q_biased, uint8_t* out, int R, int C, int pair_rows, cudaStream_t s,
+                                bool signed_codes = false);  // signed_codes: input q (not q + 128)
+
+// One warp spins until *flag reaches epoch (the copy stream writes it after a load): keeps the GPU out of
+// its idle state while the compute stream waits for an expert (p2p.cu). Timeout ~30 s -> *err_flag = 3.
+cudaError_t launch_wait_flag(const uint32_t* flag, uint32_t epoch, int32_t* err_flag, cudaStream_t s);
 
 // BF16 (round to nearest even) copy of an fp32 tensor: the BF16 shadow of an FP32 main model.
 cudaError_t launch_f32_to_bf16(const float* in, void* out, int64_t n, cudaStream_t s);

@@ -34,9 +34,15 @@
 
 namespace odmoe {
 
-constexpr int kMG_WARPS = 24;
+#ifndef MG_WARPS
+#define MG_WARPS 16
+#endif
+#ifndef MG_UNROLL
+#define MG_UNROLL 8
+#endif
+constexpr int kMG_WARPS = MG_WARPS;     // 16 warps x 2 batches x 8 units x 512 B = 128 KB in flight per SM
 constexpr int kMG_THREADS = kMG_WARPS * 32;
-constexpr int kMG_UNROLL = 4;
+constexpr int kMG_UNROLL = MG_UNROLL;
 constexpr int kMG_MAXSPLIT = 4;   // CTAs sharing one tile (grid sizing keeps it <= 3)
 constexpr int kMG_MAXE = 4;       // experts per launch
 
@@ -49,12 +55,13 @@ struct MgArgs {
   const int32_t* ids;
   int base, k, sel[kMG_MAXE];
   long long off, soff;      // byte offset of this matrix in a blob / float offset of its scales
-  float* out[kMG_MAXE];     // mode 0: a [R/2]; mode 1: y [R]
-  const void* x;            // mode 0: bf16 u [C] (shared); mode 1: fp32 a, expert e at x + e * C
+  float* out[kMG_MAXE];     // mode 0: a [R/2] in B-fragment form (4 B per element); mode 1: y [R] fp32
+  const void* x;            // mode 0: bf16 u [C] (shared); mode 1: the phase-1 activations in B-fragment
+                            // form (store_frag), expert e at x + e * C * 4 bytes
   const float* gate_w;      // mode 1: y = gate_w[pick] * (W2 a) (NULL = 1)
   int n, R, C;
-  float* gpart;             // [n][tiles][kMG_MAXSPLIT][16]
-  unsigned int* ticket;     // [n][tiles]
+  float* gpart;             // [n * tiles][kMG_MAXSPLIT][16] (global tile = expert * tiles + tile)
+  unsigned int* ticket;     // [n * tiles]
   int tiles_cap;            // tiles per CTA (smem partials)
 };
 
@@ -90,159 +97,216 @@ __device__ __forceinline__ int cta_of(long long u, long long U, int grid) {
   return p;
 }
 
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+// The activation handed from phase 1 to phase 2 in the B-fragment format (4 B per element, the size of
+// the fp32 vector it replaces): element c of k-block kb is f16 hi at uint2 [kb*8 + tq], lo at
+// [kb*8 + 4 + tq], word (c >= 8), half (c & 1), tq = (c & 7) >> 1.
+__device__ __forceinline__ void store_frag(uint32_t* frag, int p, float v) {
+  const int kb = p >> 4, c = p & 15, tq = (c & 7) >> 1;
+  const int w = (c >> 3) & 1, hf = c & 1;
+  const __half hi = __float2half_rn(v);
+  const __half lo = __float2half_rn(v - __half2float(hi));
+  __half* h = reinterpret_cast<__half*>(frag);
+  h[((kb * 8 + tq) * 2 + w) * 2 + hf] = hi;
+  h[((kb * 8 + 4 + tq) * 2 + w) * 2 + hf] = lo;
+}
+
 template <int MODE, int NE>
 __global__ void __launch_bounds__(kMG_THREADS, 1) mma_gemv_kernel(const __grid_constant__ MgArgs a) {
+  // The NE experts' units form ONE stream (expert-major): a CTA's range and a warp's slice may cross
+  // from one expert into the next, so pipeline fill, staging and tail are paid once per launch.
   extern __shared__ __align__(128) uint8_t sm[];
-  uint2* xs = reinterpret_cast<uint2*>(sm);                      // [C/16 k-blocks][8]: hi tq0..3, lo tq0..3
-  float* part = reinterpret_cast<float*>(sm + (size_t)a.C / 16 * 64);  // [warps][tiles_cap][16]
+  const int nkb = a.C / 16;
+  constexpr int NX = MODE == 0 ? 1 : NE;                             // activation vectors staged
+  uint2* xs = reinterpret_cast<uint2*>(sm);                          // [NX][C/16][8]: hi tq0..3, lo tq0..3
+  float* part = reinterpret_cast<float*>(sm + (size_t)NX * nkb * 64);  // [warps][tiles_cap][16]
+  __shared__ const uint4* sW[NE];   // expert e's packed matrix, pre-offset by -e*U units
+  __shared__ const float* sS[NE];
+  __shared__ float sG[NE];
+  __shared__ __align__(8) uint64_t xbar;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   const int g = lane >> 2, tq = lane & 3;
   const int tiles = a.R / 16, CB = a.C / 32;
-  const long long U = (long long)tiles * CB;
-  long long u0, u1;
-  split_range(U, gridDim.x, blockIdx.x, u0, u1);
-  const int t_first = (int)(u0 / CB);
-  const int t_last = u1 > u0 ? (int)((u1 - 1) / CB) : t_first - 1;
-  const long long wb = u0 + (u1 - u0) * warp / kMG_WARPS, we = u0 + (u1 - u0) * (warp + 1) / kMG_WARPS;
+  const int U = tiles * CB, UT = U * NE;
+  const int u0 = (int)((long long)UT * blockIdx.x / gridDim.x), u1 = (int)((long long)UT * (blockIdx.x + 1) / gridDim.x);
+  const int t_first = u0 / CB;                                       // global tile = e * tiles + t
+  const int t_last = u1 > u0 ? (u1 - 1) / CB : t_first - 1;
+  const int wb = u0 + (int)((long long)(u1 - u0) * warp / kMG_WARPS);
+  const int we = u0 + (int)((long long)(u1 - u0) * (warp + 1) / kMG_WARPS);
   const uint64_t pol = l2_policy(true);
   const bool indirect = a.tbl != nullptr;
-  if (indirect) asm volatile("griddepcontrol.wait;" ::: "memory");
-
-#pragma unroll
-  for (int e = 0; e < NE; ++e) {  // unrolled: every a.w[e] / a.out[e] is a compile-time parameter offset
-    int pick = a.sel[e];
+  if (indirect) asm volatile("griddepcontrol.wait;" ::: "memory");  // the expert ids come from the router
+  if (tid < NE) {
+    const int e = tid;
+    const int pick = a.sel[e];
     const uint8_t* W;
-    const float* S;
     if (indirect) {
       const int id = a.base + a.ids[pick];
       W = reinterpret_cast<const uint8_t*>(a.tbl[id]) + a.off;
-      S = a.stbl[id] + a.soff;
+      sS[e] = a.stbl[id] + a.soff;
     } else {
       W = a.w[e];
-      S = a.sc[e];
+      sS[e] = a.sc[e];
     }
-    const uint4* base = reinterpret_cast<const uint4*>(W);
-    uint4 wa[kMG_UNROLL], wc[kMG_UNROLL];
+    sW[e] = reinterpret_cast<const uint4*>(W) - (size_t)e * U * 32;
+    sG[e] = MODE == 1 ? (a.gate_w ? a.gate_w[pick] : 1.f) : 1.f;
+  }
+  if (MODE == 1 && tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&xbar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // unit v of the stream -> its 16 B for this lane
+  const uint4* adj[NE];
+#pragma unroll
+  for (int e = 0; e < NE; ++e) adj[e] = sW[e] + lane;
+  auto ld_unit = [&](int v) -> uint4 {
+    const uint4* b = adj[0];
+#pragma unroll
+    for (int e = 1; e < NE; ++e) b = v >= e * U ? adj[e] : b;
+    return ld_stream_pol(b + (size_t)v * 32, pol);
+  };
+  uint4 wa[kMG_UNROLL], wc[kMG_UNROLL];
+#pragma unroll
+  for (int i = 0; i < kMG_UNROLL; ++i)
+    if (wb + i < we) wa[i] = ld_unit(wb + i);
+  if (!indirect) asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+
+  if (MODE == 0) {  // u (bf16) -> f16 hi/lo B fragments
+    for (int i = tid; i < nkb * 4; i += kMG_THREADS) {
+      const int kb = i >> 2, q = i & 3;
+      const uint16_t* u = reinterpret_cast<const uint16_t*>(a.x) + kb * 16 + 2 * q;
+      float v[4] = {__uint_as_float((uint32_t)u[0] << 16), __uint_as_float((uint32_t)u[1] << 16),
+                    __uint_as_float((uint32_t)u[8] << 16), __uint_as_float((uint32_t)u[9] << 16)};
+      float hi[4], lo[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        hi[j] = __half2float(__float2half_rn(v[j]));
+        lo[j] = v[j] - hi[j];
+      }
+      xs[kb * 8 + q] = make_uint2(h2_bits(hi[0], hi[1]), h2_bits(hi[2], hi[3]));
+      xs[kb * 8 + 4 + q] = make_uint2(h2_bits(lo[0], lo[1]), h2_bits(lo[2], lo[3]));
+    }
+  } else if (tid == 0) {  // phase 1 left the activations in fragment form: one bulk copy per 32 KB
+    const uint32_t bytes = (uint32_t)NX * nkb * 64;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&xbar)), "r"(bytes) : "memory");
+    for (uint32_t off = 0; off < bytes; off += 32768) {
+      const uint32_t nb = bytes - off < 32768 ? bytes - off : 32768;
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_addr(sm + off)),
+                   "l"(reinterpret_cast<const char*>(a.x) + off), "r"(nb), "r"(smem_addr(&xbar))
+                   : "memory");
+    }
+  }
+  const int ntl = t_last - t_first + 1;
+  for (int i = tid; i < kMG_WARPS * a.tiles_cap * 16; i += kMG_THREADS) part[i] = 0.f;
+  __syncthreads();
+  if (MODE == 1)
+    asm volatile("{\n .reg .pred p;\n XW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra XW_%=;\n}\n" ::"r"(
+                     smem_addr(&xbar))
+                 : "memory");
+
+  float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
+  // running (global tile, column block) of the next unit; xk = this lane's B fragments of k-block 2cb
+  int tcur = wb / CB, cb = wb - tcur * CB;
+  const uint2* xlane = xs + (g >= 4 ? 4 : 0) + tq;
+  const uint2* xk = xlane + (size_t)(MODE == 0 ? 0 : tcur / tiles) * nkb * 8 + (size_t)cb * 16;
+  float* pw = part + (size_t)warp * a.tiles_cap * 16 + (tq == 0 ? g : 0);
+  auto flush = [&]() {
+    // columns 0-3 hold A.hi, 4-7 A.lo: lane (g, 0) adds lane (g, 2)'s value
+    const float h0 = c0 + __shfl_down_sync(0xffffffffu, c0, 2);
+    const float h2 = c2 + __shfl_down_sync(0xffffffffu, c2, 2);
+    if (tq == 0) {
+      float* p = pw + (tcur - t_first) * 16;
+      p[0] = h0;
+      p[8] = h2;
+    }
+    c0 = c1 = c2 = c3 = 0.f;
+  };
+  auto unit = [&](const uint4& w) {
+    const uint2 b0 = xk[0];
+    const uint2 b1 = xk[8];
+    hmma16816(c0, c1, c2, c3, u8x2_to_h2(w.x, 0x4140u), u8x2_to_h2(w.x, 0x4342u), u8x2_to_h2(w.y, 0x4140u),
+              u8x2_to_h2(w.y, 0x4342u), b0.x, b0.y);
+    hmma16816(c0, c1, c2, c3, u8x2_to_h2(w.z, 0x4140u), u8x2_to_h2(w.z, 0x4342u), u8x2_to_h2(w.w, 0x4140u),
+              u8x2_to_h2(w.w, 0x4342u), b1.x, b1.y);
+    xk += 16;
+    if (++cb == CB) {  // tile complete (warp-uniform)
+      flush();
+      ++tcur;
+      cb = 0;
+      xk = xlane + (size_t)(MODE == 0 ? 0 : tcur / tiles) * nkb * 8;
+    }
+  };
+  for (int ub = wb; ub < we; ub += 2 * kMG_UNROLL) {
 #pragma unroll
     for (int i = 0; i < kMG_UNROLL; ++i)
-      if (wb + i < we) wa[i] = ld_stream_pol(base + (wb + i) * 32 + lane, pol);
-    if (!indirect && e == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (e == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-
-    // stage the activations as f16 hi/lo B fragments (mode 0 once; mode 1 per expert)
-    if (e == 0 || MODE == 1) {
-      if (e > 0) __syncthreads();
-      const int nkb = a.C / 16;
-      for (int i = tid; i < nkb * 4; i += kMG_THREADS) {
-        const int kb = i >> 2, q = i & 3;
-        float v[4];
-        const int cols[4] = {kb * 16 + 2 * q, kb * 16 + 2 * q + 1, kb * 16 + 2 * q + 8, kb * 16 + 2 * q + 9};
+      if (ub + kMG_UNROLL + i < we) wc[i] = ld_unit(ub + kMG_UNROLL + i);
+    if (ub + kMG_UNROLL <= we) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          if (MODE == 0) v[j] = __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(a.x)[cols[j]] << 16);
-          else v[j] = reinterpret_cast<const float*>(a.x)[(size_t)e * a.C + cols[j]];
-        }
-        float hi[4], lo[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          hi[j] = __half2float(__float2half_rn(v[j]));
-          lo[j] = v[j] - hi[j];
-        }
-        xs[kb * 8 + q] = make_uint2(h2_bits(hi[0], hi[1]), h2_bits(hi[2], hi[3]));
-        xs[kb * 8 + 4 + q] = make_uint2(h2_bits(lo[0], lo[1]), h2_bits(lo[2], lo[3]));
-      }
-    }
-    const int ntl = t_last - t_first + 1;
-    for (int i = tid; i < kMG_WARPS * a.tiles_cap * 16; i += kMG_THREADS) part[i] = 0.f;
-    __syncthreads();
-
-    float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
-    // running (tile, column block) of the next unit: the slice is consumed in order
-    int tcur = (int)(wb / CB), cb = (int)(wb - (long long)tcur * CB);
-    const uint2* xl = xs + (g >= 4 ? 4 : 0) + tq;
-    auto flush = [&](int t) {
-      // columns 0-3 hold A.hi, 4-7 A.lo: lane (g, 0) adds lane (g, 2)'s value
-      const float h0 = c0 + __shfl_down_sync(0xffffffffu, c0, 2);
-      const float h2 = c2 + __shfl_down_sync(0xffffffffu, c2, 2);
-      if (tq == 0) {
-        float* p = part + ((size_t)warp * a.tiles_cap + (t - t_first)) * 16;
-        p[g] = h0;
-        p[g + 8] = h2;
-      }
-      c0 = c1 = c2 = c3 = 0.f;
-    };
-    auto consume = [&](const uint4 (&wv)[kMG_UNROLL], long long ub) {
-#pragma unroll
-      for (int i = 0; i < kMG_UNROLL; ++i) {
-        if (ub + i < we) {
-          const uint2 b0 = xl[(2 * cb) * 8];
-          const uint2 b1 = xl[(2 * cb + 1) * 8];
-          hmma16816(c0, c1, c2, c3, u8x2_to_h2(wv[i].x, 0x4140u), u8x2_to_h2(wv[i].x, 0x4342u),
-                    u8x2_to_h2(wv[i].y, 0x4140u), u8x2_to_h2(wv[i].y, 0x4342u), b0.x, b0.y);
-          hmma16816(c0, c1, c2, c3, u8x2_to_h2(wv[i].z, 0x4140u), u8x2_to_h2(wv[i].z, 0x4342u),
-                    u8x2_to_h2(wv[i].w, 0x4140u), u8x2_to_h2(wv[i].w, 0x4342u), b1.x, b1.y);
-          if (++cb == CB) {  // tile complete (warp-uniform)
-            flush(tcur);
-            ++tcur;
-            cb = 0;
-          }
-        }
-      }
-    };
-    for (long long ub = wb; ub < we; ub += 2 * kMG_UNROLL) {
+      for (int i = 0; i < kMG_UNROLL; ++i) unit(wa[i]);
+    } else {
 #pragma unroll
       for (int i = 0; i < kMG_UNROLL; ++i)
-        if (ub + kMG_UNROLL + i < we) wc[i] = ld_stream_pol(base + (ub + kMG_UNROLL + i) * 32 + lane, pol);
-      consume(wa, ub);
+        if (ub + i < we) unit(wa[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < kMG_UNROLL; ++i)
+      if (ub + 2 * kMG_UNROLL + i < we) wa[i] = ld_unit(ub + 2 * kMG_UNROLL + i);
+    if (ub + 2 * kMG_UNROLL <= we) {
+#pragma unroll
+      for (int i = 0; i < kMG_UNROLL; ++i) unit(wc[i]);
+    } else {
 #pragma unroll
       for (int i = 0; i < kMG_UNROLL; ++i)
-        if (ub + 2 * kMG_UNROLL + i < we) wa[i] = ld_stream_pol(base + (ub + 2 * kMG_UNROLL + i) * 32 + lane, pol);
-      if (ub + kMG_UNROLL < we) consume(wc, ub + kMG_UNROLL);
+        if (ub + kMG_UNROLL + i < we) unit(wc[i]);
     }
-    if (cb != 0) flush(tcur);  // the slice ended inside a tile
-    __syncthreads();
+  }
+  if (cb != 0) flush();  // the slice ended inside a tile
+  __syncthreads();
 
-    // per tile of this CTA: warps summed in a fixed order; whole tiles finalise here, cut tiles go
-    // through the cross-CTA slots (the last arrival sums the slots in CTA order)
-    float* gp = a.gpart + (size_t)e * tiles * kMG_MAXSPLIT * 16;
-    unsigned int* tk = a.ticket + (size_t)e * tiles;
-    const float gw = MODE == 1 ? (a.gate_w ? a.gate_w[pick] : 1.f) : 1.f;
-    for (int tl = warp; tl < ntl; tl += kMG_WARPS) {
-      const int t = t_first + tl;
-      float v = 0.f;
+  // per global tile of this CTA: warps summed in a fixed order; whole tiles finalise here, cut tiles
+  // go through the cross-CTA slots (the last arrival sums the slots in CTA order)
+  for (int tl = warp; tl < ntl; tl += kMG_WARPS) {
+    const int tg = t_first + tl;
+    const int e = tg / tiles, t = tg - e * tiles;
+    float v = 0.f;
+    if (lane < 16)
+      for (int w = 0; w < kMG_WARPS; ++w) v += part[((size_t)w * a.tiles_cap + tl) * 16 + lane];
+    const int tb = tg * CB, te = tb + CB;
+    const bool whole = tb >= u0 && te <= u1;
+    if (!whole) {
+      const int c_first = cta_of(tb, UT, gridDim.x), c_last = cta_of(te - 1, UT, gridDim.x);
+      const int slot = blockIdx.x - c_first;
+      if (lane < 16) a.gpart[((size_t)tg * kMG_MAXSPLIT + slot) * 16 + lane] = v;
+      __threadfence();
+      __syncwarp();
+      unsigned int prev = 0;
+      if (lane == 0) prev = atomicAdd(a.ticket + tg, 1u);
+      prev = __shfl_sync(0xffffffffu, prev, 0);
+      if (prev != (unsigned)(c_last - c_first)) continue;  // not the last arrival
+      __threadfence();
+      v = 0.f;
       if (lane < 16)
-        for (int w = 0; w < kMG_WARPS; ++w) v += part[((size_t)w * a.tiles_cap + tl) * 16 + lane];
-      const long long tb = (long long)t * CB, te = tb + CB;
-      const bool whole = tb >= u0 && te <= u1;
-      if (!whole) {
-        const int c_first = cta_of(tb, U, gridDim.x), c_last = cta_of(te - 1, U, gridDim.x);
-        const int slot = blockIdx.x - c_first;
-        if (lane < 16) gp[((size_t)t * kMG_MAXSPLIT + slot) * 16 + lane] = v;
-        __threadfence();
-        __syncwarp();
-        unsigned int prev = 0;
-        if (lane == 0) prev = atomicAdd(tk + t, 1u);
-        prev = __shfl_sync(0xffffffffu, prev, 0);
-        if (prev != (unsigned)(c_last - c_first)) continue;  // not the last arrival
-        __threadfence();
-        v = 0.f;
-        if (lane < 16)
-          for (int s2 = 0; s2 <= c_last - c_first; ++s2) v += __ldcg(gp + ((size_t)t * kMG_MAXSPLIT + s2) * 16 + lane);
-        if (lane == 0) tk[t] = 0u;
-      }
-      if (MODE == 0) {
-        // lane g < 8: gate of pair 8t + g in v (row g), its up in row g + 8 (lane g + 8)
-        const float up = __shfl_down_sync(0xffffffffu, v, 8);
-        if (lane < 8) {
-          const int p = 8 * t + lane;
-          a.out[e][p] = silu_mul(v * S[2 * p], up * S[2 * p + 1]);
-        }
-      } else if (lane < 16) {
-        const int r = 16 * t + lane;
-        a.out[e][r] = gw * (v * S[r]);
-      }
+        for (int s2 = 0; s2 <= c_last - c_first; ++s2) v += __ldcg(a.gpart + ((size_t)tg * kMG_MAXSPLIT + s2) * 16 + lane);
+      if (lane == 0) a.ticket[tg] = 0u;
     }
-    if (e + 1 < NE) __syncthreads();
+    const float* S = sS[e];
+    float* out = e == 0 ? a.out[0] : (e == 1 ? a.out[NE > 1 ? 1 : 0] : (e == 2 ? a.out[NE > 2 ? 2 : 0] : a.out[NE > 3 ? 3 : 0]));
+    if (MODE == 0) {
+      // lane g < 8: gate of pair 8t + g in v (row g), its up in row g + 8 (lane g + 8); the result goes
+      // to phase 2 in B-fragment form
+      const float up = __shfl_down_sync(0xffffffffu, v, 8);
+      if (lane < 8) {
+        const int p = 8 * t + lane;
+        store_frag(reinterpret_cast<uint32_t*>(out), p, silu_mul(v * S[2 * p], up * S[2 * p + 1]));
+      }
+    } else if (lane < 16) {
+      const int r = 16 * t + lane;
+      out[r] = sG[e] * (v * S[r]);
+    }
   }
 }
 
@@ -250,7 +314,7 @@ __global__ void __launch_bounds__(kMG_THREADS, 1) mma_gemv_kernel(const __grid_c
 // q [R][C] biased codes (q + 128, row-major) -> the fragment-packed layout above. pair_rows: W13
 // (tile row g = row 2(8t + g), tile row g + 8 = row 2(8t + g) + 1); else tile row r = row 16t + r.
 __global__ void pack_i8_frag_kernel(const uint8_t* __restrict__ q, uint8_t* __restrict__ out, int R, int C,
-                                    int pair_rows) {
+                                    int pair_rows, uint32_t flip) {
   const long long n_units = (long long)(R / 16) * (C / 32);
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n_units * 32;
        i += (long long)gridDim.x * blockDim.x) {
@@ -278,17 +342,20 @@ __global__ void pack_i8_frag_kernel(const uint8_t* __restrict__ q, uint8_t* __re
     v.y = b[4] | (b[5] << 8) | (b[6] << 16) | ((uint32_t)b[7] << 24);
     v.z = b[8] | (b[9] << 8) | (b[10] << 16) | ((uint32_t)b[11] << 24);
     v.w = b[12] | (b[13] << 8) | (b[14] << 16) | ((uint32_t)b[15] << 24);
+    v.x ^= flip; v.y ^= flip; v.z ^= flip; v.w ^= flip;  // signed q -> q + 128
     reinterpret_cast<uint4*>(out)[i] = v;
   }
 }
 
 bool mma_shadow_ok(int d, int F) { return d % 32 == 0 && F % 32 == 0 && d >= 32 && F >= 32; }
 
-cudaError_t launch_pack_i8_frag(const uint8_t* q_biased, uint8_t* out, int R, int C, int pair_rows, cudaStream_t s) {
+cudaError_t launch_pack_i8_frag(const uint8_t* q_biased, uint8_t* out, int R, int C, int pair_rows, cudaStream_t s,
+                                bool signed_codes) {
   if (R % 16 || C % 32) return cudaErrorInvalidValue;
   const long long n = (long long)(R / 16) * (C / 32) * 32;
   const int grid = (int)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096);
-  pack_i8_frag_kernel<<<grid > 0 ? grid : 1, 256, 0, s>>>(q_biased, out, R, C, pair_rows);
+  pack_i8_frag_kernel<<<grid > 0 ? grid : 1, 256, 0, s>>>(q_biased, out, R, C, pair_rows,
+                                                          signed_codes ? 0x80808080u : 0u);
   return cudaGetLastError();
 }
 
@@ -313,11 +380,11 @@ static cudaError_t mg_scratch(cudaStream_t s, long long tiles, MgScratch*& out) 
       cudaFree(m.gpart);
       cudaFree(m.ticket);
     }
-    cudaError_t e = cudaMalloc(&m.gpart, (size_t)kMG_MAXE * tiles * kMG_MAXSPLIT * 16 * sizeof(float));
+    cudaError_t e = cudaMalloc(&m.gpart, (size_t)tiles * kMG_MAXSPLIT * 16 * sizeof(float));
     if (e != cudaSuccess) return e;
-    e = cudaMalloc(&m.ticket, (size_t)kMG_MAXE * tiles * sizeof(unsigned int));
+    e = cudaMalloc(&m.ticket, (size_t)tiles * sizeof(unsigned int));
     if (e != cudaSuccess) return e;
-    e = cudaMemset(m.ticket, 0, (size_t)kMG_MAXE * tiles * sizeof(unsigned int));
+    e = cudaMemset(m.ticket, 0, (size_t)tiles * sizeof(unsigned int));
     if (e != cudaSuccess) return e;
     m.tiles = tiles;
   }
@@ -353,19 +420,28 @@ cudaError_t launch_mma_shadow(int n, const ExpertRef* ex, int mode, const void* 
     a.out[i] = out + (size_t)i * (mode == 0 ? F : d);
   }
   const int tiles = a.R / 16, CB = a.C / 32;
-  const long long U = (long long)tiles * CB;
+  const long long UT = (long long)tiles * CB * n;   // the n experts' units, one stream
   const int sms = stream_grid_sms();
-  long long gmax = U / ((CB + 1) / 2);          // a CTA's range >= half a tile: <= 3 CTAs share one
+  long long gmax = UT / ((CB + 1) / 2);         // a CTA's range >= half a tile: <= 3 CTAs share one
   if (gmax < 1) gmax = 1;
   const int grid = (int)(gmax < sms ? gmax : sms);
-  a.tiles_cap = (int)((U + grid - 1) / grid / CB) + 2;
+  a.tiles_cap = (int)((UT + grid - 1) / grid / CB) + 2;
   MgScratch* sc = nullptr;
-  cudaError_t e = mg_scratch(s, tiles, sc);
+  cudaError_t e = mg_scratch(s, (long long)tiles * kMG_MAXE, sc);
   if (e != cudaSuccess) return e;
   a.gpart = sc->gpart;
   a.ticket = sc->ticket;
-  const size_t smem = (size_t)a.C / 16 * 64 + (size_t)kMG_WARPS * a.tiles_cap * 16 * sizeof(float);
-  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  const int nx = mode == 0 ? 1 : n;             // activation vectors staged (W2: one per expert)
+  const size_t smem = (size_t)nx * a.C / 16 * 64 + (size_t)kMG_WARPS * a.tiles_cap * 16 * sizeof(float);
+  if (smem > 227 * 1024) {  // W2 of many wide experts: one launch per expert
+    if (n == 1) return cudaErrorInvalidValue;
+    for (int i = 0; i < n; ++i) {
+      e = launch_mma_shadow(1, ex + i, mode, mode == 0 ? x : (const void*)((const uint32_t*)x + (size_t)i * F), gate_w,
+                            out + (size_t)i * (mode == 0 ? F : d), d, F, s, pdl);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
   void (*kern)(const MgArgs);
   if (mode == 0) kern = n == 1 ? mma_gemv_kernel<0, 1> : n == 2 ? mma_gemv_kernel<0, 2> : n == 3 ? mma_gemv_kernel<0, 3> : mma_gemv_kernel<0, 4>;
   else kern = n == 1 ? mma_gemv_kernel<1, 1> : n == 2 ? mma_gemv_kernel<1, 2> : n == 3 ? mma_gemv_kernel<1, 3> : mma_gemv_kernel<1, 4>;

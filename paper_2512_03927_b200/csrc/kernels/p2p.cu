@@ -82,6 +82,30 @@ __global__ void __launch_bounds__(256) p2p_gather_kernel(const float* part, cons
   }
 }
 
+// Warm wait for an expert load (the on-demand path's idle-to-busy ramp): instead of letting the
+// compute stream idle on the copy event for milliseconds -- after which the next expert kernel runs
+// ~20 % slower (profiles/kb_r02_ramp_*.json: 80.1 us after a 6 ms idle gap, 66.3 us when one CTA
+// spins through the gap) -- one warp spins on the slot's flag until the copy stream has written the
+// load's epoch. A wait over ~30 s sets err_flag = 3 and returns (reported as a CUDA-side error).
+__global__ void __launch_bounds__(32) wait_flag_kernel(const uint32_t* flag, uint32_t epoch, int32_t* err_flag) {
+  if (threadIdx.x != 0) return;
+  const uint64_t t0 = globaltimer();
+  uint32_t v;
+  for (;;) {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if ((int32_t)(v - epoch) >= 0) break;
+    if (globaltimer() - t0 > 30000000000ull) {
+      *err_flag = 3;
+      break;
+    }
+  }
+}
+
+cudaError_t launch_wait_flag(const uint32_t* flag, uint32_t epoch, int32_t* err_flag, cudaStream_t s) {
+  wait_flag_kernel<<<1, 32, 0, s>>>(flag, epoch, err_flag);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_p2p_send(const float* const* y, int n, int d, float* dst, uint32_t* flag, uint32_t epoch,
                             cudaStream_t s) {
   if (d % 4) return cudaErrorInvalidValue;

@@ -15,7 +15,7 @@
 
 namespace odmoe {
 
-enum Family { K_ROUTER = 0, K_W13, K_W2, K_SHADOW, K_LM, K_EMBED, K_ATTN, K_SH_W13, K_SH_W2, K_NFAM };
+enum Family { K_ROUTER = 0, K_W13, K_W2, K_SHADOW, K_LM, K_EMBED, K_ATTN, K_SH_W13, K_SH_W2, K_SH_PASS, K_NFAM };
 
 struct Slot {
   char* dev = nullptr;
@@ -24,6 +24,8 @@ struct Slot {
   int64_t token = -1;              // decode step the occupant belongs to
   cudaEvent_t ev_w13 = nullptr, ev_done = nullptr, ev_free = nullptr;
   bool free_recorded = false;
+  uint32_t* flag = nullptr;         // device [2]: epoch of the last load whose W13 / whole blob landed
+  uint32_t epoch = 0;               // epoch of the current occupant's load
   std::shared_ptr<LoadReq> req;
 };
 
@@ -250,6 +252,7 @@ struct Ctx {
     bool own_event = true;                 // return `e` to the pool on resolution
   };
   int trace = 0;
+  int pass_timing = 0;           // option 9: CUDA events around every whole shadow pass (stats.ms_sh_pass)
   cudaEvent_t tr_origin = nullptr;
   std::vector<TraceRec> tr_pending;
   std::vector<odmoe_trace_event> tr_done;

@@ -1,9 +1,33 @@
 #include "loader.h"
 
+#include <cuda.h>
+
 #include <algorithm>
 #include <chrono>
 
 namespace odmoe {
+
+// cuStreamWriteValue32 through the runtime's driver entry point (no link-time libcuda dependency)
+typedef CUresult (*PFN_writeValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static PFN_writeValue32 write_value32() {
+  static PFN_writeValue32 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_writeValue32>(p);
+  }
+  return fn;
+}
+bool stream_write_available() { return write_value32() != nullptr; }
+static cudaError_t write_flag(cudaStream_t s, uint32_t* p, uint32_t v) {
+  // default flags: the write is ordered after (and makes visible) the stream's earlier copies
+  return write_value32()(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(p), v, 0) == CUDA_SUCCESS
+             ? cudaSuccess : cudaErrorUnknown;
+}
 
 void Loader::start(int device, cudaStream_t copy, int64_t chunk_bytes, int max_inflight) {
   device_ = device;
@@ -112,8 +136,10 @@ void Loader::run() {
       bytes_h2d += n;
       if (e == cudaSuccess && r->tr_end) e = cudaEventRecord(r->tr_end, copy_);  // end of the last chunk issued
       if (e == cudaSuccess && r->issued == r->w13_bytes && r->ev_w13) e = cudaEventRecord(r->ev_w13, copy_);
+      if (e == cudaSuccess && r->issued == r->w13_bytes && r->flag) e = write_flag(copy_, r->flag, r->epoch);
       const bool last = r->issued == r->bytes;
       if (e == cudaSuccess && last) e = cudaEventRecord(r->ev_done, copy_);
+      if (e == cudaSuccess && last && r->flag) e = write_flag(copy_, r->flag + 1, r->epoch);
       cudaEvent_t ev = nullptr;
       if (e == cudaSuccess) {
         if (ev_pool_.empty()) {

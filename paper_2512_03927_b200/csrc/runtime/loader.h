@@ -26,6 +26,8 @@
 
 namespace odmoe {
 
+bool stream_write_available();  // cuStreamWriteValue32 reachable (the warm wait needs it)
+
 struct LoadReq {
   int layer = -1, expert = -1, slot = -1;
   int64_t key = 0;                 // need order; smaller is served first
@@ -34,6 +36,8 @@ struct LoadReq {
   int64_t bytes = 0, w13_bytes = 0;
   cudaEvent_t ev_w13 = nullptr, ev_done = nullptr;  // owned by the slot
   cudaEvent_t wait_ev = nullptr;   // optional: copy stream waits on it before the first chunk
+  uint32_t* flag = nullptr;        // optional device words [w13 landed, blob landed] the copy stream sets to
+  uint32_t epoch = 0;              // `epoch` (stream memory writes) for a compute-stream spin wait
   cudaEvent_t tr_start = nullptr, tr_end = nullptr;  // optional timing events (event trace): before the
                                    // first chunk / after every chunk (the last record = end of the copy)
   // loader-owned state (guarded by Loader::mu_)

@@ -150,6 +150,7 @@ void harvest_timers(Ctx* c) {
           c->stats.ms_shadow += ms; c->stats.n_shadow++; c->stats.ms_sh_w13 += ms; c->stats.n_sh_w13 += t.units; break;
         case K_SH_W2:
           c->stats.ms_shadow += ms; c->stats.n_shadow++; c->stats.ms_sh_w2 += ms; c->stats.n_sh_w2 += t.units; break;
+        case K_SH_PASS: c->stats.ms_sh_pass += ms; c->stats.n_sh_pass++; break;
       }
     }
     if (!t.graph) {  // graph-owned events stay with the graph
@@ -633,6 +634,27 @@ void build_pool(Ctx* c, char* staging) {
   c->stats.pool_build_s = now_s() - t0;
 }
 
+// ODMOE_WARM_WAIT=0: the compute stream waits on the copy events and idles (A/B of the ramp)
+bool warm_wait_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ODMOE_WARM_WAIT");
+    v = (e && e[0] == '0') ? 0 : (stream_write_available() ? 1 : 0);
+  }
+  return v == 1;
+}
+
+// The compute stream waits for part (0 = W13, 1 = whole blob) of the slot's current load: a spinning
+// warp (warm wait) when the slot has flags, else the copy event.
+void wait_load(Ctx* c, Slot& sl, int part, cudaStream_t s) {
+  if (sl.flag) {
+    CUDA_OK(c, launch_wait_flag(sl.flag + part, sl.epoch, c->d_flag, s));
+    c->stats.kernel_launches++;
+  } else {
+    CUDA_OK(c, cudaStreamWaitEvent(s, part == 0 ? sl.ev_w13 : sl.ev_done, 0));
+  }
+}
+
 void build_slots(Ctx* c) {
   if (c->resident) return;
   const int n = c->cfg.slots_per_gpu;
@@ -642,6 +664,10 @@ void build_slots(Ctx* c) {
     CUDA_OK(c, cudaEventCreateWithFlags(&s.ev_w13, cudaEventDisableTiming));
     CUDA_OK(c, cudaEventCreateWithFlags(&s.ev_done, cudaEventDisableTiming));
     CUDA_OK(c, cudaEventCreateWithFlags(&s.ev_free, cudaEventDisableTiming));
+    if (warm_wait_enabled()) {
+      s.flag = dmalloc<uint32_t>(c, 2, "slot flag");
+      CUDA_OK(c, cudaMemset(s.flag, 0, 2 * sizeof(uint32_t)));
+    }
     s.req = std::make_shared<LoadReq>();
   }
   c->stats.resident_bytes = (int64_t)n * c->blob_bytes;
@@ -818,6 +844,14 @@ void enqueue_shadow(Ctx* c, const int32_t* token_dev, int b, bool want_token) {
   cudaEvent_t* evp = c->ev_pred_all.data() + (size_t)b * L;
   float* dh = c->dbg_sh_h_all ? c->dbg_sh_h_all + (size_t)b * L * d : nullptr;
   char* du = c->dbg_sh_u_all ? c->dbg_sh_u_all + (size_t)b * L * d * 4 : nullptr;
+  cudaEvent_t pa = nullptr, pz = nullptr;
+  if (c->pass_timing) {
+    for (cudaEvent_t* ev : {&pa, &pz}) {
+      if (!c->tev_pool.empty()) { *ev = c->tev_pool.back(); c->tev_pool.pop_back(); }
+      else CUDA_OK(c, cudaEventCreate(ev));
+    }
+    CUDA_OK(c, cudaEventRecord(pa, s));
+  }
   {
     KTimer t(c, K_SHADOW, s);
     CUDA_OK(c, launch_embed(c->sh_emb, c->sh_semb, swt, token_dev, d, c->sh_h, s));
@@ -868,6 +902,10 @@ void enqueue_shadow(Ctx* c, const int32_t* token_dev, int b, bool want_token) {
     CUDA_OK(c, launch_lm_head(c->sh_h, c->sh_lm, swt, c->V, d, c->cfg.rms_eps, c->sh_tok + b,
                               c->sh_lmlogits ? c->sh_lmlogits + (size_t)b * c->V : nullptr, c->sh_lmscratch, s,
                               false, same ? nullptr : c->sh_slm));
+  }
+  if (pa) {
+    CUDA_OK(c, cudaEventRecord(pz, s));
+    c->timed.push_back(Ctx::Timed{K_SH_PASS, pa, pz, 1, false});
   }
 }
 
@@ -1065,6 +1103,10 @@ void submit_into(Ctx* c, Slot& s, int slot, int64_t tok, int l, int e, int64_t k
   r->ev_w13 = s.ev_w13;
   r->ev_done = s.ev_done;
   r->wait_ev = s.free_recorded ? s.ev_free : nullptr;
+  if (s.flag) {
+    r->flag = s.flag;
+    r->epoch = ++s.epoch;
+  }
   if (c->trace) {
     r->tr_start = tr_event(c);
     r->tr_end = tr_event(c);
@@ -1594,7 +1636,7 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
           ExpertRef e13 = direct_ref(sl.dev, nullptr, j);
           ExpertRef e2 = direct_ref(sl.dev + c->w13_bytes, nullptr, j);
           if (c->emu > 1) {  // the N-GPU run's launches on this GPU (split W13 / W2, reserve-1 grid)
-            CUDA_OK(c, cudaStreamWaitEvent(s, sl.ev_done, 0));
+            wait_load(c, sl, 1, s);
             tr_dev(c, ODMOE_EV_COMPUTE_START, s, l, S[j], si);
             const int nsl = c->emu_sliced ? c->emu : 1;
             for (int r = 0; r < nsl; ++r) {
@@ -1605,16 +1647,16 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
               { KTimer t(c, K_W2, s); CUDA_OK(c, launch_w2(direct_ref(b2, nullptr, j), c->wt, c->d_a + (size_t)ypos * F, w_dev, yo, d, c->Fs, s)); }
             }
           } else if (fused) {  // one launch once the whole blob has landed
-            CUDA_OK(c, cudaStreamWaitEvent(s, sl.ev_done, 0));
+            wait_load(c, sl, 1, s);
             tr_dev(c, ODMOE_EV_COMPUTE_START, s, l, S[j], si);
             KTimer t(c, K_W13, s);
             CUDA_OK(c, launch_expert_fused(e13, sl.dev + c->w13_bytes, nullptr, c->wt, pkt, u_f32, c->d_a + (size_t)ypos * F,
                                            w_dev, y, d, c->Fs, s, false));
           } else {  // W13 starts as soon as its part has landed, W2 after the rest
-            CUDA_OK(c, cudaStreamWaitEvent(s, sl.ev_w13, 0));
+            wait_load(c, sl, 0, s);
             tr_dev(c, ODMOE_EV_COMPUTE_START, s, l, S[j], si);
             { KTimer t(c, K_W13, s); CUDA_OK(c, launch_w13(e13, c->wt, pkt, u_f32, c->d_a + (size_t)ypos * F, d, c->Fs, s)); }
-            CUDA_OK(c, cudaStreamWaitEvent(s, sl.ev_done, 0));
+            wait_load(c, sl, 1, s);
             { KTimer t(c, K_W2, s); CUDA_OK(c, launch_w2(e2, c->wt, c->d_a + (size_t)ypos * F, w_dev, y, d, c->Fs, s)); }
           }
           tr_dev(c, ODMOE_EV_COMPUTE_END, s, l, S[j], si);
@@ -1721,6 +1763,7 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
   if (!c->resident && (shadow_pred || gate_reuse) && (r0 || c->world > 1)) CUDA_OK(c, cudaStreamSynchronize(c->s_shadow));
   if (c->spec_step == c->step + 1) pump(c);  // the speculative pass has finished: plan what fits now
   if (c->h_flag[0] == 2) fail(c, ODMOE_E_STATE, "peer partials did not arrive (P2P combine timeout)");
+  if (c->h_flag[0] == 3) fail(c, ODMOE_E_STATE, "an expert load did not land (warm-wait timeout)");
   if (c->h_flag[0]) fail(c, ODMOE_E_NONFINITE, "non-finite router logits");
   if (c->resident) std::copy(c->h_ids, c->h_ids + (size_t)L * k, true_ids.begin());
 
@@ -1781,7 +1824,7 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
   c->step++;
   c->align_n++;
   if (c->H > 0) c->pos++;
-  if (c->cfg.time_kernels) harvest_timers(c);
+  if (c->cfg.time_kernels || c->pass_timing) harvest_timers(c);
   if (c->trace) tr_resolve(c);
   // loader statistics
   c->stats.loads_issued = c->loader.loads_issued.load();
@@ -2157,6 +2200,7 @@ void destroy_ctx(Ctx* c) {
     F(s.dev);
     if (s.ev_w13) cudaEventDestroy(s.ev_w13);
     if (s.ev_done) cudaEventDestroy(s.ev_done);
+    if (s.flag) cudaFree(s.flag);
     if (s.ev_free) cudaEventDestroy(s.ev_free);
   }
   F(c->d_h); F(c->d_pkt); F(c->d_logits); F(c->d_a); F(c->d_y); F(c->d_yred); F(c->d_zero);
@@ -2173,6 +2217,7 @@ void destroy_ctx(Ctx* c) {
     F(s.dev);
     if (s.ev_w13) cudaEventDestroy(s.ev_w13);
     if (s.ev_done) cudaEventDestroy(s.ev_done);
+    if (s.flag) cudaFree(s.flag);
     if (s.ev_free) cudaEventDestroy(s.ev_free);
   }
   if (c->h_off) cudaFreeHost(c->h_off);
@@ -2391,7 +2436,7 @@ odmoe_status odmoe_predict_ahead(void* ctx, int32_t token, int from_layer, int d
       CUDA_OK(c, cudaMemcpyAsync(c->d_tok_in, c->h_tok, 4, cudaMemcpyHostToDevice, c->s_shadow));
       enqueue_shadow(c, c->d_tok_in, pbuf, false);
       CUDA_OK(c, cudaStreamSynchronize(c->s_shadow));
-      if (c->cfg.time_kernels) harvest_timers(c);
+      if (c->cfg.time_kernels || c->pass_timing) harvest_timers(c);
       c->predict_cache_token = token;
     }
     std::vector<int32_t> P((size_t)c->L * c->k);
@@ -2457,6 +2502,9 @@ odmoe_status odmoe_set_option(void* ctx, int key, int64_t value) {
         CUDA_OK(c, cudaStreamSynchronize(c->s_main));
       }
       c->trace = (int)value;
+    } else if (key == 9) {
+      if (value != 0 && value != 1) fail(c, ODMOE_E_CONFIG, "pass timing is 0 or 1");
+      c->pass_timing = (int)value;
     } else if (key == 8) {
       if (value < 1 || value > 64) fail(c, ODMOE_E_CONFIG, "token alignment period must be in 1..64");
       if (value > 1 && (!is_shadow(c->built_pred) || c->resident || c->H > 0))
@@ -2686,6 +2734,24 @@ odmoe_status odmoe_shadow_expert_ffn(const int8_t* q13, const float* s13, const 
   if (launch_w2(direct_ref(q2, s2, gate_idx), W_I8, a_scratch, gate_w, y, d, F, S(stream)) != cudaSuccess)
     return ODMOE_E_CUDA;
   return ODMOE_OK;
+}
+
+odmoe_status odmoe_shadow_expert_ffn_packed(const uint8_t* q13p, const float* s13, const uint8_t* q2p,
+                                            const float* s2, const void* u, const float* gate_w, int gate_idx,
+                                            int d, int F, float* a_scratch, float* y, void* stream) {
+  if (!q13p || !s13 || !q2p || !s2 || !u || !a_scratch || !y || !mma_shadow_ok(d, F) || gate_idx < 0)
+    return ODMOE_E_CONFIG;
+  if (launch_w13(direct_ref(q13p, s13, gate_idx), W_I8P, u, 0, a_scratch, d, F, S(stream)) != cudaSuccess)
+    return ODMOE_E_CUDA;
+  if (launch_w2(direct_ref(q2p, s2, gate_idx), W_I8P, a_scratch, gate_w, y, d, F, S(stream)) != cudaSuccess)
+    return ODMOE_E_CUDA;
+  return ODMOE_OK;
+}
+
+odmoe_status odmoe_pack_int8_frag(const int8_t* q, int64_t R, int64_t C, int pair_rows, uint8_t* out, void* stream) {
+  if (!q || !out || R < 16 || C < 32 || R % 16 || C % 32 || R > INT32_MAX || C > INT32_MAX) return ODMOE_E_CONFIG;
+  return launch_pack_i8_frag((const uint8_t*)q, out, (int)R, (int)C, pair_rows, S(stream), true) == cudaSuccess
+             ? ODMOE_OK : ODMOE_E_CUDA;
 }
 
 odmoe_status odmoe_shadow_expert_ffn_nf4(const uint8_t* q13, const float* a13, const uint8_t* q2,

@@ -90,7 +90,8 @@ class Stats(ctypes.Structure):
         ("refine_corrections", ctypes.c_int64), ("refine_correct", ctypes.c_int64), ("refine_total", ctypes.c_int64),
         ("ms_attn", ctypes.c_double), ("n_attn", ctypes.c_int64), ("correct_in_time", ctypes.c_int64),
         ("spec_steps", ctypes.c_int64), ("early_loads", ctypes.c_int64), ("ms_sh_w13", ctypes.c_double),
-        ("ms_sh_w2", ctypes.c_double), ("n_sh_w13", ctypes.c_int64), ("n_sh_w2", ctypes.c_int64)]
+        ("ms_sh_w2", ctypes.c_double), ("n_sh_w13", ctypes.c_int64), ("n_sh_w2", ctypes.c_int64),
+        ("ms_sh_pass", ctypes.c_double), ("n_sh_pass", ctypes.c_int64)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
@@ -122,6 +123,8 @@ _ffn = _sig("odmoe_expert_ffn", [_P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P])
 _sh_ffn = _sig("odmoe_shadow_expert_ffn", [_P, _P, _P, _P, _P, _P, _I, _I, _I, _P, _P, _P])
 _lm = _sig("odmoe_lm_head_argmax", [_P, _P, _I, _I, _I, _F, _P, _P, _P, _P])
 _quant = _sig("odmoe_quantize_int8_rows", [_P, _I64, _I64, _I, _P, _P, _P])
+_sh_ffn_packed = _sig("odmoe_shadow_expert_ffn_packed", [_P, _P, _P, _P, _P, _P, _I, _I, _I, _P, _P, _P])
+_pack_frag = _sig("odmoe_pack_int8_frag", [_P, _I64, _I64, _I, _P, _P])
 _sh_ffn_nf4 = _sig("odmoe_shadow_expert_ffn_nf4", [_P, _P, _P, _P, _P, _P, _I, _I, _I, _P, _P, _P])
 _quant_nf4 = _sig("odmoe_quantize_nf4", [_P, _I64, _I64, _I, _P, _P, _P])
 _sh_ffn_fp8 = _sig("odmoe_shadow_expert_ffn_fp8", [_P, _P, _P, _P, _P, _P, _I, _I, _I, _P, _P, _P])
@@ -151,7 +154,8 @@ EXPORTED = ["odmoe_set_option", "odmoe_expert_ffn_grouped", "odmoe_prefill_group
             "odmoe_quantize_int8_rows", "odmoe_gen_weights", "odmoe_load", "odmoe_load_wait",
             "odmoe_evict", "odmoe_predict_ahead", "odmoe_decode_step", "odmoe_prefill",
             "odmoe_debug_read", "odmoe_tensor_ptr", "odmoe_shadow_expert_ffn_nf4", "odmoe_quantize_nf4",
-            "odmoe_shadow_expert_ffn_fp8", "odmoe_quantize_fp8_rows", "odmoe_trace_read"]
+            "odmoe_shadow_expert_ffn_fp8", "odmoe_quantize_fp8_rows", "odmoe_trace_read",
+            "odmoe_shadow_expert_ffn_packed", "odmoe_pack_int8_frag"]
 
 
 def abi_version() -> int:
@@ -213,6 +217,18 @@ def shadow_expert_ffn(q13, s13, q2, s2, u, a_scratch, y, gate_w=None, gate_idx=0
     d, F = q2.shape
     _check(_sh_ffn(_ptr(q13), _ptr(s13), _ptr(q2), _ptr(s2), _ptr(u), _ptr(gate_w), gate_idx, d, F,
                    _ptr(a_scratch), _ptr(y), _stream(stream)))
+
+
+def pack_int8_frag(q, out, pair_rows: bool, stream=None):
+    """int8 codes q [R, C] -> the tensor-core fragment-packed layout (uint8 [R*C])."""
+    R, C = q.shape
+    _check(_pack_frag(_ptr(q), R, C, int(pair_rows), _ptr(out), _stream(stream)))
+
+
+def shadow_expert_ffn_packed(q13p, s13, q2p, s2, u, a_scratch, y, d, F, gate_w=None, gate_idx=0, stream=None):
+    """INT8 shadow expert on the tensor cores: q13p / q2p from pack_int8_frag (W13 pair_rows=True)."""
+    _check(_sh_ffn_packed(_ptr(q13p), _ptr(s13), _ptr(q2p), _ptr(s2), _ptr(u), _ptr(gate_w), gate_idx, d, F,
+                          _ptr(a_scratch), _ptr(y), _stream(stream)))
 
 
 def shadow_expert_ffn_nf4(q13, a13, q2, a2, u, a_scratch, y, gate_w=None, gate_idx=0, stream=None):
@@ -393,6 +409,10 @@ class Engine:
                                 l_cur=e.l_cur, aux=e.aux, rank=e.rank, bytes=e.bytes, t_us=e.t_us))
             if n.value < cap:
                 return out
+
+    def set_pass_timing(self, on: bool):
+        """CUDA events around every whole shadow pass (stats ms_sh_pass / n_sh_pass)."""
+        self._ck(_set_option(self.ctx, 9, int(bool(on))))
 
     def set_position(self, pos: int):
         """Attention ctx: KV-cache position of the next decode step (0 = new sequence)."""

@@ -8,7 +8,7 @@ import pytest
 import oracle as O
 from inputs import (MIXTRAL, TINY, KIND_EMB, KIND_ROUTER, KIND_W1, KIND_W2, KIND_W3, bf16_bits_to_f32,
                     f32_to_bf16_bits, gen_expert, gen_hidden, tensor_id, weight_fp32, weight_bf16_bits)
-from tests.gpu_util import TOL_BF16, TOL_FP32, host, ids_match, l2rel, to_dev, torch, w13_interleaved
+from tests.gpu_util import TOL_BF16, TOL_FP32, assert_close, host, ids_match, l2rel, to_dev, torch, w13_interleaved
 
 pytestmark = pytest.mark.gpu
 
@@ -184,6 +184,43 @@ def test_shadow_expert_ffn_parity(od, shape):
     dq13 = O.dequantize_int8_rows(q13, s13)
     ref = O.expert_ffn(dq13[0::2], dq13[1::2], O.dequantize_int8_rows(q2, s2), u_f)
     assert l2rel(host(y), ref) <= 1e-5
+
+
+@pytest.mark.parametrize("dF", [(256, 512), (1024, 2048), (4096, 14336)])
+def test_packed_shadow_expert_ffn_parity(od, dF):
+    """The engine's INT8 shadow path on the tensor cores (reading Q32): the oracle's quantiser codes,
+    packed into the mma fragment layout, give the dequantised oracle expert element by element
+    (q exact in f16, x split hi/lo, fp32 accumulation)."""
+    t = torch()
+    d, F = dF
+    shape = type(TINY)(TINY.L, TINY.E, TINY.k, d, F, TINY.V)
+    W1, W3, W2 = gen_expert(shape, SEED, 2, 3, "bf16")
+    W13 = w13_interleaved(W1, W3).reshape(2 * F, d)
+    q13, s13 = O.quantize_int8_rows(W13)
+    q2, s2 = O.quantize_int8_rows(W2)
+    u_f = stored(O.rms_norm(gen_hidden(78, 1, d)[0]).astype(np.float32), "bf16")
+    cu = lambda x: t.from_numpy(np.ascontiguousarray(x)).cuda()  # noqa: E731
+    p13 = t.empty(2 * F * d, dtype=t.uint8, device="cuda")
+    p2 = t.empty(d * F, dtype=t.uint8, device="cuda")
+    od.pack_int8_frag(cu(q13), p13, True)
+    od.pack_int8_frag(cu(q2), p2, False)
+    a = t.empty(F, dtype=t.float32, device="cuda")
+    y = t.empty(d, dtype=t.float32, device="cuda")
+    gw = t.tensor([0.25, 0.75], dtype=t.float32, device="cuda")
+    od.shadow_expert_ffn_packed(p13, cu(s13), p2, cu(s2), to_dev(u_f, "bf16"), a, y, d, F, gate_w=gw, gate_idx=1)
+    t.cuda.synchronize()
+    dq13 = O.dequantize_int8_rows(q13, s13)
+    a_ref = O.silu(dq13[0::2] @ u_f) * (dq13[1::2] @ u_f)
+    ref = 0.75 * O.expert_ffn(dq13[0::2], dq13[1::2], O.dequantize_int8_rows(q2, s2), u_f)
+    # a_scratch holds the SwiGLU activation in the tensor cores' B-fragment form (f16 hi + lo per
+    # element, mma_gemv.cu store_frag): decode it
+    hv = a.cpu().numpy().view(np.float16).astype(np.float64)
+    p = np.arange(F)
+    kb, c = p >> 4, p & 15
+    tq, w, hf = (c & 7) >> 1, c >> 3, c & 1
+    a_got = hv[((kb * 8 + tq) * 2 + w) * 2 + hf] + hv[((kb * 8 + 4 + tq) * 2 + w) * 2 + hf]
+    assert_close(a_got, a_ref, 1e-5, what="a")
+    assert_close(host(y), ref, 1e-5, what="y")
 
 
 # ------------------------------------------------------------------ NF4 shadow (reading Q27)

@@ -28,6 +28,7 @@ def peaks():
 
 GAP_S = 0.0
 DIRTY = False
+GAP_MODE = "idle"   # idle: host sleep (GPU idle); spin: one-CTA spin kernel fills the gap; busy: HBM writes fill it
 
 
 def timeit(fn, iters, flush):
@@ -38,10 +39,17 @@ def timeit(fn, iters, flush):
             flush.add_(1)  # write 256 MB: L2 full of DIRTY lines (like just after an H2D load)
         else:
             flush.sum()  # read 256 MB (> 126 MB L2): evicts the weights with CLEAN lines
-        if GAP_S > 0:
+        if GAP_S > 0 and GAP_MODE == "idle":
             torch.cuda.synchronize()
             import time as _t
             _t.sleep(GAP_S)  # idle GPU before the launch (like the on-demand path waiting on PCIe)
+        elif GAP_S > 0 and GAP_MODE == "spin":
+            torch.cuda.synchronize()
+            torch.cuda._sleep(int(GAP_S * 1.9e9))  # one CTA spins for the gap on this stream
+        elif GAP_S > 0 and GAP_MODE == "busy":
+            torch.cuda.synchronize()
+            for _ in range(max(1, int(GAP_S / 40e-6))):
+                flush.add_(1)  # the whole GPU streams HBM for the gap (256 MB writes, ~40 us each)
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(s)
@@ -60,10 +68,12 @@ def main():
     ap.add_argument("--only", default="")
     ap.add_argument("--gap-ms", type=float, default=0.0)
     ap.add_argument("--dirty", action="store_true")
+    ap.add_argument("--gap-mode", default="idle", choices=["idle", "spin", "busy"])
     args = ap.parse_args()
-    global GAP_S, DIRTY
+    global GAP_S, DIRTY, GAP_MODE
     GAP_S = args.gap_ms * 1e-3
     DIRTY = args.dirty
+    GAP_MODE = args.gap_mode
     dev = torch.device("cuda", 0)
     flush = torch.zeros(64 << 20, dtype=torch.float32, device=dev)
     pk = peaks()
@@ -92,6 +102,16 @@ def main():
         nb = 3 * F * d + (2 * F + d) * 4
         out["expert_ffn_int8"] = dict(us_median=med * 1e6, us_best=best * 1e6, GBps=nb / med / 1e9,
                                       frac_hbm=nb / med / 1e9 / pk["hbm_gbs"], bytes=nb)
+        # the same expert on the tensor cores (fragment-packed codes; the engine's shadow path)
+        p13 = torch.empty(2 * F * d, dtype=torch.uint8, device=dev)
+        p2 = torch.empty(d * F, dtype=torch.uint8, device=dev)
+        odmoe.pack_int8_frag(q[: 2 * F * d].view(2 * F, d), p13, True)
+        odmoe.pack_int8_frag(q[2 * F * d:].view(d, F), p2, False)
+        med, best = timeit(lambda: odmoe.shadow_expert_ffn_packed(p13, sc[: 2 * F], p2, sc[2 * F:], u, a, y, d, F,
+                                                                  gate_w=gw), args.iters, flush)
+        out["expert_ffn_int8_mma"] = dict(us_median=med * 1e6, us_best=best * 1e6, GBps=nb / med / 1e9,
+                                          frac_hbm=nb / med / 1e9 / pk["hbm_gbs"], bytes=nb)
+        del p13, p2
         # NF4 shadow expert (reading Q27): codes + block absmax
         q4 = torch.empty((3 * F * d // 2,), dtype=torch.uint8, device=dev)
         a4 = torch.empty(3 * F * d // 64, device=dev)

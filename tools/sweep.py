@@ -32,6 +32,8 @@ def main():
     ap.add_argument("--attention", action="store_true", help="Mixtral attention block (32/8 heads) + 512-token prefill")
     ap.add_argument("--kv-align", default="1", help="comma list of shadow KV alignment (1 = main cache, 0 = own)")
     ap.add_argument("--refine", default="0", help="comma list of SEP refinement depths (shadow predictor only)")
+    ap.add_argument("--periods", default="1", help="comma list of token alignment periods T_p (shadow predictors)")
+    ap.add_argument("--group-size", type=int, default=0, help="groups placement: G (0 => min(k, N))")
     ap.add_argument("--out", default="")
     ap.add_argument("--build-predictor", default="shadow_int8",
                     help="predictor the engine is created with (its shadow is the one shadow predictors use)")
@@ -53,7 +55,8 @@ def main():
     eng = odmoe.Engine(device=local, rank=rank, world_size=world, nccl_id=uid,
                        predictor=odmoe.PREDICTORS[args.build_predictor],
                        slots_per_gpu=args.slots or (4 if args.placement == "sliced" and world > 1 else 2),
-                       lookahead=1, weight_seed=2512, placement=int(args.placement == "sliced"), **SHAPE,
+                       lookahead=1, weight_seed=2512, placement=int(args.placement == "sliced"),
+                       group_size=args.group_size, **SHAPE,
                        **(dict(n_heads=32, n_kv_heads=8, max_seq=2048) if args.attention else {}))
     lines = []
     combos = []
@@ -62,16 +65,18 @@ def main():
         for D in [int(x) for x in args.lookaheads.split(",")]:
             for R in ([int(x) for x in args.refine.split(",")] if pname.startswith("shadow") else [0]):
                 for A in (aligns if pname.startswith("shadow") else [1]):
-                    combos.append((pname, D, R, A))
+                    for T in ([int(x) for x in args.periods.split(",")] if pname.startswith("shadow") else [1]):
+                        combos.append((pname, D, R, A, T))
     prompt = None
     if args.attention:
         from inputs import MIXTRAL, gen_prompt
         prompt = [int(x) for x in gen_prompt(MIXTRAL, 1, 512)]
-    for pname, D, R, A in combos:
+    for pname, D, R, A, T in combos:
         if True:
             eng.set_predictor(odmoe.PREDICTORS[pname])
             eng.set_lookahead(D)
             eng.set_refine_depth(R)
+            eng.set_align_period(T)
             if args.attention:
                 if pname.startswith("shadow"):
                     eng.set_kv_align(A)
@@ -107,8 +112,11 @@ def main():
                 recb = st["refine_correct"] / st["refine_total"] if st["refine_total"] else None
                 if pname.startswith("shadow"):
                     pname = args.build_predictor
-                line = {"n_gpus": world, "placement": args.placement, "attention": args.attention,
-                        "kv_align": A, "predictor": pname, "lookahead": D, "refine_depth": R,
+                line = {"n_gpus": world, "placement": args.placement, "group_size": args.group_size,
+                        "attention": args.attention, "kv_align": A, "predictor": pname, "lookahead": D,
+                        "refine_depth": R, "align_period": T,
+                        "recall_in_time": st["correct_in_time"] / st["predicted_total"] if st["predicted_total"] else None,
+                        "spec_steps": st["spec_steps"], "early_loads_per_token": st["early_loads"] / args.steps,
                         "recall_refined": recb, "refine_corrections_per_token": st["refine_corrections"] / args.steps,
                         "tok_s": args.steps / s,
                         "ms_per_token": s / args.steps * 1e3, "recall_eq3": rec,
