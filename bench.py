@@ -538,7 +538,7 @@ def main():
         G = args.group_size or min(SHAPE["k"], n)
         ng = 1 if sliced(args, n) else max(1, n // G)
         if trace_ev is not None:
-            line["eq1"] = eq1_from_trace(trace_ev, ng, SHAPE["L"])
+            line["eq1"] = eq1_from_trace(trace_ev, ng, SHAPE["L"], gemv_ms * 1e3 if gemv_ms > 0 else None)
         sh_rf = shadow_roofline(st, args.steps, peaks["hbm_gbs"])
         if sh_rf is not None:
             sh_rf["note"] = ("per-phase CUDA events inside the decode step (the shadow stream shares the GPU with "
@@ -627,7 +627,7 @@ def shadow_roofline(st, steps, peak):
     return out
 
 
-def eq1_from_trace(ev, ng, L):
+def eq1_from_trace(ev, ng, L, t_w_kernel_us=None):
     """Eq. 1 (worked example P:137; reading Q12) against the measured per-layer trace of this
     rank: t^M_l = main-node time of layer l (previous layer's last expert end -> this layer's routing
     known), t^W_l = expert computation of layer l on this GPU, t_load = one expert load (LoadStart ->
@@ -641,7 +641,8 @@ def eq1_from_trace(ev, ng, L):
     full = max((e["bytes"] for e in by.get("LoadEnd", [])), default=0)
     starts = {}
     for e in by.get("LoadStart", []):
-        starts.setdefault((e["step"], e["layer"], e["expert"]), []).append(e["t_us"])
+        if not math.isnan(e["t_us"]):  # (a load stopped before its first chunk never started)
+            starts.setdefault((e["step"], e["layer"], e["expert"]), []).append(e["t_us"])
     loads = []
     for e in by.get("LoadEnd", []):
         key = (e["step"], e["layer"], e["expert"])
@@ -670,9 +671,12 @@ def eq1_from_trace(ev, ng, L):
         if prev is not None:
             tM.append(tr - prev)
         if (s, l) in cs and (s, l) in cw:
-            tW.append(cw[(s, l)])
+            # expert kernel time of the layer on this GPU: from the kernel timers when given (the
+            # split W13 / W2 launches at N > 1 wait for the W2 part between ComputeStart and End)
+            tw = t_w_kernel_us * len(cs[(s, l)]) if t_w_kernel_us else cw[(s, l)]
+            tW.append(tw)
             # time the layer's expert work spent waiting for its loads once the routing was known
-            stalls.append(max(ce[(s, l)]) - tr - cw[(s, l)])
+            stalls.append(max(ce[(s, l)]) - tr - tw)
     if not loads or not tM or not tW:
         return {"N_G": ng, "note": "trace incomplete on this rank"}
     mean = lambda v: sum(v) / len(v)  # noqa: E731

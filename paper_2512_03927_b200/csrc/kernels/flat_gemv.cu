@@ -349,6 +349,7 @@ struct FlatArgs {
   int d_full, F_full;
   int evict_first;       // L2 policy of the weight stream
   int accumulate;        // MODE 1/3: out[r] += result instead of out[r] = result
+  P2PSend send;          // MODE 1: send.dst != NULL -> the fused P2P combine (kernels.h)
 };
 
 struct PdlWait {
@@ -666,7 +667,29 @@ __device__ __forceinline__ void flat_phase(const FlatArgs& a, uint8_t* sm, const
 #pragma unroll
       for (int w = 0; w < kFG_WARPS; ++w) s += part[w * a.rows_cap + r];
       if (!kNF4 && sc != nullptr) s *= sc[rb + r];
-      a.out[rb + r] = a.accumulate ? a.out[rb + r] + gw * s : gw * s;
+      const float v = a.accumulate ? a.out[rb + r] + gw * s : gw * s;
+      a.out[rb + r] = v;
+      if (MODE == 1 && a.send.dst != nullptr) {  // p2p_send's sum: prev[0] + ... + this expert's output
+        float t = v;
+        if (a.send.nprev > 0) {
+          t = a.send.prev[0][rb + r];
+          for (int i = 1; i < a.send.nprev; ++i) t += a.send.prev[i][rb + r];
+          t += v;
+        }
+        a.send.dst[rb + r] = t;
+      }
+    }
+    if (MODE == 1 && a.send.dst != nullptr) {
+      __threadfence_system();
+      __syncthreads();
+      if (tid == 0) {
+        const unsigned int done = atomicAdd_system(a.send.count, 1u);
+        if (done == gridDim.x - 1) {  // every CTA's rows are out: publish the layer's epoch
+          *a.send.count = 0u;
+          __threadfence_system();
+          asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.send.flag), "r"(a.send.epoch) : "memory");
+        }
+      }
     }
   } else {
     unsigned long long best = 0ull;
@@ -1072,7 +1095,7 @@ static cudaError_t multi_launch(MultiArgs m, cudaStream_t s, bool pdl) {
 
 cudaError_t launch_experts_fused(int n, const ExpertRef* ex, const void* const* w2_direct, const float* const* s2_direct,
                                  WType wt, const void* u, int u_f32, float* a_buf, const float* gate_w,
-                                 float* const* y, int d, int F, cudaStream_t s, bool pdl) {
+                                 float* const* y, int d, int F, cudaStream_t s, bool pdl, const P2PSend* send) {
   if (n < 1 || n > kMaxMulti) return cudaErrorInvalidValue;
   MultiArgs m{};
   m.n = n;
@@ -1087,6 +1110,7 @@ cudaError_t launch_experts_fused(int n, const ExpertRef* ex, const void* const* 
       a2.ex.blob = w2_direct[i];
       a2.ex.scales = s2_direct ? s2_direct[i] : nullptr;
     }
+    if (send && i == n - 1) a2.send = *send;  // the last expert's rows carry the layer's sum
   }
   switch (wt) {
     case W_BF16: return multi_launch<__nv_bfloat16, uint16_t>(m, s, pdl);
@@ -1281,7 +1305,7 @@ static cudaError_t fused_launch(FlatArgs a13, FlatArgs a2, cudaStream_t s, bool 
 
 cudaError_t launch_expert_fused(ExpertRef ex, const void* w2_direct, const float* s2_direct, WType wt,
                                 const void* u, int u_f32, float* a_buf, const float* gate_w, float* y, int d,
-                                int F, cudaStream_t s, bool pdl) {
+                                int F, cudaStream_t s, bool pdl, const P2PSend* send) {
   FlatArgs a13{}, a2{};
   a13.ex = ex; a13.second = 0; a13.x = u; a13.x_bf16 = !u_f32; a13.R = 2 * F; a13.C = d; a13.out = a_buf;
   a13.d_full = d; a13.F_full = F;
@@ -1291,6 +1315,7 @@ cudaError_t launch_expert_fused(ExpertRef ex, const void* w2_direct, const float
     a2.ex.blob = w2_direct;
     a2.ex.scales = s2_direct;
   }
+  if (send) a2.send = *send;
   switch (wt) {
     case W_BF16: return fused_launch<__nv_bfloat16, uint16_t>(a13, a2, s, pdl);
     case W_F32: return fused_launch<float, float>(a13, a2, s, pdl);

@@ -108,42 +108,43 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 }
 
 // MODE 0: SwiGLU -> bf16 [M, N/2]; MODE 1: gate-scale -> fp32 [M, N]. STAGES: smem ring depth
-// (2 with BN = 128 leaves room for two CTAs per SM, whose epilogues then overlap the other's loads)
+// (2 with BN = 128 leaves room for two CTAs per SM, whose epilogues then overlap the other's loads).
+//
+// Persistent (round 2): a CTA walks the tiles blockIdx.x, blockIdx.x + gridDim.x, ...; the producer's
+// ring runs across tile boundaries, so the next tile's weight stages stream in while the epilogue
+// warps drain the accumulator of the current one (acc_full / acc_empty barriers hand TMEM between the
+// MMA issuer and the epilogue), and the prologue (barriers, TMEM allocation, tensor-map prefetch) is
+// paid once per CTA instead of once per tile.
 template <int BN, int MODE, int STAGES = gg_stages<BN>()>
 __global__ void __launch_bounds__(kGG_THREADS, 1)
 grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ GGMaps maps_b,
-                    const int4* __restrict__ tiles, int K, int N, void* __restrict__ out,
+                    const int4* __restrict__ tiles, int n_tiles, int K, int N, void* __restrict__ out,
                     const float* __restrict__ gate) {
   constexpr int A_BYTES = kGG_BM * kGG_BK * 2;          // one 128-row half
   constexpr int B_BYTES = BN * kGG_BK * 2;
-  constexpr int RING = STAGES * (kGG_MT * A_BYTES + B_BYTES);
+  constexpr int STAGE = kGG_MT * A_BYTES + B_BYTES;
+  constexpr int RING = STAGES * STAGE;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + RING);
   uint64_t* empty = full + kGG_MAX_ST;
-  uint64_t* acc_ready = empty + kGG_MAX_ST;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_ready + 1);
+  uint64_t* acc_full = empty + kGG_MAX_ST;
+  uint64_t* acc_empty = acc_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int4 tile = tiles[blockIdx.x];  // {expert, row0, rows (<= 256), n0}
-  const int expert = tile.x, row0 = tile.y, rows = tile.z, n0 = tile.w;
-  const int halves = rows > kGG_BM ? 2 : 1;
   const int KB = K / kGG_BK;
-  // The loads are latency-bound (ncu: the MMA issuer waits on "full"), so the weight bytes in flight
-  // set the rate. A stage is [A halves][B]; a tile with one A half packs more stages into the same
-  // ring (GEMM1: 4 x 48 KB instead of 3 x 64 KB -> 128 KB of weights in flight instead of 96).
-  const int stage_bytes = halves * A_BYTES + B_BYTES;
-  int nst = maps_b.dyn_stages ? RING / stage_bytes : STAGES;
-  nst = nst > kGG_MAX_ST ? kGG_MAX_ST : nst;
-  auto sA_of = [&](int s, int hh) { return smem + s * stage_bytes + hh * A_BYTES; };
-  auto sB_of = [&](int s) { return smem + s * stage_bytes + halves * A_BYTES; };
+  auto sA_of = [&](int s, int hh) { return smem + s * STAGE + hh * A_BYTES; };
+  auto sB_of = [&](int s) { return smem + s * STAGE + kGG_MT * A_BYTES; };
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < nst; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    mbar_init(acc_ready, 1);
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    mbar_init(acc_full, 1);
+    mbar_init(acc_empty, 4);  // one arrival per epilogue warp
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps_b.b[expert])) : "memory");
+    for (int e = 0; e < kMaxGGExperts; ++e)
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps_b.b[e])) : "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -157,72 +158,91 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_cons
 
   if (warp == 0) {
     if (lane == 0) {
-      const uint32_t tx = (uint32_t)(halves * A_BYTES + B_BYTES);
-      for (int kb = 0, s = 0, ph = 0; kb < KB; ++kb) {
-        mbar_wait(&empty[s], (uint32_t)ph ^ 1u);
-        mbar_expect_tx(&full[s], tx);
-        for (int hh = 0; hh < halves; ++hh)
-          tma_load_2d(sA_of(s, hh), &map_a, &full[s], kb * kGG_BK, row0 + hh * kGG_BM);
-        tma_load_2d(sB_of(s), &maps_b.b[expert], &full[s], kb * kGG_BK, n0);
-        if (++s == nst) { s = 0; ph ^= 1; }
+      int s = 0, ph = 0;
+      for (int ti = blockIdx.x; ti < n_tiles; ti += gridDim.x) {
+        const int4 tile = tiles[ti];  // {expert, row0, rows (<= 256), n0}
+        const int halves = tile.z > kGG_BM ? 2 : 1;
+        const uint32_t tx = (uint32_t)(halves * A_BYTES + B_BYTES);
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(&empty[s], (uint32_t)ph ^ 1u);
+          mbar_expect_tx(&full[s], tx);
+          for (int hh = 0; hh < halves; ++hh)
+            tma_load_2d(sA_of(s, hh), &map_a, &full[s], kb * kGG_BK, tile.y + hh * kGG_BM);
+          tma_load_2d(sB_of(s), &maps_b.b[tile.x], &full[s], kb * kGG_BK, tile.w);
+          if (++s == STAGES) { s = 0; ph ^= 1; }
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = umma_idesc_bf16(kGG_BM, BN);
-      for (int kb = 0, s = 0, ph = 0; kb < KB; ++kb) {
-        mbar_wait(&full[s], (uint32_t)ph);
+      int s = 0, ph = 0, it = 0;
+      for (int ti = blockIdx.x; ti < n_tiles; ti += gridDim.x, ++it) {
+        const int halves = tiles[ti].z > kGG_BM ? 2 : 1;
+        mbar_wait(acc_empty, (uint32_t)(it & 1) ^ 1u);  // the epilogue has drained the previous tile
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t b0 = smem_u32(sB_of(s));
-        for (int hh = 0; hh < halves; ++hh) {
-          const uint32_t a0 = smem_u32(sA_of(s, hh));
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(&full[s], (uint32_t)ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t b0 = smem_u32(sB_of(s));
+          for (int hh = 0; hh < halves; ++hh) {
+            const uint32_t a0 = smem_u32(sA_of(s, hh));
 #pragma unroll
-          for (int k = 0; k < kGG_BK / 16; ++k)
-            umma_bf16(tmem + (uint32_t)(hh * BN), umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32),
-                      idesc, (kb | k) != 0);
+            for (int k = 0; k < kGG_BK / 16; ++k)
+              umma_bf16(tmem + (uint32_t)(hh * BN), umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32),
+                        idesc, (kb | k) != 0);
+          }
+          umma_commit(&empty[s]);  // smem slot free once these MMAs have read it
+          if (++s == STAGES) { s = 0; ph ^= 1; }
         }
-        umma_commit(&empty[s]);  // smem slot free once these MMAs have read it
-        if (++s == nst) { s = 0; ph ^= 1; }
+        umma_commit(acc_full);
       }
-      umma_commit(acc_ready);
     }
   } else {
     // epilogue: warp w owns TMEM lanes [32*(w%4), +32) of each accumulator half
     const int q = warp & 3;
-    mbar_wait(acc_ready, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    for (int hh = 0; hh < halves; ++hh) {
-      const int r = hh * kGG_BM + q * 32 + lane;
-      const bool valid = r < rows;
-      const long long grow = (long long)row0 + r;
-      const float g = (MODE == 1 && valid) ? (gate ? gate[grow] : 1.f) : 0.f;  // no gate: plain GEMM
+    int it = 0;
+    for (int ti = blockIdx.x; ti < n_tiles; ti += gridDim.x, ++it) {
+      const int4 tile = tiles[ti];
+      const int row0 = tile.y, rows = tile.z, n0 = tile.w;
+      const int halves = rows > kGG_BM ? 2 : 1;
+      mbar_wait(acc_full, (uint32_t)(it & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      for (int hh = 0; hh < halves; ++hh) {
+        const int r = hh * kGG_BM + q * 32 + lane;
+        const bool valid = r < rows;
+        const long long grow = (long long)row0 + r;
+        const float g = (MODE == 1 && valid) ? (gate ? gate[grow] : 1.f) : 0.f;  // no gate: plain GEMM
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        uint32_t v[16];
-        tmem_ld16(tmem + (uint32_t)(hh * BN) + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, v);
-        if (!valid) continue;
-        if constexpr (MODE == 0) {
-          uint32_t packed[4];
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+          uint32_t v[16];
+          tmem_ld16(tmem + (uint32_t)(hh * BN) + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, v);
+          if (!valid) continue;
+          if constexpr (MODE == 0) {
+            uint32_t packed[4];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const float a0 = silu_mul(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]));
-            const float a1 = silu_mul(__uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
-            const __nv_bfloat162 b = __floats2bfloat162_rn(a0, a1);
-            packed[i] = *reinterpret_cast<const uint32_t*>(&b);
+            for (int i = 0; i < 4; ++i) {
+              const float a0 = silu_mul(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]));
+              const float a1 = silu_mul(__uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+              const __nv_bfloat162 b = __floats2bfloat162_rn(a0, a1);
+              packed[i] = *reinterpret_cast<const uint32_t*>(&b);
+            }
+            __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(out) + grow * (N / 2) + (n0 + c0) / 2;
+            *reinterpret_cast<uint4*>(o) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+          } else {
+            float* o = reinterpret_cast<float*>(out) + grow * N + n0 + c0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              reinterpret_cast<float4*>(o)[i] =
+                  make_float4(g * __uint_as_float(v[4 * i]), g * __uint_as_float(v[4 * i + 1]),
+                              g * __uint_as_float(v[4 * i + 2]), g * __uint_as_float(v[4 * i + 3]));
           }
-          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(out) + grow * (N / 2) + (n0 + c0) / 2;
-          *reinterpret_cast<uint4*>(o) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-        } else {
-          float* o = reinterpret_cast<float*>(out) + grow * N + n0 + c0;
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            reinterpret_cast<float4*>(o)[i] =
-                make_float4(g * __uint_as_float(v[4 * i]), g * __uint_as_float(v[4 * i + 1]),
-                            g * __uint_as_float(v[4 * i + 2]), g * __uint_as_float(v[4 * i + 3]));
         }
       }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(acc_empty)) : "memory");
     }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   }
   __syncthreads();
   if (warp == 1) {
@@ -283,7 +303,10 @@ static cudaError_t gg_launch(const GroupedGemmArgs& g, cudaStream_t s) {
   auto kern = grouped_gemm_kernel<BN, MODE, STAGES>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  kern<<<g.n_tiles, kGG_THREADS, smem, s>>>(ma, mb, g.tiles, g.K, g.N, g.out, g.gate);
+  // persistent: one CTA per SM (two with the 128-wide 2-stage variant), tiles dealt round-robin
+  const int per_sm = STAGES <= 2 ? 2 : 1;
+  const int grid = g.n_tiles < num_sms() * per_sm ? g.n_tiles : num_sms() * per_sm;
+  kern<<<grid, kGG_THREADS, smem, s>>>(ma, mb, g.tiles, g.n_tiles, g.K, g.N, g.out, g.gate);
   return cudaGetLastError();
 }
 

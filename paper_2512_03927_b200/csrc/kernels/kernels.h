@@ -78,6 +78,19 @@ cudaError_t launch_quantize_fp8(const void* w, int64_t R, int64_t C, WType wt, u
 // NF4 blockwise quantiser (reading Q27): codes [R][C/2] bytes, absmax [R][C/64]; C % 64 == 0
 cudaError_t launch_quantize_nf4(const void* w, int64_t R, int64_t C, WType wt, uint8_t* q, float* absmax,
                                 cudaStream_t s);
+// The P2P combine fused into the W2 epilogue of a GPU's LAST expert of a layer:
+// every CTA stores, for its rows, prev[0] + ... + prev[nprev-1] + (this expert's gated output) -- the
+// order of launch_p2p_send -- straight into GPU 0's receive row over NVLink, fences at system scope
+// and counts itself on `count`; the last CTA releases `epoch` in `flag` (st.release.sys).
+struct P2PSend {
+  float* dst;                 // this rank's row of GPU 0's buffer (peer memory)
+  uint32_t* flag;             // this rank's flag on GPU 0
+  uint32_t epoch;
+  unsigned int* count;        // device counter of this GPU (reset by the last CTA)
+  const float* const* prev;   // device array: this GPU's earlier gated partials of the layer
+  int nprev;
+};
+
 // Fused expert FFN (flat engine): W13+SwiGLU -> grid barrier -> W2+gate in ONE cooperative
 // launch. Direct mode: ex.blob/ex.scales = W13 (+ scales), w2_direct/s2_direct = W2 (+ scales);
 // indirect mode: the expert table entries (whole blobs). a_buf: fp32 [F] scratch.
@@ -85,7 +98,8 @@ cudaError_t launch_quantize_nf4(const void* w, int64_t R, int64_t C, WType wt, u
 // barrier, W2 of all); a_buf: fp32 [n][F]; y[i]: output of expert i (gate-weighted). bf16 / fp32.
 cudaError_t launch_experts_fused(int n, const ExpertRef* ex, const void* const* w2_direct, const float* const* s2_direct,
                                  WType wt, const void* u, int u_f32, float* a_buf, const float* gate_w,
-                                 float* const* y, int d, int F, cudaStream_t s, bool pdl);
+                                 float* const* y, int d, int F, cudaStream_t s, bool pdl,
+                                 const P2PSend* send = nullptr);  // send: fused into the last expert
 // The n (<= 4) experts of one layer, one phase per launch, not cooperative (the shadow's k experts):
 // W13+SwiGLU of all -> a_buf [n][F]; W2+gate of all -> y_buf [n][d]. Each expert's result is bitwise
 // that of launch_w13 / launch_w2; shapes the flat engine does not take fall back to those launches.
@@ -96,7 +110,7 @@ cudaError_t launch_w2_multi(int n, const ExpertRef* ex, WType wt, const float* a
                             int d, int F, cudaStream_t s, bool pdl);
 cudaError_t launch_expert_fused(ExpertRef ex, const void* w2_direct, const float* s2_direct, WType wt,
                                 const void* u, int u_f32, float* a_buf, const float* gate_w, float* y, int d,
-                                int F, cudaStream_t s, bool pdl);
+                                int F, cudaStream_t s, bool pdl, const P2PSend* send = nullptr);
 // TMA-bulk streaming variants (stream_gemv.cu), used when stream_ok(wt, row length).
 bool stream_ok(WType wt, int C);
 cudaError_t launch_w13_stream(ExpertRef ex, WType wt, const void* u, int u_f32, float* a, int d, int F,

@@ -40,6 +40,9 @@ namespace odmoe {
 #ifndef MG_UNROLL
 #define MG_UNROLL 8
 #endif
+#ifndef MG_PF
+#define MG_PF 0     // L2 bulk prefetch of the units MG_PF batches beyond the two in registers (0 = off)
+#endif
 constexpr int kMG_WARPS = MG_WARPS;     // 16 warps x 2 batches x 8 units x 512 B = 128 KB in flight per SM
 constexpr int kMG_THREADS = kMG_WARPS * 32;
 constexpr int kMG_UNROLL = MG_UNROLL;
@@ -241,6 +244,21 @@ __global__ void __launch_bounds__(kMG_THREADS, 1) mma_gemv_kernel(const __grid_c
     }
   };
   for (int ub = wb; ub < we; ub += 2 * kMG_UNROLL) {
+#if MG_PF > 0
+    if (lane == 0) {  // the 2 batches after the register pipeline, into L2 (no registers held)
+      const int p0 = ub + 2 * kMG_UNROLL * MG_PF;
+      const int p1 = min(p0 + 2 * kMG_UNROLL, we);
+      for (int pv = p0; pv < p1;) {  // one bulk prefetch per contiguous run (an expert boundary splits it)
+        int e = 0;
+#pragma unroll
+        for (int j = 1; j < NE; ++j) e += pv >= j * U;
+        const int run_end = min(p1, (e + 1) * U);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(sW[e] + (size_t)pv * 32),
+                     "r"((uint32_t)(run_end - pv) * 512u) : "memory");
+        pv = run_end;
+      }
+    }
+#endif
 #pragma unroll
     for (int i = 0; i < kMG_UNROLL; ++i)
       if (ub + kMG_UNROLL + i < we) wc[i] = ld_unit(ub + kMG_UNROLL + i);

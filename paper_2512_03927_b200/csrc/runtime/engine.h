@@ -138,6 +138,8 @@ struct Ctx {
   float* p2p_own_part = nullptr; // rank 0: the allocation (freed at destroy)
   uint32_t* p2p_own_flag = nullptr;
   uint32_t p2p_seq = 0;          // epoch of the next layer combine (same sequence on every rank)
+  unsigned int* d_p2p_count = nullptr;  // CTA counter of the send fused into the last W2 (this GPU)
+  bool p2p_fused_sent = false;   // this layer's partials already went out from the W2 epilogue
   const float** d_y1ptr = nullptr;  // device array {d_y} (one partial)
   const float** d_yptr = nullptr;    // [k] -> d_y parts (N = 1)
   const float** d_yredptr = nullptr; // [1] -> d_yred

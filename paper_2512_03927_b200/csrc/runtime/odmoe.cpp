@@ -305,7 +305,6 @@ void validate(const odmoe_config* g) {
   const int G = g->group_size > 0 ? g->group_size : std::min(g->k, g->world_size);
   if (g->world_size % G && g->emulate_world <= 1) bad("world_size must be divisible by the group size (S:251, S:269)");
   if (g->k % G) bad("k must be divisible by the group size");
-  if (g->world_size > 1 && G != g->k) bad("multi-GPU needs group_size == k (one expert per GPU per layer)");
   if (g->slots_per_gpu != -1 && g->slots_per_gpu < g->k / G) bad("slots_per_gpu must be >= k/G or -1");
   if (g->world_size > 1 && g->nccl_id == nullptr) bad("nccl_id required when world_size > 1");
   if (g->refine_depth < 0 || g->refine_depth > 4) bad("refine_depth must be in 0..4");
@@ -1286,6 +1285,10 @@ void setup_p2p(Ctx* c) {
   cudaFree(dok);
   c->p2p = ok != 0;
   c->p2p_seq = 1;
+  if (c->p2p) {
+    c->d_p2p_count = dmalloc<unsigned int>(c, 1, "p2p count");
+    CUDA_OK(c, cudaMemset(c->d_p2p_count, 0, sizeof(unsigned int)));
+  }
 }
 
 // Ranks whose expert work feeds layer l's combine (bit r = rank r).
@@ -1347,13 +1350,39 @@ void emu_combine(Ctx* c, int l, const int32_t* S, cudaStream_t s) {
   if (c->dbg_yred) CUDA_OK(c, cudaMemcpyAsync(c->dbg_yred + (size_t)l * d, c->d_yred, sizeof(float) * d, cudaMemcpyDeviceToDevice, s));
 }
 
+// The cooperative fused expert kernel at N > 1 (default since round 2; ODMOE_FUSED_NGPU=0 restores the
+// split W13 / W2 launches). Safe because every kernel that can spin beside it is either stream-ordered
+// with it (layer NCCL, P2P gather, warm wait) or the one-CTA prediction communicator, and the flat
+// engine's grid leaves one SM free at N > 1.
 bool fused_ngpu_enabled() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("ODMOE_FUSED_NGPU");
-    v = (e && e[0] == '1') ? 1 : 0;
+    v = (e && e[0] == '0') ? 0 : 1;
   }
   return v == 1;
+}
+
+// ODMOE_P2P_FUSED=0: the separate send kernel after the experts (A/B of the fused W2-epilogue send)
+bool p2p_fused_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ODMOE_P2P_FUSED");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+// The P2P combine of this rank's layer partials, fused into its last expert's W2 (odmoe.h, kernels.h)
+P2PSend p2p_send_args(Ctx* c, int nprev) {
+  P2PSend ps{};
+  ps.dst = c->p2p_part + (size_t)c->rank * c->d;
+  ps.flag = c->p2p_flag + c->rank;
+  ps.epoch = c->p2p_seq;  // the epoch the layer-end send would use
+  ps.count = c->d_p2p_count;
+  ps.prev = c->d_yptr;
+  ps.nprev = nprev;
+  return ps;
 }
 
 bool graph_enabled() {
@@ -1536,6 +1565,8 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
     n_add = multi ? 1 : k;
 
     const bool in_group = (l % c->NG) == c->my_group;
+    const bool fuse_send = c->world > 1 && c->p2p && fused && p2p_fused_enabled();
+    c->p2p_fused_sent = false;
     if (c->resident) {
       // routing consumed on the device: no host round trip per layer
       if (in_group) {
@@ -1551,8 +1582,10 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
             ys[j] = c->d_y + (size_t)j * d;
           }
           KTimer t(c, K_W13, s, mine);
+          const P2PSend ps = fuse_send ? p2p_send_args(c, mine - 1) : P2PSend{};
           CUDA_OK(c, launch_experts_fused(mine, exs, nullptr, nullptr, c->wt, pkt, u_f32, c->d_a, w_dev, ys, d,
-                                          c->Fs, s, true));
+                                          c->Fs, s, true, fuse_send ? &ps : nullptr));
+          c->p2p_fused_sent = fuse_send;
         }
         for (int j = 0; j < mine; ++j) {
           ExpertRef ex{nullptr, nullptr, (const void* const*)c->d_res_tbl, nullptr, ids_dev,
@@ -1650,8 +1683,12 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
             wait_load(c, sl, 1, s);
             tr_dev(c, ODMOE_EV_COMPUTE_START, s, l, S[j], si);
             KTimer t(c, K_W13, s);
+            const int nmine = (int)mine.size();
+            const bool last = jj == nmine - 1;
+            const P2PSend ps = (fuse_send && last) ? p2p_send_args(c, nmine - 1) : P2PSend{};
             CUDA_OK(c, launch_expert_fused(e13, sl.dev + c->w13_bytes, nullptr, c->wt, pkt, u_f32, c->d_a + (size_t)ypos * F,
-                                           w_dev, y, d, c->Fs, s, false));
+                                           w_dev, y, d, c->Fs, s, false, (fuse_send && last) ? &ps : nullptr));
+            if (fuse_send && last) c->p2p_fused_sent = true;
           } else {  // W13 starts as soon as its part has landed, W2 after the rest
             wait_load(c, sl, 0, s);
             tr_dev(c, ODMOE_EV_COMPUTE_START, s, l, S[j], si);
@@ -1688,16 +1725,17 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
       // this rank's gated partials, summed in router rank order, stored into its row of GPU 0's
       // buffer over NVLink and published with a release flag (one kernel; no NCCL reduce)
       const uint32_t ep = c->p2p_seq++;
-      if (in_group) {
+      if (in_group && !c->p2p_fused_sent) {
         CUDA_OK(c, launch_p2p_send(c->d_yptr, c->sliced ? k : k / c->G, d, c->p2p_part + (size_t)c->rank * d,
                                    c->p2p_flag + c->rank, ep, s));
         c->stats.kernel_launches++;
       }
     } else if (c->world > 1) {
       const float* send = (in_group ? c->d_y : c->d_zero);
-      if (c->sliced) {  // this rank's k gated partials, summed in router rank order
+      const int nmine = c->sliced ? k : k / c->G;
+      if (in_group && nmine > 1) {  // this rank's gated partials, summed in router rank order
         CUDA_OK(c, cudaMemsetAsync(c->d_ysum, 0, sizeof(float) * d, s));
-        CUDA_OK(c, launch_combine(c->d_ysum, c->d_yptr, k, d, s));
+        CUDA_OK(c, launch_combine(c->d_ysum, c->d_yptr, nmine, d, s));
         c->stats.kernel_launches++;
         send = c->d_ysum;
       }
@@ -2208,6 +2246,7 @@ void destroy_ctx(Ctx* c) {
   F(c->d_lmscratch); F(c->d_lmlogits);
   F(c->sh_h); F(c->sh_u); F(c->sh_ids_all); F(c->sh_w); F(c->sh_logits_all); F(c->sh_a); F(c->sh_y); F((void*)c->sh_yptr);
   F(c->sh_tok); F(c->sh_lmscratch); F(c->sh_lmlogits);
+  F(c->d_p2p_count);
   F(c->d_yemu); F(c->d_prank); F((void*)c->d_emu_ptr); F(c->dbg_yrank);
   if (c->h_emu_ptr) cudaFreeHost((void*)c->h_emu_ptr);
   F(c->dbg_h); F(c->dbg_ypart); F(c->dbg_yred); F(c->dbg_sh_h_all); F(c->dbg_sh_u_all); F(c->dbg_sh_hf_all); F(c->dbg_hfinal);

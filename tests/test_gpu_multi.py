@@ -154,7 +154,7 @@ def test_multi_gpu_attention(world):
             assert r[4] == base_pf, (world, placement, r[0])
 
 
-def _run_rank_capture(rank, world, port, q, placement, p2p):
+def _run_rank_capture(rank, world, port, q, placement, p2p, G=0):
     """One rank of a real N-GPU decode with the debug capture on rank 0: per step the token, the
     final hidden state and every layer's combined expert output (bytes)."""
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -170,7 +170,8 @@ def _run_rank_capture(rank, world, port, q, placement, p2p):
     try:
         eng = odmoe.Engine(TINY.L, TINY.E, TINY.k, TINY.d, TINY.F, TINY.V, dtype=odmoe.BF16,
                            predictor=odmoe.PRED_NONE, slots_per_gpu=4, lookahead=1, weight_seed=SEED, rank=rank,
-                           world_size=world, device=rank, nccl_id=obj[0], placement=placement, debug_capture=1)
+                           world_size=world, device=rank, nccl_id=obj[0], placement=placement, debug_capture=1,
+                           group_size=G)
         out, t_ = [], 9
         for _ in range(6):
             t_, _ = eng.decode_step(t_)
@@ -185,12 +186,12 @@ def _run_rank_capture(rank, world, port, q, placement, p2p):
     dist.destroy_process_group()
 
 
-def _capture_multi(world, placement, p2p):
+def _capture_multi(world, placement, p2p, G=0):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29900 + world * 7 + placement * 3 + int(p2p) + os.getpid() % 50
-    ps = [ctx.Process(target=_run_rank_capture, args=(r, world, port, q, placement, p2p)) for r in range(world)]
+    port = 29900 + world * 7 + placement * 3 + int(p2p) + 17 * G + os.getpid() % 50
+    ps = [ctx.Process(target=_run_rank_capture, args=(r, world, port, q, placement, p2p, G)) for r in range(world)]
     for p in ps:
         p.start()
     res = sorted([q.get(timeout=600) for _ in ps], key=lambda x: x[0])
@@ -201,11 +202,11 @@ def _capture_multi(world, placement, p2p):
     return res[0][2]
 
 
-def _capture_emulated(world, placement):
+def _capture_emulated(world, placement, G=0):
     from paper_2512_03927_b200 import odmoe
     eng = odmoe.Engine(TINY.L, TINY.E, TINY.k, TINY.d, TINY.F, TINY.V, dtype=odmoe.BF16, predictor=odmoe.PRED_NONE,
                        slots_per_gpu=4, lookahead=1, weight_seed=SEED, placement=placement, debug_capture=1,
-                       emulate_world=world)
+                       emulate_world=world, group_size=G)
     out, t_ = [], 9
     for _ in range(6):
         t_, _ = eng.decode_step(t_)
@@ -227,12 +228,12 @@ def test_multi_gpu_matches_one_gpu_emulation(world):
         pytest.skip(f"needs {world} GPUs")
     import numpy as np
     from paper_2512_03927_b200 import odmoe
-    for placement in (odmoe.PLACE_SLICED, odmoe.PLACE_GROUPS):
-        emu = _capture_emulated(world, placement)
-        real = _capture_multi(world, placement, p2p=True)
-        assert real == emu, (world, placement)
-        assert _capture_multi(world, placement, p2p=True) == real
-        nccl = _capture_multi(world, placement, p2p=False)
+    for placement, G in ((odmoe.PLACE_SLICED, 0), (odmoe.PLACE_GROUPS, 0), (odmoe.PLACE_GROUPS, 1)):
+        emu = _capture_emulated(world, placement, G)
+        real = _capture_multi(world, placement, True, G)
+        assert real == emu, (world, placement, G)
+        assert _capture_multi(world, placement, True, G) == real
+        nccl = _capture_multi(world, placement, False, G)
         for (ta, ha, ya), (tb, hb, yb) in zip(nccl, real):
             assert ta == tb
             a = np.frombuffer(ha, dtype=np.float32)
