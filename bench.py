@@ -538,7 +538,8 @@ def main():
         G = args.group_size or min(SHAPE["k"], n)
         ng = 1 if sliced(args, n) else max(1, n // G)
         if trace_ev is not None:
-            line["eq1"] = eq1_from_trace(trace_ev, ng, SHAPE["L"], gemv_ms * 1e3 if gemv_ms > 0 else None)
+            line["eq1"] = eq1_from_trace(trace_ev, ng, SHAPE["L"], gemv_ms * 1e3 if gemv_ms > 0 else None,
+                                         st["ms_router"] / max(1, st["n_router"]) * 1e3)
         sh_rf = shadow_roofline(st, args.steps, peaks["hbm_gbs"])
         if sh_rf is not None:
             sh_rf["note"] = ("per-phase CUDA events inside the decode step (the shadow stream shares the GPU with "
@@ -612,11 +613,19 @@ def leg(eng, torch, barrier, dist, tok, steps, refine, restore):
 def shadow_roofline(st, steps, peak):
     """The INT8 shadow's expert phases (one launch per phase for the k experts of a layer) against
     the HBM peak: algorithmic bytes = int8 codes + fp32 row scales of the k experts."""
-    if not st.get("n_sh_w13") or not st.get("n_sh_w2"):
+    if not st.get("n_sh_w13"):
         return None
     k, d, F = SHAPE["k"], SHAPE["d"], SHAPE["F"]
     b13 = k * (2 * F * d + 2 * F * 4)
     b2 = k * (d * F + d * 4)
+    if not st.get("n_sh_w2"):  # both phases in one (cooperative) launch per layer
+        us = st["ms_sh_w13"] / (st["n_sh_w13"] / k) * 1e3
+        return {"bound": "hbm", "kernel": "INT8 shadow expert layer (W13+SwiGLU, grid barrier, W2+gate) of the k "
+                                          "experts in one cooperative launch",
+                "layer": {"bytes": b13 + b2, "us": us, "GBps": (b13 + b2) / us / 1e3,
+                          "frac": (b13 + b2) / us / 1e3 / peak},
+                "peak": peak, "unit": "GB/s", "us_shadow_per_step": st["ms_shadow"] / steps * 1e3,
+                "frac": (b13 + b2) / us / 1e3 / peak}
     us13 = st["ms_sh_w13"] / (st["n_sh_w13"] / k) * 1e3
     us2 = st["ms_sh_w2"] / (st["n_sh_w2"] / k) * 1e3
     out = {"bound": "hbm", "kernel": "INT8 shadow experts, one launch per phase for the layer's k experts",
@@ -627,7 +636,7 @@ def shadow_roofline(st, steps, peak):
     return out
 
 
-def eq1_from_trace(ev, ng, L, t_w_kernel_us=None):
+def eq1_from_trace(ev, ng, L, t_w_kernel_us=None, t_m_kernel_us=None):
     """Eq. 1 (worked example P:137; reading Q12) against the measured per-layer trace of this
     rank: t^M_l = main-node time of layer l (previous layer's last expert end -> this layer's routing
     known), t^W_l = expert computation of layer l on this GPU, t_load = one expert load (LoadStart ->
@@ -680,7 +689,11 @@ def eq1_from_trace(ev, ng, L, t_w_kernel_us=None):
     if not loads or not tM or not tW:
         return {"N_G": ng, "note": "trace incomplete on this rank"}
     mean = lambda v: sum(v) / len(v)  # noqa: E731
-    t_M, t_W, t_load = mean(tM), mean(tW), mean(loads)
+    # t^M: the main node's own work per layer. From the trace (previous expert end -> routing known)
+    # when this rank computes every layer; with groups the previous layer ran on another GPU, so the
+    # router kernel time (kernel timers) is used
+    t_M = t_m_kernel_us if (ng > 1 and t_m_kernel_us) else mean(tM)
+    t_W, t_load = mean(tW), mean(loads)
     t_max = ng * t_M + (ng - 1) * t_W
     pred_stall = t_load > t_max
     n_stall = sum(1 for x in stalls if x > 5.0)

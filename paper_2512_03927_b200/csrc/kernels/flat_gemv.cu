@@ -836,10 +836,11 @@ cudaError_t launch_w13_flat(ExpertRef ex, WType wt, const void* u, int u_f32, fl
 }
 
 cudaError_t launch_w2_flat(ExpertRef ex, WType wt, const float* act, const float* gate_w, float* y, int d,
-                           int F, cudaStream_t s, bool pdl) {
+                           int F, cudaStream_t s, bool pdl, const P2PSend* send) {
   FlatArgs a{};
   a.ex = ex; a.second = 1; a.x = act; a.x_bf16 = 0; a.R = d; a.C = F; a.gate_w = gate_w; a.out = y;
   a.d_full = d; a.F_full = F;
+  if (send) a.send = *send;
   switch (wt) {
     case W_BF16: return fg_launch<__nv_bfloat16, float, 1>(a, s, pdl);
     case W_F32: return fg_launch<float, float, 1>(a, s, pdl);
@@ -1025,6 +1026,19 @@ static cudaError_t barrier_counter(int dev, cudaStream_t s, BarrierState*& out) 
     if (e != cudaSuccess) return e;
   }
   out = &b;
+  return cudaSuccess;
+}
+
+cudaError_t coop_barrier_next(cudaStream_t s, int grid, unsigned int** counter, unsigned int* target) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  BarrierState* bs = nullptr;
+  cudaError_t e = barrier_counter(dev, s, bs);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(g_barrier_mu);
+  bs->epoch += (unsigned int)grid;
+  *counter = bs->counter;
+  *target = bs->epoch;
   return cudaSuccess;
 }
 

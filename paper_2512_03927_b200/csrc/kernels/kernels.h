@@ -61,8 +61,9 @@ cudaError_t launch_w2(ExpertRef ex, WType wt, const float* a, const float* gate_
 int gemv_engine();
 cudaError_t launch_w13_flat(ExpertRef ex, WType wt, const void* u, int u_f32, float* a, int d, int F,
                             cudaStream_t s, bool pdl);
+struct P2PSend;
 cudaError_t launch_w2_flat(ExpertRef ex, WType wt, const float* act, const float* gate_w, float* y, int d,
-                           int F, cudaStream_t s, bool pdl);
+                           int F, cudaStream_t s, bool pdl, const P2PSend* send = nullptr);
 cudaError_t launch_lm_head_flat(const float* h, const void* W, WType wt, int V, int d, float eps,
                                 int32_t* token_out, float* logits, void* scratch, cudaStream_t s, bool pdl,
                                 const float* scales = nullptr);
@@ -199,6 +200,11 @@ cudaError_t launch_p2p_gather(const float* part, const uint32_t* flags, uint32_t
 bool mma_shadow_ok(int d, int F);
 cudaError_t launch_mma_shadow(int n, const ExpertRef* ex, int mode, const void* x, const float* gate_w,
                               float* out, int d, int F, cudaStream_t s, bool pdl);
+// Both phases of the n W_I8P experts (indirect refs) in ONE cooperative launch with a grid barrier.
+cudaError_t launch_mma_shadow_layer(int n, const ExpertRef* ex, const void* u, float* a_buf, const float* gate_w,
+                                    float* y_buf, int d, int F, cudaStream_t s, bool pdl);
+// Next grid-barrier target of stream s for a cooperative grid of `grid` CTAs (flat engine's counter).
+cudaError_t coop_barrier_next(cudaStream_t s, int grid, unsigned int** counter, unsigned int* target);
 // biased codes [R][C] (row-major) -> W_I8P layout; pair_rows: W13's gate/up pairing
 cudaError_t launch_pack_i8_frag(const uint8_t* q_biased, uint8_t* out, int R, int C, int pair_rows, cudaStream_t s,
                                 bool signed_codes = false);  // signed_codes: input q (not q + 128)

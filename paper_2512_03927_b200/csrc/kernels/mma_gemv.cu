@@ -115,11 +115,34 @@ __device__ __forceinline__ void store_frag(uint32_t* frag, int p, float v) {
   h[((kb * 8 + 4 + tq) * 2 + w) * 2 + hf] = lo;
 }
 
-template <int MODE, int NE>
-__global__ void __launch_bounds__(kMG_THREADS, 1) mma_gemv_kernel(const __grid_constant__ MgArgs a) {
+struct MgPdlWait {
+  __device__ __forceinline__ void operator()() const { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+};
+// grid-wide barrier of a cooperative launch (arrival counter with monotonically growing targets)
+struct MgGridBarrier {
+  unsigned int* counter;
+  unsigned int target;
+  __device__ __forceinline__ void operator()() const {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(counter, 1u);
+      unsigned int v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
+      } while ((int)(v - target) < 0);
+    }
+    __syncthreads();
+  }
+};
+
+// One phase: MODE 0 = W13 + SwiGLU, MODE 1 = W2 + gate, for NE experts. `wait_dep` runs once the
+// data this phase consumes from earlier work may be read (PDL wait for a stand-alone launch, the grid
+// barrier in the fused layer kernel); this phase's first weight batches are issued before it.
+template <int MODE, int NE, typename WaitFn>
+__device__ __forceinline__ void mma_phase(const MgArgs& a, uint8_t* sm, const WaitFn& wait_dep, bool ids_ready = false) {
   // The NE experts' units form ONE stream (expert-major): a CTA's range and a warp's slice may cross
   // from one expert into the next, so pipeline fill, staging and tail are paid once per launch.
-  extern __shared__ __align__(128) uint8_t sm[];
   const int nkb = a.C / 16;
   constexpr int NX = MODE == 0 ? 1 : NE;                             // activation vectors staged
   uint2* xs = reinterpret_cast<uint2*>(sm);                          // [NX][C/16][8]: hi tq0..3, lo tq0..3
@@ -139,7 +162,8 @@ __global__ void __launch_bounds__(kMG_THREADS, 1) mma_gemv_kernel(const __grid_c
   const int we = u0 + (int)((long long)(u1 - u0) * (warp + 1) / kMG_WARPS);
   const uint64_t pol = l2_policy(true);
   const bool indirect = a.tbl != nullptr;
-  if (indirect) asm volatile("griddepcontrol.wait;" ::: "memory");  // the expert ids come from the router
+  const bool early = indirect && !ids_ready;
+  if (early) wait_dep();  // the expert ids come from the router
   if (tid < NE) {
     const int e = tid;
     const int pick = a.sel[e];
@@ -174,7 +198,7 @@ __global__ void __launch_bounds__(kMG_THREADS, 1) mma_gemv_kernel(const __grid_c
 #pragma unroll
   for (int i = 0; i < kMG_UNROLL; ++i)
     if (wb + i < we) wa[i] = ld_unit(wb + i);
-  if (!indirect) asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (!early) wait_dep();
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (MODE == 0) {  // u (bf16) -> f16 hi/lo B fragments
@@ -328,6 +352,25 @@ __global__ void __launch_bounds__(kMG_THREADS, 1) mma_gemv_kernel(const __grid_c
   }
 }
 
+template <int MODE, int NE>
+__global__ void __launch_bounds__(kMG_THREADS, 1) mma_gemv_kernel(const __grid_constant__ MgArgs a) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  mma_phase<MODE, NE>(a, sm, MgPdlWait{});
+}
+
+// The shadow's whole expert layer in ONE cooperative launch: W13 + SwiGLU of the NE experts, a grid
+// barrier, W2 + gate (one launch, ramp and tail per layer instead of two). Phase 2's first weight
+// batches are in flight before the barrier.
+template <int NE>
+__global__ void __launch_bounds__(kMG_THREADS, 1)
+mma_layer_kernel(const __grid_constant__ MgArgs a13, const __grid_constant__ MgArgs a2, unsigned int* counter,
+                 unsigned int target) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  mma_phase<0, NE>(a13, sm, MgPdlWait{});
+  __syncthreads();
+  mma_phase<1, NE>(a2, sm, MgGridBarrier{counter, target}, /*ids_ready=*/true);
+}
+
 // ---------------------------------------------------------------- packing (shadow build)
 // q [R][C] biased codes (q + 128, row-major) -> the fragment-packed layout above. pair_rows: W13
 // (tile row g = row 2(8t + g), tile row g + 8 = row 2(8t + g) + 1); else tile row r = row 16t + r.
@@ -476,6 +519,85 @@ cudaError_t launch_mma_shadow(int n, const ExpertRef* ex, int mode, const void* 
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
+// The shadow's expert layer (both phases, n experts) in one cooperative launch; grid barrier
+// counter from the flat engine's per-stream state (coop_barrier_next).
+cudaError_t launch_mma_shadow_layer(int n, const ExpertRef* ex, const void* u, float* a_buf, const float* gate_w,
+                                    float* y_buf, int d, int F, cudaStream_t s, bool pdl) {
+  if (n < 1 || n > kMG_MAXE || !mma_shadow_ok(d, F)) return cudaErrorInvalidValue;
+  MgArgs a[2];
+  // one SM stays free: a one-warp kernel (the compute stream's warm wait) may hold it, and a cooperative
+  // grid only starts once all its CTAs fit
+  int grid = stream_grid_sms() < num_sms() - 1 ? stream_grid_sms() : num_sms() - 1;
+  size_t smem = 0;
+  for (int mode = 0; mode < 2; ++mode) {
+    MgArgs& g = a[mode];
+    g = MgArgs{};
+    g.n = n;
+    g.R = mode == 0 ? 2 * F : d;
+    g.C = mode == 0 ? d : F;
+    g.x = mode == 0 ? u : (const void*)a_buf;
+    g.gate_w = mode == 1 ? gate_w : nullptr;
+    const bool ind = ex[0].tbl != nullptr;
+    g.tbl = ind ? ex[0].tbl : nullptr;
+    g.stbl = ind ? ex[0].stbl : nullptr;
+    g.ids = ind ? ex[0].ids : nullptr;
+    g.base = ex[0].base;
+    g.k = ex[0].k;
+    g.off = mode == 0 ? 0 : 2LL * F * d;
+    g.soff = mode == 0 ? 0 : 2LL * F;
+    for (int i = 0; i < n; ++i) {
+      if ((ex[i].tbl != nullptr) != ind || ex[i].tbl != nullptr) {  // direct refs only through launch_mma_shadow
+        if (!ind || ex[i].tbl != g.tbl || ex[i].ids != g.ids || ex[i].base != g.base) return cudaErrorInvalidValue;
+      }
+      g.sel[i] = ex[i].sel;
+      g.w[i] = ind ? nullptr : reinterpret_cast<const uint8_t*>(ex[i].blob);
+      g.sc[i] = ind ? nullptr : ex[i].scales;
+      g.out[i] = (mode == 0 ? a_buf : y_buf) + (size_t)i * (mode == 0 ? F : d);
+    }
+    const int tiles = g.R / 16, CB = g.C / 32;
+    const long long UT = (long long)tiles * CB * n;
+    long long gmax = UT / ((CB + 1) / 2);
+    if (gmax < grid) grid = (int)(gmax > 0 ? gmax : 1);
+  }
+  if (ex[0].tbl == nullptr) return cudaErrorInvalidValue;  // the engine passes indirect (device-chosen) experts
+  MgScratch* sc = nullptr;
+  cudaError_t e = mg_scratch(s, (long long)(2 * F / 16) * kMG_MAXE, sc);
+  if (e != cudaSuccess) return e;
+  for (int mode = 0; mode < 2; ++mode) {
+    MgArgs& g = a[mode];
+    const int tiles = g.R / 16, CB = g.C / 32;
+    const long long UT = (long long)tiles * CB * n;
+    g.tiles_cap = (int)((UT + grid - 1) / grid / CB) + 2;
+    g.gpart = sc->gpart;
+    g.ticket = sc->ticket;
+    const int nx = mode == 0 ? 1 : n;
+    const size_t sm = (size_t)nx * g.C / 16 * 64 + (size_t)kMG_WARPS * g.tiles_cap * 16 * sizeof(float);
+    smem = sm > smem ? sm : smem;
+  }
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  void (*kern)(const MgArgs, const MgArgs, unsigned int*, unsigned int) =
+      n == 1 ? mma_layer_kernel<1> : n == 2 ? mma_layer_kernel<2> : n == 3 ? mma_layer_kernel<3> : mma_layer_kernel<4>;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  unsigned int* counter = nullptr;
+  unsigned int target = 0;
+  e = coop_barrier_next(s, grid, &counter, &target);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kMG_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, kern, a[0], a[1], counter, target);
 }
 
 }  // namespace odmoe

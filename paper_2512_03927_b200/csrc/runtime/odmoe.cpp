@@ -811,12 +811,30 @@ void build_buffers(Ctx* c) {
   }
 }
 
+// ODMOE_SHADOW_FUSED=1: both tensor-core shadow phases in one cooperative launch per layer. Off by
+// default: measured 83.4 us per layer vs 49.0 + 31.5 us for the two launches (ncu, profiles/
+// launches_r02_shadow_layer_fused.csv) -- the grid barrier costs more than the launch it saves.
+bool shadow_fused_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ODMOE_SHADOW_FUSED");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 // The shadow's k experts of one layer (a8 on the quantised weights): W13+SwiGLU of all k in one
 // launch, W2+gate of all k in a second one (launch_w13_multi / launch_w2_multi; bitwise the
 // per-expert launches). a: [k][F] scratch, y: [k][d] gate-weighted outputs.
 void shadow_experts(Ctx* c, const ExpertRef* ex, const void* u, int u_f32, float* a, const float* gate_w, float* y,
                     bool pdl_first, cudaStream_t s) {
   const int k = c->k, d = c->d, F = c->F;
+  // the tensor-core INT8 shadow: both phases in one cooperative launch (ODMOE_SHADOW_FUSED=0: two)
+  if (c->sh_ewt == W_I8P && ex[0].tbl != nullptr && shadow_fused_enabled() && multi_flat_ok(k, c->sh_ewt, d, F)) {
+    KTimer t(c, K_SH_W13, s, k);
+    CUDA_OK(c, launch_mma_shadow_layer(k, ex, u, a, gate_w, y, d, F, s, pdl_first));
+    return;
+  }
   // shapes the flat engine does not take run one launch per expert (count them all)
   if (!multi_flat_ok(k, c->sh_ewt, d, F)) c->stats.kernel_launches += 2 * (k - 1);
   { KTimer t(c, K_SH_W13, s, k); CUDA_OK(c, launch_w13_multi(k, ex, c->sh_ewt, u, u_f32, a, d, F, s, pdl_first)); }
@@ -1565,7 +1583,9 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
     n_add = multi ? 1 : k;
 
     const bool in_group = (l % c->NG) == c->my_group;
-    const bool fuse_send = c->world > 1 && c->p2p && fused && p2p_fused_enabled();
+    // the P2P combine rides in the last expert's W2 epilogue (fused kernel, or a flat W2 launch)
+    const bool flat_w2 = gemv_engine() == 2 && stream_ok(c->wt, c->Fs);
+    const bool fuse_send = c->world > 1 && c->p2p && (fused || flat_w2) && p2p_fused_enabled();
     c->p2p_fused_sent = false;
     if (c->resident) {
       // routing consumed on the device: no host round trip per layer
@@ -1694,7 +1714,17 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
             tr_dev(c, ODMOE_EV_COMPUTE_START, s, l, S[j], si);
             { KTimer t(c, K_W13, s); CUDA_OK(c, launch_w13(e13, c->wt, pkt, u_f32, c->d_a + (size_t)ypos * F, d, c->Fs, s)); }
             wait_load(c, sl, 1, s);
-            { KTimer t(c, K_W2, s); CUDA_OK(c, launch_w2(e2, c->wt, c->d_a + (size_t)ypos * F, w_dev, y, d, c->Fs, s)); }
+            const int nmine = (int)mine.size();
+            const bool last = jj == nmine - 1;
+            if (fuse_send && last) {  // flat W2 launch with the layer's P2P send in its epilogue
+              const P2PSend ps = p2p_send_args(c, nmine - 1);
+              KTimer t(c, K_W2, s);
+              CUDA_OK(c, launch_w2_flat(e2, c->wt, c->d_a + (size_t)ypos * F, w_dev, y, d, c->Fs, s, false, &ps));
+              c->p2p_fused_sent = true;
+            } else {
+              KTimer t(c, K_W2, s);
+              CUDA_OK(c, launch_w2(e2, c->wt, c->d_a + (size_t)ypos * F, w_dev, y, d, c->Fs, s));
+            }
           }
           tr_dev(c, ODMOE_EV_COMPUTE_END, s, l, S[j], si);
           // evict right after use: the slot is reusable once this event fires (Q16)
