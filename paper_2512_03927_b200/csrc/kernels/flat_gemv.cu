@@ -680,9 +680,11 @@ __device__ __forceinline__ void flat_phase(const FlatArgs& a, uint8_t* sm, const
       }
     }
     if (MODE == 1 && a.send.dst != nullptr) {
-      __threadfence_system();
+      // the CTA barrier orders every thread's remote stores before thread 0's system-scope fence
+      // (cumulative), so one fence per CTA publishes them (a fence per thread cost ~50 us per launch)
       __syncthreads();
       if (tid == 0) {
+        __threadfence_system();
         const unsigned int done = atomicAdd_system(a.send.count, 1u);
         if (done == gridDim.x - 1) {  // every CTA's rows are out: publish the layer's epoch
           *a.send.count = 0u;

@@ -184,9 +184,17 @@ int gemv_engine() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("ODMOE_GEMV");
-    v = (e && e[0] == 'l') ? 0 : ((e && e[0] == 't') ? 1 : 2);
+    v = (e && e[0] == 'l') ? 0 : 2;
   }
   return v;
+}
+
+// Whether the flat engine handles a [R, C] matrix of type wt (rows must be whole 512-byte groups;
+// activations must fit in shared memory).
+bool stream_ok(WType wt, int C) {
+  if (wt == W_NF4) return C % 1024 == 0 && (long long)C * 4 <= 64 * 1024;  // flat engine only
+  const int esz = wt == W_F32 ? 4 : (wt == W_BF16 ? 2 : 1);
+  return ((long long)C * esz) % 512 == 0 && (long long)C * 4 <= 64 * 1024;
 }
 
 cudaError_t launch_w13(ExpertRef ex, WType wt, const void* u, int u_f32, float* a, int d, int F,
@@ -199,7 +207,6 @@ cudaError_t launch_w13(ExpertRef ex, WType wt, const void* u, int u_f32, float* 
                             : launch_lowbit_small(ex, wt, 0, u, u_f32, d, F, nullptr, a, s);
   if (stream_ok(wt, d)) {
     if (gemv_engine() == 2) return launch_w13_flat(ex, wt, u, u_f32, a, d, F, s, pdl);
-    if (gemv_engine() == 1) return launch_w13_stream(ex, wt, u, u_f32, a, d, F, s);
   }
   switch (wt) {
     case W_BF16: return w13_impl<__nv_bfloat16>(ex, u, u_f32, a, d, F, s);
@@ -220,7 +227,6 @@ cudaError_t launch_w2(ExpertRef ex, WType wt, const float* a, const float* gate_
                             : launch_lowbit_small(ex, wt, 1, a, 1, d, F, gate_w, y, s);
   if (stream_ok(wt, F)) {
     if (gemv_engine() == 2) return launch_w2_flat(ex, wt, a, gate_w, y, d, F, s, pdl);
-    if (gemv_engine() == 1) return launch_w2_stream(ex, wt, a, gate_w, y, d, F, s);
   }
   switch (wt) {
     case W_BF16: return w2_impl<__nv_bfloat16>(ex, a, gate_w, y, d, F, s);

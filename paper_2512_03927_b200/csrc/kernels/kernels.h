@@ -56,8 +56,9 @@ cudaError_t launch_w13(ExpertRef ex, WType wt, const void* u, int u_f32, float* 
 cudaError_t launch_w2(ExpertRef ex, WType wt, const float* a, const float* gate_w, float* y, int d,
                       int F, cudaStream_t s, bool pdl = false);
 
-// GEMV engines: 2 = flat per-warp streams (flat_gemv.cu, default), 1 = TMA bulk ring
-// (stream_gemv.cu), 0 = per-row register streaming (gemv.cu); env ODMOE_GEMV=flat|tma|ldg.
+// GEMV engines: 2 = flat per-warp streams (flat_gemv.cu, default), 0 = per-row register streaming
+// (gemv.cu); env ODMOE_GEMV=flat|ldg. (The measured TMA bulk-ring engine of round 1 lives in
+// tools/ab/stream_gemv.cu, outside the library.)
 int gemv_engine();
 cudaError_t launch_w13_flat(ExpertRef ex, WType wt, const void* u, int u_f32, float* a, int d, int F,
                             cudaStream_t s, bool pdl);
@@ -112,14 +113,8 @@ cudaError_t launch_w2_multi(int n, const ExpertRef* ex, WType wt, const float* a
 cudaError_t launch_expert_fused(ExpertRef ex, const void* w2_direct, const float* s2_direct, WType wt,
                                 const void* u, int u_f32, float* a_buf, const float* gate_w, float* y, int d,
                                 int F, cudaStream_t s, bool pdl, const P2PSend* send = nullptr);
-// TMA-bulk streaming variants (stream_gemv.cu), used when stream_ok(wt, row length).
+// Rows the flat engine takes for a [R, C] matrix of type wt (whole 512-byte groups).
 bool stream_ok(WType wt, int C);
-cudaError_t launch_w13_stream(ExpertRef ex, WType wt, const void* u, int u_f32, float* a, int d, int F,
-                              cudaStream_t s);
-cudaError_t launch_w2_stream(ExpertRef ex, WType wt, const float* act, const float* gate_w, float* y, int d,
-                             int F, cudaStream_t s);
-cudaError_t launch_lm_head_stream(const float* h, const void* W, WType wt, int V, int d, float eps,
-                                  int32_t* token_out, float* logits, void* scratch, cudaStream_t s);
 
 // a10: token = argmax_v (W_o RMSNorm(h))_v, lowest id on ties. scratch >= 8*(grid+2) bytes.
 // W_I8 (the shadow's LM head, cross-token speculation): logit_v = scales[v] * (q_v . bf16(RMSNorm(h))).

@@ -128,7 +128,6 @@ cudaError_t launch_lm_head(const float* h, const void* W, WType wt, int V, int d
   if (stream_ok(wt, d)) {
     if (gemv_engine() == 2 || wt == W_I8)
       return launch_lm_head_flat(h, W, wt, V, d, eps, token_out, logits, scratch, s, pdl, scales);
-    if (gemv_engine() == 1) return launch_lm_head_stream(h, W, wt, V, d, eps, token_out, logits, scratch, s);
   }
   switch (wt) {
     case W_BF16: return lm_impl<__nv_bfloat16>(h, W, nullptr, V, d, eps, token_out, logits, scratch, s);

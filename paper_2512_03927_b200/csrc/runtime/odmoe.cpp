@@ -1381,12 +1381,15 @@ bool fused_ngpu_enabled() {
   return v == 1;
 }
 
-// ODMOE_P2P_FUSED=0: the separate send kernel after the experts (A/B of the fused W2-epilogue send)
+// ODMOE_P2P_FUSED=1: the P2P send in the last expert's W2 epilogue instead of the one-CTA send kernel.
+// Off by default: every CTA must publish its remote rows with a system-scope fence before the release,
+// and those fences cost ~30 us per launch (N = 2, sliced: 87 us per half expert with the fused send vs
+// 56.5 us with the separate send kernel; profiles/r02_m2c_*.json) -- more than the kernel it saves.
 bool p2p_fused_enabled() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("ODMOE_P2P_FUSED");
-    v = (e && e[0] == '0') ? 0 : 1;
+    v = (e && e[0] == '1') ? 1 : 0;
   }
   return v == 1;
 }

@@ -113,6 +113,65 @@ def test_route_topk_parity(od, shape, dtype, m):
     assert excused <= max(2, m // 200)
 
 
+@pytest.mark.parametrize("E,k,d,dtype,n_add", [(8, 2, 4096, "bf16", 2), (8, 2, 256, "bf16", 0), (8, 2, 4096, "fp32", 1),
+                                               (64, 8, 1024, "bf16", 2), (64, 1, 512, "bf16", 2), (16, 4, 2048, "fp32", 3),
+                                               (2, 2, 256, "bf16", 2)])
+def test_decode_router_parity(od, E, k, d, dtype, n_add):
+    """The decode step's router (m = 1: the 8-CTA cluster kernel with DSMEM reductions and warp-shuffle
+    top-k) at the limits the ABI allows (E up to 64, k up to 8, k = E, k = 1): residual bit-exact, u
+    within bf16 rounding of RMSNorm(h), logits element-wise, ids by the near-tie rule, mixture weights;
+    40 independent rows (one launch each)."""
+    t = torch()
+    shape = type(TINY)(TINY.L, E, k, d, TINY.F, TINY.V)
+    excused = 0
+    for seed in range(40):
+        h, ys, Wg, h_new, u, ids, w, lg, flag = _router_case(od, shape, dtype, 1, n_add, 300 + seed)
+        assert flag == 0
+        want = h.copy()
+        if n_add:
+            s = ys[0].astype(np.float32)
+            for y in ys[1:]:
+                s = (s + y.astype(np.float32)).astype(np.float32)
+            want = (h + s).astype(np.float32)
+        assert np.array_equal(h_new.astype(np.float32), want.astype(np.float32))
+        u_ref = O.rms_norm(h_new[0])
+        tol = 2.0 ** -8 if dtype == "bf16" else 1e-6
+        assert np.all(np.abs(u[0] - u_ref) <= tol * np.abs(u_ref) + 1e-6)
+        r_ref = O.router_logits(Wg, u[0])
+        assert np.allclose(lg[0], r_ref, rtol=0, atol=1e-5 * np.abs(r_ref).max() + 1e-7)
+        ok, exc = ids_match(ids[0], r_ref, k)
+        assert ok, (seed, ids[0], r_ref)
+        excused += exc
+        assert np.allclose(w[0], O.mixture_weights(r_ref, list(ids[0])), atol=2e-6)
+    assert excused <= 2
+
+
+def test_decode_router_ties_and_nonfinite(od):
+    """m = 1: exact ties go to the lower expert index; a non-finite logit sets the flag."""
+    t = torch()
+    E, d, k = 8, 1024, 2
+    Wg = stored(weight_fp32(SEED, tensor_id(KIND_ROUTER, 11), E, d, d), "bf16")
+    Wg[5] = Wg[2]
+    Wg[7] = Wg[2]
+    for seed in range(16):
+        h = gen_hidden(40 + seed, 1, d)
+        hd = t.from_numpy(h.copy()).cuda()
+        u = t.empty((1, d), dtype=t.bfloat16, device="cuda")
+        ids = t.empty((1, k), dtype=t.int32, device="cuda")
+        w = t.empty((1, k), dtype=t.float32, device="cuda")
+        od.route_topk(hd, to_dev(Wg, "bf16"), k, u, ids, w)
+        t.cuda.synchronize()
+        ref = O.top_k(O.router_logits(Wg, host(u)[0]), k)
+        assert list(ids.cpu().numpy()[0]) == ref
+    h = gen_hidden(7, 1, d)
+    h[0, 3] = np.inf
+    hd = t.from_numpy(h.copy()).cuda()
+    flag = t.zeros(1, dtype=t.int32, device="cuda")
+    od.route_topk(hd, to_dev(Wg, "bf16"), k, u, ids, w, flag=flag)
+    t.cuda.synchronize()
+    assert int(flag.item()) == 1
+
+
 def test_route_topk_constructed_ties(od):
     t = torch()
     E, d, k = 8, 256, 2

@@ -1,3 +1,6 @@
+// ARCHIVED A/B CODE (round 2): not compiled into libodmoe.so. The TMA bulk-ring GEMV engine measured
+// in round 1 (profiles/kbench_r01_gemv_tma.json: 114 us per expert vs the flat engine's 73 -> 65.6 us);
+// kept for reference next to DESIGN.md section 6. It no longer builds against kernels.h as is.
 // HBM-streaming GEMV engine with TMA bulk copies (the expert SwiGLU FFN at batch 1, a8; the INT8
 // shadow experts, a4; the LM head, a10). y = W x for a row-major W whose rows are consumed exactly
 // once, so the kernel is a pure HBM stream and the whole design is about keeping enough bytes in
