@@ -44,7 +44,7 @@ def parse():
                     help="device expert slots per GPU; 0 => 2 (groups: whole experts) or 2k (sliced: 1/N slices)")
     ap.add_argument("--placement", default="sliced", choices=["groups", "sliced"],
                     help="N > 1: sliced loading (SURVEY §8(f)3; default: every link serves every layer, "
-                         "measured 97.6 vs 93.6 % of the link roofline at 4 GPUs) or the paper's worker "
+                         "measured 97.6 vs 93.6 %% of the link roofline at 4 GPUs) or the paper's worker "
                          "groups (P:104)")
     ap.add_argument("--refine", type=int, default=2,
                     help="SEP refinement depth R (DESIGN.md §7); 0 = the paper's token-aligned shadow only")
@@ -64,8 +64,24 @@ def parse():
     ap.add_argument("--group-size", type=int, default=0, help="groups placement: G (0 => min(k, N))")
     ap.add_argument("--no-r0", action="store_true", help="skip the paper-only SEP (refine 0) leg")
     ap.add_argument("--trace-steps", type=int, default=2, help="steps traced for the Eq. 1 analysis (0 = skip)")
+    ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp32"],
+                    help="main-model precision; fp32 = the paper's (P:173): 704.6 MB experts, 1 slot under the "
+                         "1 GB budget (SURVEY §8(d) C4), no refinement / prefill (bf16 paths)")
+    ap.add_argument("--layer-period", type=int, default=-1,
+                    help="expert_layer_period P (odmoe.h): expert weights repeat every P layers so the host pool "
+                         "holds P layers; loads and bytes per token unchanged. -1 => 16 for fp32 (the 180 GB "
+                         "fp32 pool exceeds the box's host RAM), 0 otherwise")
     ap.add_argument("--out", default="")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.layer_period < 0:
+        a.layer_period = 16 if a.dtype == "fp32" else 0
+    if a.dtype == "fp32":
+        global EXPERT_BYTES, W13_BYTES, W2_BYTES
+        EXPERT_BYTES, W13_BYTES, W2_BYTES = 2 * EXPERT_BYTES, 2 * W13_BYTES, 2 * W2_BYTES
+        a.refine, a.prefill = 0, 0
+        if a.slots == 0:
+            a.slots = 1
+    return a
 
 
 def measured_peaks():
@@ -280,6 +296,11 @@ def n_slots(args, n):
     return args.slots or (2 * SHAPE["k"] if sliced(args, n) else 2)
 
 
+def model_kw(args, odmoe):
+    """Main-model precision and the expert-layer period (fp32 leg)."""
+    return dict(dtype=odmoe.FP32 if args.dtype == "fp32" else odmoe.BF16, expert_layer_period=args.layer_period)
+
+
 def lookahead(args, n):
     return args.lookahead or (1 if sliced(args, n) else max(1, n // 2))
 
@@ -289,6 +310,9 @@ def workload_config(args, n):
     if n == 1:
         wl = ("configs[1]: Mixtral-8x7B shape (L=32, E=8, top-2, d=4096, F=14336, V=32000), "
               "bf16, batch-1 decode, on-demand expert loading")
+        if args.dtype == "fp32":
+            wl = ("configs[3] at the paper's precision (P:173): Mixtral-8x7B shape, FP32, batch-1 decode, "
+                  f"on-demand, {n_slots(args, n)} slot(s) of 704.6 MB under the 1 GB budget")
     elif sliced(args, n):
         wl = (f"configs[2]/[3]: Mixtral-8x7B shape, bf16, batch-1 decode, sliced loading: each of {n} GPUs "
               f"loads and computes 1/{n} of every routed expert, partials reduced on GPU 0, lookahead {lookahead(args, n)}")
@@ -304,7 +328,8 @@ def workload_config(args, n):
                            (f"decode after the {args.prefill}-token prefill" if args.prefill > 0 else
                             f"decode from position {args.context} (earlier cache rows zero: synthetic context)"))
                           if args.attention else "none on the hot path (reading Q22)"),
-            "l2": "inputs larger than L2: every step streams 64 distinct 352 MB experts"}
+            "l2": f"inputs larger than L2: every step streams 64 distinct {EXPERT_BYTES / 1e6:.1f} MB experts",
+            "expert_layer_period": args.layer_period or None}
 
 
 # ---------------------------------------------------------------------------- our arm
@@ -353,7 +378,7 @@ def main():
     eng = odmoe.Engine(device=local, rank=rank, world_size=world, nccl_id=uid, predictor=pred,
                        slots_per_gpu=n_slots(args, n), lookahead=D, time_kernels=2, weight_seed=SEED,
                        refine_depth=refine, placement=int(sliced(args, n)), group_size=args.group_size,
-                       **SHAPE, **attn_kw(args))
+                       **SHAPE, **attn_kw(args), **model_kw(args, odmoe))
     if args.align_period > 1:
         eng.set_align_period(args.align_period)
     if args.attention and args.prefill <= 0:
@@ -471,14 +496,14 @@ def main():
         achieved = blob / (gemv_ms * 1e-3) / 1e9 if gemv_ms > 0 else None
         traffic = None  # ncu dram bytes of one launch pair, captured at this slice size only
         prof = os.path.join(ROOT, "profiles", "ncu_expert_gemv_r01.json")
-        if os.path.exists(prof) and not sliced(args, n):
+        if os.path.exists(prof) and not sliced(args, n) and args.dtype == "bf16":
             try:
                 traffic = json.load(open(prof)).get("dram_bytes_per_expert")
             except Exception:
                 traffic = None
         floor_us = None  # pure-read floor of one 352 MB launch (tools/pattern_bench.cu, measured)
         pf = os.path.join(ROOT, "profiles", "pattern_bench_r01.json")
-        if os.path.exists(pf) and not sliced(args, n):
+        if os.path.exists(pf) and not sliced(args, n) and args.dtype == "bf16":
             try:
                 floor_us = json.load(open(pf))["slices_336MB"]["us_mean"]
             except Exception:
@@ -490,7 +515,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dev_s / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32" if args.dtype == "fp32" else "bf16",
             "data": "synthetic (counter-based splitmix64 weights, U(+-1/sqrt(fan_in)), seed 2512; "
                     "greedy token feedback)",
             "config": workload_config(args, n),
@@ -718,7 +743,7 @@ def resident_baseline(odmoe, torch, args, dev, rank, world, dist):
         uid = obj[0]
     eng = odmoe.Engine(device=dev, rank=rank, world_size=world, nccl_id=uid, predictor=odmoe.PRED_NONE,
                        slots_per_gpu=-1, time_kernels=1, weight_seed=SEED, placement=int(sliced(args, world)),
-                       **SHAPE, **attn_kw(args))
+                       **SHAPE, **attn_kw(args), **model_kw(args, odmoe))
     if args.attention:
         eng.set_position(args.context)
     tok = 1
@@ -761,7 +786,7 @@ def resident_baseline(odmoe, torch, args, dev, rank, world, dist):
             "expert_gemv_us": gemv_ms * 1e3,
             "expert_gemv_GBps": blob / (gemv_ms * 1e-3) / 1e9 if gemv_ms > 0 else None,
             "resident_expert_bytes_per_gpu": st["resident_bytes"],
-            "hbm_roofline_tok_s_1gpu": measured_peaks()[0]["hbm_gbs"] * 1e9 / (64 * EXPERT_BYTES + SHAPE["V"] * SHAPE["d"] * 2)}
+            "hbm_roofline_tok_s_1gpu": measured_peaks()[0]["hbm_gbs"] * 1e9 / (64 * EXPERT_BYTES + SHAPE["V"] * SHAPE["d"] * EXPERT_BYTES // (3 * SHAPE["d"] * SHAPE["F"]))}
 
 
 if __name__ == "__main__":

@@ -81,7 +81,7 @@ typedef enum {
                               every expert (W13 rows of its F/N gate/up pairs, the matching W2 columns),
                               sums its k gated partials and the N partials are reduced on GPU 0. All N host
                               links serve every layer, so lookahead 1 suffices. Needs F % (16 N) == 0; not
-                              with SHADOW_SAME; slots_per_gpu counts slice slots (>= k)                */
+                              with SHADOW_SAME; slots_per_gpu counts slice slots                        */
 } odmoe_placement;
 
 typedef struct {
@@ -89,7 +89,12 @@ typedef struct {
   int32_t dtype;             /* odmoe_dtype of the main model's weights and of the normalised input u */
   int32_t predictor;         /* odmoe_predictor                                                       */
   int32_t lookahead;         /* D >= 1: loads may be issued for layers <= current + D (Q11)           */
-  int32_t slots_per_gpu;     /* device expert slots per GPU (>= k/G); -1 = fully resident baseline     */
+  int32_t slots_per_gpu;     /* device expert slots per GPU (>= 1); -1 = fully resident baseline. With
+                                fewer slots than this GPU's experts of a layer (FP32 Mixtral: 1 slot
+                                under the 1 GB budget) the experts that found no slot
+                                before the router are loaded after the previous expert's compute frees
+                                one; like misprediction reloads they count as post-router loads
+                                (reloads, reload_ids)                                                  */
   float rms_eps;             /* RMSNorm epsilon (1e-5, Q7)                                             */
   uint64_t weight_seed;      /* synthetic weights: counter-based generator               */
   uint64_t aux_seed;         /* RANDOM predictor stream                                                */
@@ -119,7 +124,13 @@ typedef struct {
                                 then over the group's ranks in rank order. Values are bitwise those of
                                 the real N-GPU run (parity of the multi-GPU arithmetic on one GPU; time
                                 is NOT emulated). On-demand decode only (no prefill)                   */
-  int32_t reserved[1];
+  int32_t expert_layer_period; /* 0 => off; P in 1..L: the expert weights of layer l are generated as
+                                those of layer l mod P (a synthetic model whose expert tensors repeat
+                                with period P; routers, embedding, LM head stay per layer). The host pool
+                                holds P layers' blobs, every load still moves one full blob, so loads and
+                                bytes per token are the full model's: used for the FP32 leg whose
+                                L-layer pool (180 GB) exceeds the GPU box's host RAM. Not with groups
+                                placement at N > 1                                                      */
   const void* nccl_id;       /* 128-byte ncclUniqueId from rank 0 (NULL when world_size == 1)          */
 } odmoe_config;
 

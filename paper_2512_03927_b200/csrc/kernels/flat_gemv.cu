@@ -132,6 +132,21 @@ template <> struct FTraits<nf4x2> { static constexpr int bits = 4; static conste
 template <> struct FDot<nf4x2, uint16_t> { static constexpr int kN = 32; };
 struct fp8e4 { uint8_t v; };  // E4M3 code (FP8 shadow, reading Q28); row scales like int8
 struct u8b { uint8_t v; };    // INT8-row code stored as q + 128 (W_U8)
+// bf16 weights (row-major, the W_BF16 blob) consumed by the tensor cores: mma.sync m16n8k16, fp32
+// accumulate (flat_phase's kMMA branch). Activations are staged as bf16 hi + lo (x = hi + lo to
+// 2^-16 relative) in B columns 0 and 1, so the fp32 W2 input keeps ~fp32 accuracy.
+struct bf16m { uint16_t v; };
+template <> struct FDot<bf16m, float> { static constexpr int kN = 8; };
+__device__ __forceinline__ void mma_bf16_16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                               uint32_t b0, uint32_t b1) {
+  asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+               "{%0,%1,%2,%3};"
+               : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+               : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+#ifndef FG_MMA_KU
+#define FG_MMA_KU 2  // (16-row tile, 32-column block) units per register batch; two batches in flight
+#endif
 template <> struct FDot<nf4x2, float> { static constexpr int kN = 32; };
 
 // QLoRA's published NF4 codebook (Dettmers et al. 2023)
@@ -370,6 +385,8 @@ __device__ __forceinline__ void flat_phase(const FlatArgs& a, uint8_t* sm, const
   auto swz4 = [](int o) { const int q = o & (Q - 1), t = o / Q; return ((t >> 5) * Q + q) * 32 + (t & 31); };
   auto swz = [&](int e) { return swz4(e / EPU) * EPU + (e & (EPU - 1)); };
   constexpr bool kNF4 = FTraits<WT>::nf4;
+  constexpr bool kMMA = std::is_same<WT, bf16m>::value;
+  static_assert(!kMMA || MODE == 0 || MODE == 1, "tensor-core path: expert phases only");
   static_assert(!kNF4 || FG_PIPE == 0, "NF4 is implemented for the default pipeline");
   float* part = reinterpret_cast<float*>(sm);                          // [warps][rows_cap]
   XT* xs = reinterpret_cast<XT*>(part + kFG_WARPS * a.rows_cap);       // [C]
@@ -418,6 +435,7 @@ __device__ __forceinline__ void flat_phase(const FlatArgs& a, uint8_t* sm, const
     split_range(a.R, gridDim.x, blockIdx.x, rb, re);
   }
   const int nrows = (int)(re - rb);
+  if constexpr (!kMMA) {
   const int Cg = a.C / N;                 // 16-byte granules per row (multiple of 32)
   const int Gr = Cg / 32;                 // 512-byte groups per row
   const long long G = (long long)nrows * Gr;
@@ -647,6 +665,120 @@ __device__ __forceinline__ void flat_phase(const FlatArgs& a, uint8_t* sm, const
     const float t = warp_sum(acc);
     if (lane == 0) part[warp * a.rows_cap + row] += t;
   }
+  } else {
+    // ---- tensor-core branch (bf16m). The CTA's rows [rb, re) are cut into 16-row tiles (the last
+    // one masked); warp w owns the columns of 32-column blocks [kb0, kb1) of EVERY tile (split-K
+    // over the warps: a row's value depends only on the warp split, not on the CTA's range), so
+    // each (row, warp) partial is written once and the epilogue's fixed-order warp sum is reused.
+    // A fragment from the row-major blob: k inside an mma may be permuted as long as A and B use
+    // the same permutation. Lane (g = lane / 4, q = lane % 4) loads 16 bytes = columns
+    // [32 kb + 8 q, +8) of rows g and g + 8; words .x/.y feed mma #1 as k-pairs q / q + 4, words
+    // .z/.w mma #2. B column 0 = x hi, column 1 = x lo (lanes 0-3 / 4-7), the others zero; the
+    // result of row g is D[g][0] + D[g][1] (lane q == 0: c0 + c1, row g + 8: c2 + c3).
+    constexpr int KU = FG_MMA_KU;
+    const int KB = a.C / 32;
+    const int kb0 = (int)((long long)KB * warp / kFG_WARPS), kb1 = (int)((long long)KB * (warp + 1) / kFG_WARPS);
+    const int nkb = kb1 - kb0;
+    const int ntiles = (nrows + 15) / 16;
+    const int g = lane >> 2, q = lane & 3;
+    const long long rowq = a.C / 8;  // uint4 per row
+    const uint4* Wl = reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(W) + rb * (long long)a.C * 2) +
+                      (long long)g * rowq + q;
+    const uint64_t pol = l2_policy(a.evict_first != 0);
+    int lt = 0, lk = 0;  // load cursor (tile, k-block within the warp's range)
+    auto load_batch = [&](uint4 (&w0)[KU], uint4 (&w1)[KU]) {
+#pragma unroll
+      for (int i = 0; i < KU; ++i) {
+        if (lt < ntiles) {
+          const uint4* p = Wl + (long long)(16 * lt) * rowq + (long long)(kb0 + lk) * 4;
+          const int r0 = 16 * lt + g;
+          w0[i] = r0 < nrows ? ld_stream_pol(p, pol) : make_uint4(0u, 0u, 0u, 0u);
+          w1[i] = r0 + 8 < nrows ? ld_stream_pol(p + 8 * rowq, pol) : make_uint4(0u, 0u, 0u, 0u);
+          if (++lk == nkb) { lk = 0; ++lt; }
+        }
+      }
+    };
+    uint4 wa0[KU], wa1[KU], wb0[KU], wb1[KU];
+    if (nkb > 0) load_batch(wa0, wa1);  // weights first: they do not depend on the previous kernel
+    if (!early) wait_dep();
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    // x as bf16 hi / lo, 8-column chunks [hi 16 B | lo 16 B] (lanes 0-3 and 4-7 read 128 bytes in one
+    // shared-memory wavefront)
+    uint4* xs4 = reinterpret_cast<uint4*>(xs);
+    if (a.x_bf16) {
+      const uint4* s4 = reinterpret_cast<const uint4*>(a.x);
+      for (int i = tid; i < a.C / 8; i += kFG_THREADS) {
+        xs4[2 * i] = s4[i];
+        xs4[2 * i + 1] = make_uint4(0u, 0u, 0u, 0u);
+      }
+    } else {
+      const float4* s4 = reinterpret_cast<const float4*>(a.x);
+      const int n8 = a.C / 8;
+      for (int i0 = tid; i0 < n8; i0 += 4 * kFG_THREADS) {
+        float4 v[4][2];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (i0 + u * kFG_THREADS < n8) {
+            v[u][0] = s4[2 * (i0 + u * kFG_THREADS)];
+            v[u][1] = s4[2 * (i0 + u * kFG_THREADS) + 1];
+          }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (i0 + u * kFG_THREADS < n8) {
+            const float e[8] = {v[u][0].x, v[u][0].y, v[u][0].z, v[u][0].w, v[u][1].x, v[u][1].y, v[u][1].z, v[u][1].w};
+            uint32_t hw[4], lw[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const __nv_bfloat16 h0 = __float2bfloat16_rn(e[2 * j]), h1 = __float2bfloat16_rn(e[2 * j + 1]);
+              const __nv_bfloat16 l0 = __float2bfloat16_rn(e[2 * j] - __bfloat162float(h0));
+              const __nv_bfloat16 l1 = __float2bfloat16_rn(e[2 * j + 1] - __bfloat162float(h1));
+              hw[j] = (uint32_t)__bfloat16_as_ushort(h0) | ((uint32_t)__bfloat16_as_ushort(h1) << 16);
+              lw[j] = (uint32_t)__bfloat16_as_ushort(l0) | ((uint32_t)__bfloat16_as_ushort(l1) << 16);
+            }
+            xs4[2 * (i0 + u * kFG_THREADS)] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+            xs4[2 * (i0 + u * kFG_THREADS) + 1] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+          }
+      }
+    }
+    for (int i = tid; i < kFG_WARPS * a.rows_cap; i += kFG_THREADS) part[i] = 0.f;
+    __syncthreads();
+    // this lane's B words: chunk kb * 4 + q, hi (g == 0) or lo (g == 1); other columns are zero
+    const uint4* xl = xs4 + 2 * (kb0 * 4 + q) + (g == 1 ? 1 : 0);
+    const bool xon = g < 2;
+    float c[4] = {0.f, 0.f, 0.f, 0.f};
+    int ct = 0, ck = 0;  // consume cursor
+    auto consume = [&](const uint4 (&w0)[KU], const uint4 (&w1)[KU]) {
+#pragma unroll
+      for (int i = 0; i < KU; ++i) {
+        if (ct < ntiles) {
+          uint4 xv = xl[8 * ck];
+          if (!xon) xv = make_uint4(0u, 0u, 0u, 0u);
+          mma_bf16_16816(c, w0[i].x, w1[i].x, w0[i].y, w1[i].y, xv.x, xv.y);
+          mma_bf16_16816(c, w0[i].z, w1[i].z, w0[i].w, w1[i].w, xv.z, xv.w);
+          if (++ck == nkb) {  // tile complete: this warp's partials of its 16 rows
+            if (q == 0) {
+              const int r = 16 * ct + g;
+              if (r < nrows) part[warp * a.rows_cap + r] = c[0] + c[1];
+              if (r + 8 < nrows) part[warp * a.rows_cap + r + 8] = c[2] + c[3];
+            }
+            c[0] = c[1] = c[2] = c[3] = 0.f;
+            ck = 0;
+            ++ct;
+          }
+        }
+      }
+    };
+    if (nkb > 0) {
+      // two register batches in flight: load batch n + 1, then consume batch n
+      while (ct < ntiles) {
+        load_batch(wb0, wb1);
+        consume(wa0, wa1);
+        if (ct >= ntiles) break;
+        load_batch(wa0, wa1);
+        consume(wb0, wb1);
+      }
+    }
+  }
   __syncthreads();
 
   if (MODE == 0) {
@@ -811,6 +943,19 @@ static cudaError_t fg_launch(FlatArgs a, cudaStream_t s, bool pdl) {
 // bf16 -> fp32 unpack of every activation pair (ALU-bound kernels; INT8 expert 57.4 -> 53.3 us,
 // FP8 55.3 -> 54.1 us, profiles/kb_r01_lowbit_*.json; NF4 is faster with bf16 activations, whose
 // 64-byte-per-lane footprint keeps shared-memory traffic lower). ODMOE_LOWBIT_X=bf16: A/B.
+// bf16 expert phases (W13 + SwiGLU, W2 + gate) on the tensor cores (bf16m) with ODMOE_MAIN_MMA=1
+// (A/B; off by default). Measured (profiles/launches_r02_expert_bf16_{mma,ffma2}.csv): 63.9 vs 62.0
+// us per expert in the ncu launch list -- the FFMA2 stream is already at the pure-read floor of a
+// 352 MB launch (62.9 us, profiles/pattern_bench_r01.json), so fewer instructions buy nothing.
+static bool main_mma() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ODMOE_MAIN_MMA");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 static bool lowbit_xf32() {
   static int v = -1;
   if (v < 0) {
@@ -826,7 +971,7 @@ cudaError_t launch_w13_flat(ExpertRef ex, WType wt, const void* u, int u_f32, fl
   a.ex = ex; a.second = 0; a.x = u; a.x_bf16 = !u_f32; a.R = 2 * F; a.C = d; a.out = a_out;
   a.d_full = d; a.F_full = F;
   switch (wt) {
-    case W_BF16: return fg_launch<__nv_bfloat16, uint16_t, 0>(a, s, pdl);
+    case W_BF16: return main_mma() ? fg_launch<bf16m, float, 0>(a, s, pdl) : fg_launch<__nv_bfloat16, uint16_t, 0>(a, s, pdl);
     case W_F32: return fg_launch<float, float, 0>(a, s, pdl);
     case W_I8: return lowbit_xf32() ? fg_launch<int8_t, float, 0>(a, s, pdl) : fg_launch<int8_t, uint16_t, 0>(a, s, pdl);
     case W_U8: return lowbit_xf32() ? fg_launch<u8b, float, 0>(a, s, pdl) : fg_launch<u8b, uint16_t, 0>(a, s, pdl);
@@ -844,7 +989,7 @@ cudaError_t launch_w2_flat(ExpertRef ex, WType wt, const float* act, const float
   a.d_full = d; a.F_full = F;
   if (send) a.send = *send;
   switch (wt) {
-    case W_BF16: return fg_launch<__nv_bfloat16, float, 1>(a, s, pdl);
+    case W_BF16: return main_mma() ? fg_launch<bf16m, float, 1>(a, s, pdl) : fg_launch<__nv_bfloat16, float, 1>(a, s, pdl);
     case W_F32: return fg_launch<float, float, 1>(a, s, pdl);
     case W_I8: return fg_launch<int8_t, float, 1>(a, s, pdl);
     case W_U8: return fg_launch<u8b, float, 1>(a, s, pdl);
@@ -1129,7 +1274,7 @@ cudaError_t launch_experts_fused(int n, const ExpertRef* ex, const void* const* 
     if (send && i == n - 1) a2.send = *send;  // the last expert's rows carry the layer's sum
   }
   switch (wt) {
-    case W_BF16: return multi_launch<__nv_bfloat16, uint16_t>(m, s, pdl);
+    case W_BF16: return main_mma() ? multi_launch<bf16m, float>(m, s, pdl) : multi_launch<__nv_bfloat16, uint16_t>(m, s, pdl);
     case W_F32: return multi_launch<float, float>(m, s, pdl);
     default: return cudaErrorInvalidValue;
   }
@@ -1228,7 +1373,7 @@ cudaError_t launch_w13_multi(int n, const ExpertRef* ex, WType wt, const void* u
     a.d_full = d; a.F_full = F;
   }
   switch (wt) {
-    case W_BF16: return fg_multi_launch<__nv_bfloat16, uint16_t, 0>(m, s, pdl);
+    case W_BF16: return main_mma() ? fg_multi_launch<bf16m, float, 0>(m, s, pdl) : fg_multi_launch<__nv_bfloat16, uint16_t, 0>(m, s, pdl);
     case W_F32: return fg_multi_launch<float, float, 0>(m, s, pdl);
     case W_I8: return lowbit_xf32() ? fg_multi_launch<int8_t, float, 0>(m, s, pdl) : fg_multi_launch<int8_t, uint16_t, 0>(m, s, pdl);
     case W_U8: return lowbit_xf32() ? fg_multi_launch<u8b, float, 0>(m, s, pdl) : fg_multi_launch<u8b, uint16_t, 0>(m, s, pdl);
@@ -1257,7 +1402,7 @@ cudaError_t launch_w2_multi(int n, const ExpertRef* ex, WType wt, const float* a
     a.out = y_buf + (size_t)i * d; a.d_full = d; a.F_full = F;
   }
   switch (wt) {
-    case W_BF16: return fg_multi_launch<__nv_bfloat16, float, 1>(m, s, pdl);
+    case W_BF16: return main_mma() ? fg_multi_launch<bf16m, float, 1>(m, s, pdl) : fg_multi_launch<__nv_bfloat16, float, 1>(m, s, pdl);
     case W_F32: return fg_multi_launch<float, float, 1>(m, s, pdl);
     case W_I8: return fg_multi_launch<int8_t, float, 1>(m, s, pdl);
     case W_U8: return fg_multi_launch<u8b, float, 1>(m, s, pdl);
@@ -1333,7 +1478,7 @@ cudaError_t launch_expert_fused(ExpertRef ex, const void* w2_direct, const float
   }
   if (send) a2.send = *send;
   switch (wt) {
-    case W_BF16: return fused_launch<__nv_bfloat16, uint16_t>(a13, a2, s, pdl);
+    case W_BF16: return main_mma() ? fused_launch<bf16m, float>(a13, a2, s, pdl) : fused_launch<__nv_bfloat16, uint16_t>(a13, a2, s, pdl);
     case W_F32: return fused_launch<float, float>(a13, a2, s, pdl);
     case W_I8: return lowbit_xf32() ? fused_launch<int8_t, float>(a13, a2, s, pdl) : fused_launch<int8_t, uint16_t>(a13, a2, s, pdl);
     case W_U8: return lowbit_xf32() ? fused_launch<u8b, float>(a13, a2, s, pdl) : fused_launch<u8b, uint16_t>(a13, a2, s, pdl);

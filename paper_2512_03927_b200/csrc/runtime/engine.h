@@ -42,6 +42,7 @@ struct Ctx {
   int Fs = 0;             // F of the blobs this rank holds (F, or F / world when sliced)
   int64_t full_bytes = 0; // one whole expert blob (generator output)
   // emulate_world (world 1): the expert arithmetic of an N-GPU run on this GPU (odmoe.h)
+  int elp = 0;                   // expert_layer_period (0 = off)
   int emu = 0;                   // emulated ranks (0 = off)
   bool emu_sliced = false;       // SLICED: blob = N slice blobs (slice r laid out as rank r's pool blob)
   int emu_G = 1, emu_NG = 1;     // GROUPS: group size and number of groups of the emulated run

@@ -270,6 +270,11 @@ std::vector<int> my_experts(const Ctx* c, int l, const int32_t* S) {
 
 bool holds_expert(const Ctx* c, int l, int e) { return c->pool_off[(size_t)l * c->E + e] >= 0; }
 
+// Expert weights of layer l are generated as those of layer l mod P (config expert_layer_period P;
+// 0 => every layer its own). The host pool then holds P layers' blobs and layer l's loads read layer
+// (l mod P)'s: the bytes per load and the loads per token are those of the full model.
+int wl(const Ctx* c, int l) { return c->elp > 0 ? l % c->elp : l; }
+
 // ------------------------------------------------------------------ validation
 void validate(const odmoe_config* g) {
   auto bad = [](const std::string& m) { fail(nullptr, ODMOE_E_CONFIG, m); };
@@ -284,7 +289,7 @@ void validate(const odmoe_config* g) {
     if (g->F % (16 * g->world_size)) bad("sliced placement needs F % (16 N) == 0");
     if (g->predictor == ODMOE_PRED_SHADOW_SAME) bad("sliced placement: SHADOW_SAME keeps whole experts");
     if (g->group_size != 0) bad("sliced placement: group_size must be 0");
-    if (g->slots_per_gpu != -1 && g->slots_per_gpu < g->k) bad("sliced placement needs slots_per_gpu >= k");
+    if (g->slots_per_gpu != -1 && g->slots_per_gpu < 1) bad("slots_per_gpu must be >= 1 or -1");
   }
   if (g->predictor == ODMOE_PRED_SHADOW_NF4 && (g->d % 64 || g->F % 64)) bad("the NF4 shadow needs d, F multiples of 64");
   if (g->emulate_world > 1) {
@@ -300,12 +305,15 @@ void validate(const odmoe_config* g) {
   } else if (g->emulate_world < 0) {
     bad("emulate_world must be 0, 1, 2, 4 or 8");
   }
+  if (g->expert_layer_period < 0 || g->expert_layer_period > g->L) bad("expert_layer_period must be in 0..L");
+  if (g->expert_layer_period > 0 && g->world_size > 1 && g->placement == ODMOE_PLACE_GROUPS)
+    bad("expert_layer_period: groups placement at N > 1 keeps per-layer pools (use sliced)");
   if (g->lookahead < 1) bad("lookahead must be >= 1");
   if (g->world_size < 1 || g->rank < 0 || g->rank >= g->world_size) bad("rank/world_size");
   const int G = g->group_size > 0 ? g->group_size : std::min(g->k, g->world_size);
   if (g->world_size % G && g->emulate_world <= 1) bad("world_size must be divisible by the group size (S:251, S:269)");
   if (g->k % G) bad("k must be divisible by the group size");
-  if (g->slots_per_gpu != -1 && g->slots_per_gpu < g->k / G) bad("slots_per_gpu must be >= k/G or -1");
+  if (g->slots_per_gpu != -1 && g->slots_per_gpu < 1) bad("slots_per_gpu must be >= 1 or -1");
   if (g->world_size > 1 && g->nccl_id == nullptr) bad("nccl_id required when world_size > 1");
   if (g->refine_depth < 0 || g->refine_depth > 4) bad("refine_depth must be in 0..4");
   if (g->refine_depth > 0 && !is_shadow(g->predictor)) bad("refine_depth needs a shadow predictor");
@@ -439,7 +447,7 @@ void build_shadow(Ctx* c, char* staging) {
       for (int e = 0; e < E; ++e) {
         const size_t i = (size_t)l * E + e;
         char* q = dmalloc<char>(c, (size_t)3 * F * d * 2, "shadow expert bf16");
-        CUDA_OK(c, launch_gen(staging, 0, l, e, 0, 0, 0, d, F, c->cfg.weight_seed, c->wt, c->s_main));
+        CUDA_OK(c, launch_gen(staging, 0, wl(c, l), e, 0, 0, 0, d, F, c->cfg.weight_seed, c->wt, c->s_main));
         CUDA_OK(c, launch_f32_to_bf16((const float*)staging, q, 3LL * F * d, c->s_main));
         c->sh_blob[i] = q;
         c->stats.shadow_bytes += (int64_t)3 * F * d * 2;
@@ -493,7 +501,7 @@ void build_shadow(Ctx* c, char* staging) {
       if (!c->res_blob.empty() && c->res_blob[i]) {
         src = c->res_blob[i];
       } else {
-        CUDA_OK(c, launch_gen(staging, 0, l, e, 0, 0, 0, d, F, c->cfg.weight_seed, c->wt, c->s_main));
+        CUDA_OK(c, launch_gen(staging, 0, wl(c, l), e, 0, 0, 0, d, F, c->cfg.weight_seed, c->wt, c->s_main));
       }
       if (nf4) {  // codes W13 [2F][d/2] then W2 [d][F/2]; absmax W13 [2F][d/64] then W2 [d][F/64]
         uint8_t* q = dmalloc<uint8_t>(c, (size_t)3 * F * d / 2, "shadow expert nf4");
@@ -548,7 +556,7 @@ bool rank_may_need(const Ctx* c, int l, int e) {
 void gen_blob(Ctx* c, int l, int e, char* dst, char* full) {
   const int d = c->d, F = c->F;
   if (c->emu > 1 && c->emu_sliced) {  // N slice blobs back to back, slice r as rank r would hold it
-    CUDA_OK(c, launch_gen(full, 0, l, e, 0, 0, 0, d, F, c->cfg.weight_seed, c->wt, c->s_main));
+    CUDA_OK(c, launch_gen(full, 0, wl(c, l), e, 0, 0, 0, d, F, c->cfg.weight_seed, c->wt, c->s_main));
     const size_t es = c->esz;
     for (int r = 0; r < c->emu; ++r) {
       char* o = dst + (size_t)r * c->emu_slice_bytes;
@@ -560,10 +568,10 @@ void gen_blob(Ctx* c, int l, int e, char* dst, char* full) {
     return;
   }
   if (!c->sliced) {
-    CUDA_OK(c, launch_gen(dst, 0, l, e, 0, 0, 0, d, F, c->cfg.weight_seed, c->wt, c->s_main));
+    CUDA_OK(c, launch_gen(dst, 0, wl(c, l), e, 0, 0, 0, d, F, c->cfg.weight_seed, c->wt, c->s_main));
     return;
   }
-  CUDA_OK(c, launch_gen(full, 0, l, e, 0, 0, 0, d, F, c->cfg.weight_seed, c->wt, c->s_main));
+  CUDA_OK(c, launch_gen(full, 0, wl(c, l), e, 0, 0, 0, d, F, c->cfg.weight_seed, c->wt, c->s_main));
   const size_t es = c->esz, f0 = (size_t)c->rank * c->Fs;
   CUDA_OK(c, cudaMemcpyAsync(dst, full + 2 * f0 * d * es, (size_t)c->w13_bytes, cudaMemcpyDeviceToDevice, c->s_main));
   CUDA_OK(c, cudaMemcpy2DAsync(dst + c->w13_bytes, (size_t)c->Fs * es, full + (size_t)2 * F * d * es + f0 * es,
@@ -577,14 +585,17 @@ void build_pool(Ctx* c, char* staging) {
   int64_t n = 0;
   for (int l = 0; l < L; ++l)
     for (int e = 0; e < E; ++e)
-      if (rank_may_need(c, l, e)) c->pool_off[(size_t)l * E + e] = (n++) * c->blob_bytes;
+      if (l != wl(c, l)) c->pool_off[(size_t)l * E + e] = c->pool_off[(size_t)wl(c, l) * E + e];
+      else if (rank_may_need(c, l, e)) c->pool_off[(size_t)l * E + e] = (n++) * c->blob_bytes;
   c->pool_bytes = n * c->blob_bytes;
   if (c->resident) {
     // fully-resident baseline: every blob this rank may need lives in HBM (same placement)
     c->res_blob.assign((size_t)L * E, nullptr);
     for (int l = 0; l < L; ++l)
       for (int e = 0; e < E; ++e)
-        if (c->pool_off[(size_t)l * E + e] >= 0 || (c->rank == 0 && c->cfg.predictor == ODMOE_PRED_SHADOW_SAME)) {
+        if (l != wl(c, l)) {
+          c->res_blob[(size_t)l * E + e] = c->res_blob[(size_t)wl(c, l) * E + e];
+        } else if (c->pool_off[(size_t)l * E + e] >= 0 || (c->rank == 0 && c->cfg.predictor == ODMOE_PRED_SHADOW_SAME)) {
           char* p = dmalloc<char>(c, c->blob_bytes, "resident expert");
           gen_blob(c, l, e, p, staging);
           c->res_blob[(size_t)l * E + e] = p;
@@ -598,7 +609,7 @@ void build_pool(Ctx* c, char* staging) {
       for (int l = 0; l < L; ++l)
         for (int e = 0; e < E; ++e) {
           char* p = dmalloc<char>(c, c->blob_bytes, "shadow-same expert");
-          CUDA_OK(c, launch_gen(p, 0, l, e, 0, 0, 0, d, F, c->cfg.weight_seed, c->wt, c->s_main));
+          CUDA_OK(c, launch_gen(p, 0, wl(c, l), e, 0, 0, 0, d, F, c->cfg.weight_seed, c->wt, c->s_main));
           c->res_blob[(size_t)l * E + e] = p;
         }
     }
@@ -613,7 +624,7 @@ void build_pool(Ctx* c, char* staging) {
     for (int l = 0; l < L; ++l)
       for (int e = 0; e < E; ++e) {
         const int64_t off = c->pool_off[(size_t)l * E + e];
-        if (off < 0) continue;
+        if (off < 0 || l != wl(c, l)) continue;
         const int b = i++ & 1;
         if (used[b]) CUDA_OK(c, cudaEventSynchronize(done[b]));
         gen_blob(c, l, e, stg[b], staging);
@@ -1656,38 +1667,68 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
               std::find(mine.begin(), mine.end(), sl.expert) == mine.end())
             release_slot(c, i);
         }
+        // a slot for a post-router load of layer l: a free one, else the furthest future prefetch
+        // is dropped and re-planned later (never a slot held by odmoe_load, token -2; the next
+        // token's early loads are furthest); -1 if every slot holds layer l's own experts
+        auto take_slot = [&]() {
+          int fs = free_slot(c);
+          if (fs >= 0) return fs;
+          int far = -1;
+          auto wpos = [&](const Slot& q) { return (q.token - c->step) * (int64_t)L + q.layer; };
+          for (int i = 0; i < (int)c->slots.size(); ++i)
+            if (c->slots[i].occupied && c->slots[i].token >= c->step && (far < 0 || wpos(c->slots[i]) > wpos(c->slots[far]))) far = i;
+          if (far < 0 || wpos(c->slots[far]) <= l) return -1;
+          if (c->slots[far].token == c->step) c->next_plan = std::min(c->next_plan, c->slots[far].layer);
+          else c->next_plan_nx = std::min(c->next_plan_nx, c->slots[far].layer);
+          release_slot(c, far);
+          return far;
+        };
         for (int e : mine) {
           if (find_slot(c, c->step, l, e) >= 0) continue;
-          int fs = free_slot(c);
+          const int fs = take_slot();
           if (fs < 0) {
-            // every slot holds a future prefetch: drop the furthest one and re-plan it later
-            int far = -1;
-            // (never a slot held by odmoe_load, token -2; the next token's early loads are furthest)
-            auto wpos = [&](const Slot& q) { return (q.token - c->step) * (int64_t)L + q.layer; };
-            for (int i = 0; i < (int)c->slots.size(); ++i)
-              if (c->slots[i].occupied && c->slots[i].token >= c->step && (far < 0 || wpos(c->slots[i]) > wpos(c->slots[far]))) far = i;
-            if (far < 0 || wpos(c->slots[far]) <= l) fail(c, ODMOE_E_BUDGET, "no slot for a reload");
-            if (c->slots[far].token == c->step) c->next_plan = std::min(c->next_plan, c->slots[far].layer);
-            else c->next_plan_nx = std::min(c->next_plan_nx, c->slots[far].layer);
-            release_slot(c, far);
-            fs = far;
+            // fewer slots than experts of the layer (e.g. FP32 Mixtral, 1 slot under the 1 GB
+            // budget): loaded in the compute loop below once an expert's slot frees
+            if ((int)c->slots.size() >= (int)mine.size()) fail(c, ODMOE_E_BUDGET, "no slot for a reload");
+            continue;
           }
           tr_host(c, ODMOE_EV_MISPREDICT, l, e, fs, 0);
           submit_load(c, fs, c->step, l, e, load_key(c, c->step, l, 0), LK_RELOAD);
           reloads++;
           c->stats.reloads++;
         }
-        // compute, in rank order of the router's output
+        // compute, in rank order of the router's output; with a slot shortage the experts
+        // already in slots go first and the deferred ones follow as slots free (each expert writes
+        // its own output row ypos, so the combine order is unchanged)
+        int ord[8], rpos[8], nord = 0;
+        bool deferred = false;
+        for (int pass = 0; pass < 2; ++pass)
+          for (int j = 0, p = 0; j < k; ++j) {
+            if (std::find(mine.begin(), mine.end(), S[j]) == mine.end()) continue;
+            const bool has = find_slot(c, c->step, l, S[j]) >= 0;
+            if (pass == 0) { rpos[j] = p; deferred |= !has; }
+            if (has == (pass == 0)) ord[nord++] = j;
+            p++;
+          }
+        const bool fuse_send_l = fuse_send && !deferred;
         int jj = 0;
-        for (int j = 0; j < k; ++j) {
-          if (std::find(mine.begin(), mine.end(), S[j]) == mine.end()) continue;
-          const int si = find_slot(c, c->step, l, S[j]);
+        for (int oi = 0; oi < nord; ++oi) {
+          const int j = ord[oi];
+          int si = find_slot(c, c->step, l, S[j]);
+          if (si < 0) {  // deferred (slot shortage): the slot the previous expert just freed; the copy
+                         // waits for that expert's compute (the slot's free event)
+            si = take_slot();
+            if (si < 0) fail(c, ODMOE_E_BUDGET, "no slot for a deferred load");
+            submit_load(c, si, c->step, l, S[j], load_key(c, c->step, l, 0), LK_RELOAD);
+            reloads++;
+            c->stats.reloads++;
+          }
           Slot& sl = c->slots[si];
           if (!c->loader.wait_issued(sl.req)) {
             if (c->loader.error() != cudaSuccess) CUDA_OK(c, c->loader.error());
             fail(c, ODMOE_E_STATE, "load was cancelled before compute");
           }
-          const int ypos = (c->world == 1 || c->sliced) ? j : jj;
+          const int ypos = (c->world == 1 || c->sliced) ? j : rpos[j];
           float* y = c->d_y + (size_t)ypos * d;
           ExpertRef e13 = direct_ref(sl.dev, nullptr, j);
           ExpertRef e2 = direct_ref(sl.dev + c->w13_bytes, nullptr, j);
@@ -1708,10 +1749,10 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
             KTimer t(c, K_W13, s);
             const int nmine = (int)mine.size();
             const bool last = jj == nmine - 1;
-            const P2PSend ps = (fuse_send && last) ? p2p_send_args(c, nmine - 1) : P2PSend{};
+            const P2PSend ps = (fuse_send_l && last) ? p2p_send_args(c, nmine - 1) : P2PSend{};
             CUDA_OK(c, launch_expert_fused(e13, sl.dev + c->w13_bytes, nullptr, c->wt, pkt, u_f32, c->d_a + (size_t)ypos * F,
-                                           w_dev, y, d, c->Fs, s, false, (fuse_send && last) ? &ps : nullptr));
-            if (fuse_send && last) c->p2p_fused_sent = true;
+                                           w_dev, y, d, c->Fs, s, false, (fuse_send_l && last) ? &ps : nullptr));
+            if (fuse_send_l && last) c->p2p_fused_sent = true;
           } else {  // W13 starts as soon as its part has landed, W2 after the rest
             wait_load(c, sl, 0, s);
             tr_dev(c, ODMOE_EV_COMPUTE_START, s, l, S[j], si);
@@ -1719,7 +1760,7 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
             wait_load(c, sl, 1, s);
             const int nmine = (int)mine.size();
             const bool last = jj == nmine - 1;
-            if (fuse_send && last) {  // flat W2 launch with the layer's P2P send in its epilogue
+            if (fuse_send_l && last) {  // flat W2 launch with the layer's P2P send in its epilogue
               const P2PSend ps = p2p_send_args(c, nmine - 1);
               KTimer t(c, K_W2, s);
               CUDA_OK(c, launch_w2_flat(e2, c->wt, c->d_a + (size_t)ypos * F, w_dev, y, d, c->Fs, s, false, &ps));
@@ -2370,6 +2411,7 @@ odmoe_status odmoe_create(const odmoe_config* cfg, void** ctx_out) {
     c->world = cfg->world_size;
     c->rank = cfg->rank;
     c->sliced = cfg->placement == ODMOE_PLACE_SLICED && c->world > 1;
+    c->elp = cfg->expert_layer_period;
     c->Fs = c->sliced ? c->F / c->world : c->F;
     c->full_bytes = 3LL * c->F * c->d * (int64_t)c->esz;
     c->blob_elems = 3LL * c->Fs * c->d;

@@ -55,7 +55,7 @@ class Config(ctypes.Structure):
                 ("debug_capture", ctypes.c_int32), ("time_kernels", ctypes.c_int32),
                 ("pool_threads", ctypes.c_int32), ("refine_depth", ctypes.c_int32),
                 ("placement", ctypes.c_int32), ("n_heads", ctypes.c_int32), ("n_kv_heads", ctypes.c_int32),
-                ("max_seq", ctypes.c_int32), ("emulate_world", ctypes.c_int32), ("reserved", ctypes.c_int32 * 1),
+                ("max_seq", ctypes.c_int32), ("emulate_world", ctypes.c_int32), ("expert_layer_period", ctypes.c_int32),
                 ("nccl_id", ctypes.c_void_p)]
 
 
@@ -326,14 +326,15 @@ class Engine:
                  slots_per_gpu=2, rms_eps=1e-5, weight_seed=2512, aux_seed=1, rank=0, world_size=1,
                  group_size=0, device=0, chunk_bytes=0, debug_capture=0, time_kernels=0,
                  nccl_id: Optional[bytes] = None, refine_depth=0, placement=0, n_heads=0, n_kv_heads=0,
-                 max_seq=0, emulate_world=0):
+                 max_seq=0, emulate_world=0, expert_layer_period=0):
         self.cfg = Config(L=L, E=E, k=k, d=d, F=F, V=V, dtype=dtype, predictor=predictor,
                           lookahead=lookahead, slots_per_gpu=slots_per_gpu, rms_eps=rms_eps,
                           weight_seed=weight_seed, aux_seed=aux_seed, rank=rank, world_size=world_size,
                           group_size=group_size, device=device, chunk_bytes=chunk_bytes,
                           debug_capture=debug_capture, time_kernels=time_kernels, pool_threads=0,
                           refine_depth=refine_depth, placement=placement, n_heads=n_heads,
-                          n_kv_heads=n_kv_heads, max_seq=max_seq, emulate_world=emulate_world)
+                          n_kv_heads=n_kv_heads, max_seq=max_seq, emulate_world=emulate_world,
+                          expert_layer_period=expert_layer_period)
         self._uid = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
         self.cfg.nccl_id = ctypes.cast(self._uid, ctypes.c_void_p) if self._uid is not None else None
         self.L, self.E, self.k, self.d, self.F, self.V = L, E, k, d, F, V

@@ -61,3 +61,15 @@ def test_product_never_imports_oracle():
                 src = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src, f
                 assert "odmoe_oracle" not in src, f
+
+
+def test_create_validates_config_before_touching_the_gpu():
+    from paper_2512_03927_b200 import odmoe
+    # invalid configs are rejected as E_CONFIG with a message, GPU or not
+    for kw, msg in ((dict(expert_layer_period=-1), "expert_layer_period"),
+                    (dict(expert_layer_period=5), "expert_layer_period"),
+                    (dict(emulate_world=3), "emulate_world"),
+                    (dict(lookahead=0), "lookahead")):
+        with pytest.raises(odmoe.OdmoeError) as ei:
+            odmoe.Engine(4, 8, 2, 256, 512, 1024, **kw)
+        assert ei.value.status == 1 and msg in str(ei.value), (kw, str(ei.value))

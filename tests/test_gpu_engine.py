@@ -127,6 +127,34 @@ def test_tiny_decode_teacher_forced(od, dtype):
     eng.close()
 
 
+@pytest.mark.parametrize("dtype,slots", [("fp32", 1), ("bf16", 2)])
+def test_expert_layer_period_teacher_forced(od, dtype, slots):
+    """expert_layer_period P = 2: layer l's experts are layer (l mod 2)'s, the host pool holds 2 layers,
+    every load still moves a whole blob. Teacher-forced per layer vs the oracle on the aliased model;
+    fp32 with ONE slot is the paper's precision under the <1 GB budget."""
+    P = 2
+    W = gen_model_weights(TINY, SEED, dtype=dtype)
+    W["experts"] = {l: W["experts"][l % P] for l in range(TINY.L)}
+    SW = O.quantize_model_int8(W)
+    eng = engine(od, TINY, dtype, predictor=od.PRED_SHADOW_INT8, slots_per_gpu=slots, debug_capture=1,
+                 expert_layer_period=P)
+    st0 = eng.stats()
+    blob = 3 * TINY.F * TINY.d * (2 if dtype == "bf16" else 4)
+    assert st0["pool_bytes"] == P * TINY.E * blob
+    tok = int(gen_prompt(TINY, 1, 1)[0])
+    excused = 0
+    for n in range(8):
+        b0 = eng.stats()["bytes_h2d"]
+        nxt, recs = eng.decode_step(tok)
+        excused += check_step_teacher_forced(eng, W, TINY, dtype, tok, nxt, SW)
+        db = eng.stats()["bytes_h2d"] - b0
+        assert db % blob == 0 and db >= TINY.L * TINY.k * blob   # whole blobs, aliased or not
+        tok = nxt
+    assert excused <= 2
+    assert eng.stats()["max_resident"] <= slots
+    eng.close()
+
+
 def test_tiny_fp32_free_run_tokens(od):
     """fp32 path, 16 tokens x 4 prompts: every token equals the oracle's greedy token for the
     same input token (no KV state => per-token teacher forcing), barring near-ties."""
@@ -173,7 +201,9 @@ def test_output_invariance_across_predictors_slots_and_modes(od):
                dict(predictor=od.PRED_SHADOW_INT8, slots_per_gpu=2, chunk_bytes=65536),
                dict(predictor=od.PRED_SHADOW_INT8, slots_per_gpu=4, lookahead=2, refine_depth=2),
                dict(predictor=od.PRED_SHADOW_INT8, slots_per_gpu=2, refine_depth=1),
-               dict(predictor=od.PRED_GATE_REUSE, slots_per_gpu=4, lookahead=2)):
+               dict(predictor=od.PRED_GATE_REUSE, slots_per_gpu=4, lookahead=2),
+               dict(predictor=od.PRED_SHADOW_INT8, slots_per_gpu=1),          # fewer slots than k:
+               dict(predictor=od.PRED_RANDOM, slots_per_gpu=1, lookahead=3)):  # deferred loads
         eng, toks, routes, _ = _run(od, TINY, 12, first, **kw)
         assert toks == base, kw
         assert routes == base_r, kw

@@ -79,6 +79,20 @@ def main():
     pk = peaks()
     out = {}
     bf = torch.bfloat16
+    if args.only == "bf16":  # the main bf16 expert alone (ncu target; ODMOE_MAIN_MMA=0/1 A/B)
+        blob = torch.empty(3 * F * d, dtype=bf, device=dev)
+        odmoe.gen_weights(blob, 0, layer=0, expert=0, d=d, F=F, seed=2512)
+        w13, w2 = blob[: 2 * F * d], blob[2 * F * d:].view(d, F)
+        u = (torch.rand(d, device=dev) - 0.5).to(bf)
+        a = torch.empty(F, device=dev)
+        y = torch.empty(d, device=dev)
+        gw = torch.ones(2, device=dev)
+        med, best = timeit(lambda: odmoe.expert_ffn(w13, w2, u, a, y, gate_w=gw), args.iters, flush)
+        nbytes = 3 * F * d * 2
+        out["expert_ffn_bf16"] = dict(us_median=med * 1e6, us_best=best * 1e6, GBps=nbytes / med / 1e9,
+                                      frac_hbm=nbytes / med / 1e9 / pk["hbm_gbs"], bytes=nbytes,
+                                      engine="mma" if os.environ.get("ODMOE_MAIN_MMA", "0") == "1" else "ffma2")
+        del blob
     if args.only in ("", "gemv", "shadow"):
         blob = torch.empty(3 * F * d, dtype=bf, device=dev)
         odmoe.gen_weights(blob, 0, layer=0, expert=0, d=d, F=F, seed=2512)
