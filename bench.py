@@ -471,6 +471,11 @@ def main():
                        "note": "odmoe_predict_ahead for 8 distinct tokens, alone on the GPU; CUDA events around each "
                                "pass on the shadow stream; bytes = the k experts' int8 codes + row scales of 32 layers"}
     if dist is not None:
+        # every rank's expert-kernel time (rank 0 shares its GPU with the shadow stream)
+        g_rank = (st["ms_w13"] + st["ms_w2"]) / max(1, st["n_w13"]) * 1e3
+        gl = [torch.zeros(1, dtype=torch.float64, device="cuda") for _ in range(world)]
+        dist.all_gather(gl, torch.tensor([g_rank], dtype=torch.float64, device="cuda"))
+        us_per_rank = [float(x[0]) for x in gl]
         tt = torch.tensor([dev_s, wall], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         dev_s, wall = float(tt[0]), float(tt[1])
@@ -479,6 +484,7 @@ def main():
         bytes_all, link_all = float(agg[0]), float(agg[1])
     else:
         bytes_all, link_all = float(st["bytes_h2d"]), link
+        us_per_rank = None
     eng.close()
     del eng
 
@@ -535,9 +541,12 @@ def main():
                          "w2_us": st["ms_w2"] / n_exp * 1e3,
                          "read_floor_us": floor_us,
                          "frac_of_read_floor": (floor_us / (gemv_ms * 1e3)) if (floor_us and gemv_ms > 0) else None,
+                         "us_per_expert_by_rank": us_per_rank,
                          "note": "CUDA events around each on-demand launch in the timed step (includes the wait "
                                  "for the copy-stream event and the idle-to-busy ramp); read_floor_us = the same "
-                                 "bytes streamed with no arithmetic in one launch (profiles/pattern_bench_r01.json)"},
+                                 "bytes streamed with no arithmetic in one launch (profiles/pattern_bench_r01.json); "
+                                 "at N > 1 `achieved` is rank 0's, whose cooperative expert launches also wait for the "
+                                 "shadow / refinement kernels sharing its GPU; us_per_expert_by_rank lists every rank"},
             "host_link": {"bound": "pcie_h2d", "achieved": bytes_all / dev_s / 1e9,
                           "peak": link_all, "unit": "GB/s", "frac": bytes_all / dev_s / 1e9 / link_all,
                           "roofline_tok_s": roof_tok, "frac_tok_s": value / roof_tok,
