@@ -357,7 +357,9 @@ odmoe_status odmoe_load(void* ctx, int layer, int expert);
 /* Block until (layer, expert) is resident; *w13 / *w2 receive its device pointers. */
 odmoe_status odmoe_load_wait(void* ctx, int layer, int expert, void** w13, void** w2);
 /* Free the slot once work already enqueued on the compute stream is done ("promptly evicts
- * it afterward"; Q16). E_STATE if the expert is not resident/loading. */
+ * it afterward"; Q16). Only the engine's compute stream is ordered before the slot's reuse:
+ * a caller that read the weights from kernels on its own streams must synchronise those streams
+ * first. E_STATE if the expert is not resident/loading. */
 odmoe_status odmoe_evict(void* ctx, int layer, int expert);
 
 /* Event trace of the decode engine (S:350-358 event schema; Eq. 1 analysis). Enabled with
