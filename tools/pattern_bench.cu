@@ -2,7 +2,9 @@
 // with (a) the flat GEMV's pattern -- each warp one contiguous slice, 8 x 16 B per lane per batch,
 // two batches in flight -- versus (b) a grid-stride pattern where all CTAs sweep the buffer
 // front to back together, (c) block-interleaved slices (64 KB blocks dealt round-robin to CTAs).
-// No arithmetic beyond an XOR per load. Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3.
+// (d) dynamic: every warp claims 32 KB chunks from a global atomic counter (the claim for its next
+// chunk is issued when it starts the current one), so SMs that get less bandwidth simply take fewer
+// chunks (no tail of slow CTAs). No arithmetic beyond an XOR per load. Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3.
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -87,6 +89,40 @@ __global__ void __launch_bounds__(WARPS * 32, 1) blocks(const uint4* __restrict_
   if (acc == 0x12345678u) out[0] = acc;
 }
 
+// (d) dynamic chunks of CH groups (CH * 512 B) claimed per warp
+constexpr long long CH = 64;
+__global__ void __launch_bounds__(WARPS * 32, 1) dynamic(const uint4* __restrict__ p, long long n16, unsigned* out,
+                                                         unsigned long long* counter) {
+  const int lane = threadIdx.x & 31;
+  const long long nch = (n16 / 32) / CH;
+  unsigned acc = 0;
+  unsigned long long cur = 0;
+  if (lane == 0) cur = atomicAdd(counter, 1ull);
+  cur = __shfl_sync(0xffffffffu, cur, 0);
+  while ((long long)cur < nch) {
+    unsigned long long nxt = 0;
+    if (lane == 0) nxt = atomicAdd(counter, 1ull);
+    const uint4* base = p + (long long)cur * CH * 32 + lane;
+    uint4 a[U], b[U];
+#pragma unroll
+    for (int i = 0; i < U; ++i) a[i] = ldg_stream(base + i * 32);
+    for (int g = 0; g < CH; g += 2 * U) {
+#pragma unroll
+      for (int i = 0; i < U; ++i) b[i] = ldg_stream(base + (g + U + i) * 32);
+#pragma unroll
+      for (int i = 0; i < U; ++i) acc ^= a[i].x ^ a[i].y ^ a[i].z ^ a[i].w;
+      if (g + 2 * U < CH) {
+#pragma unroll
+        for (int i = 0; i < U; ++i) a[i] = ldg_stream(base + (g + 2 * U + i) * 32);
+      }
+#pragma unroll
+      for (int i = 0; i < U; ++i) acc ^= b[i].x ^ b[i].y ^ b[i].z ^ b[i].w;
+    }
+    cur = __shfl_sync(0xffffffffu, nxt, 0);
+  }
+  if (acc == 0x12345678u) out[0] = acc;
+}
+
 int main() {
   const long long sizes[3] = {352321536LL, 704643072LL, 1073741824LL};
   int sms = 0;
@@ -98,21 +134,25 @@ int main() {
   cudaMalloc(&flush, 256 << 20);
   unsigned* out;
   cudaMalloc(&out, 4);
+  unsigned long long* counter;
+  cudaMalloc(&counter, 8);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  const char* names[3] = {"slices", "gridstride", "blocks64K"};
+  const char* names[4] = {"slices", "gridstride", "blocks64K", "dynamic32K"};
   printf("{\n");
-  for (int k = 0; k < 3; ++k) {
+  for (int k = 0; k < 4; ++k) {
     for (int si = 0; si < 3; ++si) {
       const long long n16 = sizes[si] / 16;
       float best = 1e9f, sum = 0.f;
       for (int it = 0; it < 12; ++it) {
         cudaMemsetAsync(flush, it, 256 << 20);
+        cudaMemsetAsync(counter, 0, 8);
         cudaEventRecord(e0);
         if (k == 0) slices<<<sms, WARPS * 32>>>((const uint4*)buf, n16, out);
         if (k == 1) gridstride<<<sms, WARPS * 32>>>((const uint4*)buf, n16, out);
         if (k == 2) blocks<<<sms, WARPS * 32>>>((const uint4*)buf, n16, out);
+        if (k == 3) dynamic<<<sms, WARPS * 32>>>((const uint4*)buf, n16, out, counter);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         float ms;
