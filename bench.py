@@ -567,6 +567,16 @@ def main():
                        "us_lm_head": st["ms_lm_head"] / max(1, st["n_lm_head"]) * 1e3,
                        "us_attention_per_step": st["ms_attn"] / args.steps * 1e3},
         }
+        # GPU memory holding experts (slots on every GPU; + the INT8 shadow on GPU 0)
+        # as fractions of the whole model's experts (the paper's "1/3 GPU memory", Q24)
+        all_experts = SHAPE["L"] * SHAPE["E"] * EXPERT_BYTES
+        slot_bytes = n * st["resident_bytes"]
+        line["memory"] = {"expert_slot_bytes_all_gpus": slot_bytes, "all_experts_bytes": all_experts,
+                          "slot_fraction": slot_bytes / all_experts, "shadow_bytes_gpu0": st["shadow_bytes"],
+                          "with_shadow_fraction": (slot_bytes + st["shadow_bytes"]) / all_experts,
+                          "resident_baseline_fraction": 1.0,
+                          "note": "peak expert slots x blob on each of the N GPUs (the <1 GB budget per GPU), and "
+                                  "that plus the INT8 shadow held by GPU 0, over all L x E experts"}
         # Eq. 1 (reading Q12): t_maxload = N_G t^M + (N_G - 1) t^W, validated per layer
         # against the event trace of the traced steps
         G = args.group_size or min(SHAPE["k"], n)
