@@ -453,6 +453,49 @@ def test_mixtral_decode_sampled_layers(od):
 
 
 @pytest.mark.slow
+def test_mixtral_fp32_one_slot_sampled_layers(od):
+    """The FP32 bench leg's launch configuration (`bench.py --dtype fp32`: the paper's precision,
+    P:173; ONE 704.6 MB slot under the 1 GB budget; expert_layer_period 16, INT8
+    shadow): two decode steps, teacher-forced oracle checks on sampled layers, including layers >= 16
+    whose experts are those of layer l - 16 (fp32 tolerance 1e-5)."""
+    shape = MIXTRAL
+    P = 16
+    eng = engine(od, shape, "fp32", predictor=od.PRED_SHADOW_INT8, slots_per_gpu=1, debug_capture=1,
+                 expert_layer_period=P)
+    tok = int(gen_prompt(shape, 1, 1)[0])
+    W = gen_model_weights(shape, SEED, dtype="fp32", layers=[])
+    from inputs import KIND_ROUTER, tensor_id, weight_fp32
+    blob = 3 * shape.d * shape.F * 4
+    for step in range(2):
+        b0 = eng.stats()["bytes_h2d"]
+        nxt, recs = eng.decode_step(tok)
+        assert eng.stats()["bytes_h2d"] - b0 >= shape.L * shape.k * blob  # every load a whole fp32 blob
+        d, k, E = shape.d, shape.k, shape.E
+        for l in ([3, 19] if step == 0 else [31]):
+            Wg = weight_fp32(SEED, tensor_id(KIND_ROUTER, l), E, d, d).reshape(E, d).astype(np.float64)
+            h = read_f32(eng, "H_IN", l, d)
+            u = read_u(eng, "U", l, d, "fp32")
+            assert np.all(np.abs(u - O.rms_norm(h)) <= 1e-6 * np.abs(O.rms_norm(h)) + 1e-6)
+            r_ref = O.router_logits(Wg, u)
+            ids = read_i32(eng, "IDS", l, k)
+            assert ids_match(ids, r_ref, k)[0]
+            w = read_f32(eng, "W", l, k)
+            yp = read_f32(eng, "Y_PART", l, k * d).reshape(k, d)
+            for j in range(k):
+                W1, W3, W2 = gen_expert(shape, SEED, l % P, int(ids[j]), "fp32")
+                assert l2rel(yp[j], w[j] * O.expert_ffn(W1, W3, W2, u)) <= 1e-5
+        z = read_f32(eng, "LM_LOGITS", 0, shape.V)
+        z_ref = O.final_logits(W["lm_head"], read_f32(eng, "H_FINAL", 0, d))
+        assert np.allclose(z, z_ref, rtol=0, atol=1e-4 * np.abs(z_ref).max())
+        zs = np.sort(z_ref)[::-1]
+        assert nxt == O.greedy_argmax(z_ref) or abs(zs[0] - zs[1]) < 1e-3 * abs(zs[0])
+        tok = nxt
+    st = eng.stats()
+    assert st["max_resident"] <= 1 and st["resident_bytes"] < 1e9  # one fp32 slot < 1 GB (P:51)
+    eng.close()
+
+
+@pytest.mark.slow
 def test_mixtral_shadow_sampled_layers(od):
     """The INT8 shadow at BASELINE.json configs[1] shape in the bench's launch configuration (the
     one-launch-per-phase multi-expert kernel over the quantised experts): on sampled layers its
