@@ -808,21 +808,11 @@ __device__ __forceinline__ void flat_phase(const FlatArgs& a, uint8_t* sm, const
           for (int i = 1; i < a.send.nprev; ++i) t += a.send.prev[i][rb + r];
           t += v;
         }
-        a.send.dst[rb + r] = t;
-      }
-    }
-    if (MODE == 1 && a.send.dst != nullptr) {
-      // the CTA barrier orders every thread's remote stores before thread 0's system-scope fence
-      // (cumulative), so one fence per CTA publishes them (a fence per thread cost ~50 us per launch)
-      __syncthreads();
-      if (tid == 0) {
-        __threadfence_system();
-        const unsigned int done = atomicAdd_system(a.send.count, 1u);
-        if (done == gridDim.x - 1) {  // every CTA's rows are out: publish the layer's epoch
-          *a.send.count = 0u;
-          __threadfence_system();
-          asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.send.flag), "r"(a.send.epoch) : "memory");
-        }
+        // one 8-byte {value, epoch} store: the receiver polls the pair, so no fence or flag is needed
+        // (a system-scope fence per CTA before a flag release cost ~30 us per launch)
+        asm volatile("st.volatile.global.v2.u32 [%0], {%1, %2};" ::"l"(a.send.dst + 2 * (rb + r)),
+                     "r"(__float_as_uint(t)), "r"(a.send.epoch)
+                     : "memory");
       }
     }
   } else {

@@ -81,14 +81,12 @@ cudaError_t launch_quantize_fp8(const void* w, int64_t R, int64_t C, WType wt, u
 cudaError_t launch_quantize_nf4(const void* w, int64_t R, int64_t C, WType wt, uint8_t* q, float* absmax,
                                 cudaStream_t s);
 // The P2P combine fused into the W2 epilogue of a GPU's LAST expert of a layer:
-// every CTA stores, for its rows, prev[0] + ... + prev[nprev-1] + (this expert's gated output) -- the
-// order of launch_p2p_send -- straight into GPU 0's receive row over NVLink, fences at system scope
-// and counts itself on `count`; the last CTA releases `epoch` in `flag` (st.release.sys).
+// every thread stores, for its rows, prev[0] + ... + prev[nprev-1] + (this expert's gated output) --
+// the order of launch_p2p_send -- straight into GPU 0's receive row over NVLink as one 8-byte
+// {value, epoch} pair (the format launch_p2p_gather polls; no fence, no flag, no counter).
 struct P2PSend {
-  float* dst;                 // this rank's row of GPU 0's buffer (peer memory)
-  uint32_t* flag;             // this rank's flag on GPU 0
+  float* dst;                 // this rank's row of GPU 0's buffer (peer memory), 2 words per element
   uint32_t epoch;
-  unsigned int* count;        // device counter of this GPU (reset by the last CTA)
   const float* const* prev;   // device array: this GPU's earlier gated partials of the layer
   int nprev;
 };
@@ -183,12 +181,12 @@ cudaError_t launch_attention(const float* q, int q_stride, int T, int H, int Hkv
                              const void* vc_past, const void* kc_cur, const void* vc_cur, int kv_stride, int kv_f32,
                              float* part, float* o_f32, void* o_bf16, int o_stride, cudaStream_t s);
 
-// P2P combine over NVLink (p2p.cu): sender sums its n partials into its row of GPU 0's buffer and
-// releases `epoch` in its flag; GPU 0 waits for the flags in `mask` and sums the rows in rank order.
-cudaError_t launch_p2p_send(const float* const* y, int n, int d, float* dst, uint32_t* flag, uint32_t epoch,
-                            cudaStream_t s);
-cudaError_t launch_p2p_gather(const float* part, const uint32_t* flags, uint32_t mask, int d, uint32_t epoch,
-                              float* out, int32_t* err_flag, cudaStream_t s);
+// P2P combine over NVLink (p2p.cu): sender sums its n partials into its row of GPU 0's buffer as
+// {value, epoch} pairs (2 words per element; no fence, no flag); GPU 0 polls the rows in `mask` until
+// every pair carries `epoch` and sums them in rank order.
+cudaError_t launch_p2p_send(const float* const* y, int n, int d, float* dst, uint32_t epoch, cudaStream_t s);
+cudaError_t launch_p2p_gather(const float* part, uint32_t mask, int d, uint32_t epoch, float* out, int32_t* err_flag,
+                              cudaStream_t s);
 
 // INT8 shadow experts on the tensor cores (mma_gemv.cu): one phase (mode 0 = W13 + SwiGLU -> out
 // [n][F], x = bf16 u; mode 1 = W2 + gate -> out [n][d], x = fp32 a [n][F]) of n <= 4 W_I8P experts.

@@ -135,11 +135,8 @@ struct Ctx {
   // P2P combine (N > 1): GPU 0 owns part [world][d] + flags [world]; every rank maps them (CUDA IPC)
   bool p2p = false;
   float* p2p_part = nullptr;     // GPU 0's receive rows (local on rank 0, IPC-mapped elsewhere)
-  uint32_t* p2p_flag = nullptr;
   float* p2p_own_part = nullptr; // rank 0: the allocation (freed at destroy)
-  uint32_t* p2p_own_flag = nullptr;
   uint32_t p2p_seq = 0;          // epoch of the next layer combine (same sequence on every rank)
-  unsigned int* d_p2p_count = nullptr;  // CTA counter of the send fused into the last W2 (this GPU)
   bool p2p_fused_sent = false;   // this layer's partials already went out from the W2 epilogue
   const float** d_y1ptr = nullptr;  // device array {d_y} (one partial)
   const float** d_yptr = nullptr;    // [k] -> d_y parts (N = 1)

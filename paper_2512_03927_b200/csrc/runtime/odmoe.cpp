@@ -1277,14 +1277,13 @@ void pump(Ctx* c) {
 void setup_p2p(Ctx* c) {
   const char* e = getenv("ODMOE_P2P");
   if ((e && e[0] == '0') || c->world > 32) return;
-  struct Handles { cudaIpcMemHandle_t part, flag; int ok; };
+  struct Handles { cudaIpcMemHandle_t part; int ok; };
   Handles h{};
   if (c->rank == 0) {
-    c->p2p_own_part = dmalloc<float>(c, (size_t)c->world * c->d, "p2p part");
-    c->p2p_own_flag = dmalloc<uint32_t>(c, 32, "p2p flags");
-    CUDA_OK(c, cudaMemset(c->p2p_own_flag, 0, 32 * sizeof(uint32_t)));
-    h.ok = cudaIpcGetMemHandle(&h.part, c->p2p_own_part) == cudaSuccess &&
-           cudaIpcGetMemHandle(&h.flag, c->p2p_own_flag) == cudaSuccess;
+    // receive rows: {value, epoch} pairs, 2 words per element (the LL format of p2p.cu)
+    c->p2p_own_part = dmalloc<float>(c, (size_t)2 * c->world * c->d, "p2p part");
+    CUDA_OK(c, cudaMemset(c->p2p_own_part, 0, sizeof(float) * 2 * c->world * c->d));
+    h.ok = cudaIpcGetMemHandle(&h.part, c->p2p_own_part) == cudaSuccess;
   }
   char* dbuf = dmalloc<char>(c, sizeof(Handles), "p2p handles");
   CUDA_OK(c, cudaMemcpy(dbuf, &h, sizeof(h), cudaMemcpyHostToDevice));
@@ -1295,15 +1294,11 @@ void setup_p2p(Ctx* c) {
   int ok = h.ok;
   if (c->rank == 0) {
     c->p2p_part = c->p2p_own_part;
-    c->p2p_flag = c->p2p_own_flag;
   } else if (ok) {
     void* pp = nullptr;
-    void* pf = nullptr;
-    ok = cudaIpcOpenMemHandle(&pp, h.part, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess &&
-         cudaIpcOpenMemHandle(&pf, h.flag, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
+    ok = cudaIpcOpenMemHandle(&pp, h.part, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
     if (!ok) cudaGetLastError();
     c->p2p_part = (float*)pp;
-    c->p2p_flag = (uint32_t*)pf;
   }
   // every rank must agree (a rank that could not map falls back with everyone else)
   int32_t* dok = dmalloc<int32_t>(c, 1, "p2p ok");
@@ -1314,10 +1309,6 @@ void setup_p2p(Ctx* c) {
   cudaFree(dok);
   c->p2p = ok != 0;
   c->p2p_seq = 1;
-  if (c->p2p) {
-    c->d_p2p_count = dmalloc<unsigned int>(c, 1, "p2p count");
-    CUDA_OK(c, cudaMemset(c->d_p2p_count, 0, sizeof(unsigned int)));
-  }
 }
 
 // Ranks whose expert work feeds layer l's combine (bit r = rank r).
@@ -1392,15 +1383,16 @@ bool fused_ngpu_enabled() {
   return v == 1;
 }
 
-// ODMOE_P2P_FUSED=1: the P2P send in the last expert's W2 epilogue instead of the one-CTA send kernel.
-// Off by default: every CTA must publish its remote rows with a system-scope fence before the release,
-// and those fences cost ~30 us per launch (N = 2, sliced: 87 us per half expert with the fused send vs
-// 56.5 us with the separate send kernel; profiles/r02_m2c_*.json) -- more than the kernel it saves.
+// The P2P send in the last expert's W2 epilogue instead of the one-CTA send kernel (ODMOE_P2P_FUSED=0:
+// the send kernel). With a flag release it needed a system-scope fence per CTA (~30 us per launch,
+// profiles/r02_m2c_*.json); since every value travels with its epoch in one 8-byte store (p2p.cu) no
+// fence is needed, and the fused send is the default: resident N = 2 295.7 vs 280.4 tok/s,
+// on-demand tok/s unchanged (profiles/r02_n2_p2p_ll_{fused_send,send_kernel}.json).
 bool p2p_fused_enabled() {
   static int v = -1;
   if (v < 0) {
-    const char* e = getenv("ODMOE_P2P_FUSED");
-    v = (e && e[0] == '1') ? 1 : 0;
+    const char* e = getenv("ODMOE_P2P_FUSED");  // default on since the {value, epoch} format (no fences)
+    v = (e && e[0] == '0') ? 0 : 1;
   }
   return v == 1;
 }
@@ -1408,10 +1400,8 @@ bool p2p_fused_enabled() {
 // The P2P combine of this rank's layer partials, fused into its last expert's W2 (odmoe.h, kernels.h)
 P2PSend p2p_send_args(Ctx* c, int nprev) {
   P2PSend ps{};
-  ps.dst = c->p2p_part + (size_t)c->rank * c->d;
-  ps.flag = c->p2p_flag + c->rank;
+  ps.dst = c->p2p_part + (size_t)2 * c->rank * c->d;
   ps.epoch = c->p2p_seq;  // the epoch the layer-end send would use
-  ps.count = c->d_p2p_count;
   ps.prev = c->d_yptr;
   ps.nprev = nprev;
   return ps;
@@ -1564,8 +1554,7 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
     int32_t* ids_dev = (int32_t*)(pkt + c->pkt_ids_off);
     float* w_dev = (float*)(pkt + c->pkt_w_off);
     if (r0 && c->p2p && l > 0) {  // layer l-1's partials from the peers (NVLink) -> d_yred
-      CUDA_OK(c, launch_p2p_gather(c->p2p_part, c->p2p_flag, p2p_mask(c, l - 1), d, c->p2p_seq - 1, c->d_yred,
-                                   c->d_flag, s));
+      CUDA_OK(c, launch_p2p_gather(c->p2p_part, p2p_mask(c, l - 1), d, c->p2p_seq - 1, c->d_yred, c->d_flag, s));
       c->stats.kernel_launches++;
       if (c->dbg_yred) CUDA_OK(c, cudaMemcpyAsync(c->dbg_yred + (size_t)(l - 1) * d, c->d_yred, sizeof(float) * d, cudaMemcpyDeviceToDevice, s));
     }
@@ -1800,8 +1789,8 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
       // buffer over NVLink and published with a release flag (one kernel; no NCCL reduce)
       const uint32_t ep = c->p2p_seq++;
       if (in_group && !c->p2p_fused_sent) {
-        CUDA_OK(c, launch_p2p_send(c->d_yptr, c->sliced ? k : k / c->G, d, c->p2p_part + (size_t)c->rank * d,
-                                   c->p2p_flag + c->rank, ep, s));
+        CUDA_OK(c, launch_p2p_send(c->d_yptr, c->sliced ? k : k / c->G, d, c->p2p_part + (size_t)2 * c->rank * d,
+                                   ep, s));
         c->stats.kernel_launches++;
       }
     } else if (c->world > 1) {
@@ -1821,8 +1810,7 @@ void decode_step_impl(Ctx* c, int32_t token_in, int32_t* token_out, odmoe_layer_
   // final combine + LM head + argmax (rank 0)
   if (r0) {
     if (c->p2p) {
-      CUDA_OK(c, launch_p2p_gather(c->p2p_part, c->p2p_flag, p2p_mask(c, L - 1), d, c->p2p_seq - 1, c->d_yred,
-                                   c->d_flag, s));
+      CUDA_OK(c, launch_p2p_gather(c->p2p_part, p2p_mask(c, L - 1), d, c->p2p_seq - 1, c->d_yred, c->d_flag, s));
       c->stats.kernel_launches++;
       if (c->dbg_yred) CUDA_OK(c, cudaMemcpyAsync(c->dbg_yred + (size_t)(L - 1) * d, c->d_yred, sizeof(float) * d, cudaMemcpyDeviceToDevice, s));
     }
@@ -2320,7 +2308,6 @@ void destroy_ctx(Ctx* c) {
   F(c->d_lmscratch); F(c->d_lmlogits);
   F(c->sh_h); F(c->sh_u); F(c->sh_ids_all); F(c->sh_w); F(c->sh_logits_all); F(c->sh_a); F(c->sh_y); F((void*)c->sh_yptr);
   F(c->sh_tok); F(c->sh_lmscratch); F(c->sh_lmlogits);
-  F(c->d_p2p_count);
   F(c->d_yemu); F(c->d_prank); F((void*)c->d_emu_ptr); F(c->dbg_yrank);
   if (c->h_emu_ptr) cudaFreeHost((void*)c->h_emu_ptr);
   F(c->dbg_h); F(c->dbg_ypart); F(c->dbg_yred); F(c->dbg_sh_h_all); F(c->dbg_sh_u_all); F(c->dbg_sh_hf_all); F(c->dbg_hfinal);
@@ -2351,10 +2338,8 @@ void destroy_ctx(Ctx* c) {
   }
   if (c->rank != 0) {
     if (c->p2p_part) cudaIpcCloseMemHandle(c->p2p_part);
-    if (c->p2p_flag) cudaIpcCloseMemHandle(c->p2p_flag);
   } else {
     if (c->p2p_own_part) cudaFree(c->p2p_own_part);
-    if (c->p2p_own_flag) cudaFree(c->p2p_own_flag);
   }
   if (c->comm_pred) ncclCommDestroy(c->comm_pred);
   if (c->comm) ncclCommDestroy(c->comm);

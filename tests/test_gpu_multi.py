@@ -154,12 +154,13 @@ def test_multi_gpu_attention(world):
             assert r[4] == base_pf, (world, placement, r[0])
 
 
-def _run_rank_capture(rank, world, port, q, placement, p2p, G=0):
+def _run_rank_capture(rank, world, port, q, placement, p2p, G=0, fused_send=False):
     """One rank of a real N-GPU decode with the debug capture on rank 0: per step the token, the
     final hidden state and every layer's combined expert output (bytes)."""
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     os.environ["ODMOE_P2P"] = "1" if p2p else "0"
+    os.environ["ODMOE_P2P_FUSED"] = "1" if fused_send else "0"
     import torch as t
     import torch.distributed as dist
     t.cuda.set_device(rank)
@@ -186,12 +187,13 @@ def _run_rank_capture(rank, world, port, q, placement, p2p, G=0):
     dist.destroy_process_group()
 
 
-def _capture_multi(world, placement, p2p, G=0):
+def _capture_multi(world, placement, p2p, G=0, fused_send=False):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29900 + world * 7 + placement * 3 + int(p2p) + 17 * G + os.getpid() % 50
-    ps = [ctx.Process(target=_run_rank_capture, args=(r, world, port, q, placement, p2p, G)) for r in range(world)]
+    port = 29900 + world * 7 + placement * 3 + int(p2p) + 17 * G + 5 * int(fused_send) + os.getpid() % 50
+    ps = [ctx.Process(target=_run_rank_capture, args=(r, world, port, q, placement, p2p, G, fused_send))
+          for r in range(world)]
     for p in ps:
         p.start()
     res = sorted([q.get(timeout=600) for _ in ps], key=lambda x: x[0])
@@ -233,6 +235,8 @@ def test_multi_gpu_matches_one_gpu_emulation(world):
         real = _capture_multi(world, placement, True, G)
         assert real == emu, (world, placement, G)
         assert _capture_multi(world, placement, True, G) == real
+        # the send fused into the last W2 epilogue ({value, epoch} pairs) sums in the send kernel's order
+        assert _capture_multi(world, placement, True, G, fused_send=True) == real, (world, placement, G)
         nccl = _capture_multi(world, placement, False, G)
         for (ta, ha, ya), (tb, hb, yb) in zip(nccl, real):
             assert ta == tb
