@@ -501,7 +501,7 @@ def main():
         blob = EXPERT_BYTES // n if sliced(args, n) else EXPERT_BYTES   # bytes one launch pair streams
         achieved = blob / (gemv_ms * 1e-3) / 1e9 if gemv_ms > 0 else None
         traffic = None  # ncu dram bytes of one launch pair, captured at this slice size only
-        prof = os.path.join(ROOT, "profiles", "ncu_expert_gemv_r01.json")
+        prof = os.path.join(ROOT, "profiles", "ncu_expert_gemv_r02.json")
         if os.path.exists(prof) and not sliced(args, n) and args.dtype == "bf16":
             try:
                 traffic = json.load(open(prof)).get("dram_bytes_per_expert")
