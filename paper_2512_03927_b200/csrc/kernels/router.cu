@@ -189,7 +189,10 @@ __global__ void __launch_bounds__(kRouterThreads) router_kernel(
 // sum of squares and E partial logits through distributed shared memory, and CTA 0 picks the top-k
 // with warp shuffles (keys (logit, -index): lowest index on ties). Every CTA reads the kRC partial
 // sums of squares in the same order, so all slices are normalised with identical bits. Each CTA
-// issues its W_g slice loads (E x d/kRC) before the dependency wait.
+// issues its W_g slice loads (E x d/kRC) before the dependency wait. The exchanges are st.async
+// stores into the receivers' shared memory that complete on the receiver's mbarrier (transaction
+// bytes), so no cluster-wide barrier sits on the critical path: the one cluster barrier (mbarrier
+// initialisation visible cluster-wide) runs before the dependency wait, under the previous kernel.
 constexpr int kRC = 8;             // CTAs per cluster
 constexpr int kRCThreads = 128;
 constexpr int kRCWarps = kRCThreads / 32;
@@ -201,7 +204,7 @@ __device__ __forceinline__ unsigned long long topk_key(float v, int id) {
 }
 
 template <typename WT>
-__global__ void __cluster_dims__(kRC, 1, 1) __launch_bounds__(kRCThreads) router_cluster_kernel(
+__global__ void __cluster_dims__(kRC, 1, 1) __launch_bounds__(kRCThreads, 1) router_cluster_kernel(
     float* __restrict__ h, const float* const* __restrict__ y_add, int n_add, const WT* __restrict__ gamma,
     const WT* __restrict__ wg, const float* __restrict__ wg_scale, int E, int d, int k, float eps,
     void* __restrict__ u_out, int32_t* __restrict__ ids, float* __restrict__ w, float* __restrict__ logits,
@@ -216,6 +219,36 @@ __global__ void __cluster_dims__(kRC, 1, 1) __launch_bounds__(kRCThreads) router
   __shared__ float ss_part[kRC];
   __shared__ float lg_part[kRC][kMaxE];
   __shared__ float red[kRCWarps];
+  __shared__ __align__(8) uint64_t bar_ss;  // this CTA: the kRC partial sums of squares have landed
+  __shared__ __align__(8) uint64_t bar_lg;  // CTA 0: the kRC x E partial logits have landed
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(r_smem(&bar_ss)));
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(r_smem(&bar_ss)), "r"(kRC * 4)
+                 : "memory");
+    if (c == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(r_smem(&bar_lg)));
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(r_smem(&bar_lg)), "r"(kRC * E * 4)
+                   : "memory");
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // remote st.async only after every CTA's barriers exist (before the dependency wait: off the path)
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+  // st.async of one fp32 into CTA `dst`'s copy of `slot`, completing on its copy of `bar`
+  auto st_async = [&](float* slot, uint64_t* bar, int dst, float v) {
+    uint32_t ra, rb;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(r_smem(slot)), "r"(dst));
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(r_smem(bar)), "r"(dst));
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(ra),
+                 "r"(__float_as_uint(v)), "r"(rb)
+                 : "memory");
+  };
+  auto wait_bar = [&](uint64_t* bar) {
+    asm volatile("{\n .reg .pred p;\n RW_%=:\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], 0;\n"
+                 " @!p bra RW_%=;\n}\n" ::"r"(r_smem(bar))
+                 : "memory");
+  };
 
   // W_g slice: expert e's chunks [e][j0 .. j0 + cols), lane i takes chunks i, i + 32, ... of the
   // experts of its warp (e = warp, warp + kRCWarps, ...); loaded before the dependency wait
@@ -251,12 +284,12 @@ __global__ void __cluster_dims__(kRC, 1, 1) __launch_bounds__(kRCThreads) router
   ss = warp_sum(ss);
   if (lane == 0) red[warp] = ss;
   __syncthreads();
-  if (tid == 0) {
+  if (tid < kRC) {  // this slice's sum of squares into slot c of every CTA (thread r -> CTA r)
     float t = 0.f;
     for (int i = 0; i < kRCWarps; ++i) t += red[i];
-    for (int r = 0; r < kRC; ++r) cluster.map_shared_rank(ss_part, r)[c] = t;  // to every CTA
+    st_async(&ss_part[c], &bar_ss, tid, t);
   }
-  cluster.sync();
+  wait_bar(&bar_ss);
   float tot = 0.f;
   for (int r = 0; r < kRC; ++r) tot += ss_part[r];  // same order everywhere: identical rstd
   const float rstd = 1.0f / sqrtf(tot / (float)d + eps);
@@ -291,10 +324,10 @@ __global__ void __cluster_dims__(kRC, 1, 1) __launch_bounds__(kRCThreads) router
       acc += dot16<WT>(wq, us + q * N);
     }
     acc = warp_sum(acc);
-    if (lane == 0) cluster.map_shared_rank(&lg_part[0][0], 0)[c * kMaxE + e] = acc;
+    if (lane == 0) st_async(&lg_part[c][e], &bar_lg, 0, acc);
   }
-  cluster.sync();
   if (c != 0 || warp != 0) return;
+  wait_bar(&bar_lg);
 
   // CTA 0, warp 0: logits (slices summed in CTA order), top-k by warp argmax, softmax
   float lv = 0.f;
