@@ -71,6 +71,7 @@ def parse():
                     help="expert_layer_period P (odmoe.h): expert weights repeat every P layers so the host pool "
                          "holds P layers; loads and bytes per token unchanged. -1 => 16 for fp32 (the 180 GB "
                          "fp32 pool exceeds the box's host RAM), 0 otherwise")
+    ap.add_argument("--chunk-mb", type=int, default=0, help="H2D copy chunk of the loader in MiB (0 = the engine's default)")
     ap.add_argument("--out", default="")
     a = ap.parse_args()
     if a.layer_period < 0:
@@ -378,7 +379,7 @@ def main():
     eng = odmoe.Engine(device=local, rank=rank, world_size=world, nccl_id=uid, predictor=pred,
                        slots_per_gpu=n_slots(args, n), lookahead=D, time_kernels=2, weight_seed=SEED,
                        refine_depth=refine, placement=int(sliced(args, n)), group_size=args.group_size,
-                       **SHAPE, **attn_kw(args), **model_kw(args, odmoe))
+                       chunk_bytes=args.chunk_mb << 20, **SHAPE, **attn_kw(args), **model_kw(args, odmoe))
     if args.align_period > 1:
         eng.set_align_period(args.align_period)
     if args.attention and args.prefill <= 0:
