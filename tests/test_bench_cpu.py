@@ -93,3 +93,27 @@ def test_fp32_leg_arguments(monkeypatch):
     b = bench.parse()
     assert b.dtype == "bf16" and b.layer_period == 0 and b.refine == 2 and bench.n_slots(b, 1) == 2
     assert bench.EXPERT_BYTES == 352321536
+
+
+def test_reference_arm_prints_one_contract_line():
+    """`bench.py --impl reference` (the oracle as the reference arm, on the host cores): exactly one JSON
+    line on stdout with the contract keys, a bounded per-step sample and zero host<->device bytes."""
+    import json
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--steps", "1",
+                          "--warmup", "0"], capture_output=True, text=True, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [x for x in out.stdout.splitlines() if x.strip()]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "dtype", "config", "cpu_baseline", "e2e"):
+        assert key in line, key
+    assert line["impl"] == "reference" and line["unit"] == "tok/s" and line["value"] > 0
+    assert line["metric"] == bench.METRIC and line["higher_is_better"] is True
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
+    assert line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] >= 1
+    # a step is one of the 32 layers of a token: the token takes at least 32 steps' time
+    assert 1.0 / line["value"] >= 32 * line["ms_per_step"] * 1e-3 * 0.99
