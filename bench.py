@@ -234,7 +234,7 @@ class OracleWalk:
         return time.perf_counter() - t0
 
 
-def oracle_sample(n_layers=8):
+def oracle_sample(n_layers=24):
     """cpu_baseline: the oracle on `n_layers` consecutive layers of one decode token plus the LM
     head, scaled to a 32-layer token."""
     walk = OracleWalk()
@@ -610,7 +610,7 @@ def main():
         if not args.no_cpu_baseline and n == 1:
             log(rank, "cpu baseline (oracle sample)")
             try:
-                line["cpu_baseline"] = oracle_sample(8)
+                line["cpu_baseline"] = oracle_sample(24)  # ~10-15 s of timed CPU work on the box
             except Exception as e:  # report, never hide
                 line["cpu_baseline"] = {"value": None, "error": repr(e)}
         out = json.dumps(line)
