@@ -1,6 +1,10 @@
 // C ABI of libodmoe.so: stateless kernel entry points and the stateful OD-MoE decode engine.
 // Contract: include/odmoe.h. Design: DESIGN.md §5-§7.
+#include <sys/syscall.h>
+#include <unistd.h>
+
 #include <algorithm>
+#include <cctype>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -578,6 +582,36 @@ void gen_blob(Ctx* c, int l, int e, char* dst, char* full) {
                                (size_t)F * es, (size_t)c->Fs * es, (size_t)d, cudaMemcpyDeviceToDevice, c->s_main));
 }
 
+// NUMA node of this rank's GPU from sysfs (-1 when unknown / single node)
+int gpu_numa_node(int dev) {
+  char bus[32] = {0};
+  if (cudaDeviceGetPCIBusId(bus, (int)sizeof(bus), dev) != cudaSuccess) return -1;
+  for (char* p = bus; *p; ++p) *p = (char)std::tolower((unsigned char)*p);
+  const std::string path = std::string("/sys/bus/pci/devices/") + bus + "/numa_node";
+  FILE* f = std::fopen(path.c_str(), "r");
+  if (!f) return -1;
+  int n = -1;
+  if (std::fscanf(f, "%d", &n) != 1) n = -1;
+  std::fclose(f);
+  return n;
+}
+
+// While alive, this thread's page allocations prefer `node` (MPOL_PREFERRED), so the pinned expert
+// pool lands next to its GPU's PCIe root on multi-socket hosts. Best effort: any error
+// leaves the default policy; a no-op on single-node hosts.
+struct NumaPreferred {
+  bool set = false;
+  explicit NumaPreferred(int node) {
+    const char* e = getenv("ODMOE_NUMA");  // ODMOE_NUMA=0: leave page placement to the kernel
+    if (node < 0 || node >= 64 || (e && e[0] == '0')) return;
+    unsigned long mask = 1ul << node;
+    set = syscall(SYS_set_mempolicy, 1 /* MPOL_PREFERRED */, &mask, 64ul) == 0;
+  }
+  ~NumaPreferred() {
+    if (set) syscall(SYS_set_mempolicy, 0 /* MPOL_DEFAULT */, nullptr, 0ul);
+  }
+};
+
 void build_pool(Ctx* c, char* staging) {
   const int L = c->L, E = c->E, d = c->d, F = c->F;
   const double t0 = now_s();
@@ -613,7 +647,10 @@ void build_pool(Ctx* c, char* staging) {
           c->res_blob[(size_t)l * E + e] = p;
         }
     }
-    c->pool = hmalloc<char>(c, (size_t)c->pool_bytes, "expert pool");
+    {
+      NumaPreferred np(gpu_numa_node(c->cfg.device));  // pages are placed when cudaHostAlloc pins them
+      c->pool = hmalloc<char>(c, (size_t)c->pool_bytes, "expert pool");
+    }
     // Fill the pool: generate each blob on the GPU, copy D2H into its pinned slot.
     char* stg[2] = {staging + c->full_bytes, staging + c->full_bytes + c->blob_bytes};
     cudaEvent_t done[2];
