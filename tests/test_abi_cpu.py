@@ -73,3 +73,28 @@ def test_create_validates_config_before_touching_the_gpu():
         with pytest.raises(odmoe.OdmoeError) as ei:
             odmoe.Engine(4, 8, 2, 256, 512, 1024, **kw)
         assert ei.value.status == 1 and msg in str(ei.value), (kw, str(ei.value))
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_bench_multi_gpu_configs_pass_validation(world):
+    """The configurations bench.py builds at N = 2 / 4 / 8 (Mixtral shape; sliced default with 2k slice
+    slots and lookahead 1, the paper's groups with G = 2, D = N/2; fp32 with one slot and
+    expert_layer_period 16; the resident baseline) are accepted by the ABI's validation: on this
+    GPU-less host they fail only at CUDA initialisation (E_CUDA), never as E_CONFIG."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("CPU-only check (with a GPU the engine would really start)")
+    from paper_2512_03927_b200 import odmoe
+    shape = dict(L=32, E=8, k=2, d=4096, F=14336, V=32000)
+    uid = bytes(128)
+    cases = [dict(placement=odmoe.PLACE_SLICED, slots_per_gpu=4, lookahead=1, refine_depth=2),
+             dict(placement=odmoe.PLACE_GROUPS, slots_per_gpu=2, lookahead=max(1, world // 2), refine_depth=2),
+             dict(placement=odmoe.PLACE_SLICED, slots_per_gpu=1, lookahead=1, dtype=odmoe.FP32,
+                  expert_layer_period=16),
+             dict(placement=odmoe.PLACE_SLICED, slots_per_gpu=-1, predictor=odmoe.PRED_NONE)]
+    for kw in cases:
+        args = dict(predictor=odmoe.PRED_SHADOW_INT8, rank=0, world_size=world, nccl_id=uid)
+        args.update(kw)
+        with pytest.raises(odmoe.OdmoeError) as ei:
+            odmoe.Engine(**shape, **args)
+        assert ei.value.status == 8, (world, kw, str(ei.value))  # E_CUDA, not E_CONFIG
