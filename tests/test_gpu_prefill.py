@@ -5,7 +5,13 @@ import pytest
 
 import oracle as O
 from inputs import MIXTRAL, TINY, gen_expert, gen_model_weights, gen_prompt
-from tests.gpu_util import TOL_BF16, host, ids_match, l2rel, to_dev, torch, w13_interleaved
+from tests.gpu_util import TOL_BF16, host, ids_match, l2rel, maxabs_rel, to_dev, torch, w13_interleaved
+
+# Element-wise bound of the grouped FFN against the oracle: the dominant error is the bf16 rounding of
+# the SwiGLU intermediate (reading Q8), emulated on the CPU with these generators at <= 3.2e-3 of
+# max|ref| (tiny shape) and <= 2e-3 (Mixtral); 1.5e-2 keeps a 5x margin and still flags a dropped or
+# zeroed output element of typical size.
+TOL_GG_ELEM = 1.5e-2
 
 pytestmark = pytest.mark.gpu
 SEED = 2512
@@ -74,6 +80,8 @@ def _grouped_case(od, shape, counts, check_rows):
             err = l2rel(yh[r], ref)
             errs.append(err)
             assert err <= TOL_BF16, (e, r, err)
+            em = maxabs_rel(yh[r], ref)
+            assert em <= TOL_GG_ELEM, (e, r, em)
     return max(errs) if errs else 0.0
 
 
